@@ -1,0 +1,254 @@
+"""TEST INFRASTRUCTURE: ctypes wrapper over the compiled reference (oracle/_ref).
+
+Only tests/, __graft_entry__.smoke() and bench.py's reference / cpu_baseline
+arm may import this module -- it is the checker, never the product path.
+
+The library is the UNMODIFIED reference (/root/reference/proj/src/
+{tensor,blocks,executor}.cpp) plus oracle/ref_shim.cpp, built by
+oracle/Makefile. States are flat float64 arrays laid out as the reference's
+State{x, y} (blocks.hpp:70-73): x [B, s_x, d] followed by y [B, s_y, d].
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "_ref", "libmglp_ref.so")
+
+_dp = C.POINTER(C.c_double)
+_lib = None
+
+
+def available() -> bool:
+    return os.path.exists(LIB_PATH)
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not available():
+            raise RuntimeError(f"reference oracle not built: {LIB_PATH} (run make -C oracle)")
+        L = C.CDLL(LIB_PATH)
+        L.ref_last_error.restype = C.c_char_p
+        L.ref_stack_num_params.restype = C.c_longlong
+        L.ref_stack_step_size.restype = C.c_double
+        L.ref_last_pair_factor.restype = C.c_double
+        _lib = L
+    return _lib
+
+
+def _ptr(a):
+    if a is None:
+        return None
+    assert a.dtype == np.float64 and a.flags.c_contiguous
+    return a.ctypes.data_as(_dp)
+
+
+class RefError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"[status {status}] {msg}")
+        self.status = status
+
+
+def _check(status):
+    if status != 0:
+        raise RefError(status, lib().ref_last_error().decode())
+
+
+KIND = {"encoder": 0, "decoder_only": 1, "encoder_decoder": 2}
+
+
+@dataclass
+class RefStackConfig:
+    kind: str = "encoder"
+    d: int = 32
+    heads: int = 2
+    ffn: int = 64
+    n_enc: int = 8
+    n_dec: int = 0
+    buffer_open: int = 0
+    buffer_close: int = 0
+    base_h: float = 1.0
+    init_std: float = 0.02
+    depth_scaled_init: bool = False
+    dropout: float = 0.0
+
+
+class RefStack:
+    """The reference LayerStack (blocks.hpp:120-175)."""
+
+    def __init__(self, cfg: RefStackConfig, seed: int):
+        self.cfg = cfg
+        h = C.c_void_p()
+        _check(lib().ref_stack_create(
+            KIND[cfg.kind], cfg.d, cfg.heads, cfg.ffn, cfg.n_enc, cfg.n_dec,
+            cfg.buffer_open, cfg.buffer_close, C.c_double(cfg.base_h),
+            C.c_double(cfg.init_std), int(cfg.depth_scaled_init), C.c_double(cfg.dropout),
+            C.c_ulonglong(seed), C.byref(h)))
+        self.h = h
+        t, ib, ie, ns = C.c_int(), C.c_int(), C.c_int(), C.c_int()
+        lib().ref_stack_info(self.h, C.byref(t), C.byref(ib), C.byref(ie), C.byref(ns))
+        self.total, self.ib, self.ie, self.n_split = t.value, ib.value, ie.value, ns.value
+
+    def __del__(self):
+        if getattr(self, "h", None) and _lib is not None:
+            _lib.ref_stack_destroy(self.h)
+            self.h = None
+
+    def num_params(self) -> int:
+        return int(lib().ref_stack_num_params(self.h))
+
+    def get_params(self) -> np.ndarray:
+        out = np.empty(self.num_params(), np.float64)
+        _check(lib().ref_stack_get_params(self.h, _ptr(out)))
+        return out
+
+    def set_params(self, flat: np.ndarray):
+        flat = np.ascontiguousarray(flat, np.float64)
+        assert flat.size == self.num_params()
+        _check(lib().ref_stack_set_params(self.h, _ptr(flat)))
+
+    def step_size(self, layer: int) -> float:
+        return float(lib().ref_stack_step_size(self.h, layer))
+
+    def refresh_dropout(self, seed, batch_index, b, sx, sy):
+        _check(lib().ref_stack_refresh_dropout(self.h, C.c_ulonglong(seed),
+                                               C.c_ulonglong(batch_index), b, sx, sy))
+
+    def state_size(self, b, sx, sy):
+        return b * (sx + sy) * self.cfg.d
+
+    def step(self, layer, dt, z, b, sx, sy):
+        z = np.ascontiguousarray(z, np.float64)
+        out = np.empty_like(z)
+        _check(lib().ref_stack_step(self.h, layer, C.c_double(dt), b, sx, sy, _ptr(z), _ptr(out)))
+        return out
+
+    def residual(self, layer, z, b, sx, sy):
+        z = np.ascontiguousarray(z, np.float64)
+        out = np.empty_like(z)
+        _check(lib().ref_stack_residual(self.h, layer, b, sx, sy, _ptr(z), _ptr(out)))
+        return out
+
+    def adjoint_step(self, layer, dt, z, lam, b, sx, sy, grads=None, gscale=0.0):
+        z = np.ascontiguousarray(z, np.float64)
+        lam = np.ascontiguousarray(lam, np.float64)
+        out = np.empty_like(z)
+        _check(lib().ref_stack_adjoint_step(self.h, layer, C.c_double(dt), b, sx, sy,
+                                            _ptr(z), _ptr(lam), _ptr(grads),
+                                            C.c_double(gscale), _ptr(out)))
+        return out
+
+    def serial_forward(self, z0, b, sx, sy):
+        z0 = np.ascontiguousarray(z0, np.float64)
+        traj = np.empty((self.total + 1, z0.size), np.float64)
+        _check(lib().ref_serial_forward(self.h, b, sx, sy, _ptr(z0), _ptr(traj)))
+        return traj
+
+    def serial_adjoint(self, traj, lam_n, b, sx, sy, grads=None):
+        traj = np.ascontiguousarray(traj, np.float64)
+        lam_n = np.ascontiguousarray(lam_n, np.float64)
+        lam = np.empty_like(traj)
+        _check(lib().ref_serial_adjoint(self.h, b, sx, sy, _ptr(traj), _ptr(lam_n),
+                                        _ptr(lam), _ptr(grads)))
+        return lam
+
+
+GUESS = {"broadcast": 0, "zero": 1, "warm": 2}
+
+
+class RefEngine:
+    """The reference LayerParallelEngine (adjoint.hpp:99-219)."""
+
+    def __init__(self, stack: RefStack, coarsen=2, levels=2, fwd_iters=2, bwd_iters=1,
+                 fwd_tol=0.0, bwd_tol=0.0, cold_guess="broadcast", warm_start=True,
+                 workers=1):
+        self.stack = stack
+        h = C.c_void_p()
+        _check(lib().ref_engine_create(stack.h, coarsen, levels, fwd_iters, bwd_iters,
+                                       C.c_double(fwd_tol), C.c_double(bwd_tol),
+                                       GUESS[cold_guess], int(warm_start), workers,
+                                       C.byref(h)))
+        self.h = h
+
+    def __del__(self):
+        if getattr(self, "h", None) and _lib is not None:
+            _lib.ref_engine_destroy(self.h)
+            self.h = None
+
+    def set_iters(self, fwd_iters, bwd_iters, fwd_tol=0.0, bwd_tol=0.0):
+        lib().ref_engine_set_iters(self.h, fwd_iters, bwd_iters, C.c_double(fwd_tol),
+                                   C.c_double(bwd_tol))
+
+    def forward(self, z0, b, sx, sy, max_trace=256):
+        z0 = np.ascontiguousarray(z0, np.float64)
+        traj = np.empty((self.stack.total + 1, z0.size), np.float64)
+        trace = np.empty(max_trace, np.float64)
+        n, conv = C.c_int(), C.c_int()
+        _check(lib().ref_engine_forward(self.h, b, sx, sy, _ptr(z0), _ptr(traj), _ptr(trace),
+                                        max_trace, C.byref(n), C.byref(conv)))
+        return traj, trace[:n.value].copy(), bool(conv.value)
+
+    def backward(self, traj, lam_n, b, sx, sy, grads=None, max_trace=256):
+        traj = np.ascontiguousarray(traj, np.float64)
+        lam_n = np.ascontiguousarray(lam_n, np.float64)
+        lam0 = np.empty_like(lam_n)
+        trace = np.empty(max_trace, np.float64)
+        n, conv = C.c_int(), C.c_int()
+        _check(lib().ref_engine_backward(self.h, b, sx, sy, _ptr(traj), _ptr(lam_n),
+                                         _ptr(lam0), _ptr(grads), _ptr(trace), max_trace,
+                                         C.byref(n), C.byref(conv)))
+        return lam0, trace[:n.value].copy(), bool(conv.value)
+
+    def snapshot(self):
+        lib().ref_engine_snapshot(self.h)
+
+    def restore(self):
+        lib().ref_engine_restore(self.h)
+
+    def reset(self):
+        lib().ref_engine_reset(self.h)
+
+
+def scalar_solve(rates, h, cf, levels, z0, iters, tol=0.0, workers=1):
+    rates = np.ascontiguousarray(rates, np.float64)
+    n = rates.size
+    states = np.empty(n + 1, np.float64)
+    trace = np.empty(max(iters, 1), np.float64)
+    nt, conv = C.c_int(), C.c_int()
+    _check(lib().ref_scalar_solve(_ptr(rates), n, C.c_double(h), cf, levels, C.c_double(z0),
+                                  iters, C.c_double(tol), workers, _ptr(states), _ptr(trace),
+                                  C.byref(nt), C.byref(conv)))
+    return states, trace[:nt.value].copy(), bool(conv.value)
+
+
+def decide(f_fwd, f_bwd, threshold, policy, cap, fwd_iters, bwd_iters) -> int:
+    d = C.c_int()
+    _check(lib().ref_decide(C.c_double(f_fwd), C.c_double(f_bwd), C.c_double(threshold),
+                            policy, cap, fwd_iters, bwd_iters, C.byref(d)))
+    return d.value
+
+
+def last_pair_factor(trace) -> float:
+    t = np.ascontiguousarray(trace, np.float64)
+    return float(lib().ref_last_pair_factor(_ptr(t), t.size))
+
+
+def gaussian_fill(seed, a, b, n, scale=1.0):
+    """scale * rng::gaussian(seed, a, b, i) for i < n (the bench z0 draw, main.cpp:121-128)."""
+    out = np.empty(n, np.float64)
+    lib().ref_gaussian_fill(C.c_ulonglong(seed), C.c_ulonglong(a), C.c_ulonglong(b),
+                            C.c_double(scale), _ptr(out), C.c_longlong(n))
+    return out
+
+
+def gaussian_fill_flat(seed, a, n, scale=1.0):
+    """scale * rng::gaussian(seed, a, i) (testutil::random_tensor, test_util.hpp:89-95)."""
+    out = np.empty(n, np.float64)
+    lib().ref_gaussian_fill_flat(C.c_ulonglong(seed), C.c_ulonglong(a), C.c_double(scale),
+                                 _ptr(out), C.c_longlong(n))
+    return out
