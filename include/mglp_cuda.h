@@ -1,0 +1,188 @@
+/* mglp_cuda.h -- C-ABI drop-in boundary for the layer-parallel (MGRIT) hot path.
+ *
+ * The reference (mglp, /root/reference/proj) exposes this path as C++
+ * classes, not an FFI: LayerStack (blocks.hpp:120-175), SolveConfig /
+ * LayerParallelEngine (adjoint.hpp:70-219) and the controller free functions
+ * (controller.hpp:63-105). Each entry point below replaces one of those
+ * members; the file:line of the replaced interface is given per function.
+ * Plain pointers and sizes only -- no torch, no C++ types.
+ *
+ * States cross the boundary as flat float64 arrays in the reference's
+ * State{x, y} layout (blocks.hpp:70-73): x [batch, s_x, d] followed by
+ * y [batch, s_y, d] (y absent unless the stack is encoder-decoder).
+ * Parameters and gradients are flat float64 arrays in visit_params order
+ * (blocks.cpp:627-646). On the device everything is fp32 with tf32x3 tensor
+ * core GEMMs; results agree with the f64 reference to ~1e-5 relative.
+ *
+ * Status codes mirror the reference's error taxonomy (errors.hpp:25-35,
+ * tools/main.cpp:244-252): 0 ok, 1 ValidationError (bad input / config),
+ * 2 ContractViolation (broken invariant, CUDA failure). mglp_last_error()
+ * returns the message of the last failing call on this thread.
+ *
+ * Threading: one engine per host thread, as in the reference.
+ */
+#ifndef MGLP_CUDA_H_
+#define MGLP_CUDA_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef int mglp_status;
+#define MGLP_OK 0
+#define MGLP_VALIDATION_ERROR 1
+#define MGLP_CONTRACT_VIOLATION 2
+
+/* ModelKind (blocks.hpp:98) */
+#define MGLP_ENCODER 0
+#define MGLP_DECODER_ONLY 1
+#define MGLP_ENCODER_DECODER 2
+
+/* InitialGuess (mgrit.hpp:30) */
+#define MGLP_GUESS_BROADCAST 0
+#define MGLP_GUESS_ZERO 1
+#define MGLP_GUESS_WARM 2
+
+/* StackConfig (blocks.hpp:100-114) */
+typedef struct {
+  int kind;
+  int d, heads, ffn;
+  int n_enc, n_dec;
+  int buffer_open, buffer_close;
+  double ln_eps;
+  double base_h;
+  double dropout; /* must be 0 on the device path */
+  double init_std;
+  int depth_scaled_init;
+} mglp_stack_desc;
+
+/* SolveConfig (adjoint.hpp:70-79) */
+typedef struct {
+  int coarsen, levels;
+  int fwd_iters, bwd_iters;
+  double fwd_tol, bwd_tol;
+  int cold_guess;
+  int warm_start;
+} mglp_solve_config;
+
+typedef struct mglp_engine mglp_engine;
+
+const char* mglp_last_error(void);
+/* library build string (arch, precision mode) */
+const char* mglp_version(void);
+
+/* LayerParallelEngine(const LayerStack&, Executor&, SolveConfig)
+ * (adjoint.hpp:101-108) + LayerStack(StackConfig, seed) shape checks
+ * (blocks.cpp:385-419). Parameters start at zero: call
+ * mglp_engine_init_params or mglp_engine_set_params. */
+mglp_status mglp_engine_create(const mglp_stack_desc* stack, const mglp_solve_config* solve,
+                               int device, mglp_engine** out);
+mglp_status mglp_engine_destroy(mglp_engine* e);
+
+/* LayerStack accessors (blocks.hpp:125-130) */
+mglp_status mglp_engine_info(mglp_engine* e, int* total_layers, int* interior_begin,
+                             int* interior_end, long long* num_params);
+mglp_status mglp_engine_step_size(mglp_engine* e, int layer, double* h);
+
+/* LayerStack(cfg, seed) parameter initialisation (blocks.cpp:432-449);
+ * bit-identical f64 values. flat_out (nullable) receives them. */
+mglp_status mglp_engine_init_params(mglp_engine* e, unsigned long long seed, double* flat_out);
+/* params() write / read in visit_params order (blocks.cpp:627-655) */
+mglp_status mglp_engine_set_params(mglp_engine* e, const double* flat, long long n);
+mglp_status mglp_engine_get_params(mglp_engine* e, double* flat, long long n);
+
+/* config() (adjoint.hpp:110-111) */
+mglp_status mglp_engine_get_config(mglp_engine* e, mglp_solve_config* cfg);
+mglp_status mglp_engine_set_config(mglp_engine* e, const mglp_solve_config* cfg);
+
+/* ForwardOutcome forward(const State& z0) (adjoint.hpp:113-137).
+ * traj_out (nullable): (total_layers+1) states. trace_out: up to max_trace
+ * residual norms; *n_trace gets the count, *converged the flag. */
+mglp_status mglp_engine_forward(mglp_engine* e, int batch, int s_x, int s_y, const double* z0,
+                                double* traj_out, double* trace_out, int max_trace,
+                                int* n_trace, int* converged);
+
+/* BackwardOutcome backward(traj, lambda_N, grads*) (adjoint.hpp:139-183).
+ * traj_in == NULL reuses the device-resident trajectory of the last forward
+ * (the common case; no host copy). grads_accum (nullable) is ACCUMULATED
+ * (+=), like the reference's caller-owned grads. */
+mglp_status mglp_engine_backward(mglp_engine* e, int batch, int s_x, int s_y,
+                                 const double* traj_in, const double* lam_n, double* lam0_out,
+                                 double* grads_accum, double* trace_out, int max_trace,
+                                 int* n_trace, int* converged);
+
+/* WarmSnapshot snapshot() / restore() / reset() (adjoint.hpp:187-206) */
+mglp_status mglp_engine_snapshot(mglp_engine* e);
+mglp_status mglp_engine_restore(mglp_engine* e);
+mglp_status mglp_engine_reset(mglp_engine* e);
+
+/* serial_forward / serial_adjoint (blocks.cpp:659-682). lam_all_out
+ * (nullable) receives lambda at every time point. */
+mglp_status mglp_serial_forward(mglp_engine* e, int batch, int s_x, int s_y, const double* z0,
+                                double* traj_out);
+mglp_status mglp_serial_adjoint(mglp_engine* e, int batch, int s_x, int s_y,
+                                const double* traj_in, const double* lam_n, double* lam_all_out,
+                                double* grads_accum);
+
+/* LayerStack::step / adjoint_step (blocks.cpp:509-514, 566-574) for one layer */
+mglp_status mglp_stack_step(mglp_engine* e, int layer, double dt, int batch, int s_x, int s_y,
+                            const double* z, double* out);
+mglp_status mglp_stack_adjoint_step(mglp_engine* e, int layer, double dt, int batch, int s_x,
+                                    int s_y, const double* z, const double* lam,
+                                    double* grads_accum, double gscale, double* out);
+
+/* ---- device-resident hot path (inputs already in HBM; no host sync) ----
+ * Pointers are device fp32 buffers of state_elems() floats (x then y).
+ * These are what bench.py times; mglp_engine_stream() is the CUDA stream
+ * every launch goes to. */
+mglp_status mglp_engine_set_shape(mglp_engine* e, int batch, int s_x, int s_y,
+                                  long long* state_elems);
+mglp_status mglp_engine_stream(mglp_engine* e, void** cuda_stream);
+mglp_status mglp_engine_forward_device(mglp_engine* e, const float* z0_dev);
+mglp_status mglp_engine_backward_device(mglp_engine* e, const float* lam_n_dev,
+                                        float* lam0_dev, int want_grads);
+mglp_status mglp_serial_forward_device(mglp_engine* e, const float* z0_dev);
+mglp_status mglp_serial_adjoint_device(mglp_engine* e, const float* lam_n_dev, float* lam0_dev,
+                                       int want_grads);
+mglp_status mglp_engine_zero_grads(mglp_engine* e);
+/* flat (visit_params order) += device gradient bank */
+mglp_status mglp_engine_get_grads(mglp_engine* e, double* flat, long long n);
+/* PhaseTrace of the last forward (which=0) or backward (which=1) solve */
+mglp_status mglp_engine_trace(mglp_engine* e, int which, double* trace_out, int max_trace,
+                              int* n_trace, int* converged);
+/* device pointer of the trajectory (total_layers+1 states) */
+mglp_status mglp_engine_traj_device(mglp_engine* e, float** traj);
+mglp_status mglp_engine_sync(mglp_engine* e);
+/* hot-path kernel launches issued since the last call (then reset) */
+mglp_status mglp_engine_take_launch_count(mglp_engine* e, long long* n);
+
+/* ---- controller (controller.hpp:63-155) ----
+ * Pure decision rule, evaluated on the device from the device-resident
+ * residual traces of the last forward and backward solves:
+ * f = last_pair_factor(trace) for each phase, decision = decide(...)
+ * (0 keep, 1 increase iterations, 2 switch to serial). On "increase", the
+ * engine's fwd/bwd iteration budgets are doubled (capped), as
+ * InexactnessMonitor::record does (controller.hpp:126-147). */
+mglp_status mglp_monitor_record(mglp_engine* e, double threshold, int policy_switch,
+                                int max_iter_cap, double* fwd_factor, double* bwd_factor,
+                                int* decision);
+
+/* ---- test hook: one GEMM family on device buffers ----
+ * C_g[M,N] = A_g . B_g^T (+ bias), g < G; A_g at A + g*a_slot (row stride
+ * lda; [M,K] or, if a_mn, [K,M]); B likewise ([N,K] or [K,N]); C at
+ * C + g*c_slot, row stride ldc. engine 0 = tcgen05 tf32x3 (the product
+ * kernel), 1 = fp32 CUDA-core reference. b_presplit exercises the
+ * pre-split (hi/lo) weight path of the tensor-core kernel. Synchronous. */
+mglp_status mglp_test_gemm(int G, int M, int N, int K, const float* A, long long a_slot, int lda,
+                           int a_mn, const float* B, long long b_slot, int ldb, int b_mn,
+                           int b_presplit, const float* bias, float* C, long long c_slot, int ldc,
+                           int engine);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MGLP_CUDA_H_ */

@@ -591,7 +591,12 @@ class MgritSolver:
         return r
 
     def norm_of(self, rows):
-        return math.sqrt(sum(self.sys.norm_sq(x) for x in rows))
+        # plain left-to-right accumulation (mgrit.hpp:189-193); Python's
+        # built-in sum() is compensated since 3.12 and would differ
+        s = 0.0
+        for x in rows:
+            s += self.sys.norm_sq(x)
+        return math.sqrt(s)
 
     def restrict_to(self, level, fine_rows):
         c, f = self.lv[level], self.lv[level - 1]

@@ -1,0 +1,567 @@
+// extern "C" boundary (include/mglp_cuda.h) over the C++ engine. Exceptions
+// never cross it: ValidationError -> 1, everything else -> 2 (errors.hpp:25-35).
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/mglp_cuda.h"
+#include "engine.h"
+
+using namespace mglp;
+
+struct mglp_engine {
+  std::unique_ptr<Engine> eng;
+  // host staging for the f64 <-> fp32 boundary
+  float* dz = nullptr;
+  float* dl = nullptr;
+  float* dl0 = nullptr;
+  long long cap = 0;
+  int B = 0, sx = 0, sy = 0;
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+template <class F>
+mglp_status guard(F&& f) {
+  try {
+    f();
+    return MGLP_OK;
+  } catch (const ValidationError& e) {
+    g_err = e.what();
+    return MGLP_VALIDATION_ERROR;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return MGLP_CONTRACT_VIOLATION;
+  } catch (...) {
+    g_err = "unknown error";
+    return MGLP_CONTRACT_VIOLATION;
+  }
+}
+
+void need(const void* p, const char* what) {
+  if (!p) throw ValidationError(std::string(what) + " must not be null");
+}
+
+struct Shape {
+  long long n_logical;  // B*(sx+sy)*d
+  long long n_dev;      // padded device state size
+};
+
+Shape ensure_shape(mglp_engine* e, int batch, int s_x, int s_y, int d) {
+  e->eng->set_shape(batch, s_x, s_y);
+  const long long nd = e->eng->state_elems();
+  if (nd > e->cap) {
+    for (float* p : {e->dz, e->dl, e->dl0})
+      if (p) cudaFree(p);
+    MGLP_CUDA(cudaMalloc(&e->dz, nd * sizeof(float)));
+    MGLP_CUDA(cudaMalloc(&e->dl, nd * sizeof(float)));
+    MGLP_CUDA(cudaMalloc(&e->dl0, nd * sizeof(float)));
+    e->cap = nd;
+  }
+  e->B = batch;
+  e->sx = s_x;
+  e->sy = s_y;
+  return Shape{(long long)batch * (s_x + s_y) * d, nd};
+}
+
+void upload(mglp_engine* e, float* dst, const double* src, const Shape& sh) {
+  std::vector<float> h(sh.n_dev, 0.f);
+  for (long long i = 0; i < sh.n_logical; ++i) h[i] = (float)src[i];
+  MGLP_CUDA(cudaMemcpyAsync(dst, h.data(), sh.n_dev * sizeof(float), cudaMemcpyHostToDevice,
+                            e->eng->stream()));
+  MGLP_CUDA(cudaStreamSynchronize(e->eng->stream()));
+}
+
+void download(mglp_engine* e, double* dst, const float* src, const Shape& sh, long long count) {
+  std::vector<float> h(sh.n_dev * count);
+  MGLP_CUDA(cudaMemcpyAsync(h.data(), src, h.size() * sizeof(float), cudaMemcpyDeviceToHost,
+                            e->eng->stream()));
+  MGLP_CUDA(cudaStreamSynchronize(e->eng->stream()));
+  for (long long s = 0; s < count; ++s)
+    for (long long i = 0; i < sh.n_logical; ++i) dst[s * sh.n_logical + i] = h[s * sh.n_dev + i];
+}
+
+void upload_traj(mglp_engine* e, const double* traj, const Shape& sh) {
+  const long long T = e->eng->total_layers() + 1;
+  std::vector<float> h(sh.n_dev * T, 0.f);
+  for (long long s = 0; s < T; ++s)
+    for (long long i = 0; i < sh.n_logical; ++i) h[s * sh.n_dev + i] = (float)traj[s * sh.n_logical + i];
+  MGLP_CUDA(cudaMemcpyAsync(e->eng->traj_dev(), h.data(), h.size() * sizeof(float),
+                            cudaMemcpyHostToDevice, e->eng->stream()));
+  MGLP_CUDA(cudaStreamSynchronize(e->eng->stream()));
+}
+
+void put_trace(mglp_engine* e, bool fwd, double* out, int max_trace, int* n, int* conv) {
+  std::vector<double> t;
+  bool c = false;
+  e->eng->read_trace(fwd, &t, &c);
+  if (out)
+    for (int i = 0; i < (int)t.size() && i < max_trace; ++i) out[i] = t[i];
+  if (n) *n = (int)t.size();
+  if (conv) *conv = c ? 1 : 0;
+}
+
+__global__ void monitor_kernel(const SolveCtrl* f, const SolveCtrl* b, double* out) {
+  // last_pair_factor (controller.hpp:63-67) on both device traces
+  auto factor = [](const SolveCtrl* c) {
+    const int n = min(c->n_trace, kMaxTrace);
+    if (n < 2 || c->trace[n - 2] == 0.0) return 0.0;
+    return c->trace[n - 1] / c->trace[n - 2];
+  };
+  out[0] = factor(f);
+  out[1] = factor(b);
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* mglp_last_error(void) { return g_err.c_str(); }
+
+const char* mglp_version(void) {
+  return "mglp-b200 sm_100a tcgen05 kind::tf32 x3 (fp32 accumulate)";
+}
+
+mglp_status mglp_engine_create(const mglp_stack_desc* stack, const mglp_solve_config* solve,
+                               int device, mglp_engine** out) {
+  return guard([&] {
+    need(stack, "stack");
+    need(solve, "solve");
+    need(out, "out");
+    StackDesc sd;
+    sd.kind = stack->kind;
+    sd.d = stack->d;
+    sd.heads = stack->heads;
+    sd.ffn = stack->ffn;
+    sd.n_enc = stack->n_enc;
+    sd.n_dec = stack->n_dec;
+    sd.buffer_open = stack->buffer_open;
+    sd.buffer_close = stack->buffer_close;
+    sd.ln_eps = stack->ln_eps;
+    sd.base_h = stack->base_h;
+    sd.dropout = stack->dropout;
+    sd.init_std = stack->init_std;
+    sd.depth_scaled_init = stack->depth_scaled_init;
+    SolveCfg c;
+    c.coarsen = solve->coarsen;
+    c.levels = solve->levels;
+    c.fwd_iters = solve->fwd_iters;
+    c.bwd_iters = solve->bwd_iters;
+    c.fwd_tol = solve->fwd_tol;
+    c.bwd_tol = solve->bwd_tol;
+    c.cold_guess = solve->cold_guess;
+    c.warm_start = solve->warm_start;
+    int ndev = 0;
+    MGLP_CUDA(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev) throw ValidationError("device index out of range");
+    auto* h = new mglp_engine;
+    try {
+      h->eng = std::make_unique<Engine>(sd, c, device, nullptr);
+    } catch (...) {
+      delete h;
+      throw;
+    }
+    *out = h;
+  });
+}
+
+mglp_status mglp_engine_destroy(mglp_engine* e) {
+  return guard([&] {
+    if (!e) return;
+    cudaSetDevice(e->eng->device());
+    for (float* p : {e->dz, e->dl, e->dl0})
+      if (p) cudaFree(p);
+    delete e;
+  });
+}
+
+mglp_status mglp_engine_info(mglp_engine* e, int* total, int* ib, int* ie, long long* np) {
+  return guard([&] {
+    need(e, "engine");
+    if (total) *total = e->eng->total_layers();
+    if (ib) *ib = e->eng->interior_begin();
+    if (ie) *ie = e->eng->interior_end();
+    if (np) *np = e->eng->num_params();
+  });
+}
+
+mglp_status mglp_engine_step_size(mglp_engine* e, int layer, double* h) {
+  return guard([&] {
+    need(e, "engine");
+    if (layer < 0 || layer >= e->eng->total_layers()) throw ValidationError("layer out of range");
+    *h = e->eng->step_size(layer);
+  });
+}
+
+mglp_status mglp_engine_init_params(mglp_engine* e, unsigned long long seed, double* flat_out) {
+  return guard([&] {
+    need(e, "engine");
+    std::vector<double> flat;
+    e->eng->init_params(seed, &flat);
+    e->eng->set_params(flat.data());
+    if (flat_out) std::memcpy(flat_out, flat.data(), flat.size() * sizeof(double));
+  });
+}
+
+mglp_status mglp_engine_set_params(mglp_engine* e, const double* flat, long long n) {
+  return guard([&] {
+    need(e, "engine");
+    need(flat, "flat");
+    if (n != e->eng->num_params()) throw ValidationError("set_params: parameter count mismatch");
+    e->eng->set_params(flat);
+  });
+}
+
+mglp_status mglp_engine_get_params(mglp_engine* e, double* flat, long long n) {
+  return guard([&] {
+    need(e, "engine");
+    need(flat, "flat");
+    if (n != e->eng->num_params()) throw ValidationError("get_params: parameter count mismatch");
+    e->eng->get_params(flat);
+  });
+}
+
+mglp_status mglp_engine_get_config(mglp_engine* e, mglp_solve_config* cfg) {
+  return guard([&] {
+    need(e, "engine");
+    need(cfg, "cfg");
+    const SolveCfg& c = e->eng->config();
+    cfg->coarsen = c.coarsen;
+    cfg->levels = c.levels;
+    cfg->fwd_iters = c.fwd_iters;
+    cfg->bwd_iters = c.bwd_iters;
+    cfg->fwd_tol = c.fwd_tol;
+    cfg->bwd_tol = c.bwd_tol;
+    cfg->cold_guess = c.cold_guess;
+    cfg->warm_start = c.warm_start;
+  });
+}
+
+mglp_status mglp_engine_set_config(mglp_engine* e, const mglp_solve_config* cfg) {
+  return guard([&] {
+    need(e, "engine");
+    need(cfg, "cfg");
+    SolveCfg& c = e->eng->config();
+    if (cfg->coarsen != c.coarsen || cfg->levels != c.levels)
+      throw ValidationError("set_config: the hierarchy (coarsen, levels) is fixed at creation");
+    c.fwd_iters = cfg->fwd_iters;
+    c.bwd_iters = cfg->bwd_iters;
+    c.fwd_tol = cfg->fwd_tol;
+    c.bwd_tol = cfg->bwd_tol;
+    c.cold_guess = cfg->cold_guess;
+    c.warm_start = cfg->warm_start;
+  });
+}
+
+mglp_status mglp_engine_forward(mglp_engine* e, int batch, int s_x, int s_y, const double* z0,
+                                double* traj_out, double* trace_out, int max_trace, int* n_trace,
+                                int* converged) {
+  return guard([&] {
+    need(e, "engine");
+    need(z0, "z0");
+    const Shape sh = ensure_shape(e, batch, s_x, s_y, e->eng->width());
+    upload(e, e->dz, z0, sh);
+    e->eng->forward_device(e->dz);
+    if (traj_out) download(e, traj_out, e->eng->traj_dev(), sh, e->eng->total_layers() + 1);
+    put_trace(e, true, trace_out, max_trace, n_trace, converged);
+  });
+}
+
+mglp_status mglp_engine_backward(mglp_engine* e, int batch, int s_x, int s_y,
+                                 const double* traj_in, const double* lam_n, double* lam0_out,
+                                 double* grads_accum, double* trace_out, int max_trace,
+                                 int* n_trace, int* converged) {
+  return guard([&] {
+    need(e, "engine");
+    need(lam_n, "lam_n");
+    if (!traj_in && (batch != e->B || s_x != e->sx || s_y != e->sy))
+      throw ValidationError("backward: no device trajectory for this shape; pass traj_in");
+    const Shape sh = ensure_shape(e, batch, s_x, s_y, e->eng->width());
+    if (traj_in) upload_traj(e, traj_in, sh);
+    upload(e, e->dl, lam_n, sh);
+    if (grads_accum) e->eng->zero_grads();
+    e->eng->backward_device(e->dl, e->dl0, grads_accum != nullptr, traj_in == nullptr);
+    if (lam0_out) download(e, lam0_out, e->dl0, sh, 1);
+    if (grads_accum) e->eng->get_grads(grads_accum);
+    put_trace(e, false, trace_out, max_trace, n_trace, converged);
+  });
+}
+
+mglp_status mglp_engine_snapshot(mglp_engine* e) {
+  return guard([&] {
+    need(e, "engine");
+    e->eng->snapshot();
+  });
+}
+
+mglp_status mglp_engine_restore(mglp_engine* e) {
+  return guard([&] {
+    need(e, "engine");
+    e->eng->restore();
+  });
+}
+
+mglp_status mglp_engine_reset(mglp_engine* e) {
+  return guard([&] {
+    need(e, "engine");
+    e->eng->reset();
+  });
+}
+
+mglp_status mglp_serial_forward(mglp_engine* e, int batch, int s_x, int s_y, const double* z0,
+                                double* traj_out) {
+  return guard([&] {
+    need(e, "engine");
+    need(z0, "z0");
+    const Shape sh = ensure_shape(e, batch, s_x, s_y, e->eng->width());
+    upload(e, e->dz, z0, sh);
+    e->eng->serial_forward_device(e->dz);
+    if (traj_out)
+      download(e, traj_out, e->eng->traj_dev(), sh, e->eng->total_layers() + 1);
+    else
+      MGLP_CUDA(cudaStreamSynchronize(e->eng->stream()));
+  });
+}
+
+mglp_status mglp_serial_adjoint(mglp_engine* e, int batch, int s_x, int s_y,
+                                const double* traj_in, const double* lam_n, double* lam_all_out,
+                                double* grads_accum) {
+  return guard([&] {
+    need(e, "engine");
+    need(lam_n, "lam_n");
+    if (!traj_in && (batch != e->B || s_x != e->sx || s_y != e->sy))
+      throw ValidationError("serial_adjoint: no device trajectory for this shape; pass traj_in");
+    const Shape sh = ensure_shape(e, batch, s_x, s_y, e->eng->width());
+    if (traj_in) {
+      upload_traj(e, traj_in, sh);
+      e->eng->invalidate_linearization();
+    }
+    upload(e, e->dl, lam_n, sh);
+    if (grads_accum) e->eng->zero_grads();
+    e->eng->serial_adjoint_device(e->dl, e->dl0, grads_accum != nullptr);
+    if (lam_all_out)
+      download(e, lam_all_out, e->eng->lam_all_dev(), sh, e->eng->total_layers() + 1);
+    if (grads_accum) e->eng->get_grads(grads_accum);
+    MGLP_CUDA(cudaStreamSynchronize(e->eng->stream()));
+  });
+}
+
+mglp_status mglp_stack_step(mglp_engine* e, int layer, double dt, int batch, int s_x, int s_y,
+                            const double* z, double* out) {
+  return guard([&] {
+    need(e, "engine");
+    need(z, "z");
+    need(out, "out");
+    const Shape sh = ensure_shape(e, batch, s_x, s_y, e->eng->width());
+    upload(e, e->dz, z, sh);
+    e->eng->step_device(layer, dt, e->dz, e->dl0);
+    download(e, out, e->dl0, sh, 1);
+  });
+}
+
+mglp_status mglp_stack_adjoint_step(mglp_engine* e, int layer, double dt, int batch, int s_x,
+                                    int s_y, const double* z, const double* lam,
+                                    double* grads_accum, double gscale, double* out) {
+  return guard([&] {
+    need(e, "engine");
+    need(z, "z");
+    need(lam, "lam");
+    need(out, "out");
+    const Shape sh = ensure_shape(e, batch, s_x, s_y, e->eng->width());
+    upload(e, e->dz, z, sh);
+    upload(e, e->dl, lam, sh);
+    if (grads_accum) e->eng->zero_grads();
+    e->eng->adjoint_step_device(layer, dt, e->dz, e->dl, e->dl0, grads_accum != nullptr, gscale);
+    download(e, out, e->dl0, sh, 1);
+    if (grads_accum) e->eng->get_grads(grads_accum);
+  });
+}
+
+mglp_status mglp_engine_set_shape(mglp_engine* e, int batch, int s_x, int s_y,
+                                  long long* state_elems) {
+  return guard([&] {
+    need(e, "engine");
+    const Shape sh = ensure_shape(e, batch, s_x, s_y, e->eng->width());
+    if (state_elems) *state_elems = sh.n_dev;
+  });
+}
+
+mglp_status mglp_engine_stream(mglp_engine* e, void** s) {
+  return guard([&] {
+    need(e, "engine");
+    need(s, "stream");
+    *s = (void*)e->eng->stream();
+  });
+}
+
+mglp_status mglp_engine_forward_device(mglp_engine* e, const float* z0_dev) {
+  return guard([&] {
+    need(e, "engine");
+    need(z0_dev, "z0_dev");
+    e->eng->forward_device(z0_dev);
+  });
+}
+
+mglp_status mglp_engine_backward_device(mglp_engine* e, const float* lam_n_dev, float* lam0_dev,
+                                        int want_grads) {
+  return guard([&] {
+    need(e, "engine");
+    need(lam_n_dev, "lam_n_dev");
+    e->eng->backward_device(lam_n_dev, lam0_dev, want_grads != 0, true);
+  });
+}
+
+mglp_status mglp_serial_forward_device(mglp_engine* e, const float* z0_dev) {
+  return guard([&] {
+    need(e, "engine");
+    need(z0_dev, "z0_dev");
+    e->eng->serial_forward_device(z0_dev);
+  });
+}
+
+mglp_status mglp_serial_adjoint_device(mglp_engine* e, const float* lam_n_dev, float* lam0_dev,
+                                       int want_grads) {
+  return guard([&] {
+    need(e, "engine");
+    need(lam_n_dev, "lam_n_dev");
+    e->eng->serial_adjoint_device(lam_n_dev, lam0_dev, want_grads != 0);
+  });
+}
+
+mglp_status mglp_engine_zero_grads(mglp_engine* e) {
+  return guard([&] {
+    need(e, "engine");
+    e->eng->zero_grads();
+  });
+}
+
+mglp_status mglp_engine_get_grads(mglp_engine* e, double* flat, long long n) {
+  return guard([&] {
+    need(e, "engine");
+    need(flat, "flat");
+    if (n != e->eng->num_params()) throw ValidationError("get_grads: parameter count mismatch");
+    e->eng->get_grads(flat);
+  });
+}
+
+mglp_status mglp_engine_trace(mglp_engine* e, int which, double* trace_out, int max_trace,
+                              int* n_trace, int* converged) {
+  return guard([&] {
+    need(e, "engine");
+    put_trace(e, which == 0, trace_out, max_trace, n_trace, converged);
+  });
+}
+
+mglp_status mglp_engine_traj_device(mglp_engine* e, float** traj) {
+  return guard([&] {
+    need(e, "engine");
+    need(traj, "traj");
+    *traj = e->eng->traj_dev();
+  });
+}
+
+mglp_status mglp_engine_sync(mglp_engine* e) {
+  return guard([&] {
+    need(e, "engine");
+    MGLP_CUDA(cudaStreamSynchronize(e->eng->stream()));
+    MGLP_CUDA(cudaGetLastError());
+  });
+}
+
+mglp_status mglp_engine_take_launch_count(mglp_engine* e, long long* n) {
+  return guard([&] {
+    need(e, "engine");
+    need(n, "n");
+    *n = e->eng->launch_count();
+    e->eng->reset_launch_count();
+  });
+}
+
+mglp_status mglp_monitor_record(mglp_engine* e, double threshold, int policy_switch,
+                                int max_iter_cap, double* fwd_factor, double* bwd_factor,
+                                int* decision) {
+  return guard([&] {
+    need(e, "engine");
+    if (threshold <= 0.0) throw ValidationError("decide: threshold must be positive");
+    double* d_out = nullptr;
+    MGLP_CUDA(cudaMalloc(&d_out, 2 * sizeof(double)));
+    monitor_kernel<<<1, 1, 0, e->eng->stream()>>>(e->eng->ctrl(true), e->eng->ctrl(false), d_out);
+    double h[2];
+    MGLP_CUDA(cudaMemcpyAsync(h, d_out, sizeof h, cudaMemcpyDeviceToHost, e->eng->stream()));
+    MGLP_CUDA(cudaStreamSynchronize(e->eng->stream()));
+    cudaFree(d_out);
+    // decide (controller.hpp:71-84) + InexactnessMonitor::record's budget update (126-147)
+    const double worst = std::max(h[0], h[1]);
+    SolveCfg& c = e->eng->config();
+    int dec = 0;
+    if (worst > threshold) {
+      if (policy_switch)
+        dec = 2;
+      else
+        dec = (c.fwd_iters < max_iter_cap || c.bwd_iters < max_iter_cap) ? 1 : 2;
+    }
+    if (dec == 1) {
+      c.fwd_iters = std::min(2 * c.fwd_iters, max_iter_cap);
+      c.bwd_iters = std::min(2 * c.bwd_iters, max_iter_cap);
+    }
+    if (fwd_factor) *fwd_factor = h[0];
+    if (bwd_factor) *bwd_factor = h[1];
+    if (decision) *decision = dec;
+  });
+}
+
+mglp_status mglp_test_gemm(int G, int M, int N, int K, const float* A, long long a_slot, int lda,
+                           int a_mn, const float* B, long long b_slot, int ldb, int b_mn,
+                           int b_presplit, const float* bias, float* Cp, long long c_slot, int ldc,
+                           int engine) {
+  return guard([&] {
+    need(A, "A");
+    need(B, "B");
+    need(Cp, "C");
+    GemmArgs g;
+    g.G = G;
+    g.M = M;
+    g.N = N;
+    g.K = K;
+    g.A.ptr = const_cast<float*>(A);
+    g.A.slot_stride = a_slot;
+    g.A.ld = lda;
+    g.a_mn = a_mn != 0;
+    g.B.ptr = const_cast<float*>(B);
+    g.B.slot_stride = b_slot;
+    g.B.ld = ldb;
+    g.b_mn = b_mn != 0;
+    g.ep.kind = EPI_STORE;
+    g.ep.out1.ptr = Cp;
+    g.ep.out1.slot_stride = c_slot;
+    g.ep.out1.ld = ldc;
+    if (bias) {
+      g.ep.bias.ptr = const_cast<float*>(bias);
+      g.ep.bias.slot_stride = 0;
+    }
+    float *hi = nullptr, *lo = nullptr;
+    if (b_presplit) {
+      const long long rows = b_mn ? K : N;
+      const long long n = (long long)(G - 1) * b_slot + rows * ldb;
+      MGLP_CUDA(cudaMalloc(&hi, n * sizeof(float)));
+      MGLP_CUDA(cudaMalloc(&lo, n * sizeof(float)));
+      launch_split_tf32(hi, lo, B, n, 0);
+      g.B.ptr = hi;
+      g.Blo = g.B;
+      g.Blo.ptr = lo;
+    }
+    if (engine == 0)
+      launch_gemm_tc(g, nullptr, 0);
+    else
+      launch_gemm_simt(g, nullptr, 0);
+    MGLP_CUDA(cudaGetLastError());
+    MGLP_CUDA(cudaDeviceSynchronize());
+    if (hi) cudaFree(hi);
+    if (lo) cudaFree(lo);
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,211 @@
+// Shared device/host types for the MGRIT hot path on sm_100a.
+//
+// Every kernel works on a *family* of G independent problems launched at once
+// (the coarse intervals of one relaxation sweep, the layers of the parameter
+// pass, ...). Member g of a family lives at an affine slot index
+// slot0 + g * step of a strided buffer (a state array, an activation arena,
+// the per-layer parameter slab), which is what `Mat` describes. This is the
+// B200 replacement for the reference's per-chunk Executor tasks
+// (executor.cpp:75-110, mgrit.hpp:125-187): one launch covers every chunk.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+
+namespace mglp {
+
+// Error taxonomy of the reference (errors.hpp:25-35): ValidationError is a
+// user-input problem (C-ABI status 1), ContractViolation a broken invariant
+// (status 2).
+struct ValidationError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct ContractViolation : std::logic_error {
+  using std::logic_error::logic_error;
+};
+
+#define MGLP_CUDA(x)                                                            \
+  do {                                                                          \
+    cudaError_t e_ = (x);                                                       \
+    if (e_ != cudaSuccess)                                                      \
+      throw ::mglp::ContractViolation(std::string("CUDA error: ") +             \
+                                      cudaGetErrorString(e_) + " at " +         \
+                                      __FILE__ + ":" + std::to_string(__LINE__)); \
+  } while (0)
+
+// A strided family of row-major fp32 matrices. Member g starts at
+// ptr + (slot0 + g*step) * slot_stride; rows are ld elements apart.
+struct Mat {
+  float* ptr = nullptr;
+  long long slot_stride = 0;  // elements between consecutive slots
+  int ld = 0;                 // row stride (elements)
+  int slot0 = 0;
+  int step = 1;
+  __host__ __device__ __forceinline__ float* at(int g) const {
+    return ptr + (long long)(slot0 + g * step) * slot_stride;
+  }
+  __host__ __device__ __forceinline__ bool ok() const { return ptr != nullptr; }
+  __host__ Mat slot(int s0, int st) const {
+    Mat m = *this;
+    m.slot0 = s0;
+    m.step = st;
+    return m;
+  }
+  __host__ Mat offset(long long elems) const {
+    Mat m = *this;
+    m.ptr += elems;
+    return m;
+  }
+};
+
+// How the propagated value p = z + dt*F of one evaluation is folded into the
+// solver state -- the four update forms of mgrit.hpp:
+//   PLAIN : v[j] = p                                   (relax_update, level 0; 273-277)
+//   FAS   : v[j] = base[j] + ((p - phib[j]) + rho[j])  (relax_update, level>0; 279-280)
+//   RES0  : r[j] = p - v[j], plus sum r^2              (residual_rows, level 0; 177)
+//   RESL  : r[j] = ((p - phib[j]) + rho[j]) - (v[j] - base[j])   (179-180)
+//   NONE  : value discarded (linearization-only evaluation)
+enum CombineMode : int { CM_PLAIN = 0, CM_FAS = 1, CM_RES0 = 2, CM_RESL = 3, CM_NONE = 4 };
+
+struct Combine {
+  int mode = CM_NONE;
+  float dt = 0.f;
+  Mat z;  // the state the step starts from (p = z + dt*F)
+  Mat out, base, phib, rho, v;
+  double* norm_partials = nullptr;  // RES0: one f64 partial per CTA, fixed order
+  int norm_base = 0;
+};
+
+__device__ __forceinline__ float combine_apply(const Combine& c, int g, long long off_out,
+                                               long long off_z, float F, double& r2) {
+  const float p = c.z.at(g)[off_z] + c.dt * F;
+  switch (c.mode) {
+    case CM_PLAIN:
+      c.out.at(g)[off_out] = p;
+      break;
+    case CM_FAS: {
+      const float corr = (p - c.phib.at(g)[off_out]) + c.rho.at(g)[off_out];
+      c.out.at(g)[off_out] = c.base.at(g)[off_out] + corr;
+    } break;
+    case CM_RES0: {
+      const float r = p - c.v.at(g)[off_out];
+      c.out.at(g)[off_out] = r;
+      r2 += (double)r * (double)r;
+    } break;
+    case CM_RESL: {
+      const float lhs = (p - c.phib.at(g)[off_out]) + c.rho.at(g)[off_out];
+      const float r = lhs - (c.v.at(g)[off_out] - c.base.at(g)[off_out]);
+      c.out.at(g)[off_out] = r;
+    } break;
+    default:
+      break;
+  }
+  return p;
+}
+
+// GEMM epilogues. acc is the fp32 accumulator of C = A.B^T (row `row`, column
+// `col`); everything else is fused here so the activations of one layer are
+// written exactly once (tensor.cpp:205-218 linear = x W^T + b, blocks.cpp:246-292).
+enum EpiKind : int {
+  EPI_STORE = 0,      // out1 = acc (+ bias)
+  EPI_BIAS_ADD2 = 1,  // a = acc + bias; o1 = add1 ? add1 + a : a -> out1; out2 = add2 + o1
+  EPI_BIAS_GELU = 2,  // h = acc + bias -> out1; gelu(h) -> out2
+  EPI_FINAL = 3,      // mo = acc + bias; F = add1 + mo; p = z + dt*F; combine
+  EPI_GELU_BWD = 4,   // out1 = acc * gelu'(aux)            (tensor.cpp:360-372)
+  EPI_GRAD_ACC = 5,   // out1 += gscale * acc               (blocks.cpp:108, 126-129)
+};
+
+struct EpiArgs {
+  int kind = EPI_STORE;
+  Mat out1, out2, add1, add2, aux;
+  Mat bias;  // bias vector family (slot = layer); null => no bias
+  float gscale = 1.f;
+  Combine cmb;  // EPI_FINAL
+};
+
+constexpr float kGeluC = 0.7978845608028654f;  // tensor.cpp:345
+constexpr float kGeluA = 0.044715f;            // tensor.cpp:346
+
+__device__ __forceinline__ float gelu_f(float v) {
+  const float t = tanhf(kGeluC * (v + kGeluA * v * v * v));
+  return 0.5f * v * (1.f + t);
+}
+
+__device__ __forceinline__ float gelu_grad_f(float v, float u) {
+  const float t = tanhf(kGeluC * (v + kGeluA * v * v * v));
+  const float dtanh = (1.f - t * t) * kGeluC * (1.f + 3.f * kGeluA * v * v);
+  return u * (0.5f * (1.f + t) + 0.5f * v * dtanh);
+}
+
+// Applies the epilogue to n consecutive columns [col0, col0+n) of one output
+// row. Returns this row-segment's contribution to the residual norm^2.
+__device__ __forceinline__ double epilogue_row(const EpiArgs& e, int g, int row, int col0,
+                                               const float* acc, int n) {
+  double r2 = 0.0;
+  const float* bias = e.bias.ok() ? e.bias.at(g) : nullptr;
+  switch (e.kind) {
+    case EPI_STORE: {
+      float* o = e.out1.at(g) + (long long)row * e.out1.ld + col0;
+      for (int i = 0; i < n; ++i) o[i] = bias ? acc[i] + bias[col0 + i] : acc[i];
+    } break;
+    case EPI_BIAS_ADD2: {
+      float* o1 = e.out1.ok() ? e.out1.at(g) + (long long)row * e.out1.ld + col0 : nullptr;
+      float* o2 = e.out2.ok() ? e.out2.at(g) + (long long)row * e.out2.ld + col0 : nullptr;
+      const float* a1 = e.add1.ok() ? e.add1.at(g) + (long long)row * e.add1.ld + col0 : nullptr;
+      const float* a2 = e.add2.at(g) + (long long)row * e.add2.ld + col0;
+      for (int i = 0; i < n; ++i) {
+        const float a = bias ? acc[i] + bias[col0 + i] : acc[i];
+        const float v1 = a1 ? a1[i] + a : a;
+        if (o1) o1[i] = v1;
+        if (o2) o2[i] = a2[i] + v1;
+      }
+    } break;
+    case EPI_BIAS_GELU: {
+      float* o1 = e.out1.at(g) + (long long)row * e.out1.ld + col0;
+      float* o2 = e.out2.at(g) + (long long)row * e.out2.ld + col0;
+      for (int i = 0; i < n; ++i) {
+        const float hv = bias ? acc[i] + bias[col0 + i] : acc[i];
+        o1[i] = hv;
+        o2[i] = gelu_f(hv);
+      }
+    } break;
+    case EPI_FINAL: {
+      const float* a1 = e.add1.at(g) + (long long)row * e.add1.ld + col0;
+      const long long off_out = (long long)row * e.cmb.out.ld + col0;
+      const long long off_z = (long long)row * e.cmb.z.ld + col0;
+      for (int i = 0; i < n; ++i) {
+        const float mo = bias ? acc[i] + bias[col0 + i] : acc[i];
+        const float F = a1[i] + mo;
+        combine_apply(e.cmb, g, off_out + i, off_z + i, F, r2);
+      }
+    } break;
+    case EPI_GELU_BWD: {
+      float* o = e.out1.at(g) + (long long)row * e.out1.ld + col0;
+      const float* hv = e.aux.at(g) + (long long)row * e.aux.ld + col0;
+      for (int i = 0; i < n; ++i) o[i] = gelu_grad_f(hv[i], acc[i]);
+    } break;
+    case EPI_GRAD_ACC: {
+      float* o = e.out1.at(g) + (long long)row * e.out1.ld + col0;
+      for (int i = 0; i < n; ++i) o[i] = o[i] + e.gscale * acc[i];
+    } break;
+  }
+  return r2;
+}
+
+// GEMM problem family: for g < G, C_g[M,N] = A_g . B_g^T with
+//   A_g [M,K] row-major ("K-major") or, if a_mn, stored [K,M] ("MN-major");
+//   B_g [N,K] row-major, or if b_mn stored [K,N].
+// B may come pre-split into tf32 hi/lo parts (weights); see gemm_tc.cu.
+struct GemmArgs {
+  int G = 1, M = 0, N = 0, K = 0;
+  Mat A, B, Blo;
+  bool a_mn = false, b_mn = false;
+  EpiArgs ep;
+};
+
+inline int ceil_div(long long a, long long b) { return (int)((a + b - 1) / b); }
+
+}  // namespace mglp

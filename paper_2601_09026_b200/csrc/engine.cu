@@ -1,0 +1,1720 @@
+// Host orchestration of the device-resident MGRIT forward solve and adjoint
+// MGRIT backpropagation. See engine.h for the map to the reference.
+#include "engine.h"
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstring>
+#include <thread>
+
+namespace mglp {
+
+namespace {
+
+// ---- counter-based RNG, bit-identical to rng.hpp:37-89 ------------------------
+inline uint64_t splitmix64(uint64_t x) {
+  x += 0x9e3779b97f4a7c15ULL;
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
+  return x ^ (x >> 31);
+}
+inline uint64_t derive(uint64_t seed, uint64_t a, uint64_t b, uint64_t c, uint64_t d) {
+  uint64_t s = splitmix64(seed ^ 0x243f6a8885a308d3ULL);
+  s = splitmix64(s ^ a);
+  s = splitmix64(s ^ b);
+  s = splitmix64(s ^ c);
+  s = splitmix64(s ^ d);
+  return s;
+}
+inline double u01(uint64_t bits) { return static_cast<double>(bits >> 11) * 0x1.0p-53; }
+inline double gaussian(uint64_t seed, uint64_t a, uint64_t b, uint64_t c, uint64_t d) {
+  const uint64_t k1 = derive(seed, a, b, c, d);
+  const uint64_t k2 = splitmix64(k1 ^ 0x452821e638d01377ULL);
+  double x1 = u01(k1);
+  const double x2 = u01(k2);
+  if (x1 <= 0.0) x1 = 0x1.0p-53;
+  return std::sqrt(-2.0 * std::log(x1)) * std::cos(6.283185307179586 * x2);
+}
+inline double truncated_gaussian(double stddev, uint64_t seed, uint64_t a, uint64_t b,
+                                 uint64_t c) {
+  for (uint64_t attempt = 0;; ++attempt) {
+    const double g = gaussian(seed, a, b, c, attempt);
+    if (g >= -2.0 && g <= 2.0) return g * stddev;
+  }
+}
+inline uint64_t fnv1a(const std::string& s) {
+  uint64_t h = 0xcbf29ce484222325ULL;
+  for (char ch : s) {
+    h ^= static_cast<unsigned char>(ch);
+    h *= 0x100000001b3ULL;
+  }
+  return h;
+}
+inline long long align32(long long n) { return (n + 31) & ~31LL; }
+
+bool depth_scaled_component(const std::string& c) {  // blocks.cpp:368-372
+  return c == "attn.v.w" || c == "attn.o.w" || c == "self.v.w" || c == "self.o.w" ||
+         c == "cross.v.w" || c == "cross.o.w" || c == "mlp.in.w" || c == "mlp.out.w";
+}
+
+Mat state_mat(float* base, long long n, int d, int slot0, int step) {
+  Mat m;
+  m.ptr = base;
+  m.slot_stride = n;
+  m.ld = d;
+  m.slot0 = slot0;
+  m.step = step;
+  return m;
+}
+
+Mat shift(Mat m, int g0) {
+  m.slot0 += g0 * m.step;
+  return m;
+}
+
+}  // namespace
+
+// =============================================================================
+// construction, parameters
+// =============================================================================
+
+Engine::Engine(const StackDesc& sd, const SolveCfg& cfg, int device,
+               std::shared_ptr<Transport> tr)
+    : sd_(sd), cfg_(cfg), device_(device), tr_(std::move(tr)) {
+  if (sd_.d <= 0 || sd_.heads <= 0 || sd_.ffn <= 0)
+    throw ValidationError("LayerStack: width, heads, ffn must be positive");
+  if (sd_.d % sd_.heads != 0) throw ValidationError("LayerStack: head count must divide width");
+  if (sd_.d % 4 != 0 || sd_.ffn % 4 != 0)
+    throw ValidationError("device stack: width and ffn must be multiples of 4");
+  if ((sd_.d / sd_.heads) % 4 != 0 || sd_.d / sd_.heads > 64)
+    throw ValidationError("device stack: head width must be a multiple of 4 and <= 64");
+  if (sd_.dropout > 0.0)
+    throw ValidationError("device stack: dropout > 0 is not supported on the device path");
+  switch (sd_.kind) {
+    case 0:
+      if (sd_.n_enc <= 0) throw ValidationError("LayerStack: n_enc must be positive");
+      total_ = n_split_ = sd_.n_enc;
+      break;
+    case 1:
+      if (sd_.n_dec <= 0) throw ValidationError("LayerStack: n_dec must be positive");
+      total_ = n_split_ = sd_.n_dec;
+      causal_ = true;
+      break;
+    case 2:
+      if (sd_.n_enc <= 0 || sd_.n_dec <= 0)
+        throw ValidationError("LayerStack: encoder-decoder needs both n_enc and n_dec");
+      total_ = sd_.n_enc + sd_.n_dec;
+      n_split_ = sd_.n_enc;
+      break;
+    default:
+      throw ValidationError("LayerStack: unknown model kind");
+  }
+  if (sd_.buffer_open < 0 || sd_.buffer_close < 0 ||
+      sd_.buffer_open + sd_.buffer_close >= total_)
+    throw ValidationError("LayerStack: buffer layers must leave a non-empty interior");
+  ib_ = sd_.buffer_open;
+  ie_ = total_ - sd_.buffer_close;
+  N_ = ie_ - ib_;
+  h_.assign(total_, sd_.base_h);  // blocks.cpp:421-430
+  if (sd_.buffer_open + sd_.buffer_close > 0)
+    for (int i = 0; i < total_; ++i)
+      h_[i] = (i < ib_ || i >= ie_) ? 1.0 : 1.0 / static_cast<double>(N_);
+  // MgritSolver construction checks (mgrit.hpp:68-95)
+  if (cfg_.coarsen < 2) throw ValidationError("MgritSolver: coarsening factor must be >= 2");
+  if (cfg_.levels < 1) throw ValidationError("MgritSolver: need at least one level");
+  long long stride = 1;
+  for (int l = 0; l < std::max(cfg_.levels - 1, 1); ++l) {
+    stride *= cfg_.coarsen;
+    if (stride > N_)
+      throw ValidationError("MgritSolver: too many levels, the coarsest would hold no full step");
+  }
+  if (N_ % stride != 0)
+    throw ValidationError("MgritSolver: step count must be divisible by coarsen^(levels-1)");
+  if (tr_ && tr_->size() > 1)
+    throw ValidationError("multi-rank engines are created through the distributed front end");
+
+  MGLP_CUDA(cudaSetDevice(device_));
+  MGLP_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+  build_layouts();
+  const size_t pbytes = (size_t)total_ * layer_stride_ * sizeof(float);
+  MGLP_CUDA(cudaMalloc(&P_, pbytes));
+  MGLP_CUDA(cudaMalloc(&Phi_, pbytes));
+  MGLP_CUDA(cudaMalloc(&Plo_, pbytes));
+  MGLP_CUDA(cudaMalloc(&Gr_, pbytes));
+  MGLP_CUDA(cudaMemsetAsync(P_, 0, pbytes, stream_));
+  MGLP_CUDA(cudaMemsetAsync(Phi_, 0, pbytes, stream_));
+  MGLP_CUDA(cudaMemsetAsync(Plo_, 0, pbytes, stream_));
+  MGLP_CUDA(cudaMemsetAsync(Gr_, 0, pbytes, stream_));
+  Gmax_ = std::max(1, N_ / cfg_.coarsen);
+  cache_valid_.assign(total_, 0);
+}
+
+Engine::~Engine() {
+  cudaSetDevice(device_);
+  if (stream_) cudaStreamSynchronize(stream_);
+  free_solver(fwd_);
+  free_solver(bwd_);
+  for (float* p : {P_, Phi_, Plo_, Gr_, scratch_, cache_, bscratch_, traj_, lam_all_,
+                   zero_state_, snap_fwd_, snap_bwd_})
+    if (p) cudaFree(p);
+  if (stream_) cudaStreamDestroy(stream_);
+}
+
+void Engine::build_layouts() {
+  const long long d = sd_.d, f = sd_.ffn;
+  lay_.resize(2);
+  for (int kind = 0; kind < 2; ++kind) {
+    LayerLayout& L = lay_[kind];
+    L.decoder = kind == 1;
+    long long off = 0;
+    auto take = [&](long long n) {
+      const long long o = off;
+      off += align32(n);
+      return o;
+    };
+    L.ln1_g = take(d);
+    L.ln1_b = take(d);
+    L.w_qkv = take(3 * d * d);
+    L.b_qkv = take(3 * d);
+    L.w_o = take(d * d);
+    L.b_o = take(d);
+    if (L.decoder) {
+      L.ln3_g = take(d);
+      L.ln3_b = take(d);
+      L.w_cq = take(d * d);
+      L.b_cq = take(d);
+      L.w_ckv = take(2 * d * d);
+      L.b_ckv = take(2 * d);
+      L.w_co = take(d * d);
+      L.b_co = take(d);
+    }
+    L.ln2_g = take(d);
+    L.ln2_b = take(d);
+    L.w_in = take(f * d);
+    L.b_in = take(f);
+    L.w_out = take(d * f);
+    L.b_out = take(d);
+    L.size = off;
+    // visit_params order (blocks.cpp:627-646)
+    long long fo = 0;
+    auto piece = [&](long long dev, long long n) {
+      L.pieces.push_back(Piece{fo, dev, n});
+      fo += n;
+    };
+    piece(L.ln1_g, d);
+    piece(L.ln1_b, d);
+    for (int q = 0; q < 3; ++q) {  // q, k, v
+      piece(L.w_qkv + q * d * d, d * d);
+      piece(L.b_qkv + q * d, d);
+    }
+    piece(L.w_o, d * d);
+    piece(L.b_o, d);
+    if (L.decoder) {
+      piece(L.ln3_g, d);
+      piece(L.ln3_b, d);
+      piece(L.w_cq, d * d);
+      piece(L.b_cq, d);
+      piece(L.w_ckv, d * d);
+      piece(L.b_ckv, d);
+      piece(L.w_ckv + d * d, d * d);
+      piece(L.b_ckv + d, d);
+      piece(L.w_co, d * d);
+      piece(L.b_co, d);
+    }
+    piece(L.ln2_g, d);
+    piece(L.ln2_b, d);
+    piece(L.w_in, f * d);
+    piece(L.b_in, f);
+    piece(L.w_out, d * f);
+    piece(L.b_out, d);
+    L.flat_size = fo;
+  }
+  layer_stride_ = std::max(lay_[0].size, sd_.kind == 2 ? lay_[1].size : 0LL);
+  n_params_flat_ = 0;
+  for (int l = 0; l < total_; ++l)
+    n_params_flat_ += lay_[(sd_.kind == 2 && l >= n_split_) ? 1 : 0].flat_size;
+}
+
+// LayerStack constructor initialisation (blocks.cpp:432-449), bit-identical
+// f64 values; runs on the host threads.
+void Engine::init_params(uint64_t seed, std::vector<double>* flat_out) {
+  static const char* enc_names[] = {"ln1.gain", "ln1.bias", "attn.q.w", "attn.q.b", "attn.k.w",
+                                    "attn.k.b", "attn.v.w", "attn.v.b", "attn.o.w", "attn.o.b",
+                                    "ln2.gain", "ln2.bias", "mlp.in.w", "mlp.in.b", "mlp.out.w",
+                                    "mlp.out.b"};
+  static const char* dec_names[] = {
+      "ln1.gain",  "ln1.bias",  "self.q.w",  "self.q.b",  "self.k.w",  "self.k.b",  "self.v.w",
+      "self.v.b",  "self.o.w",  "self.o.b",  "ln3.gain",  "ln3.bias",  "cross.q.w", "cross.q.b",
+      "cross.k.w", "cross.k.b", "cross.v.w", "cross.v.b", "cross.o.w", "cross.o.b", "ln2.gain",
+      "ln2.bias",  "mlp.in.w",  "mlp.in.b",  "mlp.out.w", "mlp.out.b"};
+  std::vector<double>& flat = *flat_out;
+  flat.assign(n_params_flat_, 0.0);
+  std::vector<long long> layer_flat(total_ + 1, 0);
+  for (int l = 0; l < total_; ++l)
+    layer_flat[l + 1] = layer_flat[l] + lay_[(sd_.kind == 2 && l >= n_split_) ? 1 : 0].flat_size;
+  const double depth_factor =
+      sd_.depth_scaled_init ? std::sqrt(std::log(2.0 * static_cast<double>(total_))) : 1.0;
+  // work items: (layer, piece) -- weights dominate, split them across threads
+  struct Item {
+    int layer, piece;
+  };
+  std::vector<Item> items;
+  for (int l = 0; l < total_; ++l) {
+    const int k = (sd_.kind == 2 && l >= n_split_) ? 1 : 0;
+    for (int p = 0; p < (int)lay_[k].pieces.size(); ++p) items.push_back({l, p});
+  }
+  unsigned nt = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+  std::vector<std::thread> th;
+  std::atomic<size_t> next{0};
+  for (unsigned t = 0; t < nt; ++t)
+    th.emplace_back([&] {
+      for (;;) {
+        const size_t i = next.fetch_add(1);
+        if (i >= items.size()) return;
+        const int l = items[i].layer;
+        const int k = (sd_.kind == 2 && l >= n_split_) ? 1 : 0;
+        const Piece& pc = lay_[k].pieces[items[i].piece];
+        const std::string comp = k ? dec_names[items[i].piece] : enc_names[items[i].piece];
+        double* t = flat.data() + layer_flat[l] + pc.flat_off;
+        if (comp.size() >= 4 && comp.compare(comp.size() - 4, 4, "gain") == 0) {
+          for (long long e = 0; e < pc.n; ++e) t[e] = 1.0;
+        } else if (comp.back() == 'w') {
+          double sd = sd_.init_std;
+          if (depth_scaled_component(comp)) sd *= depth_factor;
+          const uint64_t site = fnv1a(comp);
+          for (long long e = 0; e < pc.n; ++e)
+            t[e] = truncated_gaussian(sd, seed, 1 /*kInit*/,
+                                      (uint64_t)l * 1000003u + site, (uint64_t)e);
+        } else {
+          for (long long e = 0; e < pc.n; ++e) t[e] = 0.0;
+        }
+      }
+    });
+  for (auto& t : th) t.join();
+}
+
+void Engine::set_params(const double* flat) {
+  std::vector<float> host((size_t)total_ * layer_stride_, 0.f);
+  long long fo = 0;
+  for (int l = 0; l < total_; ++l) {
+    const LayerLayout& L = lay_[(sd_.kind == 2 && l >= n_split_) ? 1 : 0];
+    float* dst = host.data() + (size_t)l * layer_stride_;
+    for (const Piece& p : L.pieces)
+      for (long long e = 0; e < p.n; ++e) dst[p.dev_off + e] = (float)flat[fo + p.flat_off + e];
+    fo += L.flat_size;
+  }
+  MGLP_CUDA(cudaSetDevice(device_));
+  const size_t n = host.size();
+  MGLP_CUDA(cudaMemcpyAsync(P_, host.data(), n * sizeof(float), cudaMemcpyHostToDevice, stream_));
+  launch_split_tf32(Phi_, Plo_, P_, (long long)n, stream_);
+  MGLP_CUDA(cudaStreamSynchronize(stream_));
+}
+
+void Engine::get_params(double* flat) const {
+  std::vector<float> host((size_t)total_ * layer_stride_);
+  MGLP_CUDA(cudaMemcpy(host.data(), P_, host.size() * sizeof(float), cudaMemcpyDeviceToHost));
+  long long fo = 0;
+  for (int l = 0; l < total_; ++l) {
+    const LayerLayout& L = lay_[(sd_.kind == 2 && l >= n_split_) ? 1 : 0];
+    const float* src = host.data() + (size_t)l * layer_stride_;
+    for (const Piece& p : L.pieces)
+      for (long long e = 0; e < p.n; ++e) flat[fo + p.flat_off + e] = src[p.dev_off + e];
+    fo += L.flat_size;
+  }
+}
+
+void Engine::get_grads(double* flat) const {
+  MGLP_CUDA(cudaStreamSynchronize(stream_));
+  std::vector<float> host((size_t)total_ * layer_stride_);
+  MGLP_CUDA(cudaMemcpy(host.data(), Gr_, host.size() * sizeof(float), cudaMemcpyDeviceToHost));
+  long long fo = 0;
+  for (int l = 0; l < total_; ++l) {
+    const LayerLayout& L = lay_[(sd_.kind == 2 && l >= n_split_) ? 1 : 0];
+    const float* src = host.data() + (size_t)l * layer_stride_;
+    for (const Piece& p : L.pieces)
+      for (long long e = 0; e < p.n; ++e) flat[fo + p.flat_off + e] += src[p.dev_off + e];
+    fo += L.flat_size;
+  }
+}
+
+void Engine::zero_grads() {
+  MGLP_CUDA(cudaMemsetAsync(Gr_, 0, (size_t)total_ * layer_stride_ * sizeof(float), stream_));
+}
+
+// =============================================================================
+// shape-dependent buffers
+// =============================================================================
+
+void Engine::set_shape(int batch, int s_x, int s_y) {
+  if (batch == B_ && s_x == sx_ && s_y == sy_ && traj_) return;
+  if (batch <= 0 || s_x <= 0) throw ValidationError("shape: batch and s_x must be positive");
+  if ((sd_.kind == 2) != (s_y > 0))
+    throw ValidationError("shape: s_y > 0 exactly for encoder-decoder stacks");
+  MGLP_CUDA(cudaSetDevice(device_));
+  MGLP_CUDA(cudaStreamSynchronize(stream_));
+  free_solver(fwd_);
+  free_solver(bwd_);
+  for (float** p : {&scratch_, &cache_, &bscratch_, &traj_, &lam_all_, &zero_state_, &snap_fwd_,
+                    &snap_bwd_}) {
+    if (*p) cudaFree(*p);
+    *p = nullptr;
+  }
+  B_ = batch;
+  sx_ = s_x;
+  sy_ = s_y;
+  Tx_ = B_ * sx_;
+  Ty_ = B_ * sy_;
+  const long long d = sd_.d, f = sd_.ffn, H = sd_.heads;
+  x_off_ = 0;
+  y_off_ = (long long)Tx_ * d;
+  state_n_ = align32((long long)(Tx_ + Ty_) * d);
+  const long long R = std::max(Tx_, sd_.kind == 2 ? Ty_ : 0);
+  const long long smax = std::max(sx_, sy_);
+  long long off = 0;
+  auto take = [&](long long n) {
+    const long long o = off;
+    off += align32(std::max(n, 1LL));
+    return o;
+  };
+  ActLayout& a = al_;
+  a.n1 = take(R * d);
+  a.qkv = take(R * 3 * d);
+  a.ctx = take(R * d);
+  a.lse = take(B_ * H * smax);
+  a.a1 = take(R * d);
+  a.u = take(R * d);
+  a.n2 = take(R * d);
+  a.h = take(R * f);
+  a.g = take(R * f);
+  a.st1 = take(2 * R);
+  a.st2 = take(2 * R);
+  if (sd_.kind == 2) {
+    a.n3 = take(Ty_ * d);
+    a.u3 = take(Ty_ * d);
+    a.cq = take(Ty_ * d);
+    a.ckv = take((long long)Tx_ * 2 * d);
+    a.cctx = take(Ty_ * d);
+    a.clse = take(B_ * H * sy_);
+    a.ybar = take(Ty_ * d);
+    a.st3 = take(2LL * Ty_);
+  }
+  a.size = off;
+  off = 0;
+  BwdLayout& b = bl_;
+  b.dh = take(R * f);
+  b.dn2 = take(R * d);
+  b.du = take(R * d);
+  b.da1 = take(R * d);
+  b.dctx = take(R * d);
+  b.dqkv = take(R * 3 * d);
+  b.dn1 = take(R * d);
+  b.dd = take(B_ * H * smax);
+  if (sd_.kind == 2) {
+    b.dybar = take(Ty_ * d);
+    b.dy = take(Ty_ * d);
+    b.dcctx = take(Ty_ * d);
+    b.dcq = take(Ty_ * d);
+    b.dckv = take((long long)Tx_ * 2 * d);
+    b.dn3 = take(Ty_ * d);
+    b.dxe = take((long long)Tx_ * d);
+    b.dd2 = take(B_ * H * sy_);
+  }
+  b.size = off;
+  MGLP_CUDA(cudaMalloc(&scratch_, (size_t)Gmax_ * al_.size * sizeof(float)));
+  MGLP_CUDA(cudaMalloc(&cache_, (size_t)total_ * al_.size * sizeof(float)));
+  MGLP_CUDA(cudaMalloc(&bscratch_, (size_t)Gmax_ * bl_.size * sizeof(float)));
+  MGLP_CUDA(cudaMalloc(&traj_, (size_t)(total_ + 1) * state_n_ * sizeof(float)));
+  MGLP_CUDA(cudaMalloc(&lam_all_, (size_t)(total_ + 1) * state_n_ * sizeof(float)));
+  MGLP_CUDA(cudaMalloc(&zero_state_, (size_t)state_n_ * sizeof(float)));
+  MGLP_CUDA(cudaMemsetAsync(traj_, 0, (size_t)(total_ + 1) * state_n_ * sizeof(float), stream_));
+  MGLP_CUDA(cudaMemsetAsync(lam_all_, 0, (size_t)(total_ + 1) * state_n_ * sizeof(float), stream_));
+  MGLP_CUDA(cudaMemsetAsync(zero_state_, 0, (size_t)state_n_ * sizeof(float), stream_));
+  alloc_solver(fwd_, false);
+  alloc_solver(bwd_, true);
+  std::fill(cache_valid_.begin(), cache_valid_.end(), 0);
+  first_fwd_ = first_bwd_ = true;
+  MGLP_CUDA(cudaStreamSynchronize(stream_));
+}
+
+void Engine::alloc_solver(Solver& s, bool adjoint) {
+  s.adjoint = adjoint;
+  const int L = cfg_.levels;
+  s.lv.assign(std::max(L, 2), Level{});
+  int n = N_;
+  for (int l = 0; l < (int)s.lv.size(); ++l) {
+    s.lv[l].n = n;
+    if (l + 1 < (int)s.lv.size()) n /= cfg_.coarsen;
+  }
+  // level 0 of the forward solver is the trajectory window traj[ib..ie]
+  if (adjoint) {
+    MGLP_CUDA(cudaMalloc(&s.lv[0].v, (size_t)(N_ + 1) * state_n_ * sizeof(float)));
+    MGLP_CUDA(cudaMemsetAsync(s.lv[0].v, 0, (size_t)(N_ + 1) * state_n_ * sizeof(float), stream_));
+  } else {
+    s.lv[0].v = traj_ + (size_t)ib_ * state_n_;
+  }
+  for (int l = 1; l < (int)s.lv.size(); ++l) {
+    const size_t bytes = (size_t)(s.lv[l].n + 1) * state_n_ * sizeof(float);
+    MGLP_CUDA(cudaMalloc(&s.lv[l].v, bytes));
+    MGLP_CUDA(cudaMalloc(&s.lv[l].rho, bytes));
+    MGLP_CUDA(cudaMalloc(&s.lv[l].phib, bytes));
+    MGLP_CUDA(cudaMemsetAsync(s.lv[l].v, 0, bytes, stream_));
+    MGLP_CUDA(cudaMemsetAsync(s.lv[l].rho, 0, bytes, stream_));  // rho[0] stays 0
+    MGLP_CUDA(cudaMemsetAsync(s.lv[l].phib, 0, bytes, stream_));
+  }
+  MGLP_CUDA(cudaMalloc(&s.ctrl, sizeof(SolveCtrl)));
+  MGLP_CUDA(cudaMemsetAsync(s.ctrl, 0, sizeof(SolveCtrl), stream_));
+  // norm partials: generous upper bound on CTAs contributing to one residual
+  const long long per_state = (long long)ceil_div(std::max(Tx_, Ty_), 8) +
+                              elem_combine_blocks(state_n_) +
+                              (long long)ceil_div(std::max(Tx_, Ty_), 64) *
+                                  ceil_div(sd_.d, 64) + 64;
+  s.n_partials = (int)(per_state * (N_ / cfg_.coarsen + 1) * 2);
+  MGLP_CUDA(cudaMalloc(&s.partials, (size_t)s.n_partials * sizeof(double)));
+}
+
+void Engine::free_solver(Solver& s) {
+  if (s.lv.empty()) return;
+  if (s.adjoint && s.lv[0].v) cudaFree(s.lv[0].v);
+  for (size_t l = 1; l < s.lv.size(); ++l) {
+    cudaFree(s.lv[l].v);
+    cudaFree(s.lv[l].rho);
+    cudaFree(s.lv[l].phib);
+  }
+  if (s.ctrl) cudaFree(s.ctrl);
+  if (s.partials) cudaFree(s.partials);
+  s = Solver{};
+}
+
+// =============================================================================
+// operand helpers
+// =============================================================================
+
+Mat Engine::act_mat(const ActRef& r, long long off, int ld) const {
+  Mat m;
+  m.ptr = r.base + off;
+  m.slot_stride = r.stride;
+  m.ld = ld;
+  m.slot0 = r.slot0;
+  m.step = r.step;
+  return m;
+}
+Mat Engine::bwd_mat(long long off, int ld) const {
+  Mat m;
+  m.ptr = bscratch_ + off;
+  m.slot_stride = bl_.size;
+  m.ld = ld;
+  return m;
+}
+Mat Engine::par(long long off, int ld, int layer0, int step) const {
+  Mat m;
+  m.ptr = P_ + off;
+  m.slot_stride = layer_stride_;
+  m.ld = ld;
+  m.slot0 = layer0;
+  m.step = step;
+  return m;
+}
+Mat Engine::par_hi(long long off, int ld, int layer0, int step) const {
+  Mat m = par(off, ld, layer0, step);
+  m.ptr = Phi_ + off;
+  return m;
+}
+Mat Engine::par_lo(long long off, int ld, int layer0, int step) const {
+  Mat m = par(off, ld, layer0, step);
+  m.ptr = Plo_ + off;
+  return m;
+}
+Mat Engine::grad(long long off, int ld, int layer0, int step) const {
+  Mat m = par(off, ld, layer0, step);
+  m.ptr = Gr_ + off;
+  return m;
+}
+
+void Engine::gemm(GemmArgs g) {
+  ++launches_;
+#ifdef MGLP_GEMM_SIMT
+  launch_gemm_simt(g, active_, stream_);
+#else
+  launch_gemm_tc(g, active_, stream_);
+#endif
+}
+
+int Engine::gemm_blocks(const GemmArgs& g) const {
+#ifdef MGLP_GEMM_SIMT
+  return gemm_simt_blocks(g);
+#else
+  return gemm_tc_blocks(g);
+#endif
+}
+
+int Engine::take_partials(int n) {
+  const int b = pcursor_;
+  pcursor_ += n;
+  if (pcursor_ > pcap_) throw ContractViolation("residual-norm partial buffer overflow");
+  return b;
+}
+
+// =============================================================================
+// Phi: one layer step z + dt*F(z) for a family of G layers (blocks.cpp:466-514)
+// =============================================================================
+
+void Engine::eval_forward(const EvalSpec& e0) {
+  // split families that straddle the encoder/decoder boundary
+  if (sd_.kind == 2) {
+    const int first = e0.layer0, last = e0.layer0 + (e0.G - 1) * e0.layer_step;
+    const bool fdec = first >= n_split_, ldec = last >= n_split_;
+    if (fdec != ldec) {
+      int gsplit = 0;
+      while (gsplit < e0.G && ((e0.layer0 + gsplit * e0.layer_step >= n_split_) == fdec)) ++gsplit;
+      auto part = [&](int g0, int G) {
+        EvalSpec e = e0;
+        e.G = G;
+        e.layer0 = e0.layer0 + g0 * e0.layer_step;
+        e.in = shift(e0.in, g0);
+        e.lam = shift(e0.lam, g0);
+        e.act.slot0 += g0 * e0.act.step;
+        Combine& c = e.cmb;
+        c.z = shift(c.z, g0);
+        c.out = shift(c.out, g0);
+        c.base = shift(c.base, g0);
+        c.phib = shift(c.phib, g0);
+        c.rho = shift(c.rho, g0);
+        c.v = shift(c.v, g0);
+        return e;
+      };
+      eval_forward(part(0, gsplit));
+      eval_forward(part(gsplit, e0.G - gsplit));
+      return;
+    }
+  }
+  EvalSpec e = e0;
+  e.cmb.z = e.in;
+  e.cmb.dt = e.dt;
+  const int d = sd_.d;
+  if (sd_.kind == 2 && e.layer0 >= n_split_) {
+    decoder_forward(e);
+  } else {
+    Mat yp;
+    if (sd_.kind == 2) yp = e.in.offset(y_off_);
+    encoder_forward(e, Tx_, causal_, e.in.offset(x_off_), yp);
+  }
+  (void)d;
+}
+
+void Engine::encoder_forward(const EvalSpec& e, int R, bool causal, Mat X, Mat Ypass) {
+  const int d = sd_.d, f = sd_.ffn, G = e.G;
+  const LayerLayout& L = lay_[0];
+  const int l0 = e.layer0, ls = e.layer_step;
+  X.ld = d;
+  Mat n1 = act_mat(e.act, al_.n1, d), qkv = act_mat(e.act, al_.qkv, 3 * d);
+  Mat ctx = act_mat(e.act, al_.ctx, d), lse = act_mat(e.act, al_.lse, 0);
+  Mat a1 = act_mat(e.act, al_.a1, d), u = act_mat(e.act, al_.u, d);
+  Mat n2 = act_mat(e.act, al_.n2, d), hh = act_mat(e.act, al_.h, f), gg = act_mat(e.act, al_.g, f);
+  Mat st1 = act_mat(e.act, al_.st1, 2), st2 = act_mat(e.act, al_.st2, 2);
+
+  LnFwdArgs ln;
+  ln.G = G;
+  ln.rows = R;
+  ln.d = d;
+  ln.eps = (float)sd_.ln_eps;
+  ln.x = X;
+  ln.out = n1;
+  ln.stats = st1;
+  ln.gain = par(L.ln1_g, 0, l0, ls);
+  ln.bias = par(L.ln1_b, 0, l0, ls);
+  ++launches_;
+  launch_ln_fwd(ln, active_, stream_);
+
+  GemmArgs g;
+  g.G = G;
+  g.M = R;
+  g.N = 3 * d;
+  g.K = d;
+  g.A = n1;
+  g.B = par_hi(L.w_qkv, d, l0, ls);
+  g.Blo = par_lo(L.w_qkv, d, l0, ls);
+  g.ep.kind = EPI_STORE;
+  g.ep.out1 = qkv;
+  g.ep.bias = par(L.b_qkv, 0, l0, ls);
+  gemm(g);
+
+  AttnArgs at;
+  at.G = G;
+  at.B = B_;
+  at.H = sd_.heads;
+  at.dh = d / sd_.heads;
+  at.sq = at.skv = R / B_;
+  at.causal = causal;
+  at.scale = (float)(1.0 / std::sqrt((double)at.dh));
+  at.q = qkv;
+  at.k = qkv.offset(d);
+  at.v = qkv.offset(2 * d);
+  at.o = ctx;
+  at.lse = lse;
+  ++launches_;
+  launch_attn_fwd(at, active_, stream_);
+
+  g = GemmArgs{};
+  g.G = G;
+  g.M = R;
+  g.N = d;
+  g.K = d;
+  g.A = ctx;
+  g.B = par_hi(L.w_o, d, l0, ls);
+  g.Blo = par_lo(L.w_o, d, l0, ls);
+  g.ep.kind = EPI_BIAS_ADD2;
+  g.ep.out1 = a1;
+  g.ep.out2 = u;
+  g.ep.add2 = X;
+  g.ep.bias = par(L.b_o, 0, l0, ls);
+  gemm(g);
+
+  ln.x = u;
+  ln.out = n2;
+  ln.stats = st2;
+  ln.gain = par(L.ln2_g, 0, l0, ls);
+  ln.bias = par(L.ln2_b, 0, l0, ls);
+  ++launches_;
+  launch_ln_fwd(ln, active_, stream_);
+
+  g = GemmArgs{};
+  g.G = G;
+  g.M = R;
+  g.N = f;
+  g.K = d;
+  g.A = n2;
+  g.B = par_hi(L.w_in, d, l0, ls);
+  g.Blo = par_lo(L.w_in, d, l0, ls);
+  g.ep.kind = EPI_BIAS_GELU;
+  g.ep.out1 = hh;
+  g.ep.out2 = gg;
+  g.ep.bias = par(L.b_in, 0, l0, ls);
+  gemm(g);
+
+  g = GemmArgs{};
+  g.G = G;
+  g.M = R;
+  g.N = d;
+  g.K = f;
+  g.A = gg;
+  g.B = par_hi(L.w_out, f, l0, ls);
+  g.Blo = par_lo(L.w_out, f, l0, ls);
+  g.ep.kind = EPI_FINAL;
+  g.ep.add1 = a1;
+  g.ep.bias = par(L.b_out, 0, l0, ls);
+  Combine c = e.cmb;
+  const long long xo = (Ypass.ok() || sd_.kind == 2) ? x_off_ : 0;
+  auto off = [&](Mat m) { return m.ok() ? m.offset(xo) : m; };
+  c.z = off(c.z);
+  c.out = off(c.out);
+  c.base = off(c.base);
+  c.phib = off(c.phib);
+  c.rho = off(c.rho);
+  c.v = off(c.v);
+  for (Mat* m : {&c.z, &c.out, &c.base, &c.phib, &c.rho, &c.v}) m->ld = d;
+  if (c.mode == CM_RES0) c.norm_base = take_partials(gemm_blocks(g));
+  g.ep.cmb = c;
+  gemm(g);
+  if (Ypass.ok() && e.cmb.mode != CM_NONE) {
+    ElemCombineArgs ec;
+    ec.G = G;
+    ec.n = (long long)Ty_ * d;
+    Combine cy = e.cmb;
+    for (Mat* m : {&cy.z, &cy.out, &cy.base, &cy.phib, &cy.rho, &cy.v})
+      if (m->ok()) *m = m->offset(y_off_);
+    if (cy.mode == CM_RES0) cy.norm_base = take_partials(G * elem_combine_blocks(ec.n));
+    ec.cmb = cy;
+    ++launches_;
+    launch_elem_combine(ec, active_, stream_);
+  }
+}
+
+void Engine::decoder_forward(const EvalSpec& e) {
+  const int d = sd_.d, f = sd_.ffn, G = e.G;
+  const LayerLayout& L = lay_[1];
+  const int l0 = e.layer0, ls = e.layer_step;
+  const int R = Ty_;
+  Mat Y = e.in.offset(y_off_), X = e.in.offset(x_off_);
+  Y.ld = X.ld = d;
+  Mat n1 = act_mat(e.act, al_.n1, d), qkv = act_mat(e.act, al_.qkv, 3 * d);
+  Mat ctx = act_mat(e.act, al_.ctx, d), lse = act_mat(e.act, al_.lse, 0);
+  Mat a1 = act_mat(e.act, al_.a1, d), u2 = act_mat(e.act, al_.u, d);
+  Mat n2 = act_mat(e.act, al_.n2, d), hh = act_mat(e.act, al_.h, f), gg = act_mat(e.act, al_.g, f);
+  Mat st1 = act_mat(e.act, al_.st1, 2), st2 = act_mat(e.act, al_.st2, 2);
+  Mat n3 = act_mat(e.act, al_.n3, d), u3 = act_mat(e.act, al_.u3, d);
+  Mat cq = act_mat(e.act, al_.cq, d), ckv = act_mat(e.act, al_.ckv, 2 * d);
+  Mat cctx = act_mat(e.act, al_.cctx, d), clse = act_mat(e.act, al_.clse, 0);
+  Mat ybar = act_mat(e.act, al_.ybar, d), st3 = act_mat(e.act, al_.st3, 2);
+
+  LnFwdArgs ln;
+  ln.G = G;
+  ln.rows = R;
+  ln.d = d;
+  ln.eps = (float)sd_.ln_eps;
+  ln.x = Y;
+  ln.out = n1;
+  ln.stats = st1;
+  ln.gain = par(L.ln1_g, 0, l0, ls);
+  ln.bias = par(L.ln1_b, 0, l0, ls);
+  ++launches_;
+  launch_ln_fwd(ln, active_, stream_);
+
+  auto mk = [&](int M, int N, int K, Mat A, long long w, int ldw) {
+    GemmArgs g;
+    g.G = G;
+    g.M = M;
+    g.N = N;
+    g.K = K;
+    g.A = A;
+    g.B = par_hi(w, ldw, l0, ls);
+    g.Blo = par_lo(w, ldw, l0, ls);
+    return g;
+  };
+  GemmArgs g = mk(R, 3 * d, d, n1, L.w_qkv, d);
+  g.ep.kind = EPI_STORE;
+  g.ep.out1 = qkv;
+  g.ep.bias = par(L.b_qkv, 0, l0, ls);
+  gemm(g);
+
+  AttnArgs at;
+  at.G = G;
+  at.B = B_;
+  at.H = sd_.heads;
+  at.dh = d / sd_.heads;
+  at.sq = at.skv = sy_;
+  at.causal = 1;
+  at.scale = (float)(1.0 / std::sqrt((double)at.dh));
+  at.q = qkv;
+  at.k = qkv.offset(d);
+  at.v = qkv.offset(2 * d);
+  at.o = ctx;
+  at.lse = lse;
+  ++launches_;
+  launch_attn_fwd(at, active_, stream_);
+
+  g = mk(R, d, d, ctx, L.w_o, d);
+  g.ep.kind = EPI_BIAS_ADD2;
+  g.ep.out1 = a1;
+  g.ep.out2 = u3;
+  g.ep.add2 = Y;
+  g.ep.bias = par(L.b_o, 0, l0, ls);
+  gemm(g);
+
+  ln.x = u3;
+  ln.out = n3;
+  ln.stats = st3;
+  ln.gain = par(L.ln3_g, 0, l0, ls);
+  ln.bias = par(L.ln3_b, 0, l0, ls);
+  ++launches_;
+  launch_ln_fwd(ln, active_, stream_);
+
+  g = mk(R, d, d, n3, L.w_cq, d);
+  g.ep.kind = EPI_STORE;
+  g.ep.out1 = cq;
+  g.ep.bias = par(L.b_cq, 0, l0, ls);
+  gemm(g);
+
+  g = mk(Tx_, 2 * d, d, X, L.w_ckv, d);
+  g.ep.kind = EPI_STORE;
+  g.ep.out1 = ckv;
+  g.ep.bias = par(L.b_ckv, 0, l0, ls);
+  gemm(g);
+
+  at.causal = 0;
+  at.sq = sy_;
+  at.skv = sx_;
+  at.q = cq;
+  at.k = ckv;
+  at.v = ckv.offset(d);
+  at.o = cctx;
+  at.lse = clse;
+  ++launches_;
+  launch_attn_fwd(at, active_, stream_);
+
+  g = mk(R, d, d, cctx, L.w_co, d);
+  g.ep.kind = EPI_BIAS_ADD2;
+  g.ep.out1 = ybar;
+  g.ep.add1 = a1;
+  g.ep.out2 = u2;
+  g.ep.add2 = Y;
+  g.ep.bias = par(L.b_co, 0, l0, ls);
+  gemm(g);
+
+  ln.x = u2;
+  ln.out = n2;
+  ln.stats = st2;
+  ln.gain = par(L.ln2_g, 0, l0, ls);
+  ln.bias = par(L.ln2_b, 0, l0, ls);
+  ++launches_;
+  launch_ln_fwd(ln, active_, stream_);
+
+  g = mk(R, f, d, n2, L.w_in, d);
+  g.ep.kind = EPI_BIAS_GELU;
+  g.ep.out1 = hh;
+  g.ep.out2 = gg;
+  g.ep.bias = par(L.b_in, 0, l0, ls);
+  gemm(g);
+
+  g = mk(R, d, f, gg, L.w_out, f);
+  g.ep.kind = EPI_FINAL;
+  g.ep.add1 = ybar;
+  g.ep.bias = par(L.b_out, 0, l0, ls);
+  Combine c = e.cmb;
+  for (Mat* m : {&c.z, &c.out, &c.base, &c.phib, &c.rho, &c.v})
+    if (m->ok()) {
+      *m = m->offset(y_off_);
+      m->ld = d;
+    }
+  if (c.mode == CM_RES0) c.norm_base = take_partials(gemm_blocks(g));
+  g.ep.cmb = c;
+  gemm(g);
+  if (e.cmb.mode != CM_NONE) {
+    ElemCombineArgs ec;
+    ec.G = G;
+    ec.n = (long long)Tx_ * d;
+    Combine cx = e.cmb;  // x part sits at offset 0
+    if (cx.mode == CM_RES0) cx.norm_base = take_partials(G * elem_combine_blocks(ec.n));
+    ec.cmb = cx;
+    ++launches_;
+    launch_elem_combine(ec, active_, stream_);
+  }
+}
+
+// =============================================================================
+// Phi^T: lambda + dt*(dF/dz)^T lambda (+ parameter grads), blocks.cpp:516-574
+// =============================================================================
+
+void Engine::eval_adjoint(const EvalSpec& e0) {
+  if (sd_.kind == 2) {
+    const int first = e0.layer0, last = e0.layer0 + (e0.G - 1) * e0.layer_step;
+    const bool fdec = first >= n_split_, ldec = last >= n_split_;
+    if (fdec != ldec) {
+      int gsplit = 0;
+      while (gsplit < e0.G && ((e0.layer0 + gsplit * e0.layer_step >= n_split_) == fdec)) ++gsplit;
+      auto part = [&](int g0, int G) {
+        EvalSpec e = e0;
+        e.G = G;
+        e.layer0 = e0.layer0 + g0 * e0.layer_step;
+        e.in = shift(e0.in, g0);
+        e.lam = shift(e0.lam, g0);
+        e.act.slot0 += g0 * e0.act.step;
+        Combine& c = e.cmb;
+        c.z = shift(c.z, g0);
+        c.out = shift(c.out, g0);
+        c.base = shift(c.base, g0);
+        c.phib = shift(c.phib, g0);
+        c.rho = shift(c.rho, g0);
+        c.v = shift(c.v, g0);
+        return e;
+      };
+      eval_adjoint(part(0, gsplit));
+      eval_adjoint(part(gsplit, e0.G - gsplit));
+      return;
+    }
+  }
+  EvalSpec e = e0;
+  e.cmb.z = e.lam;
+  e.cmb.dt = e.dt;
+  if (sd_.kind == 2 && e.layer0 >= n_split_)
+    decoder_adjoint(e);
+  else
+    encoder_adjoint(e, causal_);
+}
+
+void Engine::encoder_adjoint(const EvalSpec& e, bool causal) {
+  const int d = sd_.d, f = sd_.ffn, G = e.G;
+  const LayerLayout& L = lay_[0];
+  const int l0 = e.layer0, ls = e.layer_step;
+  const int R = Tx_;
+  if (G > Gmax_) throw ContractViolation("adjoint family larger than scratch");
+  Mat UP = e.lam.offset(x_off_), X = e.in.offset(x_off_);
+  UP.ld = X.ld = d;
+  Mat qkv = act_mat(e.act, al_.qkv, 3 * d), ctx = act_mat(e.act, al_.ctx, d);
+  Mat lse = act_mat(e.act, al_.lse, 0), u = act_mat(e.act, al_.u, d);
+  Mat hh = act_mat(e.act, al_.h, f), gg = act_mat(e.act, al_.g, f);
+  Mat n1 = act_mat(e.act, al_.n1, d), n2 = act_mat(e.act, al_.n2, d);
+  Mat st1 = act_mat(e.act, al_.st1, 2), st2 = act_mat(e.act, al_.st2, 2);
+  Mat dh = bwd_mat(bl_.dh, f), dn2 = bwd_mat(bl_.dn2, d), du = bwd_mat(bl_.du, d);
+  Mat da1 = bwd_mat(bl_.da1, d), dctx = bwd_mat(bl_.dctx, d), dqkv = bwd_mat(bl_.dqkv, 3 * d);
+  Mat dn1 = bwd_mat(bl_.dn1, d), dd = bwd_mat(bl_.dd, 0);
+
+  auto mk = [&](int M, int N, int K, Mat A, long long w, int ldw) {
+    GemmArgs g;
+    g.G = G;
+    g.M = M;
+    g.N = N;
+    g.K = K;
+    g.A = A;
+    g.B = par_hi(w, ldw, l0, ls);
+    g.Blo = par_lo(w, ldw, l0, ls);
+    g.b_mn = true;  // dX = U . W: W [out,in] read as [K,N]
+    return g;
+  };
+  GemmArgs g = mk(R, f, d, UP, L.w_out, f);
+  g.ep.kind = EPI_GELU_BWD;
+  g.ep.out1 = dh;
+  g.ep.aux = hh;
+  gemm(g);
+
+  g = mk(R, d, f, dh, L.w_in, d);
+  g.ep.kind = EPI_STORE;
+  g.ep.out1 = dn2;
+  gemm(g);
+
+  LnBwdArgs lb;
+  lb.G = G;
+  lb.rows = R;
+  lb.d = d;
+  lb.x = u;
+  lb.stats = st2;
+  lb.up = dn2;
+  lb.gain = par(L.ln2_g, 0, l0, ls);
+  lb.out1 = du;
+  lb.out2 = da1;
+  lb.addB = UP;
+  ++launches_;
+  launch_ln_bwd(lb, active_, stream_);
+
+  g = mk(R, d, d, da1, L.w_o, d);
+  g.ep.kind = EPI_STORE;
+  g.ep.out1 = dctx;
+  gemm(g);
+
+  AttnArgs at;
+  at.G = G;
+  at.B = B_;
+  at.H = sd_.heads;
+  at.dh = d / sd_.heads;
+  at.sq = at.skv = R / B_;
+  at.causal = causal;
+  at.scale = (float)(1.0 / std::sqrt((double)at.dh));
+  at.q = qkv;
+  at.k = qkv.offset(d);
+  at.v = qkv.offset(2 * d);
+  at.o = ctx;
+  at.lse = lse;
+  at.dout = dctx;
+  at.dq = dqkv;
+  at.dk = dqkv.offset(d);
+  at.dv = dqkv.offset(2 * d);
+  at.dd = dd;
+  launches_ += 3;
+  launch_attn_bwd(at, active_, stream_);
+
+  g = mk(R, d, 3 * d, dqkv, L.w_qkv, d);
+  g.ep.kind = EPI_STORE;
+  g.ep.out1 = dn1;
+  gemm(g);
+
+  if (e.cmb.mode != CM_NONE) {
+    LnBwdArgs l1;
+    l1.G = G;
+    l1.rows = R;
+    l1.d = d;
+    l1.x = X;
+    l1.stats = st1;
+    l1.up = dn1;
+    l1.gain = par(L.ln1_g, 0, l0, ls);
+    l1.addA = du;
+    Combine c = e.cmb;
+    for (Mat* m : {&c.z, &c.out, &c.base, &c.phib, &c.rho, &c.v})
+      if (m->ok()) {
+        *m = m->offset(x_off_);
+        m->ld = d;
+      }
+    if (c.mode == CM_RES0) c.norm_base = take_partials(G * ln_bwd_blocks(R));
+    l1.cmb = c;
+    ++launches_;
+    launch_ln_bwd(l1, active_, stream_);
+    if (sd_.kind == 2) {
+      ElemCombineArgs ec;
+      ec.G = G;
+      ec.n = (long long)Ty_ * d;
+      Combine cy = e.cmb;
+      for (Mat* m : {&cy.z, &cy.out, &cy.base, &cy.phib, &cy.rho, &cy.v})
+        if (m->ok()) *m = m->offset(y_off_);
+      if (cy.mode == CM_RES0) cy.norm_base = take_partials(G * elem_combine_blocks(ec.n));
+      ec.cmb = cy;
+      ++launches_;
+      launch_elem_combine(ec, active_, stream_);
+    }
+  }
+
+  if (e.want_grads) {
+    const float gs = e.gscale;
+    auto wg = [&](int M, int N, Mat A, Mat Bm, long long w, int ldw) {
+      GemmArgs w_;
+      w_.G = G;
+      w_.M = M;
+      w_.N = N;
+      w_.K = R;
+      w_.A = A;
+      w_.B = Bm;
+      w_.a_mn = true;
+      w_.b_mn = true;
+      w_.ep.kind = EPI_GRAD_ACC;
+      w_.ep.out1 = grad(w, ldw, l0, ls);
+      w_.ep.gscale = gs;
+      gemm(w_);
+    };
+    auto cr = [&](Mat up, int cols, long long b, Mat x, Mat st, long long gn) {
+      ColRedArgs c;
+      c.G = G;
+      c.rows = R;
+      c.cols = cols;
+      c.up = up;
+      c.x = x;
+      c.stats = st;
+      c.dbias = grad(b, 0, l0, ls);
+      if (x.ok()) c.dgain = grad(gn, 0, l0, ls);
+      c.gscale = gs;
+      ++launches_;
+      launch_colred(c, active_, stream_);
+    };
+    wg(d, f, UP, gg, L.w_out, f);
+    cr(UP, d, L.b_out, Mat{}, Mat{}, 0);
+    wg(f, d, dh, n2, L.w_in, d);
+    cr(dh, f, L.b_in, Mat{}, Mat{}, 0);
+    cr(dn2, d, L.ln2_b, u, st2, L.ln2_g);
+    wg(d, d, da1, ctx, L.w_o, d);
+    cr(da1, d, L.b_o, Mat{}, Mat{}, 0);
+    wg(3 * d, d, dqkv, n1, L.w_qkv, d);
+    cr(dqkv, 3 * d, L.b_qkv, Mat{}, Mat{}, 0);
+    cr(dn1, d, L.ln1_b, X, st1, L.ln1_g);
+  }
+}
+
+void Engine::decoder_adjoint(const EvalSpec& e) {
+  const int d = sd_.d, f = sd_.ffn, G = e.G;
+  const LayerLayout& L = lay_[1];
+  const int l0 = e.layer0, ls = e.layer_step;
+  const int R = Ty_;
+  if (G > Gmax_) throw ContractViolation("adjoint family larger than scratch");
+  Mat UPy = e.lam.offset(y_off_), Y = e.in.offset(y_off_), X = e.in.offset(x_off_);
+  UPy.ld = Y.ld = X.ld = d;
+  Mat qkv = act_mat(e.act, al_.qkv, 3 * d), ctx = act_mat(e.act, al_.ctx, d);
+  Mat lse = act_mat(e.act, al_.lse, 0), u2 = act_mat(e.act, al_.u, d);
+  Mat hh = act_mat(e.act, al_.h, f), gg = act_mat(e.act, al_.g, f);
+  Mat n1 = act_mat(e.act, al_.n1, d), n2 = act_mat(e.act, al_.n2, d);
+  Mat st1 = act_mat(e.act, al_.st1, 2), st2 = act_mat(e.act, al_.st2, 2);
+  Mat n3 = act_mat(e.act, al_.n3, d), u3 = act_mat(e.act, al_.u3, d);
+  Mat cq = act_mat(e.act, al_.cq, d), ckv = act_mat(e.act, al_.ckv, 2 * d);
+  Mat cctx = act_mat(e.act, al_.cctx, d), clse = act_mat(e.act, al_.clse, 0);
+  Mat st3 = act_mat(e.act, al_.st3, 2);
+  Mat dh = bwd_mat(bl_.dh, f), dn2 = bwd_mat(bl_.dn2, d), dy = bwd_mat(bl_.dy, d);
+  Mat dybar = bwd_mat(bl_.dybar, d), dcctx = bwd_mat(bl_.dcctx, d), dcq = bwd_mat(bl_.dcq, d);
+  Mat dckv = bwd_mat(bl_.dckv, 2 * d), dn3 = bwd_mat(bl_.dn3, d), dxe = bwd_mat(bl_.dxe, d);
+  Mat da1 = bwd_mat(bl_.da1, d), dctx = bwd_mat(bl_.dctx, d), dqkv = bwd_mat(bl_.dqkv, 3 * d);
+  Mat dn1 = bwd_mat(bl_.dn1, d), dd = bwd_mat(bl_.dd, 0), dd2 = bwd_mat(bl_.dd2, 0);
+
+  auto mk = [&](int M, int N, int K, Mat A, long long w, int ldw) {
+    GemmArgs g;
+    g.G = G;
+    g.M = M;
+    g.N = N;
+    g.K = K;
+    g.A = A;
+    g.B = par_hi(w, ldw, l0, ls);
+    g.Blo = par_lo(w, ldw, l0, ls);
+    g.b_mn = true;
+    return g;
+  };
+  GemmArgs g = mk(R, f, d, UPy, L.w_out, f);
+  g.ep.kind = EPI_GELU_BWD;
+  g.ep.out1 = dh;
+  g.ep.aux = hh;
+  gemm(g);
+
+  g = mk(R, d, f, dh, L.w_in, d);
+  g.ep.kind = EPI_STORE;
+  g.ep.out1 = dn2;
+  gemm(g);
+
+  LnBwdArgs lb;
+  lb.G = G;
+  lb.rows = R;
+  lb.d = d;
+  lb.x = u2;
+  lb.stats = st2;
+  lb.up = dn2;
+  lb.gain = par(L.ln2_g, 0, l0, ls);
+  lb.out1 = dy;      // du2
+  lb.out2 = dybar;   // up + du2
+  lb.addB = UPy;
+  ++launches_;
+  launch_ln_bwd(lb, active_, stream_);
+
+  g = mk(R, d, d, dybar, L.w_co, d);
+  g.ep.kind = EPI_STORE;
+  g.ep.out1 = dcctx;
+  gemm(g);
+
+  AttnArgs at;
+  at.G = G;
+  at.B = B_;
+  at.H = sd_.heads;
+  at.dh = d / sd_.heads;
+  at.scale = (float)(1.0 / std::sqrt((double)at.dh));
+  at.causal = 0;
+  at.sq = sy_;
+  at.skv = sx_;
+  at.q = cq;
+  at.k = ckv;
+  at.v = ckv.offset(d);
+  at.o = cctx;
+  at.lse = clse;
+  at.dout = dcctx;
+  at.dq = dcq;
+  at.dk = dckv;
+  at.dv = dckv.offset(d);
+  at.dd = dd2;
+  launches_ += 3;
+  launch_attn_bwd(at, active_, stream_);
+
+  g = mk(R, d, d, dcq, L.w_cq, d);
+  g.ep.kind = EPI_STORE;
+  g.ep.out1 = dn3;
+  gemm(g);
+
+  g = mk(Tx_, d, 2 * d, dckv, L.w_ckv, d);
+  g.ep.kind = EPI_STORE;
+  g.ep.out1 = dxe;
+  gemm(g);
+
+  lb.x = u3;
+  lb.stats = st3;
+  lb.up = dn3;
+  lb.gain = par(L.ln3_g, 0, l0, ls);
+  lb.addA = dy;
+  lb.out1 = dy;     // du2 + du3
+  lb.addB = dybar;
+  lb.out2 = da1;    // dybar + du3
+  ++launches_;
+  launch_ln_bwd(lb, active_, stream_);
+
+  g = mk(R, d, d, da1, L.w_o, d);
+  g.ep.kind = EPI_STORE;
+  g.ep.out1 = dctx;
+  gemm(g);
+
+  at.causal = 1;
+  at.sq = at.skv = sy_;
+  at.q = qkv;
+  at.k = qkv.offset(d);
+  at.v = qkv.offset(2 * d);
+  at.o = ctx;
+  at.lse = lse;
+  at.dout = dctx;
+  at.dq = dqkv;
+  at.dk = dqkv.offset(d);
+  at.dv = dqkv.offset(2 * d);
+  at.dd = dd;
+  launches_ += 3;
+  launch_attn_bwd(at, active_, stream_);
+
+  g = mk(R, d, 3 * d, dqkv, L.w_qkv, d);
+  g.ep.kind = EPI_STORE;
+  g.ep.out1 = dn1;
+  gemm(g);
+
+  if (e.cmb.mode != CM_NONE) {
+    LnBwdArgs l1;
+    l1.G = G;
+    l1.rows = R;
+    l1.d = d;
+    l1.x = Y;
+    l1.stats = st1;
+    l1.up = dn1;
+    l1.gain = par(L.ln1_g, 0, l0, ls);
+    l1.addA = dy;
+    Combine c = e.cmb;
+    for (Mat* m : {&c.z, &c.out, &c.base, &c.phib, &c.rho, &c.v})
+      if (m->ok()) {
+        *m = m->offset(y_off_);
+        m->ld = d;
+      }
+    if (c.mode == CM_RES0) c.norm_base = take_partials(G * ln_bwd_blocks(R));
+    l1.cmb = c;
+    ++launches_;
+    launch_ln_bwd(l1, active_, stream_);
+    ElemCombineArgs ec;
+    ec.G = G;
+    ec.n = (long long)Tx_ * d;
+    ec.F = dxe;
+    Combine cx = e.cmb;
+    if (cx.mode == CM_RES0) cx.norm_base = take_partials(G * elem_combine_blocks(ec.n));
+    ec.cmb = cx;
+    ++launches_;
+    launch_elem_combine(ec, active_, stream_);
+  }
+
+  if (e.want_grads) {
+    const float gs = e.gscale;
+    auto wg = [&](int M, int N, int K, Mat A, Mat Bm, long long w, int ldw) {
+      GemmArgs w_;
+      w_.G = G;
+      w_.M = M;
+      w_.N = N;
+      w_.K = K;
+      w_.A = A;
+      w_.B = Bm;
+      w_.a_mn = true;
+      w_.b_mn = true;
+      w_.ep.kind = EPI_GRAD_ACC;
+      w_.ep.out1 = grad(w, ldw, l0, ls);
+      w_.ep.gscale = gs;
+      gemm(w_);
+    };
+    auto cr = [&](int rows, Mat up, int cols, long long b, Mat x, Mat st, long long gn) {
+      ColRedArgs c;
+      c.G = G;
+      c.rows = rows;
+      c.cols = cols;
+      c.up = up;
+      c.x = x;
+      c.stats = st;
+      c.dbias = grad(b, 0, l0, ls);
+      if (x.ok()) c.dgain = grad(gn, 0, l0, ls);
+      c.gscale = gs;
+      ++launches_;
+      launch_colred(c, active_, stream_);
+    };
+    wg(d, f, R, UPy, gg, L.w_out, f);
+    cr(R, UPy, d, L.b_out, Mat{}, Mat{}, 0);
+    wg(f, d, R, dh, n2, L.w_in, d);
+    cr(R, dh, f, L.b_in, Mat{}, Mat{}, 0);
+    cr(R, dn2, d, L.ln2_b, u2, st2, L.ln2_g);
+    wg(d, d, R, dybar, cctx, L.w_co, d);
+    cr(R, dybar, d, L.b_co, Mat{}, Mat{}, 0);
+    wg(d, d, R, dcq, n3, L.w_cq, d);
+    cr(R, dcq, d, L.b_cq, Mat{}, Mat{}, 0);
+    wg(2 * d, d, Tx_, dckv, X, L.w_ckv, d);
+    cr(Tx_, dckv, 2 * d, L.b_ckv, Mat{}, Mat{}, 0);
+    cr(R, dn3, d, L.ln3_b, u3, st3, L.ln3_g);
+    wg(d, d, R, da1, ctx, L.w_o, d);
+    cr(R, da1, d, L.b_o, Mat{}, Mat{}, 0);
+    wg(3 * d, d, R, dqkv, n1, L.w_qkv, d);
+    cr(R, dqkv, 3 * d, L.b_qkv, Mat{}, Mat{}, 0);
+    cr(R, dn1, d, L.ln1_b, Y, st1, L.ln1_g);
+  }
+}
+
+// =============================================================================
+// MGRIT (mgrit.hpp:58-303) on device-resident levels
+// =============================================================================
+
+Mat Engine::lv_v(const Solver& s, int l, int slot0, int step) const {
+  return state_mat(s.lv[l].v, state_n_, sd_.d, slot0, step);
+}
+Mat Engine::lv_base(const Solver& s, int l, int slot0, int step) const {
+  // base of level l is the level l-1 iterate at the coarse-aligned points
+  return state_mat(s.lv[l - 1].v, state_n_, sd_.d, slot0 * cfg_.coarsen, step * cfg_.coarsen);
+}
+Mat Engine::lv_rho(const Solver& s, int l, int slot0, int step) const {
+  return state_mat(s.lv[l].rho, state_n_, sd_.d, slot0, step);
+}
+Mat Engine::lv_phib(const Solver& s, int l, int slot0, int step) const {
+  return state_mat(s.lv[l].phib, state_n_, sd_.d, slot0, step);
+}
+
+// Steps k = k0 + g*kstep (g < G) of level `level` of system s, applied to the
+// states `in`; results folded by `cmb`.
+void Engine::sys_eval(Solver& s, int level, int k0, int kstep, int G, Mat in, Combine cmb,
+                      bool capture) {
+  if (G <= 0) return;
+  long long stride = 1;
+  for (int l = 0; l < level; ++l) stride *= cfg_.coarsen;
+  const float dt = (float)((double)stride * h_[ib_]);
+  for (int g0 = 0; g0 < G; g0 += Gmax_) {
+    const int Gc = std::min(Gmax_, G - g0);
+    EvalSpec e;
+    e.G = Gc;
+    e.dt = dt;
+    Combine c = cmb;
+    c.out = shift(c.out, g0);
+    c.base = shift(c.base, g0);
+    c.phib = shift(c.phib, g0);
+    c.rho = shift(c.rho, g0);
+    c.v = shift(c.v, g0);
+    e.cmb = c;
+    const int kk0 = k0 + g0 * kstep;
+    if (!s.adjoint) {
+      e.layer0 = ib_ + (int)(kk0 * stride);
+      e.layer_step = (int)(kstep * stride);
+      e.in = shift(in, g0);
+      if (capture)
+        e.act = ActRef{cache_, al_.size, e.layer0, e.layer_step};
+      else
+        e.act = ActRef{scratch_, al_.size, 0, 1};
+      eval_forward(e);
+    } else {
+      // adjoint step k applies layer n = N-1-k*stride at traj[ib+n] (adjoint.hpp:45-54)
+      e.layer0 = ib_ + (N_ - 1 - (int)(kk0 * stride));
+      e.layer_step = -(int)(kstep * stride);
+      e.lam = shift(in, g0);
+      e.in = state_mat(traj_, state_n_, sd_.d, e.layer0, e.layer_step);
+      e.act = ActRef{cache_, al_.size, e.layer0, e.layer_step};
+      eval_adjoint(e);
+    }
+  }
+}
+
+// v[j] = relax(Phi(v[j-1])) for j = j0 + g*jstep (mgrit.hpp:273-282)
+void Engine::relax_family(Solver& s, int level, int j0, int jstep, int G, bool capture) {
+  Combine c;
+  c.out = lv_v(s, level, j0, jstep);
+  if (level == 0) {
+    c.mode = CM_PLAIN;
+  } else {
+    c.mode = CM_FAS;
+    c.base = lv_base(s, level, j0, jstep);
+    c.phib = lv_phib(s, level, j0, jstep);
+    c.rho = lv_rho(s, level, j0, jstep);
+  }
+  sys_eval(s, level, j0 - 1, jstep, G, lv_v(s, level, j0 - 1, jstep), c, capture);
+}
+
+void Engine::f_relax(Solver& s, int level, bool capture) {  // mgrit.hpp:125-137
+  const int cf = cfg_.coarsen, nc = s.lv[level].n / cf;
+  for (int i = 1; i < cf; ++i) relax_family(s, level, i, cf, nc, capture);
+}
+
+void Engine::c_relax(Solver& s, int level) {  // mgrit.hpp:139-149
+  const int cf = cfg_.coarsen, nc = s.lv[level].n / cf;
+  relax_family(s, level, cf, cf, nc, false);
+}
+
+// Residual rows at the coarse-aligned points j = k*c_f (mgrit.hpp:159-187).
+// After F-relaxation every F-point row is exactly zero at level 0 (v[j] was
+// just set to Phi(v[j-1]) by the same deterministic kernels), and at coarser
+// levels F-point rows are never read (injection keeps only k*c_f rows), so
+// only the C-point rows are evaluated; they are written straight into the
+// next level's rho (injection, mgrit.hpp:204).
+void Engine::residual_c_rows(Solver& s, int level, bool capture) {
+  const int cf = cfg_.coarsen, nc = s.lv[level].n / cf;
+  Combine c;
+  c.out = lv_rho(s, level + 1, 1, 1);
+  c.v = lv_v(s, level, cf, cf);
+  if (level == 0) {
+    c.mode = CM_RES0;
+    c.norm_partials = s.partials;
+    c.norm_base = 0;
+  } else {
+    c.mode = CM_RESL;
+    c.base = lv_base(s, level, cf, cf);
+    c.phib = lv_phib(s, level, cf, cf);
+    c.rho = lv_rho(s, level, cf, cf);
+  }
+  if (level == 0) {
+    pcursor_ = 0;
+    pcap_ = s.n_partials;
+    sys_eval(s, level, cf - 1, cf, nc, lv_v(s, level, cf - 1, cf), c, capture);
+    launch_trace_record(s.ctrl, s.partials, pcursor_, stream_);
+    ++launches_;
+  } else {
+    sys_eval(s, level, cf - 1, cf, nc, lv_v(s, level, cf - 1, cf), c, false);
+  }
+}
+
+void Engine::restrict_to(Solver& s, int level) {  // mgrit.hpp:199-211
+  Level& c = s.lv[level];
+  const bool coarsest = level == cfg_.levels - 1;
+  // v = base (the coarsest level only needs its initial condition: exact_solve
+  // overwrites every other point)
+  launch_copy(coarsest ? 1 : c.n + 1, state_n_, lv_v(s, level, 0, 1), lv_base(s, level, 0, 1),
+              active_, stream_);
+  ++launches_;
+  Combine cm;
+  cm.mode = CM_PLAIN;
+  cm.out = lv_phib(s, level, 1, 1);
+  sys_eval(s, level, 0, 1, c.n, lv_base(s, level, 0, 1), cm, false);
+}
+
+void Engine::correct_from(Solver& s, int level) {  // mgrit.hpp:214-223
+  const int n = s.lv[level].n;
+  launch_correct(n, state_n_, lv_v(s, level - 1, cfg_.coarsen, cfg_.coarsen),
+                 lv_v(s, level, 1, 1), lv_base(s, level, 1, 1), active_, stream_);
+  ++launches_;
+}
+
+void Engine::exact_solve(Solver& s, int level) {  // mgrit.hpp:227-231
+  for (int j = 1; j <= s.lv[level].n; ++j) relax_family(s, level, j, 1, 1, false);
+}
+
+void Engine::descend(Solver& s, int level) {  // mgrit.hpp:285-296
+  if (level == cfg_.levels - 1) {
+    exact_solve(s, level);
+    return;
+  }
+  f_relax(s, level, false);
+  c_relax(s, level);
+  f_relax(s, level, false);
+  residual_c_rows(s, level, false);
+  restrict_to(s, level + 1);
+  descend(s, level + 1);
+  correct_from(s, level + 1);
+  f_relax(s, level, false);
+}
+
+void Engine::v_cycle(Solver& s, double tol) {  // mgrit.hpp:235-246
+  const bool cap = !s.adjoint;
+  const bool one_level = cfg_.levels == 1;
+  f_relax(s, 0, cap && one_level);
+  c_relax(s, 0);
+  f_relax(s, 0, cap);
+  residual_c_rows(s, 0, cap && one_level);
+  if (!one_level) {
+    restrict_to(s, 1);
+    descend(s, 1);
+    correct_from(s, 1);
+    f_relax(s, 0, cap);
+  }
+  launch_cycle_end(s.ctrl, tol, stream_);
+  ++launches_;
+}
+
+void Engine::solve(Solver& s, int iters, double tol) {  // mgrit.hpp:248-262
+  if (iters < 1) throw ValidationError("solve_forward: need at least one iteration");
+  launch_ctrl_begin(s.ctrl, stream_);
+  active_ = &s.ctrl->active;
+  for (int it = 0; it < iters; ++it) v_cycle(s, tol);
+  active_ = nullptr;
+}
+
+// =============================================================================
+// LayerParallelEngine (adjoint.hpp:113-206)
+// =============================================================================
+
+void Engine::forward_device(const float* z0_dev) {
+  MGLP_CUDA(cudaSetDevice(device_));
+  if (!traj_) throw ValidationError("forward: set_shape first");
+  std::fill(cache_valid_.begin(), cache_valid_.end(), 0);
+  MGLP_CUDA(cudaMemcpyAsync(traj_, z0_dev, state_n_ * sizeof(float), cudaMemcpyDeviceToDevice,
+                            stream_));
+  auto serial_step = [&](int l) {
+    EvalSpec e;
+    e.G = 1;
+    e.layer0 = l;
+    e.dt = (float)h_[l];
+    e.in = state_mat(traj_, state_n_, sd_.d, l, 1);
+    e.act = ActRef{cache_, al_.size, l, 1};
+    e.cmb.mode = CM_PLAIN;
+    e.cmb.out = state_mat(traj_, state_n_, sd_.d, l + 1, 1);
+    eval_forward(e);
+    cache_valid_[l] = 1;
+  };
+  for (int l = 0; l < ib_; ++l) serial_step(l);
+  const int guess = (first_fwd_ || !cfg_.warm_start) ? cfg_.cold_guess : 2;
+  first_fwd_ = false;
+  Mat v0 = lv_v(fwd_, 0, 0, 0);
+  if (guess == 0) {
+    launch_copy(N_, state_n_, lv_v(fwd_, 0, 1, 1), v0, nullptr, stream_);
+  } else if (guess == 1) {
+    launch_zero(N_, state_n_, lv_v(fwd_, 0, 1, 1), nullptr, stream_);
+  }
+  solve(fwd_, cfg_.fwd_iters, cfg_.fwd_tol);
+  // the level-0 F-relaxations captured the linearization of every layer
+  // whose input is final: all but the last layer of each coarse interval
+  // (with one level the C-point residual evaluations capture those too)
+  const int cf = cfg_.coarsen;
+  for (int i = 0; i < N_; ++i)
+    if (cfg_.levels == 1 || (i % cf) != cf - 1) cache_valid_[ib_ + i] = 1;
+  for (int l = ie_; l < total_; ++l) serial_step(l);
+}
+
+// Linearization pass for layers whose activations were not captured.
+void Engine::ensure_linearization() {
+  std::vector<int> miss;
+  for (int l = 0; l < total_; ++l)
+    if (!cache_valid_[l]) miss.push_back(l);
+  size_t i = 0;
+  while (i < miss.size()) {
+    // affine run
+    size_t j = i + 1;
+    const int step = (j < miss.size()) ? miss[j] - miss[i] : 1;
+    while (j < miss.size() && miss[j] - miss[j - 1] == step && (int)(j - i) < Gmax_) ++j;
+    EvalSpec e;
+    e.G = (int)(j - i);
+    e.layer0 = miss[i];
+    e.layer_step = step;
+    e.dt = 0.f;
+    e.in = state_mat(traj_, state_n_, sd_.d, miss[i], step);
+    e.act = ActRef{cache_, al_.size, miss[i], step};
+    e.cmb.mode = CM_NONE;
+    eval_forward(e);
+    for (size_t k = i; k < j; ++k) cache_valid_[miss[k]] = 1;
+    i = j;
+  }
+}
+
+void Engine::backward_device(const float* lamN_dev, float* lam0_dev, bool want_grads,
+                             bool traj_is_current) {
+  MGLP_CUDA(cudaSetDevice(device_));
+  if (!traj_) throw ValidationError("backward: set_shape first");
+  if (!traj_is_current) std::fill(cache_valid_.begin(), cache_valid_.end(), 0);
+  ensure_linearization();
+  const Mat LAM = state_mat(lam_all_, state_n_, sd_.d, 0, 1);
+  MGLP_CUDA(cudaMemcpyAsync(lam_all_ + (size_t)total_ * state_n_, lamN_dev,
+                            state_n_ * sizeof(float), cudaMemcpyDeviceToDevice, stream_));
+  auto serial_adj = [&](int l) {
+    EvalSpec e;
+    e.G = 1;
+    e.layer0 = l;
+    e.dt = (float)h_[l];
+    e.lam = shift(LAM, l + 1);
+    e.in = state_mat(traj_, state_n_, sd_.d, l, 1);
+    e.act = ActRef{cache_, al_.size, l, 1};
+    e.cmb.mode = CM_PLAIN;
+    e.cmb.out = shift(LAM, l);
+    e.want_grads = want_grads;
+    e.gscale = (float)h_[l];
+    eval_adjoint(e);
+  };
+  for (int l = total_ - 1; l >= ie_; --l) serial_adj(l);
+  // mu[0] = lambda at the interior end
+  MGLP_CUDA(cudaMemcpyAsync(bwd_.lv[0].v, lam_all_ + (size_t)ie_ * state_n_,
+                            state_n_ * sizeof(float), cudaMemcpyDeviceToDevice, stream_));
+  const int guess = (first_bwd_ || !cfg_.warm_start) ? cfg_.cold_guess : 2;
+  first_bwd_ = false;
+  if (guess == 0)
+    launch_copy(N_, state_n_, lv_v(bwd_, 0, 1, 1), lv_v(bwd_, 0, 0, 0), nullptr, stream_);
+  else if (guess == 1)
+    launch_zero(N_, state_n_, lv_v(bwd_, 0, 1, 1), nullptr, stream_);
+  solve(bwd_, cfg_.bwd_iters, cfg_.bwd_tol);
+  // parameter pass (adjoint.hpp:165-175): layer ib+i at traj[ib+i] with
+  // upstream mu[N-1-i], gscale = h
+  if (want_grads) {
+    for (int i0 = 0; i0 < N_; i0 += Gmax_) {
+      const int Gc = std::min(Gmax_, N_ - i0);
+      EvalSpec e;
+      e.G = Gc;
+      e.layer0 = ib_ + i0;
+      e.layer_step = 1;
+      e.dt = 0.f;
+      e.lam = lv_v(bwd_, 0, N_ - 1 - i0, -1);
+      e.in = state_mat(traj_, state_n_, sd_.d, ib_ + i0, 1);
+      e.act = ActRef{cache_, al_.size, ib_ + i0, 1};
+      e.cmb.mode = CM_NONE;
+      e.want_grads = true;
+      e.gscale = (float)h_[ib_];
+      eval_adjoint(e);
+    }
+  }
+  MGLP_CUDA(cudaMemcpyAsync(lam_all_ + (size_t)ib_ * state_n_,
+                            bwd_.lv[0].v + (size_t)N_ * state_n_, state_n_ * sizeof(float),
+                            cudaMemcpyDeviceToDevice, stream_));
+  for (int l = ib_ - 1; l >= 0; --l) serial_adj(l);
+  if (lam0_dev)
+    MGLP_CUDA(cudaMemcpyAsync(lam0_dev, lam_all_, state_n_ * sizeof(float),
+                              cudaMemcpyDeviceToDevice, stream_));
+}
+
+void Engine::read_trace(bool fwd, std::vector<double>* trace, bool* converged) {
+  SolveCtrl c;
+  MGLP_CUDA(cudaMemcpyAsync(&c, fwd ? fwd_.ctrl : bwd_.ctrl, sizeof(SolveCtrl),
+                            cudaMemcpyDeviceToHost, stream_));
+  MGLP_CUDA(cudaStreamSynchronize(stream_));
+  trace->assign(c.trace, c.trace + std::min(c.n_trace, kMaxTrace));
+  *converged = c.converged != 0;
+}
+
+void Engine::snapshot() {  // adjoint.hpp:187-194
+  const size_t bytes = (size_t)(N_ + 1) * state_n_ * sizeof(float);
+  if (!snap_fwd_) MGLP_CUDA(cudaMalloc(&snap_fwd_, bytes));
+  if (!snap_bwd_) MGLP_CUDA(cudaMalloc(&snap_bwd_, bytes));
+  MGLP_CUDA(cudaMemcpyAsync(snap_fwd_, fwd_.lv[0].v, bytes, cudaMemcpyDeviceToDevice, stream_));
+  MGLP_CUDA(cudaMemcpyAsync(snap_bwd_, bwd_.lv[0].v, bytes, cudaMemcpyDeviceToDevice, stream_));
+  snap_first_fwd_ = first_fwd_;
+  snap_first_bwd_ = first_bwd_;
+}
+
+void Engine::restore() {  // adjoint.hpp:196-201
+  if (!snap_fwd_) throw ValidationError("restore: no snapshot taken");
+  const size_t bytes = (size_t)(N_ + 1) * state_n_ * sizeof(float);
+  MGLP_CUDA(cudaMemcpyAsync(fwd_.lv[0].v, snap_fwd_, bytes, cudaMemcpyDeviceToDevice, stream_));
+  MGLP_CUDA(cudaMemcpyAsync(bwd_.lv[0].v, snap_bwd_, bytes, cudaMemcpyDeviceToDevice, stream_));
+  first_fwd_ = snap_first_fwd_;
+  first_bwd_ = snap_first_bwd_;
+  std::fill(cache_valid_.begin(), cache_valid_.end(), 0);
+}
+
+// ---- serial sweeps (blocks.cpp:659-682) ----
+void Engine::serial_forward_device(const float* z0_dev) {
+  MGLP_CUDA(cudaSetDevice(device_));
+  MGLP_CUDA(cudaMemcpyAsync(traj_, z0_dev, state_n_ * sizeof(float), cudaMemcpyDeviceToDevice,
+                            stream_));
+  for (int l = 0; l < total_; ++l) {
+    EvalSpec e;
+    e.G = 1;
+    e.layer0 = l;
+    e.dt = (float)h_[l];
+    e.in = state_mat(traj_, state_n_, sd_.d, l, 1);
+    e.act = ActRef{cache_, al_.size, l, 1};
+    e.cmb.mode = CM_PLAIN;
+    e.cmb.out = state_mat(traj_, state_n_, sd_.d, l + 1, 1);
+    eval_forward(e);
+    cache_valid_[l] = 1;
+  }
+}
+
+void Engine::serial_adjoint_device(const float* lamN_dev, float* lam0_dev, bool want_grads) {
+  MGLP_CUDA(cudaSetDevice(device_));
+  ensure_linearization();
+  const Mat LAM = state_mat(lam_all_, state_n_, sd_.d, 0, 1);
+  MGLP_CUDA(cudaMemcpyAsync(lam_all_ + (size_t)total_ * state_n_, lamN_dev,
+                            state_n_ * sizeof(float), cudaMemcpyDeviceToDevice, stream_));
+  for (int l = total_ - 1; l >= 0; --l) {
+    EvalSpec e;
+    e.G = 1;
+    e.layer0 = l;
+    e.dt = (float)h_[l];
+    e.lam = shift(LAM, l + 1);
+    e.in = state_mat(traj_, state_n_, sd_.d, l, 1);
+    e.act = ActRef{cache_, al_.size, l, 1};
+    e.cmb.mode = CM_PLAIN;
+    e.cmb.out = shift(LAM, l);
+    e.want_grads = want_grads;
+    e.gscale = (float)h_[l];
+    eval_adjoint(e);
+  }
+  if (lam0_dev)
+    MGLP_CUDA(cudaMemcpyAsync(lam0_dev, lam_all_, state_n_ * sizeof(float),
+                              cudaMemcpyDeviceToDevice, stream_));
+}
+
+// ---- single-step hooks ----
+void Engine::step_device(int layer, double dt, const float* z, float* out) {
+  if (layer < 0 || layer >= total_) throw ValidationError("step: layer out of range");
+  EvalSpec e;
+  e.G = 1;
+  e.layer0 = layer;
+  e.dt = (float)dt;
+  e.in = state_mat(const_cast<float*>(z), state_n_, sd_.d, 0, 1);
+  e.act = ActRef{scratch_, al_.size, 0, 1};
+  e.cmb.mode = CM_PLAIN;
+  e.cmb.out = state_mat(out, state_n_, sd_.d, 0, 1);
+  eval_forward(e);
+}
+
+void Engine::adjoint_step_device(int layer, double dt, const float* z, const float* lam,
+                                 float* out, bool want_grads, double gscale) {
+  if (layer < 0 || layer >= total_) throw ValidationError("adjoint_step: layer out of range");
+  EvalSpec f;
+  f.G = 1;
+  f.layer0 = layer;
+  f.in = state_mat(const_cast<float*>(z), state_n_, sd_.d, 0, 1);
+  f.act = ActRef{scratch_, al_.size, 0, 1};
+  f.cmb.mode = CM_NONE;
+  eval_forward(f);
+  EvalSpec e = f;
+  e.dt = (float)dt;
+  e.lam = state_mat(const_cast<float*>(lam), state_n_, sd_.d, 0, 1);
+  e.cmb.mode = CM_PLAIN;
+  e.cmb.out = state_mat(out, state_n_, sd_.d, 0, 1);
+  e.want_grads = want_grads;
+  e.gscale = (float)gscale;
+  eval_adjoint(e);
+}
+
+}  // namespace mglp

@@ -1,0 +1,241 @@
+// CudaLayerParallelEngine: the B200 implementation behind the C-ABI
+// (include/mglp_cuda.h). It re-expresses the reference's LayerParallelEngine
+// (adjoint.hpp:99-219) + MgritSolver (mgrit.hpp:58-303) + LayerStack
+// (blocks.hpp:120-175) as device-resident state and batched kernel launches:
+// every relaxation sweep over the N/c_f coarse intervals is ONE family of
+// launches (G = number of intervals) instead of N/c_f executor tasks.
+#pragma once
+
+#include <algorithm>
+#include <cstdint>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace mglp {
+
+struct StackDesc {
+  int kind = 0;  // 0 encoder, 1 decoder-only (causal), 2 encoder-decoder
+  int d = 32, heads = 2, ffn = 64, n_enc = 8, n_dec = 0;
+  int buffer_open = 0, buffer_close = 0;
+  double ln_eps = 1e-5, base_h = 1.0, init_std = 0.02;
+  int depth_scaled_init = 0;
+  double dropout = 0.0;
+};
+
+struct SolveCfg {
+  int coarsen = 2, levels = 2, fwd_iters = 2, bwd_iters = 1;
+  double fwd_tol = 0.0, bwd_tol = 0.0;
+  int cold_guess = 0;  // 0 broadcast, 1 zero, 2 warm
+  int warm_start = 1;
+};
+
+// Point-to-point transport between the ranks that own consecutive layer
+// blocks (NCCL over NVLink in production; an in-process loopback in tests).
+class Transport {
+ public:
+  virtual ~Transport() = default;
+  virtual int rank() const = 0;
+  virtual int size() const = 0;
+  virtual void send(const float* buf, size_t n, int peer, cudaStream_t s) = 0;
+  virtual void recv(float* buf, size_t n, int peer, cudaStream_t s) = 0;
+  // gathers `n` doubles from every rank into out[rank*n .. ]
+  virtual void allgather(const double* in, double* out, size_t n, cudaStream_t s) = 0;
+  virtual void group_start() {}
+  virtual void group_end() {}
+};
+
+class Engine {
+ public:
+  Engine(const StackDesc& sd, const SolveCfg& cfg, int device, std::shared_ptr<Transport> tr);
+  ~Engine();
+
+  // ---- LayerStack surface ----
+  long long num_params() const { return n_params_flat_; }
+  int total_layers() const { return total_; }
+  int interior_begin() const { return ib_; }
+  int interior_end() const { return ie_; }
+  double step_size(int layer) const { return h_[layer]; }
+  void init_params(uint64_t seed, std::vector<double>* flat_out);
+  void set_params(const double* flat);
+  void get_params(double* flat) const;
+  void get_grads(double* flat_accum) const;  // flat += device grads
+  void zero_grads();
+
+  // ---- shape ----
+  void set_shape(int batch, int s_x, int s_y);
+  long long state_elems() const { return state_n_; }
+  int width() const { return sd_.d; }
+  SolveCtrl* ctrl(bool fwd) const { return fwd ? fwd_.ctrl : bwd_.ctrl; }
+
+  // ---- LayerParallelEngine surface ----
+  SolveCfg& config() { return cfg_; }
+  void forward_device(const float* z0_dev);
+  void backward_device(const float* lamN_dev, float* lam0_dev, bool want_grads,
+                       bool traj_is_current);
+  void read_trace(bool fwd, std::vector<double>* trace, bool* converged);
+  void snapshot();
+  void restore();
+  void reset() { first_fwd_ = first_bwd_ = true; }
+  void invalidate_linearization() { std::fill(cache_valid_.begin(), cache_valid_.end(), 0); }
+
+  // serial reference sweeps on device (blocks.cpp:659-682)
+  void serial_forward_device(const float* z0_dev);
+  void serial_adjoint_device(const float* lamN_dev, float* lam0_dev, bool want_grads);
+
+  // device-resident trajectory, slot i = time point i (total+1 slots)
+  float* traj_dev() const { return traj_; }
+  float* lam_all_dev() const { return lam_all_; }
+  cudaStream_t stream() const { return stream_; }
+  int device() const { return device_; }
+  // number of hot-path kernel launches issued since the last reset_launch_count()
+  long long launch_count() const { return launches_; }
+  void reset_launch_count() { launches_ = 0; }
+
+  // test hooks: one Phi / Phi^T application on the device
+  void step_device(int layer, double dt, const float* z, float* out);
+  void adjoint_step_device(int layer, double dt, const float* z, const float* lam, float* out,
+                           bool want_grads, double gscale);
+
+ private:
+  // ----- parameter layout -----
+  struct Piece {
+    long long flat_off, dev_off, n;
+  };
+  struct LayerLayout {
+    bool decoder = false;
+    // device offsets (floats) within one layer's slab
+    long long ln1_g, ln1_b, w_qkv, b_qkv, w_o, b_o, ln2_g, ln2_b, w_in, b_in, w_out, b_out;
+    long long ln3_g, ln3_b, w_cq, b_cq, w_ckv, b_ckv, w_co, b_co;
+    long long size = 0;
+    std::vector<Piece> pieces;  // flat (visit_params) <-> device
+    long long flat_size = 0;
+  };
+  void build_layouts();
+
+  // ----- activation arena layout (per slot) -----
+  struct ActLayout {
+    long long n1, qkv, ctx, lse, a1, u, n2, h, g, st1, st2;            // encoder / self
+    long long n3, u3, cq, ckv, cctx, clse, ybar, st3;                  // decoder cross
+    long long size = 0;
+  };
+  struct BwdLayout {
+    long long dh, dn2, du, da1, dctx, dqkv, dn1, dd;                   // encoder / self
+    long long dybar, dy, dcctx, dcq, dckv, dn3, dxe, dd2;              // decoder
+    long long size = 0;
+  };
+
+  // a reference to G activation slots (cache: slot = layer; scratch: slot = g)
+  struct ActRef {
+    float* base;
+    long long stride;
+    int slot0, step;
+  };
+
+  // ----- Phi / Phi^T evaluation families -----
+  struct EvalSpec {
+    int G = 1;
+    int layer0 = 0, layer_step = 1;  // absolute layer of member g
+    float dt = 0.f;
+    Mat in;      // input states (full State rows)
+    ActRef act;  // where forward activations go / come from
+    Combine cmb; // z/out/base/phib/rho/v are full-State families; mode
+    bool want_grads = false;
+    float gscale = 0.f;
+    Mat lam;     // adjoint: upstream state family
+  };
+  void eval_forward(const EvalSpec& e);
+  void eval_adjoint(const EvalSpec& e);
+  void encoder_forward(const EvalSpec& e, int Rx, bool causal, Mat xin, Mat yin_passive);
+  void decoder_forward(const EvalSpec& e);
+  void encoder_adjoint(const EvalSpec& e, bool causal);
+  void decoder_adjoint(const EvalSpec& e);
+  void gemm(GemmArgs g);
+  int gemm_blocks(const GemmArgs& g) const;
+  int take_partials(int n);
+  Mat act_mat(const ActRef& r, long long off, int ld) const;
+  Mat bwd_mat(long long off, int ld) const;
+  Mat par(long long off, int ld, int layer0, int step) const;
+  Mat par_hi(long long off, int ld, int layer0, int step) const;
+  Mat par_lo(long long off, int ld, int layer0, int step) const;
+  Mat grad(long long off, int ld, int layer0, int step) const;
+
+  // ----- MGRIT solver (mgrit.hpp) -----
+  struct Level {
+    int n = 0;
+    float* v = nullptr;   // n+1 states
+    float* rho = nullptr; // n+1 (level > 0)
+    float* phib = nullptr;
+    // base of level l aliases v of level l-1 at stride c_f
+  };
+  struct Solver {
+    bool adjoint = false;
+    std::vector<Level> lv;
+    SolveCtrl* ctrl = nullptr;
+    double* partials = nullptr;
+    int n_partials = 0;
+  };
+  Mat lv_v(const Solver& s, int l, int slot0, int step) const;
+  Mat lv_base(const Solver& s, int l, int slot0, int step) const;
+  Mat lv_rho(const Solver& s, int l, int slot0, int step) const;
+  Mat lv_phib(const Solver& s, int l, int slot0, int step) const;
+  void sys_eval(Solver& s, int level, int k0, int kstep, int G, Mat in, Combine cmb,
+                bool capture);
+  void relax_family(Solver& s, int level, int j0, int jstep, int G, bool capture);
+  void f_relax(Solver& s, int level, bool capture);
+  void c_relax(Solver& s, int level);
+  void residual_c_rows(Solver& s, int level, bool capture);
+  void restrict_to(Solver& s, int level);
+  void correct_from(Solver& s, int level);
+  void exact_solve(Solver& s, int level);
+  void descend(Solver& s, int level);
+  void v_cycle(Solver& s, double tol);
+  void solve(Solver& s, int iters, double tol);
+  void alloc_solver(Solver& s, bool adjoint);
+  void free_solver(Solver& s);
+  void ensure_linearization();
+
+  // ----- members -----
+  StackDesc sd_;
+  SolveCfg cfg_;
+  int device_ = 0;
+  std::shared_ptr<Transport> tr_;
+  cudaStream_t stream_ = nullptr;
+  int total_ = 0, n_split_ = 0, ib_ = 0, ie_ = 0, N_ = 0;
+  bool causal_ = false;
+  std::vector<double> h_;
+  std::vector<LayerLayout> lay_;  // [0]=encoder kind, [1]=decoder kind
+  long long layer_stride_ = 0;
+  long long n_params_flat_ = 0;
+  float* P_ = nullptr;     // fp32 params
+  float* Phi_ = nullptr;   // tf32 hi parts
+  float* Plo_ = nullptr;   // tf32 lo parts
+  float* Gr_ = nullptr;    // fp32 grads
+  // shape
+  int B_ = 0, sx_ = 0, sy_ = 0, Tx_ = 0, Ty_ = 0;
+  long long state_n_ = 0, x_off_ = 0, y_off_ = 0;
+  ActLayout al_;
+  BwdLayout bl_;
+  int Gmax_ = 1;
+  float* scratch_ = nullptr;  // Gmax forward activation slots
+  float* cache_ = nullptr;    // total_ forward activation slots (slot = layer)
+  float* bscratch_ = nullptr; // Gmax backward slots
+  float* traj_ = nullptr;     // total_+1 states
+  float* lam_all_ = nullptr;  // total_+1 states (serial adjoint)
+  float* zero_state_ = nullptr;
+  Solver fwd_, bwd_;
+  std::vector<char> cache_valid_;
+  bool first_fwd_ = true, first_bwd_ = true;
+  // snapshot
+  float* snap_fwd_ = nullptr;
+  float* snap_bwd_ = nullptr;
+  bool snap_first_fwd_ = true, snap_first_bwd_ = true;
+  long long launches_ = 0;
+  const int* active_ = nullptr;  // current solve-control flag
+  int pcursor_ = 0, pcap_ = 0;   // residual-norm partial slots handed out
+};
+
+}  // namespace mglp

@@ -1,0 +1,100 @@
+// Launch wrappers for the hot-path kernels. All take a `const int* active`
+// solve-control flag (nullable): when *active == 0 the kernel returns
+// immediately, which is how a solve that converged (or went non-finite)
+// mid-way stops without a host round trip (mgrit.hpp:252-259).
+#pragma once
+
+#include "common.cuh"
+
+namespace mglp {
+
+// ---- LayerNorm (tensor.cpp:239-308) -----------------------------------------
+struct LnFwdArgs {
+  int G = 1, rows = 0, d = 0;
+  float eps = 1e-5f;
+  Mat x, out, stats;  // stats: [rows][2] = (mean, rstd)
+  Mat gain, bias;     // slot = layer
+};
+void launch_ln_fwd(const LnFwdArgs& a, const int* active, cudaStream_t s);
+
+// L = LNbwd(x, up); out1 = addA ? addA + L : L; out2 = addB + L;
+// optional combine of F = out1 into the solver state.
+struct LnBwdArgs {
+  int G = 1, rows = 0, d = 0;
+  Mat x, stats, up, gain;
+  Mat addA, addB, out1, out2;
+  Combine cmb;
+};
+void launch_ln_bwd(const LnBwdArgs& a, const int* active, cudaStream_t s);
+int ln_bwd_blocks(int rows);
+
+// Parameter-gradient column sums (deterministic, fixed order):
+//   dbias[j] += gscale * sum_r up[r][j]
+//   dgain[j] += gscale * sum_r up[r][j] * xhat[r][j]   (if x given)
+struct ColRedArgs {
+  int G = 1, rows = 0, cols = 0;
+  Mat up, x, stats;
+  Mat dgain, dbias;  // slot = layer
+  float gscale = 1.f;
+};
+void launch_colred(const ColRedArgs& a, const int* active, cudaStream_t s);
+
+// ---- state algebra (blocks.cpp:25-79; mgrit.hpp:199-223) --------------------
+// Passive-stream / elementwise combine: F = Fsrc ? Fsrc : 0 over n elements
+// (the stream a layer does not advance gets exactly dt*0, blocks.cpp:487,491).
+struct ElemCombineArgs {
+  int G = 1;
+  long long n = 0;
+  Mat F;  // nullable
+  Combine cmb;
+};
+void launch_elem_combine(const ElemCombineArgs& a, const int* active, cudaStream_t s);
+int elem_combine_blocks(long long n);
+
+// dst_g = src_g
+void launch_copy(int G, long long n, Mat dst, Mat src, const int* active, cudaStream_t s);
+// dst_g = dst_g + (a_g - b_g)     (correct_from, mgrit.hpp:219-221)
+void launch_correct(int G, long long n, Mat dst, Mat a, Mat b, const int* active,
+                    cudaStream_t s);
+void launch_zero(int G, long long n, Mat dst, const int* active, cudaStream_t s);
+
+// ---- solve control ------------------------------------------------------------
+constexpr int kMaxTrace = 256;
+struct SolveCtrl {
+  int active;
+  int n_trace;
+  int converged;
+  int cycles_run;
+  double pending;
+  double trace[kMaxTrace];
+};
+void launch_ctrl_begin(SolveCtrl* c, cudaStream_t s);
+// trace entry = sqrt(sum of partials[0..count)), measured mid-cycle (mgrit.hpp:235-238)
+void launch_trace_record(SolveCtrl* c, const double* partials, int count, cudaStream_t s);
+// end of one V-cycle: push the trace, stop on non-finite / converged (mgrit.hpp:252-259)
+void launch_cycle_end(SolveCtrl* c, double tol, cudaStream_t s);
+
+// ---- GEMM -------------------------------------------------------------------
+// Reference fp32 CUDA-core GEMM: test oracle for the tensor-core path only.
+void launch_gemm_simt(const GemmArgs& a, const int* active, cudaStream_t s);
+int gemm_simt_blocks(const GemmArgs& a);
+// Parity-grade tcgen05 (kind::tf32, 3-pass hi/lo split) GEMM.
+void launch_gemm_tc(const GemmArgs& a, const int* active, cudaStream_t s);
+int gemm_tc_blocks(const GemmArgs& a);
+// Splits weights into tf32 hi / lo parts (x = hi + lo exactly; hi has the
+// low 13 mantissa bits cleared).
+void launch_split_tf32(float* hi, float* lo, const float* src, long long n, cudaStream_t s);
+
+// ---- attention (blocks.cpp:142-236) -----------------------------------------
+struct AttnArgs {
+  int G = 1, B = 1, H = 1, dh = 0, sq = 0, skv = 0;
+  int causal = 0;
+  float scale = 1.f;
+  Mat q, k, v, o;  // element (b,i,h,c) at at(g)[(b*s + i)*ld + h*dh + c]
+  Mat lse;         // [B][H][sq]
+  Mat dout, dq, dk, dv, dd;  // backward: dd scratch [B][H][sq]
+};
+void launch_attn_fwd(const AttnArgs& a, const int* active, cudaStream_t s);
+void launch_attn_bwd(const AttnArgs& a, const int* active, cudaStream_t s);
+
+}  // namespace mglp

@@ -1,0 +1,375 @@
+// Row / element kernels of the hot path: LayerNorm forward and VJP
+// (tensor.cpp:239-308), parameter column sums (tensor.cpp:232-235, 303-304),
+// the MGRIT state algebra (mgrit.hpp:199-223, 273-282) and the per-cycle
+// residual-norm bookkeeping (mgrit.hpp:189-193, 248-262).
+//
+// All are HBM-bound: one warp per row with the row held in registers, grids
+// sized in multiples of the 148 SMs, no float atomics (every reduction runs
+// in a fixed order, so results never depend on scheduling).
+#include "kernels.cuh"
+
+namespace mglp {
+
+namespace {
+
+constexpr int kRowsPerBlock = 8;  // 8 warps of 32 lanes
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__device__ __forceinline__ double block_sum_f64(double v, double* smem) {
+  // fixed-order: warp shuffle tree, then warp 0 over the warp partials
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  const int nw = (blockDim.x + 31) >> 5;
+  __syncthreads();
+  if (l == 0) smem[w] = v;
+  __syncthreads();
+  double t = 0.0;
+  if (w == 0) {
+    t = l < nw ? smem[l] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+  }
+  return t;  // valid in thread 0
+}
+
+__device__ __forceinline__ bool stopped(const int* active) {
+  return active != nullptr && *(volatile const int*)active == 0;
+}
+
+// ---- LayerNorm forward --------------------------------------------------------
+template <int V>
+__global__ void __launch_bounds__(256) ln_fwd_kernel(LnFwdArgs a, const int* active) {
+  if (stopped(active)) return;
+  const int g = blockIdx.y;
+  const int row = blockIdx.x * kRowsPerBlock + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= a.rows) return;
+  const float* x = a.x.at(g) + (long long)row * a.x.ld;
+  float v[V];
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < V; ++i) {
+    const int j = lane + 32 * i;
+    v[i] = j < a.d ? x[j] : 0.f;
+    s += v[i];
+  }
+  const float inv_d = 1.f / (float)a.d;
+  const float mean = warp_sum(s) * inv_d;
+  float q = 0.f;
+#pragma unroll
+  for (int i = 0; i < V; ++i) {
+    const int j = lane + 32 * i;
+    const float c = j < a.d ? v[i] - mean : 0.f;
+    q += c * c;
+  }
+  const float var = warp_sum(q) * inv_d;
+  const float rstd = 1.f / sqrtf(var + a.eps);
+  const float* gain = a.gain.at(g);
+  const float* bias = a.bias.at(g);
+  float* o = a.out.at(g) + (long long)row * a.out.ld;
+#pragma unroll
+  for (int i = 0; i < V; ++i) {
+    const int j = lane + 32 * i;
+    if (j < a.d) o[j] = gain[j] * ((v[i] - mean) * rstd) + bias[j];
+  }
+  if (lane == 0 && a.stats.ok()) {
+    float* st = a.stats.at(g) + 2LL * row;
+    st[0] = mean;
+    st[1] = rstd;
+  }
+}
+
+// ---- LayerNorm VJP (+ fused sums and solver combine) ----------------------------
+template <int V>
+__global__ void __launch_bounds__(256) ln_bwd_kernel(LnBwdArgs a, const int* active) {
+  __shared__ double red[32];
+  if (stopped(active)) return;
+  const int g = blockIdx.y;
+  const int row = blockIdx.x * kRowsPerBlock + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  double r2 = 0.0;
+  if (row < a.rows) {
+    const float* x = a.x.at(g) + (long long)row * a.x.ld;
+    const float* up = a.up.at(g) + (long long)row * a.up.ld;
+    const float* gain = a.gain.at(g);
+    const float mean = a.stats.at(g)[2LL * row];
+    const float rstd = a.stats.at(g)[2LL * row + 1];
+    float xh[V], dxh[V];
+    float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+    for (int i = 0; i < V; ++i) {
+      const int j = lane + 32 * i;
+      if (j < a.d) {
+        xh[i] = (x[j] - mean) * rstd;
+        dxh[i] = up[j] * gain[j];
+      } else {
+        xh[i] = 0.f;
+        dxh[i] = 0.f;
+      }
+      s1 += dxh[i];
+      s2 += dxh[i] * xh[i];
+    }
+    const float inv_d = 1.f / (float)a.d;
+    const float m1 = warp_sum(s1) * inv_d;
+    const float m2 = warp_sum(s2) * inv_d;
+    const float* addA = a.addA.ok() ? a.addA.at(g) + (long long)row * a.addA.ld : nullptr;
+    const float* addB = a.addB.ok() ? a.addB.at(g) + (long long)row * a.addB.ld : nullptr;
+    float* o1 = a.out1.ok() ? a.out1.at(g) + (long long)row * a.out1.ld : nullptr;
+    float* o2 = a.out2.ok() ? a.out2.at(g) + (long long)row * a.out2.ld : nullptr;
+    const bool comb = a.cmb.mode != CM_NONE;
+    const long long off_out = comb ? (long long)row * a.cmb.out.ld : 0;
+    const long long off_z = comb ? (long long)row * a.cmb.z.ld : 0;
+#pragma unroll
+    for (int i = 0; i < V; ++i) {
+      const int j = lane + 32 * i;
+      if (j < a.d) {
+        const float L = rstd * (dxh[i] - m1 - xh[i] * m2);
+        const float v1 = addA ? addA[j] + L : L;
+        if (o1) o1[j] = v1;
+        if (o2) o2[j] = addB[j] + L;
+        if (comb) combine_apply(a.cmb, g, off_out + j, off_z + j, v1, r2);
+      }
+    }
+  }
+  if (a.cmb.mode == CM_RES0) {
+    const double t = block_sum_f64(r2, red);
+    if (threadIdx.x == 0)
+      a.cmb.norm_partials[a.cmb.norm_base + blockIdx.y * gridDim.x + blockIdx.x] = t;
+  }
+}
+
+template <template <int> class K, class Args>
+void dispatch_rows(int d, const Args& a, int G, int rows, const int* active, cudaStream_t s) {
+  dim3 grid(ceil_div(rows, kRowsPerBlock), G);
+  const int v = (d + 31) / 32;
+  if (v <= 1) K<1>::launch(grid, a, active, s);
+  else if (v <= 2) K<2>::launch(grid, a, active, s);
+  else if (v <= 4) K<4>::launch(grid, a, active, s);
+  else if (v <= 8) K<8>::launch(grid, a, active, s);
+  else if (v <= 16) K<16>::launch(grid, a, active, s);
+  else if (v <= 24) K<24>::launch(grid, a, active, s);
+  else if (v <= 32) K<32>::launch(grid, a, active, s);
+  else throw ValidationError("LayerNorm: width > 1024 is not supported");
+}
+
+template <int V>
+struct LnFwdL {
+  static void launch(dim3 g, const LnFwdArgs& a, const int* act, cudaStream_t s) {
+    ln_fwd_kernel<V><<<g, 256, 0, s>>>(a, act);
+  }
+};
+template <int V>
+struct LnBwdL {
+  static void launch(dim3 g, const LnBwdArgs& a, const int* act, cudaStream_t s) {
+    ln_bwd_kernel<V><<<g, 256, 0, s>>>(a, act);
+  }
+};
+
+// ---- column sums for parameter gradients -----------------------------------------
+__global__ void __launch_bounds__(256) colred_kernel(ColRedArgs a, const int* active) {
+  __shared__ double sb[8][33];
+  __shared__ double sg[8][33];
+  if (stopped(active)) return;
+  const int g = blockIdx.y;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int col = blockIdx.x * 32 + tx;
+  double accb = 0.0, accg = 0.0;
+  if (col < a.cols) {
+    const float* up = a.up.at(g);
+    const float* x = a.x.ok() ? a.x.at(g) : nullptr;
+    const float* st = a.x.ok() ? a.stats.at(g) : nullptr;
+    for (int r = ty; r < a.rows; r += 8) {
+      const float u = up[(long long)r * a.up.ld + col];
+      accb += (double)u;
+      if (x) {
+        const float xh = (x[(long long)r * a.x.ld + col] - st[2LL * r]) * st[2LL * r + 1];
+        accg += (double)u * (double)xh;
+      }
+    }
+  }
+  sb[ty][tx] = accb;
+  sg[ty][tx] = accg;
+  __syncthreads();
+  if (ty == 0 && col < a.cols) {
+    double tb = 0.0, tg = 0.0;
+    for (int i = 0; i < 8; ++i) {
+      tb += sb[i][tx];
+      tg += sg[i][tx];
+    }
+    if (a.dbias.ok()) {
+      float* db = a.dbias.at(g);
+      db[col] = db[col] + a.gscale * (float)tb;
+    }
+    if (a.x.ok() && a.dgain.ok()) {
+      float* dg = a.dgain.at(g);
+      dg[col] = dg[col] + a.gscale * (float)tg;
+    }
+  }
+}
+
+// ---- elementwise state algebra ------------------------------------------------------
+constexpr int kElemThreads = 256;
+constexpr int kElemPerThread = 8;
+
+__global__ void __launch_bounds__(kElemThreads) elem_combine_kernel(ElemCombineArgs a,
+                                                                    const int* active) {
+  __shared__ double red[32];
+  if (stopped(active)) return;
+  const int g = blockIdx.y;
+  double r2 = 0.0;
+  const long long base = (long long)blockIdx.x * kElemThreads * kElemPerThread + threadIdx.x;
+  const float* F = a.F.ok() ? a.F.at(g) : nullptr;
+#pragma unroll
+  for (int i = 0; i < kElemPerThread; ++i) {
+    const long long e = base + (long long)i * kElemThreads;
+    if (e < a.n) combine_apply(a.cmb, g, e, e, F ? F[e] : 0.f, r2);
+  }
+  if (a.cmb.mode == CM_RES0) {
+    const double t = block_sum_f64(r2, red);
+    if (threadIdx.x == 0)
+      a.cmb.norm_partials[a.cmb.norm_base + blockIdx.y * gridDim.x + blockIdx.x] = t;
+  }
+}
+
+__global__ void copy_kernel(int G, long long n4, Mat dst, Mat src, const int* active) {
+  if (stopped(active)) return;
+  const int g = blockIdx.y;
+  float4* d = reinterpret_cast<float4*>(dst.at(g));
+  const float4* s = reinterpret_cast<const float4*>(src.at(g));
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n4;
+       i += (long long)gridDim.x * blockDim.x)
+    d[i] = s[i];
+}
+
+__global__ void correct_kernel(int G, long long n4, Mat dst, Mat a, Mat b, const int* active) {
+  if (stopped(active)) return;
+  const int g = blockIdx.y;
+  float4* d = reinterpret_cast<float4*>(dst.at(g));
+  const float4* pa = reinterpret_cast<const float4*>(a.at(g));
+  const float4* pb = reinterpret_cast<const float4*>(b.at(g));
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n4;
+       i += (long long)gridDim.x * blockDim.x) {
+    const float4 x = d[i], u = pa[i], w = pb[i];
+    d[i] = make_float4(x.x + (u.x - w.x), x.y + (u.y - w.y), x.z + (u.z - w.z),
+                       x.w + (u.w - w.w));
+  }
+}
+
+__global__ void zero_kernel(int G, long long n4, Mat dst, const int* active) {
+  if (stopped(active)) return;
+  float4* d = reinterpret_cast<float4*>(dst.at(blockIdx.y));
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n4;
+       i += (long long)gridDim.x * blockDim.x)
+    d[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+}
+
+int stream_grid(long long n4, int G) {
+  // ~4 waves of 148 SMs across the whole family
+  long long want = (592LL + G - 1) / G;
+  long long need = (n4 + 255) / 256;
+  return (int)std::max<long long>(1, std::min(want, need));
+}
+
+// ---- solve control -------------------------------------------------------------------
+__global__ void ctrl_begin_kernel(SolveCtrl* c) {
+  c->active = 1;
+  c->n_trace = 0;
+  c->converged = 0;
+  c->cycles_run = 0;
+  c->pending = 0.0;
+}
+
+__global__ void trace_record_kernel(SolveCtrl* c, const double* partials, int count) {
+  __shared__ double red[32];
+  if (!c->active) return;
+  double s = 0.0;
+  for (int i = threadIdx.x; i < count; i += blockDim.x) s += partials[i];
+  const double t = block_sum_f64(s, red);
+  if (threadIdx.x == 0) c->pending = sqrt(t);
+}
+
+__global__ void cycle_end_kernel(SolveCtrl* c, double tol) {
+  if (!c->active) return;
+  const double nrm = c->pending;
+  if (c->n_trace < kMaxTrace) c->trace[c->n_trace] = nrm;
+  c->n_trace += 1;
+  c->cycles_run += 1;
+  if (!isfinite(nrm)) {
+    c->active = 0;
+  } else if (nrm <= tol * c->trace[0]) {
+    c->converged = 1;
+    c->active = 0;
+  }
+}
+
+}  // namespace
+
+void launch_ln_fwd(const LnFwdArgs& a, const int* active, cudaStream_t s) {
+  if (a.rows == 0 || a.G == 0) return;
+  dispatch_rows<LnFwdL>(a.d, a, a.G, a.rows, active, s);
+}
+
+int ln_bwd_blocks(int rows) { return ceil_div(rows, kRowsPerBlock); }
+
+void launch_ln_bwd(const LnBwdArgs& a, const int* active, cudaStream_t s) {
+  if (a.rows == 0 || a.G == 0) return;
+  dispatch_rows<LnBwdL>(a.d, a, a.G, a.rows, active, s);
+}
+
+void launch_colred(const ColRedArgs& a, const int* active, cudaStream_t s) {
+  if (a.rows == 0 || a.G == 0) return;
+  dim3 grid(ceil_div(a.cols, 32), a.G);
+  colred_kernel<<<grid, 256, 0, s>>>(a, active);
+}
+
+int elem_combine_blocks(long long n) {
+  return ceil_div(n, (long long)kElemThreads * kElemPerThread);
+}
+
+void launch_elem_combine(const ElemCombineArgs& a, const int* active, cudaStream_t s) {
+  if (a.n == 0 || a.G == 0) return;
+  dim3 grid(elem_combine_blocks(a.n), a.G);
+  elem_combine_kernel<<<grid, kElemThreads, 0, s>>>(a, active);
+}
+
+static void require_vec4(long long n, const char* what) {
+  if (n % 4) throw ContractViolation(std::string(what) + ": size must be a multiple of 4");
+}
+
+void launch_copy(int G, long long n, Mat dst, Mat src, const int* active, cudaStream_t s) {
+  if (G == 0 || n == 0) return;
+  require_vec4(n, "copy");
+  dim3 grid(stream_grid(n / 4, G), G);
+  copy_kernel<<<grid, 256, 0, s>>>(G, n / 4, dst, src, active);
+}
+
+void launch_correct(int G, long long n, Mat dst, Mat a, Mat b, const int* active,
+                    cudaStream_t s) {
+  if (G == 0 || n == 0) return;
+  require_vec4(n, "correct");
+  dim3 grid(stream_grid(n / 4, G), G);
+  correct_kernel<<<grid, 256, 0, s>>>(G, n / 4, dst, a, b, active);
+}
+
+void launch_zero(int G, long long n, Mat dst, const int* active, cudaStream_t s) {
+  if (G == 0 || n == 0) return;
+  require_vec4(n, "zero");
+  dim3 grid(stream_grid(n / 4, G), G);
+  zero_kernel<<<grid, 256, 0, s>>>(G, n / 4, dst, active);
+}
+
+void launch_ctrl_begin(SolveCtrl* c, cudaStream_t s) { ctrl_begin_kernel<<<1, 1, 0, s>>>(c); }
+
+void launch_trace_record(SolveCtrl* c, const double* partials, int count, cudaStream_t s) {
+  trace_record_kernel<<<1, 256, 0, s>>>(c, partials, count);
+}
+
+void launch_cycle_end(SolveCtrl* c, double tol, cudaStream_t s) {
+  cycle_end_kernel<<<1, 1, 0, s>>>(c, tol);
+}
+
+}  // namespace mglp
