@@ -159,6 +159,15 @@ mglp_status mglp_engine_sync(mglp_engine* e);
 /* hot-path kernel launches issued since the last call (then reset) */
 mglp_status mglp_engine_take_launch_count(mglp_engine* e, long long* n);
 
+/* per-kernel-class device timing for roofline reporting: when enabled, every
+ * launch is bracketed by CUDA events on the engine stream. Classes: 0 tensor
+ * core GEMM, 1 attention, 2 LayerNorm rows. Reading returns per class the
+ * summed device ms, algorithmic FLOPs, algorithmic bytes and launch count
+ * since profiling was (re)enabled. */
+mglp_status mglp_engine_profile(mglp_engine* e, int enable);
+mglp_status mglp_engine_profile_read(mglp_engine* e, double* ms, double* flops, double* bytes,
+                                     long long* launches);
+
 /* ---- controller (controller.hpp:63-155) ----
  * Pure decision rule, evaluated on the device from the device-resident
  * residual traces of the last forward and backward solves:
@@ -169,6 +178,12 @@ mglp_status mglp_engine_take_launch_count(mglp_engine* e, long long* n);
 mglp_status mglp_monitor_record(mglp_engine* e, double threshold, int policy_switch,
                                 int max_iter_cap, double* fwd_factor, double* bwd_factor,
                                 int* decision);
+
+/* Host helper: out[i] = scale * rng::gaussian(seed, a, b, i) (rng.hpp:70-79),
+ * bit-identical to the reference (same libm); the reference bench's z0 draw
+ * is (seed, kTestOnly=6, 7) with scale 0.5 (tools/main.cpp:121-128). */
+mglp_status mglp_rng_gaussian_fill(unsigned long long seed, unsigned long long a,
+                                   unsigned long long b, double scale, double* out, long long n);
 
 /* ---- test hook: one GEMM family on device buffers ----
  * C_g[M,N] = A_g . B_g^T (+ bias), g < G; A_g at A + g*a_slot (row stride

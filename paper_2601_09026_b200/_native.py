@@ -79,6 +79,10 @@ _SIGS = {
     "mglp_engine_sync": [_vp],
     "mglp_engine_take_launch_count": [_vp, _llp],
     "mglp_monitor_record": [_vp, C.c_double, C.c_int, C.c_int, _dp, _dp, _ip],
+    "mglp_engine_profile": [_vp, C.c_int],
+    "mglp_rng_gaussian_fill": [C.c_ulonglong, C.c_ulonglong, C.c_ulonglong, C.c_double, _dp,
+                               C.c_longlong],
+    "mglp_engine_profile_read": [_vp, _dp, _dp, _dp, _llp],
     "mglp_test_gemm": [C.c_int, C.c_int, C.c_int, C.c_int, _vp, C.c_longlong, C.c_int, C.c_int,
                        _vp, C.c_longlong, C.c_int, C.c_int, C.c_int, _vp, _vp, C.c_longlong,
                        C.c_int, C.c_int],

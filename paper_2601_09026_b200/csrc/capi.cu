@@ -480,6 +480,33 @@ mglp_status mglp_engine_take_launch_count(mglp_engine* e, long long* n) {
   });
 }
 
+mglp_status mglp_rng_gaussian_fill(unsigned long long seed, unsigned long long a,
+                                   unsigned long long b, double scale, double* out, long long n) {
+  return guard([&] {
+    need(out, "out");
+    rng_gaussian_fill(seed, a, b, scale, out, n);
+  });
+}
+
+mglp_status mglp_engine_profile(mglp_engine* e, int enable) {
+  return guard([&] {
+    need(e, "engine");
+    e->eng->set_profiling(enable != 0);
+  });
+}
+
+mglp_status mglp_engine_profile_read(mglp_engine* e, double* ms, double* flops, double* bytes,
+                                     long long* launches) {
+  return guard([&] {
+    need(e, "engine");
+    need(ms, "ms");
+    need(flops, "flops");
+    need(bytes, "bytes");
+    need(launches, "launches");
+    e->eng->read_profile(ms, flops, bytes, launches);
+  });
+}
+
 mglp_status mglp_monitor_record(mglp_engine* e, double threshold, int policy_switch,
                                 int max_iter_cap, double* fwd_factor, double* bwd_factor,
                                 int* decision) {
@@ -543,7 +570,7 @@ mglp_status mglp_test_gemm(int G, int M, int N, int K, const float* A, long long
       g.ep.bias.slot_stride = 0;
     }
     float *hi = nullptr, *lo = nullptr;
-    if (b_presplit) {
+    if (b_presplit && engine == 0) {
       const long long rows = b_mn ? K : N;
       const long long n = (long long)(G - 1) * b_slot + rows * ldb;
       MGLP_CUDA(cudaMalloc(&hi, n * sizeof(float)));

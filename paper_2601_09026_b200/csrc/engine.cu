@@ -12,6 +12,14 @@ namespace mglp {
 
 namespace {
 
+// algorithmic attention FLOPs: 4*B*H*sq*skv*dh forward (half
+// if causal); the VJP recomputes S and forms dP, dV, dQ, dK: 2x forward + S.
+double attn_flops(const AttnArgs& a, bool bwd) {
+  double f = 4.0 * a.G * a.B * a.H * (double)a.sq * a.skv * a.dh;
+  if (a.causal) f *= 0.5;
+  return bwd ? 2.5 * f : f;
+}
+
 // ---- counter-based RNG, bit-identical to rng.hpp:37-89 ------------------------
 inline uint64_t splitmix64(uint64_t x) {
   x += 0x9e3779b97f4a7c15ULL;
@@ -74,6 +82,17 @@ Mat shift(Mat m, int g0) {
 }
 
 }  // namespace
+
+void rng_gaussian_fill(uint64_t seed, uint64_t a, uint64_t b, double scale, double* out,
+                       long long n) {
+  const unsigned nt = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+  std::vector<std::thread> th;
+  for (unsigned t = 0; t < nt; ++t)
+    th.emplace_back([=] {
+      for (long long i = t; i < n; i += nt) out[i] = scale * gaussian(seed, a, b, (uint64_t)i, 0);
+    });
+  for (auto& x : th) x.join();
+}
 
 // =============================================================================
 // construction, parameters
@@ -158,6 +177,7 @@ Engine::~Engine() {
   for (float* p : {P_, Phi_, Plo_, Gr_, scratch_, cache_, bscratch_, traj_, lam_all_,
                    zero_state_, snap_fwd_, snap_bwd_})
     if (p) cudaFree(p);
+  for (cudaEvent_t ev : ev_pool_) cudaEventDestroy(ev);
   if (stream_) cudaStreamDestroy(stream_);
 }
 
@@ -533,11 +553,48 @@ Mat Engine::grad(long long off, int ld, int layer0, int step) const {
 
 void Engine::gemm(GemmArgs g) {
   ++launches_;
+  const double flops = 2.0 * g.G * (double)g.M * g.N * g.K;
+  timed(PROF_GEMM, flops, 0.0, [&] {
 #ifdef MGLP_GEMM_SIMT
-  launch_gemm_simt(g, active_, stream_);
+    // the reference kernel takes the unsplit fp32 weights
+    if (g.Blo.ok() && g.B.ptr >= Phi_ && g.B.ptr < Phi_ + (size_t)total_ * layer_stride_)
+      g.B.ptr = P_ + (g.B.ptr - Phi_);
+    launch_gemm_simt(g, active_, stream_);
 #else
-  launch_gemm_tc(g, active_, stream_);
+    launch_gemm_tc(g, active_, stream_);
 #endif
+  });
+}
+
+cudaEvent_t Engine::prof_event() {
+  if (ev_used_ == ev_pool_.size()) {
+    cudaEvent_t e;
+    MGLP_CUDA(cudaEventCreate(&e));
+    ev_pool_.push_back(e);
+  }
+  return ev_pool_[ev_used_++];
+}
+
+void Engine::set_profiling(bool on) {
+  profiling_ = on;
+  prof_.clear();
+  ev_used_ = 0;
+}
+
+void Engine::read_profile(double* ms, double* flops, double* bytes, long long* launches) {
+  MGLP_CUDA(cudaStreamSynchronize(stream_));
+  for (int c = 0; c < PROF_NCLASS; ++c) {
+    ms[c] = flops[c] = bytes[c] = 0.0;
+    launches[c] = 0;
+  }
+  for (const ProfRec& r : prof_) {
+    float t = 0.f;
+    MGLP_CUDA(cudaEventElapsedTime(&t, r.a, r.b));
+    ms[r.cls] += t;
+    flops[r.cls] += r.flops;
+    bytes[r.cls] += r.bytes;
+    launches[r.cls] += 1;
+  }
 }
 
 int Engine::gemm_blocks(const GemmArgs& g) const {
@@ -624,7 +681,8 @@ void Engine::encoder_forward(const EvalSpec& e, int R, bool causal, Mat X, Mat Y
   ln.gain = par(L.ln1_g, 0, l0, ls);
   ln.bias = par(L.ln1_b, 0, l0, ls);
   ++launches_;
-  launch_ln_fwd(ln, active_, stream_);
+  timed(PROF_ROW, 0.0, 8.0 * ln.G * (double)ln.rows * ln.d,
+        [&] { launch_ln_fwd(ln, active_, stream_); });
 
   GemmArgs g;
   g.G = G;
@@ -653,7 +711,7 @@ void Engine::encoder_forward(const EvalSpec& e, int R, bool causal, Mat X, Mat Y
   at.o = ctx;
   at.lse = lse;
   ++launches_;
-  launch_attn_fwd(at, active_, stream_);
+  timed(PROF_ATTN, attn_flops(at, false), 0.0, [&] { launch_attn_fwd(at, active_, stream_); });
 
   g = GemmArgs{};
   g.G = G;
@@ -676,7 +734,8 @@ void Engine::encoder_forward(const EvalSpec& e, int R, bool causal, Mat X, Mat Y
   ln.gain = par(L.ln2_g, 0, l0, ls);
   ln.bias = par(L.ln2_b, 0, l0, ls);
   ++launches_;
-  launch_ln_fwd(ln, active_, stream_);
+  timed(PROF_ROW, 0.0, 8.0 * ln.G * (double)ln.rows * ln.d,
+        [&] { launch_ln_fwd(ln, active_, stream_); });
 
   g = GemmArgs{};
   g.G = G;
@@ -758,7 +817,8 @@ void Engine::decoder_forward(const EvalSpec& e) {
   ln.gain = par(L.ln1_g, 0, l0, ls);
   ln.bias = par(L.ln1_b, 0, l0, ls);
   ++launches_;
-  launch_ln_fwd(ln, active_, stream_);
+  timed(PROF_ROW, 0.0, 8.0 * ln.G * (double)ln.rows * ln.d,
+        [&] { launch_ln_fwd(ln, active_, stream_); });
 
   auto mk = [&](int M, int N, int K, Mat A, long long w, int ldw) {
     GemmArgs g;
@@ -791,7 +851,7 @@ void Engine::decoder_forward(const EvalSpec& e) {
   at.o = ctx;
   at.lse = lse;
   ++launches_;
-  launch_attn_fwd(at, active_, stream_);
+  timed(PROF_ATTN, attn_flops(at, false), 0.0, [&] { launch_attn_fwd(at, active_, stream_); });
 
   g = mk(R, d, d, ctx, L.w_o, d);
   g.ep.kind = EPI_BIAS_ADD2;
@@ -807,7 +867,8 @@ void Engine::decoder_forward(const EvalSpec& e) {
   ln.gain = par(L.ln3_g, 0, l0, ls);
   ln.bias = par(L.ln3_b, 0, l0, ls);
   ++launches_;
-  launch_ln_fwd(ln, active_, stream_);
+  timed(PROF_ROW, 0.0, 8.0 * ln.G * (double)ln.rows * ln.d,
+        [&] { launch_ln_fwd(ln, active_, stream_); });
 
   g = mk(R, d, d, n3, L.w_cq, d);
   g.ep.kind = EPI_STORE;
@@ -830,7 +891,7 @@ void Engine::decoder_forward(const EvalSpec& e) {
   at.o = cctx;
   at.lse = clse;
   ++launches_;
-  launch_attn_fwd(at, active_, stream_);
+  timed(PROF_ATTN, attn_flops(at, false), 0.0, [&] { launch_attn_fwd(at, active_, stream_); });
 
   g = mk(R, d, d, cctx, L.w_co, d);
   g.ep.kind = EPI_BIAS_ADD2;
@@ -847,7 +908,8 @@ void Engine::decoder_forward(const EvalSpec& e) {
   ln.gain = par(L.ln2_g, 0, l0, ls);
   ln.bias = par(L.ln2_b, 0, l0, ls);
   ++launches_;
-  launch_ln_fwd(ln, active_, stream_);
+  timed(PROF_ROW, 0.0, 8.0 * ln.G * (double)ln.rows * ln.d,
+        [&] { launch_ln_fwd(ln, active_, stream_); });
 
   g = mk(R, f, d, n2, L.w_in, d);
   g.ep.kind = EPI_BIAS_GELU;
@@ -974,7 +1036,8 @@ void Engine::encoder_adjoint(const EvalSpec& e, bool causal) {
   lb.out2 = da1;
   lb.addB = UP;
   ++launches_;
-  launch_ln_bwd(lb, active_, stream_);
+  timed(PROF_ROW, 0.0, 20.0 * lb.G * (double)lb.rows * lb.d,
+        [&] { launch_ln_bwd(lb, active_, stream_); });
 
   g = mk(R, d, d, da1, L.w_o, d);
   g.ep.kind = EPI_STORE;
@@ -1000,7 +1063,7 @@ void Engine::encoder_adjoint(const EvalSpec& e, bool causal) {
   at.dv = dqkv.offset(2 * d);
   at.dd = dd;
   launches_ += 3;
-  launch_attn_bwd(at, active_, stream_);
+  timed(PROF_ATTN, attn_flops(at, true), 0.0, [&] { launch_attn_bwd(at, active_, stream_); });
 
   g = mk(R, d, 3 * d, dqkv, L.w_qkv, d);
   g.ep.kind = EPI_STORE;
@@ -1026,7 +1089,8 @@ void Engine::encoder_adjoint(const EvalSpec& e, bool causal) {
     if (c.mode == CM_RES0) c.norm_base = take_partials(G * ln_bwd_blocks(R));
     l1.cmb = c;
     ++launches_;
-    launch_ln_bwd(l1, active_, stream_);
+    timed(PROF_ROW, 0.0, 20.0 * l1.G * (double)l1.rows * l1.d,
+          [&] { launch_ln_bwd(l1, active_, stream_); });
     if (sd_.kind == 2) {
       ElemCombineArgs ec;
       ec.G = G;
@@ -1143,7 +1207,8 @@ void Engine::decoder_adjoint(const EvalSpec& e) {
   lb.out2 = dybar;   // up + du2
   lb.addB = UPy;
   ++launches_;
-  launch_ln_bwd(lb, active_, stream_);
+  timed(PROF_ROW, 0.0, 20.0 * lb.G * (double)lb.rows * lb.d,
+        [&] { launch_ln_bwd(lb, active_, stream_); });
 
   g = mk(R, d, d, dybar, L.w_co, d);
   g.ep.kind = EPI_STORE;
@@ -1170,7 +1235,7 @@ void Engine::decoder_adjoint(const EvalSpec& e) {
   at.dv = dckv.offset(d);
   at.dd = dd2;
   launches_ += 3;
-  launch_attn_bwd(at, active_, stream_);
+  timed(PROF_ATTN, attn_flops(at, true), 0.0, [&] { launch_attn_bwd(at, active_, stream_); });
 
   g = mk(R, d, d, dcq, L.w_cq, d);
   g.ep.kind = EPI_STORE;
@@ -1191,7 +1256,8 @@ void Engine::decoder_adjoint(const EvalSpec& e) {
   lb.addB = dybar;
   lb.out2 = da1;    // dybar + du3
   ++launches_;
-  launch_ln_bwd(lb, active_, stream_);
+  timed(PROF_ROW, 0.0, 20.0 * lb.G * (double)lb.rows * lb.d,
+        [&] { launch_ln_bwd(lb, active_, stream_); });
 
   g = mk(R, d, d, da1, L.w_o, d);
   g.ep.kind = EPI_STORE;
@@ -1211,7 +1277,7 @@ void Engine::decoder_adjoint(const EvalSpec& e) {
   at.dv = dqkv.offset(2 * d);
   at.dd = dd;
   launches_ += 3;
-  launch_attn_bwd(at, active_, stream_);
+  timed(PROF_ATTN, attn_flops(at, true), 0.0, [&] { launch_attn_bwd(at, active_, stream_); });
 
   g = mk(R, d, 3 * d, dqkv, L.w_qkv, d);
   g.ep.kind = EPI_STORE;
@@ -1237,7 +1303,8 @@ void Engine::decoder_adjoint(const EvalSpec& e) {
     if (c.mode == CM_RES0) c.norm_base = take_partials(G * ln_bwd_blocks(R));
     l1.cmb = c;
     ++launches_;
-    launch_ln_bwd(l1, active_, stream_);
+    timed(PROF_ROW, 0.0, 20.0 * l1.G * (double)l1.rows * l1.d,
+          [&] { launch_ln_bwd(l1, active_, stream_); });
     ElemCombineArgs ec;
     ec.G = G;
     ec.n = (long long)Tx_ * d;

@@ -48,6 +48,10 @@ class Transport {
   virtual void group_end() {}
 };
 
+// out[i] = scale * gaussian(seed, a, b, i), multithreaded, bit-identical to rng.hpp
+void rng_gaussian_fill(uint64_t seed, uint64_t a, uint64_t b, double scale, double* out,
+                       long long n);
+
 class Engine {
  public:
   Engine(const StackDesc& sd, const SolveCfg& cfg, int device, std::shared_ptr<Transport> tr);
@@ -95,6 +99,12 @@ class Engine {
   long long launch_count() const { return launches_; }
   void reset_launch_count() { launches_ = 0; }
 
+  // per-kernel-class device timing (CUDA events around every launch of the
+  // class on the engine stream); used by bench.py for the roofline, never in
+  // the timed region.
+  enum ProfClass { PROF_GEMM = 0, PROF_ATTN = 1, PROF_ROW = 2, PROF_NCLASS = 3 };
+  void set_profiling(bool on);
+  void read_profile(double* ms, double* flops, double* bytes, long long* launches);
   // test hooks: one Phi / Phi^T application on the device
   void step_device(int layer, double dt, const float* z, float* out);
   void adjoint_step_device(int layer, double dt, const float* z, const float* lam, float* out,
@@ -236,6 +246,28 @@ class Engine {
   long long launches_ = 0;
   const int* active_ = nullptr;  // current solve-control flag
   int pcursor_ = 0, pcap_ = 0;   // residual-norm partial slots handed out
+  struct ProfRec {
+    cudaEvent_t a, b;
+    int cls;
+    double flops, bytes;
+  };
+  bool profiling_ = false;
+  std::vector<ProfRec> prof_;
+  std::vector<cudaEvent_t> ev_pool_;
+  size_t ev_used_ = 0;
+  cudaEvent_t prof_event();
+  template <class F>
+  void timed(int cls, double flops, double bytes, F&& launch) {
+    if (!profiling_) {
+      launch();
+      return;
+    }
+    ProfRec r{prof_event(), prof_event(), cls, flops, bytes};
+    cudaEventRecord(r.a, stream_);
+    launch();
+    cudaEventRecord(r.b, stream_);
+    prof_.push_back(r);
+  }
 };
 
 }  // namespace mglp

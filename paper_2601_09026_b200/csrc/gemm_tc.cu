@@ -22,6 +22,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <cstdlib>
 #include <mutex>
 
 #include "kernels.cuh"
@@ -43,6 +44,7 @@ struct TcParams {
   int G, M, N, K;
   TcOperand a, b, blo;
   int b_presplit;
+  int passes;  // 3 = hi.hi + (lo.hi + hi.lo); 1 = hi.hi only (diagnostics)
   EpiArgs ep;
 };
 
@@ -86,14 +88,19 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, u
       : "memory");
 }
 
-__device__ __forceinline__ uint64_t smem_desc(const void* p, uint32_t lbo, uint32_t sbo) {
+// UMMA shared-memory descriptor. K-major operands use SWIZZLE_128B (layout
+// type 2); MN-major tf32 operands must use SWIZZLE_128B_BASE32B (type 1,
+// 32-byte granules over 4 rows -- the only MN-major layout tf32 supports,
+// matched by TMA's CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B).
+__device__ __forceinline__ uint64_t smem_desc(const void* p, uint32_t lbo, uint32_t sbo,
+                                              uint32_t layout) {
   const uint64_t addr = smem_u32(p);
   uint64_t d = 0;
   d |= (addr >> 4) & 0x3FFFull;
   d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
   d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
   d |= 1ull << 46;  // sm100 descriptor version
-  d |= 2ull << 61;  // SWIZZLE_128B
+  d |= (uint64_t)layout << 61;
   return d;
 }
 
@@ -202,7 +209,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 2) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_u32(tmem_slot)),
-                 "r"((uint32_t)BN));
+                 "r"((uint32_t)(2 * BN)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -251,8 +258,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)p.a.mn << 15) |
                              ((uint32_t)p.b.mn << 16) | ((uint32_t)(BN >> 3) << 17) |
                              ((uint32_t)(BM >> 4) << 24);
-      const uint32_t a_lbo = p.a.mn ? 4096u : 16u, a_sbo = 1024u;
-      const uint32_t b_lbo = p.b.mn ? 4096u : 16u, b_sbo = 1024u;
+      // MN-major: LBO = stride between 32-element MN blocks (one 32-row TMA
+      // box), SBO = stride between 4-row K groups of the BASE32B atom
+      const uint32_t a_lbo = p.a.mn ? 4096u : 16u, a_sbo = p.a.mn ? 512u : 1024u;
+      const uint32_t b_lbo = p.b.mn ? 4096u : 16u, b_sbo = p.b.mn ? 512u : 1024u;
+      const uint32_t a_lay = p.a.mn ? 1u : 2u, b_lay = p.b.mn ? 1u : 2u;
       const uint32_t a_kstep = p.a.mn ? 1024u : 32u;  // bytes per K=8 step
       const uint32_t b_kstep = p.b.mn ? 1024u : 32u;
       for (int kb = 0; kb < nk; ++kb) {
@@ -262,14 +272,19 @@ __global__ void __launch_bounds__(kThreads, 1)
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #pragma unroll
         for (int k = 0; k < BK / 8; ++k) {
-          const uint64_t dah = smem_desc(stage_a(s) + k * a_kstep, a_lbo, a_sbo);
-          const uint64_t dal = smem_desc(stage_alo(s) + k * a_kstep, a_lbo, a_sbo);
-          const uint64_t dbh = smem_desc(stage_b(s) + k * b_kstep, b_lbo, b_sbo);
-          const uint64_t dbl = smem_desc(stage_blo(s) + k * b_kstep, b_lbo, b_sbo);
+          const uint64_t dah = smem_desc(stage_a(s) + k * a_kstep, a_lbo, a_sbo, a_lay);
+          const uint64_t dal = smem_desc(stage_alo(s) + k * a_kstep, a_lbo, a_sbo, a_lay);
+          const uint64_t dbh = smem_desc(stage_b(s) + k * b_kstep, b_lbo, b_sbo, b_lay);
+          const uint64_t dbl = smem_desc(stage_blo(s) + k * b_kstep, b_lbo, b_sbo, b_lay);
           const uint32_t acc0 = (kb > 0 || k > 0) ? 1u : 0u;
-          mma_tf32(tmem_base, dal, dbh, idesc, acc0);  // small terms first
-          mma_tf32(tmem_base, dah, dbl, idesc, 1u);
-          mma_tf32(tmem_base, dah, dbh, idesc, 1u);
+          // main product and the two correction products accumulate in
+          // separate TMEM accumulators, so the small terms are not rounded
+          // against the large running sum
+          mma_tf32(tmem_base, dah, dbh, idesc, acc0);
+          if (p.passes > 1) {
+            mma_tf32(tmem_base + BN, dal, dbh, idesc, acc0);
+            mma_tf32(tmem_base + BN, dah, dbl, idesc, 1u);
+          }
         }
         mma_commit(&empty[s]);
       }
@@ -306,6 +321,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int c = 0; c < BN; c += 16) {
       float v[16];
       tmem_ld16(lane_addr + c, v);
+      if (p.passes > 1) {
+        float w[16];
+        tmem_ld16(lane_addr + BN + c, w);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) v[i] += w[i];
+      }
       const int col0 = n0 + c;
       const int nvalid = min(16, p.N - col0);
       if (row < p.M && nvalid > 0) r2 += epilogue_row(p.ep, g, row, col0, v, nvalid);
@@ -315,7 +336,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   if (warp == 2)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
-                 "r"((uint32_t)BN));
+                 "r"((uint32_t)(2 * BN)));
   if (p.ep.kind == EPI_FINAL && p.ep.cmb.mode == CM_RES0) {
     for (int o = 16; o > 0; o >>= 1) r2 += __shfl_xor_sync(0xffffffffu, r2, o);
     if (lane == 0) red[warp] = r2;
@@ -359,7 +380,8 @@ PFN_cuTensorMapEncodeTiled_v12000 encoder() {
 
 // Map over the slots a family touches: member g -> slot slot0 + g*step.
 // rows x cols is the [rows][cols] matrix inside one slot (row stride ld).
-CUtensorMap make_map(const Mat& m, int G, int rows, int cols, int box_rows, TcOperand* op) {
+CUtensorMap make_map(const Mat& m, int G, int rows, int cols, int box_rows, TcOperand* op,
+                     bool mn_major) {
   long long lo = m.slot0, hi = m.slot0 + (long long)(G - 1) * m.step;
   if (hi < lo) std::swap(lo, hi);
   const float* base = m.ptr + lo * m.slot_stride;
@@ -383,7 +405,9 @@ CUtensorMap make_map(const Mat& m, int G, int rows, int cols, int box_rows, TcOp
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = encoder()(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), dims,
                          strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                         CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                         mn_major ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B
+                                  : CU_TENSOR_MAP_SWIZZLE_128B,
+                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS)
     throw ContractViolation("cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
@@ -399,18 +423,23 @@ void launch_cfg(const GemmArgs& a, const int* active, cudaStream_t s) {
   p.K = a.K;
   p.ep = a.ep;
   p.b_presplit = a.Blo.ok() ? 1 : 0;
+  static const int passes = [] {
+    const char* e = getenv("MGLP_DEBUG_TF32_PASSES");
+    return e ? atoi(e) : 3;
+  }();
+  p.passes = passes;
   p.a.mn = a.a_mn;
   p.b.mn = a.b_mn;
   p.blo.mn = a.b_mn;
   // A: [M][K] (K-major) or [K][M] (MN-major); box rows: BM, or 32 K-rows
-  CUtensorMap mA = a.a_mn ? make_map(a.A, a.G, a.K, a.M, BK, &p.a)
-                          : make_map(a.A, a.G, a.M, a.K, BM, &p.a);
-  CUtensorMap mB = a.b_mn ? make_map(a.B, a.G, a.K, a.N, BK, &p.b)
-                          : make_map(a.B, a.G, a.N, a.K, BN, &p.b);
+  CUtensorMap mA = a.a_mn ? make_map(a.A, a.G, a.K, a.M, BK, &p.a, true)
+                          : make_map(a.A, a.G, a.M, a.K, BM, &p.a, false);
+  CUtensorMap mB = a.b_mn ? make_map(a.B, a.G, a.K, a.N, BK, &p.b, true)
+                          : make_map(a.B, a.G, a.N, a.K, BN, &p.b, false);
   CUtensorMap mBlo = mB;
   if (p.b_presplit)
-    mBlo = a.b_mn ? make_map(a.Blo, a.G, a.K, a.N, BK, &p.blo)
-                  : make_map(a.Blo, a.G, a.N, a.K, BN, &p.blo);
+    mBlo = a.b_mn ? make_map(a.Blo, a.G, a.K, a.N, BK, &p.blo, true)
+                  : make_map(a.Blo, a.G, a.N, a.K, BN, &p.blo, false);
   else
     p.blo = p.b;
   const int smem = Smem<BN, STAGES>::BYTES;

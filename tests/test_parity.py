@@ -262,3 +262,60 @@ def test_against_numpy_oracle_random_configs(cfg):
     assert rel(bo.phase.trace, obtr) < TOL
     assert rel(bo.lambda0.flat(), ol0.flat()) < TOL
     assert rel(gr, O.Stack.flatten(og)) < TOL
+
+
+def test_full_width_slice_against_numpy_oracle():
+    """BERT-width block (d=768, 12 heads, ffn=3072, seq 128) on a shallow
+    stack: the K=768/3072 GEMMs and 128-token attention at full size."""
+    sc = StackConfig(kind="encoder", d=768, heads=12, ffn=3072, n_enc=8)
+    st = LayerStack(sc, 7)
+    ost = O.Stack(O.StackConfig(kind="encoder", d=768, heads=12, ffn=3072, n_enc=8),
+                  np.asarray(st.params()))
+    rng = np.random.default_rng(3)
+    B, s = 2, 128
+    z0 = rng.standard_normal(B * s * 768) * 0.5
+    lam = rng.standard_normal(B * s * 768)
+    cfg = dict(coarsen=4, levels=2, fwd_iters=1, bwd_iters=1)
+    eng = LayerParallelEngine(st, SolveConfig(**cfg))
+    fo = eng.forward(State.from_flat(z0, B, s, 0, 768))
+    gr = st.zero_grads()
+    bo = eng.backward(fo.traj, State.from_flat(lam, B, s, 0, 768), gr)
+    oe = O.LayerParallelEngine(ost, O.SolveConfig(**cfg))
+    otraj, otr, _ = oe.forward(O.State.from_flat(z0, B, s, 0, 768))
+    og = ost.zero_grads()
+    ol0, obtr, _ = oe.backward(otraj, O.State.from_flat(lam, B, s, 0, 768), og)
+    assert rel(np.stack([t.flat() for t in fo.traj]), np.stack([t.flat() for t in otraj])) < TOL
+    assert rel(fo.phase.trace, otr) < TOL
+    assert rel(bo.phase.trace, obtr) < TOL
+    assert rel(bo.lambda0.flat(), ol0.flat()) < TOL
+    assert rel(gr, O.Stack.flatten(og)) < TOL
+
+
+@pytest.mark.parametrize("kind", ["encoder", "decoder_only", "encoder_decoder"])
+def test_full_size_fixed_point_and_convergence(kind):
+    """Size-independent properties at BASELINE sizes (d=768/512, 128-token
+    sequences, batch 32): one V-cycle from the device serial trajectory is a
+    bitwise fixed point; a converged MGRIT solve reproduces the serial sweep."""
+    if kind == "encoder_decoder":
+        sc = StackConfig(kind=kind, d=512, heads=8, ffn=2048, n_enc=8, n_dec=8)
+        B, sx, sy, d = 32, 128, 128, 512
+    else:
+        sc = StackConfig(kind=kind, d=768, heads=12, ffn=3072, n_enc=16 if kind == "encoder" else 0,
+                         n_dec=16 if kind == "decoder_only" else 0)
+        B, sx, sy, d = 32, 128, 0, 768
+    st = LayerStack(sc, 7)
+    n = B * (sx + sy) * d
+    rng = np.random.default_rng(0)
+    z0 = State.from_flat(rng.standard_normal(n) * 0.5, B, sx, sy, d)
+    eng = LayerParallelEngine(st, SolveConfig(coarsen=4, levels=2, fwd_iters=1, cold_guess="warm"))
+    eng._sync()
+    zf = z0.flat()
+    T0 = np.empty((st.total_layers() + 1, zf.size))
+    N.call("mglp_serial_forward", eng.handle, B, sx, sy, N.dptr(zf), N.dptr(T0))
+    fo = eng.forward(z0)
+    assert fo.phase.trace == [0.0]
+    assert np.array_equal(T0, np.stack([t.flat() for t in fo.traj]))
+    eng2 = LayerParallelEngine(st, SolveConfig(coarsen=4, levels=2, fwd_iters=8, warm_start=False))
+    f2 = eng2.forward(z0)
+    assert f2.phase.trace[-1] < 1e-5 * f2.phase.trace[0]
+    assert rel(np.stack([t.flat() for t in f2.traj]), T0) < TOL
