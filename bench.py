@@ -397,8 +397,8 @@ def run_device(args, cfg, rank, world, dist):
                                    if tf32.get("tf32_tflops_sustained") else None),
         "gemm_share_of_step": gemm_ms / sum(ms3) if sum(ms3) > 0 else None,
         "gemm_launches_per_step": gemm_n,
-        "per_class_ms": {"gemm": ms3[0], "attention": ms3[1], "layernorm": ms3[2]},
-        "attention_tflops": fl3[1] / (ms3[1] * 1e-3) / 1e12 if ms3[1] > 0 else None,
+        "per_class_ms": {"gemm_tcgen05": ms3[0], "other": ms3[1],
+                         "rows_layernorm_softmax": ms3[2]},
     }
     cpu = None
     if world == 1 and not args.no_cpu_baseline:

@@ -167,6 +167,8 @@ mglp_status mglp_engine_take_launch_count(mglp_engine* e, long long* n);
 mglp_status mglp_engine_profile(mglp_engine* e, int enable);
 mglp_status mglp_engine_profile_read(mglp_engine* e, double* ms, double* flops, double* bytes,
                                      long long* launches);
+/* per-launch rows (7 doubles each: class, M, N, K, batch, flops, ms) */
+mglp_status mglp_engine_profile_dump(mglp_engine* e, double* rows, int max_rows, int* n);
 
 /* ---- controller (controller.hpp:63-155) ----
  * Pure decision rule, evaluated on the device from the device-resident

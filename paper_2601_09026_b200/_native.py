@@ -83,6 +83,7 @@ _SIGS = {
     "mglp_rng_gaussian_fill": [C.c_ulonglong, C.c_ulonglong, C.c_ulonglong, C.c_double, _dp,
                                C.c_longlong],
     "mglp_engine_profile_read": [_vp, _dp, _dp, _dp, _llp],
+    "mglp_engine_profile_dump": [_vp, _dp, C.c_int, _ip],
     "mglp_test_gemm": [C.c_int, C.c_int, C.c_int, C.c_int, _vp, C.c_longlong, C.c_int, C.c_int,
                        _vp, C.c_longlong, C.c_int, C.c_int, C.c_int, _vp, _vp, C.c_longlong,
                        C.c_int, C.c_int],

@@ -507,6 +507,14 @@ mglp_status mglp_engine_profile_read(mglp_engine* e, double* ms, double* flops, 
   });
 }
 
+mglp_status mglp_engine_profile_dump(mglp_engine* e, double* rows, int max_rows, int* n) {
+  return guard([&] {
+    need(e, "engine");
+    need(rows, "rows");
+    *n = e->eng->dump_profile(rows, max_rows);
+  });
+}
+
 mglp_status mglp_monitor_record(mglp_engine* e, double threshold, int policy_switch,
                                 int max_iter_cap, double* fwd_factor, double* bwd_factor,
                                 int* decision) {

@@ -44,8 +44,13 @@ struct Mat {
   int ld = 0;                 // row stride (elements)
   int slot0 = 0;
   int step = 1;
+  // optional (batch, head) sub-blocks of a slot, for per-(b,h) attention GEMMs
+  long long bstride = 0, hstride = 0;
   __host__ __device__ __forceinline__ float* at(int g) const {
     return ptr + (long long)(slot0 + g * step) * slot_stride;
+  }
+  __host__ __device__ __forceinline__ float* at(int g, int b, int h) const {
+    return ptr + (long long)(slot0 + g * step) * slot_stride + b * bstride + h * hstride;
   }
   __host__ __device__ __forceinline__ bool ok() const { return ptr != nullptr; }
   __host__ Mat slot(int s0, int st) const {
@@ -123,6 +128,7 @@ struct EpiArgs {
   Mat out1, out2, add1, add2, aux;
   Mat bias;  // bias vector family (slot = layer); null => no bias
   float gscale = 1.f;
+  float alpha = 1.f;  // EPI_STORE: out1 = alpha*acc (+ bias)
   Combine cmb;  // EPI_FINAL
 };
 
@@ -142,14 +148,15 @@ __device__ __forceinline__ float gelu_grad_f(float v, float u) {
 
 // Applies the epilogue to n consecutive columns [col0, col0+n) of one output
 // row. Returns this row-segment's contribution to the residual norm^2.
-__device__ __forceinline__ double epilogue_row(const EpiArgs& e, int g, int row, int col0,
-                                               const float* acc, int n) {
+__device__ __forceinline__ double epilogue_row(const EpiArgs& e, int g, int b, int h, int row,
+                                               int col0, const float* acc, int n) {
   double r2 = 0.0;
   const float* bias = e.bias.ok() ? e.bias.at(g) : nullptr;
   switch (e.kind) {
     case EPI_STORE: {
-      float* o = e.out1.at(g) + (long long)row * e.out1.ld + col0;
-      for (int i = 0; i < n; ++i) o[i] = bias ? acc[i] + bias[col0 + i] : acc[i];
+      float* o = e.out1.at(g, b, h) + (long long)row * e.out1.ld + col0;
+      const float al = e.alpha;
+      for (int i = 0; i < n; ++i) o[i] = bias ? al * acc[i] + bias[col0 + i] : al * acc[i];
     } break;
     case EPI_BIAS_ADD2: {
       float* o1 = e.out1.ok() ? e.out1.at(g) + (long long)row * e.out1.ld + col0 : nullptr;
@@ -201,6 +208,9 @@ __device__ __forceinline__ double epilogue_row(const EpiArgs& e, int g, int row,
 // B may come pre-split into tf32 hi/lo parts (weights); see gemm_tc.cu.
 struct GemmArgs {
   int G = 1, M = 0, N = 0, K = 0;
+  // each of the G members may itself be a Bb x H grid of per-(batch, head)
+  // problems (attention); operands then use Mat::bstride / hstride
+  int Bb = 1, H = 1;
   Mat A, B, Blo;
   bool a_mn = false, b_mn = false;
   EpiArgs ep;

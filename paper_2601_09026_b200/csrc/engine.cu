@@ -12,14 +12,6 @@ namespace mglp {
 
 namespace {
 
-// algorithmic attention FLOPs: 4*B*H*sq*skv*dh forward (half
-// if causal); the VJP recomputes S and forms dP, dV, dQ, dK: 2x forward + S.
-double attn_flops(const AttnArgs& a, bool bwd) {
-  double f = 4.0 * a.G * a.B * a.H * (double)a.sq * a.skv * a.dh;
-  if (a.causal) f *= 0.5;
-  return bwd ? 2.5 * f : f;
-}
-
 // ---- counter-based RNG, bit-identical to rng.hpp:37-89 ------------------------
 inline uint64_t splitmix64(uint64_t x) {
   x += 0x9e3779b97f4a7c15ULL;
@@ -401,7 +393,7 @@ void Engine::set_shape(int batch, int s_x, int s_y) {
   a.n1 = take(R * d);
   a.qkv = take(R * 3 * d);
   a.ctx = take(R * d);
-  a.lse = take(B_ * H * smax);
+  a.P = take((long long)B_ * H * smax * ((smax + 3) & ~3));
   a.a1 = take(R * d);
   a.u = take(R * d);
   a.n2 = take(R * d);
@@ -415,7 +407,7 @@ void Engine::set_shape(int batch, int s_x, int s_y) {
     a.cq = take(Ty_ * d);
     a.ckv = take((long long)Tx_ * 2 * d);
     a.cctx = take(Ty_ * d);
-    a.clse = take(B_ * H * sy_);
+    a.cP = take((long long)B_ * H * sy_ * ((sx_ + 3) & ~3));
     a.ybar = take(Ty_ * d);
     a.st3 = take(2LL * Ty_);
   }
@@ -429,7 +421,7 @@ void Engine::set_shape(int batch, int s_x, int s_y) {
   b.dctx = take(R * d);
   b.dqkv = take(R * 3 * d);
   b.dn1 = take(R * d);
-  b.dd = take(B_ * H * smax);
+  b.dP = take((long long)B_ * H * smax * ((smax + 3) & ~3));
   if (sd_.kind == 2) {
     b.dybar = take(Ty_ * d);
     b.dy = take(Ty_ * d);
@@ -438,7 +430,7 @@ void Engine::set_shape(int batch, int s_x, int s_y) {
     b.dckv = take((long long)Tx_ * 2 * d);
     b.dn3 = take(Ty_ * d);
     b.dxe = take((long long)Tx_ * d);
-    b.dd2 = take(B_ * H * sy_);
+    b.dP2 = take((long long)B_ * H * sy_ * ((sx_ + 3) & ~3));
   }
   b.size = off;
   MGLP_CUDA(cudaMalloc(&scratch_, (size_t)Gmax_ * al_.size * sizeof(float)));
@@ -553,7 +545,8 @@ Mat Engine::grad(long long off, int ld, int layer0, int step) const {
 
 void Engine::gemm(GemmArgs g) {
   ++launches_;
-  const double flops = 2.0 * g.G * (double)g.M * g.N * g.K;
+  const double flops = 2.0 * g.G * g.Bb * g.H * (double)g.M * g.N * g.K;
+  prof_shape_ = {g.M, g.N, g.K, g.G * g.Bb * g.H};
   timed(PROF_GEMM, flops, 0.0, [&] {
 #ifdef MGLP_GEMM_SIMT
     // the reference kernel takes the unsplit fp32 weights
@@ -564,6 +557,113 @@ void Engine::gemm(GemmArgs g) {
     launch_gemm_tc(g, active_, stream_);
 #endif
   });
+}
+
+void Engine::attention_fwd(int G, Mat Q, Mat K, Mat V, Mat O, Mat P, int sq, int skv,
+                           bool causal) {
+  const int H = sd_.heads, dh = sd_.d / H;
+  auto heads = [&](Mat m, int s) {
+    m.bstride = (long long)s * m.ld;
+    m.hstride = dh;
+    return m;
+  };
+  Q = heads(Q, sq);
+  K = heads(K, skv);
+  V = heads(V, skv);
+  O = heads(O, sq);
+  const int ldp = (skv + 3) & ~3;  // 16-byte rows for TMA
+  P.ld = ldp;
+  P.hstride = (long long)sq * ldp;
+  P.bstride = (long long)H * sq * ldp;
+  GemmArgs g;
+  g.G = G;
+  g.Bb = B_;
+  g.H = H;
+  g.M = sq;
+  g.N = skv;
+  g.K = dh;
+  g.A = Q;
+  g.B = K;
+  g.ep.kind = EPI_STORE;
+  g.ep.out1 = P;
+  gemm(g);
+  SoftmaxArgs sm;
+  sm.G = G;
+  sm.rows = (long long)B_ * H * sq;
+  sm.ncols = skv;
+  sm.sq = sq;
+  sm.causal = causal;
+  sm.scale = (float)(1.0 / std::sqrt((double)dh));
+  sm.S = P;
+  ++launches_;
+  timed(PROF_ROW, 0.0, 8.0 * G * (double)sm.rows * skv, [&] { launch_softmax(sm, active_, stream_); });
+  g = GemmArgs{};
+  g.G = G;
+  g.Bb = B_;
+  g.H = H;
+  g.M = sq;
+  g.N = dh;
+  g.K = skv;
+  g.A = P;
+  g.B = V;
+  g.b_mn = true;
+  g.ep.kind = EPI_STORE;
+  g.ep.out1 = O;
+  gemm(g);
+}
+
+void Engine::attention_bwd(int G, Mat Q, Mat K, Mat V, Mat P, Mat dO, Mat dP, Mat dQ, Mat dK,
+                           Mat dV, int sq, int skv) {
+  const int H = sd_.heads, dh = sd_.d / H;
+  const float scale = (float)(1.0 / std::sqrt((double)dh));
+  auto heads = [&](Mat m, int s) {
+    m.bstride = (long long)s * m.ld;
+    m.hstride = dh;
+    return m;
+  };
+  Q = heads(Q, sq);
+  K = heads(K, skv);
+  V = heads(V, skv);
+  dO = heads(dO, sq);
+  dQ = heads(dQ, sq);
+  dK = heads(dK, skv);
+  dV = heads(dV, skv);
+  const int ldp = (skv + 3) & ~3;
+  for (Mat* m : {&P, &dP}) {
+    m->ld = ldp;
+    m->hstride = (long long)sq * ldp;
+    m->bstride = (long long)H * sq * ldp;
+  }
+  auto mk = [&](int M, int N, int K_, Mat A, bool amn, Mat B, bool bmn, Mat out, float alpha) {
+    GemmArgs g;
+    g.G = G;
+    g.Bb = B_;
+    g.H = H;
+    g.M = M;
+    g.N = N;
+    g.K = K_;
+    g.A = A;
+    g.a_mn = amn;
+    g.B = B;
+    g.b_mn = bmn;
+    g.ep.kind = EPI_STORE;
+    g.ep.out1 = out;
+    g.ep.alpha = alpha;
+    gemm(g);
+  };
+  mk(sq, skv, dh, dO, false, V, false, dP, 1.f);   // dP = dO . V^T
+  SoftmaxArgs sm;
+  sm.G = G;
+  sm.rows = (long long)B_ * H * sq;
+  sm.ncols = skv;
+  sm.sq = sq;
+  sm.S = P;
+  sm.dS = dP;
+  ++launches_;
+  timed(PROF_ROW, 0.0, 12.0 * G * (double)sm.rows * skv, [&] { launch_softmax(sm, active_, stream_); });
+  mk(skv, dh, sq, P, true, dO, true, dV, 1.f);     // dV = P^T . dO
+  mk(sq, dh, skv, dP, false, K, true, dQ, scale);  // dQ = dS . K / sqrt(dh)
+  mk(skv, dh, sq, dP, true, Q, true, dK, scale);   // dK = dS^T . Q / sqrt(dh)
 }
 
 cudaEvent_t Engine::prof_event() {
@@ -579,6 +679,26 @@ void Engine::set_profiling(bool on) {
   profiling_ = on;
   prof_.clear();
   ev_used_ = 0;
+}
+
+int Engine::dump_profile(double* out, int max_rows) {
+  MGLP_CUDA(cudaStreamSynchronize(stream_));
+  int n = 0;
+  for (const ProfRec& r : prof_) {
+    if (n >= max_rows) break;
+    float t = 0.f;
+    MGLP_CUDA(cudaEventElapsedTime(&t, r.a, r.b));
+    double* o = out + 7 * n;
+    o[0] = r.cls;
+    o[1] = r.shape[0];
+    o[2] = r.shape[1];
+    o[3] = r.shape[2];
+    o[4] = r.shape[3];
+    o[5] = r.flops;
+    o[6] = t;
+    ++n;
+  }
+  return n;
 }
 
 void Engine::read_profile(double* ms, double* flops, double* bytes, long long* launches) {
@@ -665,7 +785,7 @@ void Engine::encoder_forward(const EvalSpec& e, int R, bool causal, Mat X, Mat Y
   const int l0 = e.layer0, ls = e.layer_step;
   X.ld = d;
   Mat n1 = act_mat(e.act, al_.n1, d), qkv = act_mat(e.act, al_.qkv, 3 * d);
-  Mat ctx = act_mat(e.act, al_.ctx, d), lse = act_mat(e.act, al_.lse, 0);
+  Mat ctx = act_mat(e.act, al_.ctx, d), Pm = act_mat(e.act, al_.P, 0);
   Mat a1 = act_mat(e.act, al_.a1, d), u = act_mat(e.act, al_.u, d);
   Mat n2 = act_mat(e.act, al_.n2, d), hh = act_mat(e.act, al_.h, f), gg = act_mat(e.act, al_.g, f);
   Mat st1 = act_mat(e.act, al_.st1, 2), st2 = act_mat(e.act, al_.st2, 2);
@@ -697,21 +817,7 @@ void Engine::encoder_forward(const EvalSpec& e, int R, bool causal, Mat X, Mat Y
   g.ep.bias = par(L.b_qkv, 0, l0, ls);
   gemm(g);
 
-  AttnArgs at;
-  at.G = G;
-  at.B = B_;
-  at.H = sd_.heads;
-  at.dh = d / sd_.heads;
-  at.sq = at.skv = R / B_;
-  at.causal = causal;
-  at.scale = (float)(1.0 / std::sqrt((double)at.dh));
-  at.q = qkv;
-  at.k = qkv.offset(d);
-  at.v = qkv.offset(2 * d);
-  at.o = ctx;
-  at.lse = lse;
-  ++launches_;
-  timed(PROF_ATTN, attn_flops(at, false), 0.0, [&] { launch_attn_fwd(at, active_, stream_); });
+  attention_fwd(G, qkv, qkv.offset(d), qkv.offset(2 * d), ctx, Pm, R / B_, R / B_, causal);
 
   g = GemmArgs{};
   g.G = G;
@@ -797,13 +903,13 @@ void Engine::decoder_forward(const EvalSpec& e) {
   Mat Y = e.in.offset(y_off_), X = e.in.offset(x_off_);
   Y.ld = X.ld = d;
   Mat n1 = act_mat(e.act, al_.n1, d), qkv = act_mat(e.act, al_.qkv, 3 * d);
-  Mat ctx = act_mat(e.act, al_.ctx, d), lse = act_mat(e.act, al_.lse, 0);
+  Mat ctx = act_mat(e.act, al_.ctx, d), Pm = act_mat(e.act, al_.P, 0);
   Mat a1 = act_mat(e.act, al_.a1, d), u2 = act_mat(e.act, al_.u, d);
   Mat n2 = act_mat(e.act, al_.n2, d), hh = act_mat(e.act, al_.h, f), gg = act_mat(e.act, al_.g, f);
   Mat st1 = act_mat(e.act, al_.st1, 2), st2 = act_mat(e.act, al_.st2, 2);
   Mat n3 = act_mat(e.act, al_.n3, d), u3 = act_mat(e.act, al_.u3, d);
   Mat cq = act_mat(e.act, al_.cq, d), ckv = act_mat(e.act, al_.ckv, 2 * d);
-  Mat cctx = act_mat(e.act, al_.cctx, d), clse = act_mat(e.act, al_.clse, 0);
+  Mat cctx = act_mat(e.act, al_.cctx, d), cP = act_mat(e.act, al_.cP, 0);
   Mat ybar = act_mat(e.act, al_.ybar, d), st3 = act_mat(e.act, al_.st3, 2);
 
   LnFwdArgs ln;
@@ -837,21 +943,7 @@ void Engine::decoder_forward(const EvalSpec& e) {
   g.ep.bias = par(L.b_qkv, 0, l0, ls);
   gemm(g);
 
-  AttnArgs at;
-  at.G = G;
-  at.B = B_;
-  at.H = sd_.heads;
-  at.dh = d / sd_.heads;
-  at.sq = at.skv = sy_;
-  at.causal = 1;
-  at.scale = (float)(1.0 / std::sqrt((double)at.dh));
-  at.q = qkv;
-  at.k = qkv.offset(d);
-  at.v = qkv.offset(2 * d);
-  at.o = ctx;
-  at.lse = lse;
-  ++launches_;
-  timed(PROF_ATTN, attn_flops(at, false), 0.0, [&] { launch_attn_fwd(at, active_, stream_); });
+  attention_fwd(G, qkv, qkv.offset(d), qkv.offset(2 * d), ctx, Pm, sy_, sy_, true);
 
   g = mk(R, d, d, ctx, L.w_o, d);
   g.ep.kind = EPI_BIAS_ADD2;
@@ -882,16 +974,7 @@ void Engine::decoder_forward(const EvalSpec& e) {
   g.ep.bias = par(L.b_ckv, 0, l0, ls);
   gemm(g);
 
-  at.causal = 0;
-  at.sq = sy_;
-  at.skv = sx_;
-  at.q = cq;
-  at.k = ckv;
-  at.v = ckv.offset(d);
-  at.o = cctx;
-  at.lse = clse;
-  ++launches_;
-  timed(PROF_ATTN, attn_flops(at, false), 0.0, [&] { launch_attn_fwd(at, active_, stream_); });
+  attention_fwd(G, cq, ckv, ckv.offset(d), cctx, cP, sy_, sx_, false);
 
   g = mk(R, d, d, cctx, L.w_co, d);
   g.ep.kind = EPI_BIAS_ADD2;
@@ -993,13 +1076,13 @@ void Engine::encoder_adjoint(const EvalSpec& e, bool causal) {
   Mat UP = e.lam.offset(x_off_), X = e.in.offset(x_off_);
   UP.ld = X.ld = d;
   Mat qkv = act_mat(e.act, al_.qkv, 3 * d), ctx = act_mat(e.act, al_.ctx, d);
-  Mat lse = act_mat(e.act, al_.lse, 0), u = act_mat(e.act, al_.u, d);
+  Mat Pm = act_mat(e.act, al_.P, 0), u = act_mat(e.act, al_.u, d);
   Mat hh = act_mat(e.act, al_.h, f), gg = act_mat(e.act, al_.g, f);
   Mat n1 = act_mat(e.act, al_.n1, d), n2 = act_mat(e.act, al_.n2, d);
   Mat st1 = act_mat(e.act, al_.st1, 2), st2 = act_mat(e.act, al_.st2, 2);
   Mat dh = bwd_mat(bl_.dh, f), dn2 = bwd_mat(bl_.dn2, d), du = bwd_mat(bl_.du, d);
   Mat da1 = bwd_mat(bl_.da1, d), dctx = bwd_mat(bl_.dctx, d), dqkv = bwd_mat(bl_.dqkv, 3 * d);
-  Mat dn1 = bwd_mat(bl_.dn1, d), dd = bwd_mat(bl_.dd, 0);
+  Mat dn1 = bwd_mat(bl_.dn1, d), dPm = bwd_mat(bl_.dP, 0);
 
   auto mk = [&](int M, int N, int K, Mat A, long long w, int ldw) {
     GemmArgs g;
@@ -1044,26 +1127,8 @@ void Engine::encoder_adjoint(const EvalSpec& e, bool causal) {
   g.ep.out1 = dctx;
   gemm(g);
 
-  AttnArgs at;
-  at.G = G;
-  at.B = B_;
-  at.H = sd_.heads;
-  at.dh = d / sd_.heads;
-  at.sq = at.skv = R / B_;
-  at.causal = causal;
-  at.scale = (float)(1.0 / std::sqrt((double)at.dh));
-  at.q = qkv;
-  at.k = qkv.offset(d);
-  at.v = qkv.offset(2 * d);
-  at.o = ctx;
-  at.lse = lse;
-  at.dout = dctx;
-  at.dq = dqkv;
-  at.dk = dqkv.offset(d);
-  at.dv = dqkv.offset(2 * d);
-  at.dd = dd;
-  launches_ += 3;
-  timed(PROF_ATTN, attn_flops(at, true), 0.0, [&] { launch_attn_bwd(at, active_, stream_); });
+  attention_bwd(G, qkv, qkv.offset(d), qkv.offset(2 * d), Pm, dctx, dPm, dqkv, dqkv.offset(d),
+                dqkv.offset(2 * d), R / B_, R / B_);
 
   g = mk(R, d, 3 * d, dqkv, L.w_qkv, d);
   g.ep.kind = EPI_STORE;
@@ -1158,19 +1223,19 @@ void Engine::decoder_adjoint(const EvalSpec& e) {
   Mat UPy = e.lam.offset(y_off_), Y = e.in.offset(y_off_), X = e.in.offset(x_off_);
   UPy.ld = Y.ld = X.ld = d;
   Mat qkv = act_mat(e.act, al_.qkv, 3 * d), ctx = act_mat(e.act, al_.ctx, d);
-  Mat lse = act_mat(e.act, al_.lse, 0), u2 = act_mat(e.act, al_.u, d);
+  Mat Pm = act_mat(e.act, al_.P, 0), u2 = act_mat(e.act, al_.u, d);
   Mat hh = act_mat(e.act, al_.h, f), gg = act_mat(e.act, al_.g, f);
   Mat n1 = act_mat(e.act, al_.n1, d), n2 = act_mat(e.act, al_.n2, d);
   Mat st1 = act_mat(e.act, al_.st1, 2), st2 = act_mat(e.act, al_.st2, 2);
   Mat n3 = act_mat(e.act, al_.n3, d), u3 = act_mat(e.act, al_.u3, d);
   Mat cq = act_mat(e.act, al_.cq, d), ckv = act_mat(e.act, al_.ckv, 2 * d);
-  Mat cctx = act_mat(e.act, al_.cctx, d), clse = act_mat(e.act, al_.clse, 0);
+  Mat cctx = act_mat(e.act, al_.cctx, d), cP = act_mat(e.act, al_.cP, 0);
   Mat st3 = act_mat(e.act, al_.st3, 2);
   Mat dh = bwd_mat(bl_.dh, f), dn2 = bwd_mat(bl_.dn2, d), dy = bwd_mat(bl_.dy, d);
   Mat dybar = bwd_mat(bl_.dybar, d), dcctx = bwd_mat(bl_.dcctx, d), dcq = bwd_mat(bl_.dcq, d);
   Mat dckv = bwd_mat(bl_.dckv, 2 * d), dn3 = bwd_mat(bl_.dn3, d), dxe = bwd_mat(bl_.dxe, d);
   Mat da1 = bwd_mat(bl_.da1, d), dctx = bwd_mat(bl_.dctx, d), dqkv = bwd_mat(bl_.dqkv, 3 * d);
-  Mat dn1 = bwd_mat(bl_.dn1, d), dd = bwd_mat(bl_.dd, 0), dd2 = bwd_mat(bl_.dd2, 0);
+  Mat dn1 = bwd_mat(bl_.dn1, d), dPm = bwd_mat(bl_.dP, 0), dP2 = bwd_mat(bl_.dP2, 0);
 
   auto mk = [&](int M, int N, int K, Mat A, long long w, int ldw) {
     GemmArgs g;
@@ -1215,27 +1280,7 @@ void Engine::decoder_adjoint(const EvalSpec& e) {
   g.ep.out1 = dcctx;
   gemm(g);
 
-  AttnArgs at;
-  at.G = G;
-  at.B = B_;
-  at.H = sd_.heads;
-  at.dh = d / sd_.heads;
-  at.scale = (float)(1.0 / std::sqrt((double)at.dh));
-  at.causal = 0;
-  at.sq = sy_;
-  at.skv = sx_;
-  at.q = cq;
-  at.k = ckv;
-  at.v = ckv.offset(d);
-  at.o = cctx;
-  at.lse = clse;
-  at.dout = dcctx;
-  at.dq = dcq;
-  at.dk = dckv;
-  at.dv = dckv.offset(d);
-  at.dd = dd2;
-  launches_ += 3;
-  timed(PROF_ATTN, attn_flops(at, true), 0.0, [&] { launch_attn_bwd(at, active_, stream_); });
+  attention_bwd(G, cq, ckv, ckv.offset(d), cP, dcctx, dP2, dcq, dckv, dckv.offset(d), sy_, sx_);
 
   g = mk(R, d, d, dcq, L.w_cq, d);
   g.ep.kind = EPI_STORE;
@@ -1264,20 +1309,8 @@ void Engine::decoder_adjoint(const EvalSpec& e) {
   g.ep.out1 = dctx;
   gemm(g);
 
-  at.causal = 1;
-  at.sq = at.skv = sy_;
-  at.q = qkv;
-  at.k = qkv.offset(d);
-  at.v = qkv.offset(2 * d);
-  at.o = ctx;
-  at.lse = lse;
-  at.dout = dctx;
-  at.dq = dqkv;
-  at.dk = dqkv.offset(d);
-  at.dv = dqkv.offset(2 * d);
-  at.dd = dd;
-  launches_ += 3;
-  timed(PROF_ATTN, attn_flops(at, true), 0.0, [&] { launch_attn_bwd(at, active_, stream_); });
+  attention_bwd(G, qkv, qkv.offset(d), qkv.offset(2 * d), Pm, dctx, dPm, dqkv, dqkv.offset(d),
+                dqkv.offset(2 * d), sy_, sy_);
 
   g = mk(R, d, 3 * d, dqkv, L.w_qkv, d);
   g.ep.kind = EPI_STORE;

@@ -105,6 +105,8 @@ class Engine {
   enum ProfClass { PROF_GEMM = 0, PROF_ATTN = 1, PROF_ROW = 2, PROF_NCLASS = 3 };
   void set_profiling(bool on);
   void read_profile(double* ms, double* flops, double* bytes, long long* launches);
+  // one row per profiled launch: class, M, N, K, batch, flops, ms
+  int dump_profile(double* out, int max_rows);
   // test hooks: one Phi / Phi^T application on the device
   void step_device(int layer, double dt, const float* z, float* out);
   void adjoint_step_device(int layer, double dt, const float* z, const float* lam, float* out,
@@ -128,13 +130,13 @@ class Engine {
 
   // ----- activation arena layout (per slot) -----
   struct ActLayout {
-    long long n1, qkv, ctx, lse, a1, u, n2, h, g, st1, st2;            // encoder / self
-    long long n3, u3, cq, ckv, cctx, clse, ybar, st3;                  // decoder cross
+    long long n1, qkv, ctx, P, a1, u, n2, h, g, st1, st2;              // encoder / self
+    long long n3, u3, cq, ckv, cctx, cP, ybar, st3;                    // decoder cross
     long long size = 0;
   };
   struct BwdLayout {
-    long long dh, dn2, du, da1, dctx, dqkv, dn1, dd;                   // encoder / self
-    long long dybar, dy, dcctx, dcq, dckv, dn3, dxe, dd2;              // decoder
+    long long dh, dn2, du, da1, dctx, dqkv, dn1, dP;                   // encoder / self
+    long long dybar, dy, dcctx, dcq, dckv, dn3, dxe, dP2;              // decoder
     long long size = 0;
   };
 
@@ -164,6 +166,13 @@ class Engine {
   void encoder_adjoint(const EvalSpec& e, bool causal);
   void decoder_adjoint(const EvalSpec& e);
   void gemm(GemmArgs g);
+  // attention of a family as tcgen05 GEMMs per (batch, head):
+  // S = Q.K^T, P = softmax(S/sqrt(dh)), O = P.V (blocks.cpp:142-170) and the
+  // VJP (blocks.cpp:172-236). Q/K/V/O are token-major [tokens][ld] column
+  // slices (head h at columns h*dh); P is [B][H][sq][skv] per member.
+  void attention_fwd(int G, Mat Q, Mat K, Mat V, Mat O, Mat P, int sq, int skv, bool causal);
+  void attention_bwd(int G, Mat Q, Mat K, Mat V, Mat P, Mat dO, Mat dP, Mat dQ, Mat dK, Mat dV,
+                     int sq, int skv);
   int gemm_blocks(const GemmArgs& g) const;
   int take_partials(int n);
   Mat act_mat(const ActRef& r, long long off, int ld) const;
@@ -250,7 +259,9 @@ class Engine {
     cudaEvent_t a, b;
     int cls;
     double flops, bytes;
+    std::vector<int> shape;
   };
+  std::vector<int> prof_shape_{0, 0, 0, 0};
   bool profiling_ = false;
   std::vector<ProfRec> prof_;
   std::vector<cudaEvent_t> ev_pool_;
@@ -262,7 +273,8 @@ class Engine {
       launch();
       return;
     }
-    ProfRec r{prof_event(), prof_event(), cls, flops, bytes};
+    ProfRec r{prof_event(), prof_event(), cls, flops, bytes, prof_shape_};
+    prof_shape_ = {0, 0, 0, 0};
     cudaEventRecord(r.a, stream_);
     launch();
     cudaEventRecord(r.b, stream_);

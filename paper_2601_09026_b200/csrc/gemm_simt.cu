@@ -16,11 +16,12 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(GemmArgs a, const int* a
   __shared__ float Bs[BK][BN + 4];
   __shared__ double red[32];
   if (active && *(volatile const int*)active == 0) return;
-  const int g = blockIdx.z;
+  const int z = blockIdx.z;
+  const int hh = z % a.H, bb = (z / a.H) % a.Bb, g = z / (a.H * a.Bb);
   const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-  const float* A = a.A.at(g);
-  const float* B = a.B.at(g);
+  const float* A = a.A.at(g, bb, hh);
+  const float* B = a.B.at(g, bb, hh);
   float acc[4][4] = {};
   for (int k0 = 0; k0 < a.K; k0 += BK) {
     // 64x16 tiles, 4 elements per thread
@@ -61,7 +62,7 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(GemmArgs a, const int* a
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     const int row = m0 + ty * 4 + i;
-    if (row < a.M && nvalid > 0) r2 += epilogue_row(a.ep, g, row, col0, acc[i], nvalid);
+    if (row < a.M && nvalid > 0) r2 += epilogue_row(a.ep, g, bb, hh, row, col0, acc[i], nvalid);
   }
   if (a.ep.kind == EPI_FINAL && a.ep.cmb.mode == CM_RES0) {
     for (int o = 16; o > 0; o >>= 1) r2 += __shfl_xor_sync(0xffffffffu, r2, o);
@@ -80,12 +81,12 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(GemmArgs a, const int* a
 }  // namespace
 
 int gemm_simt_blocks(const GemmArgs& a) {
-  return ceil_div(a.N, BN) * ceil_div(a.M, BM) * a.G;
+  return ceil_div(a.N, BN) * ceil_div(a.M, BM) * a.G * a.Bb * a.H;
 }
 
 void launch_gemm_simt(const GemmArgs& a, const int* active, cudaStream_t s) {
   if (a.G == 0 || a.M == 0 || a.N == 0) return;
-  dim3 grid(ceil_div(a.N, BN), ceil_div(a.M, BM), a.G);
+  dim3 grid(ceil_div(a.N, BN), ceil_div(a.M, BM), a.G * a.Bb * a.H);
   gemm_simt_kernel<<<grid, 256, 0, s>>>(a, active);
 }
 

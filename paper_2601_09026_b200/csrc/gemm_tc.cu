@@ -22,6 +22,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <algorithm>
 #include <cstdlib>
 #include <mutex>
 
@@ -38,10 +39,16 @@ constexpr int kThreads = 256;
 struct TcOperand {
   int slot0, step;  // normalized slot coordinates (member g -> slot0 + g*step)
   int mn;           // 1 = MN-major
+  // positions of the (row, head, batch, slot) coordinates in the 5-D tensor
+  // map (dimension 0 is always the contiguous 32-wide column box); unused
+  // head / batch dimensions have extent 1 and coordinate 0
+  int pos_row, pos_h, pos_b, pos_slot;
+  int use_h, use_b;
 };
 
 struct TcParams {
   int G, M, N, K;
+  int Bb, H;
   TcOperand a, b, blo;
   int b_presplit;
   int passes;  // 3 = hi.hi + (lo.hi + hi.lo); 1 = hi.hi only (diagnostics)
@@ -79,13 +86,24 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
-__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar,
-                                            int c0, int c1, int c2) {
+__device__ __forceinline__ void tma_load_5d(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                            const int* c) {
   asm volatile(
-      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+      "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c[0]), "r"(c[1]), "r"(c[2]),
+      "r"(c[3]), "r"(c[4])
       : "memory");
+}
+
+// TMA coordinates of one box of operand `op` for problem (g, b, h)
+__device__ __forceinline__ void tma_coords(const TcOperand& op, int col, int row, int g, int b,
+                                           int h, int* c) {
+  c[0] = col;
+  c[op.pos_row] = row;
+  c[op.pos_h] = op.use_h ? h : 0;
+  c[op.pos_b] = op.use_b ? b : 0;
+  c[op.pos_slot] = op.slot0 + g * op.step;
 }
 
 // UMMA shared-memory descriptor. K-major operands use SWIZZLE_128B (layout
@@ -185,7 +203,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   double* red = reinterpret_cast<double*>(tmem_slot + 2);  // 8 doubles
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int g = blockIdx.z;
+  const int zi = blockIdx.z;
+  const int hh = zi % p.H, bb = (zi / p.H) % p.Bb, g = zi / (p.H * p.Bb);
   const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
   const int nk = (p.K + BK - 1) / BK;
   const bool convert_b = !p.b_presplit;
@@ -217,9 +236,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem_base = *tmem_slot;
 
-  const int sa = p.a.slot0 + g * p.a.step;
-  const int sb = p.b.slot0 + g * p.b.step;
-  const int sblo = p.blo.slot0 + g * p.blo.step;
 
   if (warp == 0) {
     if (lane == 0) {
@@ -231,22 +247,33 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(&empty[s], ph ^ 1);
         mbar_expect_tx(&full[s], bytes);
         const int k0 = kb * BK;
+        int c[5];
         if (!p.a.mn) {
-          tma_load_3d(stage_a(s), &mapA, &full[s], k0, m0, sa);
+          tma_coords(p.a, k0, m0, g, bb, hh, c);
+          tma_load_5d(stage_a(s), &mapA, &full[s], c);
         } else {
 #pragma unroll
-          for (int i = 0; i < BM / 32; ++i)
-            tma_load_3d(stage_a(s) + i * 4096, &mapA, &full[s], m0 + 32 * i, k0, sa);
+          for (int i = 0; i < BM / 32; ++i) {
+            tma_coords(p.a, m0 + 32 * i, k0, g, bb, hh, c);
+            tma_load_5d(stage_a(s) + i * 4096, &mapA, &full[s], c);
+          }
         }
         if (!p.b.mn) {
-          tma_load_3d(stage_b(s), &mapB, &full[s], k0, n0, sb);
-          if (!convert_b) tma_load_3d(stage_blo(s), &mapBlo, &full[s], k0, n0, sblo);
+          tma_coords(p.b, k0, n0, g, bb, hh, c);
+          tma_load_5d(stage_b(s), &mapB, &full[s], c);
+          if (!convert_b) {
+            tma_coords(p.blo, k0, n0, g, bb, hh, c);
+            tma_load_5d(stage_blo(s), &mapBlo, &full[s], c);
+          }
         } else {
 #pragma unroll
           for (int i = 0; i < BN / 32; ++i) {
-            tma_load_3d(stage_b(s) + i * 4096, &mapB, &full[s], n0 + 32 * i, k0, sb);
-            if (!convert_b)
-              tma_load_3d(stage_blo(s) + i * 4096, &mapBlo, &full[s], n0 + 32 * i, k0, sblo);
+            tma_coords(p.b, n0 + 32 * i, k0, g, bb, hh, c);
+            tma_load_5d(stage_b(s) + i * 4096, &mapB, &full[s], c);
+            if (!convert_b) {
+              tma_coords(p.blo, n0 + 32 * i, k0, g, bb, hh, c);
+              tma_load_5d(stage_blo(s) + i * 4096, &mapBlo, &full[s], c);
+            }
           }
         }
       }
@@ -329,7 +356,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       const int col0 = n0 + c;
       const int nvalid = min(16, p.N - col0);
-      if (row < p.M && nvalid > 0) r2 += epilogue_row(p.ep, g, row, col0, v, nvalid);
+      if (row < p.M && nvalid > 0) r2 += epilogue_row(p.ep, g, bb, hh, row, col0, v, nvalid);
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -378,10 +405,13 @@ PFN_cuTensorMapEncodeTiled_v12000 encoder() {
   return g_encode;
 }
 
-// Map over the slots a family touches: member g -> slot slot0 + g*step.
-// rows x cols is the [rows][cols] matrix inside one slot (row stride ld).
-CUtensorMap make_map(const Mat& m, int G, int rows, int cols, int box_rows, TcOperand* op,
-                     bool mn_major) {
+// 5-D map over the slots (and per-(batch, head) sub-blocks) a family touches:
+// member g -> slot slot0 + g*step. rows x cols is the [rows][cols] matrix of
+// one problem (row stride ld). Dimensions are ordered by increasing stride
+// (a head slice of a [tokens][3d] qkv buffer has a smaller stride than a
+// row); dimension 0 is always the contiguous columns.
+CUtensorMap make_map(const Mat& m, int G, int Bb, int H, int rows, int cols, int box_rows,
+                     TcOperand* op, bool mn_major) {
   long long lo = m.slot0, hi = m.slot0 + (long long)(G - 1) * m.step;
   if (hi < lo) std::swap(lo, hi);
   const float* base = m.ptr + lo * m.slot_stride;
@@ -389,26 +419,58 @@ CUtensorMap make_map(const Mat& m, int G, int rows, int cols, int box_rows, TcOp
   long long sstride = m.slot_stride;
   if (nslots == 1 || sstride == 0) {
     nslots = 1;
-    sstride = (long long)rows * m.ld;
+    sstride = 0;
     op->slot0 = 0;
     op->step = 0;
   } else {
     op->slot0 = (int)(m.slot0 - lo);
     op->step = m.step;
   }
-  if ((reinterpret_cast<uintptr_t>(base) & 15) || (m.ld * 4) % 16 || (sstride * 4) % 16)
-    throw ContractViolation("gemm_tc: operand is not 16-byte aligned");
+  op->use_h = (m.hstride != 0 && H > 1) ? 1 : 0;
+  op->use_b = (m.bstride != 0 && Bb > 1) ? 1 : 0;
+  struct D {
+    long long extent, stride;
+    int which, box;
+  };
+  D dims[4] = {{rows, (long long)m.ld, 0, box_rows},
+               {op->use_h ? H : 1, op->use_h ? m.hstride : 0, 1, 1},
+               {op->use_b ? Bb : 1, op->use_b ? m.bstride : 0, 2, 1},
+               {nslots, sstride, 3, 1}};
+  // used dimensions first, by increasing stride; unused (extent 1) last
+  std::sort(dims, dims + 4, [](const D& a, const D& b) {
+    const bool ua = a.stride != 0 || a.which == 0, ub = b.stride != 0 || b.which == 0;
+    if (ua != ub) return ua;
+    return a.stride < b.stride;
+  });
+  long long maxs = 16;
+  for (const D& d : dims) maxs = std::max(maxs, d.stride);
+  cuuint64_t gdim[5] = {(cuuint64_t)cols, 1, 1, 1, 1};
+  cuuint64_t gstr[4];
+  cuuint32_t box[5] = {32, 1, 1, 1, 1};
+  cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+  for (int i = 0; i < 4; ++i) {
+    gdim[i + 1] = (cuuint64_t)dims[i].extent;
+    gstr[i] = (cuuint64_t)((dims[i].stride != 0 || dims[i].which == 0) ? dims[i].stride : maxs) * 4;
+    box[i + 1] = (cuuint32_t)dims[i].box;
+    const int pos = i + 1;
+    switch (dims[i].which) {
+      case 0: op->pos_row = pos; break;
+      case 1: op->pos_h = pos; break;
+      case 2: op->pos_b = pos; break;
+      default: op->pos_slot = pos; break;
+    }
+  }
+  if ((reinterpret_cast<uintptr_t>(base) & 15))
+    throw ContractViolation("gemm_tc: operand base is not 16-byte aligned");
+  for (int i = 0; i < 4; ++i)
+    if (gstr[i] % 16 || gstr[i] == 0)
+      throw ContractViolation("gemm_tc: operand strides must be multiples of 16 bytes");
   CUtensorMap map;
-  cuuint64_t dims[3] = {(cuuint64_t)cols, (cuuint64_t)rows, (cuuint64_t)nslots};
-  cuuint64_t strides[2] = {(cuuint64_t)m.ld * 4, (cuuint64_t)sstride * 4};
-  cuuint32_t box[3] = {32, (cuuint32_t)box_rows, 1};
-  cuuint32_t estr[3] = {1, 1, 1};
-  CUresult r = encoder()(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), dims,
-                         strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+  CUresult r = encoder()(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5, const_cast<float*>(base), gdim,
+                         gstr, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                          mn_major ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B
                                   : CU_TENSOR_MAP_SWIZZLE_128B,
-                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS)
     throw ContractViolation("cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
   return map;
@@ -432,20 +494,22 @@ void launch_cfg(const GemmArgs& a, const int* active, cudaStream_t s) {
   p.b.mn = a.b_mn;
   p.blo.mn = a.b_mn;
   // A: [M][K] (K-major) or [K][M] (MN-major); box rows: BM, or 32 K-rows
-  CUtensorMap mA = a.a_mn ? make_map(a.A, a.G, a.K, a.M, BK, &p.a, true)
-                          : make_map(a.A, a.G, a.M, a.K, BM, &p.a, false);
-  CUtensorMap mB = a.b_mn ? make_map(a.B, a.G, a.K, a.N, BK, &p.b, true)
-                          : make_map(a.B, a.G, a.N, a.K, BN, &p.b, false);
+  p.Bb = a.Bb;
+  p.H = a.H;
+  CUtensorMap mA = a.a_mn ? make_map(a.A, a.G, a.Bb, a.H, a.K, a.M, BK, &p.a, true)
+                          : make_map(a.A, a.G, a.Bb, a.H, a.M, a.K, BM, &p.a, false);
+  CUtensorMap mB = a.b_mn ? make_map(a.B, a.G, a.Bb, a.H, a.K, a.N, BK, &p.b, true)
+                          : make_map(a.B, a.G, a.Bb, a.H, a.N, a.K, BN, &p.b, false);
   CUtensorMap mBlo = mB;
   if (p.b_presplit)
-    mBlo = a.b_mn ? make_map(a.Blo, a.G, a.K, a.N, BK, &p.blo, true)
-                  : make_map(a.Blo, a.G, a.N, a.K, BN, &p.blo, false);
+    mBlo = a.b_mn ? make_map(a.Blo, a.G, a.Bb, a.H, a.K, a.N, BK, &p.blo, true)
+                  : make_map(a.Blo, a.G, a.Bb, a.H, a.N, a.K, BN, &p.blo, false);
   else
     p.blo = p.b;
   const int smem = Smem<BN, STAGES>::BYTES;
   MGLP_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<BN, STAGES>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  dim3 grid(ceil_div(a.N, BN), ceil_div(a.M, BM), a.G);
+  dim3 grid(ceil_div(a.N, BN), ceil_div(a.M, BM), a.G * a.Bb * a.H);
   gemm_tc_kernel<BN, STAGES><<<grid, kThreads, smem, s>>>(mA, mB, mBlo, p, active);
   MGLP_CUDA(cudaGetLastError());
 }
@@ -456,7 +520,7 @@ constexpr int kStages = 3;
 }  // namespace
 
 int gemm_tc_blocks(const GemmArgs& a) {
-  return ceil_div(a.N, kBN) * ceil_div(a.M, BM) * a.G;
+  return ceil_div(a.N, kBN) * ceil_div(a.M, BM) * a.G * a.Bb * a.H;
 }
 
 void launch_gemm_tc(const GemmArgs& a, const int* active, cudaStream_t s) {

@@ -39,6 +39,18 @@ struct ColRedArgs {
 };
 void launch_colred(const ColRedArgs& a, const int* active, cudaStream_t s);
 
+// Row softmax of attention scores S [rows][ncols] in place (scale, causal
+// mask by query index row % sq); with dS set, the VJP dS = P (dP - sum dP P)
+// in place over dS, where S then holds P.
+struct SoftmaxArgs {
+  int G = 1;
+  long long rows = 0;
+  int ncols = 0, sq = 1, causal = 0;
+  float scale = 1.f;
+  Mat S, dS;
+};
+void launch_softmax(const SoftmaxArgs& a, const int* active, cudaStream_t s);
+
 // ---- state algebra (blocks.cpp:25-79; mgrit.hpp:199-223) --------------------
 // Passive-stream / elementwise combine: F = Fsrc ? Fsrc : 0 over n elements
 // (the stream a layer does not advance gets exactly dt*0, blocks.cpp:487,491).
@@ -84,17 +96,5 @@ int gemm_tc_blocks(const GemmArgs& a);
 // Splits weights into tf32 hi / lo parts (x = hi + lo exactly; hi has the
 // low 13 mantissa bits cleared).
 void launch_split_tf32(float* hi, float* lo, const float* src, long long n, cudaStream_t s);
-
-// ---- attention (blocks.cpp:142-236) -----------------------------------------
-struct AttnArgs {
-  int G = 1, B = 1, H = 1, dh = 0, sq = 0, skv = 0;
-  int causal = 0;
-  float scale = 1.f;
-  Mat q, k, v, o;  // element (b,i,h,c) at at(g)[(b*s + i)*ld + h*dh + c]
-  Mat lse;         // [B][H][sq]
-  Mat dout, dq, dk, dv, dd;  // backward: dd scratch [B][H][sq]
-};
-void launch_attn_fwd(const AttnArgs& a, const int* active, cudaStream_t s);
-void launch_attn_bwd(const AttnArgs& a, const int* active, cudaStream_t s);
 
 }  // namespace mglp

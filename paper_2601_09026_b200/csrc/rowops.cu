@@ -169,6 +169,81 @@ struct LnBwdL {
   }
 };
 
+// ---- attention softmax and its VJP (tensor.cpp:310-342, blocks.cpp:160-166) ------
+// P = softmax_rows(S * scale [+ causal -inf above the diagonal]) in place.
+// Masked probabilities are exactly 0, as with the reference's -1e30.
+template <int V>
+__global__ void __launch_bounds__(256) softmax_kernel(SoftmaxArgs a, const int* active) {
+  if (stopped(active)) return;
+  const int g = blockIdx.y;
+  const long long row = (long long)blockIdx.x * kRowsPerBlock + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= a.rows) return;
+  float* S = a.S.at(g) + row * a.S.ld;
+  const int qi = (int)(row % a.sq);
+  float v[V];
+  float m = -INFINITY;
+#pragma unroll
+  for (int i = 0; i < V; ++i) {
+    const int j = lane + 32 * i;
+    const bool ok = j < a.ncols && !(a.causal && j > qi);
+    v[i] = ok ? S[j] * a.scale : -INFINITY;
+    m = fmaxf(m, v[i]);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  float sum = 0.f;
+#pragma unroll
+  for (int i = 0; i < V; ++i) {
+    v[i] = v[i] == -INFINITY ? 0.f : expf(v[i] - m);
+    sum += v[i];
+  }
+  sum = warp_sum(sum);
+  const float inv = 1.f / sum;
+#pragma unroll
+  for (int i = 0; i < V; ++i) {
+    const int j = lane + 32 * i;
+    if (j < a.ncols) S[j] = v[i] * inv;
+  }
+}
+
+// dS = P * (dP - sum_j dP_j P_j), in place over dP (vjp_softmax_rows)
+template <int V>
+__global__ void __launch_bounds__(256) softmax_bwd_kernel(SoftmaxArgs a, const int* active) {
+  if (stopped(active)) return;
+  const int g = blockIdx.y;
+  const long long row = (long long)blockIdx.x * kRowsPerBlock + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= a.rows) return;
+  const float* P = a.S.at(g) + row * a.S.ld;
+  float* dP = a.dS.at(g) + row * a.dS.ld;
+  float pv[V], dv[V];
+  float t = 0.f;
+#pragma unroll
+  for (int i = 0; i < V; ++i) {
+    const int j = lane + 32 * i;
+    pv[i] = j < a.ncols ? P[j] : 0.f;
+    dv[i] = j < a.ncols ? dP[j] : 0.f;
+    t += dv[i] * pv[i];
+  }
+  t = warp_sum(t);
+#pragma unroll
+  for (int i = 0; i < V; ++i) {
+    const int j = lane + 32 * i;
+    if (j < a.ncols) dP[j] = pv[i] * (dv[i] - t);
+  }
+}
+
+template <int V>
+struct SmL {
+  static void launch(dim3 g, const SoftmaxArgs& a, const int* act, cudaStream_t s) {
+    if (a.dS.ok())
+      softmax_bwd_kernel<V><<<g, 256, 0, s>>>(a, act);
+    else
+      softmax_kernel<V><<<g, 256, 0, s>>>(a, act);
+  }
+};
+
 // ---- column sums for parameter gradients -----------------------------------------
 __global__ void __launch_bounds__(256) colred_kernel(ColRedArgs a, const int* active) {
   __shared__ double sb[8][33];
@@ -318,6 +393,12 @@ int ln_bwd_blocks(int rows) { return ceil_div(rows, kRowsPerBlock); }
 void launch_ln_bwd(const LnBwdArgs& a, const int* active, cudaStream_t s) {
   if (a.rows == 0 || a.G == 0) return;
   dispatch_rows<LnBwdL>(a.d, a, a.G, a.rows, active, s);
+}
+
+void launch_softmax(const SoftmaxArgs& a, const int* active, cudaStream_t s) {
+  if (a.rows == 0 || a.G == 0) return;
+  if (a.rows > (long long)INT32_MAX) throw ContractViolation("softmax: too many rows");
+  dispatch_rows<SmL>(a.ncols, a, a.G, (int)a.rows, active, s);
 }
 
 void launch_colred(const ColRedArgs& a, const int* active, cudaStream_t s) {
