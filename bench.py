@@ -251,14 +251,19 @@ def run_device(args, cfg, rank, world, dist):
 
     local = int(os.environ.get("LOCAL_RANK", rank))
     torch.cuda.set_device(local)
-    if world > 1:
-        raise SystemExit("multi-GPU bench requires the distributed engine (not built yet)")
     sc = StackConfig(kind=cfg["kind"], d=cfg["d"], heads=cfg["H"], ffn=cfg["ffn"],
                      n_enc=cfg["n_enc"], n_dec=cfg["n_dec"])
     so = SolveConfig(coarsen=cfg["cf"], levels=cfg["levels"], fwd_iters=cfg["fwd"],
                      bwd_iters=cfg["bwd"], warm_start=False)
-    h = C.c_void_p()
-    N.call("mglp_engine_create", C.byref(sc.desc()), C.byref(so.desc()), local, C.byref(h))
+    if world > 1:
+        # one process per GPU; rank r owns a contiguous block of coarse
+        # intervals (layers); boundary states move over NCCL inside the library
+        from paper_2601_09026_b200 import dist as D
+        uid = D.share_unique_id(dist, device=torch.device("cuda", local))
+        h = D.create_engine(sc, so, local, rank, world, uid)
+    else:
+        h = C.c_void_p()
+        N.call("mglp_engine_create", C.byref(sc.desc()), C.byref(so.desc()), local, C.byref(h))
     t0 = time.perf_counter()
     N.call("mglp_engine_init_params", h, C.c_ulonglong(7), None)
     log(f"params initialised in {time.perf_counter() - t0:.1f}s")
@@ -312,6 +317,18 @@ def run_device(args, cfg, rank, world, dist):
     for _ in range(args.warmup):
         step()
     N.call("mglp_engine_sync", h)
+    use_graph = not args.no_graph and world == 1
+    if use_graph:
+        # the whole step (both solves, ~10^3 kernels) as one CUDA graph launch
+        N.call("mglp_engine_graph_capture", h, C.c_void_p(z0.data_ptr()),
+               C.c_void_p(lam.data_ptr()), C.c_void_p(lam0.data_ptr()), 1)
+        for _ in range(2):
+            N.call("mglp_engine_graph_replay", h)
+        N.call("mglp_engine_sync", h)
+    eager_step = step
+    if use_graph:
+        def step():  # noqa: F811
+            N.call("mglp_engine_graph_replay", h)
     cnt = C.c_longlong()
     N.call("mglp_engine_take_launch_count", h, C.byref(cnt))
     with ClockSampler(local) as clk:
@@ -325,14 +342,29 @@ def run_device(args, cfg, rank, world, dist):
     N.call("mglp_engine_trace", h, 1, N.dptr(tr), 64, C.byref(nt), C.byref(cv))
     bwd_trace = list(tr[:nt.value])
 
-    # device serial fwd+bwd (same engine, same inputs) for the speedup
-    for _ in range(max(1, args.warmup // 2)):
-        serial_step()
-    serial_ms = timed(serial_step, max(1, args.steps // 2))
+    # device serial fwd+bwd on ONE GPU (same engine, same inputs) for the speedup
+    serial_ms = None
+    if rank == 0:
+        for _ in range(max(1, args.warmup // 2)):
+            serial_step()
+        torch.cuda.synchronize()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        ks = max(1, args.steps // 2)
+        a.record(stream)
+        for _ in range(ks):
+            serial_step()
+        b.record(stream)
+        torch.cuda.synchronize()
+        serial_ms = a.elapsed_time(b) / ks
+    if dist is not None:
+        obj = [serial_ms]
+        dist.broadcast_object_list(obj, src=0)
+        serial_ms = obj[0]
 
     # profiled step (outside the timed region) -> per-kernel-class device time
     N.call("mglp_engine_profile", h, 1)
-    step()
+    eager_step()
     ms3 = (C.c_double * 3)()
     fl3 = (C.c_double * 3)()
     by3 = (C.c_double * 3)()
@@ -421,9 +453,12 @@ def run_device(args, cfg, rank, world, dist):
         "config": {"workload": args.config, "desc": cfg["desc"],
                    "hierarchy": f"cf={cfg['cf']} levels={cfg['levels']} fwd={cfg['fwd']} "
                                 f"bwd={cfg['bwd']} cold broadcast guess",
-                   "parallelism": f"layer-parallel x{world}",
+                   "parallelism": f"layer-parallel x{world} (contiguous blocks of "
+                                  f"{(cfg['n_enc'] + cfg['n_dec']) // world} layers per GPU, NCCL "
+                                  f"send/recv of boundary states)",
                    "l2": "working set (states + activation cache, GBs) >> 126 MB L2",
-                   "gemm_precision": "tcgen05 kind::tf32 x3 split (fp32-accurate), fp32 accumulate"},
+                   "gemm_precision": "tcgen05 kind::tf32 x3 split (fp32-accurate), fp32 accumulate",
+                   "launch": "CUDA graph of the whole step" if use_graph else "eager"},
         "speedup_vs_serial": serial_ms / ms,
         "serial_ms_per_step": serial_ms,
         "fwd_trace": fwd_trace, "bwd_trace": bwd_trace,
@@ -446,6 +481,7 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default="bert", choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-graph", action="store_true", help="launch kernels eagerly")
     args = ap.parse_args()
     if args.warmup < 3:
         log("warmup raised to 3 (timing rules)")

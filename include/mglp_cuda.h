@@ -147,6 +147,12 @@ mglp_status mglp_engine_backward_device(mglp_engine* e, const float* lam_n_dev,
 mglp_status mglp_serial_forward_device(mglp_engine* e, const float* z0_dev);
 mglp_status mglp_serial_adjoint_device(mglp_engine* e, const float* lam_n_dev, float* lam0_dev,
                                        int want_grads);
+/* CUDA graph of one whole step (forward_device + backward_device on these
+ * fixed buffers, current config); replay is a single graph launch. The
+ * solve's stopping rule runs on the device, so the captured step is exact. */
+mglp_status mglp_engine_graph_capture(mglp_engine* e, const float* z0_dev, const float* lam_n_dev,
+                                      float* lam0_dev, int want_grads);
+mglp_status mglp_engine_graph_replay(mglp_engine* e);
 mglp_status mglp_engine_zero_grads(mglp_engine* e);
 /* flat (visit_params order) += device gradient bank */
 mglp_status mglp_engine_get_grads(mglp_engine* e, double* flat, long long n);
@@ -169,6 +175,31 @@ mglp_status mglp_engine_profile_read(mglp_engine* e, double* ms, double* flops, 
                                      long long* launches);
 /* per-launch rows (7 doubles each: class, M, N, K, batch, flops, ms) */
 mglp_status mglp_engine_profile_dump(mglp_engine* e, double* rows, int max_rows, int* n);
+
+/* ---- multi-GPU: layer blocks over ranks ----
+ * Rank r of P owns the contiguous block of coarse intervals
+ * [r*C/P, (r+1)*C/P) (C = N/c_f; P must divide the interval count of every
+ * level): its layers' parameters, activation cache and gradients. Boundary
+ * states move by NCCL send/recv over NVLink. One process per GPU: rank 0
+ * calls mglp_nccl_unique_id and shares the 128 bytes (e.g. via
+ * torch.distributed); every rank then calls mglp_engine_create_dist. The
+ * device-resident entry points (…_device) then run the distributed solve;
+ * lambda_0 is produced on rank 0, traces are identical on every rank. */
+mglp_status mglp_nccl_unique_id(void* id128);
+mglp_status mglp_engine_create_dist(const mglp_stack_desc* stack, const mglp_solve_config* solve,
+                                    int device, int rank, int world, const void* id128,
+                                    mglp_engine** out);
+/* rank, world and the owned interior layer range [layer_lo, layer_hi) */
+mglp_status mglp_engine_rank_info(mglp_engine* e, int* rank, int* world, int* layer_lo,
+                                  int* layer_hi);
+/* Test support: P virtual ranks as P engines on ONE device exchanging through
+ * device buffers (same partitioned control flow as NCCL). run_fwd_bwd runs
+ * forward_device + backward_device on all P engines concurrently (one host
+ * thread each); lam0_dev is written by rank 0. */
+mglp_status mglp_loopback_create(const mglp_stack_desc* stack, const mglp_solve_config* solve,
+                                 int device, int world, mglp_engine** engines);
+mglp_status mglp_loopback_run_fwd_bwd(mglp_engine** engines, int world, const float* z0_dev,
+                                      const float* lam_n_dev, float* lam0_dev, int want_grads);
 
 /* ---- controller (controller.hpp:63-155) ----
  * Pure decision rule, evaluated on the device from the device-resident

@@ -73,6 +73,8 @@ _SIGS = {
     "mglp_serial_forward_device": [_vp, _vp],
     "mglp_serial_adjoint_device": [_vp, _vp, _vp, C.c_int],
     "mglp_engine_zero_grads": [_vp],
+    "mglp_engine_graph_capture": [_vp, _vp, _vp, _vp, C.c_int],
+    "mglp_engine_graph_replay": [_vp],
     "mglp_engine_get_grads": [_vp, _dp, C.c_longlong],
     "mglp_engine_trace": [_vp, C.c_int, _dp, C.c_int, _ip, _ip],
     "mglp_engine_traj_device": [_vp, C.POINTER(_vp)],
@@ -84,6 +86,13 @@ _SIGS = {
                                C.c_longlong],
     "mglp_engine_profile_read": [_vp, _dp, _dp, _dp, _llp],
     "mglp_engine_profile_dump": [_vp, _dp, C.c_int, _ip],
+    "mglp_nccl_unique_id": [_vp],
+    "mglp_engine_create_dist": [C.POINTER(StackDesc), C.POINTER(SolveDesc), C.c_int, C.c_int,
+                                C.c_int, _vp, C.POINTER(_vp)],
+    "mglp_engine_rank_info": [_vp, _ip, _ip, _ip, _ip],
+    "mglp_loopback_create": [C.POINTER(StackDesc), C.POINTER(SolveDesc), C.c_int, C.c_int,
+                             C.POINTER(_vp)],
+    "mglp_loopback_run_fwd_bwd": [C.POINTER(_vp), C.c_int, _vp, _vp, _vp, C.c_int],
     "mglp_test_gemm": [C.c_int, C.c_int, C.c_int, C.c_int, _vp, C.c_longlong, C.c_int, C.c_int,
                        _vp, C.c_longlong, C.c_int, C.c_int, C.c_int, _vp, _vp, C.c_longlong,
                        C.c_int, C.c_int],

@@ -7,6 +7,9 @@
 
 #include "../../include/mglp_cuda.h"
 #include "engine.h"
+#include "transport.h"
+
+#include <thread>
 
 using namespace mglp;
 
@@ -117,20 +120,9 @@ __global__ void monitor_kernel(const SolveCtrl* f, const SolveCtrl* b, double* o
 
 }  // namespace
 
-extern "C" {
+namespace {
 
-const char* mglp_last_error(void) { return g_err.c_str(); }
-
-const char* mglp_version(void) {
-  return "mglp-b200 sm_100a tcgen05 kind::tf32 x3 (fp32 accumulate)";
-}
-
-mglp_status mglp_engine_create(const mglp_stack_desc* stack, const mglp_solve_config* solve,
-                               int device, mglp_engine** out) {
-  return guard([&] {
-    need(stack, "stack");
-    need(solve, "solve");
-    need(out, "out");
+StackDesc to_stack(const mglp_stack_desc* stack) {
     StackDesc sd;
     sd.kind = stack->kind;
     sd.d = stack->d;
@@ -145,6 +137,10 @@ mglp_status mglp_engine_create(const mglp_stack_desc* stack, const mglp_solve_co
     sd.dropout = stack->dropout;
     sd.init_std = stack->init_std;
     sd.depth_scaled_init = stack->depth_scaled_init;
+    return sd;
+}
+
+SolveCfg to_solve(const mglp_solve_config* solve) {
     SolveCfg c;
     c.coarsen = solve->coarsen;
     c.levels = solve->levels;
@@ -154,17 +150,124 @@ mglp_status mglp_engine_create(const mglp_stack_desc* stack, const mglp_solve_co
     c.bwd_tol = solve->bwd_tol;
     c.cold_guess = solve->cold_guess;
     c.warm_start = solve->warm_start;
-    int ndev = 0;
-    MGLP_CUDA(cudaGetDeviceCount(&ndev));
-    if (device < 0 || device >= ndev) throw ValidationError("device index out of range");
-    auto* h = new mglp_engine;
-    try {
-      h->eng = std::make_unique<Engine>(sd, c, device, nullptr);
-    } catch (...) {
-      delete h;
-      throw;
+    return c;
+}
+
+void check_device(int device) {
+  int ndev = 0;
+  MGLP_CUDA(cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev) throw ValidationError("device index out of range");
+}
+
+mglp_engine* wrap(std::unique_ptr<Engine> eng) {
+  auto* h = new mglp_engine;
+  h->eng = std::move(eng);
+  return h;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* mglp_last_error(void) { return g_err.c_str(); }
+
+const char* mglp_version(void) {
+  return "mglp-b200 sm_100a tcgen05 kind::tf32 x3 (fp32 accumulate)";
+}
+
+mglp_status mglp_engine_create(const mglp_stack_desc* stack, const mglp_solve_config* solve,
+                               int device, mglp_engine** out) {
+  return guard([&] {
+    need(stack, "stack");
+    need(solve, "solve");
+    need(out, "out");
+    check_device(device);
+    *out = wrap(std::make_unique<Engine>(to_stack(stack), to_solve(solve), device, nullptr));
+  });
+}
+
+mglp_status mglp_nccl_unique_id(void* id128) {
+  return guard([&] {
+    need(id128, "id128");
+    NcclUniqueId id;
+    nccl_unique_id(&id);
+    std::memcpy(id128, &id, sizeof id);
+  });
+}
+
+mglp_status mglp_engine_create_dist(const mglp_stack_desc* stack, const mglp_solve_config* solve,
+                                    int device, int rank, int world, const void* id128,
+                                    mglp_engine** out) {
+  return guard([&] {
+    need(stack, "stack");
+    need(solve, "solve");
+    need(out, "out");
+    if (world < 1 || rank < 0 || rank >= world) throw ValidationError("bad rank / world");
+    check_device(device);
+    std::shared_ptr<Transport> tr;
+    if (world > 1) {
+      need(id128, "id128");
+      NcclUniqueId id;
+      std::memcpy(&id, id128, sizeof id);
+      tr = make_nccl_transport(rank, world, id, device);
     }
-    *out = h;
+    *out = wrap(std::make_unique<Engine>(to_stack(stack), to_solve(solve), device, tr));
+  });
+}
+
+mglp_status mglp_engine_rank_info(mglp_engine* e, int* rank, int* world, int* lo, int* hi) {
+  return guard([&] {
+    need(e, "engine");
+    if (rank) *rank = e->eng->rank();
+    if (world) *world = e->eng->world();
+    int a = 0, b = 0;
+    e->eng->owned_layers(&a, &b);
+    if (lo) *lo = a;
+    if (hi) *hi = b;
+  });
+}
+
+mglp_status mglp_loopback_create(const mglp_stack_desc* stack, const mglp_solve_config* solve,
+                                 int device, int world, mglp_engine** engines) {
+  return guard([&] {
+    need(stack, "stack");
+    need(solve, "solve");
+    need(engines, "engines");
+    if (world < 1) throw ValidationError("world must be >= 1");
+    check_device(device);
+    auto hub = make_loopback_hub(world);
+    std::vector<std::unique_ptr<Engine>> made;
+    for (int r = 0; r < world; ++r)
+      made.push_back(std::make_unique<Engine>(to_stack(stack), to_solve(solve), device,
+                                              world > 1 ? make_loopback_transport(hub, r)
+                                                        : nullptr));
+    for (int r = 0; r < world; ++r) engines[r] = wrap(std::move(made[r]));
+  });
+}
+
+mglp_status mglp_loopback_run_fwd_bwd(mglp_engine** engines, int world, const float* z0_dev,
+                                      const float* lam_n_dev, float* lam0_dev, int want_grads) {
+  return guard([&] {
+    need(engines, "engines");
+    need(z0_dev, "z0_dev");
+    need(lam_n_dev, "lam_n_dev");
+    std::vector<std::thread> th;
+    std::vector<std::string> errs(world);
+    for (int r = 0; r < world; ++r)
+      th.emplace_back([&, r] {
+        try {
+          Engine& E = *engines[r]->eng;
+          MGLP_CUDA(cudaSetDevice(E.device()));
+          E.forward_device(z0_dev);
+          E.backward_device(lam_n_dev, r == 0 ? lam0_dev : nullptr, want_grads != 0, true);
+          MGLP_CUDA(cudaStreamSynchronize(E.stream()));
+        } catch (const std::exception& ex) {
+          errs[r] = ex.what();
+        }
+      });
+    for (auto& t : th) t.join();
+    for (int r = 0; r < world; ++r)
+      if (!errs[r].empty()) throw ContractViolation("rank " + std::to_string(r) + ": " + errs[r]);
   });
 }
 
@@ -485,6 +588,23 @@ mglp_status mglp_rng_gaussian_fill(unsigned long long seed, unsigned long long a
   return guard([&] {
     need(out, "out");
     rng_gaussian_fill(seed, a, b, scale, out, n);
+  });
+}
+
+mglp_status mglp_engine_graph_capture(mglp_engine* e, const float* z0_dev, const float* lam_n_dev,
+                                      float* lam0_dev, int want_grads) {
+  return guard([&] {
+    need(e, "engine");
+    need(z0_dev, "z0_dev");
+    need(lam_n_dev, "lam_n_dev");
+    e->eng->capture_step(z0_dev, lam_n_dev, lam0_dev, want_grads != 0);
+  });
+}
+
+mglp_status mglp_engine_graph_replay(mglp_engine* e) {
+  return guard([&] {
+    need(e, "engine");
+    e->eng->replay_step();
   });
 }
 

@@ -142,19 +142,31 @@ Engine::Engine(const StackDesc& sd, const SolveCfg& cfg, int device,
   }
   if (N_ % stride != 0)
     throw ValidationError("MgritSolver: step count must be divisible by coarsen^(levels-1)");
-  if (tr_ && tr_->size() > 1)
-    throw ValidationError("multi-rank engines are created through the distributed front end");
+  if (tr_) {
+    rank_ = tr_->rank();
+    world_ = tr_->size();
+  }
+  if (world_ > 1) {
+    // every level's intervals must split evenly over the ranks
+    long long n = N_;
+    for (int l = 0; l + 1 < std::max(cfg_.levels, 2); ++l) {
+      if ((n / cfg_.coarsen) % world_ != 0)
+        throw ValidationError("layer partition: the " + std::to_string(n / cfg_.coarsen) +
+                              " coarse intervals of level " + std::to_string(l) +
+                              " do not split over " + std::to_string(world_) + " ranks");
+      n /= cfg_.coarsen;
+      if (l + 2 >= cfg_.levels) break;
+    }
+  }
 
   MGLP_CUDA(cudaSetDevice(device_));
   MGLP_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
   build_layouts();
   const size_t pbytes = (size_t)total_ * layer_stride_ * sizeof(float);
   MGLP_CUDA(cudaMalloc(&P_, pbytes));
-  MGLP_CUDA(cudaMalloc(&Phi_, pbytes));
   MGLP_CUDA(cudaMalloc(&Plo_, pbytes));
   MGLP_CUDA(cudaMalloc(&Gr_, pbytes));
   MGLP_CUDA(cudaMemsetAsync(P_, 0, pbytes, stream_));
-  MGLP_CUDA(cudaMemsetAsync(Phi_, 0, pbytes, stream_));
   MGLP_CUDA(cudaMemsetAsync(Plo_, 0, pbytes, stream_));
   MGLP_CUDA(cudaMemsetAsync(Gr_, 0, pbytes, stream_));
   Gmax_ = std::max(1, N_ / cfg_.coarsen);
@@ -166,9 +178,10 @@ Engine::~Engine() {
   if (stream_) cudaStreamSynchronize(stream_);
   free_solver(fwd_);
   free_solver(bwd_);
-  for (float* p : {P_, Phi_, Plo_, Gr_, scratch_, cache_, bscratch_, traj_, lam_all_,
+  for (float* p : {P_, Plo_, Gr_, scratch_, cache_, bscratch_, traj_, lam_all_,
                    zero_state_, snap_fwd_, snap_bwd_})
     if (p) cudaFree(p);
+  drop_graph();
   for (cudaEvent_t ev : ev_pool_) cudaEventDestroy(ev);
   if (stream_) cudaStreamDestroy(stream_);
 }
@@ -319,7 +332,7 @@ void Engine::set_params(const double* flat) {
   MGLP_CUDA(cudaSetDevice(device_));
   const size_t n = host.size();
   MGLP_CUDA(cudaMemcpyAsync(P_, host.data(), n * sizeof(float), cudaMemcpyHostToDevice, stream_));
-  launch_split_tf32(Phi_, Plo_, P_, (long long)n, stream_);
+  launch_split_tf32(nullptr, Plo_, P_, (long long)n, stream_);  // hi = raw (MMA truncates)
   MGLP_CUDA(cudaStreamSynchronize(stream_));
 }
 
@@ -365,6 +378,7 @@ void Engine::set_shape(int batch, int s_x, int s_y) {
     throw ValidationError("shape: s_y > 0 exactly for encoder-decoder stacks");
   MGLP_CUDA(cudaSetDevice(device_));
   MGLP_CUDA(cudaStreamSynchronize(stream_));
+  drop_graph();
   free_solver(fwd_);
   free_solver(bwd_);
   for (float** p : {&scratch_, &cache_, &bscratch_, &traj_, &lam_all_, &zero_state_, &snap_fwd_,
@@ -442,6 +456,14 @@ void Engine::set_shape(int batch, int s_x, int s_y) {
   MGLP_CUDA(cudaMemsetAsync(traj_, 0, (size_t)(total_ + 1) * state_n_ * sizeof(float), stream_));
   MGLP_CUDA(cudaMemsetAsync(lam_all_, 0, (size_t)(total_ + 1) * state_n_ * sizeof(float), stream_));
   MGLP_CUDA(cudaMemsetAsync(zero_state_, 0, (size_t)state_n_ * sizeof(float), stream_));
+  {
+    GemmArgs probe;
+    probe.G = 1;
+    probe.M = std::max(Tx_, Ty_);
+    probe.N = sd_.d;
+    part_off_ln_ = gemm_blocks(probe);
+    part_off_elem_ = part_off_ln_ + ln_bwd_blocks(std::max(Tx_, Ty_));
+  }
   alloc_solver(fwd_, false);
   alloc_solver(bwd_, true);
   std::fill(cache_valid_.begin(), cache_valid_.end(), 0);
@@ -476,13 +498,22 @@ void Engine::alloc_solver(Solver& s, bool adjoint) {
   }
   MGLP_CUDA(cudaMalloc(&s.ctrl, sizeof(SolveCtrl)));
   MGLP_CUDA(cudaMemsetAsync(s.ctrl, 0, sizeof(SolveCtrl), stream_));
-  // norm partials: generous upper bound on CTAs contributing to one residual
-  const long long per_state = (long long)ceil_div(std::max(Tx_, Ty_), 8) +
-                              elem_combine_blocks(state_n_) +
-                              (long long)ceil_div(std::max(Tx_, Ty_), 64) *
-                                  ceil_div(sd_.d, 64) + 64;
-  s.n_partials = (int)(per_state * (N_ / cfg_.coarsen + 1) * 2);
-  MGLP_CUDA(cudaMalloc(&s.partials, (size_t)s.n_partials * sizeof(double)));
+  // owned points of every level: time position tpos owns (tpos*n_l/P, (tpos+1)*n_l/P]
+  s.tpos = adjoint ? world_ - 1 - rank_ : rank_;
+  s.p_lo.resize(s.lv.size());
+  s.p_hi.resize(s.lv.size());
+  for (size_t l = 0; l < s.lv.size(); ++l) {
+    const int per = s.lv[l].n / world_;
+    s.p_lo[l] = s.tpos * per;
+    s.p_hi[l] = (s.tpos + 1) * per;
+  }
+  // residual-norm partial slots per coarse interval: GEMM tiles | LN rows | elementwise
+  s.n_chunks = N_ / cfg_.coarsen;
+  s.slots_per_chunk = part_off_elem_ + elem_combine_blocks((long long)std::max(Tx_, Ty_) * sd_.d);
+  const size_t np = (size_t)s.n_chunks * s.slots_per_chunk;
+  MGLP_CUDA(cudaMalloc(&s.partials, np * sizeof(double)));
+  MGLP_CUDA(cudaMemsetAsync(s.partials, 0, np * sizeof(double), stream_));
+  if (world_ > 1) MGLP_CUDA(cudaMalloc(&s.gathered, np * sizeof(double)));
 }
 
 void Engine::free_solver(Solver& s) {
@@ -495,6 +526,7 @@ void Engine::free_solver(Solver& s) {
   }
   if (s.ctrl) cudaFree(s.ctrl);
   if (s.partials) cudaFree(s.partials);
+  if (s.gathered) cudaFree(s.gathered);
   s = Solver{};
 }
 
@@ -529,7 +561,7 @@ Mat Engine::par(long long off, int ld, int layer0, int step) const {
 }
 Mat Engine::par_hi(long long off, int ld, int layer0, int step) const {
   Mat m = par(off, ld, layer0, step);
-  m.ptr = Phi_ + off;
+  m.ptr = P_ + off;  // the raw fp32 weights: the MMA reads them truncated to tf32
   return m;
 }
 Mat Engine::par_lo(long long off, int ld, int layer0, int step) const {
@@ -549,9 +581,6 @@ void Engine::gemm(GemmArgs g) {
   prof_shape_ = {g.M, g.N, g.K, g.G * g.Bb * g.H};
   timed(PROF_GEMM, flops, 0.0, [&] {
 #ifdef MGLP_GEMM_SIMT
-    // the reference kernel takes the unsplit fp32 weights
-    if (g.Blo.ok() && g.B.ptr >= Phi_ && g.B.ptr < Phi_ + (size_t)total_ * layer_stride_)
-      g.B.ptr = P_ + (g.B.ptr - Phi_);
     launch_gemm_simt(g, active_, stream_);
 #else
     launch_gemm_tc(g, active_, stream_);
@@ -725,12 +754,6 @@ int Engine::gemm_blocks(const GemmArgs& g) const {
 #endif
 }
 
-int Engine::take_partials(int n) {
-  const int b = pcursor_;
-  pcursor_ += n;
-  if (pcursor_ > pcap_) throw ContractViolation("residual-norm partial buffer overflow");
-  return b;
-}
 
 // =============================================================================
 // Phi: one layer step z + dt*F(z) for a family of G layers (blocks.cpp:466-514)
@@ -758,6 +781,7 @@ void Engine::eval_forward(const EvalSpec& e0) {
         c.phib = shift(c.phib, g0);
         c.rho = shift(c.rho, g0);
         c.v = shift(c.v, g0);
+        c.norm_base = e0.cmb.norm_base + g0 * e0.cmb.norm_member_stride;
         return e;
       };
       eval_forward(part(0, gsplit));
@@ -878,7 +902,7 @@ void Engine::encoder_forward(const EvalSpec& e, int R, bool causal, Mat X, Mat Y
   c.rho = off(c.rho);
   c.v = off(c.v);
   for (Mat* m : {&c.z, &c.out, &c.base, &c.phib, &c.rho, &c.v}) m->ld = d;
-  if (c.mode == CM_RES0) c.norm_base = take_partials(gemm_blocks(g));
+  if (c.mode == CM_RES0) c.norm_base = e.cmb.norm_base;  // GEMM tiles first
   g.ep.cmb = c;
   gemm(g);
   if (Ypass.ok() && e.cmb.mode != CM_NONE) {
@@ -888,7 +912,7 @@ void Engine::encoder_forward(const EvalSpec& e, int R, bool causal, Mat X, Mat Y
     Combine cy = e.cmb;
     for (Mat* m : {&cy.z, &cy.out, &cy.base, &cy.phib, &cy.rho, &cy.v})
       if (m->ok()) *m = m->offset(y_off_);
-    if (cy.mode == CM_RES0) cy.norm_base = take_partials(G * elem_combine_blocks(ec.n));
+    if (cy.mode == CM_RES0) cy.norm_base = e.cmb.norm_base + part_off_elem_;
     ec.cmb = cy;
     ++launches_;
     launch_elem_combine(ec, active_, stream_);
@@ -1011,7 +1035,7 @@ void Engine::decoder_forward(const EvalSpec& e) {
       *m = m->offset(y_off_);
       m->ld = d;
     }
-  if (c.mode == CM_RES0) c.norm_base = take_partials(gemm_blocks(g));
+  if (c.mode == CM_RES0) c.norm_base = e.cmb.norm_base;  // GEMM tiles first
   g.ep.cmb = c;
   gemm(g);
   if (e.cmb.mode != CM_NONE) {
@@ -1019,7 +1043,7 @@ void Engine::decoder_forward(const EvalSpec& e) {
     ec.G = G;
     ec.n = (long long)Tx_ * d;
     Combine cx = e.cmb;  // x part sits at offset 0
-    if (cx.mode == CM_RES0) cx.norm_base = take_partials(G * elem_combine_blocks(ec.n));
+    if (cx.mode == CM_RES0) cx.norm_base = e.cmb.norm_base + part_off_elem_;
     ec.cmb = cx;
     ++launches_;
     launch_elem_combine(ec, active_, stream_);
@@ -1051,6 +1075,7 @@ void Engine::eval_adjoint(const EvalSpec& e0) {
         c.phib = shift(c.phib, g0);
         c.rho = shift(c.rho, g0);
         c.v = shift(c.v, g0);
+        c.norm_base = e0.cmb.norm_base + g0 * e0.cmb.norm_member_stride;
         return e;
       };
       eval_adjoint(part(0, gsplit));
@@ -1151,7 +1176,7 @@ void Engine::encoder_adjoint(const EvalSpec& e, bool causal) {
         *m = m->offset(x_off_);
         m->ld = d;
       }
-    if (c.mode == CM_RES0) c.norm_base = take_partials(G * ln_bwd_blocks(R));
+    if (c.mode == CM_RES0) c.norm_base = e.cmb.norm_base + part_off_ln_;
     l1.cmb = c;
     ++launches_;
     timed(PROF_ROW, 0.0, 20.0 * l1.G * (double)l1.rows * l1.d,
@@ -1163,7 +1188,7 @@ void Engine::encoder_adjoint(const EvalSpec& e, bool causal) {
       Combine cy = e.cmb;
       for (Mat* m : {&cy.z, &cy.out, &cy.base, &cy.phib, &cy.rho, &cy.v})
         if (m->ok()) *m = m->offset(y_off_);
-      if (cy.mode == CM_RES0) cy.norm_base = take_partials(G * elem_combine_blocks(ec.n));
+      if (cy.mode == CM_RES0) cy.norm_base = e.cmb.norm_base + part_off_elem_;
       ec.cmb = cy;
       ++launches_;
       launch_elem_combine(ec, active_, stream_);
@@ -1333,7 +1358,7 @@ void Engine::decoder_adjoint(const EvalSpec& e) {
         *m = m->offset(y_off_);
         m->ld = d;
       }
-    if (c.mode == CM_RES0) c.norm_base = take_partials(G * ln_bwd_blocks(R));
+    if (c.mode == CM_RES0) c.norm_base = e.cmb.norm_base + part_off_ln_;
     l1.cmb = c;
     ++launches_;
     timed(PROF_ROW, 0.0, 20.0 * l1.G * (double)l1.rows * l1.d,
@@ -1343,7 +1368,7 @@ void Engine::decoder_adjoint(const EvalSpec& e) {
     ec.n = (long long)Tx_ * d;
     ec.F = dxe;
     Combine cx = e.cmb;
-    if (cx.mode == CM_RES0) cx.norm_base = take_partials(G * elem_combine_blocks(ec.n));
+    if (cx.mode == CM_RES0) cx.norm_base = e.cmb.norm_base + part_off_elem_;
     ec.cmb = cx;
     ++launches_;
     launch_elem_combine(ec, active_, stream_);
@@ -1401,7 +1426,11 @@ void Engine::decoder_adjoint(const EvalSpec& e) {
 }
 
 // =============================================================================
-// MGRIT (mgrit.hpp:58-303) on device-resident levels
+// MGRIT (mgrit.hpp:58-303) on device-resident levels, block-partitioned over
+// ranks. Rank r owns the points (p_lo, p_hi] of every level (its contiguous
+// block of coarse intervals); the adjoint system runs the same
+// partition reversed in time. Point p_lo itself is a ghost copy of the
+// previous rank's last point.
 // =============================================================================
 
 Mat Engine::lv_v(const Solver& s, int l, int slot0, int step) const {
@@ -1416,6 +1445,23 @@ Mat Engine::lv_rho(const Solver& s, int l, int slot0, int step) const {
 }
 Mat Engine::lv_phib(const Solver& s, int l, int slot0, int step) const {
   return state_mat(s.lv[l].phib, state_n_, sd_.d, slot0, step);
+}
+
+int Engine::rank_at(const Solver& s, int tpos) const {
+  return s.adjoint ? world_ - 1 - tpos : tpos;
+}
+
+// ghost exchange of one state: the last local point goes to the next rank in
+// time, the previous rank's last point lands in our ghost slot
+void Engine::exchange_ghost(Solver& s, int level) {
+  if (world_ == 1) return;
+  const size_t n = (size_t)state_n_;
+  tr_->group_start();
+  if (s.tpos + 1 < world_)
+    tr_->send(s.lv[level].v + (size_t)s.p_hi[level] * n, n, rank_at(s, s.tpos + 1), stream_);
+  if (s.tpos > 0)
+    tr_->recv(s.lv[level].v + (size_t)s.p_lo[level] * n, n, rank_at(s, s.tpos - 1), stream_);
+  tr_->group_end();
 }
 
 // Steps k = k0 + g*kstep (g < G) of level `level` of system s, applied to the
@@ -1437,6 +1483,7 @@ void Engine::sys_eval(Solver& s, int level, int k0, int kstep, int G, Mat in, Co
     c.phib = shift(c.phib, g0);
     c.rho = shift(c.rho, g0);
     c.v = shift(c.v, g0);
+    c.norm_base = cmb.norm_base + g0 * cmb.norm_member_stride;
     e.cmb = c;
     const int kk0 = k0 + g0 * kstep;
     if (!s.adjoint) {
@@ -1476,13 +1523,16 @@ void Engine::relax_family(Solver& s, int level, int j0, int jstep, int G, bool c
 }
 
 void Engine::f_relax(Solver& s, int level, bool capture) {  // mgrit.hpp:125-137
-  const int cf = cfg_.coarsen, nc = s.lv[level].n / cf;
-  for (int i = 1; i < cf; ++i) relax_family(s, level, i, cf, nc, capture);
+  const int cf = cfg_.coarsen;
+  const int lo = s.p_lo[level], nc = (s.p_hi[level] - lo) / cf;
+  for (int i = 1; i < cf; ++i) relax_family(s, level, lo + i, cf, nc, capture);
 }
 
 void Engine::c_relax(Solver& s, int level) {  // mgrit.hpp:139-149
-  const int cf = cfg_.coarsen, nc = s.lv[level].n / cf;
-  relax_family(s, level, cf, cf, nc, false);
+  const int cf = cfg_.coarsen;
+  const int lo = s.p_lo[level], nc = (s.p_hi[level] - lo) / cf;
+  relax_family(s, level, lo + cf, cf, nc, false);
+  exchange_ghost(s, level);
 }
 
 // Residual rows at the coarse-aligned points j = k*c_f (mgrit.hpp:159-187).
@@ -1492,54 +1542,71 @@ void Engine::c_relax(Solver& s, int level) {  // mgrit.hpp:139-149
 // only the C-point rows are evaluated; they are written straight into the
 // next level's rho (injection, mgrit.hpp:204).
 void Engine::residual_c_rows(Solver& s, int level, bool capture) {
-  const int cf = cfg_.coarsen, nc = s.lv[level].n / cf;
+  const int cf = cfg_.coarsen;
+  const int lo = s.p_lo[level], nc = (s.p_hi[level] - lo) / cf;
   Combine c;
-  c.out = lv_rho(s, level + 1, 1, 1);
-  c.v = lv_v(s, level, cf, cf);
+  c.out = lv_rho(s, level + 1, lo / cf + 1, 1);
+  c.v = lv_v(s, level, lo + cf, cf);
   if (level == 0) {
+    // per-interval partial slots [chunk][S]: the trace is summed in interval
+    // order, independent of the rank count and of how families are launched
     c.mode = CM_RES0;
     c.norm_partials = s.partials;
-    c.norm_base = 0;
-  } else {
-    c.mode = CM_RESL;
-    c.base = lv_base(s, level, cf, cf);
-    c.phib = lv_phib(s, level, cf, cf);
-    c.rho = lv_rho(s, level, cf, cf);
-  }
-  if (level == 0) {
-    pcursor_ = 0;
-    pcap_ = s.n_partials;
-    sys_eval(s, level, cf - 1, cf, nc, lv_v(s, level, cf - 1, cf), c, capture);
-    launch_trace_record(s.ctrl, s.partials, pcursor_, stream_);
+    c.norm_base = (lo / cf) * s.slots_per_chunk;
+    c.norm_member_stride = s.slots_per_chunk;
+    const size_t total = (size_t)s.n_chunks * s.slots_per_chunk;
+    MGLP_CUDA(cudaMemsetAsync(s.partials, 0, total * sizeof(double), stream_));
+    sys_eval(s, level, lo + cf - 1, cf, nc, lv_v(s, level, lo + cf - 1, cf), c, capture);
+    const double* summed = s.partials;
+    if (world_ > 1) {
+      const size_t blk = (size_t)nc * s.slots_per_chunk;
+      tr_->allgather(s.partials + (size_t)(lo / cf) * s.slots_per_chunk, s.gathered, blk, stream_);
+      summed = s.gathered;
+    }
+    launch_trace_record(s.ctrl, summed, s.n_chunks, s.slots_per_chunk,
+                        world_ > 1 ? s.n_chunks / world_ : s.n_chunks, s.adjoint && world_ > 1,
+                        stream_);
     ++launches_;
   } else {
-    sys_eval(s, level, cf - 1, cf, nc, lv_v(s, level, cf - 1, cf), c, false);
+    c.mode = CM_RESL;
+    c.base = lv_base(s, level, lo + cf, cf);
+    c.phib = lv_phib(s, level, lo + cf, cf);
+    c.rho = lv_rho(s, level, lo + cf, cf);
+    sys_eval(s, level, lo + cf - 1, cf, nc, lv_v(s, level, lo + cf - 1, cf), c, false);
   }
 }
 
 void Engine::restrict_to(Solver& s, int level) {  // mgrit.hpp:199-211
-  Level& c = s.lv[level];
   const bool coarsest = level == cfg_.levels - 1;
-  // v = base (the coarsest level only needs its initial condition: exact_solve
-  // overwrites every other point)
-  launch_copy(coarsest ? 1 : c.n + 1, state_n_, lv_v(s, level, 0, 1), lv_base(s, level, 0, 1),
-              active_, stream_);
+  const int lo = s.p_lo[level], hi = s.p_hi[level];
+  // v = base on our points and the ghost (the coarsest level only needs its
+  // initial condition: exact_solve overwrites every other point)
+  launch_copy(coarsest ? 1 : hi - lo + 1, state_n_, lv_v(s, level, lo, 1),
+              lv_base(s, level, lo, 1), active_, stream_);
   ++launches_;
   Combine cm;
   cm.mode = CM_PLAIN;
-  cm.out = lv_phib(s, level, 1, 1);
-  sys_eval(s, level, 0, 1, c.n, lv_base(s, level, 0, 1), cm, false);
+  cm.out = lv_phib(s, level, lo + 1, 1);
+  sys_eval(s, level, lo, 1, hi - lo, lv_base(s, level, lo, 1), cm, false);
 }
 
 void Engine::correct_from(Solver& s, int level) {  // mgrit.hpp:214-223
-  const int n = s.lv[level].n;
-  launch_correct(n, state_n_, lv_v(s, level - 1, cfg_.coarsen, cfg_.coarsen),
-                 lv_v(s, level, 1, 1), lv_base(s, level, 1, 1), active_, stream_);
+  // our coarse points and the ghost (its coarse value arrived with the
+  // coarse chain / ghost exchange, so the correction is bitwise the owner's)
+  const int k0 = std::max(s.p_lo[level], 1), hi = s.p_hi[level];
+  launch_correct(hi - k0 + 1, state_n_, lv_v(s, level - 1, k0 * cfg_.coarsen, cfg_.coarsen),
+                 lv_v(s, level, k0, 1), lv_base(s, level, k0, 1), active_, stream_);
   ++launches_;
 }
 
 void Engine::exact_solve(Solver& s, int level) {  // mgrit.hpp:227-231
-  for (int j = 1; j <= s.lv[level].n; ++j) relax_family(s, level, j, 1, 1, false);
+  // the serial coarse chain, pipelined across ranks
+  const size_t n = (size_t)state_n_;
+  if (world_ > 1 && s.tpos > 0)
+    tr_->recv(s.lv[level].v + (size_t)s.p_lo[level] * n, n, rank_at(s, s.tpos - 1), stream_);
+  for (int j = s.p_lo[level] + 1; j <= s.p_hi[level]; ++j) relax_family(s, level, j, 1, 1, false);
+  if (world_ > 1 && s.tpos + 1 < world_)
+    tr_->send(s.lv[level].v + (size_t)s.p_hi[level] * n, n, rank_at(s, s.tpos + 1), stream_);
 }
 
 void Engine::descend(Solver& s, int level) {  // mgrit.hpp:285-296
@@ -1586,6 +1653,13 @@ void Engine::solve(Solver& s, int iters, double tol) {  // mgrit.hpp:248-262
 // LayerParallelEngine (adjoint.hpp:113-206)
 // =============================================================================
 
+bool Engine::owns_layer(int l) const {
+  if (l < ib_) return rank_ == 0;
+  if (l >= ie_) return rank_ == world_ - 1;
+  const int i = l - ib_;
+  return i >= fwd_.p_lo[0] && i < fwd_.p_hi[0];
+}
+
 void Engine::forward_device(const float* z0_dev) {
   MGLP_CUDA(cudaSetDevice(device_));
   if (!traj_) throw ValidationError("forward: set_shape first");
@@ -1604,6 +1678,8 @@ void Engine::forward_device(const float* z0_dev) {
     eval_forward(e);
     cache_valid_[l] = 1;
   };
+  // opening buffers run on every rank (each needs the initial condition for
+  // the broadcast guess); only rank 0 keeps their linearisation
   for (int l = 0; l < ib_; ++l) serial_step(l);
   const int guess = (first_fwd_ || !cfg_.warm_start) ? cfg_.cold_guess : 2;
   first_fwd_ = false;
@@ -1618,16 +1694,17 @@ void Engine::forward_device(const float* z0_dev) {
   // whose input is final: all but the last layer of each coarse interval
   // (with one level the C-point residual evaluations capture those too)
   const int cf = cfg_.coarsen;
-  for (int i = 0; i < N_; ++i)
+  for (int i = fwd_.p_lo[0]; i < fwd_.p_hi[0]; ++i)
     if (cfg_.levels == 1 || (i % cf) != cf - 1) cache_valid_[ib_ + i] = 1;
-  for (int l = ie_; l < total_; ++l) serial_step(l);
+  if (rank_ == world_ - 1)
+    for (int l = ie_; l < total_; ++l) serial_step(l);
 }
 
-// Linearization pass for layers whose activations were not captured.
+// Linearization pass for the owned layers whose activations were not captured.
 void Engine::ensure_linearization() {
   std::vector<int> miss;
   for (int l = 0; l < total_; ++l)
-    if (!cache_valid_[l]) miss.push_back(l);
+    if (!cache_valid_[l] && owns_layer(l)) miss.push_back(l);
   size_t i = 0;
   while (i < miss.size()) {
     // affine run
@@ -1671,10 +1748,12 @@ void Engine::backward_device(const float* lamN_dev, float* lam0_dev, bool want_g
     e.gscale = (float)h_[l];
     eval_adjoint(e);
   };
-  for (int l = total_ - 1; l >= ie_; --l) serial_adj(l);
-  // mu[0] = lambda at the interior end
+  // closing buffers on the last rank, then mu[0] = lambda at the interior end
+  if (rank_ == world_ - 1)
+    for (int l = total_ - 1; l >= ie_; --l) serial_adj(l);
   MGLP_CUDA(cudaMemcpyAsync(bwd_.lv[0].v, lam_all_ + (size_t)ie_ * state_n_,
                             state_n_ * sizeof(float), cudaMemcpyDeviceToDevice, stream_));
+  if (world_ > 1) tr_->bcast(bwd_.lv[0].v, (size_t)state_n_, world_ - 1, stream_);
   const int guess = (first_bwd_ || !cfg_.warm_start) ? cfg_.cold_guess : 2;
   first_bwd_ = false;
   if (guess == 0)
@@ -1682,11 +1761,12 @@ void Engine::backward_device(const float* lamN_dev, float* lam0_dev, bool want_g
   else if (guess == 1)
     launch_zero(N_, state_n_, lv_v(bwd_, 0, 1, 1), nullptr, stream_);
   solve(bwd_, cfg_.bwd_iters, cfg_.bwd_tol);
-  // parameter pass (adjoint.hpp:165-175): layer ib+i at traj[ib+i] with
-  // upstream mu[N-1-i], gscale = h
+  // parameter pass over the owned layers (adjoint.hpp:165-175): layer ib+i at
+  // traj[ib+i] with upstream mu[N-1-i], gscale = h
   if (want_grads) {
-    for (int i0 = 0; i0 < N_; i0 += Gmax_) {
-      const int Gc = std::min(Gmax_, N_ - i0);
+    const int i_lo = fwd_.p_lo[0], i_hi = fwd_.p_hi[0];
+    for (int i0 = i_lo; i0 < i_hi; i0 += Gmax_) {
+      const int Gc = std::min(Gmax_, i_hi - i0);
       EvalSpec e;
       e.G = Gc;
       e.layer0 = ib_ + i0;
@@ -1701,13 +1781,55 @@ void Engine::backward_device(const float* lamN_dev, float* lam0_dev, bool want_g
       eval_adjoint(e);
     }
   }
-  MGLP_CUDA(cudaMemcpyAsync(lam_all_ + (size_t)ib_ * state_n_,
-                            bwd_.lv[0].v + (size_t)N_ * state_n_, state_n_ * sizeof(float),
-                            cudaMemcpyDeviceToDevice, stream_));
-  for (int l = ib_ - 1; l >= 0; --l) serial_adj(l);
-  if (lam0_dev)
-    MGLP_CUDA(cudaMemcpyAsync(lam0_dev, lam_all_, state_n_ * sizeof(float),
+  // lambda at the interior start lives on rank 0 (the last adjoint block)
+  if (rank_ == 0) {
+    MGLP_CUDA(cudaMemcpyAsync(lam_all_ + (size_t)ib_ * state_n_,
+                              bwd_.lv[0].v + (size_t)N_ * state_n_, state_n_ * sizeof(float),
                               cudaMemcpyDeviceToDevice, stream_));
+    for (int l = ib_ - 1; l >= 0; --l) serial_adj(l);
+    if (lam0_dev)
+      MGLP_CUDA(cudaMemcpyAsync(lam0_dev, lam_all_, state_n_ * sizeof(float),
+                                cudaMemcpyDeviceToDevice, stream_));
+  }
+}
+
+void Engine::capture_step(const float* z0_dev, const float* lamN_dev, float* lam0_dev,
+                          bool want_grads) {
+  MGLP_CUDA(cudaSetDevice(device_));
+  drop_graph();
+  if (profiling_) throw ValidationError("capture_step: disable profiling first");
+  // run once uncaptured so lazily created state (TMA encoder, kernel
+  // attributes) exists and the cache bookkeeping reaches its steady state
+  forward_device(z0_dev);
+  backward_device(lamN_dev, lam0_dev, want_grads, true);
+  MGLP_CUDA(cudaStreamSynchronize(stream_));
+  const long long before = launches_;
+  cudaGraph_t g = nullptr;
+  MGLP_CUDA(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal));
+  try {
+    forward_device(z0_dev);
+    backward_device(lamN_dev, lam0_dev, want_grads, true);
+  } catch (...) {
+    cudaStreamEndCapture(stream_, &g);
+    if (g) cudaGraphDestroy(g);
+    throw;
+  }
+  MGLP_CUDA(cudaStreamEndCapture(stream_, &g));
+  graph_launches_ = launches_ - before;
+  MGLP_CUDA(cudaGraphInstantiate(&graph_exec_, g, 0));
+  MGLP_CUDA(cudaGraphDestroy(g));
+}
+
+void Engine::replay_step() {
+  if (!graph_exec_) throw ValidationError("replay_step: no captured step");
+  MGLP_CUDA(cudaGraphLaunch(graph_exec_, stream_));
+  launches_ += graph_launches_;
+}
+
+void Engine::drop_graph() {
+  if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
+  graph_exec_ = nullptr;
+  graph_launches_ = 0;
 }
 
 void Engine::read_trace(bool fwd, std::vector<double>* trace, bool* converged) {

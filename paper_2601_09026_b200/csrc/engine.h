@@ -44,6 +44,8 @@ class Transport {
   virtual void recv(float* buf, size_t n, int peer, cudaStream_t s) = 0;
   // gathers `n` doubles from every rank into out[rank*n .. ]
   virtual void allgather(const double* in, double* out, size_t n, cudaStream_t s) = 0;
+  // root's buf -> every rank's buf (n floats)
+  virtual void bcast(float* buf, size_t n, int root, cudaStream_t s) = 0;
   virtual void group_start() {}
   virtual void group_end() {}
 };
@@ -54,7 +56,16 @@ void rng_gaussian_fill(uint64_t seed, uint64_t a, uint64_t b, double scale, doub
 
 class Engine {
  public:
+  // tr == nullptr (or a 1-rank transport): single GPU. Otherwise this engine
+  // owns rank tr->rank()'s block of coarse intervals.
   Engine(const StackDesc& sd, const SolveCfg& cfg, int device, std::shared_ptr<Transport> tr);
+  int rank() const { return rank_; }
+  int world() const { return world_; }
+  // owned interior layer range [lo, hi) (interior indices)
+  void owned_layers(int* lo, int* hi) const {
+    *lo = fwd_.p_lo.empty() ? 0 : fwd_.p_lo[0];
+    *hi = fwd_.p_hi.empty() ? N_ : fwd_.p_hi[0];
+  }
   ~Engine();
 
   // ---- LayerStack surface ----
@@ -85,6 +96,15 @@ class Engine {
   void restore();
   void reset() { first_fwd_ = first_bwd_ = true; }
   void invalidate_linearization() { std::fill(cache_valid_.begin(), cache_valid_.end(), 0); }
+
+  // CUDA graph of one full training-step solve (forward_device +
+  // backward_device on fixed device buffers). Every host decision of the
+  // step is shape/config-static and the solve's stopping rule lives on the
+  // device (SolveCtrl), so the whole step is capturable; replay = one launch.
+  void capture_step(const float* z0_dev, const float* lamN_dev, float* lam0_dev, bool want_grads);
+  void replay_step();
+  void drop_graph();
+  bool has_graph() const { return graph_exec_ != nullptr; }
 
   // serial reference sweeps on device (blocks.cpp:659-682)
   void serial_forward_device(const float* z0_dev);
@@ -174,7 +194,6 @@ class Engine {
   void attention_bwd(int G, Mat Q, Mat K, Mat V, Mat P, Mat dO, Mat dP, Mat dQ, Mat dK, Mat dV,
                      int sq, int skv);
   int gemm_blocks(const GemmArgs& g) const;
-  int take_partials(int n);
   Mat act_mat(const ActRef& r, long long off, int ld) const;
   Mat bwd_mat(long long off, int ld) const;
   Mat par(long long off, int ld, int layer0, int step) const;
@@ -192,11 +211,17 @@ class Engine {
   };
   struct Solver {
     bool adjoint = false;
+    int tpos = 0;                 // this rank's position in the solver's time order
     std::vector<Level> lv;
+    std::vector<int> p_lo, p_hi;  // per level: owned points (p_lo, p_hi]; p_lo is a ghost
     SolveCtrl* ctrl = nullptr;
-    double* partials = nullptr;
-    int n_partials = 0;
+    double* partials = nullptr;   // [n_chunks][slots_per_chunk] residual-norm partials
+    double* gathered = nullptr;   // all ranks' partials (world > 1)
+    int n_chunks = 0, slots_per_chunk = 0;
   };
+  int rank_at(const Solver& s, int tpos) const;
+  void exchange_ghost(Solver& s, int level);
+  bool owns_layer(int l) const;
   Mat lv_v(const Solver& s, int l, int slot0, int step) const;
   Mat lv_base(const Solver& s, int l, int slot0, int step) const;
   Mat lv_rho(const Solver& s, int l, int slot0, int step) const;
@@ -230,8 +255,7 @@ class Engine {
   long long layer_stride_ = 0;
   long long n_params_flat_ = 0;
   float* P_ = nullptr;     // fp32 params
-  float* Phi_ = nullptr;   // tf32 hi parts
-  float* Plo_ = nullptr;   // tf32 lo parts
+  float* Plo_ = nullptr;   // tf32 lo parts (x - trunc_tf32(x)); hi = the raw P_
   float* Gr_ = nullptr;    // fp32 grads
   // shape
   int B_ = 0, sx_ = 0, sy_ = 0, Tx_ = 0, Ty_ = 0;
@@ -253,8 +277,11 @@ class Engine {
   float* snap_bwd_ = nullptr;
   bool snap_first_fwd_ = true, snap_first_bwd_ = true;
   long long launches_ = 0;
+  cudaGraphExec_t graph_exec_ = nullptr;
+  long long graph_launches_ = 0;  // hot-path kernels inside the captured step
   const int* active_ = nullptr;  // current solve-control flag
-  int pcursor_ = 0, pcap_ = 0;   // residual-norm partial slots handed out
+  int part_off_ln_ = 0, part_off_elem_ = 0;  // partial-slot offsets within an interval
+  int rank_ = 0, world_ = 1;
   struct ProfRec {
     cudaEvent_t a, b;
     int cls;

@@ -72,8 +72,8 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(GemmArgs a, const int* a
     if (threadIdx.x == 0) {
       double t = 0.0;
       for (int i = 0; i < 8; ++i) t += red[i];
-      const int blk = (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
-      a.ep.cmb.norm_partials[a.ep.cmb.norm_base + blk] = t;
+      a.ep.cmb.norm_partials[a.ep.cmb.norm_base + blockIdx.z * a.ep.cmb.norm_member_stride +
+                             blockIdx.y * gridDim.x + blockIdx.x] = t;
     }
   }
 }

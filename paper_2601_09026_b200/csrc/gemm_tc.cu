@@ -34,7 +34,7 @@ namespace {
 
 constexpr int BM = 128;
 constexpr int BK = 32;  // fp32 elements per stage = one 128-byte swizzle span
-constexpr int kThreads = 256;
+constexpr int kThreads = 384;  // producer, MMA, TMEM, idle, 4 converters, 4 epilogue
 
 struct TcOperand {
   int slot0, step;  // normalized slot coordinates (member g -> slot0 + g*step)
@@ -52,6 +52,8 @@ struct TcParams {
   TcOperand a, b, blo;
   int b_presplit;
   int passes;  // 3 = hi.hi + (lo.hi + hi.lo); 1 = hi.hi only (diagnostics)
+  int rawhi;   // feed raw x as the hi operand (the MMA truncates); 0 = write masked hi
+  int vec_ok;  // every epilogue operand row start is 16-byte aligned
   EpiArgs ep;
 };
 
@@ -156,8 +158,12 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
 
 // x -> (hi, lo): hi keeps the top 10 explicit mantissa bits (exactly a tf32),
 // lo = x - hi exactly; the tensor core then sees hi exactly and lo to ~11 bits.
+// kind::tf32 MMAs read an fp32 operand by truncating its low 13 mantissa
+// bits (measured: raw x and its masked copy give bitwise-identical products,
+// tests/test_gemm.py::test_tf32_operand_truncation), so by default only lo is
+// written and the raw tile serves as hi -- one smem store pass fewer per stage.
 __device__ __forceinline__ void split_tile(float* raw, float* lo, int nfloat, int tid,
-                                           int nthreads) {
+                                           int nthreads, int rawhi) {
   float4* r4 = reinterpret_cast<float4*>(raw);
   float4* l4 = reinterpret_cast<float4*>(lo);
   for (int i = tid; i < nfloat / 4; i += nthreads) {
@@ -171,7 +177,7 @@ __device__ __forceinline__ void split_tile(float* raw, float* lo, int nfloat, in
     l.y = x.y - h.y;
     l.z = x.z - h.z;
     l.w = x.w - h.w;
-    r4[i] = h;
+    if (!rawhi) r4[i] = h;  // rawhi: leave x in place, the MMA reads it as tf32
     l4[i] = l;
   }
 }
@@ -181,9 +187,13 @@ struct Smem {
   static constexpr int A_BYTES = BM * BK * 4;
   static constexpr int B_BYTES = BN * BK * 4;
   static constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;  // A, A_lo, B_hi, B_lo
-  static constexpr int BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 512 /*barriers*/;
 };
 
+// Persistent: each CTA walks tiles blockIdx.x, +gridDim.x, ... of the whole
+// family (problem-major, then M, then N so an A row-block is reused while hot
+// in L2). Two TMEM accumulator buffers (each = main + correction, 2*BN
+// columns) let the epilogue of tile t overlap the MMAs of tile t+1.
 template <int BN, int STAGES>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap mapA,
@@ -198,22 +208,39 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * S::STAGE_BYTES);
   uint64_t* conv = full + STAGES;
   uint64_t* empty = conv + STAGES;
-  uint64_t* tmem_full = empty + STAGES;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
-  double* red = reinterpret_cast<double*>(tmem_slot + 2);  // 8 doubles
+  uint64_t* tfull = empty + STAGES;   // [2]
+  uint64_t* tempty = tfull + 2;       // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  double* red = reinterpret_cast<double*>(tmem_slot + 2);  // [2][4]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int zi = blockIdx.z;
-  const int hh = zi % p.H, bb = (zi / p.H) % p.Bb, g = zi / (p.H * p.Bb);
-  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
   const int nk = (p.K + BK - 1) / BK;
   const bool convert_b = !p.b_presplit;
+  const int tiles_n = (p.N + BN - 1) / BN, tiles_m = (p.M + BM - 1) / BM;
+  const int per_prob = tiles_n * tiles_m;
+  const int total = per_prob * p.G * p.Bb * p.H;
 
   auto stage_a = [&](int s) { return smem + s * S::STAGE_BYTES; };
   auto stage_alo = [&](int s) { return smem + s * S::STAGE_BYTES + S::A_BYTES; };
   auto stage_b = [&](int s) { return smem + s * S::STAGE_BYTES + 2 * S::A_BYTES; };
   auto stage_blo = [&](int s) {
     return smem + s * S::STAGE_BYTES + 2 * S::A_BYTES + S::B_BYTES;
+  };
+  struct Tile {
+    int z, g, b, h, m0, n0, mt, nt;
+  };
+  auto tile_of = [&](int t) {
+    Tile T;
+    T.z = t / per_prob;
+    const int r = t % per_prob;
+    T.mt = r / tiles_n;
+    T.nt = r % tiles_n;
+    T.h = T.z % p.H;
+    T.b = (T.z / p.H) % p.Bb;
+    T.g = T.z / (p.H * p.Bb);
+    T.m0 = T.mt * BM;
+    T.n0 = T.nt * BN;
+    return T;
   };
 
   if (threadIdx.x == 0) {
@@ -222,13 +249,16 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&conv[s], 4);  // one elected lane per converter warp
       mbar_init(&empty[s], 1);
     }
-    mbar_init(tmem_full, 1);
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 4);  // one elected lane per epilogue warp
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 2) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_u32(tmem_slot)),
-                 "r"((uint32_t)(2 * BN)));
+                 "r"((uint32_t)(4 * BN)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -236,43 +266,46 @@ __global__ void __launch_bounds__(kThreads, 1)
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem_base = *tmem_slot;
 
-
   if (warp == 0) {
+    // ===== TMA producer =====
     if (lane == 0) {
-      const uint32_t bytes =
-          S::A_BYTES + S::B_BYTES + (convert_b ? 0 : S::B_BYTES);
-      for (int kb = 0; kb < nk; ++kb) {
-        const int s = kb % STAGES;
-        const uint32_t ph = (kb / STAGES) & 1;
-        mbar_wait(&empty[s], ph ^ 1);
-        mbar_expect_tx(&full[s], bytes);
-        const int k0 = kb * BK;
-        int c[5];
-        if (!p.a.mn) {
-          tma_coords(p.a, k0, m0, g, bb, hh, c);
-          tma_load_5d(stage_a(s), &mapA, &full[s], c);
-        } else {
+      const uint32_t bytes = S::A_BYTES + S::B_BYTES + (convert_b ? 0 : S::B_BYTES);
+      int kg = 0;
+      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+        const Tile T = tile_of(t);
+        for (int kb = 0; kb < nk; ++kb, ++kg) {
+          const int s = kg % STAGES;
+          const uint32_t ph = (kg / STAGES) & 1;
+          mbar_wait(&empty[s], ph ^ 1);
+          mbar_expect_tx(&full[s], bytes);
+          const int k0 = kb * BK;
+          int c[5];
+          if (!p.a.mn) {
+            tma_coords(p.a, k0, T.m0, T.g, T.b, T.h, c);
+            tma_load_5d(stage_a(s), &mapA, &full[s], c);
+          } else {
 #pragma unroll
-          for (int i = 0; i < BM / 32; ++i) {
-            tma_coords(p.a, m0 + 32 * i, k0, g, bb, hh, c);
-            tma_load_5d(stage_a(s) + i * 4096, &mapA, &full[s], c);
+            for (int i = 0; i < BM / 32; ++i) {
+              tma_coords(p.a, T.m0 + 32 * i, k0, T.g, T.b, T.h, c);
+              tma_load_5d(stage_a(s) + i * 4096, &mapA, &full[s], c);
+            }
           }
-        }
-        if (!p.b.mn) {
-          tma_coords(p.b, k0, n0, g, bb, hh, c);
-          tma_load_5d(stage_b(s), &mapB, &full[s], c);
-          if (!convert_b) {
-            tma_coords(p.blo, k0, n0, g, bb, hh, c);
-            tma_load_5d(stage_blo(s), &mapBlo, &full[s], c);
-          }
-        } else {
-#pragma unroll
-          for (int i = 0; i < BN / 32; ++i) {
-            tma_coords(p.b, n0 + 32 * i, k0, g, bb, hh, c);
-            tma_load_5d(stage_b(s) + i * 4096, &mapB, &full[s], c);
+          if (!p.b.mn) {
+            tma_coords(p.b, k0, T.n0, T.g, T.b, T.h, c);
+            tma_load_5d(stage_b(s), &mapB, &full[s], c);
             if (!convert_b) {
-              tma_coords(p.blo, n0 + 32 * i, k0, g, bb, hh, c);
-              tma_load_5d(stage_blo(s) + i * 4096, &mapBlo, &full[s], c);
+              tma_coords(p.blo, k0, T.n0, T.g, T.b, T.h, c);
+              tma_load_5d(stage_blo(s), &mapBlo, &full[s], c);
+            }
+          } else {
+#pragma unroll
+            for (int i = 0; i < BN / 32; ++i) {
+              tma_coords(p.b, T.n0 + 32 * i, k0, T.g, T.b, T.h, c);
+              tma_load_5d(stage_b(s) + i * 4096, &mapB, &full[s], c);
+              if (!convert_b) {
+                tma_coords(p.blo, T.n0 + 32 * i, k0, T.g, T.b, T.h, c);
+                tma_load_5d(stage_blo(s) + i * 4096, &mapBlo, &full[s], c);
+              }
             }
           }
         }
@@ -280,6 +313,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     __syncwarp();
   } else if (warp == 1) {
+    // ===== MMA issuer (one thread) =====
     if (lane == 0) {
       // instruction descriptor: D f32, A/B tf32, majors, N, M
       const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)p.a.mn << 15) |
@@ -292,89 +326,418 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t a_lay = p.a.mn ? 1u : 2u, b_lay = p.b.mn ? 1u : 2u;
       const uint32_t a_kstep = p.a.mn ? 1024u : 32u;  // bytes per K=8 step
       const uint32_t b_kstep = p.b.mn ? 1024u : 32u;
-      for (int kb = 0; kb < nk; ++kb) {
-        const int s = kb % STAGES;
-        const uint32_t ph = (kb / STAGES) & 1;
-        mbar_wait(&conv[s], ph);
+      int kg = 0, tc = 0;
+      for (int t = blockIdx.x; t < total; t += gridDim.x, ++tc) {
+        const int acc = tc & 1;
+        const uint32_t aph = (tc >> 1) & 1;
+        mbar_wait(&tempty[acc], aph ^ 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t tm = tmem_base + (uint32_t)(acc * 2 * BN);
+        for (int kb = 0; kb < nk; ++kb, ++kg) {
+          const int s = kg % STAGES;
+          const uint32_t ph = (kg / STAGES) & 1;
+          mbar_wait(&conv[s], ph);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #pragma unroll
-        for (int k = 0; k < BK / 8; ++k) {
-          const uint64_t dah = smem_desc(stage_a(s) + k * a_kstep, a_lbo, a_sbo, a_lay);
-          const uint64_t dal = smem_desc(stage_alo(s) + k * a_kstep, a_lbo, a_sbo, a_lay);
-          const uint64_t dbh = smem_desc(stage_b(s) + k * b_kstep, b_lbo, b_sbo, b_lay);
-          const uint64_t dbl = smem_desc(stage_blo(s) + k * b_kstep, b_lbo, b_sbo, b_lay);
-          const uint32_t acc0 = (kb > 0 || k > 0) ? 1u : 0u;
-          // main product and the two correction products accumulate in
-          // separate TMEM accumulators, so the small terms are not rounded
-          // against the large running sum
-          mma_tf32(tmem_base, dah, dbh, idesc, acc0);
-          if (p.passes > 1) {
-            mma_tf32(tmem_base + BN, dal, dbh, idesc, acc0);
-            mma_tf32(tmem_base + BN, dah, dbl, idesc, 1u);
+          for (int k = 0; k < BK / 8; ++k) {
+            const uint64_t dah = smem_desc(stage_a(s) + k * a_kstep, a_lbo, a_sbo, a_lay);
+            const uint64_t dal = smem_desc(stage_alo(s) + k * a_kstep, a_lbo, a_sbo, a_lay);
+            const uint64_t dbh = smem_desc(stage_b(s) + k * b_kstep, b_lbo, b_sbo, b_lay);
+            const uint64_t dbl = smem_desc(stage_blo(s) + k * b_kstep, b_lbo, b_sbo, b_lay);
+            const uint32_t acc0 = (kb > 0 || k > 0) ? 1u : 0u;
+            // main product and the two correction products accumulate in
+            // separate TMEM accumulators, so the small terms are not rounded
+            // against the large running sum
+            mma_tf32(tm, dah, dbh, idesc, acc0);
+            if (p.passes > 1) {
+              mma_tf32(tm + BN, dal, dbh, idesc, acc0);
+              mma_tf32(tm + BN, dah, dbl, idesc, 1u);
+            }
           }
+          mma_commit(&empty[s]);
         }
-        mma_commit(&empty[s]);
+        mma_commit(&tfull[acc]);
       }
-      mma_commit(tmem_full);
     }
     __syncwarp();
-  } else if (warp >= 4) {
+  } else if (warp >= 4 && warp < 8) {
+    // ===== hi/lo split converters =====
     const int ct = threadIdx.x - 128;  // 0..127
-    for (int kb = 0; kb < nk; ++kb) {
-      const int s = kb % STAGES;
-      const uint32_t ph = (kb / STAGES) & 1;
-      mbar_wait(&full[s], ph);
-      split_tile(reinterpret_cast<float*>(stage_a(s)), reinterpret_cast<float*>(stage_alo(s)),
-                 BM * BK, ct, 128);
-      if (convert_b)
-        split_tile(reinterpret_cast<float*>(stage_b(s)), reinterpret_cast<float*>(stage_blo(s)),
-                   BN * BK, ct, 128);
-      // generic-proxy smem writes -> visible to the tensor core (async proxy)
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&conv[s]);
-    }
-  }
-
-  // ---- epilogue: TMEM -> registers -> fused epilogue -> global ----
-  double r2 = 0.0;
-  if (warp >= 4) {
-    mbar_wait(tmem_full, 0);
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    const int q = warp & 3;
-    const int row = m0 + q * 32 + lane;
-    const uint32_t lane_addr = tmem_base + ((uint32_t)(q * 32) << 16);
-#pragma unroll 1
-    for (int c = 0; c < BN; c += 16) {
-      float v[16];
-      tmem_ld16(lane_addr + c, v);
-      if (p.passes > 1) {
-        float w[16];
-        tmem_ld16(lane_addr + BN + c, w);
-#pragma unroll
-        for (int i = 0; i < 16; ++i) v[i] += w[i];
+    int kg = 0;
+    for (int t = blockIdx.x; t < total; t += gridDim.x) {
+      for (int kb = 0; kb < nk; ++kb, ++kg) {
+        const int s = kg % STAGES;
+        const uint32_t ph = (kg / STAGES) & 1;
+        mbar_wait(&full[s], ph);
+        split_tile(reinterpret_cast<float*>(stage_a(s)), reinterpret_cast<float*>(stage_alo(s)),
+                   BM * BK, ct, 128, p.rawhi);
+        if (convert_b)
+          split_tile(reinterpret_cast<float*>(stage_b(s)),
+                     reinterpret_cast<float*>(stage_blo(s)), BN * BK, ct, 128, p.rawhi);
+        // generic-proxy smem writes -> visible to the tensor core (async proxy)
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&conv[s]);
       }
-      const int col0 = n0 + c;
-      const int nvalid = min(16, p.N - col0);
-      if (row < p.M && nvalid > 0) r2 += epilogue_row(p.ep, g, bb, hh, row, col0, v, nvalid);
+    }
+  } else if (warp >= 8) {
+    // ===== epilogue: TMEM -> registers -> fused epilogue -> global =====
+    const int q = warp & 3;
+    const bool res0 = p.ep.kind == EPI_FINAL && p.ep.cmb.mode == CM_RES0;
+    int tc = 0;
+    for (int t = blockIdx.x; t < total; t += gridDim.x, ++tc) {
+      const Tile T = tile_of(t);
+      const int acc = tc & 1;
+      const uint32_t aph = (tc >> 1) & 1;
+      mbar_wait(&tfull[acc], aph);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const int row = T.m0 + q * 32 + lane;
+      const uint32_t lane_addr =
+          tmem_base + (uint32_t)(acc * 2 * BN) + ((uint32_t)(q * 32) << 16);
+      double r2 = 0.0;
+#pragma unroll 1
+      for (int c = 0; c < BN; c += 16) {
+        float v[16];
+        tmem_ld16(lane_addr + c, v);
+        if (p.passes > 1) {
+          float w[16];
+          tmem_ld16(lane_addr + BN + c, w);
+#pragma unroll
+          for (int i = 0; i < 16; ++i) v[i] += w[i];
+        }
+        const int col0 = T.n0 + c;
+        const int nvalid = min(16, p.N - col0);
+        if (row < p.M && nvalid > 0)
+          r2 += (nvalid == 16 && p.vec_ok)
+                    ? epilogue_row16(p.ep, T.g, T.b, T.h, row, col0, v)
+                    : epilogue_row(p.ep, T.g, T.b, T.h, row, col0, v, nvalid);
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (res0) {
+        for (int o = 16; o > 0; o >>= 1) r2 += __shfl_xor_sync(0xffffffffu, r2, o);
+        if (lane == 0) red[acc * 4 + q] = r2;
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (q == 0 && lane == 0) {
+          const double tsum = red[acc * 4 + 0] + red[acc * 4 + 1] + red[acc * 4 + 2] +
+                              red[acc * 4 + 3];
+          p.ep.cmb.norm_partials[p.ep.cmb.norm_base + T.z * p.ep.cmb.norm_member_stride +
+                                 T.mt * tiles_n + T.nt] = tsum;
+        }
+      }
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   if (warp == 2)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
-                 "r"((uint32_t)(2 * BN)));
-  if (p.ep.kind == EPI_FINAL && p.ep.cmb.mode == CM_RES0) {
-    for (int o = 16; o > 0; o >>= 1) r2 += __shfl_xor_sync(0xffffffffu, r2, o);
-    if (lane == 0) red[warp] = r2;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      double t = 0.0;
-      for (int i = 0; i < kThreads / 32; ++i) t += red[i];
-      const int blk = (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
-      p.ep.cmb.norm_partials[p.ep.cmb.norm_base + blk] = t;
+                 "r"((uint32_t)(4 * BN)));
+}
+
+// ---- cta_group::2: a CTA pair computes one 256 x 256 tile --------------------
+// Each CTA of the pair holds half of A (128 rows) and half of B (128 of the
+// 256 columns) in its own smem; the leader CTA issues M=256 N=256 MMAs that
+// read both halves, and each CTA's TMEM receives its 128 rows x 256 columns.
+// Per SM this halves the B operand traffic through shared memory relative
+// to a 1-CTA 128x256 tile -- the 3-pass split makes these kernels shared-
+// memory-bandwidth bound, so this is the lever. TMEM (512 columns) holds one
+// main + one correction accumulator; 8 epilogue warps drain it quickly while
+// the producer and converters already stage the next tile.
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+
+__device__ __forceinline__ uint32_t map_to_rank(uint32_t saddr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+  return r;
+}
+
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
+               : "memory");
+}
+
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;"
+               ::: "memory");
+}
+
+__device__ __forceinline__ void mma_tf32_pair(uint32_t tmem_d, uint64_t da, uint64_t db,
+                                              uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t"
+      ".reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t"
+      "}" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void mma_commit_pair(uint64_t* bar) {
+  // arrive on the barrier at this offset in BOTH CTAs of the pair
+  const uint16_t mask = 0x3;
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(smem_u32(bar)),
+      "h"(mask)
+      : "memory");
+}
+
+constexpr int P_BM = 256;   // pair tile rows (128 per CTA)
+constexpr int P_BN = 256;   // pair tile columns (128 per CTA in smem)
+constexpr int P_STAGES = 3;
+constexpr int kThreads2 = 512;  // 0 TMA, 1 MMA, 2 TMEM, 3 idle, 4-7 convert, 8-15 epilogue
+
+struct Smem2 {
+  static constexpr int A_BYTES = 128 * BK * 4;
+  static constexpr int B_BYTES = (P_BN / 2) * BK * 4;
+  static constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;
+  static constexpr int BYTES = P_STAGES * STAGE_BYTES + 1024 + 512;
+};
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
+    gemm_tc2_kernel(const __grid_constant__ CUtensorMap mapA,
+                    const __grid_constant__ CUtensorMap mapB,
+                    const __grid_constant__ CUtensorMap mapBlo, const TcParams p,
+                    const int* active) {
+  using S = Smem2;
+  constexpr int STAGES = P_STAGES;
+  constexpr int HB = P_BN / 2;  // B rows held per CTA
+  extern __shared__ uint8_t smem_raw[];
+  // the early exit is uniform over the cluster (same flag), so no CTA is left
+  // waiting on its peer
+  if (active && *(volatile const int*)active == 0) return;
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * S::STAGE_BYTES);
+  uint64_t* conv = full + STAGES;
+  uint64_t* empty = conv + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
+  double* red = reinterpret_cast<double*>(tmem_slot + 2);  // [8]
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t cr = cluster_rank();
+  const bool leader = cr == 0;
+  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+  const int nk = (p.K + BK - 1) / BK;
+  const bool convert_b = !p.b_presplit;
+  const int tiles_n = (p.N + P_BN - 1) / P_BN, tiles_m2 = (p.M + P_BM - 1) / P_BM;
+  const int tiles_m128 = (p.M + 127) / 128;
+  const int per_prob = tiles_n * tiles_m2;
+  const int total = per_prob * p.G * p.Bb * p.H;
+
+  auto stage_a = [&](int s) { return smem + s * S::STAGE_BYTES; };
+  auto stage_alo = [&](int s) { return smem + s * S::STAGE_BYTES + S::A_BYTES; };
+  auto stage_b = [&](int s) { return smem + s * S::STAGE_BYTES + 2 * S::A_BYTES; };
+  auto stage_blo = [&](int s) {
+    return smem + s * S::STAGE_BYTES + 2 * S::A_BYTES + S::B_BYTES;
+  };
+  struct Tile {
+    int z, g, b, h, m0, n0, mt, nt;
+  };
+  auto tile_of = [&](int t) {
+    Tile T;
+    T.z = t / per_prob;
+    const int r = t % per_prob;
+    const int mt2 = r / tiles_n;
+    T.nt = r % tiles_n;
+    T.h = T.z % p.H;
+    T.b = (T.z / p.H) % p.Bb;
+    T.g = T.z / (p.H * p.Bb);
+    T.mt = mt2 * 2 + (int)cr;  // this CTA's 128-row tile
+    T.m0 = T.mt * 128;
+    T.n0 = T.nt * P_BN;
+    return T;
+  };
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&conv[s], 8);  // 4 converter warps x 2 CTAs (leader's is used)
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(tfull, 1);
+    mbar_init(tempty, 16);  // 8 epilogue warps x 2 CTAs (leader's is used)
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(512u));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  cluster_sync();  // peer barriers initialised before any remote arrive
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem_base = *tmem_slot;
+  const uint32_t conv_leader0 = map_to_rank(smem_u32(&conv[0]), 0);
+  const uint32_t tempty_leader = map_to_rank(smem_u32(tempty), 0);
+
+  if (warp == 0) {
+    // ===== TMA producer (each CTA loads its own halves) =====
+    if (lane == 0) {
+      const uint32_t bytes = S::A_BYTES + S::B_BYTES + (convert_b ? 0 : S::B_BYTES);
+      int kg = 0;
+      for (int t = pair; t < total; t += npairs) {
+        const Tile T = tile_of(t);
+        const int nb0 = T.n0 + (int)cr * HB;
+        for (int kb = 0; kb < nk; ++kb, ++kg) {
+          const int s = kg % STAGES;
+          const uint32_t ph = (kg / STAGES) & 1;
+          mbar_wait(&empty[s], ph ^ 1);
+          mbar_expect_tx(&full[s], bytes);
+          const int k0 = kb * BK;
+          int c[5];
+          if (!p.a.mn) {
+            tma_coords(p.a, k0, T.m0, T.g, T.b, T.h, c);
+            tma_load_5d(stage_a(s), &mapA, &full[s], c);
+          } else {
+#pragma unroll
+            for (int i = 0; i < 128 / 32; ++i) {
+              tma_coords(p.a, T.m0 + 32 * i, k0, T.g, T.b, T.h, c);
+              tma_load_5d(stage_a(s) + i * 4096, &mapA, &full[s], c);
+            }
+          }
+          if (!p.b.mn) {
+            tma_coords(p.b, k0, nb0, T.g, T.b, T.h, c);
+            tma_load_5d(stage_b(s), &mapB, &full[s], c);
+            if (!convert_b) {
+              tma_coords(p.blo, k0, nb0, T.g, T.b, T.h, c);
+              tma_load_5d(stage_blo(s), &mapBlo, &full[s], c);
+            }
+          } else {
+#pragma unroll
+            for (int i = 0; i < HB / 32; ++i) {
+              tma_coords(p.b, nb0 + 32 * i, k0, T.g, T.b, T.h, c);
+              tma_load_5d(stage_b(s) + i * 4096, &mapB, &full[s], c);
+              if (!convert_b) {
+                tma_coords(p.blo, nb0 + 32 * i, k0, T.g, T.b, T.h, c);
+                tma_load_5d(stage_blo(s) + i * 4096, &mapBlo, &full[s], c);
+              }
+            }
+          }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    // ===== MMA issuer: the leader's single thread drives both SMs =====
+    if (leader && lane == 0) {
+      const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)p.a.mn << 15) |
+                             ((uint32_t)p.b.mn << 16) | ((uint32_t)(P_BN >> 3) << 17) |
+                             ((uint32_t)(P_BM >> 4) << 24);
+      const uint32_t a_lbo = p.a.mn ? 4096u : 16u, a_sbo = p.a.mn ? 512u : 1024u;
+      const uint32_t b_lbo = p.b.mn ? 4096u : 16u, b_sbo = p.b.mn ? 512u : 1024u;
+      const uint32_t a_lay = p.a.mn ? 1u : 2u, b_lay = p.b.mn ? 1u : 2u;
+      const uint32_t a_kstep = p.a.mn ? 1024u : 32u;
+      const uint32_t b_kstep = p.b.mn ? 1024u : 32u;
+      int kg = 0, tc = 0;
+      for (int t = pair; t < total; t += npairs, ++tc) {
+        mbar_wait(tempty, (tc & 1) ^ 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        for (int kb = 0; kb < nk; ++kb, ++kg) {
+          const int s = kg % STAGES;
+          const uint32_t ph = (kg / STAGES) & 1;
+          mbar_wait(&conv[s], ph);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll
+          for (int k = 0; k < BK / 8; ++k) {
+            const uint64_t dah = smem_desc(stage_a(s) + k * a_kstep, a_lbo, a_sbo, a_lay);
+            const uint64_t dal = smem_desc(stage_alo(s) + k * a_kstep, a_lbo, a_sbo, a_lay);
+            const uint64_t dbh = smem_desc(stage_b(s) + k * b_kstep, b_lbo, b_sbo, b_lay);
+            const uint64_t dbl = smem_desc(stage_blo(s) + k * b_kstep, b_lbo, b_sbo, b_lay);
+            const uint32_t acc0 = (kb > 0 || k > 0) ? 1u : 0u;
+            mma_tf32_pair(tmem_base, dah, dbh, idesc, acc0);
+            if (p.passes > 1) {
+              mma_tf32_pair(tmem_base + P_BN, dal, dbh, idesc, acc0);
+              mma_tf32_pair(tmem_base + P_BN, dah, dbl, idesc, 1u);
+            }
+          }
+          mma_commit_pair(&empty[s]);
+        }
+        mma_commit_pair(tfull);
+      }
+    }
+    __syncwarp();
+  } else if (warp >= 4 && warp < 8) {
+    // ===== hi/lo split converters (own halves), then tell the leader =====
+    const int ct = threadIdx.x - 128;
+    int kg = 0;
+    for (int t = pair; t < total; t += npairs) {
+      for (int kb = 0; kb < nk; ++kb, ++kg) {
+        const int s = kg % STAGES;
+        const uint32_t ph = (kg / STAGES) & 1;
+        mbar_wait(&full[s], ph);
+        split_tile(reinterpret_cast<float*>(stage_a(s)), reinterpret_cast<float*>(stage_alo(s)),
+                   128 * BK, ct, 128, p.rawhi);
+        if (convert_b)
+          split_tile(reinterpret_cast<float*>(stage_b(s)),
+                     reinterpret_cast<float*>(stage_blo(s)), HB * BK, ct, 128, p.rawhi);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(conv_leader0 + s * 8);
+      }
+    }
+  } else if (warp >= 8) {
+    // ===== epilogue: 8 warps = 4 lane quarters x 2 column halves =====
+    const int q = warp & 3, half = (warp - 8) >> 2;
+    const bool res0 = p.ep.kind == EPI_FINAL && p.ep.cmb.mode == CM_RES0;
+    int tc = 0;
+    for (int t = pair; t < total; t += npairs, ++tc) {
+      const Tile T = tile_of(t);
+      mbar_wait(tfull, tc & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const int row = T.m0 + q * 32 + lane;
+      const uint32_t lane_addr = tmem_base + ((uint32_t)(q * 32) << 16);
+      double r2 = 0.0;
+#pragma unroll 1
+      for (int c = half * (P_BN / 2); c < (half + 1) * (P_BN / 2); c += 16) {
+        float v[16];
+        tmem_ld16(lane_addr + c, v);
+        if (p.passes > 1) {
+          float w[16];
+          tmem_ld16(lane_addr + P_BN + c, w);
+#pragma unroll
+          for (int i = 0; i < 16; ++i) v[i] += w[i];
+        }
+        const int col0 = T.n0 + c;
+        const int nvalid = min(16, p.N - col0);
+        if (row < p.M && nvalid > 0)
+          r2 += (nvalid == 16 && p.vec_ok)
+                    ? epilogue_row16(p.ep, T.g, T.b, T.h, row, col0, v)
+                    : epilogue_row(p.ep, T.g, T.b, T.h, row, col0, v, nvalid);
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(tempty_leader);
+      if (res0) {
+        // one partial per (128-row, 256-column) tile of this CTA
+        for (int o = 16; o > 0; o >>= 1) r2 += __shfl_xor_sync(0xffffffffu, r2, o);
+        if (lane == 0) red[warp - 8] = r2;
+        asm volatile("bar.sync 1, 256;" ::: "memory");
+        if (warp == 8 && lane == 0 && T.mt < tiles_m128) {
+          double tsum = 0.0;
+          for (int i = 0; i < 8; ++i) tsum += red[i];
+          p.ep.cmb.norm_partials[p.ep.cmb.norm_base + T.z * p.ep.cmb.norm_member_stride +
+                                 T.mt * tiles_n + T.nt] = tsum;
+        }
+        asm volatile("bar.sync 1, 256;" ::: "memory");
+      }
     }
   }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  cluster_sync();
+  if (warp == 2)
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "r"(512u));
 }
 
 // split kernel for weights
@@ -383,7 +746,7 @@ __global__ void split_tf32_kernel(float* hi, float* lo, const float* src, long l
        i += (long long)gridDim.x * blockDim.x) {
     const float x = src[i];
     const float h = __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
-    hi[i] = h;
+    if (hi) hi[i] = h;
     lo[i] = x - h;
   }
 }
@@ -476,9 +839,15 @@ CUtensorMap make_map(const Mat& m, int G, int Bb, int H, int rows, int cols, int
   return map;
 }
 
-template <int BN, int STAGES>
-void launch_cfg(const GemmArgs& a, const int* active, cudaStream_t s) {
+// host-side parameter block + tensor maps for one launch
+struct Prepared {
   TcParams p;
+  CUtensorMap mA, mB, mBlo;
+};
+
+Prepared prepare(const GemmArgs& a, int bm_rows, int bn_rows_b) {
+  Prepared P;
+  TcParams& p = P.p;
   p.G = a.G;
   p.M = a.M;
   p.N = a.N;
@@ -490,28 +859,76 @@ void launch_cfg(const GemmArgs& a, const int* active, cudaStream_t s) {
     return e ? atoi(e) : 3;
   }();
   p.passes = passes;
+  static const int rawhi = [] {
+    const char* e = getenv("MGLP_TF32_EXPLICIT_HI");
+    return (e && atoi(e)) ? 0 : 1;
+  }();
+  p.rawhi = rawhi;
+  {
+    auto al = [](const Mat& m) {
+      return !m.ok() || ((reinterpret_cast<uintptr_t>(m.ptr) & 15) == 0 && m.ld % 4 == 0 &&
+                         m.slot_stride % 4 == 0 && m.bstride % 4 == 0 && m.hstride % 4 == 0);
+    };
+    const EpiArgs& e = a.ep;
+    p.vec_ok = al(e.out1) && al(e.out2) && al(e.add1) && al(e.add2) && al(e.aux) && al(e.bias);
+  }
   p.a.mn = a.a_mn;
   p.b.mn = a.b_mn;
   p.blo.mn = a.b_mn;
-  // A: [M][K] (K-major) or [K][M] (MN-major); box rows: BM, or 32 K-rows
   p.Bb = a.Bb;
   p.H = a.H;
-  CUtensorMap mA = a.a_mn ? make_map(a.A, a.G, a.Bb, a.H, a.K, a.M, BK, &p.a, true)
-                          : make_map(a.A, a.G, a.Bb, a.H, a.M, a.K, BM, &p.a, false);
-  CUtensorMap mB = a.b_mn ? make_map(a.B, a.G, a.Bb, a.H, a.K, a.N, BK, &p.b, true)
-                          : make_map(a.B, a.G, a.Bb, a.H, a.N, a.K, BN, &p.b, false);
-  CUtensorMap mBlo = mB;
+  // A: [M][K] (K-major) or [K][M] (MN-major); box rows: bm_rows, or 32 K-rows
+  P.mA = a.a_mn ? make_map(a.A, a.G, a.Bb, a.H, a.K, a.M, BK, &p.a, true)
+                : make_map(a.A, a.G, a.Bb, a.H, a.M, a.K, bm_rows, &p.a, false);
+  P.mB = a.b_mn ? make_map(a.B, a.G, a.Bb, a.H, a.K, a.N, BK, &p.b, true)
+                : make_map(a.B, a.G, a.Bb, a.H, a.N, a.K, bn_rows_b, &p.b, false);
+  P.mBlo = P.mB;
   if (p.b_presplit)
-    mBlo = a.b_mn ? make_map(a.Blo, a.G, a.Bb, a.H, a.K, a.N, BK, &p.blo, true)
-                  : make_map(a.Blo, a.G, a.Bb, a.H, a.N, a.K, BN, &p.blo, false);
+    P.mBlo = a.b_mn ? make_map(a.Blo, a.G, a.Bb, a.H, a.K, a.N, BK, &p.blo, true)
+                    : make_map(a.Blo, a.G, a.Bb, a.H, a.N, a.K, bn_rows_b, &p.blo, false);
   else
     p.blo = p.b;
+  return P;
+}
+
+int num_sms() {
+  static int sms = 0;
+  if (!sms) MGLP_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
+  return sms;
+}
+
+template <int BN, int STAGES>
+void launch_cfg(const GemmArgs& a, const int* active, cudaStream_t s) {
+  Prepared P = prepare(a, BM, BN);
   const int smem = Smem<BN, STAGES>::BYTES;
   MGLP_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<BN, STAGES>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  dim3 grid(ceil_div(a.N, BN), ceil_div(a.M, BM), a.G * a.Bb * a.H);
-  gemm_tc_kernel<BN, STAGES><<<grid, kThreads, smem, s>>>(mA, mB, mBlo, p, active);
+  const long long tiles = (long long)ceil_div(a.N, BN) * ceil_div(a.M, BM) * a.G * a.Bb * a.H;
+  const int grid = (int)std::min<long long>(tiles, num_sms());
+  gemm_tc_kernel<BN, STAGES><<<grid, kThreads, smem, s>>>(P.mA, P.mB, P.mBlo, P.p, active);
   MGLP_CUDA(cudaGetLastError());
+}
+
+void launch_pair(const GemmArgs& a, const int* active, cudaStream_t s) {
+  Prepared P = prepare(a, 128, P_BN / 2);
+  const int smem = Smem2::BYTES;
+  MGLP_CUDA(cudaFuncSetAttribute(gemm_tc2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 smem));
+  const long long tiles = (long long)ceil_div(a.N, P_BN) * ceil_div(a.M, P_BM) * a.G * a.Bb * a.H;
+  const int pairs = (int)std::min<long long>(tiles, num_sms() / 2);
+  gemm_tc2_kernel<<<2 * pairs, kThreads2, smem, s>>>(P.mA, P.mB, P.mBlo, P.p, active);
+  MGLP_CUDA(cudaGetLastError());
+}
+
+// the CTA-pair kernel needs at least a full 256 x 256 tile to pay off; the
+// choice depends only on (M, N), so a given layer GEMM always runs the same
+// kernel (bitwise determinism of Phi does not depend on the family size)
+bool use_pair(const GemmArgs& a) {
+  static const int off = [] {
+    const char* e = getenv("MGLP_GEMM_NO_PAIR");
+    return e ? atoi(e) : 0;
+  }();
+  return !off && a.M >= P_BM && a.N >= P_BN;
 }
 
 constexpr int kBN = 128;
@@ -520,13 +937,18 @@ constexpr int kStages = 3;
 }  // namespace
 
 int gemm_tc_blocks(const GemmArgs& a) {
-  return ceil_div(a.N, kBN) * ceil_div(a.M, BM) * a.G * a.Bb * a.H;
+  // residual-norm partial slots: one per (128-row, column-tile) of each problem
+  const int bn = use_pair(a) ? P_BN : kBN;
+  return ceil_div(a.N, bn) * ceil_div(a.M, BM) * a.G * a.Bb * a.H;
 }
 
 void launch_gemm_tc(const GemmArgs& a, const int* active, cudaStream_t s) {
   if (a.G == 0 || a.M == 0 || a.N == 0) return;
   if (a.K == 0) throw ContractViolation("gemm_tc: K must be positive");
-  launch_cfg<kBN, kStages>(a, active, s);
+  if (use_pair(a))
+    launch_pair(a, active, s);
+  else
+    launch_cfg<kBN, kStages>(a, active, s);
 }
 
 void launch_split_tf32(float* hi, float* lo, const float* src, long long n, cudaStream_t s) {

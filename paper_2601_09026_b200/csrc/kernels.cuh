@@ -81,8 +81,10 @@ struct SolveCtrl {
   double trace[kMaxTrace];
 };
 void launch_ctrl_begin(SolveCtrl* c, cudaStream_t s);
-// trace entry = sqrt(sum of partials[0..count)), measured mid-cycle (mgrit.hpp:235-238)
-void launch_trace_record(SolveCtrl* c, const double* partials, int count, cudaStream_t s);
+// trace entry = sqrt(sum of the per-interval partials [n_chunks][S]), measured
+// mid-cycle (mgrit.hpp:235-238)
+void launch_trace_record(SolveCtrl* c, const double* partials, int n_chunks, int S, int per_rank,
+                         bool reversed, cudaStream_t s);
 // end of one V-cycle: push the trace, stop on non-finite / converged (mgrit.hpp:252-259)
 void launch_cycle_end(SolveCtrl* c, double tol, cudaStream_t s);
 

@@ -138,7 +138,7 @@ __global__ void __launch_bounds__(256) ln_bwd_kernel(LnBwdArgs a, const int* act
   if (a.cmb.mode == CM_RES0) {
     const double t = block_sum_f64(r2, red);
     if (threadIdx.x == 0)
-      a.cmb.norm_partials[a.cmb.norm_base + blockIdx.y * gridDim.x + blockIdx.x] = t;
+      a.cmb.norm_partials[a.cmb.norm_base + blockIdx.y * a.cmb.norm_member_stride + blockIdx.x] = t;
   }
 }
 
@@ -306,7 +306,7 @@ __global__ void __launch_bounds__(kElemThreads) elem_combine_kernel(ElemCombineA
   if (a.cmb.mode == CM_RES0) {
     const double t = block_sum_f64(r2, red);
     if (threadIdx.x == 0)
-      a.cmb.norm_partials[a.cmb.norm_base + blockIdx.y * gridDim.x + blockIdx.x] = t;
+      a.cmb.norm_partials[a.cmb.norm_base + blockIdx.y * a.cmb.norm_member_stride + blockIdx.x] = t;
   }
 }
 
@@ -358,13 +358,26 @@ __global__ void ctrl_begin_kernel(SolveCtrl* c) {
   c->pending = 0.0;
 }
 
-__global__ void trace_record_kernel(SolveCtrl* c, const double* partials, int count) {
+// sum of the per-interval partials in interval order (each interval's slots
+// by a fixed tree): the trace does not depend on the rank count. With
+// `reversed`, rank r's block of `per_rank` intervals holds intervals of time
+// position P-1-r (the adjoint solve's partition).
+__global__ void trace_record_kernel(SolveCtrl* c, const double* partials, int n_chunks, int S,
+                                    int per_rank, int reversed) {
   __shared__ double red[32];
   if (!c->active) return;
-  double s = 0.0;
-  for (int i = threadIdx.x; i < count; i += blockDim.x) s += partials[i];
-  const double t = block_sum_f64(s, red);
-  if (threadIdx.x == 0) c->pending = sqrt(t);
+  const int P = n_chunks / per_rank;
+  double total = 0.0;
+  for (int k = 0; k < n_chunks; ++k) {
+    const int pos = reversed ? (P - 1 - k / per_rank) * per_rank + k % per_rank : k;
+    const double* q = partials + (size_t)pos * S;
+    double s = 0.0;
+    for (int i = threadIdx.x; i < S; i += blockDim.x) s += q[i];
+    const double t = block_sum_f64(s, red);
+    if (threadIdx.x == 0) total += t;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) c->pending = sqrt(total);
 }
 
 __global__ void cycle_end_kernel(SolveCtrl* c, double tol) {
@@ -445,8 +458,9 @@ void launch_zero(int G, long long n, Mat dst, const int* active, cudaStream_t s)
 
 void launch_ctrl_begin(SolveCtrl* c, cudaStream_t s) { ctrl_begin_kernel<<<1, 1, 0, s>>>(c); }
 
-void launch_trace_record(SolveCtrl* c, const double* partials, int count, cudaStream_t s) {
-  trace_record_kernel<<<1, 256, 0, s>>>(c, partials, count);
+void launch_trace_record(SolveCtrl* c, const double* partials, int n_chunks, int S, int per_rank,
+                         bool reversed, cudaStream_t s) {
+  trace_record_kernel<<<1, 256, 0, s>>>(c, partials, n_chunks, S, per_rank, reversed ? 1 : 0);
 }
 
 void launch_cycle_end(SolveCtrl* c, double tol, cudaStream_t s) {

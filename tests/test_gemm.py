@@ -1,6 +1,7 @@
 """tcgen05 kind::tf32 x3 GEMM (the product kernel) against an fp64 torch
 reference and the fp32 CUDA-core reference kernel, through the C-ABI test hook."""
 import ctypes as C
+import os
 
 import numpy as np
 import pytest
@@ -68,3 +69,36 @@ def test_split_is_effective():
     separate correction accumulator must be fp32-class (~6e-6 at K=2048)"""
     c, ref = run(1, 256, 256, 2048, False, False, True, engine=0)
     assert relerr(c, ref) < 1.2e-5
+
+
+_TRUNC_SCRIPT = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+from paper_2601_09026_b200 import _native as N
+torch.manual_seed(0)
+M, Nn, K = 256, 256, 512
+A = torch.randn(M, K).float().cuda()
+B = torch.randn(Nn, K).float().cuda()
+C = torch.empty(M, Nn, device="cuda")
+N.call("mglp_test_gemm", 1, M, Nn, K, A.data_ptr(), 0, K, 0, B.data_ptr(), 0, K, 0, 0, None,
+       C.data_ptr(), 0, Nn, 0)
+np.save(sys.argv[2], C.cpu().numpy())
+"""
+
+
+def test_tf32_operand_truncation(tmp_path):
+    """kind::tf32 reads fp32 operands truncated to tf32: feeding the raw tile
+    as the hi part (default) is bitwise identical to writing the masked hi
+    (MGLP_TF32_EXPLICIT_HI=1). The default converter relies on this."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = tmp_path / "t.py"
+    script.write_text(_TRUNC_SCRIPT)
+    outs = []
+    for explicit in ("0", "1"):
+        out = tmp_path / f"c{explicit}.npy"
+        env = dict(os.environ, MGLP_TF32_EXPLICIT_HI=explicit)
+        subprocess.run([sys.executable, str(script), root, str(out)], check=True, env=env)
+        outs.append(np.load(out))
+    assert np.array_equal(outs[0], outs[1])
