@@ -32,7 +32,12 @@ def run(M, N_, K, a_mn, b_mn, pre, engine=0, exact=False, scaleB=1.0):
 
 mode = sys.argv[1] if len(sys.argv) > 1 else "all"
 if mode in ("all", "major"):
-    for K in (8, 32, 96):
+    for (M, Nn, K) in [(512, 512, 96), (300, 520, 100), (1024, 768, 768)]:
+        for a_mn in (0, 1):
+            for b_mn in (0, 1):
+                e, _ = run(M, Nn, K, a_mn, b_mn, 1 - b_mn)
+                print(f"pair M{M} N{Nn} K{K} a_mn={a_mn} b_mn={b_mn}: {e:.2e}", flush=True)
+    for K in ():
         for a_mn in (0, 1):
             for b_mn in (0, 1):
                 for pre in (0, 1):
