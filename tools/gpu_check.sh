@@ -1,4 +1,4 @@
-timeout 300 python tools/debug_gemm.py major 2>&1 | tail -14
-timeout 900 python -m pytest tests -q -m gpu -x 2>&1 | tail -8
+timeout 900 python -m pytest tests -q -m gpu -x 2>&1 | tail -5
+timeout 900 python tools/parity_report.py 2>&1 | tail -8
 timeout 600 python tools/profile_step.py bert 2>&1 | tail -24
 timeout 900 python bench.py --config bert --steps 3 --warmup 3 --no-cpu-baseline 2>&1 | tail -1
