@@ -178,7 +178,7 @@ Engine::~Engine() {
   if (stream_) cudaStreamSynchronize(stream_);
   free_solver(fwd_);
   free_solver(bwd_);
-  for (float* p : {P_, Plo_, Gr_, scratch_, cache_, bscratch_, traj_, lam_all_,
+  for (float* p : {P_, Plo_, Gr_, scratch_, cache_, bscratch_, bcache_, traj_, lam_all_,
                    zero_state_, snap_fwd_, snap_bwd_})
     if (p) cudaFree(p);
   drop_graph();
@@ -381,7 +381,7 @@ void Engine::set_shape(int batch, int s_x, int s_y) {
   drop_graph();
   free_solver(fwd_);
   free_solver(bwd_);
-  for (float** p : {&scratch_, &cache_, &bscratch_, &traj_, &lam_all_, &zero_state_, &snap_fwd_,
+  for (float** p : {&scratch_, &cache_, &bscratch_, &bcache_, &traj_, &lam_all_, &zero_state_, &snap_fwd_,
                     &snap_bwd_}) {
     if (*p) cudaFree(*p);
     *p = nullptr;
@@ -450,6 +450,8 @@ void Engine::set_shape(int batch, int s_x, int s_y) {
   MGLP_CUDA(cudaMalloc(&scratch_, (size_t)Gmax_ * al_.size * sizeof(float)));
   MGLP_CUDA(cudaMalloc(&cache_, (size_t)total_ * al_.size * sizeof(float)));
   MGLP_CUDA(cudaMalloc(&bscratch_, (size_t)Gmax_ * bl_.size * sizeof(float)));
+  MGLP_CUDA(cudaMalloc(&bcache_, (size_t)total_ * bl_.size * sizeof(float)));
+  bcache_valid_.assign(total_, 0);
   MGLP_CUDA(cudaMalloc(&traj_, (size_t)(total_ + 1) * state_n_ * sizeof(float)));
   MGLP_CUDA(cudaMalloc(&lam_all_, (size_t)(total_ + 1) * state_n_ * sizeof(float)));
   MGLP_CUDA(cudaMalloc(&zero_state_, (size_t)state_n_ * sizeof(float)));
@@ -543,7 +545,8 @@ Mat Engine::act_mat(const ActRef& r, long long off, int ld) const {
   m.step = r.step;
   return m;
 }
-Mat Engine::bwd_mat(long long off, int ld) const {
+Mat Engine::bwd_mat(const EvalSpec& e, long long off, int ld) const {
+  if (e.bact.base) return act_mat(e.bact, off, ld);
   Mat m;
   m.ptr = bscratch_ + off;
   m.slot_stride = bl_.size;
@@ -774,6 +777,7 @@ void Engine::eval_forward(const EvalSpec& e0) {
         e.in = shift(e0.in, g0);
         e.lam = shift(e0.lam, g0);
         e.act.slot0 += g0 * e0.act.step;
+        e.bact.slot0 += g0 * e0.bact.step;
         Combine& c = e.cmb;
         c.z = shift(c.z, g0);
         c.out = shift(c.out, g0);
@@ -1068,6 +1072,7 @@ void Engine::eval_adjoint(const EvalSpec& e0) {
         e.in = shift(e0.in, g0);
         e.lam = shift(e0.lam, g0);
         e.act.slot0 += g0 * e0.act.step;
+        e.bact.slot0 += g0 * e0.bact.step;
         Combine& c = e.cmb;
         c.z = shift(c.z, g0);
         c.out = shift(c.out, g0);
@@ -1105,9 +1110,9 @@ void Engine::encoder_adjoint(const EvalSpec& e, bool causal) {
   Mat hh = act_mat(e.act, al_.h, f), gg = act_mat(e.act, al_.g, f);
   Mat n1 = act_mat(e.act, al_.n1, d), n2 = act_mat(e.act, al_.n2, d);
   Mat st1 = act_mat(e.act, al_.st1, 2), st2 = act_mat(e.act, al_.st2, 2);
-  Mat dh = bwd_mat(bl_.dh, f), dn2 = bwd_mat(bl_.dn2, d), du = bwd_mat(bl_.du, d);
-  Mat da1 = bwd_mat(bl_.da1, d), dctx = bwd_mat(bl_.dctx, d), dqkv = bwd_mat(bl_.dqkv, 3 * d);
-  Mat dn1 = bwd_mat(bl_.dn1, d), dPm = bwd_mat(bl_.dP, 0);
+  Mat dh = bwd_mat(e, bl_.dh, f), dn2 = bwd_mat(e, bl_.dn2, d), du = bwd_mat(e, bl_.du, d);
+  Mat da1 = bwd_mat(e, bl_.da1, d), dctx = bwd_mat(e, bl_.dctx, d), dqkv = bwd_mat(e, bl_.dqkv, 3 * d);
+  Mat dn1 = bwd_mat(e, bl_.dn1, d), dPm = bwd_mat(e, bl_.dP, 0);
 
   auto mk = [&](int M, int N, int K, Mat A, long long w, int ldw) {
     GemmArgs g;
@@ -1121,77 +1126,79 @@ void Engine::encoder_adjoint(const EvalSpec& e, bool causal) {
     g.b_mn = true;  // dX = U . W: W [out,in] read as [K,N]
     return g;
   };
-  GemmArgs g = mk(R, f, d, UP, L.w_out, f);
-  g.ep.kind = EPI_GELU_BWD;
-  g.ep.out1 = dh;
-  g.ep.aux = hh;
-  gemm(g);
+  if (!e.wgrad_only) {  // dgrad chain (skipped when the backward cache holds it)
+    GemmArgs g = mk(R, f, d, UP, L.w_out, f);
+    g.ep.kind = EPI_GELU_BWD;
+    g.ep.out1 = dh;
+    g.ep.aux = hh;
+    gemm(g);
 
-  g = mk(R, d, f, dh, L.w_in, d);
-  g.ep.kind = EPI_STORE;
-  g.ep.out1 = dn2;
-  gemm(g);
+    g = mk(R, d, f, dh, L.w_in, d);
+    g.ep.kind = EPI_STORE;
+    g.ep.out1 = dn2;
+    gemm(g);
 
-  LnBwdArgs lb;
-  lb.G = G;
-  lb.rows = R;
-  lb.d = d;
-  lb.x = u;
-  lb.stats = st2;
-  lb.up = dn2;
-  lb.gain = par(L.ln2_g, 0, l0, ls);
-  lb.out1 = du;
-  lb.out2 = da1;
-  lb.addB = UP;
-  ++launches_;
-  timed(PROF_ROW, 0.0, 20.0 * lb.G * (double)lb.rows * lb.d,
-        [&] { launch_ln_bwd(lb, active_, stream_); });
-
-  g = mk(R, d, d, da1, L.w_o, d);
-  g.ep.kind = EPI_STORE;
-  g.ep.out1 = dctx;
-  gemm(g);
-
-  attention_bwd(G, qkv, qkv.offset(d), qkv.offset(2 * d), Pm, dctx, dPm, dqkv, dqkv.offset(d),
-                dqkv.offset(2 * d), R / B_, R / B_);
-
-  g = mk(R, d, 3 * d, dqkv, L.w_qkv, d);
-  g.ep.kind = EPI_STORE;
-  g.ep.out1 = dn1;
-  gemm(g);
-
-  if (e.cmb.mode != CM_NONE) {
-    LnBwdArgs l1;
-    l1.G = G;
-    l1.rows = R;
-    l1.d = d;
-    l1.x = X;
-    l1.stats = st1;
-    l1.up = dn1;
-    l1.gain = par(L.ln1_g, 0, l0, ls);
-    l1.addA = du;
-    Combine c = e.cmb;
-    for (Mat* m : {&c.z, &c.out, &c.base, &c.phib, &c.rho, &c.v})
-      if (m->ok()) {
-        *m = m->offset(x_off_);
-        m->ld = d;
-      }
-    if (c.mode == CM_RES0) c.norm_base = e.cmb.norm_base + part_off_ln_;
-    l1.cmb = c;
+    LnBwdArgs lb;
+    lb.G = G;
+    lb.rows = R;
+    lb.d = d;
+    lb.x = u;
+    lb.stats = st2;
+    lb.up = dn2;
+    lb.gain = par(L.ln2_g, 0, l0, ls);
+    lb.out1 = du;
+    lb.out2 = da1;
+    lb.addB = UP;
     ++launches_;
-    timed(PROF_ROW, 0.0, 20.0 * l1.G * (double)l1.rows * l1.d,
-          [&] { launch_ln_bwd(l1, active_, stream_); });
-    if (sd_.kind == 2) {
-      ElemCombineArgs ec;
-      ec.G = G;
-      ec.n = (long long)Ty_ * d;
-      Combine cy = e.cmb;
-      for (Mat* m : {&cy.z, &cy.out, &cy.base, &cy.phib, &cy.rho, &cy.v})
-        if (m->ok()) *m = m->offset(y_off_);
-      if (cy.mode == CM_RES0) cy.norm_base = e.cmb.norm_base + part_off_elem_;
-      ec.cmb = cy;
+    timed(PROF_ROW, 0.0, 20.0 * lb.G * (double)lb.rows * lb.d,
+          [&] { launch_ln_bwd(lb, active_, stream_); });
+
+    g = mk(R, d, d, da1, L.w_o, d);
+    g.ep.kind = EPI_STORE;
+    g.ep.out1 = dctx;
+    gemm(g);
+
+    attention_bwd(G, qkv, qkv.offset(d), qkv.offset(2 * d), Pm, dctx, dPm, dqkv, dqkv.offset(d),
+                  dqkv.offset(2 * d), R / B_, R / B_);
+
+    g = mk(R, d, 3 * d, dqkv, L.w_qkv, d);
+    g.ep.kind = EPI_STORE;
+    g.ep.out1 = dn1;
+    gemm(g);
+
+    if (e.cmb.mode != CM_NONE) {
+      LnBwdArgs l1;
+      l1.G = G;
+      l1.rows = R;
+      l1.d = d;
+      l1.x = X;
+      l1.stats = st1;
+      l1.up = dn1;
+      l1.gain = par(L.ln1_g, 0, l0, ls);
+      l1.addA = du;
+      Combine c = e.cmb;
+      for (Mat* m : {&c.z, &c.out, &c.base, &c.phib, &c.rho, &c.v})
+        if (m->ok()) {
+          *m = m->offset(x_off_);
+          m->ld = d;
+        }
+      if (c.mode == CM_RES0) c.norm_base = e.cmb.norm_base + part_off_ln_;
+      l1.cmb = c;
       ++launches_;
-      launch_elem_combine(ec, active_, stream_);
+      timed(PROF_ROW, 0.0, 20.0 * l1.G * (double)l1.rows * l1.d,
+            [&] { launch_ln_bwd(l1, active_, stream_); });
+      if (sd_.kind == 2) {
+        ElemCombineArgs ec;
+        ec.G = G;
+        ec.n = (long long)Ty_ * d;
+        Combine cy = e.cmb;
+        for (Mat* m : {&cy.z, &cy.out, &cy.base, &cy.phib, &cy.rho, &cy.v})
+          if (m->ok()) *m = m->offset(y_off_);
+        if (cy.mode == CM_RES0) cy.norm_base = e.cmb.norm_base + part_off_elem_;
+        ec.cmb = cy;
+        ++launches_;
+        launch_elem_combine(ec, active_, stream_);
+      }
     }
   }
 
@@ -1256,11 +1263,11 @@ void Engine::decoder_adjoint(const EvalSpec& e) {
   Mat cq = act_mat(e.act, al_.cq, d), ckv = act_mat(e.act, al_.ckv, 2 * d);
   Mat cctx = act_mat(e.act, al_.cctx, d), cP = act_mat(e.act, al_.cP, 0);
   Mat st3 = act_mat(e.act, al_.st3, 2);
-  Mat dh = bwd_mat(bl_.dh, f), dn2 = bwd_mat(bl_.dn2, d), dy = bwd_mat(bl_.dy, d);
-  Mat dybar = bwd_mat(bl_.dybar, d), dcctx = bwd_mat(bl_.dcctx, d), dcq = bwd_mat(bl_.dcq, d);
-  Mat dckv = bwd_mat(bl_.dckv, 2 * d), dn3 = bwd_mat(bl_.dn3, d), dxe = bwd_mat(bl_.dxe, d);
-  Mat da1 = bwd_mat(bl_.da1, d), dctx = bwd_mat(bl_.dctx, d), dqkv = bwd_mat(bl_.dqkv, 3 * d);
-  Mat dn1 = bwd_mat(bl_.dn1, d), dPm = bwd_mat(bl_.dP, 0), dP2 = bwd_mat(bl_.dP2, 0);
+  Mat dh = bwd_mat(e, bl_.dh, f), dn2 = bwd_mat(e, bl_.dn2, d), dy = bwd_mat(e, bl_.dy, d);
+  Mat dybar = bwd_mat(e, bl_.dybar, d), dcctx = bwd_mat(e, bl_.dcctx, d), dcq = bwd_mat(e, bl_.dcq, d);
+  Mat dckv = bwd_mat(e, bl_.dckv, 2 * d), dn3 = bwd_mat(e, bl_.dn3, d), dxe = bwd_mat(e, bl_.dxe, d);
+  Mat da1 = bwd_mat(e, bl_.da1, d), dctx = bwd_mat(e, bl_.dctx, d), dqkv = bwd_mat(e, bl_.dqkv, 3 * d);
+  Mat dn1 = bwd_mat(e, bl_.dn1, d), dPm = bwd_mat(e, bl_.dP, 0), dP2 = bwd_mat(e, bl_.dP2, 0);
 
   auto mk = [&](int M, int N, int K, Mat A, long long w, int ldw) {
     GemmArgs g;
@@ -1274,104 +1281,106 @@ void Engine::decoder_adjoint(const EvalSpec& e) {
     g.b_mn = true;
     return g;
   };
-  GemmArgs g = mk(R, f, d, UPy, L.w_out, f);
-  g.ep.kind = EPI_GELU_BWD;
-  g.ep.out1 = dh;
-  g.ep.aux = hh;
-  gemm(g);
+  if (!e.wgrad_only) {  // dgrad chain (skipped when the backward cache holds it)
+    GemmArgs g = mk(R, f, d, UPy, L.w_out, f);
+    g.ep.kind = EPI_GELU_BWD;
+    g.ep.out1 = dh;
+    g.ep.aux = hh;
+    gemm(g);
 
-  g = mk(R, d, f, dh, L.w_in, d);
-  g.ep.kind = EPI_STORE;
-  g.ep.out1 = dn2;
-  gemm(g);
+    g = mk(R, d, f, dh, L.w_in, d);
+    g.ep.kind = EPI_STORE;
+    g.ep.out1 = dn2;
+    gemm(g);
 
-  LnBwdArgs lb;
-  lb.G = G;
-  lb.rows = R;
-  lb.d = d;
-  lb.x = u2;
-  lb.stats = st2;
-  lb.up = dn2;
-  lb.gain = par(L.ln2_g, 0, l0, ls);
-  lb.out1 = dy;      // du2
-  lb.out2 = dybar;   // up + du2
-  lb.addB = UPy;
-  ++launches_;
-  timed(PROF_ROW, 0.0, 20.0 * lb.G * (double)lb.rows * lb.d,
-        [&] { launch_ln_bwd(lb, active_, stream_); });
-
-  g = mk(R, d, d, dybar, L.w_co, d);
-  g.ep.kind = EPI_STORE;
-  g.ep.out1 = dcctx;
-  gemm(g);
-
-  attention_bwd(G, cq, ckv, ckv.offset(d), cP, dcctx, dP2, dcq, dckv, dckv.offset(d), sy_, sx_);
-
-  g = mk(R, d, d, dcq, L.w_cq, d);
-  g.ep.kind = EPI_STORE;
-  g.ep.out1 = dn3;
-  gemm(g);
-
-  g = mk(Tx_, d, 2 * d, dckv, L.w_ckv, d);
-  g.ep.kind = EPI_STORE;
-  g.ep.out1 = dxe;
-  gemm(g);
-
-  lb.x = u3;
-  lb.stats = st3;
-  lb.up = dn3;
-  lb.gain = par(L.ln3_g, 0, l0, ls);
-  lb.addA = dy;
-  lb.out1 = dy;     // du2 + du3
-  lb.addB = dybar;
-  lb.out2 = da1;    // dybar + du3
-  ++launches_;
-  timed(PROF_ROW, 0.0, 20.0 * lb.G * (double)lb.rows * lb.d,
-        [&] { launch_ln_bwd(lb, active_, stream_); });
-
-  g = mk(R, d, d, da1, L.w_o, d);
-  g.ep.kind = EPI_STORE;
-  g.ep.out1 = dctx;
-  gemm(g);
-
-  attention_bwd(G, qkv, qkv.offset(d), qkv.offset(2 * d), Pm, dctx, dPm, dqkv, dqkv.offset(d),
-                dqkv.offset(2 * d), sy_, sy_);
-
-  g = mk(R, d, 3 * d, dqkv, L.w_qkv, d);
-  g.ep.kind = EPI_STORE;
-  g.ep.out1 = dn1;
-  gemm(g);
-
-  if (e.cmb.mode != CM_NONE) {
-    LnBwdArgs l1;
-    l1.G = G;
-    l1.rows = R;
-    l1.d = d;
-    l1.x = Y;
-    l1.stats = st1;
-    l1.up = dn1;
-    l1.gain = par(L.ln1_g, 0, l0, ls);
-    l1.addA = dy;
-    Combine c = e.cmb;
-    for (Mat* m : {&c.z, &c.out, &c.base, &c.phib, &c.rho, &c.v})
-      if (m->ok()) {
-        *m = m->offset(y_off_);
-        m->ld = d;
-      }
-    if (c.mode == CM_RES0) c.norm_base = e.cmb.norm_base + part_off_ln_;
-    l1.cmb = c;
+    LnBwdArgs lb;
+    lb.G = G;
+    lb.rows = R;
+    lb.d = d;
+    lb.x = u2;
+    lb.stats = st2;
+    lb.up = dn2;
+    lb.gain = par(L.ln2_g, 0, l0, ls);
+    lb.out1 = dy;      // du2
+    lb.out2 = dybar;   // up + du2
+    lb.addB = UPy;
     ++launches_;
-    timed(PROF_ROW, 0.0, 20.0 * l1.G * (double)l1.rows * l1.d,
-          [&] { launch_ln_bwd(l1, active_, stream_); });
-    ElemCombineArgs ec;
-    ec.G = G;
-    ec.n = (long long)Tx_ * d;
-    ec.F = dxe;
-    Combine cx = e.cmb;
-    if (cx.mode == CM_RES0) cx.norm_base = e.cmb.norm_base + part_off_elem_;
-    ec.cmb = cx;
+    timed(PROF_ROW, 0.0, 20.0 * lb.G * (double)lb.rows * lb.d,
+          [&] { launch_ln_bwd(lb, active_, stream_); });
+
+    g = mk(R, d, d, dybar, L.w_co, d);
+    g.ep.kind = EPI_STORE;
+    g.ep.out1 = dcctx;
+    gemm(g);
+
+    attention_bwd(G, cq, ckv, ckv.offset(d), cP, dcctx, dP2, dcq, dckv, dckv.offset(d), sy_, sx_);
+
+    g = mk(R, d, d, dcq, L.w_cq, d);
+    g.ep.kind = EPI_STORE;
+    g.ep.out1 = dn3;
+    gemm(g);
+
+    g = mk(Tx_, d, 2 * d, dckv, L.w_ckv, d);
+    g.ep.kind = EPI_STORE;
+    g.ep.out1 = dxe;
+    gemm(g);
+
+    lb.x = u3;
+    lb.stats = st3;
+    lb.up = dn3;
+    lb.gain = par(L.ln3_g, 0, l0, ls);
+    lb.addA = dy;
+    lb.out1 = dy;     // du2 + du3
+    lb.addB = dybar;
+    lb.out2 = da1;    // dybar + du3
     ++launches_;
-    launch_elem_combine(ec, active_, stream_);
+    timed(PROF_ROW, 0.0, 20.0 * lb.G * (double)lb.rows * lb.d,
+          [&] { launch_ln_bwd(lb, active_, stream_); });
+
+    g = mk(R, d, d, da1, L.w_o, d);
+    g.ep.kind = EPI_STORE;
+    g.ep.out1 = dctx;
+    gemm(g);
+
+    attention_bwd(G, qkv, qkv.offset(d), qkv.offset(2 * d), Pm, dctx, dPm, dqkv, dqkv.offset(d),
+                  dqkv.offset(2 * d), sy_, sy_);
+
+    g = mk(R, d, 3 * d, dqkv, L.w_qkv, d);
+    g.ep.kind = EPI_STORE;
+    g.ep.out1 = dn1;
+    gemm(g);
+
+    if (e.cmb.mode != CM_NONE) {
+      LnBwdArgs l1;
+      l1.G = G;
+      l1.rows = R;
+      l1.d = d;
+      l1.x = Y;
+      l1.stats = st1;
+      l1.up = dn1;
+      l1.gain = par(L.ln1_g, 0, l0, ls);
+      l1.addA = dy;
+      Combine c = e.cmb;
+      for (Mat* m : {&c.z, &c.out, &c.base, &c.phib, &c.rho, &c.v})
+        if (m->ok()) {
+          *m = m->offset(y_off_);
+          m->ld = d;
+        }
+      if (c.mode == CM_RES0) c.norm_base = e.cmb.norm_base + part_off_ln_;
+      l1.cmb = c;
+      ++launches_;
+      timed(PROF_ROW, 0.0, 20.0 * l1.G * (double)l1.rows * l1.d,
+            [&] { launch_ln_bwd(l1, active_, stream_); });
+      ElemCombineArgs ec;
+      ec.G = G;
+      ec.n = (long long)Tx_ * d;
+      ec.F = dxe;
+      Combine cx = e.cmb;
+      if (cx.mode == CM_RES0) cx.norm_base = e.cmb.norm_base + part_off_elem_;
+      ec.cmb = cx;
+      ++launches_;
+      launch_elem_combine(ec, active_, stream_);
+    }
   }
 
   if (e.want_grads) {
@@ -1502,6 +1511,9 @@ void Engine::sys_eval(Solver& s, int level, int k0, int kstep, int G, Mat in, Co
       e.lam = shift(in, g0);
       e.in = state_mat(traj_, state_n_, sd_.d, e.layer0, e.layer_step);
       e.act = ActRef{cache_, al_.size, e.layer0, e.layer_step};
+      // level-0 relaxation steps keep their dgrad intermediates per layer:
+      // the parameter pass then only forms dW, db for those layers
+      if (capture) e.bact = ActRef{bcache_, bl_.size, e.layer0, e.layer_step};
       eval_adjoint(e);
     }
   }
@@ -1624,10 +1636,14 @@ void Engine::descend(Solver& s, int level) {  // mgrit.hpp:285-296
   f_relax(s, level, false);
 }
 
-void Engine::v_cycle(Solver& s, double tol) {  // mgrit.hpp:235-246
-  const bool cap = !s.adjoint;
+void Engine::v_cycle(Solver& s, double tol, bool first) {  // mgrit.hpp:235-246
+  const bool cap = true;  // forward: linearisation cache; adjoint: dgrad cache
   const bool one_level = cfg_.levels == 1;
-  f_relax(s, 0, cap && one_level);
+  // Every cycle ends with the F-points equal to Phi of the current C-points
+  // (final F-relaxation, or F + residual with one level), so the opening
+  // F-relaxation of the next cycle of the same solve would recompute the same
+  // bits: only the first cycle runs it.
+  if (first) f_relax(s, 0, cap && one_level);
   c_relax(s, 0);
   f_relax(s, 0, cap);
   residual_c_rows(s, 0, cap && one_level);
@@ -1645,7 +1661,7 @@ void Engine::solve(Solver& s, int iters, double tol) {  // mgrit.hpp:248-262
   if (iters < 1) throw ValidationError("solve_forward: need at least one iteration");
   launch_ctrl_begin(s.ctrl, stream_);
   active_ = &s.ctrl->active;
-  for (int it = 0; it < iters; ++it) v_cycle(s, tol);
+  for (int it = 0; it < iters; ++it) v_cycle(s, tol, it == 0);
   active_ = nullptr;
 }
 
@@ -1762,23 +1778,44 @@ void Engine::backward_device(const float* lamN_dev, float* lam0_dev, bool want_g
     launch_zero(N_, state_n_, lv_v(bwd_, 0, 1, 1), nullptr, stream_);
   solve(bwd_, cfg_.bwd_iters, cfg_.bwd_tol);
   // parameter pass over the owned layers (adjoint.hpp:165-175): layer ib+i at
-  // traj[ib+i] with upstream mu[N-1-i], gscale = h
+  // traj[ib+i] with upstream mu[N-1-i], gscale = h. The final level-0
+  // relaxation evaluated exactly these (layer, upstream) pairs for every
+  // adjoint step k = N-1-i that is not the last of its interval, and kept
+  // their dgrad intermediates: those layers only need dW, db.
   if (want_grads) {
+    const int cf = cfg_.coarsen;
     const int i_lo = fwd_.p_lo[0], i_hi = fwd_.p_hi[0];
-    for (int i0 = i_lo; i0 < i_hi; i0 += Gmax_) {
-      const int Gc = std::min(Gmax_, i_hi - i0);
+    auto family = [&](int i0, int G, int step, bool cached) {
       EvalSpec e;
-      e.G = Gc;
+      e.G = G;
       e.layer0 = ib_ + i0;
-      e.layer_step = 1;
+      e.layer_step = step;
       e.dt = 0.f;
-      e.lam = lv_v(bwd_, 0, N_ - 1 - i0, -1);
-      e.in = state_mat(traj_, state_n_, sd_.d, ib_ + i0, 1);
-      e.act = ActRef{cache_, al_.size, ib_ + i0, 1};
+      e.lam = lv_v(bwd_, 0, N_ - 1 - i0, -step);
+      e.in = state_mat(traj_, state_n_, sd_.d, ib_ + i0, step);
+      e.act = ActRef{cache_, al_.size, ib_ + i0, step};
+      if (cached) e.bact = ActRef{bcache_, bl_.size, ib_ + i0, step};
       e.cmb.mode = CM_NONE;
       e.want_grads = true;
+      e.wgrad_only = cached;
       e.gscale = (float)h_[ib_];
       eval_adjoint(e);
+    };
+    auto cached = [&](int i) { return cfg_.levels == 1 || ((N_ - 1 - i) % cf) != cf - 1; };
+    // families with an affine layer index: the uncached layers share one
+    // residue mod c_f, the cached ones split into the other c_f-1 residues
+    std::vector<std::vector<int>> groups(cf + 1);
+    for (int i = i_lo; i < i_hi; ++i) groups[cached(i) ? i % cf : cf].push_back(i);
+    for (int gi = 0; gi <= cf; ++gi) {
+      const std::vector<int>& v = groups[gi];
+      const bool is_cached = gi < cf;
+      for (size_t a = 0; a < v.size();) {
+        size_t b = a + 1;
+        const int step = (b < v.size()) ? v[b] - v[a] : 1;
+        while (b < v.size() && v[b] - v[b - 1] == step && (int)(b - a) < Gmax_) ++b;
+        family(v[a], (int)(b - a), step, is_cached);
+        a = b;
+      }
     }
   }
   // lambda at the interior start lives on rank 0 (the last adjoint block)

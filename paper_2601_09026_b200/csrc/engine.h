@@ -178,6 +178,11 @@ class Engine {
     bool want_grads = false;
     float gscale = 0.f;
     Mat lam;     // adjoint: upstream state family
+    // adjoint: where the dgrad-chain intermediates (dh, dn2, da1, dqkv, dn1,
+    // ...) live -- null = backward scratch (slot g); the per-layer backward
+    // cache (slot = layer) when captured for the parameter pass
+    ActRef bact{nullptr, 0, 0, 1};
+    bool wgrad_only = false;  // intermediates already in bact: only form dW, db
   };
   void eval_forward(const EvalSpec& e);
   void eval_adjoint(const EvalSpec& e);
@@ -195,7 +200,7 @@ class Engine {
                      int sq, int skv);
   int gemm_blocks(const GemmArgs& g) const;
   Mat act_mat(const ActRef& r, long long off, int ld) const;
-  Mat bwd_mat(long long off, int ld) const;
+  Mat bwd_mat(const EvalSpec& e, long long off, int ld) const;
   Mat par(long long off, int ld, int layer0, int step) const;
   Mat par_hi(long long off, int ld, int layer0, int step) const;
   Mat par_lo(long long off, int ld, int layer0, int step) const;
@@ -236,7 +241,7 @@ class Engine {
   void correct_from(Solver& s, int level);
   void exact_solve(Solver& s, int level);
   void descend(Solver& s, int level);
-  void v_cycle(Solver& s, double tol);
+  void v_cycle(Solver& s, double tol, bool first);
   void solve(Solver& s, int iters, double tol);
   void alloc_solver(Solver& s, bool adjoint);
   void free_solver(Solver& s);
@@ -266,6 +271,8 @@ class Engine {
   float* scratch_ = nullptr;  // Gmax forward activation slots
   float* cache_ = nullptr;    // total_ forward activation slots (slot = layer)
   float* bscratch_ = nullptr; // Gmax backward slots
+  float* bcache_ = nullptr;   // total_ backward slots (slot = layer), for the parameter pass
+  std::vector<char> bcache_valid_;
   float* traj_ = nullptr;     // total_+1 states
   float* lam_all_ = nullptr;  // total_+1 states (serial adjoint)
   float* zero_state_ = nullptr;

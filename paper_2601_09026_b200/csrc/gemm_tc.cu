@@ -246,7 +246,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&conv[s], 4);  // one elected lane per converter warp
+      mbar_init(&conv[s], 1);  // the converter warp that owns the stage
       mbar_init(&empty[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
@@ -361,19 +361,22 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     __syncwarp();
   } else if (warp >= 4 && warp < 8) {
-    // ===== hi/lo split converters =====
-    const int ct = threadIdx.x - 128;  // 0..127
+    // ===== hi/lo split converters: converter warp c owns stage buffer c, so
+    // the stages convert concurrently and each warp waits its barrier's
+    // phases strictly in order (never a phase ahead) =====
+    const int c = warp - 4;
     int kg = 0;
     for (int t = blockIdx.x; t < total; t += gridDim.x) {
       for (int kb = 0; kb < nk; ++kb, ++kg) {
+        if (kg % STAGES != c) continue;  // one warp per stage buffer: phases in order
         const int s = kg % STAGES;
         const uint32_t ph = (kg / STAGES) & 1;
         mbar_wait(&full[s], ph);
         split_tile(reinterpret_cast<float*>(stage_a(s)), reinterpret_cast<float*>(stage_alo(s)),
-                   BM * BK, ct, 128, p.rawhi);
+                   BM * BK, lane, 32, p.rawhi);
         if (convert_b)
           split_tile(reinterpret_cast<float*>(stage_b(s)),
-                     reinterpret_cast<float*>(stage_blo(s)), BN * BK, ct, 128, p.rawhi);
+                     reinterpret_cast<float*>(stage_blo(s)), BN * BK, lane, 32, p.rawhi);
         // generic-proxy smem writes -> visible to the tensor core (async proxy)
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
@@ -559,11 +562,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&conv[s], 8);  // 4 converter warps x 2 CTAs (leader's is used)
+      mbar_init(&conv[s], 2);  // one converter warp per CTA (leader's is used)
       mbar_init(&empty[s], 1);
     }
     mbar_init(tfull, 1);
-    mbar_init(tempty, 16);  // 8 epilogue warps x 2 CTAs (leader's is used)
+    mbar_init(tempty, 2);  // one arrive per CTA (leader's is used)
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 2) {
@@ -667,22 +670,30 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
     }
     __syncwarp();
   } else if (warp >= 4 && warp < 8) {
-    // ===== hi/lo split converters (own halves), then tell the leader =====
-    const int ct = threadIdx.x - 128;
+    // ===== hi/lo split converters (own halves), then tell the leader. Warp c
+    // owns stage buffer c; the leader's converter arrives locally, the
+    // peer's with one cluster-scope release per stage =====
+    const int c = warp - 4;
     int kg = 0;
     for (int t = pair; t < total; t += npairs) {
       for (int kb = 0; kb < nk; ++kb, ++kg) {
+        if (kg % STAGES != c) continue;  // one warp per stage buffer: phases in order
         const int s = kg % STAGES;
         const uint32_t ph = (kg / STAGES) & 1;
         mbar_wait(&full[s], ph);
         split_tile(reinterpret_cast<float*>(stage_a(s)), reinterpret_cast<float*>(stage_alo(s)),
-                   128 * BK, ct, 128, p.rawhi);
+                   128 * BK, lane, 32, p.rawhi);
         if (convert_b)
           split_tile(reinterpret_cast<float*>(stage_b(s)),
-                     reinterpret_cast<float*>(stage_blo(s)), HB * BK, ct, 128, p.rawhi);
+                     reinterpret_cast<float*>(stage_blo(s)), HB * BK, lane, 32, p.rawhi);
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
-        if (lane == 0) mbar_arrive_cluster(conv_leader0 + s * 8);
+        if (lane == 0) {
+          if (leader)
+            mbar_arrive(&conv[s]);
+          else
+            mbar_arrive_cluster(conv_leader0 + s * 8);
+        }
       }
     }
   } else if (warp >= 8) {
@@ -715,8 +726,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
                     : epilogue_row(p.ep, T.g, T.b, T.h, row, col0, v, nvalid);
       }
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-      __syncwarp();
-      if (lane == 0) mbar_arrive_cluster(tempty_leader);
+      // all 8 epilogue warps done with TMEM -> one arrive per CTA
+      asm volatile("bar.sync 2, 256;" ::: "memory");
+      if (warp == 8 && lane == 0) {
+        if (leader)
+          mbar_arrive(tempty);
+        else
+          mbar_arrive_cluster(tempty_leader);
+      }
       if (res0) {
         // one partial per (128-row, 256-column) tile of this CTA
         for (int o = 16; o > 0; o >>= 1) r2 += __shfl_xor_sync(0xffffffffu, r2, o);
