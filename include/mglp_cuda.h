@@ -221,13 +221,20 @@ mglp_status mglp_rng_gaussian_fill(unsigned long long seed, unsigned long long a
 /* ---- test hook: one GEMM family on device buffers ----
  * C_g[M,N] = A_g . B_g^T (+ bias), g < G; A_g at A + g*a_slot (row stride
  * lda; [M,K] or, if a_mn, [K,M]); B likewise ([N,K] or [K,N]); C at
- * C + g*c_slot, row stride ldc. engine 0 = tcgen05 tf32x3 (the product
- * kernel), 1 = fp32 CUDA-core reference. b_presplit exercises the
- * pre-split (hi/lo) weight path of the tensor-core kernel. Synchronous. */
+ * C + g*c_slot, row stride ldc. engine 0 = tcgen05 fp16x3 split (the
+ * product kernel), 1 = fp32 CUDA-core reference. b_presplit exercises the
+ * pre-split (hi|lo) weight path of the tensor-core kernel. range_flag
+ * (nullable) receives 1 if a finite operand overflowed the fp16 split
+ * range. Synchronous. */
 mglp_status mglp_test_gemm(int G, int M, int N, int K, const float* A, long long a_slot, int lda,
                            int a_mn, const float* B, long long b_slot, int ldb, int b_mn,
                            int b_presplit, const float* bias, float* C, long long c_slot, int ldc,
-                           int engine);
+                           int engine, int* range_flag);
+
+/* ---- micro-benchmark: `reps` launches of one tensor-core GEMM family
+ * (EPI_STORE epilogue, device-resident synthetic operands), device-timed. */
+mglp_status mglp_bench_gemm(int G, int M, int N, int K, int a_mn, int b_mn, int b_presplit,
+                            int reps, float* ms_per_launch);
 
 #ifdef __cplusplus
 }

@@ -95,7 +95,9 @@ _SIGS = {
     "mglp_loopback_run_fwd_bwd": [C.POINTER(_vp), C.c_int, _vp, _vp, _vp, C.c_int],
     "mglp_test_gemm": [C.c_int, C.c_int, C.c_int, C.c_int, _vp, C.c_longlong, C.c_int, C.c_int,
                        _vp, C.c_longlong, C.c_int, C.c_int, C.c_int, _vp, _vp, C.c_longlong,
-                       C.c_int, C.c_int],
+                       C.c_int, C.c_int, _ip],
+    "mglp_bench_gemm": [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
+                        C.POINTER(C.c_float)],
 }
 
 EXPORTS = sorted(list(_SIGS) + ["mglp_last_error", "mglp_version"])

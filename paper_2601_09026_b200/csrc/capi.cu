@@ -671,7 +671,7 @@ mglp_status mglp_monitor_record(mglp_engine* e, double threshold, int policy_swi
 mglp_status mglp_test_gemm(int G, int M, int N, int K, const float* A, long long a_slot, int lda,
                            int a_mn, const float* B, long long b_slot, int ldb, int b_mn,
                            int b_presplit, const float* bias, float* Cp, long long c_slot, int ldc,
-                           int engine) {
+                           int engine, int* range_flag) {
   return guard([&] {
     need(A, "A");
     need(B, "B");
@@ -697,16 +697,18 @@ mglp_status mglp_test_gemm(int G, int M, int N, int K, const float* A, long long
       g.ep.bias.ptr = const_cast<float*>(bias);
       g.ep.bias.slot_stride = 0;
     }
-    float *hi = nullptr, *lo = nullptr;
+    float* hl = nullptr;
+    int* dflag = nullptr;
+    MGLP_CUDA(cudaMalloc(&dflag, sizeof(int)));
+    MGLP_CUDA(cudaMemset(dflag, 0, sizeof(int)));
+    g.range_flag = dflag;
     if (b_presplit && engine == 0) {
-      const long long rows = b_mn ? K : N;
-      const long long n = (long long)(G - 1) * b_slot + rows * ldb;
-      MGLP_CUDA(cudaMalloc(&hi, n * sizeof(float)));
-      MGLP_CUDA(cudaMalloc(&lo, n * sizeof(float)));
-      launch_split_tf32(hi, lo, B, n, 0);
-      g.B.ptr = hi;
-      g.Blo = g.B;
-      g.Blo.ptr = lo;
+      const long long kp = pack_hl_cols(K);
+      MGLP_CUDA(cudaMalloc(&hl, (size_t)G * N * kp * sizeof(float)));
+      launch_pack_hl(B, b_slot, ldb, hl, (long long)N * kp, (int)kp, G, N, K, b_mn != 0, 0);
+      g.Bhl.ptr = hl;
+      g.Bhl.slot_stride = (long long)N * kp;
+      g.Bhl.ld = (int)kp;
     }
     if (engine == 0)
       launch_gemm_tc(g, nullptr, 0);
@@ -714,8 +716,67 @@ mglp_status mglp_test_gemm(int G, int M, int N, int K, const float* A, long long
       launch_gemm_simt(g, nullptr, 0);
     MGLP_CUDA(cudaGetLastError());
     MGLP_CUDA(cudaDeviceSynchronize());
-    if (hi) cudaFree(hi);
-    if (lo) cudaFree(lo);
+    if (hl) cudaFree(hl);
+    int flag = 0;
+    MGLP_CUDA(cudaMemcpy(&flag, dflag, sizeof(int), cudaMemcpyDeviceToHost));
+    cudaFree(dflag);
+    if (range_flag) *range_flag = flag;
+  });
+}
+
+// ---- GEMM micro-benchmark (tools/gemm_bench.py) ----
+mglp_status mglp_bench_gemm(int G, int M, int N, int K, int a_mn, int b_mn, int b_presplit,
+                            int reps, float* ms_per_launch) {
+  return guard([&] {
+    float *A = nullptr, *B = nullptr, *Cm = nullptr, *hl = nullptr;
+    const long long na = (long long)G * M * K, nb = (long long)G * N * K,
+                    nc = (long long)G * M * N;
+    MGLP_CUDA(cudaMalloc(&A, na * sizeof(float)));
+    MGLP_CUDA(cudaMalloc(&B, nb * sizeof(float)));
+    MGLP_CUDA(cudaMalloc(&Cm, nc * sizeof(float)));
+    MGLP_CUDA(cudaMemset(A, 0x3c, na * sizeof(float)));
+    MGLP_CUDA(cudaMemset(B, 0x3c, nb * sizeof(float)));
+    GemmArgs g;
+    g.G = G;
+    g.M = M;
+    g.N = N;
+    g.K = K;
+    g.A.ptr = A;
+    g.A.slot_stride = (long long)M * K;
+    g.A.ld = a_mn ? M : K;
+    g.a_mn = a_mn != 0;
+    g.B.ptr = B;
+    g.B.slot_stride = (long long)N * K;
+    g.B.ld = b_mn ? N : K;
+    g.b_mn = b_mn != 0;
+    g.ep.kind = EPI_STORE;
+    g.ep.out1.ptr = Cm;
+    g.ep.out1.slot_stride = (long long)M * N;
+    g.ep.out1.ld = N;
+    if (b_presplit) {
+      const long long kp = pack_hl_cols(K);
+      MGLP_CUDA(cudaMalloc(&hl, (size_t)G * N * kp * sizeof(float)));
+      launch_pack_hl(B, g.B.slot_stride, g.B.ld, hl, (long long)N * kp, (int)kp, G, N, K,
+                     b_mn != 0, 0);
+      g.Bhl.ptr = hl;
+      g.Bhl.slot_stride = (long long)N * kp;
+      g.Bhl.ld = (int)kp;
+    }
+    cudaEvent_t e0, e1;
+    MGLP_CUDA(cudaEventCreate(&e0));
+    MGLP_CUDA(cudaEventCreate(&e1));
+    launch_gemm_tc(g, nullptr, 0);
+    MGLP_CUDA(cudaEventRecord(e0, 0));
+    for (int r = 0; r < reps; ++r) launch_gemm_tc(g, nullptr, 0);
+    MGLP_CUDA(cudaEventRecord(e1, 0));
+    MGLP_CUDA(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    MGLP_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    *ms_per_launch = ms / reps;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    for (float* p : {A, B, Cm, hl})
+      if (p) cudaFree(p);
   });
 }
 

@@ -299,9 +299,15 @@ struct GemmArgs {
   // each of the G members may itself be a Bb x H grid of per-(batch, head)
   // problems (attention); operands then use Mat::bstride / hstride
   int Bb = 1, H = 1;
-  Mat A, B, Blo;
+  // A, B: fp32 operands, [M][K] / [N][K] (K-major) or [K][M] / [K][N] (MN-major).
+  // Bhl (optional): B pre-split by launch_pack_hl into the fp16 hi|lo' form
+  // the tensor-core kernel stages (always K-major, [N][pad32(K)] in float
+  // units); when set, the tensor-core path reads it instead of B.
+  Mat A, B, Bhl;
   bool a_mn = false, b_mn = false;
   EpiArgs ep;
+  // set to 1 when a finite operand value overflows fp16 (|x| >= 65520)
+  int* range_flag = nullptr;
 };
 
 inline int ceil_div(long long a, long long b) { return (int)((a + b - 1) / b); }

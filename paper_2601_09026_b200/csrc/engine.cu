@@ -164,10 +164,13 @@ Engine::Engine(const StackDesc& sd, const SolveCfg& cfg, int device,
   build_layouts();
   const size_t pbytes = (size_t)total_ * layer_stride_ * sizeof(float);
   MGLP_CUDA(cudaMalloc(&P_, pbytes));
-  MGLP_CUDA(cudaMalloc(&Plo_, pbytes));
   MGLP_CUDA(cudaMalloc(&Gr_, pbytes));
+  const size_t hbytes = (size_t)total_ * hl_stride_ * sizeof(float);
+  MGLP_CUDA(cudaMalloc(&Whl_, hbytes));
+  MGLP_CUDA(cudaMalloc(&range_flag_, sizeof(int)));
   MGLP_CUDA(cudaMemsetAsync(P_, 0, pbytes, stream_));
-  MGLP_CUDA(cudaMemsetAsync(Plo_, 0, pbytes, stream_));
+  MGLP_CUDA(cudaMemsetAsync(Whl_, 0, hbytes, stream_));
+  MGLP_CUDA(cudaMemsetAsync(range_flag_, 0, sizeof(int), stream_));
   MGLP_CUDA(cudaMemsetAsync(Gr_, 0, pbytes, stream_));
   Gmax_ = std::max(1, N_ / cfg_.coarsen);
   cache_valid_.assign(total_, 0);
@@ -178,7 +181,8 @@ Engine::~Engine() {
   if (stream_) cudaStreamSynchronize(stream_);
   free_solver(fwd_);
   free_solver(bwd_);
-  for (float* p : {P_, Plo_, Gr_, scratch_, cache_, bscratch_, bcache_, traj_, lam_all_,
+  if (range_flag_) cudaFree(range_flag_);
+  for (float* p : {P_, Whl_, Gr_, scratch_, cache_, bscratch_, bcache_, traj_, lam_all_,
                    zero_state_, snap_fwd_, snap_bwd_})
     if (p) cudaFree(p);
   drop_graph();
@@ -254,8 +258,33 @@ void Engine::build_layouts() {
     piece(L.w_out, d * f);
     piece(L.b_out, d);
     L.flat_size = fo;
+    // pre-split copies of every weight matrix: [rows][pad32(cols)] and the
+    // transpose [cols][pad32(rows)]
+    long long ho = 0;
+    auto pack = [&](long long p_off, long long rows, long long cols) {
+      LayerLayout::WPack w;
+      w.p_off = p_off;
+      w.rows = (int)rows;
+      w.cols = (int)cols;
+      w.n_off = ho;
+      ho += rows * pack_hl_cols((int)cols);
+      w.t_off = ho;
+      ho += cols * pack_hl_cols((int)rows);
+      L.wpack.push_back(w);
+    };
+    pack(L.w_qkv, 3 * d, d);
+    pack(L.w_o, d, d);
+    if (L.decoder) {
+      pack(L.w_cq, d, d);
+      pack(L.w_ckv, 2 * d, d);
+      pack(L.w_co, d, d);
+    }
+    pack(L.w_in, f, d);
+    pack(L.w_out, d, f);
+    L.hl_size = ho;
   }
   layer_stride_ = std::max(lay_[0].size, sd_.kind == 2 ? lay_[1].size : 0LL);
+  hl_stride_ = std::max(lay_[0].hl_size, sd_.kind == 2 ? lay_[1].hl_size : 0LL);
   n_params_flat_ = 0;
   for (int l = 0; l < total_; ++l)
     n_params_flat_ += lay_[(sd_.kind == 2 && l >= n_split_) ? 1 : 0].flat_size;
@@ -332,7 +361,7 @@ void Engine::set_params(const double* flat) {
   MGLP_CUDA(cudaSetDevice(device_));
   const size_t n = host.size();
   MGLP_CUDA(cudaMemcpyAsync(P_, host.data(), n * sizeof(float), cudaMemcpyHostToDevice, stream_));
-  launch_split_tf32(nullptr, Plo_, P_, (long long)n, stream_);  // hi = raw (MMA truncates)
+  repack_weights();
   MGLP_CUDA(cudaStreamSynchronize(stream_));
 }
 
@@ -562,15 +591,42 @@ Mat Engine::par(long long off, int ld, int layer0, int step) const {
   m.step = step;
   return m;
 }
-Mat Engine::par_hi(long long off, int ld, int layer0, int step) const {
-  Mat m = par(off, ld, layer0, step);
-  m.ptr = P_ + off;  // the raw fp32 weights: the MMA reads them truncated to tf32
-  return m;
+Mat Engine::par_hl(const LayerLayout& L, long long off, int layer0, int step,
+                   bool transposed) const {
+  for (const LayerLayout::WPack& w : L.wpack) {
+    if (w.p_off != off) continue;
+    Mat m;
+    m.ptr = Whl_ + (transposed ? w.t_off : w.n_off);
+    m.slot_stride = hl_stride_;
+    m.ld = (int)pack_hl_cols(transposed ? w.rows : w.cols);
+    m.slot0 = layer0;
+    m.step = step;
+    return m;
+  }
+  throw ContractViolation("par_hl: no pre-split copy of the weight at this offset");
 }
-Mat Engine::par_lo(long long off, int ld, int layer0, int step) const {
-  Mat m = par(off, ld, layer0, step);
-  m.ptr = Plo_ + off;
-  return m;
+
+// Re-derive the pre-split weights from P_ (after every parameter change).
+void Engine::repack_weights() {
+  for (int kind = 0; kind < (sd_.kind == 2 ? 2 : 1); ++kind) {
+    const LayerLayout& L = lay_[kind];
+    // layers of this layout: [0, n_split_) encoders, [n_split_, total_) decoders
+    int l0 = 0, nl = total_;
+    if (sd_.kind == 2) {
+      l0 = kind == 0 ? 0 : n_split_;
+      nl = kind == 0 ? n_split_ : total_ - n_split_;
+    }
+    if (nl == 0) continue;
+    for (const LayerLayout::WPack& w : L.wpack) {
+      const float* src = P_ + (long long)l0 * layer_stride_ + w.p_off;
+      float* dn = Whl_ + (long long)l0 * hl_stride_ + w.n_off;
+      float* dt = Whl_ + (long long)l0 * hl_stride_ + w.t_off;
+      launch_pack_hl(src, layer_stride_, w.cols, dn, hl_stride_, (int)pack_hl_cols(w.cols), nl,
+                     w.rows, w.cols, false, stream_);
+      launch_pack_hl(src, layer_stride_, w.cols, dt, hl_stride_, (int)pack_hl_cols(w.rows), nl,
+                     w.cols, w.rows, true, stream_);
+    }
+  }
 }
 Mat Engine::grad(long long off, int ld, int layer0, int step) const {
   Mat m = par(off, ld, layer0, step);
@@ -582,6 +638,7 @@ void Engine::gemm(GemmArgs g) {
   ++launches_;
   const double flops = 2.0 * g.G * g.Bb * g.H * (double)g.M * g.N * g.K;
   prof_shape_ = {g.M, g.N, g.K, g.G * g.Bb * g.H};
+  g.range_flag = range_flag_;
   timed(PROF_GEMM, flops, 0.0, [&] {
 #ifdef MGLP_GEMM_SIMT
     launch_gemm_simt(g, active_, stream_);
@@ -838,8 +895,8 @@ void Engine::encoder_forward(const EvalSpec& e, int R, bool causal, Mat X, Mat Y
   g.N = 3 * d;
   g.K = d;
   g.A = n1;
-  g.B = par_hi(L.w_qkv, d, l0, ls);
-  g.Blo = par_lo(L.w_qkv, d, l0, ls);
+  g.B = par(L.w_qkv, d, l0, ls);
+  g.Bhl = par_hl(L, L.w_qkv, l0, ls, false);
   g.ep.kind = EPI_STORE;
   g.ep.out1 = qkv;
   g.ep.bias = par(L.b_qkv, 0, l0, ls);
@@ -853,8 +910,8 @@ void Engine::encoder_forward(const EvalSpec& e, int R, bool causal, Mat X, Mat Y
   g.N = d;
   g.K = d;
   g.A = ctx;
-  g.B = par_hi(L.w_o, d, l0, ls);
-  g.Blo = par_lo(L.w_o, d, l0, ls);
+  g.B = par(L.w_o, d, l0, ls);
+  g.Bhl = par_hl(L, L.w_o, l0, ls, false);
   g.ep.kind = EPI_BIAS_ADD2;
   g.ep.out1 = a1;
   g.ep.out2 = u;
@@ -877,8 +934,8 @@ void Engine::encoder_forward(const EvalSpec& e, int R, bool causal, Mat X, Mat Y
   g.N = f;
   g.K = d;
   g.A = n2;
-  g.B = par_hi(L.w_in, d, l0, ls);
-  g.Blo = par_lo(L.w_in, d, l0, ls);
+  g.B = par(L.w_in, d, l0, ls);
+  g.Bhl = par_hl(L, L.w_in, l0, ls, false);
   g.ep.kind = EPI_BIAS_GELU;
   g.ep.out1 = hh;
   g.ep.out2 = gg;
@@ -891,8 +948,8 @@ void Engine::encoder_forward(const EvalSpec& e, int R, bool causal, Mat X, Mat Y
   g.N = d;
   g.K = f;
   g.A = gg;
-  g.B = par_hi(L.w_out, f, l0, ls);
-  g.Blo = par_lo(L.w_out, f, l0, ls);
+  g.B = par(L.w_out, f, l0, ls);
+  g.Bhl = par_hl(L, L.w_out, l0, ls, false);
   g.ep.kind = EPI_FINAL;
   g.ep.add1 = a1;
   g.ep.bias = par(L.b_out, 0, l0, ls);
@@ -961,8 +1018,8 @@ void Engine::decoder_forward(const EvalSpec& e) {
     g.N = N;
     g.K = K;
     g.A = A;
-    g.B = par_hi(w, ldw, l0, ls);
-    g.Blo = par_lo(w, ldw, l0, ls);
+    g.B = par(w, ldw, l0, ls);
+    g.Bhl = par_hl(L, w, l0, ls, false);
     return g;
   };
   GemmArgs g = mk(R, 3 * d, d, n1, L.w_qkv, d);
@@ -1121,8 +1178,8 @@ void Engine::encoder_adjoint(const EvalSpec& e, bool causal) {
     g.N = N;
     g.K = K;
     g.A = A;
-    g.B = par_hi(w, ldw, l0, ls);
-    g.Blo = par_lo(w, ldw, l0, ls);
+    g.B = par(w, ldw, l0, ls);
+    g.Bhl = par_hl(L, w, l0, ls, true);
     g.b_mn = true;  // dX = U . W: W [out,in] read as [K,N]
     return g;
   };
@@ -1276,8 +1333,8 @@ void Engine::decoder_adjoint(const EvalSpec& e) {
     g.N = N;
     g.K = K;
     g.A = A;
-    g.B = par_hi(w, ldw, l0, ls);
-    g.Blo = par_lo(w, ldw, l0, ls);
+    g.B = par(w, ldw, l0, ls);
+    g.Bhl = par_hl(L, w, l0, ls, true);
     g.b_mn = true;
     return g;
   };
@@ -1871,9 +1928,16 @@ void Engine::drop_graph() {
 
 void Engine::read_trace(bool fwd, std::vector<double>* trace, bool* converged) {
   SolveCtrl c;
+  int range = 0;
   MGLP_CUDA(cudaMemcpyAsync(&c, fwd ? fwd_.ctrl : bwd_.ctrl, sizeof(SolveCtrl),
                             cudaMemcpyDeviceToHost, stream_));
+  MGLP_CUDA(cudaMemcpyAsync(&range, range_flag_, sizeof(int), cudaMemcpyDeviceToHost, stream_));
   MGLP_CUDA(cudaStreamSynchronize(stream_));
+  if (range) {
+    MGLP_CUDA(cudaMemsetAsync(range_flag_, 0, sizeof(int), stream_));
+    throw ContractViolation(
+        "a GEMM operand exceeded the fp16 range of the split tensor-core path (|x| >= 65520)");
+  }
   trace->assign(c.trace, c.trace + std::min(c.n_trace, kMaxTrace));
   *converged = c.converged != 0;
 }

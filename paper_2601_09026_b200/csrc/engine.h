@@ -145,6 +145,16 @@ class Engine {
     long long size = 0;
     std::vector<Piece> pieces;  // flat (visit_params) <-> device
     long long flat_size = 0;
+    // weight matrices in the pre-split hi|lo' form of the tensor-core GEMM
+    // (gemm_tc.cu): W [rows][cols] as a K-major B operand (forward, K = cols)
+    // and W^T (dgrad, K = rows), offsets within one layer of Whl_
+    struct WPack {
+      long long p_off;
+      int rows, cols;
+      long long n_off, t_off;
+    };
+    std::vector<WPack> wpack;
+    long long hl_size = 0;
   };
   void build_layouts();
 
@@ -202,8 +212,10 @@ class Engine {
   Mat act_mat(const ActRef& r, long long off, int ld) const;
   Mat bwd_mat(const EvalSpec& e, long long off, int ld) const;
   Mat par(long long off, int ld, int layer0, int step) const;
-  Mat par_hi(long long off, int ld, int layer0, int step) const;
-  Mat par_lo(long long off, int ld, int layer0, int step) const;
+  // pre-split weight W at P_ offset `off` of layout L as the GEMM B operand:
+  // forward (B = W, K = in) or, transposed, dgrad (B = W^T, K = out)
+  Mat par_hl(const LayerLayout& L, long long off, int layer0, int step, bool transposed) const;
+  void repack_weights();
   Mat grad(long long off, int ld, int layer0, int step) const;
 
   // ----- MGRIT solver (mgrit.hpp) -----
@@ -260,7 +272,9 @@ class Engine {
   long long layer_stride_ = 0;
   long long n_params_flat_ = 0;
   float* P_ = nullptr;     // fp32 params
-  float* Plo_ = nullptr;   // tf32 lo parts (x - trunc_tf32(x)); hi = the raw P_
+  float* Whl_ = nullptr;   // pre-split weights (LayerLayout::wpack), hl_stride_ floats per layer
+  long long hl_stride_ = 0;
+  int* range_flag_ = nullptr;  // device: a GEMM operand overflowed fp16 (gemm_tc.cu)
   float* Gr_ = nullptr;    // fp32 grads
   // shape
   int B_ = 0, sx_ = 0, sy_ = 0, Tx_ = 0, Ty_ = 0;

@@ -1,28 +1,43 @@
-// Parity-grade tensor-core GEMM for sm_100a: tcgen05.mma kind::tf32 with a
-// 3-pass hi/lo split (A_hi.B_hi + A_hi.B_lo + A_lo.B_hi, fp32 accumulation in
-// TMEM), the device counterpart of the reference's f64 matmul/linear
-// (tensor.cpp:173-237). Single-pass TF32 misses the 1e-4 parity tolerance at
-// depth 64; the split keeps ~21 mantissa bits.
+// Parity-grade tensor-core GEMM for sm_100a: tcgen05.mma kind::f16 over a
+// 3-pass fp16 hi/lo split with fp32 accumulation in TMEM, the device
+// counterpart of the reference's f64 matmul/linear (tensor.cpp:173-237).
 //
-// Structure (one 128 x BN output tile per CTA, 8 warps):
-//   warp 0      TMA producer: A (raw fp32), B_hi/B_lo (pre-split weights) or
-//               B raw, into a STAGES-deep smem ring (SWIZZLE_128B)
-//   warp 1      MMA issuer (one elected thread): 3 x (BK/8) tcgen05.mma per stage
+// Split ("fp16x3"): every fp32 operand value x becomes
+//     hi  = fp16_rn(x)                   (11 significant bits)
+//     lo' = fp16_rn((x - hi) * 2^11)     (the next 11 bits, pre-scaled so the
+//                                         residual stays a normal fp16)
+// and C = A_hi.B_hi + 2^-11 (A_lo'.B_hi + A_hi.B_lo'), the main product and
+// the correction products accumulating in separate TMEM accumulators (so the
+// small terms are not rounded against the large running sum). Per element the
+// representation error is <= 2^-22 |x| (plus 2^-35 absolute below the fp16
+// normal range): the same ~22-bit operand precision as a tf32x3 split, at the
+// fp16 tensor-core rate (2x tf32). Single-pass tensor-core GEMMs miss the
+// 1e-4 parity tolerance at depth 64. Finite values
+// |x| >= 65520 do not fit fp16: the converters raise GemmArgs::range_flag and
+// the engine reports it (no silent overflow).
+//
+// Structure (persistent; one CTA, or with cta_group::2 one CTA pair, per SM):
+//   warp 0      TMA producer: fp32 operand tiles -> staging ring
+//   warp 1      MMA issuer (one elected thread): 3 x 2 tcgen05.mma per 32-K stage
 //   warp 2      TMEM allocator
-//   warps 4-7   split converters (x -> hi = x & ~0x1fff, lo = x - hi, in smem)
-//               and then the fused epilogue: tcgen05.ld TMEM -> registers ->
-//               epilogue_row (bias / GELU / residual / MGRIT combine / grads)
-// Operands are 3-D TMA tensor maps [slot][rows][cols], so a whole family of G
-// problems (one per coarse interval or per layer) is one launch; member g
-// reads slot slot0 + g*step of each operand.
-// K-major operands load one [rows x 32] box per stage; MN-major operands
-// (weights read transposed in dgrad, activations in wgrad) load
-// [32 K-rows x 32 MN] boxes, matching the UMMA MN-major SWIZZLE_128B canonical
-// layout ((8,n),(8,k)):((1,LBO),(8,SBO)) with LBO = 4 KiB, SBO = 1 KiB.
+//   warp 3      TMA producer for a pre-split B (weights): hi|lo tiles straight
+//               into the MMA ring, no conversion
+//   warps 4-7   converters: staging (fp32, K- or MN-major) -> hi|lo fp16 tiles
+//               (always K-major SWIZZLE_128B: one 128-byte row = 32 hi + 32 lo')
+//   warps 8-    epilogue: tcgen05.ld TMEM -> registers -> epilogue_row (bias /
+//               GELU / residual / MGRIT combine / grads) -> global
+// The staging ring is released as soon as a stage is converted, so the next
+// TMA loads overlap both the conversion and the MMAs of earlier stages.
+// Operands are 5-D TMA tensor maps [slot][batch][head][rows][cols] (sorted by
+// stride), so a whole family of G problems (one per coarse interval or per
+// layer, each possibly a grid of per-(batch, head) attention problems) is one
+// launch; member g reads slot slot0 + g*step of each operand.
 #include <cuda.h>
+#include <cuda_fp16.h>
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cfloat>
 #include <cstdlib>
 #include <mutex>
 
@@ -32,16 +47,20 @@ namespace mglp {
 
 namespace {
 
-constexpr int BM = 128;
-constexpr int BK = 32;  // fp32 elements per stage = one 128-byte swizzle span
-constexpr int kThreads = 384;  // producer, MMA, TMEM, idle, 4 converters, 4 epilogue
+constexpr int BK = 32;          // K elements per stage (one 128-byte fp32 row span)
+constexpr int ROWS = 128;       // operand rows per CTA per stage (A and B)
+constexpr int STAGES = 3;
+constexpr int TILE_BYTES = ROWS * BK * 4;  // 16 KiB: fp32 staging tile == hi|lo tile
+constexpr int STAGE_BYTES = 4 * TILE_BYTES;  // stgA, stgB, hlA, hlB
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 512 /*barriers*/;
+constexpr int BSLOTS = 2 * STAGES;  // ring depth of a pre-split B
+constexpr float kLoScale = 2048.f, kLoInv = 1.f / 2048.f;
 
 struct TcOperand {
   int slot0, step;  // normalized slot coordinates (member g -> slot0 + g*step)
-  int mn;           // 1 = MN-major
   // positions of the (row, head, batch, slot) coordinates in the 5-D tensor
-  // map (dimension 0 is always the contiguous 32-wide column box); unused
-  // head / batch dimensions have extent 1 and coordinate 0
+  // map (dimension 0 is always the contiguous column box); unused head /
+  // batch dimensions have extent 1 and coordinate 0
   int pos_row, pos_h, pos_b, pos_slot;
   int use_h, use_b;
 };
@@ -49,11 +68,13 @@ struct TcOperand {
 struct TcParams {
   int G, M, N, K;
   int Bb, H;
-  TcOperand a, b, blo;
-  int b_presplit;
-  int passes;  // 3 = hi.hi + (lo.hi + hi.lo); 1 = hi.hi only (diagnostics)
-  int rawhi;   // feed raw x as the hi operand (the MMA truncates); 0 = write masked hi
-  int vec_ok;  // every epilogue operand row start is 16-byte aligned
+  TcOperand a, b;
+  int a_mn, b_mn;  // staging layout of the converted operands
+  int b_direct;    // B comes pre-split (hi|lo tiles TMA'd straight into the MMA ring)
+  int passes;      // 3 = hi.hi + (lo.hi + hi.lo); 1 = hi.hi only (diagnostics)
+  int vec_ok;      // every epilogue operand row start is 16-byte aligned
+  int* range_flag;
+  int debug;  // MGLP_DEBUG_GEMM bits (timing diagnostics only): 1 skip conversion, 2 skip epilogue stores
   EpiArgs ep;
 };
 
@@ -108,42 +129,62 @@ __device__ __forceinline__ void tma_coords(const TcOperand& op, int col, int row
   c[op.pos_slot] = op.slot0 + g * op.step;
 }
 
-// UMMA shared-memory descriptor. K-major operands use SWIZZLE_128B (layout
-// type 2); MN-major tf32 operands must use SWIZZLE_128B_BASE32B (type 1,
-// 32-byte granules over 4 rows -- the only MN-major layout tf32 supports,
-// matched by TMA's CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B).
-__device__ __forceinline__ uint64_t smem_desc(const void* p, uint32_t lbo, uint32_t sbo,
-                                              uint32_t layout) {
+// UMMA shared-memory descriptor, K-major SWIZZLE_128B (layout type 2): 8-row
+// core groups 1024 B apart (SBO); the K offset inside the 128-byte swizzle
+// span is added to the start address (+32 B per K=16 fp16 step).
+__device__ __forceinline__ uint64_t smem_desc_sw128(const void* p) {
   const uint64_t addr = smem_u32(p);
   uint64_t d = 0;
   d |= (addr >> 4) & 0x3FFFull;
-  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
-  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
-  d |= 1ull << 46;  // sm100 descriptor version
-  d |= (uint64_t)layout << 61;
+  d |= (uint64_t)(16 >> 4) << 16;    // LBO (unused for swizzled K-major)
+  d |= (uint64_t)(1024 >> 4) << 32;  // SBO
+  d |= 1ull << 46;                   // sm100 descriptor version
+  d |= 2ull << 61;                   // SWIZZLE_128B
   return d;
 }
 
-__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t da, uint64_t db,
-                                         uint32_t idesc, uint32_t accumulate) {
-  asm volatile(
-      "{\n\t"
-      ".reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t"
-      "}" ::"r"(tmem_d),
-      "l"(da), "l"(db), "r"(idesc), "r"(accumulate));
+template <int CG>
+__device__ __forceinline__ void mma_f16(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc,
+                                        uint32_t accumulate) {
+  if constexpr (CG == 1) {
+    asm volatile(
+        "{\n\t"
+        ".reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t"
+        "}" ::"r"(tmem_d),
+        "l"(da), "l"(db), "r"(idesc), "r"(accumulate));
+  } else {
+    asm volatile(
+        "{\n\t"
+        ".reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t"
+        "}" ::"r"(tmem_d),
+        "l"(da), "l"(db), "r"(idesc), "r"(accumulate));
+  }
 }
 
+template <int CG>
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
-  asm volatile(
-      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-          smem_u32(bar))
-      : "memory");
+  if constexpr (CG == 1) {
+    asm volatile(
+        "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+            smem_u32(bar))
+        : "memory");
+  } else {
+    // arrive on the barrier at this offset in BOTH CTAs of the pair
+    const uint16_t mask = 0x3;
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster."
+        "b64 [%0], %1;" ::"r"(smem_u32(bar)),
+        "h"(mask)
+        : "memory");
+  }
 }
 
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
-  uint32_t r[16];
+// 32 lanes x 16 columns of fp32 from TMEM; pair with tmem_wait()
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t* r) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
       "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
@@ -151,302 +192,11 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
         "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
         "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
       : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait() {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
-// x -> (hi, lo): hi keeps the top 10 explicit mantissa bits (exactly a tf32),
-// lo = x - hi exactly; the tensor core then sees hi exactly and lo to ~11 bits.
-// kind::tf32 MMAs read an fp32 operand by truncating its low 13 mantissa
-// bits (measured: raw x and its masked copy give bitwise-identical products,
-// tests/test_gemm.py::test_tf32_operand_truncation), so by default only lo is
-// written and the raw tile serves as hi -- one smem store pass fewer per stage.
-__device__ __forceinline__ void split_tile(float* raw, float* lo, int nfloat, int tid,
-                                           int nthreads, int rawhi) {
-  float4* r4 = reinterpret_cast<float4*>(raw);
-  float4* l4 = reinterpret_cast<float4*>(lo);
-  for (int i = tid; i < nfloat / 4; i += nthreads) {
-    float4 x = r4[i];
-    float4 h, l;
-    h.x = __uint_as_float(__float_as_uint(x.x) & 0xFFFFE000u);
-    h.y = __uint_as_float(__float_as_uint(x.y) & 0xFFFFE000u);
-    h.z = __uint_as_float(__float_as_uint(x.z) & 0xFFFFE000u);
-    h.w = __uint_as_float(__float_as_uint(x.w) & 0xFFFFE000u);
-    l.x = x.x - h.x;
-    l.y = x.y - h.y;
-    l.z = x.z - h.z;
-    l.w = x.w - h.w;
-    if (!rawhi) r4[i] = h;  // rawhi: leave x in place, the MMA reads it as tf32
-    l4[i] = l;
-  }
-}
-
-template <int BN, int STAGES>
-struct Smem {
-  static constexpr int A_BYTES = BM * BK * 4;
-  static constexpr int B_BYTES = BN * BK * 4;
-  static constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;  // A, A_lo, B_hi, B_lo
-  static constexpr int BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 512 /*barriers*/;
-};
-
-// Persistent: each CTA walks tiles blockIdx.x, +gridDim.x, ... of the whole
-// family (problem-major, then M, then N so an A row-block is reused while hot
-// in L2). Two TMEM accumulator buffers (each = main + correction, 2*BN
-// columns) let the epilogue of tile t overlap the MMAs of tile t+1.
-template <int BN, int STAGES>
-__global__ void __launch_bounds__(kThreads, 1)
-    gemm_tc_kernel(const __grid_constant__ CUtensorMap mapA,
-                   const __grid_constant__ CUtensorMap mapB,
-                   const __grid_constant__ CUtensorMap mapBlo, const TcParams p,
-                   const int* active) {
-  using S = Smem<BN, STAGES>;
-  extern __shared__ uint8_t smem_raw[];
-  if (active && *(volatile const int*)active == 0) return;
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * S::STAGE_BYTES);
-  uint64_t* conv = full + STAGES;
-  uint64_t* empty = conv + STAGES;
-  uint64_t* tfull = empty + STAGES;   // [2]
-  uint64_t* tempty = tfull + 2;       // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-  double* red = reinterpret_cast<double*>(tmem_slot + 2);  // [2][4]
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nk = (p.K + BK - 1) / BK;
-  const bool convert_b = !p.b_presplit;
-  const int tiles_n = (p.N + BN - 1) / BN, tiles_m = (p.M + BM - 1) / BM;
-  const int per_prob = tiles_n * tiles_m;
-  const int total = per_prob * p.G * p.Bb * p.H;
-
-  auto stage_a = [&](int s) { return smem + s * S::STAGE_BYTES; };
-  auto stage_alo = [&](int s) { return smem + s * S::STAGE_BYTES + S::A_BYTES; };
-  auto stage_b = [&](int s) { return smem + s * S::STAGE_BYTES + 2 * S::A_BYTES; };
-  auto stage_blo = [&](int s) {
-    return smem + s * S::STAGE_BYTES + 2 * S::A_BYTES + S::B_BYTES;
-  };
-  struct Tile {
-    int z, g, b, h, m0, n0, mt, nt;
-  };
-  auto tile_of = [&](int t) {
-    Tile T;
-    T.z = t / per_prob;
-    const int r = t % per_prob;
-    T.mt = r / tiles_n;
-    T.nt = r % tiles_n;
-    T.h = T.z % p.H;
-    T.b = (T.z / p.H) % p.Bb;
-    T.g = T.z / (p.H * p.Bb);
-    T.m0 = T.mt * BM;
-    T.n0 = T.nt * BN;
-    return T;
-  };
-
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&conv[s], 1);  // the converter warp that owns the stage
-      mbar_init(&empty[s], 1);
-    }
-    for (int a = 0; a < 2; ++a) {
-      mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 4);  // one elected lane per epilogue warp
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  if (warp == 2) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                     smem_u32(tmem_slot)),
-                 "r"((uint32_t)(4 * BN)));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-  }
-  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  __syncthreads();
-  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  const uint32_t tmem_base = *tmem_slot;
-
-  if (warp == 0) {
-    // ===== TMA producer =====
-    if (lane == 0) {
-      const uint32_t bytes = S::A_BYTES + S::B_BYTES + (convert_b ? 0 : S::B_BYTES);
-      int kg = 0;
-      for (int t = blockIdx.x; t < total; t += gridDim.x) {
-        const Tile T = tile_of(t);
-        for (int kb = 0; kb < nk; ++kb, ++kg) {
-          const int s = kg % STAGES;
-          const uint32_t ph = (kg / STAGES) & 1;
-          mbar_wait(&empty[s], ph ^ 1);
-          mbar_expect_tx(&full[s], bytes);
-          const int k0 = kb * BK;
-          int c[5];
-          if (!p.a.mn) {
-            tma_coords(p.a, k0, T.m0, T.g, T.b, T.h, c);
-            tma_load_5d(stage_a(s), &mapA, &full[s], c);
-          } else {
-#pragma unroll
-            for (int i = 0; i < BM / 32; ++i) {
-              tma_coords(p.a, T.m0 + 32 * i, k0, T.g, T.b, T.h, c);
-              tma_load_5d(stage_a(s) + i * 4096, &mapA, &full[s], c);
-            }
-          }
-          if (!p.b.mn) {
-            tma_coords(p.b, k0, T.n0, T.g, T.b, T.h, c);
-            tma_load_5d(stage_b(s), &mapB, &full[s], c);
-            if (!convert_b) {
-              tma_coords(p.blo, k0, T.n0, T.g, T.b, T.h, c);
-              tma_load_5d(stage_blo(s), &mapBlo, &full[s], c);
-            }
-          } else {
-#pragma unroll
-            for (int i = 0; i < BN / 32; ++i) {
-              tma_coords(p.b, T.n0 + 32 * i, k0, T.g, T.b, T.h, c);
-              tma_load_5d(stage_b(s) + i * 4096, &mapB, &full[s], c);
-              if (!convert_b) {
-                tma_coords(p.blo, T.n0 + 32 * i, k0, T.g, T.b, T.h, c);
-                tma_load_5d(stage_blo(s) + i * 4096, &mapBlo, &full[s], c);
-              }
-            }
-          }
-        }
-      }
-    }
-    __syncwarp();
-  } else if (warp == 1) {
-    // ===== MMA issuer (one thread) =====
-    if (lane == 0) {
-      // instruction descriptor: D f32, A/B tf32, majors, N, M
-      const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)p.a.mn << 15) |
-                             ((uint32_t)p.b.mn << 16) | ((uint32_t)(BN >> 3) << 17) |
-                             ((uint32_t)(BM >> 4) << 24);
-      // MN-major: LBO = stride between 32-element MN blocks (one 32-row TMA
-      // box), SBO = stride between 4-row K groups of the BASE32B atom
-      const uint32_t a_lbo = p.a.mn ? 4096u : 16u, a_sbo = p.a.mn ? 512u : 1024u;
-      const uint32_t b_lbo = p.b.mn ? 4096u : 16u, b_sbo = p.b.mn ? 512u : 1024u;
-      const uint32_t a_lay = p.a.mn ? 1u : 2u, b_lay = p.b.mn ? 1u : 2u;
-      const uint32_t a_kstep = p.a.mn ? 1024u : 32u;  // bytes per K=8 step
-      const uint32_t b_kstep = p.b.mn ? 1024u : 32u;
-      int kg = 0, tc = 0;
-      for (int t = blockIdx.x; t < total; t += gridDim.x, ++tc) {
-        const int acc = tc & 1;
-        const uint32_t aph = (tc >> 1) & 1;
-        mbar_wait(&tempty[acc], aph ^ 1);
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint32_t tm = tmem_base + (uint32_t)(acc * 2 * BN);
-        for (int kb = 0; kb < nk; ++kb, ++kg) {
-          const int s = kg % STAGES;
-          const uint32_t ph = (kg / STAGES) & 1;
-          mbar_wait(&conv[s], ph);
-          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-#pragma unroll
-          for (int k = 0; k < BK / 8; ++k) {
-            const uint64_t dah = smem_desc(stage_a(s) + k * a_kstep, a_lbo, a_sbo, a_lay);
-            const uint64_t dal = smem_desc(stage_alo(s) + k * a_kstep, a_lbo, a_sbo, a_lay);
-            const uint64_t dbh = smem_desc(stage_b(s) + k * b_kstep, b_lbo, b_sbo, b_lay);
-            const uint64_t dbl = smem_desc(stage_blo(s) + k * b_kstep, b_lbo, b_sbo, b_lay);
-            const uint32_t acc0 = (kb > 0 || k > 0) ? 1u : 0u;
-            // main product and the two correction products accumulate in
-            // separate TMEM accumulators, so the small terms are not rounded
-            // against the large running sum
-            mma_tf32(tm, dah, dbh, idesc, acc0);
-            if (p.passes > 1) {
-              mma_tf32(tm + BN, dal, dbh, idesc, acc0);
-              mma_tf32(tm + BN, dah, dbl, idesc, 1u);
-            }
-          }
-          mma_commit(&empty[s]);
-        }
-        mma_commit(&tfull[acc]);
-      }
-    }
-    __syncwarp();
-  } else if (warp >= 4 && warp < 8) {
-    // ===== hi/lo split converters: converter warp c owns stage buffer c, so
-    // the stages convert concurrently and each warp waits its barrier's
-    // phases strictly in order (never a phase ahead) =====
-    const int c = warp - 4;
-    int kg = 0;
-    for (int t = blockIdx.x; t < total; t += gridDim.x) {
-      for (int kb = 0; kb < nk; ++kb, ++kg) {
-        if (kg % STAGES != c) continue;  // one warp per stage buffer: phases in order
-        const int s = kg % STAGES;
-        const uint32_t ph = (kg / STAGES) & 1;
-        mbar_wait(&full[s], ph);
-        split_tile(reinterpret_cast<float*>(stage_a(s)), reinterpret_cast<float*>(stage_alo(s)),
-                   BM * BK, lane, 32, p.rawhi);
-        if (convert_b)
-          split_tile(reinterpret_cast<float*>(stage_b(s)),
-                     reinterpret_cast<float*>(stage_blo(s)), BN * BK, lane, 32, p.rawhi);
-        // generic-proxy smem writes -> visible to the tensor core (async proxy)
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&conv[s]);
-      }
-    }
-  } else if (warp >= 8) {
-    // ===== epilogue: TMEM -> registers -> fused epilogue -> global =====
-    const int q = warp & 3;
-    const bool res0 = p.ep.kind == EPI_FINAL && p.ep.cmb.mode == CM_RES0;
-    int tc = 0;
-    for (int t = blockIdx.x; t < total; t += gridDim.x, ++tc) {
-      const Tile T = tile_of(t);
-      const int acc = tc & 1;
-      const uint32_t aph = (tc >> 1) & 1;
-      mbar_wait(&tfull[acc], aph);
-      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const int row = T.m0 + q * 32 + lane;
-      const uint32_t lane_addr =
-          tmem_base + (uint32_t)(acc * 2 * BN) + ((uint32_t)(q * 32) << 16);
-      double r2 = 0.0;
-#pragma unroll 1
-      for (int c = 0; c < BN; c += 16) {
-        float v[16];
-        tmem_ld16(lane_addr + c, v);
-        if (p.passes > 1) {
-          float w[16];
-          tmem_ld16(lane_addr + BN + c, w);
-#pragma unroll
-          for (int i = 0; i < 16; ++i) v[i] += w[i];
-        }
-        const int col0 = T.n0 + c;
-        const int nvalid = min(16, p.N - col0);
-        if (row < p.M && nvalid > 0)
-          r2 += (nvalid == 16 && p.vec_ok)
-                    ? epilogue_row16(p.ep, T.g, T.b, T.h, row, col0, v)
-                    : epilogue_row(p.ep, T.g, T.b, T.h, row, col0, v, nvalid);
-      }
-      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[acc]);
-      if (res0) {
-        for (int o = 16; o > 0; o >>= 1) r2 += __shfl_xor_sync(0xffffffffu, r2, o);
-        if (lane == 0) red[acc * 4 + q] = r2;
-        asm volatile("bar.sync 1, 128;" ::: "memory");
-        if (q == 0 && lane == 0) {
-          const double tsum = red[acc * 4 + 0] + red[acc * 4 + 1] + red[acc * 4 + 2] +
-                              red[acc * 4 + 3];
-          p.ep.cmb.norm_partials[p.ep.cmb.norm_base + T.z * p.ep.cmb.norm_member_stride +
-                                 T.mt * tiles_n + T.nt] = tsum;
-        }
-      }
-    }
-  }
-  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  __syncthreads();
-  if (warp == 2)
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
-                 "r"((uint32_t)(4 * BN)));
-}
-
-// ---- cta_group::2: a CTA pair computes one 256 x 256 tile --------------------
-// Each CTA of the pair holds half of A (128 rows) and half of B (128 of the
-// 256 columns) in its own smem; the leader CTA issues M=256 N=256 MMAs that
-// read both halves, and each CTA's TMEM receives its 128 rows x 256 columns.
-// Per SM this halves the B operand traffic through shared memory relative
-// to a 1-CTA 128x256 tile -- the 3-pass split makes these kernels shared-
-// memory-bandwidth bound, so this is the lever. TMEM (512 columns) holds one
-// main + one correction accumulator; 8 epilogue warps drain it quickly while
-// the producer and converters already stage the next tile.
 __device__ __forceinline__ uint32_t cluster_rank() {
   uint32_t r;
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
@@ -469,78 +219,140 @@ __device__ __forceinline__ void cluster_sync() {
                ::: "memory");
 }
 
-__device__ __forceinline__ void mma_tf32_pair(uint32_t tmem_d, uint64_t da, uint64_t db,
-                                              uint32_t idesc, uint32_t accumulate) {
-  asm volatile(
-      "{\n\t"
-      ".reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t"
-      "}" ::"r"(tmem_d),
-      "l"(da), "l"(db), "r"(idesc), "r"(accumulate));
+__device__ __forceinline__ float4 lds128(uint32_t a) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(a));
+  return v;
+}
+__device__ __forceinline__ float lds32(uint32_t a) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts128(uint32_t a, uint4 v) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(v.x), "r"(v.y), "r"(v.z),
+               "r"(v.w)
+               : "memory");
 }
 
-__device__ __forceinline__ void mma_commit_pair(uint64_t* bar) {
-  // arrive on the barrier at this offset in BOTH CTAs of the pair
-  const uint16_t mask = 0x3;
-  asm volatile(
-      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
-      " [%0], %1;" ::"r"(smem_u32(bar)),
-      "h"(mask)
-      : "memory");
+// ---- the split ------------------------------------------------------------------
+// 8 consecutive K values -> one 16-byte hi chunk and one 16-byte lo' chunk
+__device__ __forceinline__ void split8(const float* x, uint4& hi, uint4& lo, float& amax) {
+  uint32_t h[4], l[4];
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const __half2 hh = __floats2half2_rn(x[2 * e], x[2 * e + 1]);
+    const float2 hf = __half22float2(hh);
+    // x - hf is exact (hf is x rounded to 11 bits); the 2^11 scale is exact
+    const __half2 ll = __floats2half2_rn((x[2 * e] - hf.x) * kLoScale,
+                                         (x[2 * e + 1] - hf.y) * kLoScale);
+    h[e] = *reinterpret_cast<const uint32_t*>(&hh);
+    l[e] = *reinterpret_cast<const uint32_t*>(&ll);
+    amax = fmaxf(amax, fmaxf(fabsf(x[2 * e]), fabsf(x[2 * e + 1])));
+  }
+  hi = make_uint4(h[0], h[1], h[2], h[3]);
+  lo = make_uint4(l[0], l[1], l[2], l[3]);
 }
 
-constexpr int P_BM = 256;   // pair tile rows (128 per CTA)
-constexpr int P_BN = 256;   // pair tile columns (128 per CTA in smem)
-constexpr int P_STAGES = 3;
-constexpr int kThreads2 = 512;  // 0 TMA, 1 MMA, 2 TMEM, 3 idle, 4-7 convert, 8-15 epilogue
+// One 128-row operand tile: fp32 staging -> K-major SW128 hi|lo tile (row r =
+// [32 hi | 32 lo'] in 16-byte chunks at r*128 + ((chunk ^ (r & 7)) << 4)).
+// Staging is either K-major SWIZZLE_128B ([128 rows][32 K]) or MN-major dense
+// ([32 K][128 rows]). Converter warp c (of 4) handles K chunk kc = c (8
+// values) of every row, lane = row within a 32-row block: all shared-memory
+// accesses are bank-conflict free.
+__device__ __forceinline__ void convert_tile(uint32_t stg, uint32_t hl, bool mn, int kc,
+                                             int lane, float& amax) {
+  // all staging loads first (the compiler cannot reorder them across the
+  // hi|lo stores, which it cannot prove disjoint): 4 independent rows in flight
+  float x[ROWS / 32][8];
+#pragma unroll
+  for (int rb = 0; rb < ROWS / 32; ++rb) {
+    const int r = rb * 32 + lane;
+    if (!mn) {
+      const uint32_t row = stg + r * 128;
+      const float4 u = lds128(row + (((2 * kc) ^ (r & 7)) << 4));
+      const float4 v = lds128(row + (((2 * kc + 1) ^ (r & 7)) << 4));
+      x[rb][0] = u.x; x[rb][1] = u.y; x[rb][2] = u.z; x[rb][3] = u.w;
+      x[rb][4] = v.x; x[rb][5] = v.y; x[rb][6] = v.z; x[rb][7] = v.w;
+    } else {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) x[rb][e] = lds32(stg + ((kc * 8 + e) * ROWS + r) * 4);
+    }
+  }
+#pragma unroll
+  for (int rb = 0; rb < ROWS / 32; ++rb) {
+    const int r = rb * 32 + lane;
+    uint4 hi, lo;
+    split8(x[rb], hi, lo, amax);
+    const uint32_t orow = hl + r * 128;
+    sts128(orow + ((kc ^ (r & 7)) << 4), hi);
+    sts128(orow + (((4 + kc) ^ (r & 7)) << 4), lo);
+  }
+}
 
-struct Smem2 {
-  static constexpr int A_BYTES = 128 * BK * 4;
-  static constexpr int B_BYTES = (P_BN / 2) * BK * 4;
-  static constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;
-  static constexpr int BYTES = P_STAGES * STAGE_BYTES + 1024 + 512;
+// ---- the kernel -------------------------------------------------------------------
+// CG = 1: one CTA computes a 128 x 128 tile; two TMEM accumulator buffers
+//         (each main + correction, 256 columns) let the epilogue of tile t
+//         overlap the MMAs of tile t+1.
+// CG = 2: a CTA pair computes a 256 x 256 tile with cta_group::2 MMAs issued
+//         by the leader: each CTA holds its 128 rows of A and 128 of the 256
+//         B rows; per SM the B operand traffic through shared memory halves.
+//         TMEM (512 columns) holds one main + one correction accumulator.
+template <int CG>
+struct Cfg {
+  static constexpr int TM = 128 * CG;     // tile rows
+  static constexpr int TN = 128 * CG;     // tile columns
+  static constexpr int NACC = CG == 1 ? 2 : 1;  // TMEM accumulator buffers
+  static constexpr int EPI_WARPS = 4 * CG;
+  static constexpr int THREADS = 32 * (8 + EPI_WARPS);
 };
 
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
-    gemm_tc2_kernel(const __grid_constant__ CUtensorMap mapA,
-                    const __grid_constant__ CUtensorMap mapB,
-                    const __grid_constant__ CUtensorMap mapBlo, const TcParams p,
-                    const int* active) {
-  using S = Smem2;
-  constexpr int STAGES = P_STAGES;
-  constexpr int HB = P_BN / 2;  // B rows held per CTA
+template <int CG>
+__global__ void __launch_bounds__(Cfg<CG>::THREADS, 1)
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap mapA,
+                   const __grid_constant__ CUtensorMap mapB, const TcParams p,
+                   const int* active) {
+  using C = Cfg<CG>;
+  constexpr int TN = C::TN, NACC = C::NACC;
   extern __shared__ uint8_t smem_raw[];
-  // the early exit is uniform over the cluster (same flag), so no CTA is left
+  // the early exit is uniform over a cluster (same flag): no CTA is left
   // waiting on its peer
   if (active && *(volatile const int*)active == 0) return;
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * S::STAGE_BYTES);
-  uint64_t* conv = full + STAGES;
+  uint64_t* fullA = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  uint64_t* fullB = fullA + STAGES;    // [BSLOTS]
+  uint64_t* emptyB = fullB + BSLOTS;   // [BSLOTS]
+  uint64_t* sfree = emptyB + BSLOTS;
+  uint64_t* conv = sfree + STAGES;
   uint64_t* empty = conv + STAGES;
-  uint64_t* tfull = empty + STAGES;
-  uint64_t* tempty = tfull + 1;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
-  double* red = reinterpret_cast<double*>(tmem_slot + 2);  // [8]
+  uint64_t* cdone = empty + STAGES;  // CG = 2, follower CTA: converters -> signaler
+  uint64_t* tfull = cdone + STAGES;   // [NACC]
+  uint64_t* tempty = tfull + NACC;    // [NACC]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + NACC);
+  double* red = reinterpret_cast<double*>(tmem_slot + 2);  // [NACC][EPI_WARPS]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t cr = cluster_rank();
+  const uint32_t cr = CG == 2 ? cluster_rank() : 0;
   const bool leader = cr == 0;
-  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+  const int unit = CG == 2 ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
+  const int nunits = CG == 2 ? (int)(gridDim.x >> 1) : (int)gridDim.x;
   const int nk = (p.K + BK - 1) / BK;
-  const bool convert_b = !p.b_presplit;
-  const int tiles_n = (p.N + P_BN - 1) / P_BN, tiles_m2 = (p.M + P_BM - 1) / P_BM;
+  const int tiles_n = (p.N + TN - 1) / TN, tiles_m = (p.M + C::TM - 1) / C::TM;
   const int tiles_m128 = (p.M + 127) / 128;
-  const int per_prob = tiles_n * tiles_m2;
+  const int per_prob = tiles_n * tiles_m;
   const int total = per_prob * p.G * p.Bb * p.H;
 
-  auto stage_a = [&](int s) { return smem + s * S::STAGE_BYTES; };
-  auto stage_alo = [&](int s) { return smem + s * S::STAGE_BYTES + S::A_BYTES; };
-  auto stage_b = [&](int s) { return smem + s * S::STAGE_BYTES + 2 * S::A_BYTES; };
-  auto stage_blo = [&](int s) {
-    return smem + s * S::STAGE_BYTES + 2 * S::A_BYTES + S::B_BYTES;
-  };
+  auto stg_a = [&](int s) { return smem + s * STAGE_BYTES; };
+  auto stg_b = [&](int s) { return smem + s * STAGE_BYTES + TILE_BYTES; };
+  auto hl_a = [&](int s) { return smem + s * STAGE_BYTES + 2 * TILE_BYTES; };
+  auto hl_b = [&](int s) { return smem + s * STAGE_BYTES + 3 * TILE_BYTES; };
+  // a pre-split B has no staging: its ring takes both B buffers of every
+  // stage (BSLOTS = 2 x STAGES deep), so weight tiles stream in far ahead of
+  // the MMAs and their TMA latency stays hidden
+  auto b_slot = [&](int j) { return j < STAGES ? hl_b(j) : stg_b(j - STAGES); };
   struct Tile {
     int z, g, b, h, m0, n0, mt, nt;
   };
@@ -548,223 +360,291 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
     Tile T;
     T.z = t / per_prob;
     const int r = t % per_prob;
-    const int mt2 = r / tiles_n;
     T.nt = r % tiles_n;
     T.h = T.z % p.H;
     T.b = (T.z / p.H) % p.Bb;
     T.g = T.z / (p.H * p.Bb);
-    T.mt = mt2 * 2 + (int)cr;  // this CTA's 128-row tile
+    T.mt = (r / tiles_n) * CG + (int)cr;  // this CTA's 128-row tile
     T.m0 = T.mt * 128;
-    T.n0 = T.nt * P_BN;
+    T.n0 = T.nt * TN;
     return T;
   };
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&conv[s], 2);  // one converter warp per CTA (leader's is used)
-      mbar_init(&empty[s], 1);
+    for (int j = 0; j < BSLOTS; ++j) {
+      mbar_init(&fullB[j], 1);
+      mbar_init(&emptyB[j], 1);  // MMA commit
     }
-    mbar_init(tfull, 1);
-    mbar_init(tempty, 2);  // one arrive per CTA (leader's is used)
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&fullA[s], 1);
+      mbar_init(&sfree[s], 4);  // each converter warp, after its staging reads
+      // leader: its 4 converter warps (+ the follower's signaler for CG = 2)
+      mbar_init(&conv[s], CG == 1 ? 4 : 5);
+      mbar_init(&empty[s], 1);  // MMA commit
+      mbar_init(&cdone[s], 4);
+    }
+    for (int a = 0; a < NACC; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], CG);  // one arrive per CTA
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 2) {
-    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                     smem_u32(tmem_slot)),
-                 "r"(512u));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    if constexpr (CG == 1) {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       smem_u32(tmem_slot)),
+                   "r"(512u));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       smem_u32(tmem_slot)),
+                   "r"(512u));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
-  cluster_sync();  // peer barriers initialised before any remote arrive
+  if constexpr (CG == 2) cluster_sync();  // peer barriers initialised before any remote arrive
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem_base = *tmem_slot;
-  const uint32_t conv_leader0 = map_to_rank(smem_u32(&conv[0]), 0);
-  const uint32_t tempty_leader = map_to_rank(smem_u32(tempty), 0);
 
   if (warp == 0) {
-    // ===== TMA producer (each CTA loads its own halves) =====
+    // ===== TMA producer: fp32 operand tiles into the staging ring =====
     if (lane == 0) {
-      const uint32_t bytes = S::A_BYTES + S::B_BYTES + (convert_b ? 0 : S::B_BYTES);
+      const uint32_t bytes = TILE_BYTES * (p.b_direct ? 1 : 2);
       int kg = 0;
-      for (int t = pair; t < total; t += npairs) {
+      for (int t = unit; t < total; t += nunits) {
         const Tile T = tile_of(t);
-        const int nb0 = T.n0 + (int)cr * HB;
+        const int nb0 = T.n0 + (int)cr * 128;
         for (int kb = 0; kb < nk; ++kb, ++kg) {
           const int s = kg % STAGES;
           const uint32_t ph = (kg / STAGES) & 1;
-          mbar_wait(&empty[s], ph ^ 1);
-          mbar_expect_tx(&full[s], bytes);
+          mbar_wait(&sfree[s], ph ^ 1);
+          mbar_expect_tx(&fullA[s], bytes);
           const int k0 = kb * BK;
           int c[5];
-          if (!p.a.mn) {
+          if (!p.a_mn)
             tma_coords(p.a, k0, T.m0, T.g, T.b, T.h, c);
-            tma_load_5d(stage_a(s), &mapA, &full[s], c);
-          } else {
-#pragma unroll
-            for (int i = 0; i < 128 / 32; ++i) {
-              tma_coords(p.a, T.m0 + 32 * i, k0, T.g, T.b, T.h, c);
-              tma_load_5d(stage_a(s) + i * 4096, &mapA, &full[s], c);
-            }
-          }
-          if (!p.b.mn) {
-            tma_coords(p.b, k0, nb0, T.g, T.b, T.h, c);
-            tma_load_5d(stage_b(s), &mapB, &full[s], c);
-            if (!convert_b) {
-              tma_coords(p.blo, k0, nb0, T.g, T.b, T.h, c);
-              tma_load_5d(stage_blo(s), &mapBlo, &full[s], c);
-            }
-          } else {
-#pragma unroll
-            for (int i = 0; i < HB / 32; ++i) {
-              tma_coords(p.b, nb0 + 32 * i, k0, T.g, T.b, T.h, c);
-              tma_load_5d(stage_b(s) + i * 4096, &mapB, &full[s], c);
-              if (!convert_b) {
-                tma_coords(p.blo, nb0 + 32 * i, k0, T.g, T.b, T.h, c);
-                tma_load_5d(stage_blo(s) + i * 4096, &mapBlo, &full[s], c);
-              }
-            }
+          else
+            tma_coords(p.a, T.m0, k0, T.g, T.b, T.h, c);
+          tma_load_5d(stg_a(s), &mapA, &fullA[s], c);
+          if (!p.b_direct) {
+            if (!p.b_mn)
+              tma_coords(p.b, k0, nb0, T.g, T.b, T.h, c);
+            else
+              tma_coords(p.b, nb0, k0, T.g, T.b, T.h, c);
+            tma_load_5d(stg_b(s), &mapB, &fullA[s], c);
           }
         }
       }
     }
     __syncwarp();
+  } else if (warp == 3) {
+    // ===== TMA producer for a pre-split B: hi|lo tiles into the MMA ring =====
+    if (p.b_direct && lane == 0) {
+      int kg = 0;
+      for (int t = unit; t < total; t += nunits) {
+        const Tile T = tile_of(t);
+        const int nb0 = T.n0 + (int)cr * 128;
+        for (int kb = 0; kb < nk; ++kb, ++kg) {
+          const int j = kg % BSLOTS;
+          mbar_wait(&emptyB[j], ((kg / BSLOTS) & 1) ^ 1);
+          mbar_expect_tx(&fullB[j], TILE_BYTES);
+          int c[5];
+          tma_coords(p.b, kb * BK, nb0, T.g, T.b, T.h, c);
+          tma_load_5d(b_slot(j), &mapB, &fullB[j], c);
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 2) {
+    // ===== follower CTA of a pair: forward "stage converted" to the leader =====
+    if (CG == 2 && !leader && lane == 0) {
+      const uint32_t conv_leader0 = map_to_rank(smem_u32(&conv[0]), 0);
+      int kg = 0;
+      for (int t = unit; t < total; t += nunits)
+        for (int kb = 0; kb < nk; ++kb, ++kg) {
+          const int s = kg % STAGES;
+          mbar_wait(&cdone[s], (kg / STAGES) & 1);
+          mbar_arrive_cluster(conv_leader0 + s * 8);
+        }
+    }
+    __syncwarp();
   } else if (warp == 1) {
-    // ===== MMA issuer: the leader's single thread drives both SMs =====
+    // ===== MMA issuer (one thread; for CG = 2 the leader's drives both SMs) =====
     if (leader && lane == 0) {
-      const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)p.a.mn << 15) |
-                             ((uint32_t)p.b.mn << 16) | ((uint32_t)(P_BN >> 3) << 17) |
-                             ((uint32_t)(P_BM >> 4) << 24);
-      const uint32_t a_lbo = p.a.mn ? 4096u : 16u, a_sbo = p.a.mn ? 512u : 1024u;
-      const uint32_t b_lbo = p.b.mn ? 4096u : 16u, b_sbo = p.b.mn ? 512u : 1024u;
-      const uint32_t a_lay = p.a.mn ? 1u : 2u, b_lay = p.b.mn ? 1u : 2u;
-      const uint32_t a_kstep = p.a.mn ? 1024u : 32u;
-      const uint32_t b_kstep = p.b.mn ? 1024u : 32u;
+      // instruction descriptor: D f32, A/B f16, both K-major, N, M
+      const uint32_t idesc = (1u << 4) | ((uint32_t)(TN >> 3) << 17) |
+                             ((uint32_t)(C::TM >> 4) << 24);
       int kg = 0, tc = 0;
-      for (int t = pair; t < total; t += npairs, ++tc) {
-        mbar_wait(tempty, (tc & 1) ^ 1);
+      for (int t = unit; t < total; t += nunits, ++tc) {
+        const int acc = tc % NACC;
+        const uint32_t aph = (tc / NACC) & 1;
+        mbar_wait(&tempty[acc], aph ^ 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t tm = tmem_base + (uint32_t)(acc * 2 * TN);
         for (int kb = 0; kb < nk; ++kb, ++kg) {
           const int s = kg % STAGES;
           const uint32_t ph = (kg / STAGES) & 1;
           mbar_wait(&conv[s], ph);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const int j = kg % BSLOTS;
+          const uint8_t* bt = p.b_direct ? b_slot(j) : hl_b(s);
 #pragma unroll
-          for (int k = 0; k < BK / 8; ++k) {
-            const uint64_t dah = smem_desc(stage_a(s) + k * a_kstep, a_lbo, a_sbo, a_lay);
-            const uint64_t dal = smem_desc(stage_alo(s) + k * a_kstep, a_lbo, a_sbo, a_lay);
-            const uint64_t dbh = smem_desc(stage_b(s) + k * b_kstep, b_lbo, b_sbo, b_lay);
-            const uint64_t dbl = smem_desc(stage_blo(s) + k * b_kstep, b_lbo, b_sbo, b_lay);
+          for (int k = 0; k < BK / 16; ++k) {
+            const uint64_t dah = smem_desc_sw128(hl_a(s) + k * 32);
+            const uint64_t dal = smem_desc_sw128(hl_a(s) + 64 + k * 32);
+            const uint64_t dbh = smem_desc_sw128(bt + k * 32);
+            const uint64_t dbl = smem_desc_sw128(bt + 64 + k * 32);
             const uint32_t acc0 = (kb > 0 || k > 0) ? 1u : 0u;
-            mma_tf32_pair(tmem_base, dah, dbh, idesc, acc0);
+            mma_f16<CG>(tm, dah, dbh, idesc, acc0);
             if (p.passes > 1) {
-              mma_tf32_pair(tmem_base + P_BN, dal, dbh, idesc, acc0);
-              mma_tf32_pair(tmem_base + P_BN, dah, dbl, idesc, 1u);
+              mma_f16<CG>(tm + TN, dal, dbh, idesc, acc0);
+              mma_f16<CG>(tm + TN, dah, dbl, idesc, 1u);
             }
           }
-          mma_commit_pair(&empty[s]);
+          mma_commit<CG>(&empty[s]);
+          if (p.b_direct) mma_commit<CG>(&emptyB[j]);
         }
-        mma_commit_pair(tfull);
+        mma_commit<CG>(&tfull[acc]);
       }
     }
     __syncwarp();
   } else if (warp >= 4 && warp < 8) {
-    // ===== hi/lo split converters (own halves), then tell the leader. Warp c
-    // owns stage buffer c; the leader's converter arrives locally, the
-    // peer's with one cluster-scope release per stage =====
-    const int c = warp - 4;
+    // ===== converters: staging -> hi|lo tiles; release the staging stage,
+    // then (all four warps done) signal the MMA issuer =====
+    const int kc = warp - 4;
+    float amax = 0.f;
     int kg = 0;
-    for (int t = pair; t < total; t += npairs) {
+    for (int t = unit; t < total; t += nunits) {
       for (int kb = 0; kb < nk; ++kb, ++kg) {
-        if (kg % STAGES != c) continue;  // one warp per stage buffer: phases in order
         const int s = kg % STAGES;
         const uint32_t ph = (kg / STAGES) & 1;
-        mbar_wait(&full[s], ph);
-        split_tile(reinterpret_cast<float*>(stage_a(s)), reinterpret_cast<float*>(stage_alo(s)),
-                   128 * BK, lane, 32, p.rawhi);
-        if (convert_b)
-          split_tile(reinterpret_cast<float*>(stage_b(s)),
-                     reinterpret_cast<float*>(stage_blo(s)), HB * BK, lane, 32, p.rawhi);
+        mbar_wait(&fullA[s], ph);
+        mbar_wait(&empty[s], ph ^ 1);  // hi|lo buffers no longer read by the MMAs
+        if (!(p.debug & 1)) {
+          convert_tile(smem_u32(stg_a(s)), smem_u32(hl_a(s)), p.a_mn, kc, lane, amax);
+          if (!p.b_direct)
+            convert_tile(smem_u32(stg_b(s)), smem_u32(hl_b(s)), p.b_mn, kc, lane, amax);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sfree[s]);
+        if (p.b_direct) mbar_wait(&fullB[kg % BSLOTS], (kg / BSLOTS) & 1);
+        // generic-proxy smem writes -> visible to the tensor core (async proxy)
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
-        if (lane == 0) {
-          if (leader)
-            mbar_arrive(&conv[s]);
-          else
-            mbar_arrive_cluster(conv_leader0 + s * 8);
-        }
+        // leader: straight to the MMA issuer; follower: to the signaler warp,
+        // which forwards one cluster-scope arrive (keeps the release fence of
+        // the remote arrive off the converters' critical path)
+        if (lane == 0) mbar_arrive(leader ? &conv[s] : &cdone[s]);
       }
     }
+    if (amax >= 65520.f && amax <= FLT_MAX && p.range_flag) atomicOr(p.range_flag, 1);
   } else if (warp >= 8) {
-    // ===== epilogue: 8 warps = 4 lane quarters x 2 column halves =====
-    const int q = warp & 3, half = (warp - 8) >> 2;
+    // ===== epilogue: (4 lane quarters) x (CG column halves) =====
+    const int ew = warp - 8;
+    const int q = warp & 3, half = ew >> 2;
+    constexpr int COLS = TN / CG;  // columns per epilogue warp
     const bool res0 = p.ep.kind == EPI_FINAL && p.ep.cmb.mode == CM_RES0;
+    const uint32_t tempty_leader = CG == 2 ? map_to_rank(smem_u32(&tempty[0]), 0) : 0u;
     int tc = 0;
-    for (int t = pair; t < total; t += npairs, ++tc) {
+    for (int t = unit; t < total; t += nunits, ++tc) {
       const Tile T = tile_of(t);
-      mbar_wait(tfull, tc & 1);
+      const int acc = tc % NACC;
+      const uint32_t aph = (tc / NACC) & 1;
+      mbar_wait(&tfull[acc], aph);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const int row = T.m0 + q * 32 + lane;
-      const uint32_t lane_addr = tmem_base + ((uint32_t)(q * 32) << 16);
+      const uint32_t lane_addr =
+          tmem_base + (uint32_t)(acc * 2 * TN) + ((uint32_t)(q * 32) << 16);
       double r2 = 0.0;
 #pragma unroll 1
-      for (int c = half * (P_BN / 2); c < (half + 1) * (P_BN / 2); c += 16) {
+      for (int c = half * COLS; c < (half + 1) * COLS; c += 16) {
+        // main and correction columns in flight together, one wait
+        uint32_t rv[16], rw[16];
+        tmem_ld16(lane_addr + c, rv);
+        if (p.passes > 1) tmem_ld16(lane_addr + TN + c, rw);
+        tmem_wait();
         float v[16];
-        tmem_ld16(lane_addr + c, v);
-        if (p.passes > 1) {
-          float w[16];
-          tmem_ld16(lane_addr + P_BN + c, w);
 #pragma unroll
-          for (int i = 0; i < 16; ++i) v[i] += w[i];
-        }
+        for (int i = 0; i < 16; ++i)
+          v[i] = p.passes > 1 ? fmaf(__uint_as_float(rw[i]), kLoInv, __uint_as_float(rv[i]))
+                              : __uint_as_float(rv[i]);
         const int col0 = T.n0 + c;
         const int nvalid = min(16, p.N - col0);
-        if (row < p.M && nvalid > 0)
+        if (row < p.M && nvalid > 0 && !(p.debug & 2))
           r2 += (nvalid == 16 && p.vec_ok)
                     ? epilogue_row16(p.ep, T.g, T.b, T.h, row, col0, v)
                     : epilogue_row(p.ep, T.g, T.b, T.h, row, col0, v, nvalid);
       }
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-      // all 8 epilogue warps done with TMEM -> one arrive per CTA
-      asm volatile("bar.sync 2, 256;" ::: "memory");
-      if (warp == 8 && lane == 0) {
+      // all epilogue warps of this CTA done with the buffer -> one arrive
+      asm volatile("bar.sync 2, %0;" ::"n"(32 * C::EPI_WARPS) : "memory");
+      if (ew == 0 && lane == 0) {
         if (leader)
-          mbar_arrive(tempty);
+          mbar_arrive(&tempty[acc]);
         else
-          mbar_arrive_cluster(tempty_leader);
+          mbar_arrive_cluster(tempty_leader + acc * 8);
       }
       if (res0) {
-        // one partial per (128-row, 256-column) tile of this CTA
+        // one partial per (128-row, TN-column) tile of this CTA
         for (int o = 16; o > 0; o >>= 1) r2 += __shfl_xor_sync(0xffffffffu, r2, o);
-        if (lane == 0) red[warp - 8] = r2;
-        asm volatile("bar.sync 1, 256;" ::: "memory");
-        if (warp == 8 && lane == 0 && T.mt < tiles_m128) {
+        if (lane == 0) red[acc * C::EPI_WARPS + ew] = r2;
+        asm volatile("bar.sync 1, %0;" ::"n"(32 * C::EPI_WARPS) : "memory");
+        if (ew == 0 && lane == 0 && T.mt < tiles_m128) {
           double tsum = 0.0;
-          for (int i = 0; i < 8; ++i) tsum += red[i];
+          for (int i = 0; i < C::EPI_WARPS; ++i) tsum += red[acc * C::EPI_WARPS + i];
           p.ep.cmb.norm_partials[p.ep.cmb.norm_base + T.z * p.ep.cmb.norm_member_stride +
                                  T.mt * tiles_n + T.nt] = tsum;
         }
-        asm volatile("bar.sync 1, 256;" ::: "memory");
+        if constexpr (NACC == 1)
+          asm volatile("bar.sync 1, %0;" ::"n"(32 * C::EPI_WARPS) : "memory");
       }
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
-  cluster_sync();
-  if (warp == 2)
-    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
-                 "r"(512u));
+  if constexpr (CG == 2) cluster_sync();
+  if (warp == 2) {
+    if constexpr (CG == 1)
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                   "r"(512u));
+    else
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                   "r"(512u));
+  }
 }
 
-// split kernel for weights
-__global__ void split_tf32_kernel(float* hi, float* lo, const float* src, long long n) {
+// ---- pre-split operands (weights) --------------------------------------------------
+// dst row r of slot g = for each 32-wide K block: 32 hi | 32 lo' fp16 values
+// (K zero-padded to a multiple of 32); with `transpose`, B = src^T.
+__global__ void pack_hl_kernel(const float* __restrict__ src, long long src_slot, int src_ld,
+                               float* __restrict__ dst, long long dst_slot, int dst_ld, int G,
+                               int rows, int K, int transpose) {
+  const int kblocks = (K + BK - 1) / BK;
+  const long long n = (long long)G * rows * kblocks * 4;  // 8-value chunks
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x) {
-    const float x = src[i];
-    const float h = __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
-    if (hi) hi[i] = h;
-    lo[i] = x - h;
+    const int chunk = (int)(i % (kblocks * 4));
+    const long long rg = i / (kblocks * 4);
+    const int r = (int)(rg % rows);
+    const int g = (int)(rg / rows);
+    const int k0 = chunk * 8;
+    float x[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const int k = k0 + e;
+      x[e] = k < K ? (transpose ? src[g * src_slot + (long long)k * src_ld + r]
+                                : src[g * src_slot + (long long)r * src_ld + k])
+                   : 0.f;
+    }
+    uint4 hi, lo;
+    float amax = 0.f;
+    split8(x, hi, lo, amax);
+    uint8_t* row = reinterpret_cast<uint8_t*>(dst + g * dst_slot + (long long)r * dst_ld) +
+                   (chunk >> 2) * 128;
+    *reinterpret_cast<uint4*>(row + (chunk & 3) * 16) = hi;
+    *reinterpret_cast<uint4*>(row + 64 + (chunk & 3) * 16) = lo;
   }
 }
 
@@ -789,9 +669,11 @@ PFN_cuTensorMapEncodeTiled_v12000 encoder() {
 // member g -> slot slot0 + g*step. rows x cols is the [rows][cols] matrix of
 // one problem (row stride ld). Dimensions are ordered by increasing stride
 // (a head slice of a [tokens][3d] qkv buffer has a smaller stride than a
-// row); dimension 0 is always the contiguous columns.
+// row); dimension 0 is always the contiguous columns. Boxes are
+// [box_rows][box_cols]: K-major tiles [128][32] with SWIZZLE_128B, MN-major
+// staging tiles [32 K][128] dense.
 CUtensorMap make_map(const Mat& m, int G, int Bb, int H, int rows, int cols, int box_rows,
-                     TcOperand* op, bool mn_major) {
+                     int box_cols, bool swizzle, TcOperand* op) {
   long long lo = m.slot0, hi = m.slot0 + (long long)(G - 1) * m.step;
   if (hi < lo) std::swap(lo, hi);
   const float* base = m.ptr + lo * m.slot_stride;
@@ -826,7 +708,7 @@ CUtensorMap make_map(const Mat& m, int G, int Bb, int H, int rows, int cols, int
   for (const D& d : dims) maxs = std::max(maxs, d.stride);
   cuuint64_t gdim[5] = {(cuuint64_t)cols, 1, 1, 1, 1};
   cuuint64_t gstr[4];
-  cuuint32_t box[5] = {32, 1, 1, 1, 1};
+  cuuint32_t box[5] = {(cuuint32_t)box_cols, 1, 1, 1, 1};
   cuuint32_t estr[5] = {1, 1, 1, 1, 1};
   for (int i = 0; i < 4; ++i) {
     gdim[i + 1] = (cuuint64_t)dims[i].extent;
@@ -848,8 +730,7 @@ CUtensorMap make_map(const Mat& m, int G, int Bb, int H, int rows, int cols, int
   CUtensorMap map;
   CUresult r = encoder()(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5, const_cast<float*>(base), gdim,
                          gstr, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                         mn_major ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B
-                                  : CU_TENSOR_MAP_SWIZZLE_128B,
+                         swizzle ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS)
     throw ContractViolation("cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
@@ -859,28 +740,30 @@ CUtensorMap make_map(const Mat& m, int G, int Bb, int H, int rows, int cols, int
 // host-side parameter block + tensor maps for one launch
 struct Prepared {
   TcParams p;
-  CUtensorMap mA, mB, mBlo;
+  CUtensorMap mA, mB;
 };
 
-Prepared prepare(const GemmArgs& a, int bm_rows, int bn_rows_b) {
+Prepared prepare(const GemmArgs& a) {
   Prepared P;
   TcParams& p = P.p;
   p.G = a.G;
   p.M = a.M;
   p.N = a.N;
   p.K = a.K;
+  p.Bb = a.Bb;
+  p.H = a.H;
   p.ep = a.ep;
-  p.b_presplit = a.Blo.ok() ? 1 : 0;
+  p.range_flag = a.range_flag;
   static const int passes = [] {
-    const char* e = getenv("MGLP_DEBUG_TF32_PASSES");
+    const char* e = getenv("MGLP_DEBUG_SPLIT_PASSES");
     return e ? atoi(e) : 3;
   }();
   p.passes = passes;
-  static const int rawhi = [] {
-    const char* e = getenv("MGLP_TF32_EXPLICIT_HI");
-    return (e && atoi(e)) ? 0 : 1;
+  static const int debug = [] {
+    const char* e = getenv("MGLP_DEBUG_GEMM");
+    return e ? atoi(e) : 0;
   }();
-  p.rawhi = rawhi;
+  p.debug = debug;
   {
     auto al = [](const Mat& m) {
       return !m.ok() || ((reinterpret_cast<uintptr_t>(m.ptr) & 15) == 0 && m.ld % 4 == 0 &&
@@ -889,22 +772,19 @@ Prepared prepare(const GemmArgs& a, int bm_rows, int bn_rows_b) {
     const EpiArgs& e = a.ep;
     p.vec_ok = al(e.out1) && al(e.out2) && al(e.add1) && al(e.add2) && al(e.aux) && al(e.bias);
   }
-  p.a.mn = a.a_mn;
-  p.b.mn = a.b_mn;
-  p.blo.mn = a.b_mn;
-  p.Bb = a.Bb;
-  p.H = a.H;
-  // A: [M][K] (K-major) or [K][M] (MN-major); box rows: bm_rows, or 32 K-rows
-  P.mA = a.a_mn ? make_map(a.A, a.G, a.Bb, a.H, a.K, a.M, BK, &p.a, true)
-                : make_map(a.A, a.G, a.Bb, a.H, a.M, a.K, bm_rows, &p.a, false);
-  P.mB = a.b_mn ? make_map(a.B, a.G, a.Bb, a.H, a.K, a.N, BK, &p.b, true)
-                : make_map(a.B, a.G, a.Bb, a.H, a.N, a.K, bn_rows_b, &p.b, false);
-  P.mBlo = P.mB;
-  if (p.b_presplit)
-    P.mBlo = a.b_mn ? make_map(a.Blo, a.G, a.Bb, a.H, a.K, a.N, BK, &p.blo, true)
-                    : make_map(a.Blo, a.G, a.Bb, a.H, a.N, a.K, bn_rows_b, &p.blo, false);
-  else
-    p.blo = p.b;
+  p.a_mn = a.a_mn;
+  p.b_direct = a.Bhl.ok() ? 1 : 0;
+  p.b_mn = p.b_direct ? 0 : a.b_mn;
+  // A: [M][K] (K-major) or [K][M] (MN-major)
+  P.mA = a.a_mn ? make_map(a.A, a.G, a.Bb, a.H, a.K, a.M, BK, ROWS, false, &p.a)
+                : make_map(a.A, a.G, a.Bb, a.H, a.M, a.K, ROWS, BK, true, &p.a);
+  if (p.b_direct) {
+    const int kp = ceil_div(a.K, BK) * BK;  // packed row: kp floats = kp hi + kp lo'
+    P.mB = make_map(a.Bhl, a.G, a.Bb, a.H, a.N, kp, ROWS, BK, true, &p.b);
+  } else {
+    P.mB = a.b_mn ? make_map(a.B, a.G, a.Bb, a.H, a.K, a.N, BK, ROWS, false, &p.b)
+                  : make_map(a.B, a.G, a.Bb, a.H, a.N, a.K, ROWS, BK, true, &p.b);
+  }
   return P;
 }
 
@@ -914,26 +794,36 @@ int num_sms() {
   return sms;
 }
 
-template <int BN, int STAGES>
-void launch_cfg(const GemmArgs& a, const int* active, cudaStream_t s) {
-  Prepared P = prepare(a, BM, BN);
-  const int smem = Smem<BN, STAGES>::BYTES;
-  MGLP_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<BN, STAGES>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  const long long tiles = (long long)ceil_div(a.N, BN) * ceil_div(a.M, BM) * a.G * a.Bb * a.H;
-  const int grid = (int)std::min<long long>(tiles, num_sms());
-  gemm_tc_kernel<BN, STAGES><<<grid, kThreads, smem, s>>>(P.mA, P.mB, P.mBlo, P.p, active);
-  MGLP_CUDA(cudaGetLastError());
-}
-
-void launch_pair(const GemmArgs& a, const int* active, cudaStream_t s) {
-  Prepared P = prepare(a, 128, P_BN / 2);
-  const int smem = Smem2::BYTES;
-  MGLP_CUDA(cudaFuncSetAttribute(gemm_tc2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 smem));
-  const long long tiles = (long long)ceil_div(a.N, P_BN) * ceil_div(a.M, P_BM) * a.G * a.Bb * a.H;
-  const int pairs = (int)std::min<long long>(tiles, num_sms() / 2);
-  gemm_tc2_kernel<<<2 * pairs, kThreads2, smem, s>>>(P.mA, P.mB, P.mBlo, P.p, active);
+template <int CG>
+void launch_cg(const GemmArgs& a, const int* active, cudaStream_t s) {
+  using C = Cfg<CG>;
+  Prepared P = prepare(a);
+  static bool attr = [] {
+    MGLP_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<CG>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
+    return true;
+  }();
+  (void)attr;
+  const long long tiles =
+      (long long)ceil_div(a.N, C::TN) * ceil_div(a.M, C::TM) * a.G * a.Bb * a.H;
+  const int units = (int)std::min<long long>(tiles, num_sms() / CG);
+  if constexpr (CG == 1) {
+    gemm_tc_kernel<1><<<units, C::THREADS, SMEM_BYTES, s>>>(P.mA, P.mB, P.p, active);
+  } else {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(2 * units);
+    cfg.blockDim = dim3(C::THREADS);
+    cfg.dynamicSmemBytes = SMEM_BYTES;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    MGLP_CUDA(cudaLaunchKernelEx(&cfg, gemm_tc_kernel<2>, P.mA, P.mB, P.p, active));
+  }
   MGLP_CUDA(cudaGetLastError());
 }
 
@@ -945,33 +835,39 @@ bool use_pair(const GemmArgs& a) {
     const char* e = getenv("MGLP_GEMM_NO_PAIR");
     return e ? atoi(e) : 0;
   }();
-  return !off && a.M >= P_BM && a.N >= P_BN;
+  return !off && a.M >= 256 && a.N >= 256;
 }
-
-constexpr int kBN = 128;
-constexpr int kStages = 3;
 
 }  // namespace
 
 int gemm_tc_blocks(const GemmArgs& a) {
   // residual-norm partial slots: one per (128-row, column-tile) of each problem
-  const int bn = use_pair(a) ? P_BN : kBN;
-  return ceil_div(a.N, bn) * ceil_div(a.M, BM) * a.G * a.Bb * a.H;
+  const int tn = use_pair(a) ? Cfg<2>::TN : Cfg<1>::TN;
+  return ceil_div(a.N, tn) * ceil_div(a.M, 128) * a.G * a.Bb * a.H;
 }
 
 void launch_gemm_tc(const GemmArgs& a, const int* active, cudaStream_t s) {
   if (a.G == 0 || a.M == 0 || a.N == 0) return;
   if (a.K == 0) throw ContractViolation("gemm_tc: K must be positive");
   if (use_pair(a))
-    launch_pair(a, active, s);
+    launch_cg<2>(a, active, s);
   else
-    launch_cfg<kBN, kStages>(a, active, s);
+    launch_cg<1>(a, active, s);
 }
 
-void launch_split_tf32(float* hi, float* lo, const float* src, long long n, cudaStream_t s) {
-  if (n == 0) return;
-  const int blocks = (int)std::min<long long>(148 * 8, (n + 255) / 256);
-  split_tf32_kernel<<<blocks, 256, 0, s>>>(hi, lo, src, n);
+long long pack_hl_cols(int K) { return (long long)ceil_div(K, BK) * BK; }
+
+void launch_pack_hl(const float* src, long long src_slot, int src_ld, float* dst,
+                    long long dst_slot, int dst_ld, int G, int rows, int K, bool transpose,
+                    cudaStream_t s) {
+  if (G == 0 || rows == 0 || K == 0) return;
+  if (dst_ld < pack_hl_cols(K) || (dst_ld % 4) || (reinterpret_cast<uintptr_t>(dst) & 15))
+    throw ContractViolation("pack_hl: destination rows must hold pad32(K) 16-byte aligned floats");
+  const long long n = (long long)G * rows * ceil_div(K, BK) * 4;
+  const int blocks = (int)std::min<long long>(148 * 16, (n + 255) / 256);
+  pack_hl_kernel<<<blocks, 256, 0, s>>>(src, src_slot, src_ld, dst, dst_slot, dst_ld, G, rows, K,
+                                        transpose ? 1 : 0);
+  MGLP_CUDA(cudaGetLastError());
 }
 
 }  // namespace mglp

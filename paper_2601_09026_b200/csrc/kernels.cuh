@@ -92,11 +92,16 @@ void launch_cycle_end(SolveCtrl* c, double tol, cudaStream_t s);
 // Reference fp32 CUDA-core GEMM: test oracle for the tensor-core path only.
 void launch_gemm_simt(const GemmArgs& a, const int* active, cudaStream_t s);
 int gemm_simt_blocks(const GemmArgs& a);
-// Parity-grade tcgen05 (kind::tf32, 3-pass hi/lo split) GEMM.
+// Parity-grade tcgen05 (kind::f16, 3-pass fp16 hi/lo split) GEMM.
 void launch_gemm_tc(const GemmArgs& a, const int* active, cudaStream_t s);
 int gemm_tc_blocks(const GemmArgs& a);
-// Splits weights into tf32 hi / lo parts (x = hi + lo exactly; hi has the
-// low 13 mantissa bits cleared).
-void launch_split_tf32(float* hi, float* lo, const float* src, long long n, cudaStream_t s);
+// Pre-splits a family of G matrices into the hi|lo' form GemmArgs::Bhl
+// expects: dst row r = per 32-wide K block [32 fp16 hi | 32 fp16 lo'], K
+// zero-padded to pack_hl_cols(K) (floats per row). transpose: B = src^T
+// (src is [K][rows]).
+long long pack_hl_cols(int K);
+void launch_pack_hl(const float* src, long long src_slot, int src_ld, float* dst,
+                    long long dst_slot, int dst_ld, int G, int rows, int K, bool transpose,
+                    cudaStream_t s);
 
 }  // namespace mglp

@@ -1,5 +1,6 @@
-"""tcgen05 kind::tf32 x3 GEMM (the product kernel) against an fp64 torch
-reference and the fp32 CUDA-core reference kernel, through the C-ABI test hook."""
+"""tcgen05 kind::f16 3-pass split GEMM (the product kernel) against an fp64
+torch reference and the fp32 CUDA-core reference kernel, through the C-ABI
+test hook."""
 import ctypes as C
 import os
 
@@ -22,7 +23,7 @@ def run(G, M, N_, K, a_mn, b_mn, presplit, engine, bias=False, seed=0):
     ldb = N_ if b_mn else K
     N.call("mglp_test_gemm", G, M, N_, K, A.data_ptr(), A[0].numel(), lda, int(a_mn),
            B.data_ptr(), B[0].numel(), ldb, int(b_mn), int(presplit),
-           None if bv is None else bv.data_ptr(), Cm.data_ptr(), M * N_, N_, engine)
+           None if bv is None else bv.data_ptr(), Cm.data_ptr(), M * N_, N_, engine, None)
     Ad = A.double().transpose(1, 2) if a_mn else A.double()
     Bd = B.double().transpose(1, 2) if b_mn else B.double()
     ref = Ad @ Bd.transpose(1, 2)
@@ -53,7 +54,7 @@ def test_tc_matches_fp64(shape):
     c, ref = run(G, M, N_, K, a_mn, b_mn, pre, engine=0, bias=True)
     assert not torch.isnan(c).any()
     e = relerr(c, ref)
-    # tf32x3 with fp32 tensor-core accumulation: ~1e-6 at K~100, ~1e-5 at K=4096
+    # fp16x3 split with fp32 tensor-core accumulation: ~1e-6 at K~100, ~1e-5 at K=4096
     assert e < 2e-5, e
 
 
@@ -65,40 +66,72 @@ def test_simt_reference_kernel(shape):
 
 
 def test_split_is_effective():
-    """single-pass tf32 sits at ~8e-4 (measured); the 3-pass split with a
-    separate correction accumulator must be fp32-class (~6e-6 at K=2048)"""
+    """the 3-pass fp16 split with a separate correction accumulator must be
+    fp32-class (~6e-6 at K=2048); a single fp16 pass sits at ~5e-4"""
     c, ref = run(1, 256, 256, 2048, False, False, True, engine=0)
     assert relerr(c, ref) < 1.2e-5
 
 
-_TRUNC_SCRIPT = r"""
+def test_small_magnitudes_keep_precision():
+    """operands far below the fp16 normal range (1e-6) still give fp32-class
+    products: lo' is pre-scaled by 2^11, so only the hi part is subnormal"""
+    g = torch.Generator(device="cpu").manual_seed(3)
+    M, Nn, K = 256, 256, 512
+    A = (torch.randn(M, K, generator=g) * 1e-6).float().cuda()
+    B = (torch.randn(Nn, K, generator=g) * 1e-3).float().cuda()
+    Cm = torch.empty(M, Nn, device="cuda")
+    N.call("mglp_test_gemm", 1, M, Nn, K, A.data_ptr(), 0, K, 0, B.data_ptr(), 0, K, 0, 1,
+           None, Cm.data_ptr(), 0, Nn, 0, None)
+    ref = A.double() @ B.double().T
+    assert relerr(Cm.double(), ref) < 2e-4
+
+
+def test_range_flag_reports_fp16_overflow():
+    """a finite operand value beyond the fp16 range is reported, never
+    silently turned into inf/NaN products"""
+    M, Nn, K = 128, 128, 64
+    A = torch.ones(M, K, device="cuda")
+    B = torch.ones(Nn, K, device="cuda") * 0.5
+    Cm = torch.empty(M, Nn, device="cuda")
+    flag = C.c_int(7)
+    N.call("mglp_test_gemm", 1, M, Nn, K, A.data_ptr(), 0, K, 0, B.data_ptr(), 0, K, 0, 0,
+           None, Cm.data_ptr(), 0, Nn, 0, C.byref(flag))
+    assert flag.value == 0
+    A[3, 5] = 1.0e5
+    N.call("mglp_test_gemm", 1, M, Nn, K, A.data_ptr(), 0, K, 0, B.data_ptr(), 0, K, 0, 0,
+           None, Cm.data_ptr(), 0, Nn, 0, C.byref(flag))
+    assert flag.value == 1
+
+
+_PASSES_SCRIPT = r"""
 import sys, numpy as np, torch
 sys.path.insert(0, sys.argv[1])
 from paper_2601_09026_b200 import _native as N
 torch.manual_seed(0)
-M, Nn, K = 256, 256, 512
+M, Nn, K = 256, 256, 2048
 A = torch.randn(M, K).float().cuda()
 B = torch.randn(Nn, K).float().cuda()
 C = torch.empty(M, Nn, device="cuda")
 N.call("mglp_test_gemm", 1, M, Nn, K, A.data_ptr(), 0, K, 0, B.data_ptr(), 0, K, 0, 0, None,
-       C.data_ptr(), 0, Nn, 0)
-np.save(sys.argv[2], C.cpu().numpy())
+       C.data_ptr(), 0, Nn, 0, None)
+ref = A.double() @ B.double().T
+print(float((C.double() - ref).abs().max() / ref.abs().max()))
 """
 
 
-def test_tf32_operand_truncation(tmp_path):
-    """kind::tf32 reads fp32 operands truncated to tf32: feeding the raw tile
-    as the hi part (default) is bitwise identical to writing the masked hi
-    (MGLP_TF32_EXPLICIT_HI=1). The default converter relies on this."""
+def test_single_pass_misses_parity(tmp_path):
+    """diagnostic switch MGLP_DEBUG_SPLIT_PASSES=1 (hi.hi only): the error is
+    ~100x the 3-pass split's, i.e. the correction passes are what make the
+    tensor-core path parity grade"""
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     script = tmp_path / "t.py"
-    script.write_text(_TRUNC_SCRIPT)
-    outs = []
-    for explicit in ("0", "1"):
-        out = tmp_path / f"c{explicit}.npy"
-        env = dict(os.environ, MGLP_TF32_EXPLICIT_HI=explicit)
-        subprocess.run([sys.executable, str(script), root, str(out)], check=True, env=env)
-        outs.append(np.load(out))
-    assert np.array_equal(outs[0], outs[1])
+    script.write_text(_PASSES_SCRIPT)
+    errs = []
+    for passes in ("1", "3"):
+        env = dict(os.environ, MGLP_DEBUG_SPLIT_PASSES=passes)
+        out = subprocess.run([sys.executable, str(script), root], check=True, env=env,
+                             capture_output=True, text=True).stdout
+        errs.append(float(out.strip().splitlines()[-1]))
+    assert errs[0] > 1e-4 and errs[1] < 1.2e-5, errs

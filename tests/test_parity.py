@@ -4,7 +4,8 @@ float64 numpy restatement (oracle/mglp_oracle.py).
 
 Tolerance (north star): max|device - reference| / max|reference| <= 1e-4 for
 states, residual norms, lambda_0 and gradients; the device runs fp32 with
-tf32x3 tensor-core GEMMs, so observed errors are ~1e-6.
+3-pass fp16-split tensor-core GEMMs (~22-bit operands, fp32 accumulation),
+so observed errors are ~1e-6.
 """
 import ctypes as C
 import glob
