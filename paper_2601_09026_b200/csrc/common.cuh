@@ -136,24 +136,22 @@ struct EpiArgs {
 constexpr float kGeluC = 0.7978845608028654f;  // tensor.cpp:345
 constexpr float kGeluA = 0.044715f;            // tensor.cpp:346
 
-// tanh(u) = sign(u) (1 - 2 / (exp(2|u|) + 1)); expf is ~1 ulp, so t is
-// accurate to a few ulp in absolute terms, and 1+t (the only way GELU uses
-// it) to fp32 precision -- cheaper than tanhf in the GEMM epilogues.
-__device__ __forceinline__ float tanh_f(float u) {
-  const float e = expf(2.f * fabsf(u));
-  const float t = 1.f - 2.f / (e + 1.f);
-  return copysignf(t, u);
+// tanh-GELU (tensor.cpp:345-372) through the logistic form
+//   0.5 (1 + tanh(u)) = s = 1 / (1 + exp(-2u)),   gelu(v) = v s,
+//   gelu'(v) = s + 2 v s (1 - s) c (1 + 3 a v^2),  u = c (v + a v^3):
+// one exp and one reciprocal per element (few-ulp accurate; exp(-2u) -> inf
+// gives s = 0, the exact limit).
+__device__ __forceinline__ float gelu_s(float v) {
+  const float u = kGeluC * fmaf(kGeluA * v * v, v, v);
+  return __frcp_rn(1.f + expf(-2.f * u));
 }
 
-__device__ __forceinline__ float gelu_f(float v) {
-  const float t = tanh_f(kGeluC * (v + kGeluA * v * v * v));
-  return 0.5f * v * (1.f + t);
-}
+__device__ __forceinline__ float gelu_f(float v) { return v * gelu_s(v); }
 
-__device__ __forceinline__ float gelu_grad_f(float v, float u) {
-  const float t = tanh_f(kGeluC * (v + kGeluA * v * v * v));
-  const float dtanh = (1.f - t * t) * kGeluC * (1.f + 3.f * kGeluA * v * v);
-  return u * (0.5f * (1.f + t) + 0.5f * v * dtanh);
+__device__ __forceinline__ float gelu_grad_f(float v, float up) {
+  const float s = gelu_s(v);
+  const float ds = 2.f * s * (1.f - s) * kGeluC * fmaf(3.f * kGeluA * v, v, 1.f);
+  return up * fmaf(v, ds, s);
 }
 
 // Applies the epilogue to n consecutive columns [col0, col0+n) of one output
@@ -161,14 +159,16 @@ __device__ __forceinline__ float gelu_grad_f(float v, float u) {
 __device__ __forceinline__ double epilogue_row(const EpiArgs& e, int g, int b, int h, int row,
                                                int col0, const float* acc, int n);
 
-// 16 full columns: the same epilogue through 128-bit loads/stores
-__device__ __forceinline__ double epilogue_row16(const EpiArgs& e, int g, int b, int h, int row,
-                                                 int col0, const float* acc) {
+// W (a multiple of 4) full columns: the same epilogue through 128-bit
+// loads/stores (W = 4: one float4 per thread, lanes along a row)
+template <int W>
+__device__ __forceinline__ double epilogue_rowv(const EpiArgs& e, int g, int b, int h, int row,
+                                                int col0, const float* acc) {
   double r2 = 0.0;
   const float* bias = e.bias.ok() ? e.bias.at(g) + col0 : nullptr;
-  float bv[16];
+  float bv[W];
 #pragma unroll
-  for (int i = 0; i < 16; i += 4) {
+  for (int i = 0; i < W; i += 4) {
     if (bias) {
       const float4 t = *reinterpret_cast<const float4*>(bias + i);
       bv[i] = t.x; bv[i + 1] = t.y; bv[i + 2] = t.z; bv[i + 3] = t.w;
@@ -178,29 +178,29 @@ __device__ __forceinline__ double epilogue_row16(const EpiArgs& e, int g, int b,
   }
   auto ld4 = [](const float* p, float* v) {
 #pragma unroll
-    for (int i = 0; i < 16; i += 4) {
+    for (int i = 0; i < W; i += 4) {
       const float4 t = *reinterpret_cast<const float4*>(p + i);
       v[i] = t.x; v[i + 1] = t.y; v[i + 2] = t.z; v[i + 3] = t.w;
     }
   };
   auto st4 = [](float* p, const float* v) {
 #pragma unroll
-    for (int i = 0; i < 16; i += 4)
+    for (int i = 0; i < W; i += 4)
       *reinterpret_cast<float4*>(p + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
   };
-  float o[16], t1[16];
+  float o[W], t1[W];
   switch (e.kind) {
     case EPI_STORE: {
 #pragma unroll
-      for (int i = 0; i < 16; ++i) o[i] = bias ? e.alpha * acc[i] + bv[i] : e.alpha * acc[i];
+      for (int i = 0; i < W; ++i) o[i] = bias ? e.alpha * acc[i] + bv[i] : e.alpha * acc[i];
       st4(e.out1.at(g, b, h) + (long long)row * e.out1.ld + col0, o);
     } break;
     case EPI_BIAS_ADD2: {
-      float a2[16];
+      float a2[W];
       ld4(e.add2.at(g) + (long long)row * e.add2.ld + col0, a2);
       if (e.add1.ok()) ld4(e.add1.at(g) + (long long)row * e.add1.ld + col0, t1);
 #pragma unroll
-      for (int i = 0; i < 16; ++i) {
+      for (int i = 0; i < W; ++i) {
         const float a = acc[i] + bv[i];
         o[i] = e.add1.ok() ? t1[i] + a : a;
         t1[i] = a2[i] + o[i];
@@ -210,7 +210,7 @@ __device__ __forceinline__ double epilogue_row16(const EpiArgs& e, int g, int b,
     } break;
     case EPI_BIAS_GELU: {
 #pragma unroll
-      for (int i = 0; i < 16; ++i) {
+      for (int i = 0; i < W; ++i) {
         o[i] = acc[i] + bv[i];
         t1[i] = gelu_f(o[i]);
       }
@@ -220,18 +220,18 @@ __device__ __forceinline__ double epilogue_row16(const EpiArgs& e, int g, int b,
     case EPI_GELU_BWD: {
       ld4(e.aux.at(g) + (long long)row * e.aux.ld + col0, t1);
 #pragma unroll
-      for (int i = 0; i < 16; ++i) o[i] = gelu_grad_f(t1[i], acc[i]);
+      for (int i = 0; i < W; ++i) o[i] = gelu_grad_f(t1[i], acc[i]);
       st4(e.out1.at(g) + (long long)row * e.out1.ld + col0, o);
     } break;
     case EPI_GRAD_ACC: {
       float* p = e.out1.at(g) + (long long)row * e.out1.ld + col0;
       ld4(p, t1);
 #pragma unroll
-      for (int i = 0; i < 16; ++i) o[i] = t1[i] + e.gscale * acc[i];
+      for (int i = 0; i < W; ++i) o[i] = t1[i] + e.gscale * acc[i];
       st4(p, o);
     } break;
     default:
-      return epilogue_row(e, g, b, h, row, col0, acc, 16);
+      return epilogue_row(e, g, b, h, row, col0, acc, W);
   }
   return r2;
 }

@@ -685,6 +685,7 @@ void Engine::attention_fwd(int G, Mat Q, Mat K, Mat V, Mat O, Mat P, int sq, int
   sm.scale = (float)(1.0 / std::sqrt((double)dh));
   sm.S = P;
   ++launches_;
+  prof_shape_ = {1, sm.ncols, 0, G};
   timed(PROF_ROW, 0.0, 8.0 * G * (double)sm.rows * skv, [&] { launch_softmax(sm, active_, stream_); });
   g = GemmArgs{};
   g.G = G;
@@ -749,6 +750,7 @@ void Engine::attention_bwd(int G, Mat Q, Mat K, Mat V, Mat P, Mat dO, Mat dP, Ma
   sm.S = P;
   sm.dS = dP;
   ++launches_;
+  prof_shape_ = {2, sm.ncols, 0, G};
   timed(PROF_ROW, 0.0, 12.0 * G * (double)sm.rows * skv, [&] { launch_softmax(sm, active_, stream_); });
   mk(skv, dh, sq, P, true, dO, true, dV, 1.f);     // dV = P^T . dO
   mk(sq, dh, skv, dP, false, K, true, dQ, scale);  // dQ = dS . K / sqrt(dh)
@@ -783,7 +785,7 @@ int Engine::dump_profile(double* out, int max_rows) {
     o[2] = r.shape[1];
     o[3] = r.shape[2];
     o[4] = r.shape[3];
-    o[5] = r.flops;
+    o[5] = r.cls == PROF_ROW ? r.bytes : r.flops;  // row kernels: HBM bytes
     o[6] = t;
     ++n;
   }
@@ -886,6 +888,7 @@ void Engine::encoder_forward(const EvalSpec& e, int R, bool causal, Mat X, Mat Y
   ln.gain = par(L.ln1_g, 0, l0, ls);
   ln.bias = par(L.ln1_b, 0, l0, ls);
   ++launches_;
+  prof_shape_ = {3, ln.d, 0, ln.G};
   timed(PROF_ROW, 0.0, 8.0 * ln.G * (double)ln.rows * ln.d,
         [&] { launch_ln_fwd(ln, active_, stream_); });
 
@@ -925,6 +928,7 @@ void Engine::encoder_forward(const EvalSpec& e, int R, bool causal, Mat X, Mat Y
   ln.gain = par(L.ln2_g, 0, l0, ls);
   ln.bias = par(L.ln2_b, 0, l0, ls);
   ++launches_;
+  prof_shape_ = {3, ln.d, 0, ln.G};
   timed(PROF_ROW, 0.0, 8.0 * ln.G * (double)ln.rows * ln.d,
         [&] { launch_ln_fwd(ln, active_, stream_); });
 
@@ -976,7 +980,9 @@ void Engine::encoder_forward(const EvalSpec& e, int R, bool causal, Mat X, Mat Y
     if (cy.mode == CM_RES0) cy.norm_base = e.cmb.norm_base + part_off_elem_;
     ec.cmb = cy;
     ++launches_;
-    launch_elem_combine(ec, active_, stream_);
+    prof_shape_ = {6, 0, 0, ec.G};
+    timed(PROF_ROW, 0.0, 12.0 * ec.G * (double)ec.n,
+          [&] { launch_elem_combine(ec, active_, stream_); });
   }
 }
 
@@ -1008,6 +1014,7 @@ void Engine::decoder_forward(const EvalSpec& e) {
   ln.gain = par(L.ln1_g, 0, l0, ls);
   ln.bias = par(L.ln1_b, 0, l0, ls);
   ++launches_;
+  prof_shape_ = {3, ln.d, 0, ln.G};
   timed(PROF_ROW, 0.0, 8.0 * ln.G * (double)ln.rows * ln.d,
         [&] { launch_ln_fwd(ln, active_, stream_); });
 
@@ -1044,6 +1051,7 @@ void Engine::decoder_forward(const EvalSpec& e) {
   ln.gain = par(L.ln3_g, 0, l0, ls);
   ln.bias = par(L.ln3_b, 0, l0, ls);
   ++launches_;
+  prof_shape_ = {3, ln.d, 0, ln.G};
   timed(PROF_ROW, 0.0, 8.0 * ln.G * (double)ln.rows * ln.d,
         [&] { launch_ln_fwd(ln, active_, stream_); });
 
@@ -1076,6 +1084,7 @@ void Engine::decoder_forward(const EvalSpec& e) {
   ln.gain = par(L.ln2_g, 0, l0, ls);
   ln.bias = par(L.ln2_b, 0, l0, ls);
   ++launches_;
+  prof_shape_ = {3, ln.d, 0, ln.G};
   timed(PROF_ROW, 0.0, 8.0 * ln.G * (double)ln.rows * ln.d,
         [&] { launch_ln_fwd(ln, active_, stream_); });
 
@@ -1107,7 +1116,9 @@ void Engine::decoder_forward(const EvalSpec& e) {
     if (cx.mode == CM_RES0) cx.norm_base = e.cmb.norm_base + part_off_elem_;
     ec.cmb = cx;
     ++launches_;
-    launch_elem_combine(ec, active_, stream_);
+    prof_shape_ = {6, 0, 0, ec.G};
+    timed(PROF_ROW, 0.0, 12.0 * ec.G * (double)ec.n,
+          [&] { launch_elem_combine(ec, active_, stream_); });
   }
 }
 
@@ -1207,6 +1218,7 @@ void Engine::encoder_adjoint(const EvalSpec& e, bool causal) {
     lb.out2 = da1;
     lb.addB = UP;
     ++launches_;
+    prof_shape_ = {4, lb.d, 0, lb.G};
     timed(PROF_ROW, 0.0, 20.0 * lb.G * (double)lb.rows * lb.d,
           [&] { launch_ln_bwd(lb, active_, stream_); });
 
@@ -1242,6 +1254,7 @@ void Engine::encoder_adjoint(const EvalSpec& e, bool causal) {
       if (c.mode == CM_RES0) c.norm_base = e.cmb.norm_base + part_off_ln_;
       l1.cmb = c;
       ++launches_;
+      prof_shape_ = {4, l1.d, 0, l1.G};
       timed(PROF_ROW, 0.0, 20.0 * l1.G * (double)l1.rows * l1.d,
             [&] { launch_ln_bwd(l1, active_, stream_); });
       if (sd_.kind == 2) {
@@ -1254,7 +1267,9 @@ void Engine::encoder_adjoint(const EvalSpec& e, bool causal) {
         if (cy.mode == CM_RES0) cy.norm_base = e.cmb.norm_base + part_off_elem_;
         ec.cmb = cy;
         ++launches_;
-        launch_elem_combine(ec, active_, stream_);
+        prof_shape_ = {6, 0, 0, ec.G};
+        timed(PROF_ROW, 0.0, 12.0 * ec.G * (double)ec.n,
+              [&] { launch_elem_combine(ec, active_, stream_); });
       }
     }
   }
@@ -1288,7 +1303,9 @@ void Engine::encoder_adjoint(const EvalSpec& e, bool causal) {
       if (x.ok()) c.dgain = grad(gn, 0, l0, ls);
       c.gscale = gs;
       ++launches_;
-      launch_colred(c, active_, stream_);
+      prof_shape_ = {5, c.cols, 0, c.G};
+      timed(PROF_ROW, 0.0, (x.ok() ? 8.0 : 4.0) * c.G * (double)c.rows * c.cols,
+            [&] { launch_colred(c, active_, stream_); });
     };
     wg(d, f, UP, gg, L.w_out, f);
     cr(UP, d, L.b_out, Mat{}, Mat{}, 0);
@@ -1362,6 +1379,7 @@ void Engine::decoder_adjoint(const EvalSpec& e) {
     lb.out2 = dybar;   // up + du2
     lb.addB = UPy;
     ++launches_;
+    prof_shape_ = {4, lb.d, 0, lb.G};
     timed(PROF_ROW, 0.0, 20.0 * lb.G * (double)lb.rows * lb.d,
           [&] { launch_ln_bwd(lb, active_, stream_); });
 
@@ -1391,6 +1409,7 @@ void Engine::decoder_adjoint(const EvalSpec& e) {
     lb.addB = dybar;
     lb.out2 = da1;    // dybar + du3
     ++launches_;
+    prof_shape_ = {4, lb.d, 0, lb.G};
     timed(PROF_ROW, 0.0, 20.0 * lb.G * (double)lb.rows * lb.d,
           [&] { launch_ln_bwd(lb, active_, stream_); });
 
@@ -1426,6 +1445,7 @@ void Engine::decoder_adjoint(const EvalSpec& e) {
       if (c.mode == CM_RES0) c.norm_base = e.cmb.norm_base + part_off_ln_;
       l1.cmb = c;
       ++launches_;
+      prof_shape_ = {4, l1.d, 0, l1.G};
       timed(PROF_ROW, 0.0, 20.0 * l1.G * (double)l1.rows * l1.d,
             [&] { launch_ln_bwd(l1, active_, stream_); });
       ElemCombineArgs ec;
@@ -1436,7 +1456,9 @@ void Engine::decoder_adjoint(const EvalSpec& e) {
       if (cx.mode == CM_RES0) cx.norm_base = e.cmb.norm_base + part_off_elem_;
       ec.cmb = cx;
       ++launches_;
-      launch_elem_combine(ec, active_, stream_);
+      prof_shape_ = {6, 0, 0, ec.G};
+      timed(PROF_ROW, 0.0, 12.0 * ec.G * (double)ec.n,
+            [&] { launch_elem_combine(ec, active_, stream_); });
     }
   }
 
@@ -1469,7 +1491,9 @@ void Engine::decoder_adjoint(const EvalSpec& e) {
       if (x.ok()) c.dgain = grad(gn, 0, l0, ls);
       c.gscale = gs;
       ++launches_;
-      launch_colred(c, active_, stream_);
+      prof_shape_ = {5, c.cols, 0, c.G};
+      timed(PROF_ROW, 0.0, (x.ok() ? 8.0 : 4.0) * c.G * (double)c.rows * c.cols,
+            [&] { launch_colred(c, active_, stream_); });
     };
     wg(d, f, R, UPy, gg, L.w_out, f);
     cr(R, UPy, d, L.b_out, Mat{}, Mat{}, 0);
@@ -1650,8 +1674,11 @@ void Engine::restrict_to(Solver& s, int level) {  // mgrit.hpp:199-211
   const int lo = s.p_lo[level], hi = s.p_hi[level];
   // v = base on our points and the ghost (the coarsest level only needs its
   // initial condition: exact_solve overwrites every other point)
-  launch_copy(coarsest ? 1 : hi - lo + 1, state_n_, lv_v(s, level, lo, 1),
-              lv_base(s, level, lo, 1), active_, stream_);
+  prof_shape_ = {7, 0, 0, coarsest ? 1 : hi - lo + 1};
+  timed(PROF_ROW, 0.0, 8.0 * (coarsest ? 1 : hi - lo + 1) * (double)state_n_, [&] {
+    launch_copy(coarsest ? 1 : hi - lo + 1, state_n_, lv_v(s, level, lo, 1),
+                lv_base(s, level, lo, 1), active_, stream_);
+  });
   ++launches_;
   Combine cm;
   cm.mode = CM_PLAIN;
@@ -1663,8 +1690,11 @@ void Engine::correct_from(Solver& s, int level) {  // mgrit.hpp:214-223
   // our coarse points and the ghost (its coarse value arrived with the
   // coarse chain / ghost exchange, so the correction is bitwise the owner's)
   const int k0 = std::max(s.p_lo[level], 1), hi = s.p_hi[level];
-  launch_correct(hi - k0 + 1, state_n_, lv_v(s, level - 1, k0 * cfg_.coarsen, cfg_.coarsen),
-                 lv_v(s, level, k0, 1), lv_base(s, level, k0, 1), active_, stream_);
+  prof_shape_ = {8, 0, 0, hi - k0 + 1};
+  timed(PROF_ROW, 0.0, 16.0 * (hi - k0 + 1) * (double)state_n_, [&] {
+    launch_correct(hi - k0 + 1, state_n_, lv_v(s, level - 1, k0 * cfg_.coarsen, cfg_.coarsen),
+                   lv_v(s, level, k0, 1), lv_base(s, level, k0, 1), active_, stream_);
+  });
   ++launches_;
 }
 

@@ -52,7 +52,8 @@ constexpr int ROWS = 128;       // operand rows per CTA per stage (A and B)
 constexpr int STAGES = 3;
 constexpr int TILE_BYTES = ROWS * BK * 4;  // 16 KiB: fp32 staging tile == hi|lo tile
 constexpr int STAGE_BYTES = 4 * TILE_BYTES;  // stgA, stgB, hlA, hlB
-constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 512 /*barriers*/;
+// + barriers (512 B) + per-epilogue-warp 32 x 16 fp32 transpose buffers
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 512 + 8 * 2048;
 constexpr int BSLOTS = 2 * STAGES;  // ring depth of a pre-split B
 constexpr float kLoScale = 2048.f, kLoInv = 1.f / 2048.f;
 
@@ -547,6 +548,7 @@ __global__ void __launch_bounds__(Cfg<CG>::THREADS, 1)
     constexpr int COLS = TN / CG;  // columns per epilogue warp
     const bool res0 = p.ep.kind == EPI_FINAL && p.ep.cmb.mode == CM_RES0;
     const uint32_t tempty_leader = CG == 2 ? map_to_rank(smem_u32(&tempty[0]), 0) : 0u;
+    const uint32_t ebuf = smem_u32(smem + STAGES * STAGE_BYTES + 512) + ew * 2048;
     int tc = 0;
     for (int t = unit; t < total; t += nunits, ++tc) {
       const Tile T = tile_of(t);
@@ -554,7 +556,6 @@ __global__ void __launch_bounds__(Cfg<CG>::THREADS, 1)
       const uint32_t aph = (tc / NACC) & 1;
       mbar_wait(&tfull[acc], aph);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const int row = T.m0 + q * 32 + lane;
       const uint32_t lane_addr =
           tmem_base + (uint32_t)(acc * 2 * TN) + ((uint32_t)(q * 32) << 16);
       double r2 = 0.0;
@@ -565,26 +566,65 @@ __global__ void __launch_bounds__(Cfg<CG>::THREADS, 1)
         tmem_ld16(lane_addr + c, rv);
         if (p.passes > 1) tmem_ld16(lane_addr + TN + c, rw);
         tmem_wait();
-        float v[16];
+        if (c + 16 == (half + 1) * COLS) {
+          // last TMEM read of this tile by this warp: once every epilogue
+          // warp is here, the accumulator can take the next tile's MMAs
+          asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+          asm volatile("bar.sync 2, %0;" ::"n"(32 * C::EPI_WARPS) : "memory");
+          if (ew == 0 && lane == 0) {
+            if (leader)
+              mbar_arrive(&tempty[acc]);
+            else
+              mbar_arrive_cluster(tempty_leader + acc * 8);
+          }
+        }
+        if constexpr (CG == 1) {
+          // small problems (attention, per-layer): lane = row, 16 columns
+          float v[16];
 #pragma unroll
-        for (int i = 0; i < 16; ++i)
-          v[i] = p.passes > 1 ? fmaf(__uint_as_float(rw[i]), kLoInv, __uint_as_float(rv[i]))
-                              : __uint_as_float(rv[i]);
-        const int col0 = T.n0 + c;
-        const int nvalid = min(16, p.N - col0);
-        if (row < p.M && nvalid > 0 && !(p.debug & 2))
-          r2 += (nvalid == 16 && p.vec_ok)
-                    ? epilogue_row16(p.ep, T.g, T.b, T.h, row, col0, v)
-                    : epilogue_row(p.ep, T.g, T.b, T.h, row, col0, v, nvalid);
-      }
-      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-      // all epilogue warps of this CTA done with the buffer -> one arrive
-      asm volatile("bar.sync 2, %0;" ::"n"(32 * C::EPI_WARPS) : "memory");
-      if (ew == 0 && lane == 0) {
-        if (leader)
-          mbar_arrive(&tempty[acc]);
-        else
-          mbar_arrive_cluster(tempty_leader + acc * 8);
+          for (int i = 0; i < 16; ++i) {
+            const float mv = __uint_as_float(rv[i]);
+            v[i] = p.passes > 1 ? fmaf(__uint_as_float(rw[i]), kLoInv, mv) : mv;
+          }
+          const int row = T.m0 + q * 32 + lane;
+          const int col0 = T.n0 + c;
+          const int nvalid = min(16, p.N - col0);
+          if (row < p.M && nvalid > 0 && !(p.debug & 2))
+            r2 += (nvalid == 16 && p.vec_ok)
+                      ? epilogue_rowv<16>(p.ep, T.g, T.b, T.h, row, col0, v)
+                      : epilogue_row(p.ep, T.g, T.b, T.h, row, col0, v, nvalid);
+        } else {
+          // lane = row: stage the 32 x 16 chunk in shared memory (16-byte
+          // pieces XOR-swizzled by row pair: conflict-free both ways), then
+          // read it back with 4 lanes per row so every global access of the
+          // epilogue covers 64 contiguous bytes of a row
+#pragma unroll
+          for (int cc = 0; cc < 4; ++cc) {
+            uint4 w4;
+            float* f = reinterpret_cast<float*>(&w4);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const float mv = __uint_as_float(rv[4 * cc + i]);
+              f[i] = p.passes > 1 ? fmaf(__uint_as_float(rw[4 * cc + i]), kLoInv, mv) : mv;
+            }
+            sts128(ebuf + lane * 64 + ((cc ^ ((lane >> 1) & 3)) << 4), w4);
+          }
+          __syncwarp();
+          const int col = T.n0 + c + (lane & 3) * 4;
+          const int nvalid = min(4, p.N - col);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const int r = i * 8 + (lane >> 2), cc = lane & 3;
+            const float4 w = lds128(ebuf + r * 64 + ((cc ^ ((r >> 1) & 3)) << 4));
+            const float v[4] = {w.x, w.y, w.z, w.w};
+            const int row = T.m0 + q * 32 + r;
+            if (row < p.M && nvalid > 0 && !(p.debug & 2))
+              r2 += (nvalid == 4 && p.vec_ok)
+                        ? epilogue_rowv<4>(p.ep, T.g, T.b, T.h, row, col, v)
+                        : epilogue_row(p.ep, T.g, T.b, T.h, row, col, v, nvalid);
+          }
+          __syncwarp();
+        }
       }
       if (res0) {
         // one partial per (128-row, TN-column) tile of this CTA
@@ -831,11 +871,13 @@ void launch_cg(const GemmArgs& a, const int* active, cudaStream_t s) {
 // choice depends only on (M, N), so a given layer GEMM always runs the same
 // kernel (bitwise determinism of Phi does not depend on the family size)
 bool use_pair(const GemmArgs& a) {
+  // MGLP_GEMM_NO_PAIR: bitmask over EpiKind (bit k: epilogue kind k stays on
+  // the 1-CTA kernel, whose double-buffered TMEM overlaps the epilogue)
   static const int off = [] {
     const char* e = getenv("MGLP_GEMM_NO_PAIR");
-    return e ? atoi(e) : 0;
+    return e ? (int)strtol(e, nullptr, 0) : 0;
   }();
-  return !off && a.M >= 256 && a.N >= 256;
+  return !((off >> a.ep.kind) & 1) && a.M >= 256 && a.N >= 256;
 }
 
 }  // namespace

@@ -51,8 +51,15 @@ for cls, M, Nn, K, b, fl, ms in rows:
     agg[key][2] += fl
 tot = rows[:, 6].sum()
 print(f"{name}: {n.value} launches, {tot:.1f} ms in profiled kernels")
-for key, (cnt, ms, fl) in sorted(agg.items(), key=lambda kv: -kv[1][1])[:40]:
+ROWK = {0: "row?", 1: "softmax", 2: "softmax_bwd", 3: "ln_fwd", 4: "ln_bwd", 5: "colred",
+        6: "combine", 7: "copy", 8: "correct"}
+for key, (cnt, ms, fl) in sorted(agg.items(), key=lambda kv: -kv[1][1])[:60]:
     cls, M, Nn, K, b = key
+    if cls == 2:  # row kernel: (kind, cols, -, G); fl = HBM bytes
+        gbs = fl / (ms * 1e-3) / 1e9 if ms > 0 else 0
+        print(f"row   {ROWK.get(M, M):12s} cols {Nn:5d}   x{b:5d}  n={cnt:4d}  {ms:8.2f} ms "
+              f"({100*ms/tot:5.1f}%)  {gbs:7.0f} GB/s")
+        continue
     tf = fl / (ms * 1e-3) / 1e12 if ms > 0 else 0
     label = ["gemm", "other", "row"][cls]
     print(f"{label:5s} M{M:6d} N{Nn:5d} K{K:5d} x{b:5d}  n={cnt:4d}  {ms:8.2f} ms ({100*ms/tot:5.1f}%)  {tf:7.1f} TF/s")
