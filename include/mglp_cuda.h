@@ -11,8 +11,9 @@
  * State{x, y} layout (blocks.hpp:70-73): x [batch, s_x, d] followed by
  * y [batch, s_y, d] (y absent unless the stack is encoder-decoder).
  * Parameters and gradients are flat float64 arrays in visit_params order
- * (blocks.cpp:627-646). On the device everything is fp32 with tf32x3 tensor
- * core GEMMs; results agree with the f64 reference to ~1e-5 relative.
+ * (blocks.cpp:627-646). On the device everything is fp32 with 3-pass
+ * fp16-split tensor-core GEMMs (~22-bit operands, fp32 accumulation);
+ * results agree with the f64 reference to ~1e-5 relative.
  *
  * Status codes mirror the reference's error taxonomy (errors.hpp:25-35,
  * tools/main.cpp:244-252): 0 ok, 1 ValidationError (bad input / config),
@@ -235,6 +236,71 @@ mglp_status mglp_test_gemm(int G, int M, int N, int K, const float* A, long long
  * (EPI_STORE epilogue, device-resident synthetic operands), device-timed. */
 mglp_status mglp_bench_gemm(int G, int M, int N, int K, int a_mn, int b_mn, int b_presplit,
                             int reps, float* ms_per_launch);
+
+/* ---- training edge: the reference's Trainer::run_update on the device ----
+ * (training.cpp:230-268): make_batch (tasks.cpp:45-89, bit-exact tokens),
+ * Model::embed / logits / cross_entropy / head_backward / embed_backward
+ * (model.cpp:133-275) and Optimizer::step (optimizer.cpp:43-88, f64 master
+ * parameters and moments), around the layer-parallel engine. Parameters are
+ * flat float64 arrays in Model::param_tensors order (model.cpp:74-92). */
+
+/* TaskSpec (tasks.hpp:24-42); kind 0 copy_sequence, 1 token_classification,
+ * 2 tiny_translation */
+typedef struct {
+  int kind;
+  int vocab, seq_len, train_size, val_size;
+  unsigned long long seed;
+} mglp_task_desc;
+
+/* OptConfig (optimizer.hpp:24-34); kind 0 sgd, 1 adam, 2 adamw */
+typedef struct {
+  int kind;
+  double lr, beta1, beta2, eps, weight_decay, momentum;
+} mglp_opt_desc;
+
+typedef struct mglp_trainer mglp_trainer;
+
+/* Trainer(task, ModelConfig{stack, vocab, max_seq}, TrainConfig) +
+ * Model(mcfg, seed) init (training.cpp:74-90, model.cpp:50-72) */
+mglp_status mglp_trainer_create(const mglp_stack_desc* stack, const mglp_solve_config* solve,
+                                const mglp_task_desc* task, const mglp_opt_desc* opt, int vocab,
+                                int max_seq, int batch_size, unsigned long long seed, int device,
+                                mglp_trainer** out);
+mglp_status mglp_trainer_destroy(mglp_trainer* t);
+/* run_update(k, parallel, apply) (training.cpp:230-268): loss of batch k */
+mglp_status mglp_trainer_update(mglp_trainer* t, long long k, int parallel, int apply,
+                                double* loss);
+/* evaluate() (training.cpp:296-310): validation token accuracy */
+mglp_status mglp_trainer_evaluate(mglp_trainer* t, double* accuracy);
+mglp_status mglp_trainer_num_params(mglp_trainer* t, long long* n);
+mglp_status mglp_trainer_get_params(mglp_trainer* t, double* flat);
+mglp_status mglp_trainer_set_params(mglp_trainer* t, const double* flat);
+/* gradients of the last update (zeroed at the start of every update) */
+mglp_status mglp_trainer_get_grads(mglp_trainer* t, double* flat);
+/* logits of the last update / evaluation batch, [batch*seq][vocab] */
+mglp_status mglp_trainer_read_logits(mglp_trainer* t, float* out);
+/* test hook: make_batch(task, split, start, batch) on the device
+ * (tasks.cpp:45-89); tgt_in may be NULL for single-stream tasks */
+mglp_status mglp_trainer_read_batch(mglp_trainer* t, int split, long long start, int* src,
+                                    int* tgt_in, int* tgt_out);
+/* the engine's SolveConfig iteration budget (engine_->config(),
+ * training.cpp:118-119, controller.hpp:126-147) and its warm snapshot */
+mglp_status mglp_trainer_get_iters(mglp_trainer* t, int* fwd_iters, int* bwd_iters);
+mglp_status mglp_trainer_set_iters(mglp_trainer* t, int fwd_iters, int bwd_iters);
+mglp_status mglp_trainer_snapshot(mglp_trainer* t);
+mglp_status mglp_trainer_restore(mglp_trainer* t);
+/* residual-norm trace of the last forward (fwd = 1) / adjoint solve */
+mglp_status mglp_trainer_trace(mglp_trainer* t, int fwd, double* out, int cap, int* n,
+                               int* converged);
+/* MGLP v1 checkpoint (checkpoint.cpp:88-180): save writes *len bytes into
+ * out when cap suffices (always reports *len); load overwrites parameters and
+ * optimizer state and reports the stored batch counter and config echo. */
+mglp_status mglp_trainer_save_checkpoint(mglp_trainer* t, long long batch, const char* echo,
+                                         long long echo_len, char* out, long long cap,
+                                         long long* len);
+mglp_status mglp_trainer_load_checkpoint(mglp_trainer* t, const char* blob, long long len,
+                                         long long* batch, char* echo, long long echo_cap,
+                                         long long* echo_len, int* has_optimizer);
 
 #ifdef __cplusplus
 }

@@ -252,3 +252,89 @@ def gaussian_fill_flat(seed, a, n, scale=1.0):
     lib().ref_gaussian_fill_flat(C.c_ulonglong(seed), C.c_ulonglong(a), C.c_double(scale),
                                  _ptr(out), C.c_longlong(n))
     return out
+
+
+# ---- training edge: make_batch, Model init, run_training -----------
+TASK_KIND = {"copy_sequence": 0, "token_classification": 1, "tiny_translation": 2}
+OPT_KIND = {"sgd": 0, "adam": 1, "adamw": 2}
+MODE = {"serial": 0, "layer_parallel": 1, "switching": 2}
+GUESS = {"broadcast": 0, "zero": 1, "warm": 2}
+
+
+def _task_arr(task):
+    return np.array([TASK_KIND[task.kind], task.vocab, task.seq_len, task.train_size,
+                     task.val_size, task.seed], dtype=np.float64)
+
+
+def _model_arr(m):
+    s = m.stack
+    return np.array([KIND[s.kind], s.d, s.heads, s.ffn, s.n_enc, s.n_dec, s.buffer_open,
+                     s.buffer_close, s.base_h, s.init_std, float(s.depth_scaled_init), s.dropout,
+                     m.vocab, m.max_seq], dtype=np.float64)
+
+
+def _train_arr(t):
+    so, ind, o = t.solve, t.indicator, t.opt
+    return np.array([MODE[t.mode], OPT_KIND[o.kind], o.lr, o.beta1, o.beta2, o.eps,
+                     o.weight_decay, o.momentum, so.coarsen, so.levels, so.fwd_iters,
+                     so.bwd_iters, so.fwd_tol, so.bwd_tol, GUESS[so.cold_guess],
+                     float(so.warm_start), ind.probe_period, ind.threshold, ind.policy,
+                     ind.max_iter_cap, float(ind.use_probe_gradient), t.batch_size, t.epochs,
+                     t.seed, t.manual_switch_batch, t.val_every], dtype=np.float64)
+
+
+def make_batch(task, split, start, batch):
+    """tasks.cpp:45-89 -> (src, tgt_in or None, tgt_out) int32 [batch*seq]"""
+    n = batch * task.seq_len
+    src, tin, tout = (np.zeros(n, dtype=np.int32) for _ in range(3))
+    ip = lambda a: a.ctypes.data_as(C.POINTER(C.c_int))  # noqa: E731
+    _check(lib().ref_make_batch(TASK_KIND[task.kind], task.vocab, task.seq_len, task.train_size,
+                                task.val_size, C.c_ulonglong(task.seed), split,
+                                C.c_longlong(start), batch, ip(src), ip(tin), ip(tout)))
+    return src, (tin if task.kind == "tiny_translation" else None), tout
+
+
+def model_params(mcfg, seed):
+    """Model(mcfg, seed).param_tensors() (model.cpp:50-92) -> (flat, shapes)"""
+    m = _model_arr(mcfg)
+    n, k = C.c_longlong(), C.c_longlong()
+    _check(lib().ref_model_params(_ptr(m), C.c_ulonglong(seed), None, C.byref(n), None,
+                                  C.byref(k)))
+    flat = np.zeros(n.value)
+    sh = np.zeros(k.value, dtype=np.int64)
+    _check(lib().ref_model_params(_ptr(m), C.c_ulonglong(seed), _ptr(flat), C.byref(n),
+                                  sh.ctypes.data_as(C.POINTER(C.c_longlong)), C.byref(k)))
+    shapes, i = [], 0
+    while i < len(sh):
+        r = int(sh[i])
+        shapes.append(tuple(int(x) for x in sh[i + 1:i + 1 + r]))
+        i += 1 + r
+    return flat, shapes
+
+
+def config_echo(task, mcfg, tcfg) -> str:
+    t, m, r = _task_arr(task), _model_arr(mcfg), _train_arr(tcfg)
+    n = C.c_longlong()
+    buf = C.create_string_buffer(4096)
+    _check(lib().ref_config_echo(_ptr(t), _ptr(m), _ptr(r), buf, 4096, C.byref(n)))
+    return buf.raw[: n.value].decode()
+
+
+def run_training(task, mcfg, tcfg, start_state: bytes = b""):
+    """run_training (training.cpp:348-360) -> dict(csv, final_state,
+    switch_state, switch_batch)"""
+    t, m, r = _task_arr(task), _model_arr(mcfg), _train_arr(tcfg)
+    L = lib()
+    csv_len, st_len, sw_len, sw_b = (C.c_longlong() for _ in range(4))
+    args = (_ptr(t), _ptr(m), _ptr(r), start_state or None, C.c_longlong(len(start_state or b"")))
+    _check(L.ref_run_training(*args, None, 0, C.byref(csv_len), None, 0, C.byref(st_len), None,
+                              C.byref(sw_len), C.byref(sw_b)))
+    # the run is deterministic: re-run with buffers sized from the first call
+    cap = max(st_len.value, sw_len.value)
+    csv = C.create_string_buffer(csv_len.value + 1)
+    st = C.create_string_buffer(cap + 1)
+    sw = C.create_string_buffer(cap + 1)
+    _check(L.ref_run_training(*args, csv, csv_len.value + 1, C.byref(csv_len), st, cap + 1,
+                              C.byref(st_len), sw, C.byref(sw_len), C.byref(sw_b)))
+    return {"csv": csv.raw[: csv_len.value].decode(), "final_state": st.raw[: st_len.value],
+            "switch_state": sw.raw[: sw_len.value], "switch_batch": sw_b.value}

@@ -13,6 +13,11 @@
 //   ref_engine_*         LayerParallelEngine (adjoint.hpp:99-219)
 //   ref_scalar_*         MgritSolver<ScalarLinearSystem> (mgrit.hpp, systems.hpp:30-71)
 //   ref_decide           controller.hpp:71-84
+//   ref_make_batch       make_batch (tasks.cpp:45-89)
+//   ref_model_*          Model ctor / param_tensors (model.cpp:50-100)
+//   ref_run_training     run_training -> metrics CSV + final MGLP v1
+//                        checkpoint (training.cpp:92-135, 315-352;
+//                        checkpoint.cpp:88-112)
 // State buffers are flat f64: x [B,s_x,d] followed by y [B,s_y,d] (y absent
 // when s_y == 0), exactly the State{x,y} of blocks.hpp:70-73.
 // Status: 0 ok, 1 ValidationError, 2 ContractViolation / other (errors.hpp:25-35).
@@ -30,6 +35,11 @@
 #include "mglp/mgrit.hpp"
 #include "mglp/rng.hpp"
 #include "mglp/systems.hpp"
+#include "mglp/checkpoint.hpp"
+#include "mglp/model.hpp"
+#include "mglp/optimizer.hpp"
+#include "mglp/tasks.hpp"
+#include "mglp/training.hpp"
 
 using namespace mglp;
 
@@ -412,6 +422,154 @@ void ref_gaussian_fill_flat(unsigned long long seed, unsigned long long a,
                             double scale, double* out, long long n) {
   for (long long i = 0; i < n; ++i)
     out[i] = scale * rng::gaussian(seed, a, (std::uint64_t)i);
+}
+
+// ---- training edge ----------------------------------------------
+
+int ref_make_batch(int kind, int vocab, int seq, int train_size, int val_size,
+                   unsigned long long seed, int split, long long start, int batch,
+                   int* src, int* tgt_in, int* tgt_out) {
+  return guard([&] {
+    TaskSpec t;
+    t.kind = static_cast<TaskKind>(kind);
+    t.vocab = vocab;
+    t.seq_len = seq;
+    t.train_size = train_size;
+    t.val_size = val_size;
+    t.seed = seed;
+    const TokenBatch b = make_batch(t, split, start, batch);
+    std::memcpy(src, b.src.data(), b.src.size() * sizeof(int));
+    std::memcpy(tgt_out, b.tgt_out.data(), b.tgt_out.size() * sizeof(int));
+    if (tgt_in && !b.tgt_in.empty())
+      std::memcpy(tgt_in, b.tgt_in.data(), b.tgt_in.size() * sizeof(int));
+  });
+}
+
+struct RefRun {
+  TaskSpec task;
+  ModelConfig model;
+  TrainConfig train;
+};
+
+// cfg arrays (all f64 so the ctypes side stays one signature):
+//  task  [kind, vocab, seq, train_size, val_size, seed]
+//  model [kind, d, heads, ffn, n_enc, n_dec, open, close, base_h, init_std,
+//         depth_scaled, dropout, vocab, max_seq]
+//  train [mode, opt_kind, lr, beta1, beta2, eps, wd, momentum, coarsen,
+//         levels, fwd_iters, bwd_iters, fwd_tol, bwd_tol, cold_guess,
+//         warm_start, probe_period, threshold, policy, cap, use_probe_grad,
+//         batch, epochs, seed, manual_switch, val_every]
+static RefRun make_run(const double* t, const double* m, const double* r) {
+  RefRun o;
+  o.task.kind = static_cast<TaskKind>((int)t[0]);
+  o.task.vocab = (int)t[1];
+  o.task.seq_len = (int)t[2];
+  o.task.train_size = (int)t[3];
+  o.task.val_size = (int)t[4];
+  o.task.seed = (std::uint64_t)t[5];
+  StackConfig& c = o.model.stack;
+  c.kind = static_cast<ModelKind>((int)m[0]);
+  c.d = (int)m[1];
+  c.heads = (int)m[2];
+  c.ffn = (int)m[3];
+  c.n_enc = (int)m[4];
+  c.n_dec = (int)m[5];
+  c.buffer_open = (int)m[6];
+  c.buffer_close = (int)m[7];
+  c.base_h = m[8];
+  c.init_std = m[9];
+  c.depth_scaled_init = m[10] != 0.0;
+  c.dropout = m[11];
+  o.model.vocab = (int)m[12];
+  o.model.max_seq = (int)m[13];
+  TrainConfig& tc = o.train;
+  tc.mode = static_cast<TrainMode>((int)r[0]);
+  tc.opt.kind = static_cast<OptKind>((int)r[1]);
+  tc.opt.lr = r[2];
+  tc.opt.beta1 = r[3];
+  tc.opt.beta2 = r[4];
+  tc.opt.eps = r[5];
+  tc.opt.weight_decay = r[6];
+  tc.opt.momentum = r[7];
+  tc.solve.coarsen = (int)r[8];
+  tc.solve.levels = (int)r[9];
+  tc.solve.fwd_iters = (int)r[10];
+  tc.solve.bwd_iters = (int)r[11];
+  tc.solve.fwd_tol = r[12];
+  tc.solve.bwd_tol = r[13];
+  tc.solve.cold_guess = static_cast<InitialGuess>((int)r[14]);
+  tc.solve.warm_start = r[15] != 0.0;
+  tc.indicator.probe_period = (int)r[16];
+  tc.indicator.threshold = r[17];
+  tc.indicator.policy = static_cast<IndicatorPolicy>((int)r[18]);
+  tc.indicator.max_iter_cap = (int)r[19];
+  tc.indicator.use_probe_gradient = r[20] != 0.0;
+  tc.batch_size = (int)r[21];
+  tc.epochs = (int)r[22];
+  tc.seed = (std::uint64_t)r[23];
+  tc.manual_switch_batch = (long long)r[24];
+  tc.val_every = (int)r[25];
+  return o;
+}
+
+// metrics CSV and the final checkpoint (and the handover one, if any); the
+// size outputs are always written, the buffers only when large enough
+int ref_run_training(const double* task, const double* model, const double* train,
+                     const char* start_state, long long start_len, char* csv,
+                     long long csv_cap, long long* csv_len, char* final_state,
+                     long long state_cap, long long* state_len, char* switch_state,
+                     long long* switch_len, long long* switch_batch) {
+  return guard([&] {
+    const RefRun r = make_run(task, model, train);
+    const std::string start =
+        start_state ? std::string(start_state, (std::size_t)start_len) : std::string();
+    const TrainResult res = run_training(r.task, r.model, r.train, start);
+    *csv_len = (long long)res.csv.size();
+    if (csv && (long long)res.csv.size() <= csv_cap)
+      std::memcpy(csv, res.csv.data(), res.csv.size());
+    *state_len = (long long)res.final_state.size();
+    if (final_state && (long long)res.final_state.size() <= state_cap)
+      std::memcpy(final_state, res.final_state.data(), res.final_state.size());
+    *switch_len = (long long)res.switch_state.size();
+    *switch_batch = res.switch_batch;
+    if (switch_state && (long long)res.switch_state.size() <= state_cap)
+      std::memcpy(switch_state, res.switch_state.data(), res.switch_state.size());
+  });
+}
+
+// config_echo (training.cpp:329-346)
+int ref_config_echo(const double* task, const double* model, const double* train, char* out,
+                    long long cap, long long* len) {
+  return guard([&] {
+    const RefRun r = make_run(task, model, train);
+    const std::string e = config_echo(r.task, r.model, r.train);
+    *len = (long long)e.size();
+    if (out && (long long)e.size() <= cap) std::memcpy(out, e.data(), e.size());
+  });
+}
+
+// Model(cfg, seed) parameters in param_tensors order (model.cpp:74-92) and
+// their shapes (rank-prefixed dims, one tensor after another)
+int ref_model_params(const double* model, unsigned long long seed, double* flat,
+                     long long* n_flat, long long* shapes, long long* n_shapes) {
+  return guard([&] {
+    RefRun r = make_run(std::vector<double>(6, 1.0).data(), model,
+                        std::vector<double>(26, 0.0).data());
+    Model mdl(r.model, seed);
+    long long n = 0, k = 0;
+    for (Tensor* t : mdl.param_tensors()) {
+      if (flat) std::memcpy(flat + n, t->data(), t->size() * sizeof(double));
+      n += (long long)t->size();
+      if (shapes) shapes[k] = (long long)t->rank();
+      ++k;
+      for (std::size_t a = 0; a < t->rank(); ++a) {
+        if (shapes) shapes[k] = (long long)t->dim(a);
+        ++k;
+      }
+    }
+    *n_flat = n;
+    *n_shapes = k;
+  });
 }
 
 }  // extern "C"

@@ -30,6 +30,17 @@ class StackDesc(C.Structure):
                 ("depth_scaled_init", C.c_int)]
 
 
+class TaskDesc(C.Structure):
+    _fields_ = [("kind", C.c_int), ("vocab", C.c_int), ("seq_len", C.c_int),
+                ("train_size", C.c_int), ("val_size", C.c_int), ("seed", C.c_ulonglong)]
+
+
+class OptDesc(C.Structure):
+    _fields_ = [("kind", C.c_int), ("lr", C.c_double), ("beta1", C.c_double),
+                ("beta2", C.c_double), ("eps", C.c_double), ("weight_decay", C.c_double),
+                ("momentum", C.c_double)]
+
+
 class SolveDesc(C.Structure):
     _fields_ = [("coarsen", C.c_int), ("levels", C.c_int), ("fwd_iters", C.c_int),
                 ("bwd_iters", C.c_int), ("fwd_tol", C.c_double), ("bwd_tol", C.c_double),
@@ -96,6 +107,27 @@ _SIGS = {
     "mglp_test_gemm": [C.c_int, C.c_int, C.c_int, C.c_int, _vp, C.c_longlong, C.c_int, C.c_int,
                        _vp, C.c_longlong, C.c_int, C.c_int, C.c_int, _vp, _vp, C.c_longlong,
                        C.c_int, C.c_int, _ip],
+    "mglp_trainer_create": [C.POINTER(StackDesc), C.POINTER(SolveDesc), C.POINTER(TaskDesc),
+                            C.POINTER(OptDesc), C.c_int, C.c_int, C.c_int, C.c_ulonglong,
+                            C.c_int, C.POINTER(_vp)],
+    "mglp_trainer_destroy": [_vp],
+    "mglp_trainer_update": [_vp, C.c_longlong, C.c_int, C.c_int, _dp],
+    "mglp_trainer_evaluate": [_vp, _dp],
+    "mglp_trainer_num_params": [_vp, _llp],
+    "mglp_trainer_get_params": [_vp, _dp],
+    "mglp_trainer_set_params": [_vp, _dp],
+    "mglp_trainer_get_grads": [_vp, _dp],
+    "mglp_trainer_read_logits": [_vp, _fp],
+    "mglp_trainer_read_batch": [_vp, C.c_int, C.c_longlong, _ip, _ip, _ip],
+    "mglp_trainer_get_iters": [_vp, _ip, _ip],
+    "mglp_trainer_set_iters": [_vp, C.c_int, C.c_int],
+    "mglp_trainer_snapshot": [_vp],
+    "mglp_trainer_restore": [_vp],
+    "mglp_trainer_trace": [_vp, C.c_int, _dp, C.c_int, _ip, _ip],
+    "mglp_trainer_save_checkpoint": [_vp, C.c_longlong, C.c_char_p, C.c_longlong, C.c_char_p,
+                                     C.c_longlong, _llp],
+    "mglp_trainer_load_checkpoint": [_vp, C.c_char_p, C.c_longlong, _llp, C.c_char_p,
+                                     C.c_longlong, _llp, _ip],
     "mglp_bench_gemm": [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
                         C.POINTER(C.c_float)],
 }

@@ -7,6 +7,7 @@
 
 #include "../../include/mglp_cuda.h"
 #include "engine.h"
+#include "trainer.h"
 #include "transport.h"
 
 #include <thread>
@@ -777,6 +778,181 @@ mglp_status mglp_bench_gemm(int G, int M, int N, int K, int a_mn, int b_mn, int 
     cudaEventDestroy(e1);
     for (float* p : {A, B, Cm, hl})
       if (p) cudaFree(p);
+  });
+}
+
+// ---- training edge ---------------------------------------------------------------
+struct mglp_trainer {
+  std::unique_ptr<Trainer> t;
+};
+
+mglp_status mglp_trainer_create(const mglp_stack_desc* stack, const mglp_solve_config* solve,
+                                const mglp_task_desc* task, const mglp_opt_desc* opt, int vocab,
+                                int max_seq, int batch_size, unsigned long long seed, int device,
+                                mglp_trainer** out) {
+  return guard([&] {
+    need(stack, "stack");
+    need(solve, "solve");
+    need(task, "task");
+    need(opt, "opt");
+    need(out, "out");
+    TaskDesc td;
+    td.kind = task->kind;
+    td.vocab = task->vocab;
+    td.seq_len = task->seq_len;
+    td.train_size = task->train_size;
+    td.val_size = task->val_size;
+    td.seed = task->seed;
+    OptDesc od;
+    od.kind = opt->kind;
+    od.lr = opt->lr;
+    od.beta1 = opt->beta1;
+    od.beta2 = opt->beta2;
+    od.eps = opt->eps;
+    od.weight_decay = opt->weight_decay;
+    od.momentum = opt->momentum;
+    auto* h = new mglp_trainer;
+    try {
+      h->t = std::make_unique<Trainer>(to_stack(stack), to_solve(solve), vocab, max_seq, td, od,
+                                       batch_size, seed, device);
+    } catch (...) {
+      delete h;
+      throw;
+    }
+    *out = h;
+  });
+}
+
+mglp_status mglp_trainer_destroy(mglp_trainer* t) {
+  return guard([&] { delete t; });
+}
+
+static Trainer& tr(mglp_trainer* t) {
+  if (!t || !t->t) throw ValidationError("null trainer");
+  return *t->t;
+}
+
+mglp_status mglp_trainer_update(mglp_trainer* t, long long k, int parallel, int apply,
+                                double* loss) {
+  return guard([&] {
+    const double l = tr(t).update(k, parallel != 0, apply != 0);
+    if (loss) *loss = l;
+  });
+}
+
+mglp_status mglp_trainer_evaluate(mglp_trainer* t, double* accuracy) {
+  return guard([&] {
+    need(accuracy, "accuracy");
+    *accuracy = tr(t).evaluate();
+  });
+}
+
+mglp_status mglp_trainer_num_params(mglp_trainer* t, long long* n) {
+  return guard([&] {
+    need(n, "n");
+    *n = tr(t).num_params();
+  });
+}
+
+mglp_status mglp_trainer_get_params(mglp_trainer* t, double* flat) {
+  return guard([&] {
+    need(flat, "flat");
+    tr(t).get_params(flat);
+  });
+}
+
+mglp_status mglp_trainer_set_params(mglp_trainer* t, const double* flat) {
+  return guard([&] {
+    need(flat, "flat");
+    tr(t).set_params(flat);
+  });
+}
+
+mglp_status mglp_trainer_get_grads(mglp_trainer* t, double* flat) {
+  return guard([&] {
+    need(flat, "flat");
+    tr(t).get_grads(flat);
+  });
+}
+
+mglp_status mglp_trainer_read_logits(mglp_trainer* t, float* out) {
+  return guard([&] {
+    need(out, "out");
+    tr(t).read_logits(out);
+  });
+}
+
+mglp_status mglp_trainer_read_batch(mglp_trainer* t, int split, long long start, int* src,
+                                    int* tgt_in, int* tgt_out) {
+  return guard([&] {
+    need(src, "src");
+    need(tgt_out, "tgt_out");
+    tr(t).read_batch(split, start, src, tgt_in, tgt_out);
+  });
+}
+
+mglp_status mglp_trainer_get_iters(mglp_trainer* t, int* fwd_iters, int* bwd_iters) {
+  return guard([&] {
+    const SolveCfg& c = tr(t).engine().config();
+    if (fwd_iters) *fwd_iters = c.fwd_iters;
+    if (bwd_iters) *bwd_iters = c.bwd_iters;
+  });
+}
+
+mglp_status mglp_trainer_set_iters(mglp_trainer* t, int fwd_iters, int bwd_iters) {
+  return guard([&] {
+    if (fwd_iters < 1 || bwd_iters < 1) throw ValidationError("iterations must be >= 1");
+    SolveCfg& c = tr(t).engine().config();
+    c.fwd_iters = fwd_iters;
+    c.bwd_iters = bwd_iters;
+    tr(t).engine().drop_graph();
+  });
+}
+
+mglp_status mglp_trainer_snapshot(mglp_trainer* t) {
+  return guard([&] { tr(t).engine().snapshot(); });
+}
+
+mglp_status mglp_trainer_restore(mglp_trainer* t) {
+  return guard([&] { tr(t).engine().restore(); });
+}
+
+mglp_status mglp_trainer_trace(mglp_trainer* t, int fwd, double* out, int cap, int* n,
+                               int* converged) {
+  return guard([&] {
+    std::vector<double> trace;
+    bool conv = false;
+    tr(t).engine().read_trace(fwd != 0, &trace, &conv);
+    const int m = (int)std::min<size_t>(trace.size(), (size_t)std::max(cap, 0));
+    if (out) std::copy(trace.begin(), trace.begin() + m, out);
+    if (n) *n = (int)trace.size();
+    if (converged) *converged = conv ? 1 : 0;
+  });
+}
+
+mglp_status mglp_trainer_save_checkpoint(mglp_trainer* t, long long batch, const char* echo,
+                                         long long echo_len, char* out, long long cap,
+                                         long long* len) {
+  return guard([&] {
+    need(len, "len");
+    const std::string blob =
+        tr(t).save_checkpoint(batch, echo ? std::string(echo, (size_t)echo_len) : std::string());
+    *len = (long long)blob.size();
+    if (out && (long long)blob.size() <= cap) std::memcpy(out, blob.data(), blob.size());
+  });
+}
+
+mglp_status mglp_trainer_load_checkpoint(mglp_trainer* t, const char* blob, long long len,
+                                         long long* batch, char* echo, long long echo_cap,
+                                         long long* echo_len, int* has_optimizer) {
+  return guard([&] {
+    need(blob, "blob");
+    const CheckpointMeta m = tr(t).load_checkpoint(std::string(blob, (size_t)len));
+    if (batch) *batch = m.batch;
+    if (echo_len) *echo_len = (long long)m.config_echo.size();
+    if (echo && (long long)m.config_echo.size() <= echo_cap)
+      std::memcpy(echo, m.config_echo.data(), m.config_echo.size());
+    if (has_optimizer) *has_optimizer = m.has_optimizer ? 1 : 0;
   });
 }
 

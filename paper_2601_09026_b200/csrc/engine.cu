@@ -1,6 +1,7 @@
 // Host orchestration of the device-resident MGRIT forward solve and adjoint
 // MGRIT backpropagation. See engine.h for the map to the reference.
 #include "engine.h"
+#include "rng.h"
 
 #include <algorithm>
 #include <atomic>
@@ -12,45 +13,6 @@ namespace mglp {
 
 namespace {
 
-// ---- counter-based RNG, bit-identical to rng.hpp:37-89 ------------------------
-inline uint64_t splitmix64(uint64_t x) {
-  x += 0x9e3779b97f4a7c15ULL;
-  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
-  x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
-  return x ^ (x >> 31);
-}
-inline uint64_t derive(uint64_t seed, uint64_t a, uint64_t b, uint64_t c, uint64_t d) {
-  uint64_t s = splitmix64(seed ^ 0x243f6a8885a308d3ULL);
-  s = splitmix64(s ^ a);
-  s = splitmix64(s ^ b);
-  s = splitmix64(s ^ c);
-  s = splitmix64(s ^ d);
-  return s;
-}
-inline double u01(uint64_t bits) { return static_cast<double>(bits >> 11) * 0x1.0p-53; }
-inline double gaussian(uint64_t seed, uint64_t a, uint64_t b, uint64_t c, uint64_t d) {
-  const uint64_t k1 = derive(seed, a, b, c, d);
-  const uint64_t k2 = splitmix64(k1 ^ 0x452821e638d01377ULL);
-  double x1 = u01(k1);
-  const double x2 = u01(k2);
-  if (x1 <= 0.0) x1 = 0x1.0p-53;
-  return std::sqrt(-2.0 * std::log(x1)) * std::cos(6.283185307179586 * x2);
-}
-inline double truncated_gaussian(double stddev, uint64_t seed, uint64_t a, uint64_t b,
-                                 uint64_t c) {
-  for (uint64_t attempt = 0;; ++attempt) {
-    const double g = gaussian(seed, a, b, c, attempt);
-    if (g >= -2.0 && g <= 2.0) return g * stddev;
-  }
-}
-inline uint64_t fnv1a(const std::string& s) {
-  uint64_t h = 0xcbf29ce484222325ULL;
-  for (char ch : s) {
-    h ^= static_cast<unsigned char>(ch);
-    h *= 0x100000001b3ULL;
-  }
-  return h;
-}
 inline long long align32(long long n) { return (n + 31) & ~31LL; }
 
 bool depth_scaled_component(const std::string& c) {  // blocks.cpp:368-372
@@ -346,6 +308,35 @@ void Engine::init_params(uint64_t seed, std::vector<double>* flat_out) {
       }
     });
   for (auto& t : th) t.join();
+}
+
+void Engine::flat_to_slab(const double* flat, double* slab) const {
+  std::fill(slab, slab + slab_elems(), 0.0);
+  long long fo = 0;
+  for (int l = 0; l < total_; ++l) {
+    const LayerLayout& L = lay_[(sd_.kind == 2 && l >= n_split_) ? 1 : 0];
+    double* dst = slab + (size_t)l * layer_stride_;
+    for (const Piece& p : L.pieces)
+      for (long long e = 0; e < p.n; ++e) dst[p.dev_off + e] = flat[fo + p.flat_off + e];
+    fo += L.flat_size;
+  }
+}
+
+void Engine::slab_to_flat(const double* slab, double* flat) const {
+  long long fo = 0;
+  for (int l = 0; l < total_; ++l) {
+    const LayerLayout& L = lay_[(sd_.kind == 2 && l >= n_split_) ? 1 : 0];
+    const double* src = slab + (size_t)l * layer_stride_;
+    for (const Piece& p : L.pieces)
+      for (long long e = 0; e < p.n; ++e) flat[fo + p.flat_off + e] = src[p.dev_off + e];
+    fo += L.flat_size;
+  }
+}
+
+void Engine::params_updated() {
+  MGLP_CUDA(cudaSetDevice(device_));
+  repack_weights();
+  invalidate_linearization();
 }
 
 void Engine::set_params(const double* flat) {

@@ -79,6 +79,18 @@ class Engine {
   void get_params(double* flat) const;
   void get_grads(double* flat_accum) const;  // flat += device grads
   void zero_grads();
+  // device parameter / gradient slabs (fp32, layer-major, kernel layout) and
+  // the host mapping between that layout and the flat visit_params order
+  // (blocks.cpp:627-646): the trainer's optimizer runs over whole slabs
+  float* params_dev() const { return P_; }
+  float* grads_dev() const { return Gr_; }
+  long long slab_elems() const { return (long long)total_ * layer_stride_; }
+  void flat_to_slab(const double* flat, double* slab) const;  // slab zero-filled first
+  void slab_to_flat(const double* slab, double* flat) const;
+  // after P_ changed on the device: re-derive the pre-split GEMM weights
+  void params_updated();
+  long long y_offset() const { return y_off_; }
+  int batch() const { return B_; }
 
   // ---- shape ----
   void set_shape(int batch, int s_x, int s_y);
