@@ -362,6 +362,18 @@ def run_device(args, cfg, rank, world, dist):
         dist.broadcast_object_list(obj, src=0)
         serial_ms = obj[0]
 
+    # monitor probe step (controller.hpp:88-105 ProbeScope: both budgets
+    # doubled for one batch, SURVEY 8(d) GPT row), eager, outside the timed region
+    sdesc = N.SolveDesc()
+    N.call("mglp_engine_get_config", h, C.byref(sdesc))
+    f0, b0 = sdesc.fwd_iters, sdesc.bwd_iters
+    sdesc.fwd_iters, sdesc.bwd_iters = 2 * f0, 2 * b0
+    N.call("mglp_engine_set_config", h, C.byref(sdesc))
+    eager_step()
+    probe_ms = timed(eager_step, 1)
+    sdesc.fwd_iters, sdesc.bwd_iters = f0, b0
+    N.call("mglp_engine_set_config", h, C.byref(sdesc))
+
     # profiled step (outside the timed region) -> per-kernel-class device time
     N.call("mglp_engine_profile", h, 1)
     eager_step()
@@ -455,6 +467,8 @@ def run_device(args, cfg, rank, world, dist):
                                      "fp32 accumulate",
                    "launch": "CUDA graph of the whole step" if use_graph else "eager"},
         "speedup_vs_serial": serial_ms / ms,
+        "monitor_probe_ms_per_step": probe_ms,
+        "monitor_probe_budget": f"fwd={2 * f0} bwd={2 * b0} (ProbeScope doubling, eager launch)",
         "serial_ms_per_step": serial_ms,
         "fwd_trace": fwd_trace, "bwd_trace": bwd_trace,
         "roofline": roofline,
