@@ -233,9 +233,10 @@ mglp_status mglp_test_gemm(int G, int M, int N, int K, const float* A, long long
                            int engine, int* range_flag);
 
 /* ---- micro-benchmark: `reps` launches of one tensor-core GEMM family
- * (EPI_STORE epilogue, device-resident synthetic operands), device-timed. */
+ * (epilogue kind epi: 0 store, 2 bias+GELU (two outputs), 4 GELU-backward;
+ * device-resident synthetic operands), device-timed. */
 mglp_status mglp_bench_gemm(int G, int M, int N, int K, int a_mn, int b_mn, int b_presplit,
-                            int reps, float* ms_per_launch);
+                            int epi, int reps, float* ms_per_launch);
 
 /* ---- training edge: the reference's Trainer::run_update on the device ----
  * (training.cpp:230-268): make_batch (tasks.cpp:45-89, bit-exact tokens),

@@ -129,7 +129,7 @@ _SIGS = {
     "mglp_trainer_load_checkpoint": [_vp, C.c_char_p, C.c_longlong, _llp, C.c_char_p,
                                      C.c_longlong, _llp, _ip],
     "mglp_bench_gemm": [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
-                        C.POINTER(C.c_float)],
+                        C.c_int, C.POINTER(C.c_float)],
 }
 
 EXPORTS = sorted(list(_SIGS) + ["mglp_last_error", "mglp_version"])

@@ -727,9 +727,10 @@ mglp_status mglp_test_gemm(int G, int M, int N, int K, const float* A, long long
 
 // ---- GEMM micro-benchmark (tools/gemm_bench.py) ----
 mglp_status mglp_bench_gemm(int G, int M, int N, int K, int a_mn, int b_mn, int b_presplit,
-                            int reps, float* ms_per_launch) {
+                            int epi, int reps, float* ms_per_launch) {
   return guard([&] {
-    float *A = nullptr, *B = nullptr, *Cm = nullptr, *hl = nullptr;
+    float *A = nullptr, *B = nullptr, *Cm = nullptr, *hl = nullptr, *C2 = nullptr,
+          *bias = nullptr;
     const long long na = (long long)G * M * K, nb = (long long)G * N * K,
                     nc = (long long)G * M * N;
     MGLP_CUDA(cudaMalloc(&A, na * sizeof(float)));
@@ -754,6 +755,21 @@ mglp_status mglp_bench_gemm(int G, int M, int N, int K, int a_mn, int b_mn, int 
     g.ep.out1.ptr = Cm;
     g.ep.out1.slot_stride = (long long)M * N;
     g.ep.out1.ld = N;
+    if (epi == EPI_BIAS_GELU || epi == EPI_GELU_BWD) {
+      MGLP_CUDA(cudaMalloc(&C2, nc * sizeof(float)));
+      MGLP_CUDA(cudaMalloc(&bias, (size_t)N * sizeof(float)));
+      MGLP_CUDA(cudaMemset(C2, 0, nc * sizeof(float)));
+      MGLP_CUDA(cudaMemset(bias, 0, (size_t)N * sizeof(float)));
+      g.ep.kind = epi;
+      Mat m2 = g.ep.out1;
+      m2.ptr = C2;
+      if (epi == EPI_BIAS_GELU) {
+        g.ep.out2 = m2;
+        g.ep.bias.ptr = bias;
+      } else {
+        g.ep.aux = m2;
+      }
+    }
     if (b_presplit) {
       const long long kp = pack_hl_cols(K);
       MGLP_CUDA(cudaMalloc(&hl, (size_t)G * N * kp * sizeof(float)));
@@ -776,7 +792,7 @@ mglp_status mglp_bench_gemm(int G, int M, int N, int K, int a_mn, int b_mn, int 
     *ms_per_launch = ms / reps;
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
-    for (float* p : {A, B, Cm, hl})
+    for (float* p : {A, B, Cm, hl, C2, bias})
       if (p) cudaFree(p);
   });
 }

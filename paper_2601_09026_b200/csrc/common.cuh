@@ -143,7 +143,7 @@ constexpr float kGeluA = 0.044715f;            // tensor.cpp:346
 // gives s = 0, the exact limit).
 __device__ __forceinline__ float gelu_s(float v) {
   const float u = kGeluC * fmaf(kGeluA * v * v, v, v);
-  return __frcp_rn(1.f + expf(-2.f * u));
+  return __fdividef(1.f, 1.f + expf(-2.f * u));  // 1 + e >= 1: the fast reciprocal is exact to 2 ulp
 }
 
 __device__ __forceinline__ float gelu_f(float v) { return v * gelu_s(v); }
@@ -232,6 +232,136 @@ __device__ __forceinline__ double epilogue_rowv(const EpiArgs& e, int g, int b, 
     } break;
     default:
       return epilogue_row(e, g, b, h, row, col0, acc, W);
+  }
+  return r2;
+}
+
+// Four rows x 4 columns (one float4 per row; rows[i] < 0 = invalid): every
+// global operand of the four rows is loaded first, then the math, then the
+// stores -- four independent row segments in flight per thread, so a
+// latency-bound epilogue (operands read from HBM) overlaps its loads.
+// Requires 16-byte aligned rows for every operand (TcParams::vec_ok).
+__device__ __forceinline__ float4 ld4g(const float* p) { return *reinterpret_cast<const float4*>(p); }
+__device__ __forceinline__ void st4g(float* p, float4 v) { *reinterpret_cast<float4*>(p) = v; }
+__device__ __forceinline__ const float* rowp(const Mat& m, int g, long long row, int col) {
+  return m.at(g) + row * m.ld + col;
+}
+
+__device__ __forceinline__ double epilogue_4x4(const EpiArgs& e, int g, int b, int h,
+                                               const int* rows, int col, const float4* acc) {
+  double r2 = 0.0;
+  float4 bv = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (e.bias.ok()) bv = ld4g(e.bias.at(g) + col);
+  auto add = [](float4 a, float4 c) {
+    return make_float4(a.x + c.x, a.y + c.y, a.z + c.z, a.w + c.w);
+  };
+  float4 x1[4], x2[4];
+  switch (e.kind) {
+    case EPI_STORE: {
+      const float al = e.alpha;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        if (rows[i] < 0) continue;
+        const float4 a = acc[i];
+        float4 o = make_float4(al * a.x, al * a.y, al * a.z, al * a.w);
+        if (e.bias.ok()) o = add(o, bv);
+        st4g(e.out1.at(g, b, h) + (long long)rows[i] * e.out1.ld + col, o);
+      }
+    } break;
+    case EPI_BIAS_ADD2: {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        if (rows[i] < 0) continue;
+        x2[i] = ld4g(rowp(e.add2, g, rows[i], col));
+        if (e.add1.ok()) x1[i] = ld4g(rowp(e.add1, g, rows[i], col));
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        if (rows[i] < 0) continue;
+        const float4 a = add(acc[i], bv);
+        const float4 o1 = e.add1.ok() ? add(x1[i], a) : a;
+        if (e.out1.ok()) st4g(e.out1.at(g) + (long long)rows[i] * e.out1.ld + col, o1);
+        if (e.out2.ok()) st4g(e.out2.at(g) + (long long)rows[i] * e.out2.ld + col, add(x2[i], o1));
+      }
+    } break;
+    case EPI_BIAS_GELU: {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        if (rows[i] < 0) continue;
+        const float4 hv = add(acc[i], bv);
+        st4g(e.out1.at(g) + (long long)rows[i] * e.out1.ld + col, hv);
+        st4g(e.out2.at(g) + (long long)rows[i] * e.out2.ld + col,
+             make_float4(gelu_f(hv.x), gelu_f(hv.y), gelu_f(hv.z), gelu_f(hv.w)));
+      }
+    } break;
+    case EPI_GELU_BWD: {
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        if (rows[i] >= 0) x1[i] = ld4g(rowp(e.aux, g, rows[i], col));
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        if (rows[i] < 0) continue;
+        const float4 a = acc[i], v = x1[i];
+        st4g(e.out1.at(g) + (long long)rows[i] * e.out1.ld + col,
+             make_float4(gelu_grad_f(v.x, a.x), gelu_grad_f(v.y, a.y), gelu_grad_f(v.z, a.z),
+                         gelu_grad_f(v.w, a.w)));
+      }
+    } break;
+    case EPI_GRAD_ACC: {
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        if (rows[i] >= 0) x1[i] = ld4g(rowp(e.out1, g, rows[i], col));
+      const float gs = e.gscale;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        if (rows[i] < 0) continue;
+        const float4 a = acc[i], o = x1[i];
+        st4g(e.out1.at(g) + (long long)rows[i] * e.out1.ld + col,
+             make_float4(o.x + gs * a.x, o.y + gs * a.y, o.z + gs * a.z, o.w + gs * a.w));
+      }
+    } break;
+    case EPI_FINAL: {
+      // one row at a time, its (up to five) operands loaded together
+      const Combine& c = e.cmb;
+      const bool fas = c.mode == CM_FAS, res0 = c.mode == CM_RES0, resl = c.mode == CM_RESL;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        if (rows[i] < 0) continue;
+        const float4 a1v = ld4g(rowp(e.add1, g, rows[i], col));
+        const float4 zv = ld4g(rowp(c.z, g, rows[i], col));
+        float4 pb = make_float4(0.f, 0.f, 0.f, 0.f), rh = pb, bs = pb, vv = pb;
+        if (fas || resl) {
+          pb = ld4g(rowp(c.phib, g, rows[i], col));
+          rh = ld4g(rowp(c.rho, g, rows[i], col));
+          bs = ld4g(rowp(c.base, g, rows[i], col));
+        }
+        if (res0 || resl) vv = ld4g(rowp(c.v, g, rows[i], col));
+        const float* a = &acc[i].x;
+        float o[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const float mo = e.bias.ok() ? a[k] + (&bv.x)[k] : a[k];
+          const float F = (&a1v.x)[k] + mo;
+          const float p = (&zv.x)[k] + c.dt * F;
+          if (fas) {
+            const float corr = (p - (&pb.x)[k]) + (&rh.x)[k];
+            o[k] = (&bs.x)[k] + corr;
+          } else if (res0) {
+            const float r = p - (&vv.x)[k];
+            o[k] = r;
+            r2 += (double)r * (double)r;
+          } else if (resl) {
+            const float lhs = (p - (&pb.x)[k]) + (&rh.x)[k];
+            o[k] = lhs - ((&vv.x)[k] - (&bs.x)[k]);
+          } else {
+            o[k] = p;
+          }
+        }
+        if (c.mode != CM_NONE)
+          st4g(c.out.at(g) + (long long)rows[i] * c.out.ld + col,
+               make_float4(o[0], o[1], o[2], o[3]));
+      }
+    } break;
   }
   return r2;
 }

@@ -612,18 +612,25 @@ __global__ void __launch_bounds__(Cfg<CG>::THREADS, 1)
           __syncwarp();
           const int col = T.n0 + c + (lane & 3) * 4;
           const int nvalid = min(4, p.N - col);
+          float4 w[4];
+          int rows[4];
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
             const int r = i * 8 + (lane >> 2), cc = lane & 3;
-            const float4 w = lds128(ebuf + r * 64 + ((cc ^ ((r >> 1) & 3)) << 4));
-            const float v[4] = {w.x, w.y, w.z, w.w};
+            w[i] = lds128(ebuf + r * 64 + ((cc ^ ((r >> 1) & 3)) << 4));
             const int row = T.m0 + q * 32 + r;
-            if (row < p.M && nvalid > 0 && !(p.debug & 2))
-              r2 += (nvalid == 4 && p.vec_ok)
-                        ? epilogue_rowv<4>(p.ep, T.g, T.b, T.h, row, col, v)
-                        : epilogue_row(p.ep, T.g, T.b, T.h, row, col, v, nvalid);
+            rows[i] = (row < p.M && nvalid > 0) ? row : -1;
           }
           __syncwarp();
+          if (!(p.debug & 2)) {
+            if (nvalid == 4 && p.vec_ok) {
+              r2 += epilogue_4x4(p.ep, T.g, T.b, T.h, rows, col, w);
+            } else {
+#pragma unroll
+              for (int i = 0; i < 4; ++i)
+                if (rows[i] >= 0) r2 += epilogue_row(p.ep, T.g, T.b, T.h, rows[i], col, &w[i].x, nvalid);
+            }
+          }
         }
       }
       if (res0) {
@@ -810,7 +817,9 @@ Prepared prepare(const GemmArgs& a) {
                          m.slot_stride % 4 == 0 && m.bstride % 4 == 0 && m.hstride % 4 == 0);
     };
     const EpiArgs& e = a.ep;
-    p.vec_ok = al(e.out1) && al(e.out2) && al(e.add1) && al(e.add2) && al(e.aux) && al(e.bias);
+    const Combine& c = e.cmb;
+    p.vec_ok = al(e.out1) && al(e.out2) && al(e.add1) && al(e.add2) && al(e.aux) && al(e.bias) &&
+               al(c.z) && al(c.out) && al(c.base) && al(c.phib) && al(c.rho) && al(c.v);
   }
   p.a_mn = a.a_mn;
   p.b_direct = a.Bhl.ok() ? 1 : 0;

@@ -8,8 +8,10 @@ import sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2601_09026_b200 import _native as N  # noqa: E402
 
-SHAPES = [  # (name, G, M, N, K, a_mn, b_mn, presplit)
+SHAPES = [  # (name, G, M, N, K, a_mn, b_mn, presplit[, epilogue kind])
     ("mlp_in  fwd", 16, 4096, 3072, 768, 0, 0, 1),
+    ("mlp_in  fwd gelu", 16, 4096, 3072, 768, 0, 0, 1, 2),
+    ("mlp_out dgrad gelu'", 16, 4096, 3072, 768, 0, 1, 1, 4),
     ("mlp_out fwd", 16, 4096, 768, 3072, 0, 0, 1),
     ("qkv     fwd", 16, 4096, 2304, 768, 0, 0, 1),
     ("o       fwd", 16, 4096, 768, 768, 0, 0, 1),
@@ -22,13 +24,13 @@ SHAPES = [  # (name, G, M, N, K, a_mn, b_mn, presplit)
 reps = int(sys.argv[1]) if len(sys.argv) > 1 else 5
 out = {}
 only = os.environ.get("ONLY")
-for name, G, M, Nn, K, amn, bmn, pre in SHAPES:
+for name, G, M, Nn, K, amn, bmn, pre, *epi in SHAPES:
     if only and only not in name:
         continue
     ms = C.c_float()
-    N.call("mglp_bench_gemm", G, M, Nn, K, amn, bmn, pre, reps, C.byref(ms))
+    N.call("mglp_bench_gemm", G, M, Nn, K, amn, bmn, pre, epi[0] if epi else 0, reps, C.byref(ms))
     tf = 2.0 * G * M * Nn * K / (ms.value * 1e-3) / 1e12
-    print(f"{name:14s} G={G:5d} M={M:5d} N={Nn:5d} K={K:5d}  {ms.value:8.3f} ms  {tf:7.1f} TF/s",
+    print(f"{name:20s} G={G:5d} M={M:5d} N={Nn:5d} K={K:5d}  {ms.value:8.3f} ms  {tf:7.1f} TF/s",
           flush=True)
     out[name] = {"ms": ms.value, "tflops": tf}
 os.makedirs("gpurun_out", exist_ok=True)
