@@ -232,6 +232,22 @@ mglp_status mglp_test_gemm(int G, int M, int N, int K, const float* A, long long
                            int b_presplit, const float* bias, float* C, long long c_slot, int ldc,
                            int engine, int* range_flag);
 
+/* ---- test hook: the fused tcgen05 attention (attn_tc.cu) on device buffers ----
+ * Q, K, V (and dO, dQ, dK, dV, O) are [B][s][ld] token rows with head h at
+ * column h*dh (the qkv layout of the layer); P is [B][H][sq][pad4(skv)].
+ * Forward always; with dO set, also the backward (dQ, dK, dV overwritten).
+ * sq, skv <= 128 and multiples of 8, dh 32 or 64 (else status 1). The
+ * reference's attention / vjp_attention (blocks.cpp:142-236). Synchronous. */
+mglp_status mglp_test_attention(int B, int H, int sq, int skv, int dh, int causal, const float* Q,
+                                const float* K, const float* V, int ld, float* O, float* P,
+                                const float* dO, float* dQ, float* dK, float* dV,
+                                int* range_flag);
+
+/* ---- micro-benchmark: `reps` launches of the fused attention over G x B x H
+ * heads of length s (forward, or backward when `backward`), device-timed. */
+mglp_status mglp_bench_attention(int G, int B, int H, int s, int dh, int causal, int backward,
+                                 int reps, float* ms_per_launch);
+
 /* ---- micro-benchmark: `reps` launches of one tensor-core GEMM family
  * (epilogue kind epi: 0 store, 2 bias+GELU (two outputs), 4 GELU-backward;
  * device-resident synthetic operands), device-timed. */

@@ -130,6 +130,8 @@ _SIGS = {
                                      C.c_longlong, _llp, _ip],
     "mglp_bench_gemm": [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
                         C.c_int, C.POINTER(C.c_float)],
+    "mglp_test_attention": [C.c_int] * 6 + [_vp, _vp, _vp, C.c_int] + [_vp] * 6 + [_ip],
+    "mglp_bench_attention": [C.c_int] * 8 + [C.POINTER(C.c_float)],
 }
 
 EXPORTS = sorted(list(_SIGS) + ["mglp_last_error", "mglp_version"])

@@ -1,0 +1,622 @@
+// Fused multi-head attention on tcgen05 for sequences of <= 128 tokens: the
+// device form of the reference's attention / vjp_attention
+// (blocks.cpp:142-236; softmax_rows / vjp_softmax_rows, tensor.cpp:310-342).
+//
+// Persistent kernels, one CTA per SM, looping over the (member g, batch b,
+// head h) problems of a family. Every operand is split into fp16 hi / lo'
+// exactly as in gemm_tc.cu (same ~22-bit operand precision; main and
+// correction products in separate TMEM accumulators), but the whole per-head
+// problem stays on chip:
+//   forward   S = Q K^T (TMEM) -> softmax (one thread per query row and half
+//             of the keys; the reference's scale, -inf causal mask,
+//             max-subtracted exp and 1/sum) -> P (global, for the backward,
+//             and hi/lo' in smem) -> O = P V (TMEM) -> O
+//   backward  dP = dO V^T and dV = P^T dO (TMEM) -> dS = P (dP - rowsum(dP P))
+//             (hi/lo' in smem) -> dQ = dS K / sqrt(dh), dK = dS^T Q / sqrt(dh)
+// replacing 2 + 4 tensor-core GEMM launches and 2 softmax row kernels (and the
+// S / dS round trips through HBM) per attention evaluation.
+//
+// Data movement: rows are fetched with cp.async.bulk into an fp32 staging
+// buffer (completion on an mbarrier, no register cost, the next problem's
+// first operands prefetched while the current one computes) and converted
+// smem -> smem. Every operand is kept ONCE, in its natural row-major
+// orientation, as a pair of fp16 SWIZZLE_128B tiles (hi, lo'): [rows][64
+// columns] blocks, 16-byte chunk c of row r at (c ^ (r & 7)). The same tile
+// is a K-major operand (rows = M/N, K = columns) for one MMA and an MN-major
+// operand (rows = K, columns = M/N; UMMA descriptor LBO = block stride, major
+// bit set in the instruction descriptor) for another, so nothing is ever
+// transposed: Q (S: A, K-major; dK: B, MN-major), K (S: B, K; dQ: B, MN),
+// V (PV: B, MN; dP: B, K), dO (dP: A, K; dV: B, MN), P (PV: A, K; dV: A, MN),
+// dS (dQ: A, K; dK: A, MN).
+#include <cfloat>
+
+#include "kernels.cuh"
+#include "tc_common.cuh"
+
+namespace mglp {
+
+using namespace tc;
+
+namespace {
+
+constexpr int kThreads = 256;  // 8 warps; warp w owns TMEM lanes 32 (w & 3), column half w >> 2
+
+__device__ __forceinline__ int rup(int x, int m) { return (x + m - 1) / m * m; }
+
+// SWIZZLE_128B UMMA descriptor; lbo only matters for MN-major operands with
+// more than one 64-wide MN block
+__device__ __forceinline__ uint64_t desc_sw128(uint32_t addr, uint32_t lbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((addr >> 4) & 0x3FFFu);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
+  d |= (uint64_t)(1024 >> 4) << 32;
+  d |= 1ull << 46;
+  d |= 2ull << 61;
+  return d;
+}
+
+// kind::f16 instruction descriptor: f32 accumulate, f16 A/B, major bits
+__device__ __forceinline__ uint32_t idesc(int N, bool a_mn, bool b_mn) {
+  return (1u << 4) | (a_mn ? 1u << 15 : 0u) | (b_mn ? 1u << 16 : 0u) |
+         ((uint32_t)(N >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+}
+
+// One operand of an MMA: a hi/lo tile pair with `rows` rows, used K-major
+// (K = tile columns) or MN-major (K = tile rows).
+struct Opnd {
+  uint32_t hi, lo;
+  int rows;
+  bool mn;
+  __device__ __forceinline__ uint32_t at(int k16) const {
+    return mn ? (uint32_t)(k16 * 2048) : (uint32_t)((k16 >> 2) * rows * 128 + (k16 & 3) * 32);
+  }
+  __device__ __forceinline__ uint32_t lbo() const { return mn ? (uint32_t)(rows * 128) : 16u; }
+};
+
+// D = A . B^T over nk16 K steps with the 3-pass split: main (tm) and
+// correction (tcor) accumulators (M = 128)
+__device__ __forceinline__ void mma3(uint32_t tm, uint32_t tcor, const Opnd& A, const Opnd& B,
+                                     int N, int nk16) {
+  const uint32_t id = idesc(N, A.mn, B.mn);
+  for (int k = 0; k < nk16; ++k) {
+    const uint32_t oa = A.at(k), ob = B.at(k);
+    const uint64_t dah = desc_sw128(A.hi + oa, A.lbo()), dal = desc_sw128(A.lo + oa, A.lbo());
+    const uint64_t dbh = desc_sw128(B.hi + ob, B.lbo()), dbl = desc_sw128(B.lo + ob, B.lbo());
+    const uint32_t acc = k > 0 ? 1u : 0u;
+    mma_f16<1>(tm, dah, dbh, id, acc);
+    mma_f16<1>(tcor, dal, dbh, id, acc);
+    mma_f16<1>(tcor, dah, dbl, id, 1u);
+  }
+}
+
+// byte offset of 16-byte chunk c (8 fp16 columns) of row r in a tile with R rows
+__device__ __forceinline__ uint32_t chunk_off(int R, int r, int c) {
+  return (uint32_t)((c >> 3) * R * 128 + r * 128 + (((c & 7) ^ (r & 7)) << 4));
+}
+
+// fp32 staging rows [0, nvalid) x ncols (pitch ncols) -> hi/lo tiles of R
+// rows (rows >= nvalid become 0). ncols multiple of 8.
+__device__ __forceinline__ void conv_rows(uint32_t stg, int nvalid, int R, int ncols, uint32_t thi,
+                                          uint32_t tlo, int tid, int nthr, float& amax) {
+  const int cpr = ncols >> 3;
+  for (int i = tid; i < R * cpr; i += nthr) {
+    const int r = i / cpr, c = i - r * cpr;
+    float x[8];
+    if (r < nvalid) {
+      const uint32_t s = stg + (uint32_t)((r * ncols + c * 8) * 4);
+      const float4 u = lds128(s), w = lds128(s + 16);
+      x[0] = u.x; x[1] = u.y; x[2] = u.z; x[3] = u.w;
+      x[4] = w.x; x[5] = w.y; x[6] = w.z; x[7] = w.w;
+    } else {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) x[e] = 0.f;
+    }
+    uint4 hi, lo;
+    split8(x, hi, lo, amax);
+    const uint32_t off = chunk_off(R, r, c);
+    sts128(thi + off, hi);
+    sts128(tlo + off, lo);
+  }
+}
+
+// 8 values of row r (chunk c) into a hi/lo tile pair
+__device__ __forceinline__ void put8(uint32_t thi, uint32_t tlo, int R, int r, int c,
+                                     const float* x, float& amax) {
+  uint4 hi, lo;
+  split8(x, hi, lo, amax);
+  const uint32_t off = chunk_off(R, r, c);
+  sts128(thi + off, hi);
+  sts128(tlo + off, lo);
+}
+
+__device__ __forceinline__ void fence_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void tc_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+
+// 16 columns of main + correction -> combined fp32 (one TMEM wait)
+__device__ __forceinline__ void tmem_pair16(uint32_t tmain, uint32_t tcor, float* out) {
+  uint32_t rm[16], rc[16];
+  tmem_ld16(tmain, rm);
+  tmem_ld16(tcor, rc);
+  tmem_wait();
+#pragma unroll
+  for (int e = 0; e < 16; ++e) out[e] = fmaf(__uint_as_float(rc[e]), kLoInv, __uint_as_float(rm[e]));
+}
+
+// this warp's TMEM lanes -> global rows (row < nvalid), columns [c0, c0 + nc)
+// (nc multiple of 16, <= 32), scaled by alpha
+__device__ __forceinline__ void rows_out(uint32_t tmain, uint32_t tcor, float* out, long long ld,
+                                         int row, int nvalid, int c0, int nc, float alpha) {
+#pragma unroll
+  for (int c = 0; c < 32; c += 16) {
+    if (c < nc) {
+      float v[16];
+      tmem_pair16(tmain + c0 + c, tcor + c0 + c, v);
+      if (row < nvalid) {
+        float* o = out + row * ld + c0 + c;
+#pragma unroll
+        for (int e = 0; e < 16; e += 4)
+          *reinterpret_cast<float4*>(o + e) =
+              make_float4(alpha * v[e], alpha * v[e + 1], alpha * v[e + 2], alpha * v[e + 3]);
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ void problem_of(const AttnArgs& a, int z, int& g, int& b, int& h) {
+  h = z % a.H;
+  b = (z / a.H) % a.Bb;
+  g = z / (a.H * a.Bb);
+}
+
+__device__ __forceinline__ void tmem_alloc(uint32_t* slot, uint32_t cols) {
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                   smem_u32(slot)),
+               "r"(cols));
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+}
+__device__ __forceinline__ void tmem_free(uint32_t base, uint32_t cols) {
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(base), "r"(cols));
+}
+
+// tensor maps of the operand families (one [rows][cols] box per problem)
+struct AttnTma {
+  CUtensorMap m[5];
+  TcOperand op[5];
+};
+enum { TQ = 0, TK = 1, TV = 2, TP = 3, TDO = 4 };
+
+__device__ __forceinline__ void tma_box(uint32_t dst, const AttnTma& t, int which, int g, int b,
+                                        int h, uint64_t* bar) {
+  int c[5];
+  tma_coords(t.op[which], 0, 0, g, b, h, c);
+  asm volatile(
+      "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(&t.m[which])), "r"(smem_u32(bar)), "r"(c[0]), "r"(c[1]),
+      "r"(c[2]), "r"(c[3]), "r"(c[4])
+      : "memory");
+}
+
+constexpr int TILE64 = 128 * 128;       // one hi (or lo) tile: 128 rows x 64 fp16
+constexpr int PAIR64 = 2 * TILE64;      // hi + lo
+constexpr int PAIR128 = 2 * PAIR64;     // hi + lo, two 64-column blocks
+
+// ---- forward -------------------------------------------------------------------
+// smem: staging fp32 [Q | K | V] (3 x 32 KB) | tiles: [Q | K] (-> P) | V | barriers
+__global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_constant__ AttnTma tm, const AttnArgs a, const int* active) {
+  extern __shared__ uint8_t smem_raw[];
+  if (active && *(volatile const int*)active == 0) return;
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int q4 = warp & 3, half = warp >> 2;
+  const int sq = a.sq, skv = a.skv, dh = a.dh;
+  const int skv16 = rup(skv, 16);
+  const uint32_t base = smem_u32(smem);
+  const uint32_t stQ = base, stK = base + 128 * 64 * 4, stV = base + 2 * 128 * 64 * 4;
+  const uint32_t tiles = base + 3 * 128 * 64 * 4;
+  const Opnd Qt{tiles, tiles + TILE64, 128, false};
+  const Opnd Kt{tiles + PAIR64, tiles + PAIR64 + TILE64, 128, false};
+  const Opnd Pt{tiles, tiles + 2 * TILE64, 128, false};  // over [Q | K]: hi blocks 0-1, lo blocks 0-1
+  const Opnd Vt{tiles + PAIR128, tiles + PAIR128 + TILE64, 128, true};
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 3 * 128 * 64 * 4 + PAIR128 + PAIR64);
+  uint64_t* st_full = &bars[0];
+  uint64_t* s_bar = &bars[1];
+  uint64_t* o_bar = &bars[2];
+  float* xch = reinterpret_cast<float*>(bars + 4);  // [2][128] row max / sum exchange
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(xch + 256);
+  const int nprob = a.G * a.Bb * a.H;
+
+  auto issue_loads = [&](int z) {
+    int g, b, h;
+    problem_of(a, z, g, b, h);
+    if (lane == 0) {
+      mbar_expect_tx(st_full, (uint32_t)((sq + 2 * skv) * dh * 4));
+      tma_box(stQ, tm, TQ, g, b, h, st_full);
+      tma_box(stK, tm, TK, g, b, h, st_full);
+      tma_box(stV, tm, TV, g, b, h, st_full);
+    }
+    __syncwarp();
+  };
+
+  if (tid == 0) {
+    mbar_init(st_full, 1);
+    mbar_init(s_bar, 1);
+    mbar_init(o_bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) tmem_alloc(tslot, 256);
+  tc_before();
+  __syncthreads();
+  tc_after();
+  const uint32_t tmem = *tslot;
+  const uint32_t trow = tmem + ((uint32_t)(q4 * 32) << 16);
+  const int i = q4 * 32 + lane;  // query row = TMEM lane
+  float amax = 0.f;
+  if (warp == 0 && (int)blockIdx.x < nprob) issue_loads(blockIdx.x);
+
+  int it = 0;
+  for (int z = blockIdx.x; z < nprob; z += gridDim.x, ++it) {
+    int g, b, h;
+    problem_of(a, z, g, b, h);
+    const uint32_t ph = it & 1;
+    mbar_wait(st_full, ph);
+    conv_rows(stQ, sq, 128, dh, Qt.hi, Qt.lo, tid, kThreads, amax);
+    conv_rows(stK, skv, skv16, dh, Kt.hi, Kt.lo, tid, kThreads, amax);
+    conv_rows(stV, skv, skv16, dh, Vt.hi, Vt.lo, tid, kThreads, amax);
+    fence_async_smem();
+    tc_before();
+    __syncthreads();
+    tc_after();
+    if (warp == 0 && z + (int)gridDim.x < nprob) issue_loads(z + gridDim.x);  // staging is free
+    if (tid == 0) {
+      mma3(tmem, tmem + 128, Qt, Kt, skv16, dh >> 4);  // S
+      mma_commit<1>(s_bar);
+    }
+    // ---- softmax_rows(S * scale) with the causal mask (tensor.cpp:310-326,
+    // blocks.cpp:160-166): row i, keys [64 half, 64 half + 64) ----
+    mbar_wait(s_bar, ph);
+    tc_after();
+    const int c0 = half * 64;
+    const bool any = c0 < skv16;  // warp-uniform
+    float v[64];
+    float m = -INFINITY;
+    if (any) {
+#pragma unroll
+      for (int c = 0; c < 64; c += 16) {
+        if (c0 + c < skv16) {
+          tmem_pair16(trow + c0 + c, trow + 128 + c0 + c, v + c);
+        } else {
+#pragma unroll
+          for (int e = 0; e < 16; ++e) v[c + e] = 0.f;
+        }
+      }
+#pragma unroll
+      for (int e = 0; e < 64; ++e) {
+        const int j = c0 + e;
+        const bool ok = j < skv && !(a.causal && j > i);
+        v[e] = ok ? v[e] * a.scale : -INFINITY;
+        m = fmaxf(m, v[e]);
+      }
+    }
+    xch[half * 128 + i] = m;
+    tc_before();
+    __syncthreads();
+    m = fmaxf(xch[i], xch[128 + i]);
+    float sum = 0.f;
+    if (any) {
+#pragma unroll
+      for (int e = 0; e < 64; ++e) {
+        v[e] = v[e] == -INFINITY ? 0.f : expf(v[e] - m);
+        sum += v[e];
+      }
+    }
+    __syncthreads();  // every max read before the sums overwrite xch
+    xch[half * 128 + i] = sum;
+    __syncthreads();
+    const float inv = 1.f / (xch[i] + xch[128 + i]);
+    if (any) {
+#pragma unroll
+      for (int e = 0; e < 64; ++e) v[e] *= inv;
+      if (a.P.ok() && i < sq) {
+        float* prow = a.P.at(g, b, h) + i * (long long)a.P.ld + c0;
+#pragma unroll
+        for (int e = 0; e < 64; e += 4)
+          if (c0 + e < skv) *reinterpret_cast<float4*>(prow + e) = make_float4(v[e], v[e + 1], v[e + 2], v[e + 3]);
+      }
+      // P (row i, K = keys) as the A operand of O = P V; zero beyond skv
+#pragma unroll
+      for (int c = 0; c < 8; ++c)
+        if (c0 + c * 8 < skv16) put8(Pt.hi, Pt.lo, 128, i, half * 8 + c, v + c * 8, amax);
+    }
+    fence_async_smem();
+    tc_before();
+    __syncthreads();
+    if (tid == 0) {
+      tc_after();
+      mma3(tmem, tmem + 128, Pt, Vt, dh, skv16 >> 4);  // O
+      mma_commit<1>(o_bar);
+    }
+    mbar_wait(o_bar, ph);
+    tc_after();
+    rows_out(trow, trow + 128, a.O.at(g, b, h), a.O.ld, i, sq, half * (dh >> 1), dh >> 1, 1.f);
+    tc_before();
+    __syncthreads();  // TMEM and tiles free for the next problem
+  }
+  if (amax >= 65520.f && amax <= FLT_MAX && a.range_flag) atomicOr(a.range_flag, 1);
+  tc_before();
+  __syncthreads();
+  if (warp == 0) tmem_free(tmem, 256);
+}
+
+// ---- backward ------------------------------------------------------------------
+// smem: staging fp32 64 KB ([dO | V], then P, then [Q | K]) | tiles:
+//   T0 = [dO | V] (-> dS), T1 = P (-> [Q | K]) | barriers
+// TMEM: dP main [0,128) corr [128,256); dV main [256,..) corr [384,..);
+//       dQ main [0,..) corr [64,..); dK main [128,..) corr [192,..)
+__global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_constant__ AttnTma tm, const AttnArgs a, const int* active) {
+  extern __shared__ uint8_t smem_raw[];
+  if (active && *(volatile const int*)active == 0) return;
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int q4 = warp & 3, half = warp >> 2;
+  const int sq = a.sq, skv = a.skv, dh = a.dh;
+  const int skv16 = rup(skv, 16), sq16 = rup(sq, 16);
+  const uint32_t base = smem_u32(smem);
+  const uint32_t stg = base;                    // 64 KB
+  const uint32_t st2 = base + 128 * 64 * 4;     // second half of the staging
+  const uint32_t T0 = base + 2 * 128 * 64 * 4;  // 64 KB
+  const uint32_t T1 = T0 + PAIR128;             // 64 KB
+  const Opnd dOk{T0, T0 + TILE64, 128, false};            // dP: A
+  const Opnd dOm{T0, T0 + TILE64, 128, true};             // dV: B
+  const Opnd Vk{T0 + PAIR64, T0 + PAIR64 + TILE64, 128, false};  // dP: B
+  const Opnd dSk{T0, T0 + 2 * TILE64, 128, false};        // dQ: A
+  const Opnd dSm{T0, T0 + 2 * TILE64, 128, true};         // dK: A
+  const Opnd Pm{T1, T1 + 2 * TILE64, 128, true};          // dV: A
+  const Opnd Qm{T1, T1 + TILE64, 128, true};              // dK: B
+  const Opnd Km{T1 + PAIR64, T1 + PAIR64 + TILE64, 128, true};  // dQ: B
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 2 * 128 * 64 * 4 + 2 * PAIR128);
+  uint64_t* st_full = &bars[0];
+  uint64_t* m_bar = &bars[1];
+  float* xch = reinterpret_cast<float*>(bars + 4);  // [2][128] row-sum exchange
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(xch + 256);
+  const int nprob = a.G * a.Bb * a.H;
+
+  auto load_dov = [&](int z) {
+    int g, b, h;
+    problem_of(a, z, g, b, h);
+    if (lane == 0) {
+      mbar_expect_tx(st_full, (uint32_t)((sq + skv) * dh * 4));
+      tma_box(stg, tm, TDO, g, b, h, st_full);
+      tma_box(st2, tm, TV, g, b, h, st_full);
+    }
+    __syncwarp();
+  };
+
+  if (tid == 0) {
+    mbar_init(st_full, 1);
+    mbar_init(m_bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) tmem_alloc(tslot, 512);
+  tc_before();
+  __syncthreads();
+  tc_after();
+  const uint32_t tmem = *tslot;
+  const uint32_t trow = tmem + ((uint32_t)(q4 * 32) << 16);
+  const int r = q4 * 32 + lane;  // TMEM lane: query row (dP, dQ) or key row (dV, dK)
+  float amax = 0.f;
+  if (warp == 0 && (int)blockIdx.x < nprob) load_dov(blockIdx.x);
+
+  uint32_t stp = 0, mp = 0;  // barrier phases
+  for (int z = blockIdx.x; z < nprob; z += gridDim.x) {
+    int g, b, h;
+    problem_of(a, z, g, b, h);
+    const float* P = a.P.at(g, b, h);
+    // (1) dO, V -> T0
+    mbar_wait(st_full, stp);
+    stp ^= 1;
+    conv_rows(stg, sq, 128, dh, dOk.hi, dOk.lo, tid, kThreads, amax);
+    conv_rows(st2, skv, skv16, dh, Vk.hi, Vk.lo, tid, kThreads, amax);
+    fence_async_smem();  // staging reads ordered before the bulk copies that reuse it
+    __syncthreads();
+    if (warp == 0) {
+      if (lane == 0) {
+        mbar_expect_tx(st_full, (uint32_t)(sq * skv * 4));
+        tma_box(stg, tm, TP, g, b, h, st_full);
+      }
+      __syncwarp();
+    }
+    // (2) P -> T1 (rows >= sq zero: K padding of dV)
+    mbar_wait(st_full, stp);
+    stp ^= 1;
+    conv_rows(stg, sq, 128, skv, Pm.hi, Pm.lo, tid, kThreads, amax);
+    fence_async_smem();
+    tc_before();
+    __syncthreads();
+    tc_after();
+    if (warp == 0) {
+      if (lane == 0) {
+        mbar_expect_tx(st_full, (uint32_t)((sq + skv) * dh * 4));
+        tma_box(stg, tm, TQ, g, b, h, st_full);
+        tma_box(st2, tm, TK, g, b, h, st_full);
+      }
+      __syncwarp();
+    }
+    if (tid == 0) {
+      mma3(tmem, tmem + 128, dOk, Vk, skv16, dh >> 4);        // dP = dO V^T
+      mma3(tmem + 256, tmem + 384, Pm, dOm, dh, sq16 >> 4);  // dV = P^T dO
+      mma_commit<1>(m_bar);
+    }
+    mbar_wait(m_bar, mp);
+    mp ^= 1;
+    tc_after();
+    // (3) vjp_softmax_rows (tensor.cpp:328-342): dS = P (dP - sum_j dP_j P_j),
+    // row r = query, keys [64 half, +64)
+    {
+      const int c0 = half * 64;
+      const bool any = c0 < skv16;
+      const bool live = r < sq;
+      const float* prow = P + (long long)r * a.P.ld + c0;
+      float dp[64];
+      float t = 0.f;
+      if (any) {
+#pragma unroll
+        for (int c = 0; c < 64; c += 16) {
+          if (c0 + c < skv16) {
+            tmem_pair16(trow + c0 + c, trow + 128 + c0 + c, dp + c);
+          } else {
+#pragma unroll
+            for (int e = 0; e < 16; ++e) dp[c + e] = 0.f;
+          }
+        }
+#pragma unroll
+        for (int e = 0; e < 64; e += 4) {
+          if (live && c0 + e < skv) {
+            const float4 p4 = *reinterpret_cast<const float4*>(prow + e);
+            t += dp[e] * p4.x;
+            t += dp[e + 1] * p4.y;
+            t += dp[e + 2] * p4.z;
+            t += dp[e + 3] * p4.w;
+          }
+        }
+      }
+      xch[half * 128 + r] = t;
+      tc_before();
+      __syncthreads();  // also: dP / dV MMAs done -> T0 may take dS
+      t = xch[r] + xch[128 + r];
+      if (any) {
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          if (c0 + c * 8 < skv16) {
+            float ds[8];
+#pragma unroll
+            for (int e = 0; e < 8; e += 4) {
+              const int j = c * 8 + e;
+              float4 p4 = make_float4(0.f, 0.f, 0.f, 0.f);
+              if (live && c0 + j < skv) p4 = *reinterpret_cast<const float4*>(prow + j);
+              ds[e] = p4.x * (dp[j] - t);
+              ds[e + 1] = p4.y * (dp[j + 1] - t);
+              ds[e + 2] = p4.z * (dp[j + 2] - t);
+              ds[e + 3] = p4.w * (dp[j + 3] - t);
+            }
+            put8(dSk.hi, dSk.lo, 128, r, half * 8 + c, ds, amax);
+          }
+        }
+      }
+    }
+    // dV rows (keys) while the staging of Q, K lands
+    rows_out(trow + 256, trow + 384, a.dV.at(g, b, h), a.dV.ld, r, skv, half * (dh >> 1), dh >> 1, 1.f);
+    // (4) Q, K -> T1 (the dV MMA is done)
+    mbar_wait(st_full, stp);
+    stp ^= 1;
+    conv_rows(stg, sq, sq16, dh, Qm.hi, Qm.lo, tid, kThreads, amax);
+    conv_rows(st2, skv, skv16, dh, Km.hi, Km.lo, tid, kThreads, amax);
+    fence_async_smem();
+    tc_before();
+    __syncthreads();
+    tc_after();
+    if (warp == 0 && z + (int)gridDim.x < nprob) load_dov(z + gridDim.x);
+    if (tid == 0) {
+      mma3(tmem, tmem + 64, dSk, Km, dh, skv16 >> 4);         // dQ = dS K
+      mma3(tmem + 128, tmem + 192, dSm, Qm, dh, sq16 >> 4);   // dK = dS^T Q
+      mma_commit<1>(m_bar);
+    }
+    mbar_wait(m_bar, mp);
+    mp ^= 1;
+    tc_after();
+    rows_out(trow, trow + 64, a.dQ.at(g, b, h), a.dQ.ld, r, sq, half * (dh >> 1), dh >> 1, a.scale);
+    rows_out(trow + 128, trow + 192, a.dK.at(g, b, h), a.dK.ld, r, skv, half * (dh >> 1), dh >> 1,
+             a.scale);
+    tc_before();
+    __syncthreads();
+  }
+  if (amax >= 65520.f && amax <= FLT_MAX && a.range_flag) atomicOr(a.range_flag, 1);
+  tc_before();
+  __syncthreads();
+  if (warp == 0) tmem_free(tmem, 512);
+}
+
+constexpr int kFwdSmem = 1024 + 3 * 128 * 64 * 4 + PAIR128 + PAIR64 + 64 + 256 * 4 + 16;
+constexpr int kBwdSmem = 1024 + 2 * 128 * 64 * 4 + 2 * PAIR128 + 64 + 256 * 4 + 16;
+
+bool aligned(const Mat& m) {
+  return !m.ok() || ((reinterpret_cast<uintptr_t>(m.ptr) & 15) == 0 && m.ld % 4 == 0 &&
+                     m.slot_stride % 4 == 0 && m.bstride % 4 == 0 && m.hstride % 4 == 0);
+}
+
+int num_sms() {
+  static int sms = 0;
+  if (!sms) MGLP_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
+  return sms;
+}
+
+AttnTma maps(const AttnArgs& a, bool backward) {
+  AttnTma t{};
+  auto mk = [&](int which, const Mat& m, int rows, int cols) {
+    t.m[which] = tc_make_map(m, a.G, a.Bb, a.H, rows, cols, rows, cols, false, &t.op[which]);
+  };
+  mk(TQ, a.Q, a.sq, a.dh);
+  mk(TK, a.K, a.skv, a.dh);
+  mk(TV, a.V, a.skv, a.dh);
+  if (backward) {
+    mk(TP, a.P, a.sq, a.skv);
+    mk(TDO, a.dO, a.sq, a.dh);
+  }
+  return t;
+}
+
+}  // namespace
+
+bool attn_tc_supported(const AttnArgs& a, bool backward) {
+  if (a.sq < 1 || a.skv < 1 || a.sq > 128 || a.skv > 128) return false;
+  if (a.sq % 8 || a.skv % 8) return false;
+  if (a.dh != 32 && a.dh != 64) return false;
+  if (!aligned(a.Q) || !aligned(a.K) || !aligned(a.V) || !aligned(a.O) || !aligned(a.P))
+    return false;
+  if (backward && (!aligned(a.dO) || !aligned(a.dQ) || !aligned(a.dK) || !aligned(a.dV) || !a.P.ok()))
+    return false;
+  return true;
+}
+
+void launch_attn_fwd(const AttnArgs& a, const int* active, cudaStream_t s) {
+  if (!attn_tc_supported(a, false)) throw ContractViolation("attn_fwd: unsupported shape");
+  static bool attr = [] {
+    MGLP_CUDA(cudaFuncSetAttribute(attn_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   kFwdSmem));
+    return true;
+  }();
+  (void)attr;
+  const long long n = (long long)a.G * a.Bb * a.H;
+  if (n == 0) return;
+  const int grid = (int)std::min<long long>(n, num_sms());
+  AttnTma t = maps(a, false);
+  attn_fwd_kernel<<<grid, kThreads, kFwdSmem, s>>>(t, a, active);
+  MGLP_CUDA(cudaGetLastError());
+}
+
+void launch_attn_bwd(const AttnArgs& a, const int* active, cudaStream_t s) {
+  if (!attn_tc_supported(a, true)) throw ContractViolation("attn_bwd: unsupported shape");
+  static bool attr = [] {
+    MGLP_CUDA(cudaFuncSetAttribute(attn_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   kBwdSmem));
+    return true;
+  }();
+  (void)attr;
+  const long long n = (long long)a.G * a.Bb * a.H;
+  if (n == 0) return;
+  const int grid = (int)std::min<long long>(n, num_sms());
+  AttnTma t = maps(a, true);
+  attn_bwd_kernel<<<grid, kThreads, kBwdSmem, s>>>(t, a, active);
+  MGLP_CUDA(cudaGetLastError());
+}
+
+}  // namespace mglp

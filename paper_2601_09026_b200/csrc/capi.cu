@@ -725,6 +725,124 @@ mglp_status mglp_test_gemm(int G, int M, int N, int K, const float* A, long long
   });
 }
 
+// ---- test / bench hook: the fused tcgen05 attention (attn_tc.cu) ----
+namespace {
+AttnArgs attn_args(int B, int H, int sq, int skv, int dh, int causal, const float* Q, const float* K,
+                   const float* V, int ld, float* O, float* P, const float* dO, float* dQ, float* dK,
+                   float* dV) {
+  auto heads = [&](const float* p, int s, int ldm) {
+    Mat m;
+    m.ptr = const_cast<float*>(p);
+    m.ld = ldm;
+    m.bstride = (long long)s * ldm;
+    m.hstride = dh;
+    return m;
+  };
+  AttnArgs a;
+  a.G = 1;
+  a.Bb = B;
+  a.H = H;
+  a.sq = sq;
+  a.skv = skv;
+  a.dh = dh;
+  a.causal = causal;
+  a.scale = (float)(1.0 / std::sqrt((double)dh));
+  a.Q = heads(Q, sq, ld);
+  a.K = heads(K, skv, ld);
+  a.V = heads(V, skv, ld);
+  a.O = heads(O, sq, ld);
+  const int ldp = (skv + 3) & ~3;
+  a.P.ptr = P;
+  a.P.ld = ldp;
+  a.P.hstride = (long long)sq * ldp;
+  a.P.bstride = (long long)H * sq * ldp;
+  if (dO) {
+    a.dO = heads(dO, sq, ld);
+    a.dQ = heads(dQ, sq, ld);
+    a.dK = heads(dK, skv, ld);
+    a.dV = heads(dV, skv, ld);
+  }
+  return a;
+}
+}  // namespace
+
+mglp_status mglp_test_attention(int B, int H, int sq, int skv, int dh, int causal, const float* Q,
+                                const float* K, const float* V, int ld, float* O, float* P,
+                                const float* dO, float* dQ, float* dK, float* dV,
+                                int* range_flag) {
+  return guard([&] {
+    need(Q, "Q");
+    need(K, "K");
+    need(V, "V");
+    need(O, "O");
+    need(P, "P");
+    AttnArgs a = attn_args(B, H, sq, skv, dh, causal, Q, K, V, ld, O, P, dO, dQ, dK, dV);
+    if (!attn_tc_supported(a, dO != nullptr))
+      throw ValidationError("fused attention: unsupported shape (sq, skv <= 128, multiples of 8; dh 32 or 64)");
+    int* dflag = nullptr;
+    MGLP_CUDA(cudaMalloc(&dflag, sizeof(int)));
+    MGLP_CUDA(cudaMemset(dflag, 0, sizeof(int)));
+    a.range_flag = dflag;
+    launch_attn_fwd(a, nullptr, 0);
+    if (dO) launch_attn_bwd(a, nullptr, 0);
+    MGLP_CUDA(cudaDeviceSynchronize());
+    int flag = 0;
+    MGLP_CUDA(cudaMemcpy(&flag, dflag, sizeof(int), cudaMemcpyDeviceToHost));
+    cudaFree(dflag);
+    if (range_flag) *range_flag = flag;
+  });
+}
+
+mglp_status mglp_bench_attention(int G, int B, int H, int s, int dh, int causal, int backward,
+                                 int reps, float* ms_per_launch) {
+  return guard([&] {
+    const int d = H * dh, ld = 3 * d;
+    const long long ntok = (long long)G * B * s;
+    float *qkv = nullptr, *O = nullptr, *P = nullptr, *dO = nullptr, *dqkv = nullptr;
+    const int ldp = (s + 3) & ~3;
+    const long long np = (long long)G * B * H * s * ldp;
+    MGLP_CUDA(cudaMalloc(&qkv, ntok * ld * sizeof(float)));
+    MGLP_CUDA(cudaMalloc(&dqkv, ntok * ld * sizeof(float)));
+    MGLP_CUDA(cudaMalloc(&O, ntok * d * sizeof(float)));
+    MGLP_CUDA(cudaMalloc(&dO, ntok * d * sizeof(float)));
+    MGLP_CUDA(cudaMalloc(&P, np * sizeof(float)));
+    MGLP_CUDA(cudaMemset(qkv, 0x3c, ntok * ld * sizeof(float)));
+    MGLP_CUDA(cudaMemset(dO, 0x3c, ntok * d * sizeof(float)));
+    AttnArgs a = attn_args(B, H, s, s, dh, causal, qkv, qkv + d, qkv + 2 * d, ld, O, P,
+                           backward ? dO : nullptr, dqkv, dqkv + d, dqkv + 2 * d);
+    a.G = G;
+    a.O.ld = d;
+    a.O.bstride = (long long)s * d;
+    a.dO.ld = d;
+    a.dO.bstride = (long long)s * d;
+    for (Mat* m : {&a.Q, &a.K, &a.V, &a.dQ, &a.dK, &a.dV}) m->slot_stride = (long long)B * s * ld;
+    for (Mat* m : {&a.O, &a.dO}) m->slot_stride = (long long)B * s * d;
+    a.P.slot_stride = (long long)B * H * s * ldp;
+    if (!attn_tc_supported(a, backward != 0)) throw ValidationError("bench_attention: unsupported shape");
+    cudaEvent_t e0, e1;
+    MGLP_CUDA(cudaEventCreate(&e0));
+    MGLP_CUDA(cudaEventCreate(&e1));
+    auto run = [&] {
+      if (backward)
+        launch_attn_bwd(a, nullptr, 0);
+      else
+        launch_attn_fwd(a, nullptr, 0);
+    };
+    run();
+    run();
+    MGLP_CUDA(cudaEventRecord(e0, 0));
+    for (int i = 0; i < reps; ++i) run();
+    MGLP_CUDA(cudaEventRecord(e1, 0));
+    MGLP_CUDA(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    MGLP_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    *ms_per_launch = ms / reps;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    for (float* p : {qkv, O, P, dO, dqkv}) cudaFree(p);
+  });
+}
+
 // ---- GEMM micro-benchmark (tools/gemm_bench.py) ----
 mglp_status mglp_bench_gemm(int G, int M, int N, int K, int a_mn, int b_mn, int b_presplit,
                             int epi, int reps, float* ms_per_launch) {

@@ -639,6 +639,22 @@ void Engine::gemm(GemmArgs g) {
   });
 }
 
+// The fused tcgen05 attention (attn_tc.cu) covers sq, skv <= 128; longer
+// sequences run as tensor-core GEMMs + softmax row kernels. The choice depends
+// only on the shape, so a given layer always takes the same path (Phi stays
+// deterministic across families). MGLP_NO_FUSED_ATTN=1 forces the unfused path.
+static bool use_fused_attn() {
+#ifdef MGLP_GEMM_SIMT
+  return false;
+#else
+  static const bool on = [] {
+    const char* e = getenv("MGLP_NO_FUSED_ATTN");
+    return !(e && atoi(e) != 0);
+  }();
+  return on;
+#endif
+}
+
 void Engine::attention_fwd(int G, Mat Q, Mat K, Mat V, Mat O, Mat P, int sq, int skv,
                            bool causal) {
   const int H = sd_.heads, dh = sd_.d / H;
@@ -655,6 +671,30 @@ void Engine::attention_fwd(int G, Mat Q, Mat K, Mat V, Mat O, Mat P, int sq, int
   P.ld = ldp;
   P.hstride = (long long)sq * ldp;
   P.bstride = (long long)H * sq * ldp;
+  if (use_fused_attn()) {
+    AttnArgs at;
+    at.G = G;
+    at.Bb = B_;
+    at.H = H;
+    at.sq = sq;
+    at.skv = skv;
+    at.dh = dh;
+    at.causal = causal ? 1 : 0;
+    at.scale = (float)(1.0 / std::sqrt((double)dh));
+    at.Q = Q;
+    at.K = K;
+    at.V = V;
+    at.O = O;
+    at.P = P;
+    at.range_flag = range_flag_;
+    if (attn_tc_supported(at, false)) {
+      ++launches_;
+      prof_shape_ = {sq, skv, dh, G * B_ * H};
+      timed(PROF_ATTN, 4.0 * G * B_ * H * (double)sq * skv * dh, 0.0,
+            [&] { launch_attn_fwd(at, active_, stream_); });
+      return;
+    }
+  }
   GemmArgs g;
   g.G = G;
   g.Bb = B_;
@@ -714,6 +754,32 @@ void Engine::attention_bwd(int G, Mat Q, Mat K, Mat V, Mat P, Mat dO, Mat dP, Ma
     m->ld = ldp;
     m->hstride = (long long)sq * ldp;
     m->bstride = (long long)H * sq * ldp;
+  }
+  if (use_fused_attn()) {
+    AttnArgs at;
+    at.G = G;
+    at.Bb = B_;
+    at.H = H;
+    at.sq = sq;
+    at.skv = skv;
+    at.dh = dh;
+    at.scale = scale;
+    at.Q = Q;
+    at.K = K;
+    at.V = V;
+    at.P = P;
+    at.dO = dO;
+    at.dQ = dQ;
+    at.dK = dK;
+    at.dV = dV;
+    at.range_flag = range_flag_;
+    if (attn_tc_supported(at, true)) {
+      ++launches_;
+      prof_shape_ = {-sq, skv, dh, G * B_ * H};
+      timed(PROF_ATTN, 8.0 * G * B_ * H * (double)sq * skv * dh, 0.0,
+            [&] { launch_attn_bwd(at, active_, stream_); });
+      return;
+    }
   }
   auto mk = [&](int M, int N, int K_, Mat A, bool amn, Mat B, bool bmn, Mat out, float alpha) {
     GemmArgs g;

@@ -104,4 +104,20 @@ void launch_pack_hl(const float* src, long long src_slot, int src_ld, float* dst
                     long long dst_slot, int dst_ld, int G, int rows, int K, bool transpose,
                     cudaStream_t s);
 
+// ---- fused attention (attn_tc.cu), sq, skv <= 128, dh in {32, 64} -------------
+// One CTA per (member g, batch b, head h); operands address (g, b, h) through
+// Mat::at(g, b, h). Forward: O = softmax(Q K^T * scale [causal]) V, P stored
+// when P is set. Backward (P required): dQ = scale dS K, dK = scale dS^T Q,
+// dV = P^T dO with dS = P (dO V^T - rowsum(...)).
+struct AttnArgs {
+  int G = 1, Bb = 1, H = 1, sq = 0, skv = 0, dh = 0, causal = 0;
+  float scale = 1.f;
+  Mat Q, K, V, O, P;
+  Mat dO, dQ, dK, dV;
+  int* range_flag = nullptr;
+};
+bool attn_tc_supported(const AttnArgs& a, bool backward);
+void launch_attn_fwd(const AttnArgs& a, const int* active, cudaStream_t s);
+void launch_attn_bwd(const AttnArgs& a, const int* active, cudaStream_t s);
+
 }  // namespace mglp

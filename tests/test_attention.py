@@ -1,0 +1,122 @@
+"""Fused tcgen05 attention (attn_tc.cu) against an fp64 torch restatement of
+the reference's attention / vjp_attention (blocks.cpp:142-236: per-head
+scores * 1/sqrt(dh), -1e30 causal mask, stable softmax_rows, P.V, and the VJP
+dS = P (dP - rowsum(dP P))), through the C-ABI test hook."""
+import math
+
+import pytest
+
+torch = pytest.importorskip("torch")
+from paper_2601_09026_b200 import _native as N  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+
+def reference(Q, K, V, dO, B, H, sq, skv, dh, causal):
+    Qd, Kd, Vd, dOd = (t.double() for t in (Q, K, V, dO))
+    O = torch.zeros(B, sq, H * dh, dtype=torch.float64)
+    P = torch.zeros(B, H, sq, skv, dtype=torch.float64)
+    dQ = torch.zeros_like(Qd[..., :H * dh])
+    dK = torch.zeros(B, skv, H * dh, dtype=torch.float64)
+    dV = torch.zeros(B, skv, H * dh, dtype=torch.float64)
+    sc = 1.0 / math.sqrt(dh)
+    for b in range(B):
+        for h in range(H):
+            sl = slice(h * dh, (h + 1) * dh)
+            q, k, v, do = Qd[b, :, sl], Kd[b, :, sl], Vd[b, :, sl], dOd[b, :, sl]
+            s = q @ k.T * sc
+            if causal:
+                s = s.masked_fill(torch.ones(sq, skv).triu(1).bool(), -1e30)
+            p = torch.softmax(s, dim=-1)
+            P[b, h] = p
+            O[b, :, sl] = p @ v
+            dp = do @ v.T
+            ds = p * (dp - (dp * p).sum(-1, keepdim=True))
+            dQ[b, :, sl] = ds @ k * sc
+            dK[b, :, sl] = ds.T @ q * sc
+            dV[b, :, sl] = p.T @ do
+    return O, P, dQ, dK, dV
+
+
+def run(B, H, sq, skv, dh, causal, seed=0, scale=1.0):
+    g = torch.Generator().manual_seed(seed)
+    d = H * dh
+    ld = 3 * d  # the qkv row layout of a layer
+    qkv_q = torch.randn(B, sq, ld, generator=g) * scale
+    qkv_kv = torch.randn(B, skv, ld, generator=g) * scale
+    Q = qkv_q[..., :d].contiguous()
+    K = qkv_kv[..., d:2 * d].contiguous()
+    V = qkv_kv[..., 2 * d:].contiguous()
+    dO = torch.randn(B, sq, d, generator=g)
+    # device buffers with row stride ld (heads interleaved in a token row)
+    dq = qkv_q.clone().cuda()
+    dkv = qkv_kv.clone().cuda()
+    ddo = torch.zeros(B, sq, ld, device="cuda")
+    ddo[..., :d] = dO.cuda()
+    O = torch.full((B, sq, ld), float("nan"), device="cuda")
+    ldp = (skv + 3) & ~3
+    P = torch.full((B, H, sq, ldp), float("nan"), device="cuda")
+    dQ = torch.full((B, sq, ld), float("nan"), device="cuda")
+    dKV = torch.full((B, skv, ld), float("nan"), device="cuda")
+    N.call("mglp_test_attention", B, H, sq, skv, dh, int(causal), dq.data_ptr(),
+           dkv[..., d:].data_ptr(), dkv[..., 2 * d:].data_ptr(), ld, O.data_ptr(), P.data_ptr(),
+           ddo.data_ptr(), dQ.data_ptr(), dKV[..., d:].data_ptr(), dKV[..., 2 * d:].data_ptr(), None)
+    ref = reference(Q, K, V, dO, B, H, sq, skv, dh, causal)
+    got = (O[..., :d].cpu(), P[..., :skv].cpu(), dQ[..., :d].cpu(), dKV[..., d:2 * d].cpu(),
+           dKV[..., 2 * d:].cpu())
+    return got, ref
+
+
+def relerr(a, b):
+    return float((a.double() - b).abs().max() / b.abs().max())
+
+
+SHAPES = [  # B, H, sq, skv, dh, causal
+    (2, 2, 32, 32, 32, False),     # BASELINE configs[0] head shape
+    (2, 3, 128, 128, 64, False),   # BERT / MT head shape
+    (2, 2, 128, 128, 64, True),    # causal self-attention
+    (1, 2, 64, 128, 64, False),    # cross-attention, sq != skv
+    (2, 1, 128, 40, 32, False),    # skv not a multiple of 16 / 32
+    (1, 2, 8, 8, 64, True),        # minimal sequence
+    (1, 1, 96, 24, 64, False),
+]
+
+
+@pytest.mark.parametrize("shape", SHAPES)
+def test_fused_attention_matches_fp64(shape):
+    B, H, sq, skv, dh, causal = shape
+    got, ref = run(B, H, sq, skv, dh, causal)
+    names = ["O", "P", "dQ", "dK", "dV"]
+    for n, a, b in zip(names, got, ref):
+        assert not torch.isnan(a).any(), n
+        e = relerr(a, b)
+        assert e < 2e-5, (n, e)
+
+
+def test_causal_probabilities_are_exactly_zero_above_diagonal():
+    got, _ = run(1, 2, 64, 64, 64, True, seed=4)
+    P = got[1]
+    mask = torch.ones(64, 64).triu(1).bool()
+    assert (P[..., mask] == 0).all()
+
+
+def test_range_flag_on_fp16_overflow():
+    B, H, s, dh = 1, 1, 32, 32
+    d = H * dh
+    x = torch.randn(B, s, 3 * d, device="cuda")
+    x[0, 3, 5] = 1e5  # a query value beyond the fp16 split range
+    O = torch.zeros(B, s, 3 * d, device="cuda")
+    P = torch.zeros(B, H, s, s, device="cuda")
+    import ctypes as C
+    flag = C.c_int(0)
+    N.call("mglp_test_attention", B, H, s, s, dh, 0, x.data_ptr(), x[..., d:].data_ptr(),
+           x[..., 2 * d:].data_ptr(), 3 * d, O.data_ptr(), P.data_ptr(), None, None, None, None,
+           C.byref(flag))
+    assert flag.value == 1
+
+
+def test_unsupported_shape_is_a_validation_error():
+    x = torch.zeros(1, 200, 192, device="cuda")
+    with pytest.raises(N.ValidationError):
+        N.call("mglp_test_attention", 1, 1, 200, 200, 64, 0, x.data_ptr(), x.data_ptr(),
+               x.data_ptr(), 192, x.data_ptr(), x.data_ptr(), None, None, None, None, None)

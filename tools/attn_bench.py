@@ -1,0 +1,28 @@
+"""Device-timed fused attention (attn_tc.cu) on the hot-path head shapes
+(C-ABI mglp_bench_attention). Usage: python tools/attn_bench.py [reps]"""
+import ctypes as C
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2601_09026_b200 import _native as N  # noqa: E402
+
+SHAPES = [  # name, G, B, H, s, dh, causal
+    ("bert x16", 16, 32, 12, 128, 64, 0),
+    ("bert x1", 1, 32, 12, 128, 64, 0),
+    ("mt dec causal x16", 16, 32, 8, 128, 64, 1),
+    ("tiny x4", 4, 8, 2, 32, 32, 0),
+]
+reps = int(sys.argv[1]) if len(sys.argv) > 1 else 10
+out = {}
+for name, G, B, H, s, dh, causal in SHAPES:
+    for bwd in (0, 1):
+        ms = C.c_float()
+        N.call("mglp_bench_attention", G, B, H, s, dh, causal, bwd, reps, C.byref(ms))
+        fl = (8.0 if bwd else 4.0) * G * B * H * s * s * dh
+        key = f"{name} {'bwd' if bwd else 'fwd'}"
+        print(f"{key:24s} {ms.value:8.3f} ms  {fl / (ms.value * 1e-3) / 1e12:7.1f} TF/s", flush=True)
+        out[key] = {"ms": ms.value, "tflops": fl / (ms.value * 1e-3) / 1e12}
+os.makedirs("gpurun_out", exist_ok=True)
+json.dump(out, open(f"gpurun_out/attn_bench{os.environ.get('TAG', '')}.json", "w"), indent=1)
