@@ -112,6 +112,50 @@ __device__ __forceinline__ float combine_apply(const Combine& c, int g, long lon
   return p;
 }
 
+// combine_apply over 4 consecutive elements (16-byte aligned rows): same
+// per-element arithmetic, r^2 accumulated in element order
+__device__ __forceinline__ float4 combine_apply4(const Combine& c, int g, long long off_out,
+                                                 long long off_z, float4 F, double& r2) {
+  const float4 z = *reinterpret_cast<const float4*>(c.z.at(g) + off_z);
+  float4 p = make_float4(z.x + c.dt * F.x, z.y + c.dt * F.y, z.z + c.dt * F.z, z.w + c.dt * F.w);
+  float4 o = p;
+  switch (c.mode) {
+    case CM_PLAIN:
+      break;
+    case CM_FAS: {
+      const float4 pb = *reinterpret_cast<const float4*>(c.phib.at(g) + off_out);
+      const float4 rh = *reinterpret_cast<const float4*>(c.rho.at(g) + off_out);
+      const float4 bs = *reinterpret_cast<const float4*>(c.base.at(g) + off_out);
+      o.x = bs.x + ((p.x - pb.x) + rh.x);
+      o.y = bs.y + ((p.y - pb.y) + rh.y);
+      o.z = bs.z + ((p.z - pb.z) + rh.z);
+      o.w = bs.w + ((p.w - pb.w) + rh.w);
+    } break;
+    case CM_RES0: {
+      const float4 v = *reinterpret_cast<const float4*>(c.v.at(g) + off_out);
+      o = make_float4(p.x - v.x, p.y - v.y, p.z - v.z, p.w - v.w);
+      r2 += (double)o.x * (double)o.x;
+      r2 += (double)o.y * (double)o.y;
+      r2 += (double)o.z * (double)o.z;
+      r2 += (double)o.w * (double)o.w;
+    } break;
+    case CM_RESL: {
+      const float4 pb = *reinterpret_cast<const float4*>(c.phib.at(g) + off_out);
+      const float4 rh = *reinterpret_cast<const float4*>(c.rho.at(g) + off_out);
+      const float4 bs = *reinterpret_cast<const float4*>(c.base.at(g) + off_out);
+      const float4 v = *reinterpret_cast<const float4*>(c.v.at(g) + off_out);
+      o.x = ((p.x - pb.x) + rh.x) - (v.x - bs.x);
+      o.y = ((p.y - pb.y) + rh.y) - (v.y - bs.y);
+      o.z = ((p.z - pb.z) + rh.z) - (v.z - bs.z);
+      o.w = ((p.w - pb.w) + rh.w) - (v.w - bs.w);
+    } break;
+    default:
+      return p;
+  }
+  *reinterpret_cast<float4*>(c.out.at(g) + off_out) = o;
+  return p;
+}
+
 // GEMM epilogues. acc is the fp32 accumulator of C = A.B^T (row `row`, column
 // `col`); everything else is fused here so the activations of one layer are
 // written exactly once (tensor.cpp:205-218 linear = x W^T + b, blocks.cpp:246-292).
@@ -214,7 +258,7 @@ __device__ __forceinline__ double epilogue_rowv(const EpiArgs& e, int g, int b, 
         o[i] = acc[i] + bv[i];
         t1[i] = gelu_f(o[i]);
       }
-      st4(e.out1.at(g) + (long long)row * e.out1.ld + col0, o);
+      if (e.out1.ok()) st4(e.out1.at(g) + (long long)row * e.out1.ld + col0, o);
       st4(e.out2.at(g) + (long long)row * e.out2.ld + col0, t1);
     } break;
     case EPI_GELU_BWD: {
@@ -289,7 +333,7 @@ __device__ __forceinline__ double epilogue_4x4(const EpiArgs& e, int g, int b, i
       for (int i = 0; i < 4; ++i) {
         if (rows[i] < 0) continue;
         const float4 hv = add(acc[i], bv);
-        st4g(e.out1.at(g) + (long long)rows[i] * e.out1.ld + col, hv);
+        if (e.out1.ok()) st4g(e.out1.at(g) + (long long)rows[i] * e.out1.ld + col, hv);
         st4g(e.out2.at(g) + (long long)rows[i] * e.out2.ld + col,
              make_float4(gelu_f(hv.x), gelu_f(hv.y), gelu_f(hv.z), gelu_f(hv.w)));
       }
@@ -389,11 +433,11 @@ __device__ __forceinline__ double epilogue_row(const EpiArgs& e, int g, int b, i
       }
     } break;
     case EPI_BIAS_GELU: {
-      float* o1 = e.out1.at(g) + (long long)row * e.out1.ld + col0;
+      float* o1 = e.out1.ok() ? e.out1.at(g) + (long long)row * e.out1.ld + col0 : nullptr;
       float* o2 = e.out2.at(g) + (long long)row * e.out2.ld + col0;
       for (int i = 0; i < n; ++i) {
         const float hv = bias ? acc[i] + bias[col0 + i] : acc[i];
-        o1[i] = hv;
+        if (o1) o1[i] = hv;
         o2[i] = gelu_f(hv);
       }
     } break;

@@ -656,7 +656,7 @@ static bool use_fused_attn() {
 }
 
 void Engine::attention_fwd(int G, Mat Q, Mat K, Mat V, Mat O, Mat P, int sq, int skv,
-                           bool causal) {
+                           bool causal, bool keep_p) {
   const int H = sd_.heads, dh = sd_.d / H;
   auto heads = [&](Mat m, int s) {
     m.bstride = (long long)s * m.ld;
@@ -688,6 +688,8 @@ void Engine::attention_fwd(int G, Mat Q, Mat K, Mat V, Mat O, Mat P, int sq, int
     at.P = P;
     at.range_flag = range_flag_;
     if (attn_tc_supported(at, false)) {
+      // P is only an intermediate of the backward: not stored for scratch evaluations
+      if (!keep_p) at.P = Mat{};
       ++launches_;
       prof_shape_ = {sq, skv, dh, G * B_ * H};
       timed(PROF_ATTN, 4.0 * G * B_ * H * (double)sq * skv * dh, 0.0,
@@ -962,7 +964,8 @@ void Engine::encoder_forward(const EvalSpec& e, int R, bool causal, Mat X, Mat Y
   g.ep.bias = par(L.b_qkv, 0, l0, ls);
   gemm(g);
 
-  attention_fwd(G, qkv, qkv.offset(d), qkv.offset(2 * d), ctx, Pm, R / B_, R / B_, causal);
+  attention_fwd(G, qkv, qkv.offset(d), qkv.offset(2 * d), ctx, Pm, R / B_, R / B_, causal,
+                keep_lin(e));
 
   g = GemmArgs{};
   g.G = G;
@@ -998,7 +1001,7 @@ void Engine::encoder_forward(const EvalSpec& e, int R, bool causal, Mat X, Mat Y
   g.B = par(L.w_in, d, l0, ls);
   g.Bhl = par_hl(L, L.w_in, l0, ls, false);
   g.ep.kind = EPI_BIAS_GELU;
-  g.ep.out1 = hh;
+  if (keep_lin(e)) g.ep.out1 = hh;  // pre-activation: only the backward reads it
   g.ep.out2 = gg;
   g.ep.bias = par(L.b_in, 0, l0, ls);
   gemm(g);
@@ -1092,7 +1095,7 @@ void Engine::decoder_forward(const EvalSpec& e) {
   g.ep.bias = par(L.b_qkv, 0, l0, ls);
   gemm(g);
 
-  attention_fwd(G, qkv, qkv.offset(d), qkv.offset(2 * d), ctx, Pm, sy_, sy_, true);
+  attention_fwd(G, qkv, qkv.offset(d), qkv.offset(2 * d), ctx, Pm, sy_, sy_, true, keep_lin(e));
 
   g = mk(R, d, d, ctx, L.w_o, d);
   g.ep.kind = EPI_BIAS_ADD2;
@@ -1124,7 +1127,7 @@ void Engine::decoder_forward(const EvalSpec& e) {
   g.ep.bias = par(L.b_ckv, 0, l0, ls);
   gemm(g);
 
-  attention_fwd(G, cq, ckv, ckv.offset(d), cctx, cP, sy_, sx_, false);
+  attention_fwd(G, cq, ckv, ckv.offset(d), cctx, cP, sy_, sx_, false, keep_lin(e));
 
   g = mk(R, d, d, cctx, L.w_co, d);
   g.ep.kind = EPI_BIAS_ADD2;
@@ -1147,7 +1150,7 @@ void Engine::decoder_forward(const EvalSpec& e) {
 
   g = mk(R, f, d, n2, L.w_in, d);
   g.ep.kind = EPI_BIAS_GELU;
-  g.ep.out1 = hh;
+  if (keep_lin(e)) g.ep.out1 = hh;  // pre-activation: only the backward reads it
   g.ep.out2 = gg;
   g.ep.bias = par(L.b_in, 0, l0, ls);
   gemm(g);
@@ -2115,6 +2118,7 @@ void Engine::adjoint_step_device(int layer, double dt, const float* z, const flo
   f.layer0 = layer;
   f.in = state_mat(const_cast<float*>(z), state_n_, sd_.d, 0, 1);
   f.act = ActRef{scratch_, al_.size, 0, 1};
+  f.keep_act = true;
   f.cmb.mode = CM_NONE;
   eval_forward(f);
   EvalSpec e = f;

@@ -205,6 +205,7 @@ class Engine {
     // cache (slot = layer) when captured for the parameter pass
     ActRef bact{nullptr, 0, 0, 1};
     bool wgrad_only = false;  // intermediates already in bact: only form dW, db
+    bool keep_act = false;    // scratch activations are read by a following adjoint
   };
   void eval_forward(const EvalSpec& e);
   void eval_adjoint(const EvalSpec& e);
@@ -217,7 +218,11 @@ class Engine {
   // S = Q.K^T, P = softmax(S/sqrt(dh)), O = P.V (blocks.cpp:142-170) and the
   // VJP (blocks.cpp:172-236). Q/K/V/O are token-major [tokens][ld] column
   // slices (head h at columns h*dh); P is [B][H][sq][skv] per member.
-  void attention_fwd(int G, Mat Q, Mat K, Mat V, Mat O, Mat P, int sq, int skv, bool causal);
+  void attention_fwd(int G, Mat Q, Mat K, Mat V, Mat O, Mat P, int sq, int skv, bool causal,
+                     bool keep_p);
+  // the activations of this evaluation are the linearization the adjoint
+  // reads (cache), not per-evaluation scratch
+  bool keep_lin(const EvalSpec& e) const { return e.act.base != scratch_ || e.keep_act; }
   void attention_bwd(int G, Mat Q, Mat K, Mat V, Mat P, Mat dO, Mat dP, Mat dQ, Mat dK, Mat dV,
                      int sq, int skv);
   int gemm_blocks(const GemmArgs& g) const;

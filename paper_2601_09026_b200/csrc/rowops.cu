@@ -142,6 +142,173 @@ __global__ void __launch_bounds__(256) ln_bwd_kernel(LnBwdArgs a, const int* act
   }
 }
 
+// ---- 128-bit vectorised forms (d % 4 == 0, 16-byte aligned rows): lane
+// handles float4 q = lane + 32 i; all of a row's loads are issued before any
+// arithmetic (the row lives in registers) ----
+__device__ __forceinline__ float4 ld4(const float* p) { return *reinterpret_cast<const float4*>(p); }
+__device__ __forceinline__ void st4(float* p, float4 v) { *reinterpret_cast<float4*>(p) = v; }
+
+template <int V4>
+__global__ void __launch_bounds__(256) ln_fwd4_kernel(LnFwdArgs a, const int* active) {
+  if (stopped(active)) return;
+  const int g = blockIdx.y;
+  const int row = blockIdx.x * kRowsPerBlock + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= a.rows) return;
+  const float* x = a.x.at(g) + (long long)row * a.x.ld;
+  const int d4 = a.d >> 2;
+  float4 v[V4];
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < V4; ++i) {
+    const int q = lane + 32 * i;
+    v[i] = q < d4 ? ld4(x + 4 * q) : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+#pragma unroll
+  for (int i = 0; i < V4; ++i) s += (v[i].x + v[i].y) + (v[i].z + v[i].w);
+  const float inv_d = 1.f / (float)a.d;
+  const float mean = warp_sum(s) * inv_d;
+  float qs = 0.f;
+#pragma unroll
+  for (int i = 0; i < V4; ++i) {
+    if (lane + 32 * i < d4) {
+      const float c0 = v[i].x - mean, c1 = v[i].y - mean, c2 = v[i].z - mean, c3 = v[i].w - mean;
+      qs += (c0 * c0 + c1 * c1) + (c2 * c2 + c3 * c3);
+    }
+  }
+  const float var = warp_sum(qs) * inv_d;
+  const float rstd = 1.f / sqrtf(var + a.eps);
+  const float* gain = a.gain.at(g);
+  const float* bias = a.bias.at(g);
+  float* o = a.out.at(g) + (long long)row * a.out.ld;
+#pragma unroll
+  for (int i = 0; i < V4; ++i) {
+    const int q = lane + 32 * i;
+    if (q < d4) {
+      const float4 gn = ld4(gain + 4 * q), bs = ld4(bias + 4 * q);
+      st4(o + 4 * q, make_float4(gn.x * ((v[i].x - mean) * rstd) + bs.x,
+                                 gn.y * ((v[i].y - mean) * rstd) + bs.y,
+                                 gn.z * ((v[i].z - mean) * rstd) + bs.z,
+                                 gn.w * ((v[i].w - mean) * rstd) + bs.w));
+    }
+  }
+  if (lane == 0 && a.stats.ok()) {
+    float* st = a.stats.at(g) + 2LL * row;
+    st[0] = mean;
+    st[1] = rstd;
+  }
+}
+
+template <int V4>
+__global__ void __launch_bounds__(256) ln_bwd4_kernel(LnBwdArgs a, const int* active) {
+  __shared__ double red[32];
+  if (stopped(active)) return;
+  const int g = blockIdx.y;
+  const int row = blockIdx.x * kRowsPerBlock + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  const int d4 = a.d >> 2;
+  double r2 = 0.0;
+  if (row < a.rows) {
+    const float* x = a.x.at(g) + (long long)row * a.x.ld;
+    const float* up = a.up.at(g) + (long long)row * a.up.ld;
+    const float* gain = a.gain.at(g);
+    const float mean = a.stats.at(g)[2LL * row];
+    const float rstd = a.stats.at(g)[2LL * row + 1];
+    float4 xh[V4], dxh[V4];
+#pragma unroll
+    for (int i = 0; i < V4; ++i) {
+      const int q = lane + 32 * i;
+      if (q < d4) {
+        xh[i] = ld4(x + 4 * q);
+        dxh[i] = ld4(up + 4 * q);
+      }
+    }
+    float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+    for (int i = 0; i < V4; ++i) {
+      const int q = lane + 32 * i;
+      if (q < d4) {
+        const float4 gn = ld4(gain + 4 * q);
+        xh[i] = make_float4((xh[i].x - mean) * rstd, (xh[i].y - mean) * rstd,
+                            (xh[i].z - mean) * rstd, (xh[i].w - mean) * rstd);
+        dxh[i] = make_float4(dxh[i].x * gn.x, dxh[i].y * gn.y, dxh[i].z * gn.z, dxh[i].w * gn.w);
+        s1 += (dxh[i].x + dxh[i].y) + (dxh[i].z + dxh[i].w);
+        s2 += (dxh[i].x * xh[i].x + dxh[i].y * xh[i].y) + (dxh[i].z * xh[i].z + dxh[i].w * xh[i].w);
+      }
+    }
+    const float inv_d = 1.f / (float)a.d;
+    const float m1 = warp_sum(s1) * inv_d;
+    const float m2 = warp_sum(s2) * inv_d;
+    const float* addA = a.addA.ok() ? a.addA.at(g) + (long long)row * a.addA.ld : nullptr;
+    const float* addB = a.addB.ok() ? a.addB.at(g) + (long long)row * a.addB.ld : nullptr;
+    float* o1 = a.out1.ok() ? a.out1.at(g) + (long long)row * a.out1.ld : nullptr;
+    float* o2 = a.out2.ok() ? a.out2.at(g) + (long long)row * a.out2.ld : nullptr;
+    const bool comb = a.cmb.mode != CM_NONE;
+    const long long off_out = comb ? (long long)row * a.cmb.out.ld : 0;
+    const long long off_z = comb ? (long long)row * a.cmb.z.ld : 0;
+    float4 ad[V4];
+#pragma unroll
+    for (int i = 0; i < V4; ++i) {
+      const int q = lane + 32 * i;
+      if (q < d4) {
+        if (addA) ad[i] = ld4(addA + 4 * q);
+        else if (addB) ad[i] = ld4(addB + 4 * q);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < V4; ++i) {
+      const int q = lane + 32 * i;
+      if (q < d4) {
+        const float4 L = make_float4(rstd * (dxh[i].x - m1 - xh[i].x * m2),
+                                     rstd * (dxh[i].y - m1 - xh[i].y * m2),
+                                     rstd * (dxh[i].z - m1 - xh[i].z * m2),
+                                     rstd * (dxh[i].w - m1 - xh[i].w * m2));
+        const float4 v1 = addA ? make_float4(ad[i].x + L.x, ad[i].y + L.y, ad[i].z + L.z, ad[i].w + L.w) : L;
+        if (o1) st4(o1 + 4 * q, v1);
+        if (o2) {
+          const float4 b = addA ? ld4(addB + 4 * q) : ad[i];
+          st4(o2 + 4 * q, make_float4(b.x + L.x, b.y + L.y, b.z + L.z, b.w + L.w));
+        }
+        if (comb) combine_apply4(a.cmb, g, off_out + 4 * q, off_z + 4 * q, v1, r2);
+      }
+    }
+  }
+  if (a.cmb.mode == CM_RES0) {
+    const double t = block_sum_f64(r2, red);
+    if (threadIdx.x == 0)
+      a.cmb.norm_partials[a.cmb.norm_base + blockIdx.y * a.cmb.norm_member_stride + blockIdx.x] = t;
+  }
+}
+
+template <int V4>
+struct LnFwd4L {
+  static void launch(dim3 g, const LnFwdArgs& a, const int* act, cudaStream_t s) {
+    ln_fwd4_kernel<V4><<<g, 256, 0, s>>>(a, act);
+  }
+};
+template <int V4>
+struct LnBwd4L {
+  static void launch(dim3 g, const LnBwdArgs& a, const int* act, cudaStream_t s) {
+    ln_bwd4_kernel<V4><<<g, 256, 0, s>>>(a, act);
+  }
+};
+
+template <template <int> class K, class Args>
+void dispatch_rows4(int d, const Args& a, int G, int rows, const int* active, cudaStream_t s) {
+  dim3 grid(ceil_div(rows, kRowsPerBlock), G);
+  const int v = (d / 4 + 31) / 32;
+  if (v <= 1) K<1>::launch(grid, a, active, s);
+  else if (v <= 2) K<2>::launch(grid, a, active, s);
+  else if (v <= 4) K<4>::launch(grid, a, active, s);
+  else if (v <= 6) K<6>::launch(grid, a, active, s);
+  else K<8>::launch(grid, a, active, s);
+}
+
+bool vec_ok(const Mat& m) {
+  return !m.ok() || ((reinterpret_cast<uintptr_t>(m.ptr) & 15) == 0 && m.ld % 4 == 0 &&
+                     m.slot_stride % 4 == 0);
+}
+
 template <template <int> class K, class Args>
 void dispatch_rows(int d, const Args& a, int G, int rows, const int* active, cudaStream_t s) {
   dim3 grid(ceil_div(rows, kRowsPerBlock), G);
@@ -398,14 +565,23 @@ __global__ void cycle_end_kernel(SolveCtrl* c, double tol) {
 
 void launch_ln_fwd(const LnFwdArgs& a, const int* active, cudaStream_t s) {
   if (a.rows == 0 || a.G == 0) return;
-  dispatch_rows<LnFwdL>(a.d, a, a.G, a.rows, active, s);
+  if (a.d % 4 == 0 && vec_ok(a.x) && vec_ok(a.out) && vec_ok(a.gain) && vec_ok(a.bias))
+    dispatch_rows4<LnFwd4L>(a.d, a, a.G, a.rows, active, s);
+  else
+    dispatch_rows<LnFwdL>(a.d, a, a.G, a.rows, active, s);
 }
 
 int ln_bwd_blocks(int rows) { return ceil_div(rows, kRowsPerBlock); }
 
 void launch_ln_bwd(const LnBwdArgs& a, const int* active, cudaStream_t s) {
   if (a.rows == 0 || a.G == 0) return;
-  dispatch_rows<LnBwdL>(a.d, a, a.G, a.rows, active, s);
+  const Combine& c = a.cmb;
+  if (a.d % 4 == 0 && vec_ok(a.x) && vec_ok(a.up) && vec_ok(a.gain) && vec_ok(a.addA) &&
+      vec_ok(a.addB) && vec_ok(a.out1) && vec_ok(a.out2) && vec_ok(c.z) && vec_ok(c.out) &&
+      vec_ok(c.base) && vec_ok(c.phib) && vec_ok(c.rho) && vec_ok(c.v))
+    dispatch_rows4<LnBwd4L>(a.d, a, a.G, a.rows, active, s);
+  else
+    dispatch_rows<LnBwdL>(a.d, a, a.G, a.rows, active, s);
 }
 
 void launch_softmax(const SoftmaxArgs& a, const int* active, cudaStream_t s) {
