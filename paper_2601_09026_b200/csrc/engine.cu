@@ -147,6 +147,7 @@ Engine::~Engine() {
   for (float* p : {P_, Whl_, Gr_, scratch_, cache_, bscratch_, bcache_, traj_, lam_all_,
                    zero_state_, snap_fwd_, snap_bwd_})
     if (p) cudaFree(p);
+  if (colred_part_) cudaFree(colred_part_);
   drop_graph();
   for (cudaEvent_t ev : ev_pool_) cudaEventDestroy(ev);
   if (stream_) cudaStreamDestroy(stream_);
@@ -401,6 +402,8 @@ void Engine::set_shape(int batch, int s_x, int s_y) {
   drop_graph();
   free_solver(fwd_);
   free_solver(bwd_);
+  if (colred_part_) cudaFree(colred_part_);
+  colred_part_ = nullptr;
   for (float** p : {&scratch_, &cache_, &bscratch_, &bcache_, &traj_, &lam_all_, &zero_state_, &snap_fwd_,
                     &snap_bwd_}) {
     if (*p) cudaFree(*p);
@@ -471,6 +474,9 @@ void Engine::set_shape(int batch, int s_x, int s_y) {
   MGLP_CUDA(cudaMalloc(&cache_, (size_t)total_ * al_.size * sizeof(float)));
   MGLP_CUDA(cudaMalloc(&bscratch_, (size_t)Gmax_ * bl_.size * sizeof(float)));
   MGLP_CUDA(cudaMalloc(&bcache_, (size_t)total_ * bl_.size * sizeof(float)));
+  colred_cap_ = (long long)std::max(total_, Gmax_) * kColRedChunks *
+                std::max(std::max(3 * sd_.d, sd_.ffn), 2 * sd_.d) * 2;
+  MGLP_CUDA(cudaMalloc(&colred_part_, (size_t)colred_cap_ * sizeof(double)));
   bcache_valid_.assign(total_, 0);
   MGLP_CUDA(cudaMalloc(&traj_, (size_t)(total_ + 1) * state_n_ * sizeof(float)));
   MGLP_CUDA(cudaMalloc(&lam_all_, (size_t)(total_ + 1) * state_n_ * sizeof(float)));
@@ -1362,6 +1368,8 @@ void Engine::encoder_adjoint(const EvalSpec& e, bool causal) {
       c.dbias = grad(b, 0, l0, ls);
       if (x.ok()) c.dgain = grad(gn, 0, l0, ls);
       c.gscale = gs;
+      c.partials = colred_part_;
+      c.partials_cap = colred_cap_;
       ++launches_;
       prof_shape_ = {5, c.cols, 0, c.G};
       timed(PROF_ROW, 0.0, (x.ok() ? 8.0 : 4.0) * c.G * (double)c.rows * c.cols,
@@ -1550,6 +1558,8 @@ void Engine::decoder_adjoint(const EvalSpec& e) {
       c.dbias = grad(b, 0, l0, ls);
       if (x.ok()) c.dgain = grad(gn, 0, l0, ls);
       c.gscale = gs;
+      c.partials = colred_part_;
+      c.partials_cap = colred_cap_;
       ++launches_;
       prof_shape_ = {5, c.cols, 0, c.G};
       timed(PROF_ROW, 0.0, (x.ok() ? 8.0 : 4.0) * c.G * (double)c.rows * c.cols,

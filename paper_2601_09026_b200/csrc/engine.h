@@ -302,6 +302,8 @@ class Engine {
   float* scratch_ = nullptr;  // Gmax forward activation slots
   float* cache_ = nullptr;    // total_ forward activation slots (slot = layer)
   float* bscratch_ = nullptr; // Gmax backward slots
+  double* colred_part_ = nullptr;  // f64 column-sum partials (rowops.cu colred)
+  long long colred_cap_ = 0;
   float* bcache_ = nullptr;   // total_ backward slots (slot = layer), for the parameter pass
   std::vector<char> bcache_valid_;
   float* traj_ = nullptr;     // total_+1 states

@@ -36,7 +36,12 @@ struct ColRedArgs {
   Mat up, x, stats;
   Mat dgain, dbias;  // slot = layer
   float gscale = 1.f;
+  // optional f64 scratch (>= G * kColRedChunks * cols * 2 doubles): enables the
+  // two-stage row-chunked form (fixed-order partials, then an ordered sum)
+  double* partials = nullptr;
+  long long partials_cap = 0;
 };
+constexpr int kColRedChunks = 8;
 void launch_colred(const ColRedArgs& a, const int* active, cudaStream_t s);
 
 // Row softmax of attention scores S [rows][ncols] in place (scale, causal

@@ -309,6 +309,82 @@ bool vec_ok(const Mat& m) {
                      m.slot_stride % 4 == 0);
 }
 
+// Column sums in two stages: stage 1 = (128-column tile, row chunk, member)
+// blocks, float4 rows, f64 partials reduced over the 8 row lanes in fixed
+// order; stage 2 = ordered sum over the chunks, scaled into the gradients.
+__global__ void __launch_bounds__(256) colred_part_kernel(ColRedArgs a, const int* active) {
+  __shared__ double sb[8][129];
+  __shared__ double sg[8][129];
+  if (stopped(active)) return;
+  const int g = blockIdx.z, chunk = blockIdx.y;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int c = blockIdx.x * 128 + 4 * tx;
+  const int rpc = (a.rows + kColRedChunks - 1) / kColRedChunks;
+  const int r0 = chunk * rpc, r1 = min(a.rows, r0 + rpc);
+  double b[4] = {0.0, 0.0, 0.0, 0.0}, gs[4] = {0.0, 0.0, 0.0, 0.0};
+  if (c < a.cols) {
+    const float* up = a.up.at(g);
+    const float* x = a.x.ok() ? a.x.at(g) : nullptr;
+    const float* st = x ? a.stats.at(g) : nullptr;
+#pragma unroll 4
+    for (int r = r0 + ty; r < r1; r += 8) {
+      const float4 u = ld4(up + (long long)r * a.up.ld + c);
+      b[0] += (double)u.x;
+      b[1] += (double)u.y;
+      b[2] += (double)u.z;
+      b[3] += (double)u.w;
+      if (x) {
+        const float4 xv = ld4(x + (long long)r * a.x.ld + c);
+        const float m = st[2LL * r], rs = st[2LL * r + 1];
+        gs[0] += (double)u.x * (double)((xv.x - m) * rs);
+        gs[1] += (double)u.y * (double)((xv.y - m) * rs);
+        gs[2] += (double)u.z * (double)((xv.z - m) * rs);
+        gs[3] += (double)u.w * (double)((xv.w - m) * rs);
+      }
+    }
+  }
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    sb[ty][4 * tx + e] = b[e];
+    sg[ty][4 * tx + e] = gs[e];
+  }
+  __syncthreads();
+  if (threadIdx.x < 128) {
+    const int col = blockIdx.x * 128 + threadIdx.x;
+    if (col < a.cols) {
+      double tb = 0.0, tg = 0.0;
+      for (int i = 0; i < 8; ++i) {
+        tb += sb[i][threadIdx.x];
+        tg += sg[i][threadIdx.x];
+      }
+      double* p = a.partials + (((long long)g * kColRedChunks + chunk) * a.cols + col) * 2;
+      p[0] = tb;
+      p[1] = tg;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) colred_sum_kernel(ColRedArgs a, const int* active) {
+  if (stopped(active)) return;
+  const int g = blockIdx.y;
+  const int col = blockIdx.x * 256 + threadIdx.x;
+  if (col >= a.cols) return;
+  double tb = 0.0, tg = 0.0;
+  for (int ch = 0; ch < kColRedChunks; ++ch) {
+    const double* p = a.partials + (((long long)g * kColRedChunks + ch) * a.cols + col) * 2;
+    tb += p[0];
+    tg += p[1];
+  }
+  if (a.dbias.ok()) {
+    float* db = a.dbias.at(g);
+    db[col] = db[col] + a.gscale * (float)tb;
+  }
+  if (a.x.ok() && a.dgain.ok()) {
+    float* dg = a.dgain.at(g);
+    dg[col] = dg[col] + a.gscale * (float)tg;
+  }
+}
+
 template <template <int> class K, class Args>
 void dispatch_rows(int d, const Args& a, int G, int rows, const int* active, cudaStream_t s) {
   dim3 grid(ceil_div(rows, kRowsPerBlock), G);
@@ -592,6 +668,12 @@ void launch_softmax(const SoftmaxArgs& a, const int* active, cudaStream_t s) {
 
 void launch_colred(const ColRedArgs& a, const int* active, cudaStream_t s) {
   if (a.rows == 0 || a.G == 0) return;
+  if (a.partials && a.cols % 4 == 0 && vec_ok(a.up) && vec_ok(a.x) &&
+      (long long)a.G * kColRedChunks * a.cols * 2 <= a.partials_cap) {
+    colred_part_kernel<<<dim3(ceil_div(a.cols, 128), kColRedChunks, a.G), 256, 0, s>>>(a, active);
+    colred_sum_kernel<<<dim3(ceil_div(a.cols, 256), a.G), 256, 0, s>>>(a, active);
+    return;
+  }
   dim3 grid(ceil_div(a.cols, 32), a.G);
   colred_kernel<<<grid, 256, 0, s>>>(a, active);
 }
