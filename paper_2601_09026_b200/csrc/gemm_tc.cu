@@ -38,6 +38,7 @@
 
 #include <algorithm>
 #include <cfloat>
+#include <cstdio>
 #include <cstdlib>
 #include <mutex>
 
@@ -52,12 +53,15 @@ namespace {
 
 constexpr int BK = 32;          // K elements per stage (one 128-byte fp32 row span)
 constexpr int ROWS = 128;       // operand rows per CTA per stage (A and B)
-constexpr int STAGES = 3;
 constexpr int TILE_BYTES = ROWS * BK * 4;  // 16 KiB: fp32 staging tile == hi|lo tile
-constexpr int STAGE_BYTES = 4 * TILE_BYTES;  // stgA, stgB, hlA, hlB
-// + barriers (512 B) + per-epilogue-warp 32 x 16 fp32 transpose buffers
-constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 512 + 8 * 2048;
-constexpr int BSLOTS = 2 * STAGES;  // ring depth of a pre-split B
+// 12 tile slots shared by the rings. B converted in smem: 3 staging stages
+// (stgA, stgB) + 3 hi|lo stages (hlA, hlB). B pre-split: A staging, hi|lo A
+// and the B ring 4 deep each (measured best of the 12-slot splits; the
+// mainloop is MMA-bound at the power-capped clock, not load-bound).
+constexpr int NSLOTS = 12;
+constexpr int MAXR = 8;  // barrier array length
+// + barriers (1 KiB) + per-epilogue-warp 32 x 16 fp32 transpose buffers
+constexpr int SMEM_BYTES = NSLOTS * TILE_BYTES + 1024 /*align*/ + 1024 + 8 * 2048;
 
 
 struct TcParams {
@@ -67,8 +71,10 @@ struct TcParams {
   int a_mn, b_mn;  // staging layout of the converted operands
   int b_direct;    // B comes pre-split (hi|lo tiles TMA'd straight into the MMA ring)
   int passes;      // 3 = hi.hi + (lo.hi + hi.lo); 1 = hi.hi only (diagnostics)
+  int ring_a, ring_h, ring_b;  // pre-split B: staging / hi|lo / B ring depths
   int vec_ok;      // every epilogue operand row start is 16-byte aligned
   int* range_flag;
+  unsigned long long* prof;  // MGLP_GEMM_PROF: cycles spent per barrier wait kind (diagnostics)
   int debug;  // MGLP_DEBUG_GEMM bits (timing diagnostics only): 1 skip conversion, 2 skip epilogue stores
   EpiArgs ep;
 };
@@ -140,14 +146,14 @@ __global__ void __launch_bounds__(Cfg<CG>::THREADS, 1)
   if (active && *(volatile const int*)active == 0) return;
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
-  uint64_t* fullA = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
-  uint64_t* fullB = fullA + STAGES;    // [BSLOTS]
-  uint64_t* emptyB = fullB + BSLOTS;   // [BSLOTS]
-  uint64_t* sfree = emptyB + BSLOTS;
-  uint64_t* conv = sfree + STAGES;
-  uint64_t* empty = conv + STAGES;
-  uint64_t* cdone = empty + STAGES;  // CG = 2, follower CTA: converters -> signaler
-  uint64_t* tfull = cdone + STAGES;   // [NACC]
+  uint64_t* fullA = reinterpret_cast<uint64_t*>(smem + NSLOTS * TILE_BYTES);  // [NA]
+  uint64_t* fullB = fullA + MAXR;    // [NB]
+  uint64_t* emptyB = fullB + MAXR;   // [NB]
+  uint64_t* sfree = emptyB + MAXR;   // [NA]
+  uint64_t* conv = sfree + MAXR;     // [NH]
+  uint64_t* empty = conv + MAXR;     // [NH]
+  uint64_t* cdone = empty + MAXR;    // [NH] CG = 2, follower CTA: converters -> signaler
+  uint64_t* tfull = cdone + MAXR;    // [NACC]
   uint64_t* tempty = tfull + NACC;    // [NACC]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + NACC);
   double* red = reinterpret_cast<double*>(tmem_slot + 2);  // [NACC][EPI_WARPS]
@@ -163,14 +169,15 @@ __global__ void __launch_bounds__(Cfg<CG>::THREADS, 1)
   const int per_prob = tiles_n * tiles_m;
   const int total = per_prob * p.G * p.Bb * p.H;
 
-  auto stg_a = [&](int s) { return smem + s * STAGE_BYTES; };
-  auto stg_b = [&](int s) { return smem + s * STAGE_BYTES + TILE_BYTES; };
-  auto hl_a = [&](int s) { return smem + s * STAGE_BYTES + 2 * TILE_BYTES; };
-  auto hl_b = [&](int s) { return smem + s * STAGE_BYTES + 3 * TILE_BYTES; };
-  // a pre-split B has no staging: its ring takes both B buffers of every
-  // stage (BSLOTS = 2 x STAGES deep), so weight tiles stream in far ahead of
-  // the MMAs and their TMA latency stays hidden
-  auto b_slot = [&](int j) { return j < STAGES ? hl_b(j) : stg_b(j - STAGES); };
+  // ring depths: NA staging stages, NH hi|lo stages, NB pre-split B slots
+  const bool direct = p.b_direct != 0;
+  const int NA = direct ? p.ring_a : 3, NH = direct ? p.ring_h : 3, NB = p.ring_b;
+  auto slot = [&](int i) { return smem + i * TILE_BYTES; };
+  auto stg_a = [&](int s) { return direct ? slot(s) : slot(2 * s); };
+  auto stg_b = [&](int s) { return slot(2 * s + 1); };
+  auto hl_a = [&](int s) { return direct ? slot(NA + s) : slot(6 + 2 * s); };
+  auto hl_b = [&](int s) { return slot(7 + 2 * s); };
+  auto b_slot = [&](int j) { return slot(NA + NH + j); };
   struct Tile {
     int z, g, b, h, m0, n0, mt, nt;
   };
@@ -189,17 +196,15 @@ __global__ void __launch_bounds__(Cfg<CG>::THREADS, 1)
   };
 
   if (threadIdx.x == 0) {
-    for (int j = 0; j < BSLOTS; ++j) {
+    for (int j = 0; j < MAXR; ++j) {
       mbar_init(&fullB[j], 1);
       mbar_init(&emptyB[j], 1);  // MMA commit
-    }
-    for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&fullA[s], 1);
-      mbar_init(&sfree[s], 4);  // each converter warp, after its staging reads
+      mbar_init(&fullA[j], 1);
+      mbar_init(&sfree[j], 4);  // each converter warp, after its staging reads
       // leader: its 4 converter warps (+ the follower's signaler for CG = 2)
-      mbar_init(&conv[s], CG == 1 ? 4 : 5);
-      mbar_init(&empty[s], 1);  // MMA commit
-      mbar_init(&cdone[s], 4);
+      mbar_init(&conv[j], CG == 1 ? 4 : 5);
+      mbar_init(&empty[j], 1);  // MMA commit
+      mbar_init(&cdone[j], 4);
     }
     for (int a = 0; a < NACC; ++a) {
       mbar_init(&tfull[a], 1);
@@ -225,6 +230,22 @@ __global__ void __launch_bounds__(Cfg<CG>::THREADS, 1)
   if constexpr (CG == 2) cluster_sync();  // peer barriers initialised before any remote arrive
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem_base = *tmem_slot;
+  // diagnostics: cycles a role spends waiting, per barrier kind
+  unsigned long long wt = 0;
+  auto wait = [&](uint64_t* bar, uint32_t parity) {
+    if (p.prof) {
+      const long long t0 = clock64();
+      mbar_wait(bar, parity);
+      wt += (unsigned long long)(clock64() - t0);
+    } else {
+      mbar_wait(bar, parity);
+    }
+  };
+  auto flush = [&](int kind) {
+    if (p.prof && wt) atomicAdd(&p.prof[kind], wt);
+    wt = 0;
+  };
+  const long long t_start = clock64();
 
   if (warp == 0) {
     // ===== TMA producer: fp32 operand tiles into the staging ring =====
@@ -235,9 +256,10 @@ __global__ void __launch_bounds__(Cfg<CG>::THREADS, 1)
         const Tile T = tile_of(t);
         const int nb0 = T.n0 + (int)cr * 128;
         for (int kb = 0; kb < nk; ++kb, ++kg) {
-          const int s = kg % STAGES;
-          const uint32_t ph = (kg / STAGES) & 1;
-          mbar_wait(&sfree[s], ph ^ 1);
+          const int s = kg % NA;
+          const uint32_t ph = (kg / NA) & 1;
+          wait(&sfree[s], ph ^ 1);
+          flush(0);
           mbar_expect_tx(&fullA[s], bytes);
           const int k0 = kb * BK;
           int c[5];
@@ -265,8 +287,9 @@ __global__ void __launch_bounds__(Cfg<CG>::THREADS, 1)
         const Tile T = tile_of(t);
         const int nb0 = T.n0 + (int)cr * 128;
         for (int kb = 0; kb < nk; ++kb, ++kg) {
-          const int j = kg % BSLOTS;
-          mbar_wait(&emptyB[j], ((kg / BSLOTS) & 1) ^ 1);
+          const int j = kg % NB;
+          wait(&emptyB[j], ((kg / NB) & 1) ^ 1);
+          flush(1);
           mbar_expect_tx(&fullB[j], TILE_BYTES);
           int c[5];
           tma_coords(p.b, kb * BK, nb0, T.g, T.b, T.h, c);
@@ -282,8 +305,9 @@ __global__ void __launch_bounds__(Cfg<CG>::THREADS, 1)
       int kg = 0;
       for (int t = unit; t < total; t += nunits)
         for (int kb = 0; kb < nk; ++kb, ++kg) {
-          const int s = kg % STAGES;
-          mbar_wait(&cdone[s], (kg / STAGES) & 1);
+          const int s = kg % NH;
+          wait(&cdone[s], (kg / NH) & 1);
+          flush(2);
           mbar_arrive_cluster(conv_leader0 + s * 8);
         }
     }
@@ -298,15 +322,17 @@ __global__ void __launch_bounds__(Cfg<CG>::THREADS, 1)
       for (int t = unit; t < total; t += nunits, ++tc) {
         const int acc = tc % NACC;
         const uint32_t aph = (tc / NACC) & 1;
-        mbar_wait(&tempty[acc], aph ^ 1);
+        wait(&tempty[acc], aph ^ 1);
+        flush(3);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t tm = tmem_base + (uint32_t)(acc * 2 * TN);
         for (int kb = 0; kb < nk; ++kb, ++kg) {
-          const int s = kg % STAGES;
-          const uint32_t ph = (kg / STAGES) & 1;
-          mbar_wait(&conv[s], ph);
+          const int s = kg % NH;
+          const uint32_t ph = (kg / NH) & 1;
+          wait(&conv[s], ph);
+          flush(4);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-          const int j = kg % BSLOTS;
+          const int j = kg % NB;
           const uint8_t* bt = p.b_direct ? b_slot(j) : hl_b(s);
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k) {
@@ -336,18 +362,20 @@ __global__ void __launch_bounds__(Cfg<CG>::THREADS, 1)
     int kg = 0;
     for (int t = unit; t < total; t += nunits) {
       for (int kb = 0; kb < nk; ++kb, ++kg) {
-        const int s = kg % STAGES;
-        const uint32_t ph = (kg / STAGES) & 1;
-        mbar_wait(&fullA[s], ph);
-        mbar_wait(&empty[s], ph ^ 1);  // hi|lo buffers no longer read by the MMAs
+        const int sa = kg % NA, s = kg % NH;
+        wait(&fullA[sa], (kg / NA) & 1);
+        if (kc == 0 && lane == 0) flush(5);
+        wait(&empty[s], ((kg / NH) & 1) ^ 1);  // hi|lo buffers no longer read by the MMAs
+        if (kc == 0 && lane == 0) flush(6);
         if (!(p.debug & 1)) {
-          convert_tile(smem_u32(stg_a(s)), smem_u32(hl_a(s)), p.a_mn, kc, lane, amax);
+          convert_tile(smem_u32(stg_a(sa)), smem_u32(hl_a(s)), p.a_mn, kc, lane, amax);
           if (!p.b_direct)
-            convert_tile(smem_u32(stg_b(s)), smem_u32(hl_b(s)), p.b_mn, kc, lane, amax);
+            convert_tile(smem_u32(stg_b(sa)), smem_u32(hl_b(s)), p.b_mn, kc, lane, amax);
         }
         __syncwarp();
-        if (lane == 0) mbar_arrive(&sfree[s]);
-        if (p.b_direct) mbar_wait(&fullB[kg % BSLOTS], (kg / BSLOTS) & 1);
+        if (lane == 0) mbar_arrive(&sfree[sa]);
+        if (p.b_direct) wait(&fullB[kg % NB], (kg / NB) & 1);
+        if (kc == 0 && lane == 0) flush(7);
         // generic-proxy smem writes -> visible to the tensor core (async proxy)
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
@@ -365,13 +393,14 @@ __global__ void __launch_bounds__(Cfg<CG>::THREADS, 1)
     constexpr int COLS = TN / CG;  // columns per epilogue warp
     const bool res0 = p.ep.kind == EPI_FINAL && p.ep.cmb.mode == CM_RES0;
     const uint32_t tempty_leader = CG == 2 ? map_to_rank(smem_u32(&tempty[0]), 0) : 0u;
-    const uint32_t ebuf = smem_u32(smem + STAGES * STAGE_BYTES + 512) + ew * 2048;
+    const uint32_t ebuf = smem_u32(smem + NSLOTS * TILE_BYTES + 1024) + ew * 2048;
     int tc = 0;
     for (int t = unit; t < total; t += nunits, ++tc) {
       const Tile T = tile_of(t);
       const int acc = tc % NACC;
       const uint32_t aph = (tc / NACC) & 1;
-      mbar_wait(&tfull[acc], aph);
+      wait(&tfull[acc], aph);
+      if (ew == 0 && lane == 0) flush(8);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const uint32_t lane_addr =
           tmem_base + (uint32_t)(acc * 2 * TN) + ((uint32_t)(q * 32) << 16);
@@ -468,6 +497,7 @@ __global__ void __launch_bounds__(Cfg<CG>::THREADS, 1)
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
+  if (p.prof && threadIdx.x == 0) atomicAdd(&p.prof[9], (unsigned long long)(clock64() - t_start));
   if constexpr (CG == 2) cluster_sync();
   if (warp == 2) {
     if constexpr (CG == 1)
@@ -623,11 +653,37 @@ Prepared prepare(const GemmArgs& a) {
     return e ? atoi(e) : 3;
   }();
   p.passes = passes;
+  // ring depths for a pre-split B (12 slots): MGLP_GEMM_RINGS="a,h,b" overrides
+  static const int* rings = [] {
+    static int r[3] = {4, 4, 4};
+    if (const char* e = getenv("MGLP_GEMM_RINGS")) {
+      int a = 0, h = 0, b = 0;
+      if (sscanf(e, "%d,%d,%d", &a, &h, &b) == 3 && a >= 1 && h >= 1 && b >= 1 && a <= MAXR &&
+          h <= MAXR && b <= MAXR && a + h + b <= NSLOTS) {
+        r[0] = a;
+        r[1] = h;
+        r[2] = b;
+      }
+    }
+    return r;
+  }();
+  p.ring_a = rings[0];
+  p.ring_h = rings[1];
+  p.ring_b = rings[2];
   static const int debug = [] {
     const char* e = getenv("MGLP_DEBUG_GEMM");
     return e ? atoi(e) : 0;
   }();
   p.debug = debug;
+  p.prof = nullptr;
+  static unsigned long long* prof_buf = [] {
+    unsigned long long* b = nullptr;
+    if (getenv("MGLP_GEMM_PROF")) {
+      if (cudaMalloc(&b, 16 * sizeof(unsigned long long)) != cudaSuccess) b = nullptr;
+    }
+    return b;
+  }();
+  p.prof = prof_buf;
   {
     auto al = [](const Mat& m) {
       return !m.ok() || ((reinterpret_cast<uintptr_t>(m.ptr) & 15) == 0 && m.ld % 4 == 0 &&
@@ -691,6 +747,20 @@ void launch_cg(const GemmArgs& a, const int* active, cudaStream_t s) {
     MGLP_CUDA(cudaLaunchKernelEx(&cfg, gemm_tc_kernel<2>, P.mA, P.mB, P.p, active));
   }
   MGLP_CUDA(cudaGetLastError());
+  if (P.p.prof) {
+    // diagnostics: average cycles per CTA spent in each wait kind
+    unsigned long long h[16];
+    MGLP_CUDA(cudaDeviceSynchronize());
+    MGLP_CUDA(cudaMemcpy(h, P.p.prof, sizeof(h), cudaMemcpyDeviceToHost));
+    MGLP_CUDA(cudaMemset(P.p.prof, 0, sizeof(h)));
+    const double n = (double)(CG * units);
+    static const char* names[10] = {"prodA.sfree", "prodB.emptyB", "signal.cdone", "mma.tempty",
+                                    "mma.conv",    "cvt.fullA",    "cvt.empty",    "cvt.fullB",
+                                    "epi.tfull",   "total"};
+    fprintf(stderr, "[gemm_prof CG=%d M=%d N=%d K=%d G=%d]", CG, a.M, a.N, a.K, a.G);
+    for (int i = 0; i < 10; ++i) fprintf(stderr, " %s=%.0f", names[i], h[i] / n);
+    fprintf(stderr, "\n");
+  }
 }
 
 // the CTA-pair kernel needs at least a full 256 x 256 tile to pay off; the
