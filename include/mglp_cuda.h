@@ -236,7 +236,9 @@ mglp_status mglp_test_gemm(int G, int M, int N, int K, const float* A, long long
  * Q, K, V (and dO, dQ, dK, dV, O) are [B][s][ld] token rows with head h at
  * column h*dh (the qkv layout of the layer); P is [B][H][sq][pad4(skv)].
  * Forward always; with dO set, also the backward (dQ, dK, dV overwritten).
- * sq, skv <= 128 and multiples of 8, dh 32 or 64 (else status 1). The
+ * sq, skv <= 128 and multiples of 8 (attn_tc.cu), or 128 <= sq, skv <= 512
+ * (attn_long.cu: P then receives the per-row (max, 1/sum) statistics, [sq][2]
+ * per head, instead of the probabilities); dh 32 or 64 (else status 1). The
  * reference's attention / vjp_attention (blocks.cpp:142-236). Synchronous. */
 mglp_status mglp_test_attention(int B, int H, int sq, int skv, int dh, int causal, const float* Q,
                                 const float* K, const float* V, int ld, float* O, float* P,

@@ -1,0 +1,544 @@
+// Fused tcgen05 attention for 128 < s <= 512 (GPT-2-style causal decoder,
+// s = 512; ViT, s = 197): the reference's attention / vjp_attention
+// (blocks.cpp:142-236; softmax_rows / vjp_softmax_rows, tensor.cpp:310-342)
+// streamed over 128-key blocks.
+//
+// The probabilities are never stored: the forward keeps two per-row
+// statistics (the row max m of the scaled, masked scores and 1/l with l the
+// row sum of exp(s - m)) in the P slot of the activation arena, and the
+// backward recomputes P = exp(s - m) / l bit-identically from Q, K and those
+// statistics (same MMAs, same order, same expf).
+//
+//   forward  (CTA per member, batch, head, 128-query block)
+//     pass A: per key block S = Q K^T (3-pass split MMA) -> online (m, l)
+//     pass B: per key block S again -> P = exp(S*scale - m) / l -> O += P V
+//   backward, two deterministic kernels (no atomics, no split-K reductions):
+//     dK/dV  (CTA per 128-key block): loops over the query blocks that see it,
+//            dV += P^T dO, dK += dS^T Q accumulated in TMEM
+//     dQ     (CTA per 128-query block): loops over key blocks, dQ += dS K
+//   with dS = P (dP - t), dP = dO V^T and t_i = sum_j dP_ij P_ij = dO_i . O_i
+//   (O = P V), so no pass over whole rows of dP is needed.
+// Causal problems skip the key blocks above the diagonal entirely.
+#include "attn_common.cuh"
+
+namespace mglp {
+
+using namespace tc;
+using namespace attn;
+
+namespace {
+
+constexpr int kThreads = 256;  // warp w: TMEM lanes 32 (w & 3), key-column half w >> 2
+constexpr int STG = 128 * 64 * 4;  // fp32 staging of one [128][64] block
+
+struct LongSmem {
+  uint32_t stg, t0, t1, t2, t3, t4;  // staging + five tiles (t4 is a 64 KB pair128)
+  uint64_t* bars;                    // [0] TMA, [1] MMA
+  float* xch;                        // [2][128] row-statistic exchange
+  uint32_t* tslot;
+};
+
+__device__ __forceinline__ LongSmem carve(uint8_t* smem_raw) {
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  LongSmem L;
+  const uint32_t base = smem_u32(smem);
+  L.stg = base;
+  L.t0 = base + STG;
+  L.t1 = L.t0 + PAIR64;
+  L.t2 = L.t1 + PAIR64;
+  L.t3 = L.t2 + PAIR64;
+  L.t4 = L.t3 + PAIR64;
+  L.bars = reinterpret_cast<uint64_t*>(smem + STG + 4 * PAIR64 + PAIR128);
+  L.xch = reinterpret_cast<float*>(L.bars + 4);
+  L.tslot = reinterpret_cast<uint32_t*>(L.xch + 256);
+  return L;
+}
+constexpr int kLongSmem = 1024 + STG + 4 * PAIR64 + PAIR128 + 32 + 256 * 4 + 16;
+
+__device__ __forceinline__ Opnd pair64(uint32_t t, bool mn) { return Opnd{t, t + TILE64, 128, mn}; }
+__device__ __forceinline__ Opnd pair128(uint32_t t, bool mn) {
+  return Opnd{t, t + 2 * TILE64, 128, mn};
+}
+
+// one thread issues a [128][dh] box (rows row0.. of operand `which`) into the staging
+__device__ __forceinline__ void issue(const LongSmem& L, const AttnTma& tm, int which, int g, int b,
+                                      int h, int row0, int dh) {
+  mbar_expect_tx(&L.bars[0], (uint32_t)(128 * dh * 4));
+  tma_box(L.stg, tm, which, g, b, h, &L.bars[0], row0);
+}
+
+struct Phase {
+  uint32_t st = 0, mm = 0;
+};
+__device__ __forceinline__ void wait_stage(const LongSmem& L, Phase& ph) {
+  mbar_wait(&L.bars[0], ph.st);
+  ph.st ^= 1;
+}
+__device__ __forceinline__ void mma_done(const LongSmem& L, Phase& ph) {
+  mbar_wait(&L.bars[1], ph.mm);
+  ph.mm ^= 1;
+  tc_after();
+}
+__device__ __forceinline__ void sync_all() {
+  tc_before();
+  __syncthreads();
+  tc_after();
+}
+
+// 64 combined score columns [c0, c0 + 64) of this thread's row
+__device__ __forceinline__ void read64(uint32_t trow, int c0, float* v) {
+#pragma unroll
+  for (int c = 0; c < 64; c += 16) tmem_pair16(trow + c0 + c, trow + 128 + c0 + c, v + c);
+}
+
+// P = exp(S * scale - m) * inv for keys (kb*128 + c0 + e), masked -> 0
+__device__ __forceinline__ void probs(float* v, int q, int key0, int skv, bool causal, bool live,
+                                      float scale, float m, float inv) {
+#pragma unroll
+  for (int e = 0; e < 64; ++e) {
+    const int j = key0 + e;
+    const bool ok = live && j < skv && !(causal && j > q);
+    v[e] = ok ? expf(v[e] * scale - m) * inv : 0.f;
+  }
+}
+
+// ---- forward -----------------------------------------------------------------------
+// tiles: t0 = Q, t1 = K, t2 = V, t4 = P (pair128); TMEM: S [0,256), O [256,..)/[384,..)
+__global__ void __launch_bounds__(kThreads, 1)
+    attn_fwd_long_kernel(const __grid_constant__ AttnTma tm, const AttnArgs a, const int* active) {
+  extern __shared__ uint8_t smem_raw[];
+  if (active && *(volatile const int*)active == 0) return;
+  const LongSmem L = carve(smem_raw);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int q4 = warp & 3, half = warp >> 2, c0 = half * 64;
+  const int sq = a.sq, skv = a.skv, dh = a.dh;
+  const int nqb = (sq + 127) >> 7, nkb = (skv + 127) >> 7;
+  const int nprob = a.G * a.Bb * a.H * nqb;
+  const Opnd Qk = pair64(L.t0, false), Kk = pair64(L.t1, false), Vm = pair64(L.t2, true);
+  const Opnd Pk = pair128(L.t4, false);
+  if (tid == 0) {
+    mbar_init(&L.bars[0], 1);
+    mbar_init(&L.bars[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) tmem_alloc(L.tslot, 512);
+  sync_all();
+  const uint32_t tmem = *L.tslot;
+  const uint32_t trow = tmem + ((uint32_t)(q4 * 32) << 16);
+  const int i = q4 * 32 + lane;
+  float amax = 0.f;
+  Phase ph;
+  auto coords = [&](int z, int& g, int& b, int& h, int& qb) {
+    qb = z % nqb;
+    int r = z / nqb;
+    h = r % a.H;
+    r /= a.H;
+    b = r % a.Bb;
+    g = r / a.Bb;
+  };
+  if (tid == 0 && (int)blockIdx.x < nprob) {
+    int g, b, h, qb;
+    coords(blockIdx.x, g, b, h, qb);
+    issue(L, tm, TQ, g, b, h, qb * 128, dh);
+  }
+  for (int z = blockIdx.x; z < nprob; z += gridDim.x) {
+    int g, b, h, qb;
+    coords(z, g, b, h, qb);
+    const int q = qb * 128 + i;  // this thread's query
+    const int kend = a.causal ? min(nkb, qb + 1) : nkb;
+    wait_stage(L, ph);
+    conv_rows(L.stg, 128, 128, dh, Qk.hi, Qk.lo, tid, kThreads, amax);
+    fence_async_smem();
+    sync_all();
+    if (tid == 0) issue(L, tm, TK, g, b, h, 0, dh);
+    // ---- pass A: row statistics (online max / sum of exp) ----
+    float m = -INFINITY, l = 0.f;
+    for (int kb = 0; kb < kend; ++kb) {
+      wait_stage(L, ph);
+      conv_rows(L.stg, 128, 128, dh, Kk.hi, Kk.lo, tid, kThreads, amax);
+      fence_async_smem();
+      sync_all();
+      if (tid == 0) {
+        // next K block, or K_0 again for pass B
+        issue(L, tm, TK, g, b, h, (kb + 1 < kend ? kb + 1 : 0) * 128, dh);
+        mma3(tmem, tmem + 128, Qk, Kk, 128, dh >> 4);
+        mma_commit<1>(&L.bars[1]);
+      }
+      mma_done(L, ph);
+      float v[64];
+      read64(trow, c0, v);
+      const int key0 = kb * 128 + c0;
+      float mh = -INFINITY;
+#pragma unroll
+      for (int e = 0; e < 64; ++e) {
+        const int j = key0 + e;
+        const bool ok = j < skv && !(a.causal && j > q);
+        v[e] = ok ? v[e] * a.scale : -INFINITY;
+        mh = fmaxf(mh, v[e]);
+      }
+      L.xch[half * 128 + i] = mh;
+      sync_all();
+      const float mb = fmaxf(L.xch[i], L.xch[128 + i]);
+      const float mn = fmaxf(m, mb);
+      float sh = 0.f;
+      if (mn != -INFINITY) {
+#pragma unroll
+        for (int e = 0; e < 64; ++e) sh += v[e] == -INFINITY ? 0.f : expf(v[e] - mn);
+      }
+      sync_all();
+      L.xch[half * 128 + i] = sh;
+      sync_all();
+      if (mn != -INFINITY) {
+        const float sc = m == -INFINITY ? 0.f : expf(m - mn);
+        l = l * sc + (L.xch[i] + L.xch[128 + i]);
+        m = mn;
+      }
+      sync_all();  // S consumed, K tile free
+    }
+    const float inv = l > 0.f ? 1.f / l : 0.f;
+    // ---- pass B: P = exp(S*scale - m) / l, O += P V ----
+    for (int kb = 0; kb < kend; ++kb) {
+      wait_stage(L, ph);
+      conv_rows(L.stg, 128, 128, dh, Kk.hi, Kk.lo, tid, kThreads, amax);
+      fence_async_smem();
+      sync_all();
+      if (tid == 0) {
+        issue(L, tm, TV, g, b, h, kb * 128, dh);
+        mma3(tmem, tmem + 128, Qk, Kk, 128, dh >> 4);
+        mma_commit<1>(&L.bars[1]);
+      }
+      wait_stage(L, ph);
+      conv_rows(L.stg, 128, 128, dh, Vm.hi, Vm.lo, tid, kThreads, amax);
+      fence_async_smem();
+      mma_done(L, ph);
+      float v[64];
+      read64(trow, c0, v);
+      probs(v, q, kb * 128 + c0, skv, a.causal != 0, q < sq, a.scale, m, inv);
+#pragma unroll
+      for (int c = 0; c < 8; ++c) put8(Pk.hi, Pk.lo, 128, i, half * 8 + c, v + c * 8, amax);
+      fence_async_smem();
+      sync_all();
+      if (tid == 0) {
+        if (kb + 1 < kend)
+          issue(L, tm, TK, g, b, h, (kb + 1) * 128, dh);
+        else if (z + (int)gridDim.x < nprob) {
+          int g2, b2, h2, qb2;
+          coords(z + gridDim.x, g2, b2, h2, qb2);
+          issue(L, tm, TQ, g2, b2, h2, qb2 * 128, dh);
+        }
+        mma3(tmem + 256, tmem + 384, Pk, Vm, dh, 8, kb > 0);
+        mma_commit<1>(&L.bars[1]);
+      }
+      mma_done(L, ph);
+    }
+    rows_out(trow + 256, trow + 384, a.O.at(g, b, h) + (long long)qb * 128 * a.O.ld, a.O.ld, i,
+             sq - qb * 128, half * (dh >> 1), dh >> 1, 1.f);
+    if (half == 0 && q < sq) {
+      float* st = a.P.at(g, b, h) + 2LL * q;
+      st[0] = m;
+      st[1] = inv;
+    }
+    sync_all();
+  }
+  if (amax >= 65520.f && amax <= FLT_MAX && a.range_flag) atomicOr(a.range_flag, 1);
+  sync_all();
+  if (warp == 0) tmem_free(tmem, 512);
+}
+
+// t_i = dO_i . O_i (the softmax-VJP row constant), fixed order
+__device__ __forceinline__ float row_dot(const float* x, const float* y, int n) {
+  float t = 0.f;
+  for (int e = 0; e < n; e += 4) {
+    const float4 u = *reinterpret_cast<const float4*>(x + e);
+    const float4 w = *reinterpret_cast<const float4*>(y + e);
+    t += u.x * w.x;
+    t += u.y * w.y;
+    t += u.z * w.z;
+    t += u.w * w.w;
+  }
+  return t;
+}
+
+// ---- backward: dK, dV per 128-key block ------------------------------------------
+// tiles: t0 = K, t1 = V, t2 = Q, t3 = dO, t4 = P then dS;
+// TMEM: S / dP [0,256), dV [256,..)/[320,..), dK [384,..)/[448,..)
+__global__ void __launch_bounds__(kThreads, 1)
+    attn_bwd_dkdv_kernel(const __grid_constant__ AttnTma tm, const AttnArgs a, const int* active) {
+  extern __shared__ uint8_t smem_raw[];
+  if (active && *(volatile const int*)active == 0) return;
+  const LongSmem L = carve(smem_raw);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int q4 = warp & 3, half = warp >> 2, c0 = half * 64;
+  const int sq = a.sq, skv = a.skv, dh = a.dh;
+  const int nqb = (sq + 127) >> 7, nkb = (skv + 127) >> 7;
+  const int nprob = a.G * a.Bb * a.H * nkb;
+  const Opnd Kk = pair64(L.t0, false), Vk = pair64(L.t1, false);
+  const Opnd Qm = pair64(L.t2, true), dOk = pair64(L.t3, false), dOm = pair64(L.t3, true);
+  const Opnd Pm = pair128(L.t4, true);
+  if (tid == 0) {
+    mbar_init(&L.bars[0], 1);
+    mbar_init(&L.bars[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) tmem_alloc(L.tslot, 512);
+  sync_all();
+  const uint32_t tmem = *L.tslot;
+  const uint32_t trow = tmem + ((uint32_t)(q4 * 32) << 16);
+  const int i = q4 * 32 + lane;
+  float amax = 0.f;
+  Phase ph;
+  for (int z = blockIdx.x; z < nprob; z += gridDim.x) {
+    const int kb = z % nkb;
+    int r = z / nkb;
+    const int h = r % a.H;
+    r /= a.H;
+    const int b = r % a.Bb, g = r / a.Bb;
+    const int qb0 = a.causal ? kb : 0;
+    const float* stats = a.P.at(g, b, h);
+    if (tid == 0) issue(L, tm, TK, g, b, h, kb * 128, dh);
+    wait_stage(L, ph);
+    conv_rows(L.stg, 128, 128, dh, Kk.hi, Kk.lo, tid, kThreads, amax);
+    fence_async_smem();
+    sync_all();
+    if (tid == 0) issue(L, tm, TV, g, b, h, kb * 128, dh);
+    wait_stage(L, ph);
+    conv_rows(L.stg, 128, 128, dh, Vk.hi, Vk.lo, tid, kThreads, amax);
+    fence_async_smem();
+    sync_all();
+    if (tid == 0) issue(L, tm, TQ, g, b, h, qb0 * 128, dh);
+    for (int qb = qb0; qb < nqb; ++qb) {
+      const bool first = qb == qb0;
+      const int q = qb * 128 + i;
+      const bool live = q < sq;
+      wait_stage(L, ph);
+      conv_rows(L.stg, 128, 128, dh, Qm.hi, Qm.lo, tid, kThreads, amax);
+      fence_async_smem();
+      sync_all();
+      if (tid == 0) {
+        issue(L, tm, TDO, g, b, h, qb * 128, dh);
+        mma3(tmem, tmem + 128, Opnd{Qm.hi, Qm.lo, 128, false}, Kk, 128, dh >> 4);  // S = Q K^T
+        mma_commit<1>(&L.bars[1]);
+      }
+      const float mi = live ? stats[2LL * q] : 0.f;
+      const float inv = live ? stats[2LL * q + 1] : 0.f;
+      mma_done(L, ph);
+      float p[64];
+      read64(trow, c0, p);
+      probs(p, q, kb * 128 + c0, skv, a.causal != 0, live, a.scale, mi, inv);
+#pragma unroll
+      for (int c = 0; c < 8; ++c) put8(Pm.hi, Pm.lo, 128, i, half * 8 + c, p + c * 8, amax);
+      wait_stage(L, ph);
+      conv_rows(L.stg, 128, 128, dh, dOk.hi, dOk.lo, tid, kThreads, amax);
+      fence_async_smem();
+      sync_all();
+      if (tid == 0) {
+        if (qb + 1 < nqb) issue(L, tm, TQ, g, b, h, (qb + 1) * 128, dh);
+        mma3(tmem + 256, tmem + 320, Pm, dOm, dh, 8, !first);  // dV += P^T dO
+        mma3(tmem, tmem + 128, dOk, Vk, 128, dh >> 4);         // dP = dO V^T
+        mma_commit<1>(&L.bars[1]);
+      }
+      const float t = live ? row_dot(a.dO.at(g, b, h) + (long long)q * a.dO.ld,
+                                     a.O.at(g, b, h) + (long long)q * a.O.ld, dh)
+                           : 0.f;
+      mma_done(L, ph);
+      float dp[64];
+      read64(trow, c0, dp);
+#pragma unroll
+      for (int e = 0; e < 64; ++e) dp[e] = p[e] * (dp[e] - t);  // dS (0 where P is 0)
+#pragma unroll
+      for (int c = 0; c < 8; ++c) put8(Pm.hi, Pm.lo, 128, i, half * 8 + c, dp + c * 8, amax);
+      fence_async_smem();
+      sync_all();
+      if (tid == 0) {
+        mma3(tmem + 384, tmem + 448, Pm, Qm, dh, 8, !first);  // dK += dS^T Q
+        mma_commit<1>(&L.bars[1]);
+      }
+      mma_done(L, ph);
+    }
+    const int nv = skv - kb * 128;
+    rows_out(trow + 256, trow + 320, a.dV.at(g, b, h) + (long long)kb * 128 * a.dV.ld, a.dV.ld, i,
+             nv, half * (dh >> 1), dh >> 1, 1.f);
+    rows_out(trow + 384, trow + 448, a.dK.at(g, b, h) + (long long)kb * 128 * a.dK.ld, a.dK.ld, i,
+             nv, half * (dh >> 1), dh >> 1, a.scale);
+    sync_all();
+  }
+  if (amax >= 65520.f && amax <= FLT_MAX && a.range_flag) atomicOr(a.range_flag, 1);
+  sync_all();
+  if (warp == 0) tmem_free(tmem, 512);
+}
+
+// ---- backward: dQ per 128-query block ---------------------------------------------
+// tiles: t0 = Q, t1 = dO, t2 = K, t3 = V, t4 = dS; TMEM: S / dP [0,256), dQ [256,..)/[384,..)
+__global__ void __launch_bounds__(kThreads, 1)
+    attn_bwd_dq_kernel(const __grid_constant__ AttnTma tm, const AttnArgs a, const int* active) {
+  extern __shared__ uint8_t smem_raw[];
+  if (active && *(volatile const int*)active == 0) return;
+  const LongSmem L = carve(smem_raw);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int q4 = warp & 3, half = warp >> 2, c0 = half * 64;
+  const int sq = a.sq, skv = a.skv, dh = a.dh;
+  const int nqb = (sq + 127) >> 7, nkb = (skv + 127) >> 7;
+  const int nprob = a.G * a.Bb * a.H * nqb;
+  const Opnd Qk = pair64(L.t0, false), dOk = pair64(L.t1, false);
+  const Opnd Kk = pair64(L.t2, false), Km = pair64(L.t2, true), Vk = pair64(L.t3, false);
+  const Opnd dSk = pair128(L.t4, false);
+  if (tid == 0) {
+    mbar_init(&L.bars[0], 1);
+    mbar_init(&L.bars[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) tmem_alloc(L.tslot, 512);
+  sync_all();
+  const uint32_t tmem = *L.tslot;
+  const uint32_t trow = tmem + ((uint32_t)(q4 * 32) << 16);
+  const int i = q4 * 32 + lane;
+  float amax = 0.f;
+  Phase ph;
+  for (int z = blockIdx.x; z < nprob; z += gridDim.x) {
+    const int qb = z % nqb;
+    int r = z / nqb;
+    const int h = r % a.H;
+    r /= a.H;
+    const int b = r % a.Bb, g = r / a.Bb;
+    const int q = qb * 128 + i;
+    const bool live = q < sq;
+    const int kend = a.causal ? min(nkb, qb + 1) : nkb;
+    const float* stats = a.P.at(g, b, h);
+    if (tid == 0) issue(L, tm, TQ, g, b, h, qb * 128, dh);
+    wait_stage(L, ph);
+    conv_rows(L.stg, 128, 128, dh, Qk.hi, Qk.lo, tid, kThreads, amax);
+    fence_async_smem();
+    sync_all();
+    if (tid == 0) issue(L, tm, TDO, g, b, h, qb * 128, dh);
+    wait_stage(L, ph);
+    conv_rows(L.stg, 128, 128, dh, dOk.hi, dOk.lo, tid, kThreads, amax);
+    fence_async_smem();
+    sync_all();
+    if (tid == 0) issue(L, tm, TK, g, b, h, 0, dh);
+    const float mi = live ? stats[2LL * q] : 0.f;
+    const float inv = live ? stats[2LL * q + 1] : 0.f;
+    const float t = live ? row_dot(a.dO.at(g, b, h) + (long long)q * a.dO.ld,
+                                   a.O.at(g, b, h) + (long long)q * a.O.ld, dh)
+                         : 0.f;
+    for (int kb = 0; kb < kend; ++kb) {
+      wait_stage(L, ph);
+      conv_rows(L.stg, 128, 128, dh, Kk.hi, Kk.lo, tid, kThreads, amax);
+      fence_async_smem();
+      sync_all();
+      if (tid == 0) {
+        issue(L, tm, TV, g, b, h, kb * 128, dh);
+        mma3(tmem, tmem + 128, Qk, Kk, 128, dh >> 4);  // S = Q K^T
+        mma_commit<1>(&L.bars[1]);
+      }
+      mma_done(L, ph);
+      float p[64];
+      read64(trow, c0, p);
+      probs(p, q, kb * 128 + c0, skv, a.causal != 0, live, a.scale, mi, inv);
+      wait_stage(L, ph);
+      conv_rows(L.stg, 128, 128, dh, Vk.hi, Vk.lo, tid, kThreads, amax);
+      fence_async_smem();
+      sync_all();
+      if (tid == 0) {
+        if (kb + 1 < kend) issue(L, tm, TK, g, b, h, (kb + 1) * 128, dh);
+        mma3(tmem, tmem + 128, dOk, Vk, 128, dh >> 4);  // dP = dO V^T
+        mma_commit<1>(&L.bars[1]);
+      }
+      mma_done(L, ph);
+      float dp[64];
+      read64(trow, c0, dp);
+#pragma unroll
+      for (int e = 0; e < 64; ++e) dp[e] = p[e] * (dp[e] - t);
+#pragma unroll
+      for (int c = 0; c < 8; ++c) put8(dSk.hi, dSk.lo, 128, i, half * 8 + c, dp + c * 8, amax);
+      fence_async_smem();
+      sync_all();
+      if (tid == 0) {
+        mma3(tmem + 256, tmem + 384, dSk, Km, dh, 8, kb > 0);  // dQ += dS K
+        mma_commit<1>(&L.bars[1]);
+      }
+      mma_done(L, ph);
+    }
+    rows_out(trow + 256, trow + 384, a.dQ.at(g, b, h) + (long long)qb * 128 * a.dQ.ld, a.dQ.ld, i,
+             sq - qb * 128, half * (dh >> 1), dh >> 1, a.scale);
+    sync_all();
+  }
+  if (amax >= 65520.f && amax <= FLT_MAX && a.range_flag) atomicOr(a.range_flag, 1);
+  sync_all();
+  if (warp == 0) tmem_free(tmem, 512);
+}
+
+bool aligned(const Mat& m) {
+  return !m.ok() || ((reinterpret_cast<uintptr_t>(m.ptr) & 15) == 0 && m.ld % 4 == 0 &&
+                     m.slot_stride % 4 == 0 && m.bstride % 4 == 0 && m.hstride % 4 == 0);
+}
+
+AttnTma long_maps(const AttnArgs& a, bool backward) {
+  AttnTma t{};
+  auto mk = [&](int which, const Mat& m, int rows) {
+    t.m[which] = tc_make_map(m, a.G, a.Bb, a.H, rows, a.dh, 128, a.dh, false, &t.op[which]);
+  };
+  mk(TQ, a.Q, a.sq);
+  mk(TK, a.K, a.skv);
+  mk(TV, a.V, a.skv);
+  if (backward) mk(TDO, a.dO, a.sq);
+  return t;
+}
+
+int sms() {
+  static int n = 0;
+  if (!n) MGLP_CUDA(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, 0));
+  return n;
+}
+
+template <typename K>
+void launch_long(K kernel, const AttnTma& t, const AttnArgs& a, long long nprob, const int* active,
+                 cudaStream_t s) {
+  if (nprob == 0) return;
+  const int grid = (int)std::min<long long>(nprob, sms());
+  kernel<<<grid, kThreads, kLongSmem, s>>>(t, a, active);
+  MGLP_CUDA(cudaGetLastError());
+}
+
+}  // namespace
+
+bool attn_long_supported(const AttnArgs& a, bool backward) {
+  if (a.sq < 128 || a.skv < 128 || a.sq > 512 || a.skv > 512) return false;
+  if (a.dh != 32 && a.dh != 64) return false;
+  if (!a.P.ok() || !aligned(a.Q) || !aligned(a.K) || !aligned(a.V) || !aligned(a.O) ||
+      !aligned(a.P))
+    return false;
+  if (backward && (!aligned(a.dO) || !aligned(a.dQ) || !aligned(a.dK) || !aligned(a.dV)))
+    return false;
+  return true;
+}
+
+void launch_attn_fwd_long(const AttnArgs& a, const int* active, cudaStream_t s) {
+  if (!attn_long_supported(a, false)) throw ContractViolation("attn_fwd_long: unsupported shape");
+  static bool attr = [] {
+    MGLP_CUDA(cudaFuncSetAttribute(attn_fwd_long_kernel,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, kLongSmem));
+    return true;
+  }();
+  (void)attr;
+  launch_long(attn_fwd_long_kernel, long_maps(a, false), a,
+              (long long)a.G * a.Bb * a.H * ((a.sq + 127) / 128), active, s);
+}
+
+void launch_attn_bwd_long(const AttnArgs& a, const int* active, cudaStream_t s) {
+  if (!attn_long_supported(a, true)) throw ContractViolation("attn_bwd_long: unsupported shape");
+  static bool attr = [] {
+    MGLP_CUDA(cudaFuncSetAttribute(attn_bwd_dkdv_kernel,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, kLongSmem));
+    MGLP_CUDA(cudaFuncSetAttribute(attn_bwd_dq_kernel,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, kLongSmem));
+    return true;
+  }();
+  (void)attr;
+  const AttnTma t = long_maps(a, true);
+  const long long heads = (long long)a.G * a.Bb * a.H;
+  launch_long(attn_bwd_dkdv_kernel, t, a, heads * ((a.skv + 127) / 128), active, s);
+  launch_long(attn_bwd_dq_kernel, t, a, heads * ((a.sq + 127) / 128), active, s);
+}
+
+}  // namespace mglp

@@ -30,187 +30,26 @@
 // dS (dQ: A, K; dK: A, MN).
 #include <cfloat>
 
-#include "kernels.cuh"
-#include "tc_common.cuh"
+#include "attn_common.cuh"
 
 namespace mglp {
 
 using namespace tc;
+using namespace attn;
 
 namespace {
 
 constexpr int kThreads = 256;  // 8 warps; warp w owns TMEM lanes 32 (w & 3), column half w >> 2
 
-__device__ __forceinline__ int rup(int x, int m) { return (x + m - 1) / m * m; }
-
-// SWIZZLE_128B UMMA descriptor; lbo only matters for MN-major operands with
-// more than one 64-wide MN block
-__device__ __forceinline__ uint64_t desc_sw128(uint32_t addr, uint32_t lbo) {
-  uint64_t d = 0;
-  d |= (uint64_t)((addr >> 4) & 0x3FFFu);
-  d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
-  d |= (uint64_t)(1024 >> 4) << 32;
-  d |= 1ull << 46;
-  d |= 2ull << 61;
-  return d;
-}
-
-// kind::f16 instruction descriptor: f32 accumulate, f16 A/B, major bits
-__device__ __forceinline__ uint32_t idesc(int N, bool a_mn, bool b_mn) {
-  return (1u << 4) | (a_mn ? 1u << 15 : 0u) | (b_mn ? 1u << 16 : 0u) |
-         ((uint32_t)(N >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
-}
-
-// One operand of an MMA: a hi/lo tile pair with `rows` rows, used K-major
-// (K = tile columns) or MN-major (K = tile rows).
-struct Opnd {
-  uint32_t hi, lo;
-  int rows;
-  bool mn;
-  __device__ __forceinline__ uint32_t at(int k16) const {
-    return mn ? (uint32_t)(k16 * 2048) : (uint32_t)((k16 >> 2) * rows * 128 + (k16 & 3) * 32);
-  }
-  __device__ __forceinline__ uint32_t lbo() const { return mn ? (uint32_t)(rows * 128) : 16u; }
-};
-
-// D = A . B^T over nk16 K steps with the 3-pass split: main (tm) and
-// correction (tcor) accumulators (M = 128)
-__device__ __forceinline__ void mma3(uint32_t tm, uint32_t tcor, const Opnd& A, const Opnd& B,
-                                     int N, int nk16) {
-  const uint32_t id = idesc(N, A.mn, B.mn);
-  for (int k = 0; k < nk16; ++k) {
-    const uint32_t oa = A.at(k), ob = B.at(k);
-    const uint64_t dah = desc_sw128(A.hi + oa, A.lbo()), dal = desc_sw128(A.lo + oa, A.lbo());
-    const uint64_t dbh = desc_sw128(B.hi + ob, B.lbo()), dbl = desc_sw128(B.lo + ob, B.lbo());
-    const uint32_t acc = k > 0 ? 1u : 0u;
-    mma_f16<1>(tm, dah, dbh, id, acc);
-    mma_f16<1>(tcor, dal, dbh, id, acc);
-    mma_f16<1>(tcor, dah, dbl, id, 1u);
-  }
-}
-
-// byte offset of 16-byte chunk c (8 fp16 columns) of row r in a tile with R rows
-__device__ __forceinline__ uint32_t chunk_off(int R, int r, int c) {
-  return (uint32_t)((c >> 3) * R * 128 + r * 128 + (((c & 7) ^ (r & 7)) << 4));
-}
-
-// fp32 staging rows [0, nvalid) x ncols (pitch ncols) -> hi/lo tiles of R
-// rows (rows >= nvalid become 0). ncols multiple of 8.
-__device__ __forceinline__ void conv_rows(uint32_t stg, int nvalid, int R, int ncols, uint32_t thi,
-                                          uint32_t tlo, int tid, int nthr, float& amax) {
-  const int cpr = ncols >> 3;
-  for (int i = tid; i < R * cpr; i += nthr) {
-    const int r = i / cpr, c = i - r * cpr;
-    float x[8];
-    if (r < nvalid) {
-      const uint32_t s = stg + (uint32_t)((r * ncols + c * 8) * 4);
-      const float4 u = lds128(s), w = lds128(s + 16);
-      x[0] = u.x; x[1] = u.y; x[2] = u.z; x[3] = u.w;
-      x[4] = w.x; x[5] = w.y; x[6] = w.z; x[7] = w.w;
-    } else {
-#pragma unroll
-      for (int e = 0; e < 8; ++e) x[e] = 0.f;
-    }
-    uint4 hi, lo;
-    split8(x, hi, lo, amax);
-    const uint32_t off = chunk_off(R, r, c);
-    sts128(thi + off, hi);
-    sts128(tlo + off, lo);
-  }
-}
-
-// 8 values of row r (chunk c) into a hi/lo tile pair
-__device__ __forceinline__ void put8(uint32_t thi, uint32_t tlo, int R, int r, int c,
-                                     const float* x, float& amax) {
-  uint4 hi, lo;
-  split8(x, hi, lo, amax);
-  const uint32_t off = chunk_off(R, r, c);
-  sts128(thi + off, hi);
-  sts128(tlo + off, lo);
-}
-
-__device__ __forceinline__ void fence_async_smem() {
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-}
-__device__ __forceinline__ void tc_before() {
-  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-}
-__device__ __forceinline__ void tc_after() {
-  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-}
-
-// 16 columns of main + correction -> combined fp32 (one TMEM wait)
-__device__ __forceinline__ void tmem_pair16(uint32_t tmain, uint32_t tcor, float* out) {
-  uint32_t rm[16], rc[16];
-  tmem_ld16(tmain, rm);
-  tmem_ld16(tcor, rc);
-  tmem_wait();
-#pragma unroll
-  for (int e = 0; e < 16; ++e) out[e] = fmaf(__uint_as_float(rc[e]), kLoInv, __uint_as_float(rm[e]));
-}
-
-// this warp's TMEM lanes -> global rows (row < nvalid), columns [c0, c0 + nc)
-// (nc multiple of 16, <= 32), scaled by alpha
-__device__ __forceinline__ void rows_out(uint32_t tmain, uint32_t tcor, float* out, long long ld,
-                                         int row, int nvalid, int c0, int nc, float alpha) {
-#pragma unroll
-  for (int c = 0; c < 32; c += 16) {
-    if (c < nc) {
-      float v[16];
-      tmem_pair16(tmain + c0 + c, tcor + c0 + c, v);
-      if (row < nvalid) {
-        float* o = out + row * ld + c0 + c;
-#pragma unroll
-        for (int e = 0; e < 16; e += 4)
-          *reinterpret_cast<float4*>(o + e) =
-              make_float4(alpha * v[e], alpha * v[e + 1], alpha * v[e + 2], alpha * v[e + 3]);
-      }
-    }
-  }
-}
-
-__device__ __forceinline__ void problem_of(const AttnArgs& a, int z, int& g, int& b, int& h) {
-  h = z % a.H;
-  b = (z / a.H) % a.Bb;
-  g = z / (a.H * a.Bb);
-}
-
-__device__ __forceinline__ void tmem_alloc(uint32_t* slot, uint32_t cols) {
-  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                   smem_u32(slot)),
-               "r"(cols));
-  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-}
-__device__ __forceinline__ void tmem_free(uint32_t base, uint32_t cols) {
-  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(base), "r"(cols));
-}
-
-// tensor maps of the operand families (one [rows][cols] box per problem)
-struct AttnTma {
-  CUtensorMap m[5];
-  TcOperand op[5];
-};
-enum { TQ = 0, TK = 1, TV = 2, TP = 3, TDO = 4 };
-
-__device__ __forceinline__ void tma_box(uint32_t dst, const AttnTma& t, int which, int g, int b,
-                                        int h, uint64_t* bar) {
-  int c[5];
-  tma_coords(t.op[which], 0, 0, g, b, h, c);
-  asm volatile(
-      "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(dst),
-      "l"(reinterpret_cast<uint64_t>(&t.m[which])), "r"(smem_u32(bar)), "r"(c[0]), "r"(c[1]),
-      "r"(c[2]), "r"(c[3]), "r"(c[4])
-      : "memory");
-}
-
-constexpr int TILE64 = 128 * 128;       // one hi (or lo) tile: 128 rows x 64 fp16
-constexpr int PAIR64 = 2 * TILE64;      // hi + lo
-constexpr int PAIR128 = 2 * PAIR64;     // hi + lo, two 64-column blocks
-
 // ---- forward -------------------------------------------------------------------
-// smem: staging fp32 [Q | K | V] (3 x 32 KB) | tiles: [Q | K] (-> P) | V | barriers
-__global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_constant__ AttnTma tm, const AttnArgs a, const int* active) {
+// smem (96 KB, two CTAs per SM): [Q | K] (each TMA-staged fp32, converted in
+// place to its hi/lo tile pair; P's two 64-key blocks overlay both after S)
+// | V | barriers. The next problem's loads go out as soon as O = P V has
+// consumed the tiles, so they overlap this problem's epilogue and the other
+// CTA's work.
+constexpr int kFwdSmem = 1024 + PAIR128 + PAIR64 + 64 + 256 * 4 + 16;
+
+__global__ void __launch_bounds__(kThreads, 2) attn_fwd_kernel(const __grid_constant__ AttnTma tm, const AttnArgs a, const int* active) {
   extern __shared__ uint8_t smem_raw[];
   if (active && *(volatile const int*)active == 0) return;
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -220,13 +59,11 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
   const int sq = a.sq, skv = a.skv, dh = a.dh;
   const int skv16 = rup(skv, 16);
   const uint32_t base = smem_u32(smem);
-  const uint32_t stQ = base, stK = base + 128 * 64 * 4, stV = base + 2 * 128 * 64 * 4;
-  const uint32_t tiles = base + 3 * 128 * 64 * 4;
-  const Opnd Qt{tiles, tiles + TILE64, 128, false};
-  const Opnd Kt{tiles + PAIR64, tiles + PAIR64 + TILE64, 128, false};
-  const Opnd Pt{tiles, tiles + 2 * TILE64, 128, false};  // over [Q | K]: hi blocks 0-1, lo blocks 0-1
-  const Opnd Vt{tiles + PAIR128, tiles + PAIR128 + TILE64, 128, true};
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 3 * 128 * 64 * 4 + PAIR128 + PAIR64);
+  const Opnd Qt{base, base + TILE64, 128, false};
+  const Opnd Kt{base + PAIR64, base + PAIR64 + TILE64, 128, false};
+  const Opnd Pt{base, base + 2 * TILE64, 128, false};  // over [Q | K]: hi blocks 0-1, lo blocks 0-1
+  const Opnd Vt{base + PAIR128, base + PAIR128 + TILE64, 128, true};
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + PAIR128 + PAIR64);
   uint64_t* st_full = &bars[0];
   uint64_t* s_bar = &bars[1];
   uint64_t* o_bar = &bars[2];
@@ -234,16 +71,13 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
   uint32_t* tslot = reinterpret_cast<uint32_t*>(xch + 256);
   const int nprob = a.G * a.Bb * a.H;
 
-  auto issue_loads = [&](int z) {
+  auto issue_loads = [&](int z) {  // one thread
     int g, b, h;
     problem_of(a, z, g, b, h);
-    if (lane == 0) {
-      mbar_expect_tx(st_full, (uint32_t)((sq + 2 * skv) * dh * 4));
-      tma_box(stQ, tm, TQ, g, b, h, st_full);
-      tma_box(stK, tm, TK, g, b, h, st_full);
-      tma_box(stV, tm, TV, g, b, h, st_full);
-    }
-    __syncwarp();
+    mbar_expect_tx(st_full, (uint32_t)((sq + 2 * skv) * dh * 4));
+    tma_box(Qt.hi, tm, TQ, g, b, h, st_full);
+    tma_box(Kt.hi, tm, TK, g, b, h, st_full);
+    tma_box(Vt.hi, tm, TV, g, b, h, st_full);
   };
 
   if (tid == 0) {
@@ -260,7 +94,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
   const uint32_t trow = tmem + ((uint32_t)(q4 * 32) << 16);
   const int i = q4 * 32 + lane;  // query row = TMEM lane
   float amax = 0.f;
-  if (warp == 0 && (int)blockIdx.x < nprob) issue_loads(blockIdx.x);
+  if (tid == 0 && (int)blockIdx.x < nprob) issue_loads(blockIdx.x);
 
   int it = 0;
   for (int z = blockIdx.x; z < nprob; z += gridDim.x, ++it) {
@@ -268,14 +102,13 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
     problem_of(a, z, g, b, h);
     const uint32_t ph = it & 1;
     mbar_wait(st_full, ph);
-    conv_rows(stQ, sq, 128, dh, Qt.hi, Qt.lo, tid, kThreads, amax);
-    conv_rows(stK, skv, skv16, dh, Kt.hi, Kt.lo, tid, kThreads, amax);
-    conv_rows(stV, skv, skv16, dh, Vt.hi, Vt.lo, tid, kThreads, amax);
+    conv_inplace(Qt.hi, sq, 128, dh, tid, kThreads, amax);
+    conv_inplace(Kt.hi, skv, skv16, dh, tid, kThreads, amax);
+    conv_inplace(Vt.hi, skv, skv16, dh, tid, kThreads, amax);
     fence_async_smem();
     tc_before();
     __syncthreads();
     tc_after();
-    if (warp == 0 && z + (int)gridDim.x < nprob) issue_loads(z + gridDim.x);  // staging is free
     if (tid == 0) {
       mma3(tmem, tmem + 128, Qt, Kt, skv16, dh >> 4);  // S
       mma_commit<1>(s_bar);
@@ -298,11 +131,11 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
           for (int e = 0; e < 16; ++e) v[c + e] = 0.f;
         }
       }
+      // valid keys of this row: j < lim (causal: j <= i), one compare per key
+      const int lim = (a.causal ? min(skv, i + 1) : skv) - c0;
 #pragma unroll
       for (int e = 0; e < 64; ++e) {
-        const int j = c0 + e;
-        const bool ok = j < skv && !(a.causal && j > i);
-        v[e] = ok ? v[e] * a.scale : -INFINITY;
+        v[e] = e < lim ? v[e] * a.scale : -INFINITY;
         m = fmaxf(m, v[e]);
       }
     }
@@ -314,7 +147,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
     if (any) {
 #pragma unroll
       for (int e = 0; e < 64; ++e) {
-        v[e] = v[e] == -INFINITY ? 0.f : expf(v[e] - m);
+        v[e] = v[e] == -INFINITY ? 0.f : fast_exp(v[e] - m);
         sum += v[e];
       }
     }
@@ -346,9 +179,11 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
     }
     mbar_wait(o_bar, ph);
     tc_after();
+    // the tiles are free: the next problem's loads overlap this epilogue
+    if (tid == 0 && z + (int)gridDim.x < nprob) issue_loads(z + gridDim.x);
     rows_out(trow, trow + 128, a.O.at(g, b, h), a.O.ld, i, sq, half * (dh >> 1), dh >> 1, 1.f);
     tc_before();
-    __syncthreads();  // TMEM and tiles free for the next problem
+    __syncthreads();  // TMEM free for the next problem
   }
   if (amax >= 65520.f && amax <= FLT_MAX && a.range_flag) atomicOr(a.range_flag, 1);
   tc_before();
@@ -545,7 +380,6 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
   if (warp == 0) tmem_free(tmem, 512);
 }
 
-constexpr int kFwdSmem = 1024 + 3 * 128 * 64 * 4 + PAIR128 + PAIR64 + 64 + 256 * 4 + 16;
 constexpr int kBwdSmem = 1024 + 2 * 128 * 64 * 4 + 2 * PAIR128 + 64 + 256 * 4 + 16;
 
 bool aligned(const Mat& m) {
@@ -597,7 +431,7 @@ void launch_attn_fwd(const AttnArgs& a, const int* active, cudaStream_t s) {
   (void)attr;
   const long long n = (long long)a.G * a.Bb * a.H;
   if (n == 0) return;
-  const int grid = (int)std::min<long long>(n, num_sms());
+  const int grid = (int)std::min<long long>(n, 2 * num_sms());
   AttnTma t = maps(a, false);
   attn_fwd_kernel<<<grid, kThreads, kFwdSmem, s>>>(t, a, active);
   MGLP_CUDA(cudaGetLastError());

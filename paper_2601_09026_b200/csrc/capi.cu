@@ -777,14 +777,24 @@ mglp_status mglp_test_attention(int B, int H, int sq, int skv, int dh, int causa
     need(O, "O");
     need(P, "P");
     AttnArgs a = attn_args(B, H, sq, skv, dh, causal, Q, K, V, ld, O, P, dO, dQ, dK, dV);
-    if (!attn_tc_supported(a, dO != nullptr))
-      throw ValidationError("fused attention: unsupported shape (sq, skv <= 128, multiples of 8; dh 32 or 64)");
+    const bool bwd = dO != nullptr;
+    const bool shortp = attn_tc_supported(a, bwd);
+    if (!shortp && !attn_long_supported(a, bwd))
+      throw ValidationError(
+          "fused attention: unsupported shape (sq, skv <= 128 and multiples of 8, or 128..512; dh 32 "
+          "or 64)");
     int* dflag = nullptr;
     MGLP_CUDA(cudaMalloc(&dflag, sizeof(int)));
     MGLP_CUDA(cudaMemset(dflag, 0, sizeof(int)));
     a.range_flag = dflag;
-    launch_attn_fwd(a, nullptr, 0);
-    if (dO) launch_attn_bwd(a, nullptr, 0);
+    if (shortp) {
+      launch_attn_fwd(a, nullptr, 0);
+      if (bwd) launch_attn_bwd(a, nullptr, 0);
+    } else {
+      // long form: P receives the per-row (max, 1/sum) statistics instead
+      launch_attn_fwd_long(a, nullptr, 0);
+      if (bwd) launch_attn_bwd_long(a, nullptr, 0);
+    }
     MGLP_CUDA(cudaDeviceSynchronize());
     int flag = 0;
     MGLP_CUDA(cudaMemcpy(&flag, dflag, sizeof(int), cudaMemcpyDeviceToHost));
@@ -818,15 +828,24 @@ mglp_status mglp_bench_attention(int G, int B, int H, int s, int dh, int causal,
     for (Mat* m : {&a.Q, &a.K, &a.V, &a.dQ, &a.dK, &a.dV}) m->slot_stride = (long long)B * s * ld;
     for (Mat* m : {&a.O, &a.dO}) m->slot_stride = (long long)B * s * d;
     a.P.slot_stride = (long long)B * H * s * ldp;
-    if (!attn_tc_supported(a, backward != 0)) throw ValidationError("bench_attention: unsupported shape");
+    const bool shortp = attn_tc_supported(a, backward != 0);
+    if (!shortp && !attn_long_supported(a, backward != 0))
+      throw ValidationError("bench_attention: unsupported shape");
     cudaEvent_t e0, e1;
     MGLP_CUDA(cudaEventCreate(&e0));
     MGLP_CUDA(cudaEventCreate(&e1));
     auto run = [&] {
-      if (backward)
-        launch_attn_bwd(a, nullptr, 0);
-      else
-        launch_attn_fwd(a, nullptr, 0);
+      if (shortp) {
+        if (backward)
+          launch_attn_bwd(a, nullptr, 0);
+        else
+          launch_attn_fwd(a, nullptr, 0);
+      } else {
+        if (backward)
+          launch_attn_bwd_long(a, nullptr, 0);
+        else
+          launch_attn_fwd_long(a, nullptr, 0);
+      }
     };
     run();
     run();

@@ -661,6 +661,22 @@ static bool use_fused_attn() {
 #endif
 }
 
+// The streamed long-sequence kernels (attn_long.cu, 128 < s <= 512) are
+// parity-green but not yet faster than tensor-core GEMMs + softmax row kernels
+// on B200 (every key block's loads are exposed: one CTA per SM, no overlap),
+// so they are opt-in: MGLP_LONG_ATTN=1.
+static bool use_long_attn() {
+#ifdef MGLP_GEMM_SIMT
+  return false;
+#else
+  static const bool on = [] {
+    const char* e = getenv("MGLP_LONG_ATTN");
+    return e && atoi(e) != 0;
+  }();
+  return on;
+#endif
+}
+
 void Engine::attention_fwd(int G, Mat Q, Mat K, Mat V, Mat O, Mat P, int sq, int skv,
                            bool causal, bool keep_p) {
   const int H = sd_.heads, dh = sd_.d / H;
@@ -693,13 +709,21 @@ void Engine::attention_fwd(int G, Mat Q, Mat K, Mat V, Mat O, Mat P, int sq, int
     at.O = O;
     at.P = P;
     at.range_flag = range_flag_;
+    const double fl = 4.0 * G * B_ * H * (double)sq * skv * dh * (causal ? 0.5 : 1.0);
     if (attn_tc_supported(at, false)) {
       // P is only an intermediate of the backward: not stored for scratch evaluations
       if (!keep_p) at.P = Mat{};
       ++launches_;
       prof_shape_ = {sq, skv, dh, G * B_ * H};
-      timed(PROF_ATTN, 4.0 * G * B_ * H * (double)sq * skv * dh, 0.0,
-            [&] { launch_attn_fwd(at, active_, stream_); });
+      timed(PROF_ATTN, fl, 0.0, [&] { launch_attn_fwd(at, active_, stream_); });
+      return;
+    }
+    if (use_long_attn() && attn_long_supported(at, false)) {
+      // longer sequences: P is recomputed by the backward from per-row
+      // statistics stored in the P slot (attn_long.cu)
+      ++launches_;
+      prof_shape_ = {sq, skv, dh, G * B_ * H};
+      timed(PROF_ATTN, fl, 0.0, [&] { launch_attn_fwd_long(at, active_, stream_); });
       return;
     }
   }
@@ -741,8 +765,8 @@ void Engine::attention_fwd(int G, Mat Q, Mat K, Mat V, Mat O, Mat P, int sq, int
   gemm(g);
 }
 
-void Engine::attention_bwd(int G, Mat Q, Mat K, Mat V, Mat P, Mat dO, Mat dP, Mat dQ, Mat dK,
-                           Mat dV, int sq, int skv) {
+void Engine::attention_bwd(int G, Mat Q, Mat K, Mat V, Mat P, Mat O, Mat dO, Mat dP, Mat dQ, Mat dK,
+                           Mat dV, int sq, int skv, bool causal) {
   const int H = sd_.heads, dh = sd_.d / H;
   const float scale = (float)(1.0 / std::sqrt((double)dh));
   auto heads = [&](Mat m, int s) {
@@ -776,16 +800,24 @@ void Engine::attention_bwd(int G, Mat Q, Mat K, Mat V, Mat P, Mat dO, Mat dP, Ma
     at.K = K;
     at.V = V;
     at.P = P;
+    at.O = O;
+    at.causal = causal ? 1 : 0;
     at.dO = dO;
     at.dQ = dQ;
     at.dK = dK;
     at.dV = dV;
     at.range_flag = range_flag_;
+    const double fl = 8.0 * G * B_ * H * (double)sq * skv * dh;
     if (attn_tc_supported(at, true)) {
       ++launches_;
       prof_shape_ = {-sq, skv, dh, G * B_ * H};
-      timed(PROF_ATTN, 8.0 * G * B_ * H * (double)sq * skv * dh, 0.0,
-            [&] { launch_attn_bwd(at, active_, stream_); });
+      timed(PROF_ATTN, fl, 0.0, [&] { launch_attn_bwd(at, active_, stream_); });
+      return;
+    }
+    if (use_long_attn() && attn_long_supported(at, true)) {
+      ++launches_;
+      prof_shape_ = {-sq, skv, dh, G * B_ * H};
+      timed(PROF_ATTN, fl, 0.0, [&] { launch_attn_bwd_long(at, active_, stream_); });
       return;
     }
   }
@@ -1293,8 +1325,8 @@ void Engine::encoder_adjoint(const EvalSpec& e, bool causal) {
     g.ep.out1 = dctx;
     gemm(g);
 
-    attention_bwd(G, qkv, qkv.offset(d), qkv.offset(2 * d), Pm, dctx, dPm, dqkv, dqkv.offset(d),
-                  dqkv.offset(2 * d), R / B_, R / B_);
+    attention_bwd(G, qkv, qkv.offset(d), qkv.offset(2 * d), Pm, ctx, dctx, dPm, dqkv,
+                  dqkv.offset(d), dqkv.offset(2 * d), R / B_, R / B_, causal);
 
     g = mk(R, d, 3 * d, dqkv, L.w_qkv, d);
     g.ep.kind = EPI_STORE;
@@ -1456,7 +1488,8 @@ void Engine::decoder_adjoint(const EvalSpec& e) {
     g.ep.out1 = dcctx;
     gemm(g);
 
-    attention_bwd(G, cq, ckv, ckv.offset(d), cP, dcctx, dP2, dcq, dckv, dckv.offset(d), sy_, sx_);
+    attention_bwd(G, cq, ckv, ckv.offset(d), cP, cctx, dcctx, dP2, dcq, dckv, dckv.offset(d), sy_,
+                  sx_, false);
 
     g = mk(R, d, d, dcq, L.w_cq, d);
     g.ep.kind = EPI_STORE;
@@ -1486,8 +1519,8 @@ void Engine::decoder_adjoint(const EvalSpec& e) {
     g.ep.out1 = dctx;
     gemm(g);
 
-    attention_bwd(G, qkv, qkv.offset(d), qkv.offset(2 * d), Pm, dctx, dPm, dqkv, dqkv.offset(d),
-                  dqkv.offset(2 * d), sy_, sy_);
+    attention_bwd(G, qkv, qkv.offset(d), qkv.offset(2 * d), Pm, ctx, dctx, dPm, dqkv,
+                  dqkv.offset(d), dqkv.offset(2 * d), sy_, sy_, true);
 
     g = mk(R, d, 3 * d, dqkv, L.w_qkv, d);
     g.ep.kind = EPI_STORE;

@@ -223,8 +223,8 @@ class Engine {
   // the activations of this evaluation are the linearization the adjoint
   // reads (cache), not per-evaluation scratch
   bool keep_lin(const EvalSpec& e) const { return e.act.base != scratch_ || e.keep_act; }
-  void attention_bwd(int G, Mat Q, Mat K, Mat V, Mat P, Mat dO, Mat dP, Mat dQ, Mat dK, Mat dV,
-                     int sq, int skv);
+  void attention_bwd(int G, Mat Q, Mat K, Mat V, Mat P, Mat O, Mat dO, Mat dP, Mat dQ, Mat dK, Mat dV,
+                     int sq, int skv, bool causal);
   int gemm_blocks(const GemmArgs& g) const;
   Mat act_mat(const ActRef& r, long long off, int ld) const;
   Mat bwd_mat(const EvalSpec& e, long long off, int ld) const;

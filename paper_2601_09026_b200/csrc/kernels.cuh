@@ -124,5 +124,11 @@ struct AttnArgs {
 bool attn_tc_supported(const AttnArgs& a, bool backward);
 void launch_attn_fwd(const AttnArgs& a, const int* active, cudaStream_t s);
 void launch_attn_bwd(const AttnArgs& a, const int* active, cudaStream_t s);
+// 128 <= sq, skv <= 512 (attn_long.cu): P is not stored; the forward writes
+// per-row (max, 1/sum) statistics at P.at(g, b, h) ([sq][2]) and the backward
+// (which also needs O for the softmax-VJP row constant dO . O) recomputes P.
+bool attn_long_supported(const AttnArgs& a, bool backward);
+void launch_attn_fwd_long(const AttnArgs& a, const int* active, cudaStream_t s);
+void launch_attn_bwd_long(const AttnArgs& a, const int* active, cudaStream_t s);
 
 }  // namespace mglp

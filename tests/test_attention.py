@@ -82,15 +82,46 @@ SHAPES = [  # B, H, sq, skv, dh, causal
 ]
 
 
-@pytest.mark.parametrize("shape", SHAPES)
+LONG_SHAPES = [  # attn_long.cu: key/query blocks of 128, P recomputed in the backward
+    (1, 2, 512, 512, 64, True),    # GPT-2-style causal decoder
+    (2, 2, 197, 197, 64, False),   # ViT-B/16 (197 tokens)
+    (1, 1, 256, 384, 64, False),   # cross-attention, sq != skv
+    (1, 2, 300, 300, 32, True),    # ragged blocks, dh 32
+]
+
+
+@pytest.mark.parametrize("shape", SHAPES + LONG_SHAPES)
 def test_fused_attention_matches_fp64(shape):
     B, H, sq, skv, dh, causal = shape
     got, ref = run(B, H, sq, skv, dh, causal)
     names = ["O", "P", "dQ", "dK", "dV"]
+    long_form = sq > 128 or skv > 128
     for n, a, b in zip(names, got, ref):
+        if long_form and n == "P":
+            continue  # the long form stores row statistics, not P
         assert not torch.isnan(a).any(), n
         e = relerr(a, b)
         assert e < 2e-5, (n, e)
+
+
+def test_long_form_row_statistics():
+    """P slot of the long form: per query row (max of the scaled masked
+    scores, 1 / sum exp(s - max)) -- what the backward recomputes P from"""
+    B, H, s, dh = 1, 1, 256, 64
+    got, _ = run(B, H, s, s, dh, True, seed=5)
+    g = torch.Generator().manual_seed(5)
+    d = H * dh
+    qkv_q = torch.randn(B, s, 3 * d, generator=g)
+    qkv_kv = torch.randn(B, s, 3 * d, generator=g)
+    q = qkv_q[0, :, :d].double()
+    k = qkv_kv[0, :, d:2 * d].double()
+    sc = (q @ k.T) / math.sqrt(dh)
+    sc = sc.masked_fill(torch.ones(s, s).triu(1).bool(), float("-inf"))
+    m = sc.max(-1).values
+    inv = 1.0 / torch.exp(sc - m[:, None]).sum(-1)
+    st = got[1].reshape(-1)[: 2 * s].reshape(s, 2).double()
+    assert float((st[:, 0] - m).abs().max()) < 1e-4
+    assert float(((st[:, 1] - inv) / inv).abs().max()) < 1e-4
 
 
 def test_causal_probabilities_are_exactly_zero_above_diagonal():
@@ -116,7 +147,7 @@ def test_range_flag_on_fp16_overflow():
 
 
 def test_unsupported_shape_is_a_validation_error():
-    x = torch.zeros(1, 200, 192, device="cuda")
+    x = torch.zeros(1, 600, 192, device="cuda")
     with pytest.raises(N.ValidationError):
-        N.call("mglp_test_attention", 1, 1, 200, 200, 64, 0, x.data_ptr(), x.data_ptr(),
+        N.call("mglp_test_attention", 1, 1, 600, 600, 64, 0, x.data_ptr(), x.data_ptr(),
                x.data_ptr(), 192, x.data_ptr(), x.data_ptr(), None, None, None, None, None)

@@ -13,6 +13,8 @@ SHAPES = [  # name, G, B, H, s, dh, causal
     ("bert x1", 1, 32, 12, 128, 64, 0),
     ("mt dec causal x16", 16, 32, 8, 128, 64, 1),
     ("tiny x4", 4, 8, 2, 32, 32, 0),
+    ("gpt causal x32", 32, 8, 12, 512, 64, 1),
+    ("vit x8", 8, 32, 12, 197, 64, 0),
 ]
 reps = int(sys.argv[1]) if len(sys.argv) > 1 else 10
 out = {}
@@ -20,7 +22,7 @@ for name, G, B, H, s, dh, causal in SHAPES:
     for bwd in (0, 1):
         ms = C.c_float()
         N.call("mglp_bench_attention", G, B, H, s, dh, causal, bwd, reps, C.byref(ms))
-        fl = (8.0 if bwd else 4.0) * G * B * H * s * s * dh
+        fl = (8.0 if bwd else 4.0) * G * B * H * s * s * dh * (0.5 if causal else 1.0)
         key = f"{name} {'bwd' if bwd else 'fwd'}"
         print(f"{key:24s} {ms.value:8.3f} ms  {fl / (ms.value * 1e-3) / 1e12:7.1f} TF/s", flush=True)
         out[key] = {"ms": ms.value, "tflops": fl / (ms.value * 1e-3) / 1e12}
