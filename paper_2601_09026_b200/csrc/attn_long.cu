@@ -7,7 +7,8 @@
 // statistics (the row max m of the scaled, masked scores and 1/l with l the
 // row sum of exp(s - m)) in the P slot of the activation arena, and the
 // backward recomputes P = exp(s - m) / l bit-identically from Q, K and those
-// statistics (same MMAs, same order, same expf).
+// statistics (same MMAs, same order, same exponential). The backward also
+// keeps t_i = dO_i . O_i there ([2 sq + i]).
 //
 //   forward  (CTA per member, batch, head, 128-query block)
 //     pass A: per key block S = Q K^T (3-pass split MMA) -> online (m, l)
@@ -92,15 +93,18 @@ __device__ __forceinline__ void read64(uint32_t trow, int c0, float* v) {
   for (int c = 0; c < 64; c += 16) tmem_pair16(trow + c0 + c, trow + 128 + c0 + c, v + c);
 }
 
+// number of valid keys of query q among keys [key0, key0 + 64): j < skv and,
+// causal, j <= q (one compare per key in the loops)
+__device__ __forceinline__ int key_limit(int q, int key0, int skv, bool causal, bool live) {
+  return live ? (causal ? min(skv, q + 1) : skv) - key0 : 0;
+}
+
 // P = exp(S * scale - m) * inv for keys (kb*128 + c0 + e), masked -> 0
 __device__ __forceinline__ void probs(float* v, int q, int key0, int skv, bool causal, bool live,
                                       float scale, float m, float inv) {
+  const int lim = key_limit(q, key0, skv, causal, live);
 #pragma unroll
-  for (int e = 0; e < 64; ++e) {
-    const int j = key0 + e;
-    const bool ok = live && j < skv && !(causal && j > q);
-    v[e] = ok ? expf(v[e] * scale - m) * inv : 0.f;
-  }
+  for (int e = 0; e < 64; ++e) v[e] = e < lim ? fast_exp(v[e] * scale - m) * inv : 0.f;
 }
 
 // ---- forward -----------------------------------------------------------------------
@@ -168,13 +172,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       mma_done(L, ph);
       float v[64];
       read64(trow, c0, v);
-      const int key0 = kb * 128 + c0;
+      const int lim = key_limit(q, kb * 128 + c0, skv, a.causal != 0, true);
       float mh = -INFINITY;
 #pragma unroll
       for (int e = 0; e < 64; ++e) {
-        const int j = key0 + e;
-        const bool ok = j < skv && !(a.causal && j > q);
-        v[e] = ok ? v[e] * a.scale : -INFINITY;
+        v[e] = e < lim ? v[e] * a.scale : -INFINITY;
         mh = fmaxf(mh, v[e]);
       }
       L.xch[half * 128 + i] = mh;
@@ -184,13 +186,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       float sh = 0.f;
       if (mn != -INFINITY) {
 #pragma unroll
-        for (int e = 0; e < 64; ++e) sh += v[e] == -INFINITY ? 0.f : expf(v[e] - mn);
+        for (int e = 0; e < 64; ++e) sh += v[e] == -INFINITY ? 0.f : fast_exp(v[e] - mn);
       }
       sync_all();
       L.xch[half * 128 + i] = sh;
       sync_all();
       if (mn != -INFINITY) {
-        const float sc = m == -INFINITY ? 0.f : expf(m - mn);
+        const float sc = m == -INFINITY ? 0.f : fast_exp(m - mn);
         l = l * sc + (L.xch[i] + L.xch[128 + i]);
         m = mn;
       }
@@ -338,9 +340,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         mma3(tmem, tmem + 128, dOk, Vk, 128, dh >> 4);         // dP = dO V^T
         mma_commit<1>(&L.bars[1]);
       }
-      const float t = live ? row_dot(a.dO.at(g, b, h) + (long long)q * a.dO.ld,
-                                     a.O.at(g, b, h) + (long long)q * a.O.ld, dh)
-                           : 0.f;
+      const float t = live ? stats[2LL * sq + q] : 0.f;  // dO . O, written by the dQ kernel
       mma_done(L, ph);
       float dp[64];
       read64(trow, c0, dp);
@@ -421,6 +421,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     const float t = live ? row_dot(a.dO.at(g, b, h) + (long long)q * a.dO.ld,
                                    a.O.at(g, b, h) + (long long)q * a.O.ld, dh)
                          : 0.f;
+    // published for the dK/dV kernel (launched after this one) next to the row statistics
+    if (live && half == 0) const_cast<float*>(stats)[2LL * sq + q] = t;
     for (int kb = 0; kb < kend; ++kb) {
       wait_stage(L, ph);
       conv_rows(L.stg, 128, 128, dh, Kk.hi, Kk.lo, tid, kThreads, amax);
@@ -537,8 +539,9 @@ void launch_attn_bwd_long(const AttnArgs& a, const int* active, cudaStream_t s) 
   (void)attr;
   const AttnTma t = long_maps(a, true);
   const long long heads = (long long)a.G * a.Bb * a.H;
-  launch_long(attn_bwd_dkdv_kernel, t, a, heads * ((a.skv + 127) / 128), active, s);
+  // dQ first: it also publishes t_i = dO_i . O_i (at P + 2 sq + i) for dK / dV
   launch_long(attn_bwd_dq_kernel, t, a, heads * ((a.sq + 127) / 128), active, s);
+  launch_long(attn_bwd_dkdv_kernel, t, a, heads * ((a.skv + 127) / 128), active, s);
 }
 
 }  // namespace mglp

@@ -661,17 +661,16 @@ static bool use_fused_attn() {
 #endif
 }
 
-// The streamed long-sequence kernels (attn_long.cu, 128 < s <= 512) are
-// parity-green but not yet faster than tensor-core GEMMs + softmax row kernels
-// on B200 (every key block's loads are exposed: one CTA per SM, no overlap),
-// so they are opt-in: MGLP_LONG_ATTN=1.
+// Sequences of 128 < s <= 512 use the streamed kernels (attn_long.cu);
+// MGLP_LONG_ATTN=0 falls back to tensor-core GEMMs + softmax row kernels
+// (S and P round-trip through HBM).
 static bool use_long_attn() {
 #ifdef MGLP_GEMM_SIMT
   return false;
 #else
   static const bool on = [] {
     const char* e = getenv("MGLP_LONG_ATTN");
-    return e && atoi(e) != 0;
+    return !(e && atoi(e) == 0);
   }();
   return on;
 #endif
