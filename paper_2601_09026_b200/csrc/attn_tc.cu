@@ -301,6 +301,18 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
       const bool any = c0 < skv16;
       const bool live = r < sq;
       const float* prow = P + (long long)r * a.P.ld + c0;
+      // this half-row of P, loaded once (zero beyond skv and for rows >= sq)
+      const int lim = live ? skv - c0 : 0;
+      float pv[64];
+#pragma unroll
+      for (int e = 0; e < 64; e += 4) {
+        const float4 p4 = e < lim ? *reinterpret_cast<const float4*>(prow + e)
+                                  : make_float4(0.f, 0.f, 0.f, 0.f);
+        pv[e] = p4.x;
+        pv[e + 1] = p4.y;
+        pv[e + 2] = p4.z;
+        pv[e + 3] = p4.w;
+      }
       float dp[64];
       float t = 0.f;
       if (any) {
@@ -314,15 +326,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
           }
         }
 #pragma unroll
-        for (int e = 0; e < 64; e += 4) {
-          if (live && c0 + e < skv) {
-            const float4 p4 = *reinterpret_cast<const float4*>(prow + e);
-            t += dp[e] * p4.x;
-            t += dp[e + 1] * p4.y;
-            t += dp[e + 2] * p4.z;
-            t += dp[e + 3] * p4.w;
-          }
-        }
+        for (int e = 0; e < 64; ++e) t += dp[e] * pv[e];
       }
       xch[half * 128 + r] = t;
       tc_before();
@@ -334,15 +338,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
           if (c0 + c * 8 < skv16) {
             float ds[8];
 #pragma unroll
-            for (int e = 0; e < 8; e += 4) {
-              const int j = c * 8 + e;
-              float4 p4 = make_float4(0.f, 0.f, 0.f, 0.f);
-              if (live && c0 + j < skv) p4 = *reinterpret_cast<const float4*>(prow + j);
-              ds[e] = p4.x * (dp[j] - t);
-              ds[e + 1] = p4.y * (dp[j + 1] - t);
-              ds[e + 2] = p4.z * (dp[j + 2] - t);
-              ds[e + 3] = p4.w * (dp[j + 3] - t);
-            }
+            for (int e = 0; e < 8; ++e) ds[e] = pv[c * 8 + e] * (dp[c * 8 + e] - t);
             put8(dSk.hi, dSk.lo, 128, r, half * 8 + c, ds, amax);
           }
         }
