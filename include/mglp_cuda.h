@@ -232,6 +232,17 @@ mglp_status mglp_test_gemm(int G, int M, int N, int K, const float* A, long long
                            int b_presplit, const float* bias, float* C, long long c_slot, int ldc,
                            int engine, int* range_flag);
 
+/* ---- Lipschitz probe (lipschitz.cpp:53-149, estimate_lipschitz /
+ * estimate_stack) on the device: for each layer in `layers` (NULL: every
+ * layer, n_layers ignored) the max over `samples` draws of
+ * ||F(x + delta) - F(x)|| / ||delta|| of the layer's residual map F, x =
+ * input_scale * N(.), delta = delta_scale * N(.) over one [1, seq_len, d]
+ * sequence (the reference's rng streams kProbeInput / kProbeDelta, folded
+ * per layer). estimates: one double per probed layer. Synchronous. */
+mglp_status mglp_engine_lipschitz(mglp_engine* e, int samples, double delta_scale,
+                                  double input_scale, int seq_len, unsigned long long seed,
+                                  const int* layers, int n_layers, double* estimates);
+
 /* ---- test hook: the fused tcgen05 attention (attn_tc.cu) on device buffers ----
  * Q, K, V (and dO, dQ, dK, dV, O) are [B][s][ld] token rows with head h at
  * column h*dh (the qkv layout of the layer); P is [B][H][sq][pad4(skv)].

@@ -214,6 +214,35 @@ class RefEngine:
         lib().ref_engine_reset(self.h)
 
 
+def lipschitz_estimate(stack: "RefStack", layer, samples, delta_scale, input_scale, seq_len,
+                       seed) -> float:
+    """estimate_lipschitz(stack, layer, cfg, seed).estimate (lipschitz.cpp:90-139)"""
+    out = C.c_double()
+    _check(lib().ref_lipschitz_estimate(stack.h, layer, samples, C.c_double(delta_scale),
+                                        C.c_double(input_scale), seq_len, C.c_ulonglong(seed),
+                                        C.byref(out)))
+    return out.value
+
+
+def lipschitz_select(estimates, k_open, k_close):
+    """select_buffer_layers (lipschitz.cpp:151-184) -> (buffered, interior_spike)"""
+    est = np.ascontiguousarray(estimates, np.float64)
+    buf = (C.c_int * max(1, len(est)))()
+    nb, sp = C.c_int(), C.c_int()
+    _check(lib().ref_lipschitz_select(_ptr(est), len(est), k_open, k_close, buf, C.byref(nb),
+                                      C.byref(sp)))
+    return [buf[i] for i in range(nb.value)], bool(sp.value)
+
+
+def lipschitz_recommend(amps, threshold=2.0):
+    """recommend_buffers (lipschitz.cpp:219-239) -> (k_open, k_close)"""
+    a = np.ascontiguousarray(amps, np.float64)
+    ko, kc = C.c_int(), C.c_int()
+    _check(lib().ref_lipschitz_recommend(_ptr(a), len(a), C.c_double(threshold), C.byref(ko),
+                                         C.byref(kc)))
+    return ko.value, kc.value
+
+
 def scalar_solve(rates, h, cf, levels, z0, iters, tol=0.0, workers=1):
     rates = np.ascontiguousarray(rates, np.float64)
     n = rates.size

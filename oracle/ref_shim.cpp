@@ -15,6 +15,8 @@
 //   ref_decide           controller.hpp:71-84
 //   ref_make_batch       make_batch (tasks.cpp:45-89)
 //   ref_model_*          Model ctor / param_tensors (model.cpp:50-100)
+//   ref_lipschitz_*      estimate_lipschitz / select_buffer_layers /
+//                        recommend_buffers (lipschitz.cpp:53-239)
 //   ref_run_training     run_training -> metrics CSV + final MGLP v1
 //                        checkpoint (training.cpp:92-135, 315-352;
 //                        checkpoint.cpp:88-112)
@@ -28,6 +30,7 @@
 #include <string>
 #include <vector>
 
+#include "mglp/lipschitz.hpp"
 #include "mglp/adjoint.hpp"
 #include "mglp/blocks.hpp"
 #include "mglp/controller.hpp"
@@ -569,6 +572,46 @@ int ref_model_params(const double* model, unsigned long long seed, double* flat,
     }
     *n_flat = n;
     *n_shapes = k;
+  });
+}
+
+// ---- Lipschitz probe (lipschitz.cpp) -----------------------------------------
+
+int ref_lipschitz_estimate(void* h, int layer, int samples, double delta_scale,
+                           double input_scale, int seq_len, unsigned long long seed,
+                           double* out) {
+  return guard([&] {
+    ProbeConfig cfg;
+    cfg.samples = samples;
+    cfg.delta_scale = delta_scale;
+    cfg.input_scale = input_scale;
+    cfg.seq_len = seq_len;
+    *out = estimate_lipschitz(*static_cast<RefStack*>(h)->stack, layer, cfg, seed).estimate;
+  });
+}
+
+int ref_lipschitz_select(const double* est, int n, int k_open, int k_close, int* buffered,
+                         int* n_buffered, int* spike) {
+  return guard([&] {
+    std::vector<LipschitzEstimate> es(n);
+    for (int i = 0; i < n; ++i) {
+      es[i].layer = i;
+      es[i].estimate = est[i];
+    }
+    const BufferPlan plan = select_buffer_layers(es, k_open, k_close);
+    *n_buffered = (int)plan.buffered.size();
+    for (size_t i = 0; i < plan.buffered.size(); ++i) buffered[i] = plan.buffered[i];
+    *spike = plan.interior_spike ? 1 : 0;
+  });
+}
+
+int ref_lipschitz_recommend(const double* amps, int n, double threshold, int* k_open,
+                            int* k_close) {
+  return guard([&] {
+    const BufferRecommendation rec =
+        recommend_buffers(std::vector<double>(amps, amps + n), threshold);
+    *k_open = rec.k_open;
+    *k_close = rec.k_close;
   });
 }
 

@@ -1,5 +1,6 @@
 // extern "C" boundary (include/mglp_cuda.h) over the C++ engine. Exceptions
 // never cross it: ValidationError -> 1, everything else -> 2 (errors.hpp:25-35).
+#include <algorithm>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -297,6 +298,24 @@ mglp_status mglp_engine_step_size(mglp_engine* e, int layer, double* h) {
     need(e, "engine");
     if (layer < 0 || layer >= e->eng->total_layers()) throw ValidationError("layer out of range");
     *h = e->eng->step_size(layer);
+  });
+}
+
+mglp_status mglp_engine_lipschitz(mglp_engine* e, int samples, double delta_scale,
+                                  double input_scale, int seq_len, unsigned long long seed,
+                                  const int* layers, int n_layers, double* estimates) {
+  return guard([&] {
+    need(e, "engine");
+    need(estimates, "estimates");
+    std::vector<int> ls;
+    if (layers) {
+      ls.assign(layers, layers + n_layers);
+    } else {
+      for (int l = 0; l < e->eng->total_layers(); ++l) ls.push_back(l);
+    }
+    std::vector<double> est;
+    lipschitz_probe(*e->eng, samples, delta_scale, input_scale, seq_len, seed, ls, &est);
+    std::copy(est.begin(), est.end(), estimates);
   });
 }
 

@@ -470,19 +470,21 @@ void Engine::set_shape(int batch, int s_x, int s_y) {
     b.dP2 = take((long long)B_ * H * sy_ * ((sx_ + 3) & ~3));
   }
   b.size = off;
+  const long long cache_slots = eval_only_ ? 1 : total_;
   MGLP_CUDA(cudaMalloc(&scratch_, (size_t)Gmax_ * al_.size * sizeof(float)));
-  MGLP_CUDA(cudaMalloc(&cache_, (size_t)total_ * al_.size * sizeof(float)));
+  MGLP_CUDA(cudaMalloc(&cache_, (size_t)cache_slots * al_.size * sizeof(float)));
   MGLP_CUDA(cudaMalloc(&bscratch_, (size_t)Gmax_ * bl_.size * sizeof(float)));
-  MGLP_CUDA(cudaMalloc(&bcache_, (size_t)total_ * bl_.size * sizeof(float)));
+  MGLP_CUDA(cudaMalloc(&bcache_, (size_t)cache_slots * bl_.size * sizeof(float)));
   colred_cap_ = (long long)std::max(total_, Gmax_) * kColRedChunks *
                 std::max(std::max(3 * sd_.d, sd_.ffn), 2 * sd_.d) * 2;
   MGLP_CUDA(cudaMalloc(&colred_part_, (size_t)colred_cap_ * sizeof(double)));
   bcache_valid_.assign(total_, 0);
-  MGLP_CUDA(cudaMalloc(&traj_, (size_t)(total_ + 1) * state_n_ * sizeof(float)));
-  MGLP_CUDA(cudaMalloc(&lam_all_, (size_t)(total_ + 1) * state_n_ * sizeof(float)));
+  const long long traj_slots = eval_only_ ? 1 : total_ + 1;
+  MGLP_CUDA(cudaMalloc(&traj_, (size_t)traj_slots * state_n_ * sizeof(float)));
+  MGLP_CUDA(cudaMalloc(&lam_all_, (size_t)traj_slots * state_n_ * sizeof(float)));
   MGLP_CUDA(cudaMalloc(&zero_state_, (size_t)state_n_ * sizeof(float)));
-  MGLP_CUDA(cudaMemsetAsync(traj_, 0, (size_t)(total_ + 1) * state_n_ * sizeof(float), stream_));
-  MGLP_CUDA(cudaMemsetAsync(lam_all_, 0, (size_t)(total_ + 1) * state_n_ * sizeof(float), stream_));
+  MGLP_CUDA(cudaMemsetAsync(traj_, 0, (size_t)traj_slots * state_n_ * sizeof(float), stream_));
+  MGLP_CUDA(cudaMemsetAsync(lam_all_, 0, (size_t)traj_slots * state_n_ * sizeof(float), stream_));
   MGLP_CUDA(cudaMemsetAsync(zero_state_, 0, (size_t)state_n_ * sizeof(float), stream_));
   {
     GemmArgs probe;
@@ -492,8 +494,10 @@ void Engine::set_shape(int batch, int s_x, int s_y) {
     part_off_ln_ = gemm_blocks(probe);
     part_off_elem_ = part_off_ln_ + ln_bwd_blocks(std::max(Tx_, Ty_));
   }
-  alloc_solver(fwd_, false);
-  alloc_solver(bwd_, true);
+  if (!eval_only_) {
+    alloc_solver(fwd_, false);
+    alloc_solver(bwd_, true);
+  }
   std::fill(cache_valid_.begin(), cache_valid_.end(), 0);
   first_fwd_ = first_bwd_ = true;
   MGLP_CUDA(cudaStreamSynchronize(stream_));
@@ -950,6 +954,7 @@ void Engine::eval_forward(const EvalSpec& e0) {
   }
   EvalSpec e = e0;
   e.cmb.z = e.in;
+  if (e.residual_only) e.cmb.z = state_mat(zero_state_, 0, sd_.d, 0, 0);  // p = 0 + dt F
   e.cmb.dt = e.dt;
   const int d = sd_.d;
   if (sd_.kind == 2 && e.layer0 >= n_split_) {
@@ -2139,6 +2144,23 @@ void Engine::serial_adjoint_device(const float* lamN_dev, float* lam0_dev, bool 
 }
 
 // ---- single-step hooks ----
+void Engine::residual_device(int layer, const float* z, int G, float* F) {
+  if (layer < 0 || layer >= total_) throw ValidationError("residual: layer out of range");
+  for (int g0 = 0; g0 < G; g0 += Gmax_) {
+    EvalSpec e;
+    e.G = std::min(Gmax_, G - g0);
+    e.layer0 = layer;
+    e.layer_step = 0;
+    e.dt = 1.f;
+    e.in = state_mat(const_cast<float*>(z) + (long long)g0 * state_n_, state_n_, sd_.d, 0, 1);
+    e.act = ActRef{scratch_, al_.size, 0, 1};
+    e.residual_only = true;
+    e.cmb.mode = CM_PLAIN;
+    e.cmb.out = state_mat(F + (long long)g0 * state_n_, state_n_, sd_.d, 0, 1);
+    eval_forward(e);
+  }
+}
+
 void Engine::step_device(int layer, double dt, const float* z, float* out) {
   if (layer < 0 || layer >= total_) throw ValidationError("step: layer out of range");
   EvalSpec e;

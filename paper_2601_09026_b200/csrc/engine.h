@@ -93,6 +93,12 @@ class Engine {
   int batch() const { return B_; }
 
   // ---- shape ----
+  // eval-only engines (the Lipschitz probe) skip the per-layer activation
+  // caches and trajectory storage: they only run residual_device
+  void set_eval_only(bool on) {
+    eval_only_ = on;
+    if (on) Gmax_ = 2;  // families of at most two evaluations (x, x + delta)
+  }
   void set_shape(int batch, int s_x, int s_y);
   long long state_elems() const { return state_n_; }
   int width() const { return sd_.d; }
@@ -100,6 +106,7 @@ class Engine {
 
   // ---- LayerParallelEngine surface ----
   SolveCfg& config() { return cfg_; }
+  const SolveCfg& config() const { return cfg_; }
   void forward_device(const float* z0_dev);
   void backward_device(const float* lamN_dev, float* lam0_dev, bool want_grads,
                        bool traj_is_current);
@@ -117,6 +124,13 @@ class Engine {
   void replay_step();
   void drop_graph();
   bool has_graph() const { return graph_exec_ != nullptr; }
+
+  // F(z_g) of one layer for a family of G input states (LayerStack::residual,
+  // blocks.cpp:466-514, without the step or any solver combine): the map the
+  // Lipschitz probe differentiates (lipschitz.cpp:120-129)
+  void residual_device(int layer, const float* z, int G, float* F);
+  const StackDesc& stack_desc() const { return sd_; }
+  int n_split() const { return n_split_; }
 
   // serial reference sweeps on device (blocks.cpp:659-682)
   void serial_forward_device(const float* z0_dev);
@@ -206,6 +220,7 @@ class Engine {
     ActRef bact{nullptr, 0, 0, 1};
     bool wgrad_only = false;  // intermediates already in bact: only form dW, db
     bool keep_act = false;    // scratch activations are read by a following adjoint
+    bool residual_only = false;  // out = F(z) (the combine starts from a zero state)
   };
   void eval_forward(const EvalSpec& e);
   void eval_adjoint(const EvalSpec& e);
@@ -279,6 +294,7 @@ class Engine {
   // ----- members -----
   StackDesc sd_;
   SolveCfg cfg_;
+  bool eval_only_ = false;
   int device_ = 0;
   std::shared_ptr<Transport> tr_;
   cudaStream_t stream_ = nullptr;
@@ -348,5 +364,11 @@ class Engine {
     prof_.push_back(r);
   }
 };
+
+// Lipschitz probe (probe.cu; lipschitz.cpp:53-149): per requested layer the
+// max over `samples` draws of ||F(x + delta) - F(x)|| / ||delta||.
+void lipschitz_probe(const Engine& src, int samples, double delta_scale, double input_scale,
+                     int seq_len, uint64_t seed, const std::vector<int>& layers,
+                     std::vector<double>* est);
 
 }  // namespace mglp
