@@ -424,19 +424,36 @@ def run_device(args, cfg, rank, world, dist):
         pass
     gemm_ms, gemm_fl, gemm_n = ms3[0], fl3[0], ln3[0]
     achieved = gemm_fl / (gemm_ms * 1e-3) / 1e12 if gemm_ms > 0 else 0.0
+    attn_ms, attn_fl = ms3[1], fl3[1]
     bf16_peak = peaks.get("bf16_tflops_sustained", 1400.0)
+    # DRAM traffic per launch of the dominant kernel from the committed ncu
+    # --set full capture (tools/gpu_ncu_final.sh -> tools/ncu_summarize.py)
+    traffic, traffic_src = None, None
+    try:
+        tj = json.load(open(os.path.join(ROOT, "profiles", "r01_ncu_traffic.json")))
+        traffic, traffic_src = tj["traffic_bytes_per_launch"], tj["source"]
+    except Exception:
+        pass
     roofline = {
         "kernel": "gemm_tc_kernel (tcgen05 kind::f16, 3-pass fp16 hi/lo split, fp32 accumulate)",
         "bound": "tensor", "achieved": achieved, "peak": bf16_peak, "unit": "TFLOP/s",
         "frac": achieved / bf16_peak,
         "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained (measured)",
-        "traffic": None,
+        "traffic": traffic,
+        "traffic_unit": "bytes per launch (dram read + write)",
+        "traffic_source": traffic_src,
+        "achieved_how": "algorithmic GEMM FLOPs of one profiled iteration / sum of CUDA-event "
+                        "durations of its GEMM launches (engine stream)",
         # the split issues 3 dense fp16 MMAs per algorithmic one: its ceiling is peak/3
         "frac_of_split_ceiling": achieved / (bf16_peak / 3.0),
         "gemm_share_of_step": gemm_ms / sum(ms3) if sum(ms3) > 0 else None,
         "gemm_launches_per_step": gemm_n,
-        "per_class_ms": {"gemm_tcgen05": ms3[0], "other": ms3[1],
-                         "rows_layernorm_softmax": ms3[2]},
+        "attention": {"kernels": "attn_fwd/bwd (s<=128) or attn_fwd_long/bwd_dkdv/bwd_dq "
+                                 "(128<s<=512): fused tcgen05 per (batch, head)",
+                      "achieved": attn_fl / (attn_ms * 1e-3) / 1e12 if attn_ms > 0 else None,
+                      "unit": "TFLOP/s", "launches_per_step": ln3[1]},
+        "per_class_ms": {"gemm_tcgen05": ms3[0], "attention_tcgen05": ms3[1],
+                         "rows_layernorm_colsum_state": ms3[2]},
     }
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
