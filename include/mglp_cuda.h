@@ -232,6 +232,17 @@ mglp_status mglp_test_gemm(int G, int M, int N, int K, const float* A, long long
                            int b_presplit, const float* bias, float* C, long long c_slot, int ldc,
                            int engine, int* range_flag);
 
+/* ---- frozen dropout masks: LayerStack::refresh_dropout / clear_dropout
+ * (blocks.cpp:576-599). refresh sets the shape and generates, on the device,
+ * the masks of batch `batch_index` for every layer and site from the
+ * reference's counter streams (bit-identical keep / drop decisions); they
+ * apply to every following step / adjoint step / solve of that shape until
+ * cleared or refreshed. No-ops when the stack's dropout is <= 0. */
+mglp_status mglp_engine_refresh_dropout(mglp_engine* e, unsigned long long seed,
+                                        unsigned long long batch_index, int batch, int s_x,
+                                        int s_y);
+mglp_status mglp_engine_clear_dropout(mglp_engine* e);
+
 /* ---- Lipschitz probe (lipschitz.cpp:53-149, estimate_lipschitz /
  * estimate_stack) on the device: for each layer in `layers` (NULL: every
  * layer, n_layers ignored) the max over `samples` draws of

@@ -132,6 +132,8 @@ _SIGS = {
                         C.c_int, C.POINTER(C.c_float)],
     "mglp_test_attention": [C.c_int] * 6 + [_vp, _vp, _vp, C.c_int] + [_vp] * 6 + [_ip],
     "mglp_bench_attention": [C.c_int] * 8 + [C.POINTER(C.c_float)],
+    "mglp_engine_refresh_dropout": [_vp, C.c_ulonglong, C.c_ulonglong, C.c_int, C.c_int, C.c_int],
+    "mglp_engine_clear_dropout": [_vp],
     "mglp_engine_lipschitz": [_vp, C.c_int, C.c_double, C.c_double, C.c_int, C.c_ulonglong, _ip,
                               C.c_int, _dp],
 }

@@ -301,6 +301,23 @@ mglp_status mglp_engine_step_size(mglp_engine* e, int layer, double* h) {
   });
 }
 
+mglp_status mglp_engine_refresh_dropout(mglp_engine* e, unsigned long long seed,
+                                        unsigned long long batch_index, int batch, int s_x,
+                                        int s_y) {
+  return guard([&] {
+    need(e, "engine");
+    e->eng->set_shape(batch, s_x, s_y);
+    e->eng->refresh_dropout(seed, batch_index);
+  });
+}
+
+mglp_status mglp_engine_clear_dropout(mglp_engine* e) {
+  return guard([&] {
+    need(e, "engine");
+    e->eng->clear_dropout();
+  });
+}
+
 mglp_status mglp_engine_lipschitz(mglp_engine* e, int samples, double delta_scale,
                                   double input_scale, int seq_len, unsigned long long seed,
                                   const int* layers, int n_layers, double* estimates) {

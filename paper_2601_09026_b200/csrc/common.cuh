@@ -168,6 +168,25 @@ enum EpiKind : int {
   EPI_GRAD_ACC = 5,   // out1 += gscale * acc               (blocks.cpp:108, 126-129)
 };
 
+// Frozen dropout masks (blocks.cpp:576-599) as generated by
+// Engine::refresh_dropout: one byte per element (1 = keep) of every (layer,
+// site) [B, s, d] tensor, value 1/keep where kept. The member g of a family
+// uses block (layer0 + g*step) * 3 + site; element index = row * cols + col.
+struct DropMask {
+  const unsigned char* m = nullptr;  // [total layers][3][slot]; null = no dropout
+  long long slot = 0;                // elements per (layer, site) block
+  int layer0 = 0, step = 1, site = 0;
+  int cols = 0;
+  float scale = 1.f;  // 1 / keep
+  __host__ __device__ bool on() const { return m != nullptr; }
+  __device__ __forceinline__ const unsigned char* at(int g, long long row) const {
+    return m + ((long long)(layer0 + g * step) * 3 + site) * slot + row * cols;
+  }
+};
+
+__device__ __forceinline__ float drop_val(const DropMask& m, int g, long long row, int col) {
+  return m.at(g, row)[col] ? m.scale : 0.f;
+}
 struct EpiArgs {
   int kind = EPI_STORE;
   Mat out1, out2, add1, add2, aux;
@@ -175,6 +194,12 @@ struct EpiArgs {
   float gscale = 1.f;
   float alpha = 1.f;  // EPI_STORE: out1 = alpha*acc (+ bias)
   Combine cmb;  // EPI_FINAL
+  // EPI_BIAS_ADD2 / EPI_FINAL: the projection output (acc + bias) is a
+  // dropout site (attention output phi1 / phi3, MLP output phi2). Applied by
+  // the scalar epilogue_row only: a GEMM with an active mask takes that path
+  // (gemm_tc.cu clears vec_ok), so the vectorised epilogues keep their
+  // register budget.
+  DropMask drop;
 };
 
 constexpr float kGeluC = 0.7978845608028654f;  // tensor.cpp:345
@@ -426,7 +451,8 @@ __device__ __forceinline__ double epilogue_row(const EpiArgs& e, int g, int b, i
       const float* a1 = e.add1.ok() ? e.add1.at(g) + (long long)row * e.add1.ld + col0 : nullptr;
       const float* a2 = e.add2.at(g) + (long long)row * e.add2.ld + col0;
       for (int i = 0; i < n; ++i) {
-        const float a = bias ? acc[i] + bias[col0 + i] : acc[i];
+        float a = bias ? acc[i] + bias[col0 + i] : acc[i];
+        if (e.drop.on()) a *= drop_val(e.drop, g, row, col0 + i);
         const float v1 = a1 ? a1[i] + a : a;
         if (o1) o1[i] = v1;
         if (o2) o2[i] = a2[i] + v1;
@@ -446,7 +472,8 @@ __device__ __forceinline__ double epilogue_row(const EpiArgs& e, int g, int b, i
       const long long off_out = (long long)row * e.cmb.out.ld + col0;
       const long long off_z = (long long)row * e.cmb.z.ld + col0;
       for (int i = 0; i < n; ++i) {
-        const float mo = bias ? acc[i] + bias[col0 + i] : acc[i];
+        float mo = bias ? acc[i] + bias[col0 + i] : acc[i];
+        if (e.drop.on()) mo *= drop_val(e.drop, g, row, col0 + i);
         const float F = a1[i] + mo;
         combine_apply(e.cmb, g, off_out + i, off_z + i, F, r2);
       }

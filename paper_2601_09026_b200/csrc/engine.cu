@@ -62,8 +62,6 @@ Engine::Engine(const StackDesc& sd, const SolveCfg& cfg, int device,
     throw ValidationError("device stack: width and ffn must be multiples of 4");
   if ((sd_.d / sd_.heads) % 4 != 0 || sd_.d / sd_.heads > 64)
     throw ValidationError("device stack: head width must be a multiple of 4 and <= 64");
-  if (sd_.dropout > 0.0)
-    throw ValidationError("device stack: dropout > 0 is not supported on the device path");
   switch (sd_.kind) {
     case 0:
       if (sd_.n_enc <= 0) throw ValidationError("LayerStack: n_enc must be positive");
@@ -148,6 +146,7 @@ Engine::~Engine() {
                    zero_state_, snap_fwd_, snap_bwd_})
     if (p) cudaFree(p);
   if (colred_part_) cudaFree(colred_part_);
+  if (drop_masks_) cudaFree(drop_masks_);
   drop_graph();
   for (cudaEvent_t ev : ev_pool_) cudaEventDestroy(ev);
   if (stream_) cudaStreamDestroy(stream_);
@@ -400,6 +399,7 @@ void Engine::set_shape(int batch, int s_x, int s_y) {
   MGLP_CUDA(cudaSetDevice(device_));
   MGLP_CUDA(cudaStreamSynchronize(stream_));
   drop_graph();
+  drop_on_ = false;  // masks are per shape: refresh_dropout again
   free_solver(fwd_);
   free_solver(bwd_);
   if (colred_part_) cudaFree(colred_part_);
@@ -459,6 +459,10 @@ void Engine::set_shape(int batch, int s_x, int s_y) {
   b.dqkv = take(R * 3 * d);
   b.dn1 = take(R * d);
   b.dP = take((long long)B_ * H * smax * ((smax + 3) & ~3));
+  // dropout: the upstream of the MLP branch and of the cross-attention output
+  // with their masks applied (the operands of those branches' dgrad / wgrad)
+  b.upm = take(sd_.dropout > 0.0 ? R * d : 0);
+  b.dcpre = take(sd_.dropout > 0.0 && sd_.kind == 2 ? Ty_ * d : 0);
   if (sd_.kind == 2) {
     b.dybar = take(Ty_ * d);
     b.dy = take(Ty_ * d);
@@ -1018,6 +1022,7 @@ void Engine::encoder_forward(const EvalSpec& e, int R, bool causal, Mat X, Mat Y
   g.B = par(L.w_o, d, l0, ls);
   g.Bhl = par_hl(L, L.w_o, l0, ls, false);
   g.ep.kind = EPI_BIAS_ADD2;
+  g.ep.drop = dmask(0, l0, ls);  // attention output phi1
   g.ep.out1 = a1;
   g.ep.out2 = u;
   g.ep.add2 = X;
@@ -1057,6 +1062,7 @@ void Engine::encoder_forward(const EvalSpec& e, int R, bool causal, Mat X, Mat Y
   g.B = par(L.w_out, f, l0, ls);
   g.Bhl = par_hl(L, L.w_out, l0, ls, false);
   g.ep.kind = EPI_FINAL;
+  g.ep.drop = dmask(1, l0, ls);  // MLP output phi2
   g.ep.add1 = a1;
   g.ep.bias = par(L.b_out, 0, l0, ls);
   Combine c = e.cmb;
@@ -1141,6 +1147,7 @@ void Engine::decoder_forward(const EvalSpec& e) {
 
   g = mk(R, d, d, ctx, L.w_o, d);
   g.ep.kind = EPI_BIAS_ADD2;
+  g.ep.drop = dmask(0, l0, ls);  // self-attention output phi1
   g.ep.out1 = a1;
   g.ep.out2 = u3;
   g.ep.add2 = Y;
@@ -1173,6 +1180,7 @@ void Engine::decoder_forward(const EvalSpec& e) {
 
   g = mk(R, d, d, cctx, L.w_co, d);
   g.ep.kind = EPI_BIAS_ADD2;
+  g.ep.drop = dmask(2, l0, ls);  // cross-attention output phi3
   g.ep.out1 = ybar;
   g.ep.add1 = a1;
   g.ep.out2 = u2;
@@ -1199,6 +1207,7 @@ void Engine::decoder_forward(const EvalSpec& e) {
 
   g = mk(R, d, f, gg, L.w_out, f);
   g.ep.kind = EPI_FINAL;
+  g.ep.drop = dmask(1, l0, ls);  // MLP output phi2
   g.ep.add1 = ybar;
   g.ep.bias = par(L.b_out, 0, l0, ls);
   Combine c = e.cmb;
@@ -1283,6 +1292,10 @@ void Engine::encoder_adjoint(const EvalSpec& e, bool causal) {
   Mat dh = bwd_mat(e, bl_.dh, f), dn2 = bwd_mat(e, bl_.dn2, d), du = bwd_mat(e, bl_.du, d);
   Mat da1 = bwd_mat(e, bl_.da1, d), dctx = bwd_mat(e, bl_.dctx, d), dqkv = bwd_mat(e, bl_.dqkv, 3 * d);
   Mat dn1 = bwd_mat(e, bl_.dn1, d), dPm = bwd_mat(e, bl_.dP, 0);
+  // dropout (blocks.cpp:259-271): the MLP branch sees UP * phi2, the
+  // attention branch (UP + du) * phi1
+  const bool drop = drop_on_;
+  const Mat UPm = drop ? bwd_mat(e, bl_.upm, d) : UP;
 
   auto mk = [&](int M, int N, int K, Mat A, long long w, int ldw) {
     GemmArgs g;
@@ -1297,7 +1310,13 @@ void Engine::encoder_adjoint(const EvalSpec& e, bool causal) {
     return g;
   };
   if (!e.wgrad_only) {  // dgrad chain (skipped when the backward cache holds it)
-    GemmArgs g = mk(R, f, d, UP, L.w_out, f);
+    if (drop) {
+      ++launches_;
+      prof_shape_ = {7, d, 0, G};
+      timed(PROF_ROW, 0.0, 8.0 * G * (double)R * d,
+            [&] { launch_mask_copy(G, R, d, UPm, UP, dmask(1, l0, ls), active_, stream_); });
+    }
+    GemmArgs g = mk(R, f, d, UPm, L.w_out, f);
     g.ep.kind = EPI_GELU_BWD;
     g.ep.out1 = dh;
     g.ep.aux = hh;
@@ -1319,6 +1338,7 @@ void Engine::encoder_adjoint(const EvalSpec& e, bool causal) {
     lb.out1 = du;
     lb.out2 = da1;
     lb.addB = UP;
+    lb.drop2 = dmask(0, l0, ls);
     ++launches_;
     prof_shape_ = {4, lb.d, 0, lb.G};
     timed(PROF_ROW, 0.0, 20.0 * lb.G * (double)lb.rows * lb.d,
@@ -1411,8 +1431,8 @@ void Engine::encoder_adjoint(const EvalSpec& e, bool causal) {
       timed(PROF_ROW, 0.0, (x.ok() ? 8.0 : 4.0) * c.G * (double)c.rows * c.cols,
             [&] { launch_colred(c, active_, stream_); });
     };
-    wg(d, f, UP, gg, L.w_out, f);
-    cr(UP, d, L.b_out, Mat{}, Mat{}, 0);
+    wg(d, f, UPm, gg, L.w_out, f);
+    cr(UPm, d, L.b_out, Mat{}, Mat{}, 0);
     wg(f, d, dh, n2, L.w_in, d);
     cr(dh, f, L.b_in, Mat{}, Mat{}, 0);
     cr(dn2, d, L.ln2_b, u, st2, L.ln2_g);
@@ -1446,6 +1466,11 @@ void Engine::decoder_adjoint(const EvalSpec& e) {
   Mat dckv = bwd_mat(e, bl_.dckv, 2 * d), dn3 = bwd_mat(e, bl_.dn3, d), dxe = bwd_mat(e, bl_.dxe, d);
   Mat da1 = bwd_mat(e, bl_.da1, d), dctx = bwd_mat(e, bl_.dctx, d), dqkv = bwd_mat(e, bl_.dqkv, 3 * d);
   Mat dn1 = bwd_mat(e, bl_.dn1, d), dPm = bwd_mat(e, bl_.dP, 0), dP2 = bwd_mat(e, bl_.dP2, 0);
+  // dropout (blocks.cpp:312-324): MLP branch UP * phi2, cross-attention
+  // output dybar * phi3, self-attention output (dybar + du3) * phi1
+  const bool drop = drop_on_;
+  const Mat UPm = drop ? bwd_mat(e, bl_.upm, d) : UPy;
+  const Mat dcp = drop ? bwd_mat(e, bl_.dcpre, d) : dybar;
 
   auto mk = [&](int M, int N, int K, Mat A, long long w, int ldw) {
     GemmArgs g;
@@ -1460,7 +1485,13 @@ void Engine::decoder_adjoint(const EvalSpec& e) {
     return g;
   };
   if (!e.wgrad_only) {  // dgrad chain (skipped when the backward cache holds it)
-    GemmArgs g = mk(R, f, d, UPy, L.w_out, f);
+    if (drop) {
+      ++launches_;
+      prof_shape_ = {7, d, 0, G};
+      timed(PROF_ROW, 0.0, 8.0 * G * (double)R * d,
+            [&] { launch_mask_copy(G, R, d, UPm, UPy, dmask(1, l0, ls), active_, stream_); });
+    }
+    GemmArgs g = mk(R, f, d, UPm, L.w_out, f);
     g.ep.kind = EPI_GELU_BWD;
     g.ep.out1 = dh;
     g.ep.aux = hh;
@@ -1487,7 +1518,13 @@ void Engine::decoder_adjoint(const EvalSpec& e) {
     timed(PROF_ROW, 0.0, 20.0 * lb.G * (double)lb.rows * lb.d,
           [&] { launch_ln_bwd(lb, active_, stream_); });
 
-    g = mk(R, d, d, dybar, L.w_co, d);
+    if (drop) {
+      ++launches_;
+      prof_shape_ = {7, d, 0, G};
+      timed(PROF_ROW, 0.0, 8.0 * G * (double)R * d,
+            [&] { launch_mask_copy(G, R, d, dcp, dybar, dmask(2, l0, ls), active_, stream_); });
+    }
+    g = mk(R, d, d, dcp, L.w_co, d);
     g.ep.kind = EPI_STORE;
     g.ep.out1 = dcctx;
     gemm(g);
@@ -1513,6 +1550,7 @@ void Engine::decoder_adjoint(const EvalSpec& e) {
     lb.out1 = dy;     // du2 + du3
     lb.addB = dybar;
     lb.out2 = da1;    // dybar + du3
+    lb.drop2 = dmask(0, l0, ls);
     ++launches_;
     prof_shape_ = {4, lb.d, 0, lb.G};
     timed(PROF_ROW, 0.0, 20.0 * lb.G * (double)lb.rows * lb.d,
@@ -1602,13 +1640,13 @@ void Engine::decoder_adjoint(const EvalSpec& e) {
       timed(PROF_ROW, 0.0, (x.ok() ? 8.0 : 4.0) * c.G * (double)c.rows * c.cols,
             [&] { launch_colred(c, active_, stream_); });
     };
-    wg(d, f, R, UPy, gg, L.w_out, f);
-    cr(R, UPy, d, L.b_out, Mat{}, Mat{}, 0);
+    wg(d, f, R, UPm, gg, L.w_out, f);
+    cr(R, UPm, d, L.b_out, Mat{}, Mat{}, 0);
     wg(f, d, R, dh, n2, L.w_in, d);
     cr(R, dh, f, L.b_in, Mat{}, Mat{}, 0);
     cr(R, dn2, d, L.ln2_b, u2, st2, L.ln2_g);
-    wg(d, d, R, dybar, cctx, L.w_co, d);
-    cr(R, dybar, d, L.b_co, Mat{}, Mat{}, 0);
+    wg(d, d, R, dcp, cctx, L.w_co, d);
+    cr(R, dcp, d, L.b_co, Mat{}, Mat{}, 0);
     wg(d, d, R, dcq, n3, L.w_cq, d);
     cr(R, dcq, d, L.b_cq, Mat{}, Mat{}, 0);
     wg(2 * d, d, Tx_, dckv, X, L.w_ckv, d);
@@ -2144,6 +2182,85 @@ void Engine::serial_adjoint_device(const float* lamN_dev, float* lam0_dev, bool 
 }
 
 // ---- single-step hooks ----
+namespace {
+// byte masks of every (layer, site) block: element i keeps iff
+// u01(splitmix64(key ^ i)) < keep (blocks.cpp:583-589; rng.hpp derive/u01),
+// key = the first four derive rounds, precomputed per block on the host
+__global__ void dropout_gen_kernel(unsigned char* m, const unsigned long long* keys,
+                                   const int* rows, long long slot, int d, int nblocks,
+                                   double keep_thr) {
+  const int blk = blockIdx.y;
+  if (blk >= nblocks) return;
+  const long long n = (long long)rows[blk] * d;
+  unsigned char* out = m + (long long)blk * slot;
+  const unsigned long long key = keys[blk];
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    out[i] = (double)(splitmix64(key ^ (unsigned long long)i) >> 11) < keep_thr ? 1 : 0;
+}
+}  // namespace
+
+void Engine::refresh_dropout(uint64_t seed, uint64_t batch_index) {
+  drop_on_ = false;
+  if (sd_.dropout <= 0.0) return;
+  if (!traj_) throw ValidationError("refresh_dropout: set the shape first");
+  const long long slot = (long long)std::max(Tx_, Ty_) * sd_.d;
+  const int nblk = total_ * 3;
+  MGLP_CUDA(cudaSetDevice(device_));
+  if (drop_slot_ != slot) {
+    if (drop_masks_) cudaFree(drop_masks_);
+    drop_masks_ = nullptr;
+    MGLP_CUDA(cudaMalloc(&drop_masks_, (size_t)nblk * slot));
+    drop_slot_ = slot;
+  }
+  // rng::derive(seed, kDropout, batch_index, layer*8 + site, i): the first
+  // four splitmix rounds per (layer, site) here, the last (^ i) on the device
+  std::vector<unsigned long long> keys((size_t)nblk);
+  std::vector<int> rows((size_t)nblk);
+  for (int l = 0; l < total_; ++l) {
+    const bool dec = sd_.kind == 2 && l >= n_split_;
+    for (int site = 0; site < 3; ++site) {
+      uint64_t k = splitmix64(seed ^ 0x243f6a8885a308d3ULL);
+      k = splitmix64(k ^ (uint64_t)kRngDropout);
+      k = splitmix64(k ^ batch_index);
+      k = splitmix64(k ^ ((uint64_t)l * 8 + (uint64_t)site));
+      keys[(size_t)l * 3 + site] = k;
+      // phi1, phi2 on every layer; phi3 (cross-attention) on decoder layers
+      rows[(size_t)l * 3 + site] = (site < 2 || dec) ? (dec ? Ty_ : Tx_) : 0;
+    }
+  }
+  unsigned long long* dkeys = nullptr;
+  int* drows = nullptr;
+  MGLP_CUDA(cudaMalloc(&dkeys, keys.size() * sizeof(unsigned long long)));
+  MGLP_CUDA(cudaMalloc(&drows, rows.size() * sizeof(int)));
+  MGLP_CUDA(cudaMemcpyAsync(dkeys, keys.data(), keys.size() * sizeof(unsigned long long),
+                            cudaMemcpyHostToDevice, stream_));
+  MGLP_CUDA(cudaMemcpyAsync(drows, rows.data(), rows.size() * sizeof(int), cudaMemcpyHostToDevice,
+                            stream_));
+  const double keep = 1.0 - sd_.dropout;
+  const int gx = (int)std::min<long long>((slot + 255) / 256, 256);
+  dropout_gen_kernel<<<dim3(gx, nblk), 256, 0, stream_>>>(drop_masks_, dkeys, drows, slot, sd_.d,
+                                                          nblk, keep * 0x1.0p53);
+  MGLP_CUDA(cudaGetLastError());
+  MGLP_CUDA(cudaStreamSynchronize(stream_));
+  cudaFree(dkeys);
+  cudaFree(drows);
+  drop_on_ = true;
+}
+
+DropMask Engine::dmask(int site, int layer0, int layer_step) const {
+  DropMask m;
+  if (!drop_on_) return m;
+  m.m = drop_masks_;
+  m.slot = drop_slot_;
+  m.layer0 = layer0;
+  m.step = layer_step;
+  m.site = site;
+  m.cols = sd_.d;
+  m.scale = (float)(1.0 / (1.0 - sd_.dropout));
+  return m;
+}
+
 void Engine::residual_device(int layer, const float* z, int G, float* F) {
   if (layer < 0 || layer >= total_) throw ValidationError("residual: layer out of range");
   for (int g0 = 0; g0 < G; g0 += Gmax_) {

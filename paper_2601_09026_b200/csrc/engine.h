@@ -92,6 +92,14 @@ class Engine {
   long long y_offset() const { return y_off_; }
   int batch() const { return B_; }
 
+  // ---- frozen dropout masks (blocks.cpp:576-599) ----
+  // refresh: the masks of batch `batch_index` (per layer and site, generated
+  // on the fly from the reference's counter streams); clear: no masks (the
+  // exact map, as for evaluation). No-ops when the stack's dropout is 0.
+  void refresh_dropout(uint64_t seed, uint64_t batch_index);
+  void clear_dropout() { drop_on_ = false; }
+  bool dropout_active() const { return drop_on_; }
+
   // ---- shape ----
   // eval-only engines (the Lipschitz probe) skip the per-layer activation
   // caches and trajectory storage: they only run residual_device
@@ -193,6 +201,7 @@ class Engine {
   struct BwdLayout {
     long long dh, dn2, du, da1, dctx, dqkv, dn1, dP;                   // encoder / self
     long long dybar, dy, dcctx, dcq, dckv, dn3, dxe, dP2;              // decoder
+    long long upm = 0, dcpre = 0;  // dropout: masked upstream of the MLP / cross-attention branch
     long long size = 0;
   };
 
@@ -295,6 +304,10 @@ class Engine {
   StackDesc sd_;
   SolveCfg cfg_;
   bool eval_only_ = false;
+  unsigned char* drop_masks_ = nullptr;  // device [total][3][drop_slot_] keep bytes
+  long long drop_slot_ = 0;
+  bool drop_on_ = false;
+  DropMask dmask(int site, int layer0, int layer_step) const;
   int device_ = 0;
   std::shared_ptr<Transport> tr_;
   cudaStream_t stream_ = nullptr;

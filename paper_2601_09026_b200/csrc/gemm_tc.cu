@@ -692,7 +692,8 @@ Prepared prepare(const GemmArgs& a) {
     const EpiArgs& e = a.ep;
     const Combine& c = e.cmb;
     p.vec_ok = al(e.out1) && al(e.out2) && al(e.add1) && al(e.add2) && al(e.aux) && al(e.bias) &&
-               al(c.z) && al(c.out) && al(c.base) && al(c.phib) && al(c.rho) && al(c.v);
+               al(c.z) && al(c.out) && al(c.base) && al(c.phib) && al(c.rho) && al(c.v) &&
+               !e.drop.on();  // dropout sites use the scalar epilogue (common.cuh)
   }
   p.a_mn = a.a_mn;
   p.b_direct = a.Bhl.ok() ? 1 : 0;

@@ -24,6 +24,7 @@ struct LnBwdArgs {
   Mat x, stats, up, gain;
   Mat addA, addB, out1, out2;
   Combine cmb;
+  DropMask drop2;  // out2 = (addB + L) * mask: the VJP through a dropout site
 };
 void launch_ln_bwd(const LnBwdArgs& a, const int* active, cudaStream_t s);
 int ln_bwd_blocks(int rows);
@@ -70,6 +71,9 @@ int elem_combine_blocks(long long n);
 
 // dst_g = src_g
 void launch_copy(int G, long long n, Mat dst, Mat src, const int* active, cudaStream_t s);
+// dst_g[r][c] = src_g[r][c] * mask(r, c)  (rows x d; hadamard with a dropout site)
+void launch_mask_copy(int G, int rows, int d, Mat dst, Mat src, const DropMask& m,
+                      const int* active, cudaStream_t s);
 // dst_g = dst_g + (a_g - b_g)     (correct_from, mgrit.hpp:219-221)
 void launch_correct(int G, long long n, Mat dst, Mat a, Mat b, const int* active,
                     cudaStream_t s);

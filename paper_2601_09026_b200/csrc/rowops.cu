@@ -130,7 +130,7 @@ __global__ void __launch_bounds__(256) ln_bwd_kernel(LnBwdArgs a, const int* act
         const float L = rstd * (dxh[i] - m1 - xh[i] * m2);
         const float v1 = addA ? addA[j] + L : L;
         if (o1) o1[j] = v1;
-        if (o2) o2[j] = addB[j] + L;
+        if (o2) o2[j] = a.drop2.on() ? (addB[j] + L) * drop_val(a.drop2, g, row, j) : addB[j] + L;
         if (comb) combine_apply(a.cmb, g, off_out + j, off_z + j, v1, r2);
       }
     }
@@ -267,7 +267,14 @@ __global__ void __launch_bounds__(256) ln_bwd4_kernel(LnBwdArgs a, const int* ac
         if (o1) st4(o1 + 4 * q, v1);
         if (o2) {
           const float4 b = addA ? ld4(addB + 4 * q) : ad[i];
-          st4(o2 + 4 * q, make_float4(b.x + L.x, b.y + L.y, b.z + L.z, b.w + L.w));
+          float4 w = make_float4(b.x + L.x, b.y + L.y, b.z + L.z, b.w + L.w);
+          if (a.drop2.on()) {
+            w.x *= drop_val(a.drop2, g, row, 4 * q);
+            w.y *= drop_val(a.drop2, g, row, 4 * q + 1);
+            w.z *= drop_val(a.drop2, g, row, 4 * q + 2);
+            w.w *= drop_val(a.drop2, g, row, 4 * q + 3);
+          }
+          st4(o2 + 4 * q, w);
         }
         if (comb) combine_apply4(a.cmb, g, off_out + 4 * q, off_z + 4 * q, v1, r2);
       }
@@ -697,6 +704,28 @@ void launch_copy(int G, long long n, Mat dst, Mat src, const int* active, cudaSt
   require_vec4(n, "copy");
   dim3 grid(stream_grid(n / 4, G), G);
   copy_kernel<<<grid, 256, 0, s>>>(G, n / 4, dst, src, active);
+}
+
+__global__ void __launch_bounds__(256) mask_copy_kernel(int rows, int d, Mat dst, Mat src,
+                                                        DropMask m, const int* active) {
+  if (stopped(active)) return;
+  const int g = blockIdx.y;
+  const long long n = (long long)rows * d;
+  for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < n;
+       k += (long long)gridDim.x * blockDim.x) {
+    const long long r = k / d;
+    const int c = (int)(k - r * d);
+    dst.at(g)[r * dst.ld + c] = src.at(g)[r * src.ld + c] * drop_val(m, g, r, c);
+  }
+}
+
+void launch_mask_copy(int G, int rows, int d, Mat dst, Mat src, const DropMask& m,
+                      const int* active, cudaStream_t s) {
+  if (G == 0 || rows == 0) return;
+  const long long n = (long long)rows * d;
+  const int blocks = (int)std::min<long long>((n + 255) / 256, 148 * 8);
+  mask_copy_kernel<<<dim3(blocks, G), 256, 0, s>>>(rows, d, dst, src, m, active);
+  MGLP_CUDA(cudaGetLastError());
 }
 
 void launch_correct(int G, long long n, Mat dst, Mat a, Mat b, const int* active,

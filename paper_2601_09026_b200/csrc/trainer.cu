@@ -251,7 +251,7 @@ struct Reader {
 Trainer::Trainer(const StackDesc& sd, const SolveCfg& solve, int vocab, int max_seq,
                  const TaskDesc& task, const OptDesc& opt, int batch_size, uint64_t seed,
                  int device)
-    : sd_(sd), task_(task), opt_(opt) {
+    : sd_(sd), task_(task), opt_(opt), seed_(seed) {
   if (vocab < 2) throw ValidationError("Model: vocab must be >= 2");
   if (max_seq < 1) throw ValidationError("Model: max_seq must be >= 1");
   if (task.vocab != vocab) throw ValidationError("train: task and model vocabularies differ");
@@ -265,8 +265,6 @@ Trainer::Trainer(const StackDesc& sd, const SolveCfg& solve, int vocab, int max_
   if (opt.beta1 < 0.0 || opt.beta1 >= 1.0 || opt.beta2 < 0.0 || opt.beta2 >= 1.0)
     throw ValidationError("Optimizer: betas must lie in [0, 1)");
   if (opt.eps <= 0.0) throw ValidationError("Optimizer: eps must be positive");
-  if (sd.dropout != 0.0)
-    throw ValidationError("device trainer: dropout > 0 is not supported (frozen masks: next row)");
   V_ = vocab;
   S_ = max_seq;
   B_ = batch_size;
@@ -668,6 +666,8 @@ void Trainer::optimizer_step() {
 double Trainer::update(long long k, bool parallel, bool apply) {
   MGLP_CUDA(cudaSetDevice(eng_->device()));
   make_batch(0, k * B_);
+  // frozen masks of batch k (training.cpp:209-210); no-op without dropout
+  eng_->refresh_dropout(seed_, (uint64_t)k);
   embed();
   Engine& e = *eng_;
   if (parallel)
@@ -700,6 +700,7 @@ int Trainer::correct_predictions() {
 
 double Trainer::evaluate() {
   MGLP_CUDA(cudaSetDevice(eng_->device()));
+  eng_->clear_dropout();  // the exact map (training.cpp:296-300)
   const int vb = task_.val_size / B_;
   double acc = 0.0;
   Engine& e = *eng_;

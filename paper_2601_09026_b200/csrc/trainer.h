@@ -88,6 +88,7 @@ class Trainer {
   StackDesc sd_;
   TaskDesc task_;
   OptDesc opt_;
+  uint64_t seed_ = 0;  // TrainConfig::seed: model init and dropout streams
   int V_, S_, B_, T_, d_, ldv_;
   bool two_stream_;
   std::unique_ptr<Engine> eng_;

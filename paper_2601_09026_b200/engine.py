@@ -149,6 +149,8 @@ class LayerStack:
         self._params = np.empty(self._np, np.float64)
         N.call("mglp_engine_init_params", self._eng.h, C.c_ulonglong(seed), N.dptr(self._params))
         self.version = 0
+        self._dropout = None        # (seed, batch_index, batch, s_x, s_y) of the live masks
+        self.dropout_version = 0
 
     # ---- accessors (blocks.hpp:124-134) ----
     def config(self):
@@ -193,6 +195,19 @@ class LayerStack:
         self._params = flat.copy()
         N.call("mglp_engine_set_params", self._eng.h, N.dptr(self._params), self._np)
         self.version += 1
+
+    # ---- dropout (blocks.cpp:576-599) ----
+    def refresh_dropout(self, seed: int, batch_index: int, batch: int, s_x: int, s_y: int):
+        """Frozen masks of one batch for every layer (no-op if dropout <= 0)."""
+        N.call("mglp_engine_refresh_dropout", self._eng.h, C.c_ulonglong(seed),
+               C.c_ulonglong(batch_index), batch, s_x, s_y)
+        self._dropout = (seed, batch_index, batch, s_x, s_y)
+        self.dropout_version += 1
+
+    def clear_dropout(self):
+        N.call("mglp_engine_clear_dropout", self._eng.h)
+        self._dropout = None
+        self.dropout_version += 1
 
     def zero_grads(self) -> np.ndarray:
         return np.zeros(self._np, np.float64)
@@ -247,6 +262,7 @@ class LayerParallelEngine:
         self._cfg = cfg
         self._eng = _Handle(_open_engine(stack.cfg, cfg, stack.device if device is None else device))
         self._synced = -1
+        self._drop_synced = 0
         self._traj_key = None
 
     def _sync(self):
@@ -254,6 +270,15 @@ class LayerParallelEngine:
             p = np.ascontiguousarray(self.stack._params)
             N.call("mglp_engine_set_params", self._eng.h, N.dptr(p), p.size)
             self._synced = self.stack.version
+        if self._drop_synced != self.stack.dropout_version:
+            # the stack's frozen masks (the reference engine reads them from the stack)
+            if self.stack._dropout is not None:
+                seed, k, b, sx, sy = self.stack._dropout
+                N.call("mglp_engine_refresh_dropout", self._eng.h, C.c_ulonglong(seed),
+                       C.c_ulonglong(k), b, sx, sy)
+            else:
+                N.call("mglp_engine_clear_dropout", self._eng.h)
+            self._drop_synced = self.stack.dropout_version
         N.call("mglp_engine_set_config", self._eng.h, C.byref(self._cfg.desc()))
 
     def config(self) -> SolveConfig:
