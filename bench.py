@@ -317,14 +317,24 @@ def run_device(args, cfg, rank, world, dist):
     for _ in range(args.warmup):
         step()
     N.call("mglp_engine_sync", h)
-    use_graph = not args.no_graph and world == 1
+    use_graph = not args.no_graph
+    graph_note = None
     if use_graph:
-        # the whole step (both solves, ~10^3 kernels) as one CUDA graph launch
-        N.call("mglp_engine_graph_capture", h, C.c_void_p(z0.data_ptr()),
-               C.c_void_p(lam.data_ptr()), C.c_void_p(lam0.data_ptr()), 1)
-        for _ in range(2):
-            N.call("mglp_engine_graph_replay", h)
-        N.call("mglp_engine_sync", h)
+        # the whole step (both solves, ~10^3 kernels, and with N > 1 the NCCL
+        # boundary exchanges, which NCCL records into the graph) as one launch;
+        # any capture failure falls back to eager launches (same op order on
+        # every rank, so mixed ranks still match)
+        try:
+            N.call("mglp_engine_graph_capture", h, C.c_void_p(z0.data_ptr()),
+                   C.c_void_p(lam.data_ptr()), C.c_void_p(lam0.data_ptr()), 1)
+            for _ in range(2):
+                N.call("mglp_engine_graph_replay", h)
+            N.call("mglp_engine_sync", h)
+        except Exception as ex:  # noqa: BLE001 -- reported in the JSON line
+            use_graph = False
+            graph_note = f"graph capture failed, eager: {ex}"
+            log(graph_note)
+            N.call("mglp_engine_sync", h)
     eager_step = step
     if use_graph:
         def step():  # noqa: F811
@@ -482,7 +492,8 @@ def run_device(args, cfg, rank, world, dist):
                    "l2": "working set (states + activation cache, GBs) >> 126 MB L2",
                    "gemm_precision": "tcgen05 kind::f16 3-pass split (hi + 2^-11 lo', ~22-bit operands), "
                                      "fp32 accumulate",
-                   "launch": "CUDA graph of the whole step" if use_graph else "eager"},
+                   "launch": "CUDA graph of the whole step" if use_graph else
+                             (graph_note or "eager")},
         "speedup_vs_serial": serial_ms / ms,
         "monitor_probe_ms_per_step": probe_ms,
         "monitor_probe_budget": f"fwd={2 * f0} bwd={2 * b0} (ProbeScope doubling, eager launch)",
