@@ -108,31 +108,47 @@ __device__ __forceinline__ void probs(float* v, int q, int key0, int skv, bool c
 }
 
 // ---- forward -----------------------------------------------------------------------
-// tiles: t0 = Q, t1 = K, t2 = V, t4 = P (pair128); TMEM: S [0,256), O [256,..)/[384,..)
+// smem (no staging: TMA lands fp32 in a tile region, converted in place):
+//   Q | K[2] | V[2] | P (pair128); K and V double-buffered so the next block's
+//   load is in flight while the current one computes.
+// TMEM: S [0,256), O [256,..)/[384,..)
+constexpr int kFwdLongSmem = 1024 + 5 * PAIR64 + PAIR128 + 8 * 8 + 256 * 4 + 16;
+
 __global__ void __launch_bounds__(kThreads, 1)
     attn_fwd_long_kernel(const __grid_constant__ AttnTma tm, const AttnArgs a, const int* active) {
   extern __shared__ uint8_t smem_raw[];
   if (active && *(volatile const int*)active == 0) return;
-  const LongSmem L = carve(smem_raw);
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  const uint32_t base = smem_u32(smem);
+  const uint32_t tQ = base, tK[2] = {base + PAIR64, base + 2 * PAIR64},
+                 tV[2] = {base + 3 * PAIR64, base + 4 * PAIR64}, tP = base + 5 * PAIR64;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 5 * PAIR64 + PAIR128);
+  uint64_t* bQ = &bars[0];
+  uint64_t* bK = &bars[1];  // [2]
+  uint64_t* bV = &bars[3];  // [2]
+  uint64_t* bM = &bars[5];
+  float* xch = reinterpret_cast<float*>(bars + 8);
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(xch + 256);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int q4 = warp & 3, half = warp >> 2, c0 = half * 64;
   const int sq = a.sq, skv = a.skv, dh = a.dh;
   const int nqb = (sq + 127) >> 7, nkb = (skv + 127) >> 7;
   const int nprob = a.G * a.Bb * a.H * nqb;
-  const Opnd Qk = pair64(L.t0, false), Kk = pair64(L.t1, false), Vm = pair64(L.t2, true);
-  const Opnd Pk = pair128(L.t4, false);
+  const uint32_t box = (uint32_t)(128 * dh * 4);
+  const Opnd Qk = pair64(tQ, false), Pk = pair128(tP, false);
   if (tid == 0) {
-    mbar_init(&L.bars[0], 1);
-    mbar_init(&L.bars[1], 1);
+    for (int i = 0; i < 6; ++i) mbar_init(&bars[i], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == 0) tmem_alloc(L.tslot, 512);
+  if (warp == 0) tmem_alloc(tslot, 512);
   sync_all();
-  const uint32_t tmem = *L.tslot;
+  const uint32_t tmem = *tslot;
   const uint32_t trow = tmem + ((uint32_t)(q4 * 32) << 16);
   const int i = q4 * 32 + lane;
   float amax = 0.f;
-  Phase ph;
+  // completed-load counts per buffer (-> mbarrier phases), identical in every thread
+  uint32_t nq = 0, nk[2] = {0, 0}, nv[2] = {0, 0}, nm = 0;
   auto coords = [&](int z, int& g, int& b, int& h, int& qb) {
     qb = z % nqb;
     int r = z / nqb;
@@ -141,105 +157,113 @@ __global__ void __launch_bounds__(kThreads, 1)
     b = r % a.Bb;
     g = r / a.Bb;
   };
+  auto load = [&](uint32_t dst, uint64_t* bar, int which, int g, int b, int h, int row0) {
+    mbar_expect_tx(bar, box);
+    tma_box(dst, tm, which, g, b, h, bar, row0);
+  };
+  auto mma_wait = [&]() {
+    mbar_wait(bM, nm & 1);
+    ++nm;
+    tc_after();
+  };
   if (tid == 0 && (int)blockIdx.x < nprob) {
     int g, b, h, qb;
     coords(blockIdx.x, g, b, h, qb);
-    issue(L, tm, TQ, g, b, h, qb * 128, dh);
+    load(tQ, bQ, TQ, g, b, h, qb * 128);
+    load(tK[0], &bK[0], TK, g, b, h, 0);
   }
   for (int z = blockIdx.x; z < nprob; z += gridDim.x) {
     int g, b, h, qb;
     coords(z, g, b, h, qb);
     const int q = qb * 128 + i;  // this thread's query
     const int kend = a.causal ? min(nkb, qb + 1) : nkb;
-    wait_stage(L, ph);
-    conv_rows(L.stg, 128, 128, dh, Qk.hi, Qk.lo, tid, kThreads, amax);
-    fence_async_smem();
-    sync_all();
-    if (tid == 0) issue(L, tm, TK, g, b, h, 0, dh);
-    // ---- pass A: row statistics (online max / sum of exp) ----
-    float m = -INFINITY, l = 0.f;
-    for (int kb = 0; kb < kend; ++kb) {
-      wait_stage(L, ph);
-      conv_rows(L.stg, 128, 128, dh, Kk.hi, Kk.lo, tid, kThreads, amax);
+    mbar_wait(bQ, nq & 1);
+    ++nq;
+    conv_inplace(tQ, 128, 128, dh, tid, kThreads, amax);
+    float m = -INFINITY, l = 0.f, inv = 0.f;
+    // steps 0..kend-1: pass A (row statistics); kend..2 kend-1: pass B
+    for (int st = 0; st < 2 * kend; ++st) {
+      const bool pb = st >= kend;
+      const int kb = pb ? st - kend : st, kbuf = st & 1;
+      mbar_wait(&bK[kbuf], nk[kbuf] & 1);
+      ++nk[kbuf];
+      conv_inplace(tK[kbuf], 128, 128, dh, tid, kThreads, amax);
       fence_async_smem();
       sync_all();
       if (tid == 0) {
-        // next K block, or K_0 again for pass B
-        issue(L, tm, TK, g, b, h, (kb + 1 < kend ? kb + 1 : 0) * 128, dh);
-        mma3(tmem, tmem + 128, Qk, Kk, 128, dh >> 4);
-        mma_commit<1>(&L.bars[1]);
-      }
-      mma_done(L, ph);
-      float v[64];
-      read64(trow, c0, v);
-      const int lim = key_limit(q, kb * 128 + c0, skv, a.causal != 0, true);
-      float mh = -INFINITY;
-#pragma unroll
-      for (int e = 0; e < 64; ++e) {
-        v[e] = e < lim ? v[e] * a.scale : -INFINITY;
-        mh = fmaxf(mh, v[e]);
-      }
-      L.xch[half * 128 + i] = mh;
-      sync_all();
-      const float mb = fmaxf(L.xch[i], L.xch[128 + i]);
-      const float mn = fmaxf(m, mb);
-      float sh = 0.f;
-      if (mn != -INFINITY) {
-#pragma unroll
-        for (int e = 0; e < 64; ++e) sh += v[e] == -INFINITY ? 0.f : fast_exp(v[e] - mn);
-      }
-      sync_all();
-      L.xch[half * 128 + i] = sh;
-      sync_all();
-      if (mn != -INFINITY) {
-        const float sc = m == -INFINITY ? 0.f : fast_exp(m - mn);
-        l = l * sc + (L.xch[i] + L.xch[128 + i]);
-        m = mn;
-      }
-      sync_all();  // S consumed, K tile free
-    }
-    const float inv = l > 0.f ? 1.f / l : 0.f;
-    // ---- pass B: P = exp(S*scale - m) / l, O += P V ----
-    for (int kb = 0; kb < kend; ++kb) {
-      wait_stage(L, ph);
-      conv_rows(L.stg, 128, 128, dh, Kk.hi, Kk.lo, tid, kThreads, amax);
-      fence_async_smem();
-      sync_all();
-      if (tid == 0) {
-        issue(L, tm, TV, g, b, h, kb * 128, dh);
-        mma3(tmem, tmem + 128, Qk, Kk, 128, dh >> 4);
-        mma_commit<1>(&L.bars[1]);
-      }
-      wait_stage(L, ph);
-      conv_rows(L.stg, 128, 128, dh, Vm.hi, Vm.lo, tid, kThreads, amax);
-      fence_async_smem();
-      mma_done(L, ph);
-      float v[64];
-      read64(trow, c0, v);
-      probs(v, q, kb * 128 + c0, skv, a.causal != 0, q < sq, a.scale, m, inv);
-#pragma unroll
-      for (int c = 0; c < 8; ++c) put8(Pk.hi, Pk.lo, 128, i, half * 8 + c, v + c * 8, amax);
-      fence_async_smem();
-      sync_all();
-      if (tid == 0) {
-        if (kb + 1 < kend)
-          issue(L, tm, TK, g, b, h, (kb + 1) * 128, dh);
-        else if (z + (int)gridDim.x < nprob) {
-          int g2, b2, h2, qb2;
-          coords(z + gridDim.x, g2, b2, h2, qb2);
-          issue(L, tm, TQ, g2, b2, h2, qb2 * 128, dh);
+        // the other K buffer held the block of step st-1, whose S is done
+        if (st + 1 < 2 * kend) {
+          const int nb = st + 1 < kend ? st + 1 : st + 1 - kend;
+          load(tK[(st + 1) & 1], &bK[(st + 1) & 1], TK, g, b, h, nb * 128);
         }
-        mma3(tmem + 256, tmem + 384, Pk, Vm, dh, 8, kb > 0);
-        mma_commit<1>(&L.bars[1]);
+        // V one step ahead: V_0 during the last statistics step, V_kb+1 during pass-B step kb
+        if (st == kend - 1) load(tV[0], &bV[0], TV, g, b, h, 0);
+        if (pb && kb + 1 < kend) load(tV[(kb + 1) & 1], &bV[(kb + 1) & 1], TV, g, b, h, (kb + 1) * 128);
+        mma3(tmem, tmem + 128, Qk, pair64(tK[kbuf], false), 128, dh >> 4);  // S = Q K^T
+        mma_commit<1>(bM);
       }
-      mma_done(L, ph);
+      mma_wait();
+      float v[64];
+      read64(trow, c0, v);
+      if (!pb) {
+        // online (max, sum of exp) of the scaled, masked scores
+        const int lim = key_limit(q, kb * 128 + c0, skv, a.causal != 0, true);
+        float mh = -INFINITY;
+#pragma unroll
+        for (int e = 0; e < 64; ++e) {
+          v[e] = e < lim ? v[e] * a.scale : -INFINITY;
+          mh = fmaxf(mh, v[e]);
+        }
+        xch[half * 128 + i] = mh;
+        sync_all();
+        const float mb = fmaxf(xch[i], xch[128 + i]);
+        const float mn = fmaxf(m, mb);
+        float sh = 0.f;
+        if (mn != -INFINITY) {
+#pragma unroll
+          for (int e = 0; e < 64; ++e) sh += v[e] == -INFINITY ? 0.f : fast_exp(v[e] - mn);
+        }
+        sync_all();
+        xch[half * 128 + i] = sh;
+        sync_all();
+        if (mn != -INFINITY) {
+          const float sc = m == -INFINITY ? 0.f : fast_exp(m - mn);
+          l = l * sc + (xch[i] + xch[128 + i]);
+          m = mn;
+        }
+        if (st == kend - 1) inv = l > 0.f ? 1.f / l : 0.f;
+        sync_all();  // xch reads done; S consumed
+      } else {
+        // P = exp(S*scale - m) / l -> tile; O += P V
+        const int vbuf = kb & 1;
+        mbar_wait(&bV[vbuf], nv[vbuf] & 1);
+        ++nv[vbuf];
+        conv_inplace(tV[vbuf], 128, 128, dh, tid, kThreads, amax);
+        probs(v, q, kb * 128 + c0, skv, a.causal != 0, q < sq, a.scale, m, inv);
+#pragma unroll
+        for (int c = 0; c < 8; ++c) put8(Pk.hi, Pk.lo, 128, i, half * 8 + c, v + c * 8, amax);
+        fence_async_smem();
+        sync_all();
+        if (tid == 0) {
+          mma3(tmem + 256, tmem + 384, Pk, pair64(tV[vbuf], true), dh, 8, kb > 0);
+          mma_commit<1>(bM);
+        }
+        mma_wait();
+      }
+    }
+    // Q and both K buffers are free: the next problem's first loads overlap the epilogue
+    if (tid == 0 && z + (int)gridDim.x < nprob) {
+      int g2, b2, h2, qb2;
+      coords(z + gridDim.x, g2, b2, h2, qb2);
+      load(tQ, bQ, TQ, g2, b2, h2, qb2 * 128);
+      load(tK[0], &bK[0], TK, g2, b2, h2, 0);
     }
     rows_out(trow + 256, trow + 384, a.O.at(g, b, h) + (long long)qb * 128 * a.O.ld, a.O.ld, i,
              sq - qb * 128, half * (dh >> 1), dh >> 1, 1.f);
     if (half == 0 && q < sq) {
-      float* st = a.P.at(g, b, h) + 2LL * q;
-      st[0] = m;
-      st[1] = inv;
+      float* stp = a.P.at(g, b, h) + 2LL * q;
+      stp[0] = m;
+      stp[1] = inv;
     }
     sync_all();
   }
@@ -495,10 +519,10 @@ int sms() {
 
 template <typename K>
 void launch_long(K kernel, const AttnTma& t, const AttnArgs& a, long long nprob, const int* active,
-                 cudaStream_t s) {
+                 cudaStream_t s, int smem = kLongSmem) {
   if (nprob == 0) return;
   const int grid = (int)std::min<long long>(nprob, sms());
-  kernel<<<grid, kThreads, kLongSmem, s>>>(t, a, active);
+  kernel<<<grid, kThreads, smem, s>>>(t, a, active);
   MGLP_CUDA(cudaGetLastError());
 }
 
@@ -519,12 +543,12 @@ void launch_attn_fwd_long(const AttnArgs& a, const int* active, cudaStream_t s) 
   if (!attn_long_supported(a, false)) throw ContractViolation("attn_fwd_long: unsupported shape");
   static bool attr = [] {
     MGLP_CUDA(cudaFuncSetAttribute(attn_fwd_long_kernel,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, kLongSmem));
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, kFwdLongSmem));
     return true;
   }();
   (void)attr;
   launch_long(attn_fwd_long_kernel, long_maps(a, false), a,
-              (long long)a.G * a.Bb * a.H * ((a.sq + 127) / 128), active, s);
+              (long long)a.G * a.Bb * a.H * ((a.sq + 127) / 128), active, s, kFwdLongSmem);
 }
 
 void launch_attn_bwd_long(const AttnArgs& a, const int* active, cudaStream_t s) {
