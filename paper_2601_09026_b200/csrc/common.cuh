@@ -162,9 +162,9 @@ __device__ __forceinline__ float4 combine_apply4(const Combine& c, int g, long l
 enum EpiKind : int {
   EPI_STORE = 0,      // out1 = acc (+ bias)
   EPI_BIAS_ADD2 = 1,  // a = acc + bias; o1 = add1 ? add1 + a : a -> out1; out2 = add2 + o1
-  EPI_BIAS_GELU = 2,  // h = acc + bias -> out1; gelu(h) -> out2
+  EPI_BIAS_GELU = 2,  // h = acc + bias: gelu'(h) -> out1 (for the VJP), gelu(h) -> out2
   EPI_FINAL = 3,      // mo = acc + bias; F = add1 + mo; p = z + dt*F; combine
-  EPI_GELU_BWD = 4,   // out1 = acc * gelu'(aux)            (tensor.cpp:360-372)
+  EPI_GELU_BWD = 4,   // out1 = acc * aux, aux = gelu'(h)   (tensor.cpp:360-372)
   EPI_GRAD_ACC = 5,   // out1 += gscale * acc               (blocks.cpp:108, 126-129)
 };
 
@@ -217,11 +217,14 @@ __device__ __forceinline__ float gelu_s(float v) {
 
 __device__ __forceinline__ float gelu_f(float v) { return v * gelu_s(v); }
 
-__device__ __forceinline__ float gelu_grad_f(float v, float up) {
-  const float s = gelu_s(v);
+// gelu'(v) given s = gelu_s(v); the backward multiplies it into the upstream
+// (up * gelu'(v), tensor.cpp:360-372), so storing gelu'(v) in the forward
+// instead of v gives the bitwise-same VJP
+__device__ __forceinline__ float gelu_deriv_s(float v, float s) {
   const float ds = 2.f * s * (1.f - s) * kGeluC * fmaf(3.f * kGeluA * v, v, 1.f);
-  return up * fmaf(v, ds, s);
+  return fmaf(v, ds, s);
 }
+__device__ __forceinline__ float gelu_grad_f(float v, float up) { return up * gelu_deriv_s(v, gelu_s(v)); }
 
 // Applies the epilogue to n consecutive columns [col0, col0+n) of one output
 // row. Returns this row-segment's contribution to the residual norm^2.
@@ -280,8 +283,9 @@ __device__ __forceinline__ double epilogue_rowv(const EpiArgs& e, int g, int b, 
     case EPI_BIAS_GELU: {
 #pragma unroll
       for (int i = 0; i < W; ++i) {
-        o[i] = acc[i] + bv[i];
-        t1[i] = gelu_f(o[i]);
+        const float hv = acc[i] + bv[i], sv = gelu_s(hv);
+        t1[i] = hv * sv;
+        o[i] = gelu_deriv_s(hv, sv);
       }
       if (e.out1.ok()) st4(e.out1.at(g) + (long long)row * e.out1.ld + col0, o);
       st4(e.out2.at(g) + (long long)row * e.out2.ld + col0, t1);
@@ -289,7 +293,7 @@ __device__ __forceinline__ double epilogue_rowv(const EpiArgs& e, int g, int b, 
     case EPI_GELU_BWD: {
       ld4(e.aux.at(g) + (long long)row * e.aux.ld + col0, t1);
 #pragma unroll
-      for (int i = 0; i < W; ++i) o[i] = gelu_grad_f(t1[i], acc[i]);
+      for (int i = 0; i < W; ++i) o[i] = acc[i] * t1[i];
       st4(e.out1.at(g) + (long long)row * e.out1.ld + col0, o);
     } break;
     case EPI_GRAD_ACC: {
@@ -358,9 +362,13 @@ __device__ __forceinline__ double epilogue_4x4(const EpiArgs& e, int g, int b, i
       for (int i = 0; i < 4; ++i) {
         if (rows[i] < 0) continue;
         const float4 hv = add(acc[i], bv);
-        if (e.out1.ok()) st4g(e.out1.at(g) + (long long)rows[i] * e.out1.ld + col, hv);
+        const float4 sv = make_float4(gelu_s(hv.x), gelu_s(hv.y), gelu_s(hv.z), gelu_s(hv.w));
+        if (e.out1.ok())
+          st4g(e.out1.at(g) + (long long)rows[i] * e.out1.ld + col,
+               make_float4(gelu_deriv_s(hv.x, sv.x), gelu_deriv_s(hv.y, sv.y),
+                           gelu_deriv_s(hv.z, sv.z), gelu_deriv_s(hv.w, sv.w)));
         st4g(e.out2.at(g) + (long long)rows[i] * e.out2.ld + col,
-             make_float4(gelu_f(hv.x), gelu_f(hv.y), gelu_f(hv.z), gelu_f(hv.w)));
+             make_float4(hv.x * sv.x, hv.y * sv.y, hv.z * sv.z, hv.w * sv.w));
       }
     } break;
     case EPI_GELU_BWD: {
@@ -372,8 +380,7 @@ __device__ __forceinline__ double epilogue_4x4(const EpiArgs& e, int g, int b, i
         if (rows[i] < 0) continue;
         const float4 a = acc[i], v = x1[i];
         st4g(e.out1.at(g) + (long long)rows[i] * e.out1.ld + col,
-             make_float4(gelu_grad_f(v.x, a.x), gelu_grad_f(v.y, a.y), gelu_grad_f(v.z, a.z),
-                         gelu_grad_f(v.w, a.w)));
+             make_float4(a.x * v.x, a.y * v.y, a.z * v.z, a.w * v.w));
       }
     } break;
     case EPI_GRAD_ACC: {
@@ -463,8 +470,9 @@ __device__ __forceinline__ double epilogue_row(const EpiArgs& e, int g, int b, i
       float* o2 = e.out2.at(g) + (long long)row * e.out2.ld + col0;
       for (int i = 0; i < n; ++i) {
         const float hv = bias ? acc[i] + bias[col0 + i] : acc[i];
-        if (o1) o1[i] = hv;
-        o2[i] = gelu_f(hv);
+        const float sv = gelu_s(hv);
+        if (o1) o1[i] = gelu_deriv_s(hv, sv);
+        o2[i] = hv * sv;
       }
     } break;
     case EPI_FINAL: {
@@ -480,8 +488,8 @@ __device__ __forceinline__ double epilogue_row(const EpiArgs& e, int g, int b, i
     } break;
     case EPI_GELU_BWD: {
       float* o = e.out1.at(g) + (long long)row * e.out1.ld + col0;
-      const float* hv = e.aux.at(g) + (long long)row * e.aux.ld + col0;
-      for (int i = 0; i < n; ++i) o[i] = gelu_grad_f(hv[i], acc[i]);
+      const float* dv = e.aux.at(g) + (long long)row * e.aux.ld + col0;
+      for (int i = 0; i < n; ++i) o[i] = acc[i] * dv[i];
     } break;
     case EPI_GRAD_ACC: {
       float* o = e.out1.at(g) + (long long)row * e.out1.ld + col0;

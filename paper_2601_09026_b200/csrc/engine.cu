@@ -1048,7 +1048,7 @@ void Engine::encoder_forward(const EvalSpec& e, int R, bool causal, Mat X, Mat Y
   g.B = par(L.w_in, d, l0, ls);
   g.Bhl = par_hl(L, L.w_in, l0, ls, false);
   g.ep.kind = EPI_BIAS_GELU;
-  if (keep_lin(e)) g.ep.out1 = hh;  // pre-activation: only the backward reads it
+  if (keep_lin(e)) g.ep.out1 = hh;  // gelu'(h): only the backward reads it
   g.ep.out2 = gg;
   g.ep.bias = par(L.b_in, 0, l0, ls);
   gemm(g);
@@ -1200,7 +1200,7 @@ void Engine::decoder_forward(const EvalSpec& e) {
 
   g = mk(R, f, d, n2, L.w_in, d);
   g.ep.kind = EPI_BIAS_GELU;
-  if (keep_lin(e)) g.ep.out1 = hh;  // pre-activation: only the backward reads it
+  if (keep_lin(e)) g.ep.out1 = hh;  // gelu'(h): only the backward reads it
   g.ep.out2 = gg;
   g.ep.bias = par(L.b_in, 0, l0, ls);
   gemm(g);
