@@ -212,7 +212,11 @@ constexpr float kGeluA = 0.044715f;            // tensor.cpp:346
 // gives s = 0, the exact limit).
 __device__ __forceinline__ float gelu_s(float v) {
   const float u = kGeluC * fmaf(kGeluA * v * v, v, v);
-  return __fdividef(1.f, 1.f + expf(-2.f * u));  // 1 + e >= 1: the fast reciprocal is exact to 2 ulp
+  // exp(-2u) = 2^(-2u log2 e) on the SFU (ex2.approx: ~2 ulp, plus the
+  // rounding of the scaled argument; s = 1/(1+e) stays within ~1e-6 relative)
+  float e;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(u * -2.8853900817779268f));
+  return __fdividef(1.f, 1.f + e);  // 1 + e >= 1: the fast reciprocal is exact to 2 ulp
 }
 
 __device__ __forceinline__ float gelu_f(float v) { return v * gelu_s(v); }
