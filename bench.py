@@ -222,6 +222,7 @@ def run_reference_arm(args, cfg, rank, world):
                    f"cf={cfg['cf']} levels={cfg['levels']} fwd={cfg['fwd']} bwd={cfg['bwd']}"},
         "serial_ms": statistics.median(s["serial_ms"] for s in samples),
         "cpu_baseline": {"value": ms, "unit": "ms/iteration", "cores": threads,
+                         "measured_threads": 1,
                          "kind": "reference", "sample": s0["sample"]},
         "e2e": {"value": ms, "unit": "ms/iteration", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
@@ -473,6 +474,7 @@ def run_device(args, cfg, rank, world, dist):
                 threads = max(1, min(os.cpu_count() or 1, cfg["n_enc"] + cfg["n_dec"]))
                 s = reference_sample(cfg, threads)
                 cpu = {"value": s["ms"], "unit": "ms/iteration", "cores": threads,
+                       "measured_threads": 1,
                        "kind": "reference", "sample": s["sample"],
                        "serial_ms": s["serial_ms"]}
         except Exception as ex:  # reported, never fatal
