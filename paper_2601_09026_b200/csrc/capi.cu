@@ -174,7 +174,7 @@ extern "C" {
 const char* mglp_last_error(void) { return g_err.c_str(); }
 
 const char* mglp_version(void) {
-  return "mglp-b200 sm_100a tcgen05 kind::tf32 x3 (fp32 accumulate)";
+  return "mglp-b200 sm_100a tcgen05 kind::f16 3-pass hi/lo split (fp32 accumulate)";
 }
 
 mglp_status mglp_engine_create(const mglp_stack_desc* stack, const mglp_solve_config* solve,

@@ -506,7 +506,7 @@ __device__ __forceinline__ double epilogue_row(const EpiArgs& e, int g, int b, i
 // GEMM problem family: for g < G, C_g[M,N] = A_g . B_g^T with
 //   A_g [M,K] row-major ("K-major") or, if a_mn, stored [K,M] ("MN-major");
 //   B_g [N,K] row-major, or if b_mn stored [K,N].
-// B may come pre-split into tf32 hi/lo parts (weights); see gemm_tc.cu.
+// B may come pre-split into fp16 hi/lo' parts (weights); see gemm_tc.cu.
 struct GemmArgs {
   int G = 1, M = 0, N = 0, K = 0;
   // each of the G members may itself be a Bb x H grid of per-(batch, head)
