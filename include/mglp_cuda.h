@@ -224,7 +224,8 @@ mglp_status mglp_rng_gaussian_fill(unsigned long long seed, unsigned long long a
  * lda; [M,K] or, if a_mn, [K,M]); B likewise ([N,K] or [K,N]); C at
  * C + g*c_slot, row stride ldc. engine 0 = tcgen05 fp16x3 split (the
  * product kernel), 1 = fp32 CUDA-core reference. b_presplit exercises the
- * pre-split (hi|lo) weight path of the tensor-core kernel. range_flag
+ * pre-split (hi|lo) weight path of the tensor-core kernel (bit 1 set: a
+ * K-major A is pre-split too -- the converter-free mainloop). range_flag
  * (nullable) receives 1 if a finite operand overflowed the fp16 split
  * range. Synchronous. */
 mglp_status mglp_test_gemm(int G, int M, int N, int K, const float* A, long long a_slot, int lda,

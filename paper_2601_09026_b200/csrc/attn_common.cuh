@@ -194,6 +194,30 @@ __device__ __forceinline__ void rows_out(uint32_t tmain, uint32_t tcor, float* o
   }
 }
 
+// the forward O rows: fp32 (out, nullable) and/or pre-split hi|lo' (hl,
+// nullable; the O-projection GEMM's A operand, common.cuh st_hl4). hl follows
+// out's strides; the head's column offset must be a multiple of 32 so the
+// fp32 offset of the head equals its packed byte offset.
+__device__ __forceinline__ void rows_out_o(uint32_t tmain, uint32_t tcor, float* out, float* hl,
+                                           long long ld, int row, int nvalid, int c0, int nc,
+                                           float& amax) {
+#pragma unroll
+  for (int c = 0; c < 32; c += 16) {
+    if (c < nc) {
+      float v[16];
+      tmem_pair16(tmain + c0 + c, tcor + c0 + c, v);
+      if (row < nvalid) {
+#pragma unroll
+        for (int e = 0; e < 16; e += 4) {
+          const float4 x = make_float4(v[e], v[e + 1], v[e + 2], v[e + 3]);
+          if (out) *reinterpret_cast<float4*>(out + row * ld + c0 + c + e) = x;
+          if (hl) st_hl4(hl + row * ld, c0 + c + e, x, amax);
+        }
+      }
+    }
+  }
+}
+
 __device__ __forceinline__ void problem_of(const AttnArgs& a, int z, int& g, int& b, int& h) {
   h = z % a.H;
   b = (z / a.H) % a.Bb;

@@ -258,8 +258,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       load(tQ, bQ, TQ, g2, b2, h2, qb2 * 128);
       load(tK[0], &bK[0], TK, g2, b2, h2, 0);
     }
-    rows_out(trow + 256, trow + 384, a.O.at(g, b, h) + (long long)qb * 128 * a.O.ld, a.O.ld, i,
-             sq - qb * 128, half * (dh >> 1), dh >> 1, 1.f);
+    {
+      const long long ld = a.Ohl.ok() ? a.Ohl.ld : a.O.ld;
+      rows_out_o(trow + 256, trow + 384,
+                 a.O.ok() ? a.O.at(g, b, h) + (long long)qb * 128 * ld : nullptr,
+                 a.Ohl.ok() ? a.Ohl.at(g, b, h) + (long long)qb * 128 * ld : nullptr, ld, i,
+                 sq - qb * 128, half * (dh >> 1), dh >> 1, amax);
+    }
     if (half == 0 && q < sq) {
       float* stp = a.P.at(g, b, h) + 2LL * q;
       stp[0] = m;

@@ -181,7 +181,9 @@ __global__ void __launch_bounds__(kThreads, 2) attn_fwd_kernel(const __grid_cons
     tc_after();
     // the tiles are free: the next problem's loads overlap this epilogue
     if (tid == 0 && z + (int)gridDim.x < nprob) issue_loads(z + gridDim.x);
-    rows_out(trow, trow + 128, a.O.at(g, b, h), a.O.ld, i, sq, half * (dh >> 1), dh >> 1, 1.f);
+    rows_out_o(trow, trow + 128, a.O.ok() ? a.O.at(g, b, h) : nullptr,
+               a.Ohl.ok() ? a.Ohl.at(g, b, h) : nullptr, a.Ohl.ok() ? a.Ohl.ld : a.O.ld, i, sq,
+               half * (dh >> 1), dh >> 1, amax);
     tc_before();
     __syncthreads();  // TMEM free for the next problem
   }

@@ -739,6 +739,7 @@ mglp_status mglp_test_gemm(int G, int M, int N, int K, const float* A, long long
     MGLP_CUDA(cudaMalloc(&dflag, sizeof(int)));
     MGLP_CUDA(cudaMemset(dflag, 0, sizeof(int)));
     g.range_flag = dflag;
+    float* ahl = nullptr;
     if (b_presplit && engine == 0) {
       const long long kp = pack_hl_cols(K);
       MGLP_CUDA(cudaMalloc(&hl, (size_t)G * N * kp * sizeof(float)));
@@ -746,6 +747,13 @@ mglp_status mglp_test_gemm(int G, int M, int N, int K, const float* A, long long
       g.Bhl.ptr = hl;
       g.Bhl.slot_stride = (long long)N * kp;
       g.Bhl.ld = (int)kp;
+      if ((b_presplit & 2) && !a_mn) {  // A pre-split too: the converter-free mainloop
+        MGLP_CUDA(cudaMalloc(&ahl, (size_t)G * M * kp * sizeof(float)));
+        launch_pack_hl(A, a_slot, lda, ahl, (long long)M * kp, (int)kp, G, M, K, false, 0);
+        g.Ahl.ptr = ahl;
+        g.Ahl.slot_stride = (long long)M * kp;
+        g.Ahl.ld = (int)kp;
+      }
     }
     if (engine == 0)
       launch_gemm_tc(g, nullptr, 0);
@@ -754,6 +762,7 @@ mglp_status mglp_test_gemm(int G, int M, int N, int K, const float* A, long long
     MGLP_CUDA(cudaGetLastError());
     MGLP_CUDA(cudaDeviceSynchronize());
     if (hl) cudaFree(hl);
+    if (ahl) cudaFree(ahl);
     int flag = 0;
     MGLP_CUDA(cudaMemcpy(&flag, dflag, sizeof(int), cudaMemcpyDeviceToHost));
     cudaFree(dflag);
@@ -902,6 +911,7 @@ mglp_status mglp_bench_attention(int G, int B, int H, int s, int dh, int causal,
 mglp_status mglp_bench_gemm(int G, int M, int N, int K, int a_mn, int b_mn, int b_presplit,
                             int epi, int reps, float* ms_per_launch) {
   return guard([&] {
+    float* ahl = nullptr;
     float *A = nullptr, *B = nullptr, *Cm = nullptr, *hl = nullptr, *C2 = nullptr,
           *bias = nullptr;
     const long long na = (long long)G * M * K, nb = (long long)G * N * K,
@@ -951,6 +961,14 @@ mglp_status mglp_bench_gemm(int G, int M, int N, int K, int a_mn, int b_mn, int 
       g.Bhl.ptr = hl;
       g.Bhl.slot_stride = (long long)N * kp;
       g.Bhl.ld = (int)kp;
+      if ((b_presplit & 2) && !a_mn) {
+        MGLP_CUDA(cudaMalloc(&ahl, (size_t)G * M * kp * sizeof(float)));
+        launch_pack_hl(A, g.A.slot_stride, g.A.ld, ahl, (long long)M * kp, (int)kp, G, M, K,
+                       false, 0);
+        g.Ahl.ptr = ahl;
+        g.Ahl.slot_stride = (long long)M * kp;
+        g.Ahl.ld = (int)kp;
+      }
     }
     cudaEvent_t e0, e1;
     MGLP_CUDA(cudaEventCreate(&e0));
@@ -965,7 +983,7 @@ mglp_status mglp_bench_gemm(int G, int M, int N, int K, int a_mn, int b_mn, int 
     *ms_per_launch = ms / reps;
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
-    for (float* p : {A, B, Cm, hl, C2, bias})
+    for (float* p : {ahl, A, B, Cm, hl, C2, bias})
       if (p) cudaFree(p);
   });
 }

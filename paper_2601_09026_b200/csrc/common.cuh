@@ -9,6 +9,7 @@
 // (executor.cpp:75-110, mgrit.hpp:125-187): one launch covers every chunk.
 #pragma once
 
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -168,6 +169,36 @@ enum EpiKind : int {
   EPI_GRAD_ACC = 5,   // out1 += gscale * acc               (blocks.cpp:108, 126-129)
 };
 
+// ---- activations produced pre-split for the tensor-core GEMM ----------------
+// Row layout of a hi|lo' buffer (GemmArgs::Ahl / Bhl, gemm_tc.cu): per 32-wide
+// column block 128 bytes = 32 fp16 hi then 32 fp16 lo'. The split is
+// bit-identical to the GEMM converters' (split8), so a GEMM reading it gives
+// exactly the bits of reading the fp32 values. `row` points at the row start.
+__device__ __forceinline__ void st_hl4(float* row, int col, float4 v, float& amax) {
+  const __half2 h01 = __floats2half2_rn(v.x, v.y), h23 = __floats2half2_rn(v.z, v.w);
+  const float2 f01 = __half22float2(h01), f23 = __half22float2(h23);
+  const __half2 l01 = __floats2half2_rn((v.x - f01.x) * 2048.f, (v.y - f01.y) * 2048.f);
+  const __half2 l23 = __floats2half2_rn((v.z - f23.x) * 2048.f, (v.w - f23.y) * 2048.f);
+  amax = fmaxf(amax, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
+  char* b = reinterpret_cast<char*>(row) + (col >> 5) * 128 + (col & 31) * 2;
+  *reinterpret_cast<uint2*>(b) =
+      make_uint2(*reinterpret_cast<const uint32_t*>(&h01), *reinterpret_cast<const uint32_t*>(&h23));
+  *reinterpret_cast<uint2*>(b + 64) =
+      make_uint2(*reinterpret_cast<const uint32_t*>(&l01), *reinterpret_cast<const uint32_t*>(&l23));
+}
+__device__ __forceinline__ void st_hl1(float* row, int col, float v, float& amax) {
+  const __half h = __float2half_rn(v);
+  const __half l = __float2half_rn((v - __half2float(h)) * 2048.f);
+  amax = fmaxf(amax, fabsf(v));
+  __half* b = reinterpret_cast<__half*>(reinterpret_cast<char*>(row) + (col >> 5) * 128) + (col & 31);
+  b[0] = h;
+  b[32] = l;
+}
+// a finite value beyond the fp16 split range (the GEMM converters' flag)
+__device__ __forceinline__ void hl_range_check(float amax, int* flag) {
+  if (flag && amax >= 65520.f && amax <= 3.402823466e38f) atomicOr(flag, 1);
+}
+
 // Frozen dropout masks (blocks.cpp:576-599) as generated by
 // Engine::refresh_dropout: one byte per element (1 = keep) of every (layer,
 // site) [B, s, d] tensor, value 1/keep where kept. The member g of a family
@@ -194,6 +225,10 @@ struct EpiArgs {
   float gscale = 1.f;
   float alpha = 1.f;  // EPI_STORE: out1 = alpha*acc (+ bias)
   Combine cmb;  // EPI_FINAL
+  // EPI_BIAS_GELU: gelu(h) also (or only) as a pre-split hi|lo' buffer for
+  // the next GEMM's A operand (see st_hl4); range_flag for its split
+  Mat hl2;
+  int* range_flag = nullptr;
   // EPI_BIAS_ADD2 / EPI_FINAL: the projection output (acc + bias) is a
   // dropout site (attention output phi1 / phi3, MLP output phi2). Applied by
   // the scalar epilogue_row only: a GEMM with an active mask takes that path
@@ -292,7 +327,15 @@ __device__ __forceinline__ double epilogue_rowv(const EpiArgs& e, int g, int b, 
         o[i] = gelu_deriv_s(hv, sv);
       }
       if (e.out1.ok()) st4(e.out1.at(g) + (long long)row * e.out1.ld + col0, o);
-      st4(e.out2.at(g) + (long long)row * e.out2.ld + col0, t1);
+      if (e.out2.ok()) st4(e.out2.at(g) + (long long)row * e.out2.ld + col0, t1);
+      if (e.hl2.ok()) {
+        float amax = 0.f;
+        float* hr = e.hl2.at(g) + (long long)row * e.hl2.ld;
+#pragma unroll
+        for (int i = 0; i < W; i += 4)
+          st_hl4(hr, col0 + i, make_float4(t1[i], t1[i + 1], t1[i + 2], t1[i + 3]), amax);
+        hl_range_check(amax, e.range_flag);
+      }
     } break;
     case EPI_GELU_BWD: {
       ld4(e.aux.at(g) + (long long)row * e.aux.ld + col0, t1);
@@ -371,8 +414,13 @@ __device__ __forceinline__ double epilogue_4x4(const EpiArgs& e, int g, int b, i
           st4g(e.out1.at(g) + (long long)rows[i] * e.out1.ld + col,
                make_float4(gelu_deriv_s(hv.x, sv.x), gelu_deriv_s(hv.y, sv.y),
                            gelu_deriv_s(hv.z, sv.z), gelu_deriv_s(hv.w, sv.w)));
-        st4g(e.out2.at(g) + (long long)rows[i] * e.out2.ld + col,
-             make_float4(hv.x * sv.x, hv.y * sv.y, hv.z * sv.z, hv.w * sv.w));
+        const float4 gv = make_float4(hv.x * sv.x, hv.y * sv.y, hv.z * sv.z, hv.w * sv.w);
+        if (e.out2.ok()) st4g(e.out2.at(g) + (long long)rows[i] * e.out2.ld + col, gv);
+        if (e.hl2.ok()) {
+          float amax = 0.f;
+          st_hl4(e.hl2.at(g) + (long long)rows[i] * e.hl2.ld, col, gv, amax);
+          hl_range_check(amax, e.range_flag);
+        }
       }
     } break;
     case EPI_GELU_BWD: {
@@ -471,13 +519,17 @@ __device__ __forceinline__ double epilogue_row(const EpiArgs& e, int g, int b, i
     } break;
     case EPI_BIAS_GELU: {
       float* o1 = e.out1.ok() ? e.out1.at(g) + (long long)row * e.out1.ld + col0 : nullptr;
-      float* o2 = e.out2.at(g) + (long long)row * e.out2.ld + col0;
+      float* o2 = e.out2.ok() ? e.out2.at(g) + (long long)row * e.out2.ld + col0 : nullptr;
+      float* hr = e.hl2.ok() ? e.hl2.at(g) + (long long)row * e.hl2.ld : nullptr;
+      float amax = 0.f;
       for (int i = 0; i < n; ++i) {
         const float hv = bias ? acc[i] + bias[col0 + i] : acc[i];
         const float sv = gelu_s(hv);
         if (o1) o1[i] = gelu_deriv_s(hv, sv);
-        o2[i] = hv * sv;
+        if (o2) o2[i] = hv * sv;
+        if (hr) st_hl1(hr, col0 + i, hv * sv, amax);
       }
+      if (hr) hl_range_check(amax, e.range_flag);
     } break;
     case EPI_FINAL: {
       const float* a1 = e.add1.at(g) + (long long)row * e.add1.ld + col0;
@@ -517,6 +569,9 @@ struct GemmArgs {
   // the tensor-core kernel stages (always K-major, [N][pad32(K)] in float
   // units); when set, the tensor-core path reads it instead of B.
   Mat A, B, Bhl;
+  // Ahl (optional, K-major A only, with a pre-split B): A produced in the same
+  // hi|lo' form by the kernel that wrote it -- the mainloop runs converter-free
+  Mat Ahl;
   bool a_mn = false, b_mn = false;
   EpiArgs ep;
   // set to 1 when a finite operand value overflows fp16 (|x| >= 65520)

@@ -142,7 +142,7 @@ Engine::~Engine() {
   free_solver(fwd_);
   free_solver(bwd_);
   if (range_flag_) cudaFree(range_flag_);
-  for (float* p : {P_, Whl_, Gr_, scratch_, cache_, bscratch_, bcache_, traj_, lam_all_,
+  for (float* p : {P_, Whl_, Gr_, scratch_, hlscr_, cache_, bscratch_, bcache_, traj_, lam_all_,
                    zero_state_, snap_fwd_, snap_bwd_})
     if (p) cudaFree(p);
   if (colred_part_) cudaFree(colred_part_);
@@ -404,8 +404,8 @@ void Engine::set_shape(int batch, int s_x, int s_y) {
   free_solver(bwd_);
   if (colred_part_) cudaFree(colred_part_);
   colred_part_ = nullptr;
-  for (float** p : {&scratch_, &cache_, &bscratch_, &bcache_, &traj_, &lam_all_, &zero_state_, &snap_fwd_,
-                    &snap_bwd_}) {
+  for (float** p : {&scratch_, &hlscr_, &cache_, &bscratch_, &bcache_, &traj_, &lam_all_, &zero_state_,
+                    &snap_fwd_, &snap_bwd_}) {
     if (*p) cudaFree(*p);
     *p = nullptr;
   }
@@ -476,6 +476,22 @@ void Engine::set_shape(int batch, int s_x, int s_y) {
   b.size = off;
   const long long cache_slots = eval_only_ ? 1 : total_;
   MGLP_CUDA(cudaMalloc(&scratch_, (size_t)Gmax_ * al_.size * sizeof(float)));
+  {
+    // pre-split A operands: the forward GEMMs of 32-aligned widths skip the
+    // fp32 -> hi|lo' conversion (MGLP_NO_PRESPLIT_A=1 disables)
+    static const bool off = [] {
+      const char* e = getenv("MGLP_NO_PRESPLIT_A");
+      return e && atoi(e) != 0;
+    }();
+    hl_cap_ = 0;
+    hl_slot_ = 0;
+    const int dh = sd_.d / sd_.heads;
+    if (!off && sd_.d % 32 == 0 && sd_.ffn % 32 == 0 && dh % 32 == 0) {
+      hl_slot_ = (long long)std::max(Tx_, Ty_) * (sd_.d + std::max(sd_.d, sd_.ffn));
+      MGLP_CUDA(cudaMalloc(&hlscr_, (size_t)Gmax_ * hl_slot_ * sizeof(float)));
+      hl_cap_ = Gmax_;
+    }
+  }
   MGLP_CUDA(cudaMalloc(&cache_, (size_t)cache_slots * al_.size * sizeof(float)));
   MGLP_CUDA(cudaMalloc(&bscratch_, (size_t)Gmax_ * bl_.size * sizeof(float)));
   MGLP_CUDA(cudaMalloc(&bcache_, (size_t)cache_slots * bl_.size * sizeof(float)));
@@ -684,8 +700,24 @@ static bool use_long_attn() {
 #endif
 }
 
-void Engine::attention_fwd(int G, Mat Q, Mat K, Mat V, Mat O, Mat P, int sq, int skv,
-                           bool causal, bool keep_p) {
+Mat Engine::hl_mat(int G, int which, int cols) const {
+  Mat m;
+#ifdef MGLP_GEMM_SIMT
+  (void)G;
+  (void)which;
+  (void)cols;
+  return m;  // the SIMT GEMMs read fp32 operands only
+#else
+  if (!hlscr_ || G > hl_cap_ || cols % 32) return m;
+  m.ptr = hlscr_ + (which ? (long long)std::max(Tx_, Ty_) * sd_.d : 0);
+  m.slot_stride = hl_slot_;
+  m.ld = cols;
+  return m;
+#endif
+}
+
+bool Engine::attention_fwd(int G, Mat Q, Mat K, Mat V, Mat O, Mat P, int sq, int skv,
+                           bool causal, bool keep_p, Mat Ohl) {
   const int H = sd_.heads, dh = sd_.d / H;
   auto heads = [&](Mat m, int s) {
     m.bstride = (long long)s * m.ld;
@@ -717,21 +749,30 @@ void Engine::attention_fwd(int G, Mat Q, Mat K, Mat V, Mat O, Mat P, int sq, int
     at.P = P;
     at.range_flag = range_flag_;
     const double fl = 4.0 * G * B_ * H * (double)sq * skv * dh * (causal ? 0.5 : 1.0);
+    // O pre-split for the O-projection; fp32 O only where the backward reads it
+    auto with_hl = [&] {
+      if (!Ohl.ok() || dh % 32) return false;
+      at.Ohl = heads(Ohl, sq);
+      if (!keep_p) at.O = Mat{};
+      return true;
+    };
     if (attn_tc_supported(at, false)) {
       // P is only an intermediate of the backward: not stored for scratch evaluations
       if (!keep_p) at.P = Mat{};
+      const bool hl = with_hl();
       ++launches_;
       prof_shape_ = {sq, skv, dh, G * B_ * H};
       timed(PROF_ATTN, fl, 0.0, [&] { launch_attn_fwd(at, active_, stream_); });
-      return;
+      return hl;
     }
     if (use_long_attn() && attn_long_supported(at, false)) {
       // longer sequences: P is recomputed by the backward from per-row
       // statistics stored in the P slot (attn_long.cu)
+      const bool hl = with_hl();
       ++launches_;
       prof_shape_ = {sq, skv, dh, G * B_ * H};
       timed(PROF_ATTN, fl, 0.0, [&] { launch_attn_fwd_long(at, active_, stream_); });
-      return;
+      return hl;
     }
   }
   GemmArgs g;
@@ -770,6 +811,7 @@ void Engine::attention_fwd(int G, Mat Q, Mat K, Mat V, Mat O, Mat P, int sq, int
   g.ep.kind = EPI_STORE;
   g.ep.out1 = O;
   gemm(g);
+  return false;
 }
 
 void Engine::attention_bwd(int G, Mat Q, Mat K, Mat V, Mat P, Mat O, Mat dO, Mat dP, Mat dQ, Mat dK,
@@ -982,13 +1024,26 @@ void Engine::encoder_forward(const EvalSpec& e, int R, bool causal, Mat X, Mat Y
   Mat n2 = act_mat(e.act, al_.n2, d), hh = act_mat(e.act, al_.h, f), gg = act_mat(e.act, al_.g, f);
   Mat st1 = act_mat(e.act, al_.st1, 2), st2 = act_mat(e.act, al_.st2, 2);
 
+  // pre-split A operands (hl_mat): the LN outputs, attention O and GELU
+  // output are written as hi|lo' rows for the next GEMM; their fp32 forms only
+  // where the backward reads them (keep_lin)
+  const bool keep = keep_lin(e);
+  auto pre = [&](int which, int cols, long long w) {
+    Mat m = hl_mat(G, which, cols);
+    return (m.ok() && par_hl(L, w, l0, ls, false).ok()) ? m : Mat{};
+  };
+  const Mat h_n1 = pre(0, d, L.w_qkv), h_ctx = pre(1, d, L.w_o), h_n2 = pre(0, d, L.w_in),
+            h_g = pre(1, f, L.w_out);
+
   LnFwdArgs ln;
   ln.G = G;
   ln.rows = R;
   ln.d = d;
   ln.eps = (float)sd_.ln_eps;
   ln.x = X;
-  ln.out = n1;
+  ln.out = (keep || !h_n1.ok()) ? n1 : Mat{};
+  ln.out_hl = h_n1;
+  ln.range_flag = range_flag_;
   ln.stats = st1;
   ln.gain = par(L.ln1_g, 0, l0, ls);
   ln.bias = par(L.ln1_b, 0, l0, ls);
@@ -1003,6 +1058,7 @@ void Engine::encoder_forward(const EvalSpec& e, int R, bool causal, Mat X, Mat Y
   g.N = 3 * d;
   g.K = d;
   g.A = n1;
+  g.Ahl = h_n1;
   g.B = par(L.w_qkv, d, l0, ls);
   g.Bhl = par_hl(L, L.w_qkv, l0, ls, false);
   g.ep.kind = EPI_STORE;
@@ -1010,8 +1066,8 @@ void Engine::encoder_forward(const EvalSpec& e, int R, bool causal, Mat X, Mat Y
   g.ep.bias = par(L.b_qkv, 0, l0, ls);
   gemm(g);
 
-  attention_fwd(G, qkv, qkv.offset(d), qkv.offset(2 * d), ctx, Pm, R / B_, R / B_, causal,
-                keep_lin(e));
+  const bool ctx_hl = attention_fwd(G, qkv, qkv.offset(d), qkv.offset(2 * d), ctx, Pm, R / B_,
+                                    R / B_, causal, keep, h_ctx);
 
   g = GemmArgs{};
   g.G = G;
@@ -1019,6 +1075,7 @@ void Engine::encoder_forward(const EvalSpec& e, int R, bool causal, Mat X, Mat Y
   g.N = d;
   g.K = d;
   g.A = ctx;
+  if (ctx_hl) g.Ahl = h_ctx;
   g.B = par(L.w_o, d, l0, ls);
   g.Bhl = par_hl(L, L.w_o, l0, ls, false);
   g.ep.kind = EPI_BIAS_ADD2;
@@ -1030,7 +1087,8 @@ void Engine::encoder_forward(const EvalSpec& e, int R, bool causal, Mat X, Mat Y
   gemm(g);
 
   ln.x = u;
-  ln.out = n2;
+  ln.out = (keep || !h_n2.ok()) ? n2 : Mat{};
+  ln.out_hl = h_n2;
   ln.stats = st2;
   ln.gain = par(L.ln2_g, 0, l0, ls);
   ln.bias = par(L.ln2_b, 0, l0, ls);
@@ -1045,11 +1103,14 @@ void Engine::encoder_forward(const EvalSpec& e, int R, bool causal, Mat X, Mat Y
   g.N = f;
   g.K = d;
   g.A = n2;
+  g.Ahl = h_n2;
   g.B = par(L.w_in, d, l0, ls);
   g.Bhl = par_hl(L, L.w_in, l0, ls, false);
   g.ep.kind = EPI_BIAS_GELU;
-  if (keep_lin(e)) g.ep.out1 = hh;  // gelu'(h): only the backward reads it
-  g.ep.out2 = gg;
+  if (keep) g.ep.out1 = hh;  // gelu'(h): only the backward reads it
+  if (keep || !h_g.ok()) g.ep.out2 = gg;
+  g.ep.hl2 = h_g;
+  g.ep.range_flag = range_flag_;
   g.ep.bias = par(L.b_in, 0, l0, ls);
   gemm(g);
 
@@ -1059,6 +1120,7 @@ void Engine::encoder_forward(const EvalSpec& e, int R, bool causal, Mat X, Mat Y
   g.N = d;
   g.K = f;
   g.A = gg;
+  g.Ahl = h_g;
   g.B = par(L.w_out, f, l0, ls);
   g.Bhl = par_hl(L, L.w_out, l0, ls, false);
   g.ep.kind = EPI_FINAL;
@@ -1111,13 +1173,24 @@ void Engine::decoder_forward(const EvalSpec& e) {
   Mat cctx = act_mat(e.act, al_.cctx, d), cP = act_mat(e.act, al_.cP, 0);
   Mat ybar = act_mat(e.act, al_.ybar, d), st3 = act_mat(e.act, al_.st3, 2);
 
+  // pre-split A operands as in encoder_forward
+  const bool keep = keep_lin(e);
+  auto pre = [&](int which, int cols, long long w) {
+    Mat m = hl_mat(G, which, cols);
+    return (m.ok() && par_hl(L, w, l0, ls, false).ok()) ? m : Mat{};
+  };
+  const Mat h_n1 = pre(0, d, L.w_qkv), h_ctx = pre(1, d, L.w_o), h_n3 = pre(0, d, L.w_cq),
+            h_cctx = pre(1, d, L.w_co), h_n2 = pre(0, d, L.w_in), h_g = pre(1, f, L.w_out);
+
   LnFwdArgs ln;
   ln.G = G;
   ln.rows = R;
   ln.d = d;
   ln.eps = (float)sd_.ln_eps;
   ln.x = Y;
-  ln.out = n1;
+  ln.out = (keep || !h_n1.ok()) ? n1 : Mat{};
+  ln.out_hl = h_n1;
+  ln.range_flag = range_flag_;
   ln.stats = st1;
   ln.gain = par(L.ln1_g, 0, l0, ls);
   ln.bias = par(L.ln1_b, 0, l0, ls);
@@ -1138,14 +1211,17 @@ void Engine::decoder_forward(const EvalSpec& e) {
     return g;
   };
   GemmArgs g = mk(R, 3 * d, d, n1, L.w_qkv, d);
+  g.Ahl = h_n1;
   g.ep.kind = EPI_STORE;
   g.ep.out1 = qkv;
   g.ep.bias = par(L.b_qkv, 0, l0, ls);
   gemm(g);
 
-  attention_fwd(G, qkv, qkv.offset(d), qkv.offset(2 * d), ctx, Pm, sy_, sy_, true, keep_lin(e));
+  const bool ctx_hl =
+      attention_fwd(G, qkv, qkv.offset(d), qkv.offset(2 * d), ctx, Pm, sy_, sy_, true, keep, h_ctx);
 
   g = mk(R, d, d, ctx, L.w_o, d);
+  if (ctx_hl) g.Ahl = h_ctx;
   g.ep.kind = EPI_BIAS_ADD2;
   g.ep.drop = dmask(0, l0, ls);  // self-attention output phi1
   g.ep.out1 = a1;
@@ -1155,7 +1231,8 @@ void Engine::decoder_forward(const EvalSpec& e) {
   gemm(g);
 
   ln.x = u3;
-  ln.out = n3;
+  ln.out = (keep || !h_n3.ok()) ? n3 : Mat{};
+  ln.out_hl = h_n3;
   ln.stats = st3;
   ln.gain = par(L.ln3_g, 0, l0, ls);
   ln.bias = par(L.ln3_b, 0, l0, ls);
@@ -1165,6 +1242,7 @@ void Engine::decoder_forward(const EvalSpec& e) {
         [&] { launch_ln_fwd(ln, active_, stream_); });
 
   g = mk(R, d, d, n3, L.w_cq, d);
+  g.Ahl = h_n3;
   g.ep.kind = EPI_STORE;
   g.ep.out1 = cq;
   g.ep.bias = par(L.b_cq, 0, l0, ls);
@@ -1176,9 +1254,11 @@ void Engine::decoder_forward(const EvalSpec& e) {
   g.ep.bias = par(L.b_ckv, 0, l0, ls);
   gemm(g);
 
-  attention_fwd(G, cq, ckv, ckv.offset(d), cctx, cP, sy_, sx_, false, keep_lin(e));
+  const bool cctx_hl =
+      attention_fwd(G, cq, ckv, ckv.offset(d), cctx, cP, sy_, sx_, false, keep, h_cctx);
 
   g = mk(R, d, d, cctx, L.w_co, d);
+  if (cctx_hl) g.Ahl = h_cctx;
   g.ep.kind = EPI_BIAS_ADD2;
   g.ep.drop = dmask(2, l0, ls);  // cross-attention output phi3
   g.ep.out1 = ybar;
@@ -1189,7 +1269,8 @@ void Engine::decoder_forward(const EvalSpec& e) {
   gemm(g);
 
   ln.x = u2;
-  ln.out = n2;
+  ln.out = (keep || !h_n2.ok()) ? n2 : Mat{};
+  ln.out_hl = h_n2;
   ln.stats = st2;
   ln.gain = par(L.ln2_g, 0, l0, ls);
   ln.bias = par(L.ln2_b, 0, l0, ls);
@@ -1199,13 +1280,17 @@ void Engine::decoder_forward(const EvalSpec& e) {
         [&] { launch_ln_fwd(ln, active_, stream_); });
 
   g = mk(R, f, d, n2, L.w_in, d);
+  g.Ahl = h_n2;
   g.ep.kind = EPI_BIAS_GELU;
-  if (keep_lin(e)) g.ep.out1 = hh;  // gelu'(h): only the backward reads it
-  g.ep.out2 = gg;
+  if (keep) g.ep.out1 = hh;  // gelu'(h): only the backward reads it
+  if (keep || !h_g.ok()) g.ep.out2 = gg;
+  g.ep.hl2 = h_g;
+  g.ep.range_flag = range_flag_;
   g.ep.bias = par(L.b_in, 0, l0, ls);
   gemm(g);
 
   g = mk(R, d, f, gg, L.w_out, f);
+  g.Ahl = h_g;
   g.ep.kind = EPI_FINAL;
   g.ep.drop = dmask(1, l0, ls);  // MLP output phi2
   g.ep.add1 = ybar;

@@ -242,8 +242,14 @@ class Engine {
   // S = Q.K^T, P = softmax(S/sqrt(dh)), O = P.V (blocks.cpp:142-170) and the
   // VJP (blocks.cpp:172-236). Q/K/V/O are token-major [tokens][ld] column
   // slices (head h at columns h*dh); P is [B][H][sq][skv] per member.
-  void attention_fwd(int G, Mat Q, Mat K, Mat V, Mat O, Mat P, int sq, int skv, bool causal,
-                     bool keep_p);
+  // Ohl (optional): also write O pre-split for the O-projection (returns
+  // whether it did; O itself is then skipped unless keep_p)
+  bool attention_fwd(int G, Mat Q, Mat K, Mat V, Mat O, Mat P, int sq, int skv, bool causal,
+                     bool keep_p, Mat Ohl = Mat{});
+  // the family's pre-split activation buffer `which` (0: [rows][d] LN outputs,
+  // 1: [rows][cols <= max(d, ffn)] attention O / GELU output; hi|lo' rows, the
+  // next forward GEMM's A operand); empty when unavailable
+  Mat hl_mat(int G, int which, int cols) const;
   // the activations of this evaluation are the linearization the adjoint
   // reads (cache), not per-evaluation scratch
   bool keep_lin(const EvalSpec& e) const { return e.act.base != scratch_ || e.keep_act; }
@@ -329,6 +335,12 @@ class Engine {
   BwdLayout bl_;
   int Gmax_ = 1;
   float* scratch_ = nullptr;  // Gmax forward activation slots
+  // pre-split forward GEMM A operands (LN outputs, attention O, GELU output):
+  // two buffers per member ([max(Tx,Ty)][d] and [max(Tx,Ty)][max(d,ffn)]),
+  // alternating stage by stage so a GEMM never writes the buffer it reads
+  float* hlscr_ = nullptr;
+  long long hl_slot_ = 0;
+  int hl_cap_ = 0;
   float* cache_ = nullptr;    // total_ forward activation slots (slot = layer)
   float* bscratch_ = nullptr; // Gmax backward slots
   double* colred_part_ = nullptr;  // f64 column-sum partials (rowops.cu colred)

@@ -70,6 +70,7 @@ struct TcParams {
   TcOperand a, b;
   int a_mn, b_mn;  // staging layout of the converted operands
   int b_direct;    // B comes pre-split (hi|lo tiles TMA'd straight into the MMA ring)
+  int a_direct;    // A too (K-major, produced pre-split): no conversion at all
   int passes;      // 3 = hi.hi + (lo.hi + hi.lo); 1 = hi.hi only (diagnostics)
   int ring_a, ring_h, ring_b;  // pre-split B: staging / hi|lo / B ring depths
   int vec_ok;      // every epilogue operand row start is 16-byte aligned
@@ -170,8 +171,11 @@ __global__ void __launch_bounds__(Cfg<CG>::THREADS, 1)
   const int total = per_prob * p.G * p.Bb * p.H;
 
   // ring depths: NA staging stages, NH hi|lo stages, NB pre-split B slots
-  const bool direct = p.b_direct != 0;
-  const int NA = direct ? p.ring_a : 3, NH = direct ? p.ring_h : 3, NB = p.ring_b;
+  const bool direct = p.b_direct != 0, adirect = p.a_direct != 0;
+  // both operands pre-split: 6 A + 6 B hi|lo slots, no staging
+  const int NA = adirect ? 0 : (direct ? p.ring_a : 3);
+  const int NH = adirect ? 6 : (direct ? p.ring_h : 3);
+  const int NB = adirect ? 6 : p.ring_b;
   auto slot = [&](int i) { return smem + i * TILE_BYTES; };
   auto stg_a = [&](int s) { return direct ? slot(s) : slot(2 * s); };
   auto stg_b = [&](int s) { return slot(2 * s + 1); };
@@ -249,7 +253,23 @@ __global__ void __launch_bounds__(Cfg<CG>::THREADS, 1)
 
   if (warp == 0) {
     // ===== TMA producer: fp32 operand tiles into the staging ring =====
-    if (lane == 0) {
+    if (lane == 0 && adirect) {
+      // pre-split A: hi|lo tiles straight into the MMA ring once the MMAs
+      // have released the slot
+      int kg = 0;
+      for (int t = unit; t < total; t += nunits) {
+        const Tile T = tile_of(t);
+        for (int kb = 0; kb < nk; ++kb, ++kg) {
+          const int s = kg % NH;
+          wait(&empty[s], ((kg / NH) & 1) ^ 1);
+          flush(0);
+          mbar_expect_tx(&fullA[s], TILE_BYTES);
+          int c[5];
+          tma_coords(p.a, kb * BK, T.m0, T.g, T.b, T.h, c);
+          tma_load_5d(hl_a(s), &mapA, &fullA[s], c);
+        }
+      }
+    } else if (lane == 0) {
       const uint32_t bytes = TILE_BYTES * (p.b_direct ? 1 : 2);
       int kg = 0;
       for (int t = unit; t < total; t += nunits) {
@@ -362,6 +382,15 @@ __global__ void __launch_bounds__(Cfg<CG>::THREADS, 1)
     int kg = 0;
     for (int t = unit; t < total; t += nunits) {
       for (int kb = 0; kb < nk; ++kb, ++kg) {
+        if (adirect) {
+          // nothing to convert: relay "A and B landed" to the MMA issuer
+          const int s = kg % NH;
+          wait(&fullA[s], (kg / NH) & 1);
+          wait(&fullB[kg % NB], (kg / NB) & 1);
+          __syncwarp();
+          if (lane == 0) mbar_arrive(leader ? &conv[s] : &cdone[s]);
+          continue;
+        }
         const int sa = kg % NA, s = kg % NH;
         wait(&fullA[sa], (kg / NA) & 1);
         if (kc == 0 && lane == 0) flush(5);
@@ -698,9 +727,15 @@ Prepared prepare(const GemmArgs& a) {
   p.a_mn = a.a_mn;
   p.b_direct = a.Bhl.ok() ? 1 : 0;
   p.b_mn = p.b_direct ? 0 : a.b_mn;
+  p.a_direct = (a.Ahl.ok() && p.b_direct && !a.a_mn) ? 1 : 0;
   // A: [M][K] (K-major) or [K][M] (MN-major)
-  P.mA = a.a_mn ? make_map(a.A, a.G, a.Bb, a.H, a.K, a.M, BK, ROWS, false, &p.a)
-                : make_map(a.A, a.G, a.Bb, a.H, a.M, a.K, ROWS, BK, true, &p.a);
+  if (p.a_direct) {
+    const int kpa = ceil_div(a.K, BK) * BK;  // packed row: hi|lo per 32-wide K block
+    P.mA = make_map(a.Ahl, a.G, a.Bb, a.H, a.M, kpa, ROWS, BK, true, &p.a);
+  } else {
+    P.mA = a.a_mn ? make_map(a.A, a.G, a.Bb, a.H, a.K, a.M, BK, ROWS, false, &p.a)
+                  : make_map(a.A, a.G, a.Bb, a.H, a.M, a.K, ROWS, BK, true, &p.a);
+  }
   if (p.b_direct) {
     const int kp = ceil_div(a.K, BK) * BK;  // packed row: kp floats = kp hi + kp lo'
     P.mB = make_map(a.Bhl, a.G, a.Bb, a.H, a.N, kp, ROWS, BK, true, &p.b);

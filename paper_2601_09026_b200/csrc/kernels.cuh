@@ -12,8 +12,10 @@ namespace mglp {
 struct LnFwdArgs {
   int G = 1, rows = 0, d = 0;
   float eps = 1e-5f;
-  Mat x, out, stats;  // stats: [rows][2] = (mean, rstd)
+  Mat x, out, stats;  // stats: [rows][2] = (mean, rstd); out nullable
   Mat gain, bias;     // slot = layer
+  Mat out_hl;         // optional: out pre-split (hi|lo' rows) for the next GEMM
+  int* range_flag = nullptr;
 };
 void launch_ln_fwd(const LnFwdArgs& a, const int* active, cudaStream_t s);
 
@@ -123,6 +125,7 @@ struct AttnArgs {
   float scale = 1.f;
   Mat Q, K, V, O, P;
   Mat dO, dQ, dK, dV;
+  Mat Ohl;  // forward, optional: O pre-split (hi|lo' rows) for the O-projection
   int* range_flag = nullptr;
 };
 bool attn_tc_supported(const AttnArgs& a, bool backward);

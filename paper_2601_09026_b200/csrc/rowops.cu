@@ -70,12 +70,19 @@ __global__ void __launch_bounds__(256) ln_fwd_kernel(LnFwdArgs a, const int* act
   const float rstd = 1.f / sqrtf(var + a.eps);
   const float* gain = a.gain.at(g);
   const float* bias = a.bias.at(g);
-  float* o = a.out.at(g) + (long long)row * a.out.ld;
+  float* o = a.out.ok() ? a.out.at(g) + (long long)row * a.out.ld : nullptr;
+  float* hl = a.out_hl.ok() ? a.out_hl.at(g) + (long long)row * a.out_hl.ld : nullptr;
+  float amax = 0.f;
 #pragma unroll
   for (int i = 0; i < V; ++i) {
     const int j = lane + 32 * i;
-    if (j < a.d) o[j] = gain[j] * ((v[i] - mean) * rstd) + bias[j];
+    if (j < a.d) {
+      const float y = gain[j] * ((v[i] - mean) * rstd) + bias[j];
+      if (o) o[j] = y;
+      if (hl) st_hl1(hl, j, y, amax);
+    }
   }
+  if (hl) hl_range_check(amax, a.range_flag);
   if (lane == 0 && a.stats.ok()) {
     float* st = a.stats.at(g) + 2LL * row;
     st[0] = mean;
@@ -180,18 +187,23 @@ __global__ void __launch_bounds__(256) ln_fwd4_kernel(LnFwdArgs a, const int* ac
   const float rstd = 1.f / sqrtf(var + a.eps);
   const float* gain = a.gain.at(g);
   const float* bias = a.bias.at(g);
-  float* o = a.out.at(g) + (long long)row * a.out.ld;
+  float* o = a.out.ok() ? a.out.at(g) + (long long)row * a.out.ld : nullptr;
+  float* hl = a.out_hl.ok() ? a.out_hl.at(g) + (long long)row * a.out_hl.ld : nullptr;
+  float amax = 0.f;
 #pragma unroll
   for (int i = 0; i < V4; ++i) {
     const int q = lane + 32 * i;
     if (q < d4) {
       const float4 gn = ld4(gain + 4 * q), bs = ld4(bias + 4 * q);
-      st4(o + 4 * q, make_float4(gn.x * ((v[i].x - mean) * rstd) + bs.x,
-                                 gn.y * ((v[i].y - mean) * rstd) + bs.y,
-                                 gn.z * ((v[i].z - mean) * rstd) + bs.z,
-                                 gn.w * ((v[i].w - mean) * rstd) + bs.w));
+      const float4 y = make_float4(gn.x * ((v[i].x - mean) * rstd) + bs.x,
+                                   gn.y * ((v[i].y - mean) * rstd) + bs.y,
+                                   gn.z * ((v[i].z - mean) * rstd) + bs.z,
+                                   gn.w * ((v[i].w - mean) * rstd) + bs.w);
+      if (o) st4(o + 4 * q, y);
+      if (hl) st_hl4(hl, 4 * q, y, amax);
     }
   }
+  if (hl) hl_range_check(amax, a.range_flag);
   if (lane == 0 && a.stats.ok()) {
     float* st = a.stats.at(g) + 2LL * row;
     st[0] = mean;
@@ -648,7 +660,8 @@ __global__ void cycle_end_kernel(SolveCtrl* c, double tol) {
 
 void launch_ln_fwd(const LnFwdArgs& a, const int* active, cudaStream_t s) {
   if (a.rows == 0 || a.G == 0) return;
-  if (a.d % 4 == 0 && vec_ok(a.x) && vec_ok(a.out) && vec_ok(a.gain) && vec_ok(a.bias))
+  if (a.d % 4 == 0 && vec_ok(a.x) && vec_ok(a.out) && vec_ok(a.out_hl) && vec_ok(a.gain) &&
+      vec_ok(a.bias))
     dispatch_rows4<LnFwd4L>(a.d, a, a.G, a.rows, active, s);
   else
     dispatch_rows<LnFwdL>(a.d, a, a.G, a.rows, active, s);

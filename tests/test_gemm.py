@@ -65,6 +65,23 @@ def test_simt_reference_kernel(shape):
     assert relerr(c, ref) < 5e-6
 
 
+@pytest.mark.parametrize("shape", [(2, 256, 512, 768), (1, 300, 260, 100), (3, 512, 256, 3072)])
+def test_presplit_a_is_bitwise_the_converted_path(shape):
+    """A produced pre-split (hi|lo' rows) and TMA'd straight into the MMA ring
+    gives exactly the bits of the in-kernel conversion"""
+    G, M, N_, K = shape
+    g = torch.Generator(device="cpu").manual_seed(2)
+    A = torch.randn(G, M, K, generator=g).float().cuda()
+    B = (torch.randn(G, N_, K, generator=g) * 0.05).float().cuda()
+    outs = []
+    for flag in (1, 3):
+        C = torch.full((G, M, N_), float("nan"), device="cuda")
+        N.call("mglp_test_gemm", G, M, N_, K, A.data_ptr(), M * K, K, 0, B.data_ptr(), N_ * K, K,
+               0, flag, None, C.data_ptr(), M * N_, N_, 0, None)
+        outs.append(C)
+    assert torch.equal(outs[0], outs[1])
+
+
 def test_split_is_effective():
     """the 3-pass fp16 split with a separate correction accumulator must be
     fp32-class (~6e-6 at K=2048); a single fp16 pass sits at ~5e-4"""

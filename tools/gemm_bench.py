@@ -10,11 +10,15 @@ from paper_2601_09026_b200 import _native as N  # noqa: E402
 
 SHAPES = [  # (name, G, M, N, K, a_mn, b_mn, presplit[, epilogue kind])
     ("mlp_in  fwd", 16, 4096, 3072, 768, 0, 0, 1),
+    ("mlp_in  fwd A-hl", 16, 4096, 3072, 768, 0, 0, 3),
     ("mlp_in  fwd gelu", 16, 4096, 3072, 768, 0, 0, 1, 2),
     ("mlp_out dgrad gelu'", 16, 4096, 3072, 768, 0, 1, 1, 4),
     ("mlp_out fwd", 16, 4096, 768, 3072, 0, 0, 1),
+    ("mlp_out fwd A-hl", 16, 4096, 768, 3072, 0, 0, 3),
     ("qkv     fwd", 16, 4096, 2304, 768, 0, 0, 1),
+    ("qkv     fwd A-hl", 16, 4096, 2304, 768, 0, 0, 3),
     ("o       fwd", 16, 4096, 768, 768, 0, 0, 1),
+    ("o       fwd A-hl", 16, 4096, 768, 768, 0, 0, 3),
     ("mlp_in  dgrad", 16, 4096, 768, 3072, 0, 1, 1),
     ("wgrad w_in", 16, 3072, 768, 4096, 1, 1, 0),
     ("attn S", 6144, 128, 128, 64, 0, 0, 0),
