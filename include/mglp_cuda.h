@@ -270,7 +270,7 @@ mglp_status mglp_test_attention(int B, int H, int sq, int skv, int dh, int causa
 
 /* ---- micro-benchmark: `reps` launches of the fused attention over G x B x H
  * heads of length s (forward, or backward when `backward`), device-timed. */
-mglp_status mglp_bench_attention(int G, int B, int H, int s, int dh, int causal, int backward,
+mglp_status mglp_bench_attention(int G, int B, int H, int s, int dh, int causal, int backward /* 0 fwd, 1 bwd, 2 fwd no P, 3 fwd no P, O pre-split */,
                                  int reps, float* ms_per_launch);
 
 /* ---- micro-benchmark: `reps` launches of one tensor-core GEMM family

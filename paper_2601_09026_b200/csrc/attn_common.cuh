@@ -207,11 +207,24 @@ __device__ __forceinline__ void rows_out_o(uint32_t tmain, uint32_t tcor, float*
       float v[16];
       tmem_pair16(tmain + c0 + c, tcor + c0 + c, v);
       if (row < nvalid) {
+        if (out) {
 #pragma unroll
-        for (int e = 0; e < 16; e += 4) {
-          const float4 x = make_float4(v[e], v[e + 1], v[e + 2], v[e + 3]);
-          if (out) *reinterpret_cast<float4*>(out + row * ld + c0 + c + e) = x;
-          if (hl) st_hl4(hl + row * ld, c0 + c + e, x, amax);
+          for (int e = 0; e < 16; e += 4)
+            *reinterpret_cast<float4*>(out + row * ld + c0 + c + e) =
+                make_float4(v[e], v[e + 1], v[e + 2], v[e + 3]);
+        }
+        if (hl) {
+          // 8 values -> one 16-byte hi and one 16-byte lo' store (as many
+          // stores as the fp32 row)
+#pragma unroll
+          for (int e = 0; e < 16; e += 8) {
+            uint4 hi, lo;
+            split8(v + e, hi, lo, amax);
+            const int col = c0 + c + e;
+            char* p = reinterpret_cast<char*>(hl + row * ld) + (col >> 5) * 128 + (col & 31) * 2;
+            *reinterpret_cast<uint4*>(p) = hi;
+            *reinterpret_cast<uint4*>(p + 64) = lo;
+          }
         }
       }
     }

@@ -257,7 +257,6 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
   for (int z = blockIdx.x; z < nprob; z += gridDim.x) {
     int g, b, h;
     problem_of(a, z, g, b, h);
-    const float* P = a.P.at(g, b, h);
     // (1) dO, V -> T0
     mbar_wait(st_full, stp);
     stp ^= 1;
@@ -302,18 +301,29 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
       const int c0 = half * 64;
       const bool any = c0 < skv16;
       const bool live = r < sq;
-      const float* prow = P + (long long)r * a.P.ld + c0;
-      // this half-row of P, loaded once (zero beyond skv and for rows >= sq)
+      // this half-row of P (zero beyond skv and for rows >= sq) from the
+      // hi/lo' tiles just converted for the dV MMA: p = hi + 2^-11 lo', the
+      // operand value the MMAs use (<= 2^-22 relative from the stored fp32 P;
+      // no second read of P from global memory)
       const int lim = live ? skv - c0 : 0;
       float pv[64];
 #pragma unroll
-      for (int e = 0; e < 64; e += 4) {
-        const float4 p4 = e < lim ? *reinterpret_cast<const float4*>(prow + e)
-                                  : make_float4(0.f, 0.f, 0.f, 0.f);
-        pv[e] = p4.x;
-        pv[e + 1] = p4.y;
-        pv[e + 2] = p4.z;
-        pv[e + 3] = p4.w;
+      for (int cc = 0; cc < 8; ++cc) {
+        if (cc * 8 < lim) {
+          const uint32_t off = chunk_off(128, r, half * 8 + cc);
+          const uint4 h4 = lds128u(Pm.hi + off), l4 = lds128u(Pm.lo + off);
+          const uint32_t hw[4] = {h4.x, h4.y, h4.z, h4.w}, lw[4] = {l4.x, l4.y, l4.z, l4.w};
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const float2 hf = __half22float2(*reinterpret_cast<const __half2*>(&hw[k]));
+            const float2 lf = __half22float2(*reinterpret_cast<const __half2*>(&lw[k]));
+            pv[cc * 8 + 2 * k] = fmaf(lf.x, kLoInv, hf.x);
+            pv[cc * 8 + 2 * k + 1] = fmaf(lf.y, kLoInv, hf.y);
+          }
+        } else {
+#pragma unroll
+          for (int e = 0; e < 8; ++e) pv[cc * 8 + e] = 0.f;
+        }
       }
       float dp[64];
       float t = 0.f;

@@ -873,9 +873,18 @@ mglp_status mglp_bench_attention(int G, int B, int H, int s, int dh, int causal,
     for (Mat* m : {&a.Q, &a.K, &a.V, &a.dQ, &a.dK, &a.dV}) m->slot_stride = (long long)B * s * ld;
     for (Mat* m : {&a.O, &a.dO}) m->slot_stride = (long long)B * s * d;
     a.P.slot_stride = (long long)B * H * s * ldp;
+    // backward: 0 forward (P / row statistics stored), 1 backward,
+    // 2 forward without P (s <= 128), 3 as 2 with O written pre-split only
+    const int mode = backward;
+    backward = mode == 1;
     const bool shortp = attn_tc_supported(a, backward != 0);
     if (!shortp && !attn_long_supported(a, backward != 0))
       throw ValidationError("bench_attention: unsupported shape");
+    if (mode >= 2 && shortp) a.P = Mat{};
+    if (mode == 3) {
+      a.Ohl = a.O;
+      a.O = Mat{};
+    }
     cudaEvent_t e0, e1;
     MGLP_CUDA(cudaEventCreate(&e0));
     MGLP_CUDA(cudaEventCreate(&e1));
