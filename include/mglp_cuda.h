@@ -261,8 +261,11 @@ mglp_status mglp_engine_lipschitz(mglp_engine* e, int samples, double delta_scal
  * Forward always; with dO set, also the backward (dQ, dK, dV overwritten).
  * sq, skv <= 128 and multiples of 8 (attn_tc.cu), or 128 <= sq, skv <= 512
  * (attn_long.cu: P then receives the per-row (max, 1/sum) statistics, [sq][2]
- * per head, instead of the probabilities); dh 32 or 64 (else status 1). The
- * reference's attention / vjp_attention (blocks.cpp:142-236). Synchronous. */
+ * per head, instead of the probabilities); dh 32 or 64 (else status 1).
+ * causal bit 0: causal mask; bit 1 (sq = skv = 128 only): P is kept in the
+ * pre-split form the engine uses at s = 128 (the forward's hi|lo' tiles, 64
+ * KiB per head; not probabilities). The reference's attention /
+ * vjp_attention (blocks.cpp:142-236). Synchronous. */
 mglp_status mglp_test_attention(int B, int H, int sq, int skv, int dh, int causal, const float* Q,
                                 const float* K, const float* V, int ld, float* O, float* P,
                                 const float* dO, float* dQ, float* dK, float* dV,

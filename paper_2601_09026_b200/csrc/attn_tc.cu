@@ -158,7 +158,7 @@ __global__ void __launch_bounds__(kThreads, 2) attn_fwd_kernel(const __grid_cons
     if (any) {
 #pragma unroll
       for (int e = 0; e < 64; ++e) v[e] *= inv;
-      if (a.P.ok() && i < sq) {
+      if (a.P.ok() && !a.p_hl && i < sq) {
         float* prow = a.P.at(g, b, h) + i * (long long)a.P.ld + c0;
 #pragma unroll
         for (int e = 0; e < 64; e += 4)
@@ -176,11 +176,17 @@ __global__ void __launch_bounds__(kThreads, 2) attn_fwd_kernel(const __grid_cons
       tc_after();
       mma3(tmem, tmem + 128, Pt, Vt, dh, skv16 >> 4);  // O
       mma_commit<1>(o_bar);
+      // P for the backward: the hi|lo' tiles themselves (async, coalesced)
+      if (a.P.ok() && a.p_hl) bulk_store(a.P.at(g, b, h), Pt.hi, 4 * TILE64);
     }
     mbar_wait(o_bar, ph);
     tc_after();
-    // the tiles are free: the next problem's loads overlap this epilogue
-    if (tid == 0 && z + (int)gridDim.x < nprob) issue_loads(z + gridDim.x);
+    // the tiles are free (once the P copy has read them): the next problem's
+    // loads overlap this epilogue
+    if (tid == 0 && z + (int)gridDim.x < nprob) {
+      bulk_store_wait_read();
+      issue_loads(z + gridDim.x);
+    }
     rows_out_o(trow, trow + 128, a.O.ok() ? a.O.at(g, b, h) : nullptr,
                a.Ohl.ok() ? a.Ohl.at(g, b, h) : nullptr, a.Ohl.ok() ? a.Ohl.ld : a.O.ld, i, sq,
                half * (dh >> 1), dh >> 1, amax);
@@ -188,6 +194,7 @@ __global__ void __launch_bounds__(kThreads, 2) attn_fwd_kernel(const __grid_cons
     __syncthreads();  // TMEM free for the next problem
   }
   if (amax >= 65520.f && amax <= FLT_MAX && a.range_flag) atomicOr(a.range_flag, 1);
+  if (tid == 0) bulk_store_wait();
   tc_before();
   __syncthreads();
   if (warp == 0) tmem_free(tmem, 256);
@@ -223,6 +230,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 2 * 128 * 64 * 4 + 2 * PAIR128);
   uint64_t* st_full = &bars[0];
   uint64_t* m_bar = &bars[1];
+  uint64_t* p_full = &bars[2];  // p_hl: the pre-split P tiles landed in T1
   float* xch = reinterpret_cast<float*>(bars + 4);  // [2][128] row-sum exchange
   uint32_t* tslot = reinterpret_cast<uint32_t*>(xch + 256);
   const int nprob = a.G * a.Bb * a.H;
@@ -238,9 +246,18 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
     __syncwarp();
   };
 
+  const bool phl = a.p_hl != 0;
+  auto load_p = [&](int z) {  // one thread: T1 is free
+    int g, b, h;
+    problem_of(a, z, g, b, h);
+    mbar_expect_tx(p_full, 4 * TILE64);
+    bulk_load(T1, a.P.at(g, b, h), 4 * TILE64, p_full);
+  };
+
   if (tid == 0) {
     mbar_init(st_full, 1);
     mbar_init(m_bar, 1);
+    mbar_init(p_full, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) tmem_alloc(tslot, 512);
@@ -252,8 +269,9 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
   const int r = q4 * 32 + lane;  // TMEM lane: query row (dP, dQ) or key row (dV, dK)
   float amax = 0.f;
   if (warp == 0 && (int)blockIdx.x < nprob) load_dov(blockIdx.x);
+  if (phl && tid == 0 && (int)blockIdx.x < nprob) load_p(blockIdx.x);
 
-  uint32_t stp = 0, mp = 0;  // barrier phases
+  uint32_t stp = 0, mp = 0, pp = 0;  // barrier phases
   for (int z = blockIdx.x; z < nprob; z += gridDim.x) {
     int g, b, h;
     problem_of(a, z, g, b, h);
@@ -264,18 +282,24 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
     conv_rows(st2, skv, skv16, dh, Vk.hi, Vk.lo, tid, kThreads, amax);
     fence_async_smem();  // staging reads ordered before the bulk copies that reuse it
     __syncthreads();
-    if (warp == 0) {
-      if (lane == 0) {
-        mbar_expect_tx(st_full, (uint32_t)(sq * skv * 4));
-        tma_box(stg, tm, TP, g, b, h, st_full);
+    if (phl) {
+      // (2') P arrives pre-split in T1 (sq = skv = 128: no padding rows)
+      mbar_wait(p_full, pp);
+      pp ^= 1;
+    } else {
+      if (warp == 0) {
+        if (lane == 0) {
+          mbar_expect_tx(st_full, (uint32_t)(sq * skv * 4));
+          tma_box(stg, tm, TP, g, b, h, st_full);
+        }
+        __syncwarp();
       }
-      __syncwarp();
+      // (2) P -> T1 (rows >= sq zero: K padding of dV)
+      mbar_wait(st_full, stp);
+      stp ^= 1;
+      conv_rows(stg, sq, 128, skv, Pm.hi, Pm.lo, tid, kThreads, amax);
+      fence_async_smem();
     }
-    // (2) P -> T1 (rows >= sq zero: K padding of dV)
-    mbar_wait(st_full, stp);
-    stp ^= 1;
-    conv_rows(stg, sq, 128, skv, Pm.hi, Pm.lo, tid, kThreads, amax);
-    fence_async_smem();
     tc_before();
     __syncthreads();
     tc_after();
@@ -376,6 +400,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
     mbar_wait(m_bar, mp);
     mp ^= 1;
     tc_after();
+    // T1 (Q | K) is free: the next problem's P streams in under this epilogue
+    if (phl && tid == 0 && z + (int)gridDim.x < nprob) load_p(z + gridDim.x);
     rows_out(trow, trow + 64, a.dQ.at(g, b, h), a.dQ.ld, r, sq, half * (dh >> 1), dh >> 1, a.scale);
     rows_out(trow + 128, trow + 192, a.dK.at(g, b, h), a.dK.ld, r, skv, half * (dh >> 1), dh >> 1,
              a.scale);
@@ -425,6 +451,11 @@ bool attn_tc_supported(const AttnArgs& a, bool backward) {
   if (!aligned(a.Q) || !aligned(a.K) || !aligned(a.V) || !aligned(a.O) || !aligned(a.P))
     return false;
   if (backward && (!aligned(a.dO) || !aligned(a.dQ) || !aligned(a.dK) || !aligned(a.dV) || !a.P.ok()))
+    return false;
+  // pre-split P: 128 x 128 problems whose P slots are 64 KiB apart
+  if (a.p_hl && a.P.ok() &&
+      (a.sq != 128 || a.skv != 128 || a.P.ld != 128 || (a.Bb > 1 && a.P.bstride % (128 * 128)) ||
+       (a.H > 1 && a.P.hstride != 128 * 128)))
     return false;
   return true;
 }

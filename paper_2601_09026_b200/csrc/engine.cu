@@ -716,6 +716,17 @@ Mat Engine::hl_mat(int G, int which, int cols) const {
 #endif
 }
 
+// s = 128: the fused kernels keep P in its pre-split form (AttnArgs::p_hl):
+// one 64 KiB hi|lo' tile set per (member, batch, head), exactly the fp32
+// P slot. A function of the shape only, so forward and backward agree.
+bool Engine::p_hl_ok(int sq, int skv, const Mat& P) const {
+  static const bool off = [] {
+    const char* e = getenv("MGLP_ATTN_P_FP32");
+    return e && atoi(e) != 0;
+  }();
+  return !off && sq == 128 && skv == 128 && P.ld == 128 && use_fused_attn();
+}
+
 bool Engine::attention_fwd(int G, Mat Q, Mat K, Mat V, Mat O, Mat P, int sq, int skv,
                            bool causal, bool keep_p, Mat Ohl) {
   const int H = sd_.heads, dh = sd_.d / H;
@@ -748,6 +759,7 @@ bool Engine::attention_fwd(int G, Mat Q, Mat K, Mat V, Mat O, Mat P, int sq, int
     at.O = O;
     at.P = P;
     at.range_flag = range_flag_;
+    at.p_hl = p_hl_ok(sq, skv, P) ? 1 : 0;
     const double fl = 4.0 * G * B_ * H * (double)sq * skv * dh * (causal ? 0.5 : 1.0);
     // O pre-split for the O-projection; fp32 O only where the backward reads it
     auto with_hl = [&] {
@@ -856,6 +868,7 @@ void Engine::attention_bwd(int G, Mat Q, Mat K, Mat V, Mat P, Mat O, Mat dO, Mat
     at.dK = dK;
     at.dV = dV;
     at.range_flag = range_flag_;
+    at.p_hl = p_hl_ok(sq, skv, P) ? 1 : 0;  // as the forward stored it
     const double fl = 8.0 * G * B_ * H * (double)sq * skv * dh;
     if (attn_tc_supported(at, true)) {
       ++launches_;

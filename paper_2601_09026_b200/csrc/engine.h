@@ -250,6 +250,7 @@ class Engine {
   // 1: [rows][cols <= max(d, ffn)] attention O / GELU output; hi|lo' rows, the
   // next forward GEMM's A operand); empty when unavailable
   Mat hl_mat(int G, int which, int cols) const;
+  bool p_hl_ok(int sq, int skv, const Mat& P) const;
   // the activations of this evaluation are the linearization the adjoint
   // reads (cache), not per-evaluation scratch
   bool keep_lin(const EvalSpec& e) const { return e.act.base != scratch_ || e.keep_act; }

@@ -126,6 +126,10 @@ struct AttnArgs {
   Mat Q, K, V, O, P;
   Mat dO, dQ, dK, dV;
   Mat Ohl;  // forward, optional: O pre-split (hi|lo' rows) for the O-projection
+  // s = 128 fused path (attn_tc.cu): P is kept in its pre-split form, the
+  // forward's hi|lo' MMA operand tiles (64 KiB per problem, exactly the fp32
+  // P slot), bulk-copied out by the forward and back in by the backward
+  int p_hl = 0;
   int* range_flag = nullptr;
 };
 bool attn_tc_supported(const AttnArgs& a, bool backward);

@@ -61,7 +61,7 @@ def run(B, H, sq, skv, dh, causal, seed=0, scale=1.0):
     N.call("mglp_test_attention", B, H, sq, skv, dh, int(causal), dq.data_ptr(),
            dkv[..., d:].data_ptr(), dkv[..., 2 * d:].data_ptr(), ld, O.data_ptr(), P.data_ptr(),
            ddo.data_ptr(), dQ.data_ptr(), dKV[..., d:].data_ptr(), dKV[..., 2 * d:].data_ptr(), None)
-    ref = reference(Q, K, V, dO, B, H, sq, skv, dh, causal)
+    ref = reference(Q, K, V, dO, B, H, sq, skv, dh, int(causal) & 1)
     got = (O[..., :d].cpu(), P[..., :skv].cpu(), dQ[..., :d].cpu(), dKV[..., d:2 * d].cpu(),
            dKV[..., 2 * d:].cpu())
     return got, ref
@@ -151,3 +151,16 @@ def test_unsupported_shape_is_a_validation_error():
     with pytest.raises(N.ValidationError):
         N.call("mglp_test_attention", 1, 1, 600, 600, 64, 0, x.data_ptr(), x.data_ptr(),
                x.data_ptr(), 192, x.data_ptr(), x.data_ptr(), None, None, None, None, None)
+
+
+@pytest.mark.parametrize("causal", [False, True])
+def test_presplit_p_is_bitwise_the_fp32_p_path(causal):
+    """s = 128: the engine keeps P as the forward's hi|lo' operand tiles
+    (bulk-copied out and back in) instead of fp32 probabilities; the backward
+    converts an fp32 P into exactly those tiles, so O, dQ, dK, dV must agree
+    bit for bit"""
+    a, ref = run(2, 3, 128, 128, 64, causal, seed=5)
+    b, _ = run(2, 3, 128, 128, 64, int(causal) | 2, seed=5)
+    for n, x, y in zip(["O", "dQ", "dK", "dV"], (a[0],) + a[2:], (b[0],) + b[2:]):
+        assert torch.equal(x, y), n
+    assert relerr(b[0], ref[0]) < 1e-5
