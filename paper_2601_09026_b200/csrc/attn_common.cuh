@@ -194,18 +194,22 @@ __device__ __forceinline__ void rows_out(uint32_t tmain, uint32_t tcor, float* o
   }
 }
 
-// the forward O rows: fp32 (out, nullable) and/or pre-split hi|lo' (hl,
-// nullable; the O-projection GEMM's A operand, common.cuh st_hl4). hl follows
-// out's strides; the head's column offset must be a multiple of 32 so the
-// fp32 offset of the head equals its packed byte offset.
-__device__ __forceinline__ void rows_out_o(uint32_t tmain, uint32_t tcor, float* out, float* hl,
-                                           long long ld, int row, int nvalid, int c0, int nc,
-                                           float& amax) {
+// output rows (forward O; backward dQ, dK, dV) scaled by alpha: fp32 (out,
+// nullable) and/or pre-split hi|lo' (hl, nullable; the next GEMM's A operand,
+// common.cuh). hl follows out's strides; the head's column offset must be a
+// multiple of 32 so the fp32 offset of the head equals its packed byte offset.
+__device__ __forceinline__ void rows_out_hl(uint32_t tmain, uint32_t tcor, float* out, float* hl,
+                                            long long ld, int row, int nvalid, int c0, int nc,
+                                            float alpha, float& amax) {
 #pragma unroll
   for (int c = 0; c < 32; c += 16) {
     if (c < nc) {
       float v[16];
       tmem_pair16(tmain + c0 + c, tcor + c0 + c, v);
+      if (alpha != 1.f) {
+#pragma unroll
+        for (int e = 0; e < 16; ++e) v[e] *= alpha;
+      }
       if (row < nvalid) {
         if (out) {
 #pragma unroll

@@ -260,10 +260,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     {
       const long long ld = a.Ohl.ok() ? a.Ohl.ld : a.O.ld;
-      rows_out_o(trow + 256, trow + 384,
-                 a.O.ok() ? a.O.at(g, b, h) + (long long)qb * 128 * ld : nullptr,
-                 a.Ohl.ok() ? a.Ohl.at(g, b, h) + (long long)qb * 128 * ld : nullptr, ld, i,
-                 sq - qb * 128, half * (dh >> 1), dh >> 1, amax);
+      rows_out_hl(trow + 256, trow + 384,
+                  a.O.ok() ? a.O.at(g, b, h) + (long long)qb * 128 * ld : nullptr,
+                  a.Ohl.ok() ? a.Ohl.at(g, b, h) + (long long)qb * 128 * ld : nullptr, ld, i,
+                  sq - qb * 128, half * (dh >> 1), dh >> 1, 1.f, amax);
     }
     if (half == 0 && q < sq) {
       float* stp = a.P.at(g, b, h) + 2LL * q;
@@ -386,10 +386,17 @@ __global__ void __launch_bounds__(kThreads, 1)
       mma_done(L, ph);
     }
     const int nv = skv - kb * 128;
-    rows_out(trow + 256, trow + 320, a.dV.at(g, b, h) + (long long)kb * 128 * a.dV.ld, a.dV.ld, i,
-             nv, half * (dh >> 1), dh >> 1, 1.f);
-    rows_out(trow + 384, trow + 448, a.dK.at(g, b, h) + (long long)kb * 128 * a.dK.ld, a.dK.ld, i,
-             nv, half * (dh >> 1), dh >> 1, a.scale);
+    {
+      const long long ldv = a.dVhl.ok() ? a.dVhl.ld : a.dV.ld;
+      const long long ldk = a.dKhl.ok() ? a.dKhl.ld : a.dK.ld;
+      const long long ov = (long long)kb * 128 * ldv, ok = (long long)kb * 128 * ldk;
+      rows_out_hl(trow + 256, trow + 320, a.dV.ok() ? a.dV.at(g, b, h) + ov : nullptr,
+                  a.dVhl.ok() ? a.dVhl.at(g, b, h) + ov : nullptr, ldv, i, nv, half * (dh >> 1),
+                  dh >> 1, 1.f, amax);
+      rows_out_hl(trow + 384, trow + 448, a.dK.ok() ? a.dK.at(g, b, h) + ok : nullptr,
+                  a.dKhl.ok() ? a.dKhl.at(g, b, h) + ok : nullptr, ldk, i, nv, half * (dh >> 1),
+                  dh >> 1, a.scale, amax);
+    }
     sync_all();
   }
   if (amax >= 65520.f && amax <= FLT_MAX && a.range_flag) atomicOr(a.range_flag, 1);
@@ -490,8 +497,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       mma_done(L, ph);
     }
-    rows_out(trow + 256, trow + 384, a.dQ.at(g, b, h) + (long long)qb * 128 * a.dQ.ld, a.dQ.ld, i,
-             sq - qb * 128, half * (dh >> 1), dh >> 1, a.scale);
+    {
+      const long long ldq = a.dQhl.ok() ? a.dQhl.ld : a.dQ.ld;
+      const long long oq = (long long)qb * 128 * ldq;
+      rows_out_hl(trow + 256, trow + 384, a.dQ.ok() ? a.dQ.at(g, b, h) + oq : nullptr,
+                  a.dQhl.ok() ? a.dQhl.at(g, b, h) + oq : nullptr, ldq, i, sq - qb * 128,
+                  half * (dh >> 1), dh >> 1, a.scale, amax);
+    }
     sync_all();
   }
   if (amax >= 65520.f && amax <= FLT_MAX && a.range_flag) atomicOr(a.range_flag, 1);

@@ -187,9 +187,9 @@ __global__ void __launch_bounds__(kThreads, 2) attn_fwd_kernel(const __grid_cons
       bulk_store_wait_read();
       issue_loads(z + gridDim.x);
     }
-    rows_out_o(trow, trow + 128, a.O.ok() ? a.O.at(g, b, h) : nullptr,
-               a.Ohl.ok() ? a.Ohl.at(g, b, h) : nullptr, a.Ohl.ok() ? a.Ohl.ld : a.O.ld, i, sq,
-               half * (dh >> 1), dh >> 1, amax);
+    rows_out_hl(trow, trow + 128, a.O.ok() ? a.O.at(g, b, h) : nullptr,
+                a.Ohl.ok() ? a.Ohl.at(g, b, h) : nullptr, a.Ohl.ok() ? a.Ohl.ld : a.O.ld, i, sq,
+                half * (dh >> 1), dh >> 1, 1.f, amax);
     tc_before();
     __syncthreads();  // TMEM free for the next problem
   }
@@ -381,7 +381,9 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
       }
     }
     // dV rows (keys) while the staging of Q, K lands
-    rows_out(trow + 256, trow + 384, a.dV.at(g, b, h), a.dV.ld, r, skv, half * (dh >> 1), dh >> 1, 1.f);
+    rows_out_hl(trow + 256, trow + 384, a.dV.ok() ? a.dV.at(g, b, h) : nullptr,
+                a.dVhl.ok() ? a.dVhl.at(g, b, h) : nullptr, a.dVhl.ok() ? a.dVhl.ld : a.dV.ld, r,
+                skv, half * (dh >> 1), dh >> 1, 1.f, amax);
     // (4) Q, K -> T1 (the dV MMA is done)
     mbar_wait(st_full, stp);
     stp ^= 1;
@@ -402,9 +404,12 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
     tc_after();
     // T1 (Q | K) is free: the next problem's P streams in under this epilogue
     if (phl && tid == 0 && z + (int)gridDim.x < nprob) load_p(z + gridDim.x);
-    rows_out(trow, trow + 64, a.dQ.at(g, b, h), a.dQ.ld, r, sq, half * (dh >> 1), dh >> 1, a.scale);
-    rows_out(trow + 128, trow + 192, a.dK.at(g, b, h), a.dK.ld, r, skv, half * (dh >> 1), dh >> 1,
-             a.scale);
+    rows_out_hl(trow, trow + 64, a.dQ.ok() ? a.dQ.at(g, b, h) : nullptr,
+                a.dQhl.ok() ? a.dQhl.at(g, b, h) : nullptr, a.dQhl.ok() ? a.dQhl.ld : a.dQ.ld, r,
+                sq, half * (dh >> 1), dh >> 1, a.scale, amax);
+    rows_out_hl(trow + 128, trow + 192, a.dK.ok() ? a.dK.at(g, b, h) : nullptr,
+                a.dKhl.ok() ? a.dKhl.at(g, b, h) : nullptr, a.dKhl.ok() ? a.dKhl.ld : a.dK.ld, r,
+                skv, half * (dh >> 1), dh >> 1, a.scale, amax);
     tc_before();
     __syncthreads();
   }

@@ -341,7 +341,15 @@ __device__ __forceinline__ double epilogue_rowv(const EpiArgs& e, int g, int b, 
       ld4(e.aux.at(g) + (long long)row * e.aux.ld + col0, t1);
 #pragma unroll
       for (int i = 0; i < W; ++i) o[i] = acc[i] * t1[i];
-      st4(e.out1.at(g) + (long long)row * e.out1.ld + col0, o);
+      if (e.out1.ok()) st4(e.out1.at(g) + (long long)row * e.out1.ld + col0, o);
+      if (e.hl2.ok()) {
+        float amax = 0.f;
+        float* hr = e.hl2.at(g) + (long long)row * e.hl2.ld;
+#pragma unroll
+        for (int i = 0; i < W; i += 4)
+          st_hl4(hr, col0 + i, make_float4(o[i], o[i + 1], o[i + 2], o[i + 3]), amax);
+        hl_range_check(amax, e.range_flag);
+      }
     } break;
     case EPI_GRAD_ACC: {
       float* p = e.out1.at(g) + (long long)row * e.out1.ld + col0;
@@ -431,8 +439,13 @@ __device__ __forceinline__ double epilogue_4x4(const EpiArgs& e, int g, int b, i
       for (int i = 0; i < 4; ++i) {
         if (rows[i] < 0) continue;
         const float4 a = acc[i], v = x1[i];
-        st4g(e.out1.at(g) + (long long)rows[i] * e.out1.ld + col,
-             make_float4(a.x * v.x, a.y * v.y, a.z * v.z, a.w * v.w));
+        const float4 dv = make_float4(a.x * v.x, a.y * v.y, a.z * v.z, a.w * v.w);
+        if (e.out1.ok()) st4g(e.out1.at(g) + (long long)rows[i] * e.out1.ld + col, dv);
+        if (e.hl2.ok()) {
+          float amax = 0.f;
+          st_hl4(e.hl2.at(g) + (long long)rows[i] * e.hl2.ld, col, dv, amax);
+          hl_range_check(amax, e.range_flag);
+        }
       }
     } break;
     case EPI_GRAD_ACC: {
@@ -543,9 +556,16 @@ __device__ __forceinline__ double epilogue_row(const EpiArgs& e, int g, int b, i
       }
     } break;
     case EPI_GELU_BWD: {
-      float* o = e.out1.at(g) + (long long)row * e.out1.ld + col0;
+      float* o = e.out1.ok() ? e.out1.at(g) + (long long)row * e.out1.ld + col0 : nullptr;
+      float* hr = e.hl2.ok() ? e.hl2.at(g) + (long long)row * e.hl2.ld : nullptr;
       const float* dv = e.aux.at(g) + (long long)row * e.aux.ld + col0;
-      for (int i = 0; i < n; ++i) o[i] = acc[i] * dv[i];
+      float amax = 0.f;
+      for (int i = 0; i < n; ++i) {
+        const float x = acc[i] * dv[i];
+        if (o) o[i] = x;
+        if (hr) st_hl1(hr, col0 + i, x, amax);
+      }
+      if (hr) hl_range_check(amax, e.range_flag);
     } break;
     case EPI_GRAD_ACC: {
       float* o = e.out1.at(g) + (long long)row * e.out1.ld + col0;

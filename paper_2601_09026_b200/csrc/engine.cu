@@ -727,6 +727,15 @@ bool Engine::p_hl_ok(int sq, int skv, const Mat& P) const {
   return !off && sq == 128 && skv == 128 && P.ld == 128 && use_fused_attn();
 }
 
+// the adjoint's pre-split dgrad operands (MGLP_NO_PRESPLIT_DGRAD=1 disables)
+Mat Engine::dgrad_hl(int G, int which, int cols) const {
+  static const bool off = [] {
+    const char* e = getenv("MGLP_NO_PRESPLIT_DGRAD");
+    return e && atoi(e) != 0;
+  }();
+  return off ? Mat{} : hl_mat(G, which, cols);
+}
+
 bool Engine::attention_fwd(int G, Mat Q, Mat K, Mat V, Mat O, Mat P, int sq, int skv,
                            bool causal, bool keep_p, Mat Ohl) {
   const int H = sd_.heads, dh = sd_.d / H;
@@ -826,8 +835,9 @@ bool Engine::attention_fwd(int G, Mat Q, Mat K, Mat V, Mat O, Mat P, int sq, int
   return false;
 }
 
-void Engine::attention_bwd(int G, Mat Q, Mat K, Mat V, Mat P, Mat O, Mat dO, Mat dP, Mat dQ, Mat dK,
-                           Mat dV, int sq, int skv, bool causal) {
+bool Engine::attention_bwd(int G, Mat Q, Mat K, Mat V, Mat P, Mat O, Mat dO, Mat dP, Mat dQ, Mat dK,
+                           Mat dV, int sq, int skv, bool causal, Mat dQhl, Mat dKhl, Mat dVhl,
+                           bool keep32) {
   const int H = sd_.heads, dh = sd_.d / H;
   const float scale = (float)(1.0 / std::sqrt((double)dh));
   auto heads = [&](Mat m, int s) {
@@ -870,17 +880,29 @@ void Engine::attention_bwd(int G, Mat Q, Mat K, Mat V, Mat P, Mat O, Mat dO, Mat
     at.range_flag = range_flag_;
     at.p_hl = p_hl_ok(sq, skv, P) ? 1 : 0;  // as the forward stored it
     const double fl = 8.0 * G * B_ * H * (double)sq * skv * dh;
+    // pre-split gradients for the QKV dgrad; fp32 only where a weight
+    // gradient reads them
+    auto with_hl = [&] {
+      if (!dQhl.ok() || !dKhl.ok() || !dVhl.ok() || dh % 32) return false;
+      at.dQhl = heads(dQhl, sq);
+      at.dKhl = heads(dKhl, skv);
+      at.dVhl = heads(dVhl, skv);
+      if (!keep32) at.dQ = at.dK = at.dV = Mat{};
+      return true;
+    };
     if (attn_tc_supported(at, true)) {
+      const bool hl = with_hl();
       ++launches_;
       prof_shape_ = {-sq, skv, dh, G * B_ * H};
       timed(PROF_ATTN, fl, 0.0, [&] { launch_attn_bwd(at, active_, stream_); });
-      return;
+      return hl;
     }
     if (use_long_attn() && attn_long_supported(at, true)) {
+      const bool hl = with_hl();
       ++launches_;
       prof_shape_ = {-sq, skv, dh, G * B_ * H};
       timed(PROF_ATTN, fl, 0.0, [&] { launch_attn_bwd_long(at, active_, stream_); });
-      return;
+      return hl;
     }
   }
   auto mk = [&](int M, int N, int K_, Mat A, bool amn, Mat B, bool bmn, Mat out, float alpha) {
@@ -914,6 +936,7 @@ void Engine::attention_bwd(int G, Mat Q, Mat K, Mat V, Mat P, Mat O, Mat dO, Mat
   mk(skv, dh, sq, P, true, dO, true, dV, 1.f);     // dV = P^T . dO
   mk(sq, dh, skv, dP, false, K, true, dQ, scale);  // dQ = dS . K / sqrt(dh)
   mk(skv, dh, sq, dP, true, Q, true, dK, scale);   // dK = dS^T . Q / sqrt(dh)
+  return false;
 }
 
 cudaEvent_t Engine::prof_event() {
@@ -1414,13 +1437,20 @@ void Engine::encoder_adjoint(const EvalSpec& e, bool causal) {
       timed(PROF_ROW, 0.0, 8.0 * G * (double)R * d,
             [&] { launch_mask_copy(G, R, d, UPm, UP, dmask(1, l0, ls), active_, stream_); });
     }
+    // pre-split dgrad A operands (dh, da1; hl_mat); their fp32 forms only
+    // where a weight gradient reads them (this call, or the captured chain)
+    const bool keepb = e.want_grads || e.bact.base != nullptr;
+    const Mat h_dh = dgrad_hl(G, 1, f), h_da1 = dgrad_hl(G, 0, d);
     GemmArgs g = mk(R, f, d, UPm, L.w_out, f);
     g.ep.kind = EPI_GELU_BWD;
-    g.ep.out1 = dh;
+    if (keepb || !h_dh.ok()) g.ep.out1 = dh;
+    g.ep.hl2 = h_dh;
+    g.ep.range_flag = range_flag_;
     g.ep.aux = hh;
     gemm(g);
 
     g = mk(R, d, f, dh, L.w_in, d);
+    g.Ahl = h_dh;
     g.ep.kind = EPI_STORE;
     g.ep.out1 = dn2;
     gemm(g);
@@ -1434,7 +1464,9 @@ void Engine::encoder_adjoint(const EvalSpec& e, bool causal) {
     lb.up = dn2;
     lb.gain = par(L.ln2_g, 0, l0, ls);
     lb.out1 = du;
-    lb.out2 = da1;
+    if (keepb || !h_da1.ok()) lb.out2 = da1;
+    lb.out2_hl = h_da1;
+    lb.range_flag = range_flag_;
     lb.addB = UP;
     lb.drop2 = dmask(0, l0, ls);
     ++launches_;
@@ -1443,14 +1475,19 @@ void Engine::encoder_adjoint(const EvalSpec& e, bool causal) {
           [&] { launch_ln_bwd(lb, active_, stream_); });
 
     g = mk(R, d, d, da1, L.w_o, d);
+    g.Ahl = h_da1;
     g.ep.kind = EPI_STORE;
     g.ep.out1 = dctx;
     gemm(g);
 
-    attention_bwd(G, qkv, qkv.offset(d), qkv.offset(2 * d), Pm, ctx, dctx, dPm, dqkv,
-                  dqkv.offset(d), dqkv.offset(2 * d), R / B_, R / B_, causal);
+    const Mat h_dqkv = dgrad_hl(G, 1, 3 * d);
+    const bool dqkv_hl =
+        attention_bwd(G, qkv, qkv.offset(d), qkv.offset(2 * d), Pm, ctx, dctx, dPm, dqkv,
+                      dqkv.offset(d), dqkv.offset(2 * d), R / B_, R / B_, causal, h_dqkv,
+                      h_dqkv.offset(d), h_dqkv.offset(2 * d), keepb);
 
     g = mk(R, d, 3 * d, dqkv, L.w_qkv, d);
+    if (dqkv_hl) g.Ahl = h_dqkv;
     g.ep.kind = EPI_STORE;
     g.ep.out1 = dn1;
     gemm(g);
@@ -1589,13 +1626,19 @@ void Engine::decoder_adjoint(const EvalSpec& e) {
       timed(PROF_ROW, 0.0, 8.0 * G * (double)R * d,
             [&] { launch_mask_copy(G, R, d, UPm, UPy, dmask(1, l0, ls), active_, stream_); });
     }
+    // pre-split dgrad A operands as in encoder_adjoint
+    const bool keepb = e.want_grads || e.bact.base != nullptr;
+    const Mat h_dh = dgrad_hl(G, 1, f), h_da1 = dgrad_hl(G, 0, d);
     GemmArgs g = mk(R, f, d, UPm, L.w_out, f);
     g.ep.kind = EPI_GELU_BWD;
-    g.ep.out1 = dh;
+    if (keepb || !h_dh.ok()) g.ep.out1 = dh;
+    g.ep.hl2 = h_dh;
+    g.ep.range_flag = range_flag_;
     g.ep.aux = hh;
     gemm(g);
 
     g = mk(R, d, f, dh, L.w_in, d);
+    g.Ahl = h_dh;
     g.ep.kind = EPI_STORE;
     g.ep.out1 = dn2;
     gemm(g);
@@ -1647,7 +1690,9 @@ void Engine::decoder_adjoint(const EvalSpec& e) {
     lb.addA = dy;
     lb.out1 = dy;     // du2 + du3
     lb.addB = dybar;
-    lb.out2 = da1;    // dybar + du3
+    lb.out2 = (keepb || !h_da1.ok()) ? da1 : Mat{};  // dybar + du3
+    lb.out2_hl = h_da1;
+    lb.range_flag = range_flag_;
     lb.drop2 = dmask(0, l0, ls);
     ++launches_;
     prof_shape_ = {4, lb.d, 0, lb.G};
@@ -1655,14 +1700,19 @@ void Engine::decoder_adjoint(const EvalSpec& e) {
           [&] { launch_ln_bwd(lb, active_, stream_); });
 
     g = mk(R, d, d, da1, L.w_o, d);
+    g.Ahl = h_da1;
     g.ep.kind = EPI_STORE;
     g.ep.out1 = dctx;
     gemm(g);
 
-    attention_bwd(G, qkv, qkv.offset(d), qkv.offset(2 * d), Pm, ctx, dctx, dPm, dqkv,
-                  dqkv.offset(d), dqkv.offset(2 * d), sy_, sy_, true);
+    const Mat h_dqkv = dgrad_hl(G, 1, 3 * d);
+    const bool dqkv_hl =
+        attention_bwd(G, qkv, qkv.offset(d), qkv.offset(2 * d), Pm, ctx, dctx, dPm, dqkv,
+                      dqkv.offset(d), dqkv.offset(2 * d), sy_, sy_, true, h_dqkv, h_dqkv.offset(d),
+                      h_dqkv.offset(2 * d), keepb);
 
     g = mk(R, d, 3 * d, dqkv, L.w_qkv, d);
+    if (dqkv_hl) g.Ahl = h_dqkv;
     g.ep.kind = EPI_STORE;
     g.ep.out1 = dn1;
     gemm(g);

@@ -251,11 +251,16 @@ class Engine {
   // next forward GEMM's A operand); empty when unavailable
   Mat hl_mat(int G, int which, int cols) const;
   bool p_hl_ok(int sq, int skv, const Mat& P) const;
+  Mat dgrad_hl(int G, int which, int cols) const;
   // the activations of this evaluation are the linearization the adjoint
   // reads (cache), not per-evaluation scratch
   bool keep_lin(const EvalSpec& e) const { return e.act.base != scratch_ || e.keep_act; }
-  void attention_bwd(int G, Mat Q, Mat K, Mat V, Mat P, Mat O, Mat dO, Mat dP, Mat dQ, Mat dK, Mat dV,
-                     int sq, int skv, bool causal);
+  // dQhl/dKhl/dVhl (optional): also write the gradients pre-split for the
+  // QKV dgrad (returns whether it did; the fp32 ones are then skipped unless
+  // keep32)
+  bool attention_bwd(int G, Mat Q, Mat K, Mat V, Mat P, Mat O, Mat dO, Mat dP, Mat dQ, Mat dK, Mat dV,
+                     int sq, int skv, bool causal, Mat dQhl = Mat{}, Mat dKhl = Mat{},
+                     Mat dVhl = Mat{}, bool keep32 = true);
   int gemm_blocks(const GemmArgs& g) const;
   Mat act_mat(const ActRef& r, long long off, int ld) const;
   Mat bwd_mat(const EvalSpec& e, long long off, int ld) const;

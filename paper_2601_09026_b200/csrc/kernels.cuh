@@ -27,6 +27,8 @@ struct LnBwdArgs {
   Mat addA, addB, out1, out2;
   Combine cmb;
   DropMask drop2;  // out2 = (addB + L) * mask: the VJP through a dropout site
+  Mat out2_hl;     // optional: out2 pre-split (hi|lo' rows) for the next dgrad GEMM
+  int* range_flag = nullptr;
 };
 void launch_ln_bwd(const LnBwdArgs& a, const int* active, cudaStream_t s);
 int ln_bwd_blocks(int rows);
@@ -126,6 +128,7 @@ struct AttnArgs {
   Mat Q, K, V, O, P;
   Mat dO, dQ, dK, dV;
   Mat Ohl;  // forward, optional: O pre-split (hi|lo' rows) for the O-projection
+  Mat dQhl, dKhl, dVhl;  // backward, optional: pre-split gradients for the QKV dgrad
   // s = 128 fused path (attn_tc.cu): P is kept in its pre-split form, the
   // forward's hi|lo' MMA operand tiles (64 KiB per problem, exactly the fp32
   // P slot), bulk-copied out by the forward and back in by the backward

@@ -127,6 +127,8 @@ __global__ void __launch_bounds__(256) ln_bwd_kernel(LnBwdArgs a, const int* act
     const float* addB = a.addB.ok() ? a.addB.at(g) + (long long)row * a.addB.ld : nullptr;
     float* o1 = a.out1.ok() ? a.out1.at(g) + (long long)row * a.out1.ld : nullptr;
     float* o2 = a.out2.ok() ? a.out2.at(g) + (long long)row * a.out2.ld : nullptr;
+    float* h2 = a.out2_hl.ok() ? a.out2_hl.at(g) + (long long)row * a.out2_hl.ld : nullptr;
+    float amax = 0.f;
     const bool comb = a.cmb.mode != CM_NONE;
     const long long off_out = comb ? (long long)row * a.cmb.out.ld : 0;
     const long long off_z = comb ? (long long)row * a.cmb.z.ld : 0;
@@ -137,10 +139,16 @@ __global__ void __launch_bounds__(256) ln_bwd_kernel(LnBwdArgs a, const int* act
         const float L = rstd * (dxh[i] - m1 - xh[i] * m2);
         const float v1 = addA ? addA[j] + L : L;
         if (o1) o1[j] = v1;
-        if (o2) o2[j] = a.drop2.on() ? (addB[j] + L) * drop_val(a.drop2, g, row, j) : addB[j] + L;
+        if (o2 || h2) {
+          const float w =
+              a.drop2.on() ? (addB[j] + L) * drop_val(a.drop2, g, row, j) : addB[j] + L;
+          if (o2) o2[j] = w;
+          if (h2) st_hl1(h2, j, w, amax);
+        }
         if (comb) combine_apply(a.cmb, g, off_out + j, off_z + j, v1, r2);
       }
     }
+    if (h2) hl_range_check(amax, a.range_flag);
   }
   if (a.cmb.mode == CM_RES0) {
     const double t = block_sum_f64(r2, red);
@@ -255,6 +263,8 @@ __global__ void __launch_bounds__(256) ln_bwd4_kernel(LnBwdArgs a, const int* ac
     const float* addB = a.addB.ok() ? a.addB.at(g) + (long long)row * a.addB.ld : nullptr;
     float* o1 = a.out1.ok() ? a.out1.at(g) + (long long)row * a.out1.ld : nullptr;
     float* o2 = a.out2.ok() ? a.out2.at(g) + (long long)row * a.out2.ld : nullptr;
+    float* h2 = a.out2_hl.ok() ? a.out2_hl.at(g) + (long long)row * a.out2_hl.ld : nullptr;
+    float amax = 0.f;
     const bool comb = a.cmb.mode != CM_NONE;
     const long long off_out = comb ? (long long)row * a.cmb.out.ld : 0;
     const long long off_z = comb ? (long long)row * a.cmb.z.ld : 0;
@@ -277,7 +287,7 @@ __global__ void __launch_bounds__(256) ln_bwd4_kernel(LnBwdArgs a, const int* ac
                                      rstd * (dxh[i].w - m1 - xh[i].w * m2));
         const float4 v1 = addA ? make_float4(ad[i].x + L.x, ad[i].y + L.y, ad[i].z + L.z, ad[i].w + L.w) : L;
         if (o1) st4(o1 + 4 * q, v1);
-        if (o2) {
+        if (o2 || h2) {
           const float4 b = addA ? ld4(addB + 4 * q) : ad[i];
           float4 w = make_float4(b.x + L.x, b.y + L.y, b.z + L.z, b.w + L.w);
           if (a.drop2.on()) {
@@ -286,11 +296,13 @@ __global__ void __launch_bounds__(256) ln_bwd4_kernel(LnBwdArgs a, const int* ac
             w.z *= drop_val(a.drop2, g, row, 4 * q + 2);
             w.w *= drop_val(a.drop2, g, row, 4 * q + 3);
           }
-          st4(o2 + 4 * q, w);
+          if (o2) st4(o2 + 4 * q, w);
+          if (h2) st_hl4(h2, 4 * q, w, amax);
         }
         if (comb) combine_apply4(a.cmb, g, off_out + 4 * q, off_z + 4 * q, v1, r2);
       }
     }
+    if (h2) hl_range_check(amax, a.range_flag);
   }
   if (a.cmb.mode == CM_RES0) {
     const double t = block_sum_f64(r2, red);
@@ -673,7 +685,7 @@ void launch_ln_bwd(const LnBwdArgs& a, const int* active, cudaStream_t s) {
   if (a.rows == 0 || a.G == 0) return;
   const Combine& c = a.cmb;
   if (a.d % 4 == 0 && vec_ok(a.x) && vec_ok(a.up) && vec_ok(a.gain) && vec_ok(a.addA) &&
-      vec_ok(a.addB) && vec_ok(a.out1) && vec_ok(a.out2) && vec_ok(c.z) && vec_ok(c.out) &&
+      vec_ok(a.addB) && vec_ok(a.out1) && vec_ok(a.out2) && vec_ok(a.out2_hl) && vec_ok(c.z) && vec_ok(c.out) &&
       vec_ok(c.base) && vec_ok(c.phib) && vec_ok(c.rho) && vec_ok(c.v))
     dispatch_rows4<LnBwd4L>(a.d, a, a.G, a.rows, active, s);
   else
