@@ -727,6 +727,21 @@ bool Engine::p_hl_ok(int sq, int skv, const Mat& P) const {
   return !off && sq == 128 && skv == 128 && P.ld == 128 && use_fused_attn();
 }
 
+// The adjoint's upstream state (lambda, or its dropout-masked copy) as the
+// first dgrad GEMM's pre-split A operand: one streaming pack (HBM-bound, ~1/3
+// of the converters' cost inside the MMA-bound GEMM) into hl buffer 0.
+Mat Engine::pack_upstream(int G, int rows, const Mat& up) {
+  Mat h = dgrad_hl(G, 0, sd_.d);
+  if (!h.ok()) return h;
+  ++launches_;
+  prof_shape_ = {8, sd_.d, 0, G};
+  timed(PROF_ROW, 0.0, 8.0 * G * (double)rows * sd_.d, [&] {
+    launch_pack_hl(up.at(0), up.step * up.slot_stride, up.ld, h.ptr, h.slot_stride, h.ld, G, rows,
+                   sd_.d, false, stream_, range_flag_);
+  });
+  return h;
+}
+
 // the adjoint's pre-split dgrad operands (MGLP_NO_PRESPLIT_DGRAD=1 disables)
 Mat Engine::dgrad_hl(int G, int which, int cols) const {
   static const bool off = [] {
@@ -1442,6 +1457,7 @@ void Engine::encoder_adjoint(const EvalSpec& e, bool causal) {
     const bool keepb = e.want_grads || e.bact.base != nullptr;
     const Mat h_dh = dgrad_hl(G, 1, f), h_da1 = dgrad_hl(G, 0, d);
     GemmArgs g = mk(R, f, d, UPm, L.w_out, f);
+    g.Ahl = pack_upstream(G, R, UPm);
     g.ep.kind = EPI_GELU_BWD;
     if (keepb || !h_dh.ok()) g.ep.out1 = dh;
     g.ep.hl2 = h_dh;
@@ -1630,6 +1646,7 @@ void Engine::decoder_adjoint(const EvalSpec& e) {
     const bool keepb = e.want_grads || e.bact.base != nullptr;
     const Mat h_dh = dgrad_hl(G, 1, f), h_da1 = dgrad_hl(G, 0, d);
     GemmArgs g = mk(R, f, d, UPm, L.w_out, f);
+    g.Ahl = pack_upstream(G, R, UPm);
     g.ep.kind = EPI_GELU_BWD;
     if (keepb || !h_dh.ok()) g.ep.out1 = dh;
     g.ep.hl2 = h_dh;

@@ -252,6 +252,7 @@ class Engine {
   Mat hl_mat(int G, int which, int cols) const;
   bool p_hl_ok(int sq, int skv, const Mat& P) const;
   Mat dgrad_hl(int G, int which, int cols) const;
+  Mat pack_upstream(int G, int rows, const Mat& up);
   // the activations of this evaluation are the linearization the adjoint
   // reads (cache), not per-evaluation scratch
   bool keep_lin(const EvalSpec& e) const { return e.act.base != scratch_ || e.keep_act; }

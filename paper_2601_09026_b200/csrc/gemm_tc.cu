@@ -543,9 +543,10 @@ __global__ void __launch_bounds__(Cfg<CG>::THREADS, 1)
 // (K zero-padded to a multiple of 32); with `transpose`, B = src^T.
 __global__ void pack_hl_kernel(const float* __restrict__ src, long long src_slot, int src_ld,
                                float* __restrict__ dst, long long dst_slot, int dst_ld, int G,
-                               int rows, int K, int transpose) {
+                               int rows, int K, int transpose, int vec, int* range_flag) {
   const int kblocks = (K + BK - 1) / BK;
   const long long n = (long long)G * rows * kblocks * 4;  // 8-value chunks
+  float amax = 0.f;
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x) {
     const int chunk = (int)(i % (kblocks * 4));
@@ -554,21 +555,28 @@ __global__ void pack_hl_kernel(const float* __restrict__ src, long long src_slot
     const int g = (int)(rg / rows);
     const int k0 = chunk * 8;
     float x[8];
+    if (vec) {  // row-major source, 16-byte rows, K % 8 == 0
+      const float4* p = reinterpret_cast<const float4*>(src + g * src_slot + (long long)r * src_ld + k0);
+      const float4 u = p[0], v = p[1];
+      x[0] = u.x; x[1] = u.y; x[2] = u.z; x[3] = u.w;
+      x[4] = v.x; x[5] = v.y; x[6] = v.z; x[7] = v.w;
+    } else {
 #pragma unroll
-    for (int e = 0; e < 8; ++e) {
-      const int k = k0 + e;
-      x[e] = k < K ? (transpose ? src[g * src_slot + (long long)k * src_ld + r]
-                                : src[g * src_slot + (long long)r * src_ld + k])
-                   : 0.f;
+      for (int e = 0; e < 8; ++e) {
+        const int k = k0 + e;
+        x[e] = k < K ? (transpose ? src[g * src_slot + (long long)k * src_ld + r]
+                                  : src[g * src_slot + (long long)r * src_ld + k])
+                     : 0.f;
+      }
     }
     uint4 hi, lo;
-    float amax = 0.f;
     split8(x, hi, lo, amax);
     uint8_t* row = reinterpret_cast<uint8_t*>(dst + g * dst_slot + (long long)r * dst_ld) +
                    (chunk >> 2) * 128;
     *reinterpret_cast<uint4*>(row + (chunk & 3) * 16) = hi;
     *reinterpret_cast<uint4*>(row + 64 + (chunk & 3) * 16) = lo;
   }
+  if (range_flag && amax >= 65520.f && amax <= FLT_MAX) atomicOr(range_flag, 1);
 }
 
 // ---- host side: tensor maps ---------------------------------------------------
@@ -838,14 +846,16 @@ long long pack_hl_cols(int K) { return (long long)ceil_div(K, BK) * BK; }
 
 void launch_pack_hl(const float* src, long long src_slot, int src_ld, float* dst,
                     long long dst_slot, int dst_ld, int G, int rows, int K, bool transpose,
-                    cudaStream_t s) {
+                    cudaStream_t s, int* range_flag) {
   if (G == 0 || rows == 0 || K == 0) return;
   if (dst_ld < pack_hl_cols(K) || (dst_ld % 4) || (reinterpret_cast<uintptr_t>(dst) & 15))
     throw ContractViolation("pack_hl: destination rows must hold pad32(K) 16-byte aligned floats");
   const long long n = (long long)G * rows * ceil_div(K, BK) * 4;
   const int blocks = (int)std::min<long long>(148 * 16, (n + 255) / 256);
+  const bool vec = !transpose && K % 32 == 0 && src_ld % 4 == 0 && src_slot % 4 == 0 &&
+                   (reinterpret_cast<uintptr_t>(src) & 15) == 0;
   pack_hl_kernel<<<blocks, 256, 0, s>>>(src, src_slot, src_ld, dst, dst_slot, dst_ld, G, rows, K,
-                                        transpose ? 1 : 0);
+                                        transpose ? 1 : 0, vec ? 1 : 0, range_flag);
   MGLP_CUDA(cudaGetLastError());
 }
 

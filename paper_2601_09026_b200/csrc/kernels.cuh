@@ -115,7 +115,7 @@ int gemm_tc_blocks(const GemmArgs& a);
 long long pack_hl_cols(int K);
 void launch_pack_hl(const float* src, long long src_slot, int src_ld, float* dst,
                     long long dst_slot, int dst_ld, int G, int rows, int K, bool transpose,
-                    cudaStream_t s);
+                    cudaStream_t s, int* range_flag = nullptr);
 
 // ---- fused attention (attn_tc.cu), sq, skv <= 128, dh in {32, 64} -------------
 // One CTA per (member g, batch b, head h); operands address (g, b, h) through

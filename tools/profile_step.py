@@ -52,7 +52,7 @@ for cls, M, Nn, K, b, fl, ms in rows:
 tot = rows[:, 6].sum()
 print(f"{name}: {n.value} launches, {tot:.1f} ms in profiled kernels")
 ROWK = {0: "row?", 1: "softmax", 2: "softmax_bwd", 3: "ln_fwd", 4: "ln_bwd", 5: "colred",
-        6: "combine", 7: "copy", 8: "correct"}
+        6: "combine", 7: "copy", 8: "correct|pack"}
 for key, (cnt, ms, fl) in sorted(agg.items(), key=lambda kv: -kv[1][1])[:60]:
     cls, M, Nn, K, b = key
     if cls == 2:  # row kernel: (kind, cols, -, G); fl = HBM bytes
