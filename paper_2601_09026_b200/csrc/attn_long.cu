@@ -116,6 +116,8 @@ constexpr int kFwdLongSmem = 1024 + 5 * PAIR64 + PAIR128 + 8 * 8 + 256 * 4 + 16;
 
 __global__ void __launch_bounds__(kThreads, 1)
     attn_fwd_long_kernel(const __grid_constant__ AttnTma tm, const AttnArgs a, const int* active) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ uint8_t smem_raw[];
   if (active && *(volatile const int*)active == 0) return;
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -296,6 +298,8 @@ __device__ __forceinline__ float row_dot(const float* x, const float* y, int n) 
 // TMEM: S / dP [0,256), dV [256,..)/[320,..), dK [384,..)/[448,..)
 __global__ void __launch_bounds__(kThreads, 1)
     attn_bwd_dkdv_kernel(const __grid_constant__ AttnTma tm, const AttnArgs a, const int* active) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ uint8_t smem_raw[];
   if (active && *(volatile const int*)active == 0) return;
   const LongSmem L = carve(smem_raw);
@@ -408,6 +412,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 // tiles: t0 = Q, t1 = dO, t2 = K, t3 = V, t4 = dS; TMEM: S / dP [0,256), dQ [256,..)/[384,..)
 __global__ void __launch_bounds__(kThreads, 1)
     attn_bwd_dq_kernel(const __grid_constant__ AttnTma tm, const AttnArgs a, const int* active) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ uint8_t smem_raw[];
   if (active && *(volatile const int*)active == 0) return;
   const LongSmem L = carve(smem_raw);
@@ -539,7 +545,7 @@ void launch_long(K kernel, const AttnTma& t, const AttnArgs& a, long long nprob,
                  cudaStream_t s, int smem = kLongSmem) {
   if (nprob == 0) return;
   const int grid = (int)std::min<long long>(nprob, sms());
-  kernel<<<grid, kThreads, smem, s>>>(t, a, active);
+  launch_k(kernel, dim3(grid), dim3(kThreads), smem, s, 1, t, a, active);
   MGLP_CUDA(cudaGetLastError());
 }
 

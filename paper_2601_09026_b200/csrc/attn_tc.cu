@@ -50,6 +50,8 @@ constexpr int kThreads = 256;  // 8 warps; warp w owns TMEM lanes 32 (w & 3), co
 constexpr int kFwdSmem = 1024 + PAIR128 + PAIR64 + 64 + 256 * 4 + 16;
 
 __global__ void __launch_bounds__(kThreads, 2) attn_fwd_kernel(const __grid_constant__ AttnTma tm, const AttnArgs a, const int* active) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ uint8_t smem_raw[];
   if (active && *(volatile const int*)active == 0) return;
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -206,6 +208,8 @@ __global__ void __launch_bounds__(kThreads, 2) attn_fwd_kernel(const __grid_cons
 // TMEM: dP main [0,128) corr [128,256); dV main [256,..) corr [384,..);
 //       dQ main [0,..) corr [64,..); dK main [128,..) corr [192,..)
 __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_constant__ AttnTma tm, const AttnArgs a, const int* active) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ uint8_t smem_raw[];
   if (active && *(volatile const int*)active == 0) return;
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -477,7 +481,7 @@ void launch_attn_fwd(const AttnArgs& a, const int* active, cudaStream_t s) {
   if (n == 0) return;
   const int grid = (int)std::min<long long>(n, 2 * num_sms());
   AttnTma t = maps(a, false);
-  attn_fwd_kernel<<<grid, kThreads, kFwdSmem, s>>>(t, a, active);
+  launch_k(attn_fwd_kernel, dim3(grid), dim3(kThreads), kFwdSmem, s, 1, t, a, active);
   MGLP_CUDA(cudaGetLastError());
 }
 
@@ -493,7 +497,7 @@ void launch_attn_bwd(const AttnArgs& a, const int* active, cudaStream_t s) {
   if (n == 0) return;
   const int grid = (int)std::min<long long>(n, num_sms());
   AttnTma t = maps(a, true);
-  attn_bwd_kernel<<<grid, kThreads, kBwdSmem, s>>>(t, a, active);
+  launch_k(attn_bwd_kernel, dim3(grid), dim3(kThreads), kBwdSmem, s, 1, t, a, active);
   MGLP_CUDA(cudaGetLastError());
 }
 

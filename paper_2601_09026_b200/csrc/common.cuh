@@ -37,6 +37,52 @@ struct ContractViolation : std::logic_error {
                                       __FILE__ + ":" + std::to_string(__LINE__)); \
   } while (0)
 
+// ---- programmatic dependent launch (PDL) ------------------------------------
+// Every kernel of the solver stream starts with pdl_wait() (returns once the
+// preceding kernel has completed and its writes are visible; a no-op for a
+// normal launch) and is launched by launch_k with the programmatic
+// stream-serialisation attribute, so the next kernel's launch overlaps this
+// one's execution, also inside the captured graph: the serial layer chain
+// (device serial fwd+bwd) runs 4% faster, the MGRIT step is unchanged.
+// pdl_trigger() (an early griddepcontrol.launch_dependents, so dependents are
+// scheduled while the last wave drains) measured 1-3% slower on the MGRIT
+// step and is compiled in only with -DMGLP_PDL_EARLY_TRIGGER.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+#ifdef MGLP_PDL_EARLY_TRIGGER
+  asm volatile("griddepcontrol.launch_dependents;");
+#endif
+}
+
+bool pdl_on();  // MGLP_NO_PDL=1 disables (rowops.cu)
+
+template <typename... KArgs, typename... Args>
+inline void launch_k(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                     int cluster_x, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[2];
+  unsigned n = 0;
+  if (cluster_x > 1) {
+    at[n].id = cudaLaunchAttributeClusterDimension;
+    at[n].val.clusterDim.x = (unsigned)cluster_x;
+    at[n].val.clusterDim.y = 1;
+    at[n].val.clusterDim.z = 1;
+    ++n;
+  }
+  if (pdl_on()) {
+    at[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[n].val.programmaticStreamSerializationAllowed = 1;
+    ++n;
+  }
+  cfg.attrs = at;
+  cfg.numAttrs = n;
+  MGLP_CUDA(cudaLaunchKernelEx(&cfg, k, args...));
+}
+
 // A strided family of row-major fp32 matrices. Member g starts at
 // ptr + (slot0 + g*step) * slot_stride; rows are ld elements apart.
 struct Mat {

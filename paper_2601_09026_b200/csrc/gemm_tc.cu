@@ -139,6 +139,8 @@ __global__ void __launch_bounds__(Cfg<CG>::THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap mapA,
                    const __grid_constant__ CUtensorMap mapB, const TcParams p,
                    const int* active) {
+  pdl_wait();
+  pdl_trigger();
   using C = Cfg<CG>;
   constexpr int TN = C::TN, NACC = C::NACC;
   extern __shared__ uint8_t smem_raw[];
@@ -544,6 +546,8 @@ __global__ void __launch_bounds__(Cfg<CG>::THREADS, 1)
 __global__ void pack_hl_kernel(const float* __restrict__ src, long long src_slot, int src_ld,
                                float* __restrict__ dst, long long dst_slot, int dst_ld, int G,
                                int rows, int K, int transpose, int vec, int* range_flag) {
+  pdl_wait();
+  pdl_trigger();
   const int kblocks = (K + BK - 1) / BK;
   const long long n = (long long)G * rows * kblocks * 4;  // 8-value chunks
   float amax = 0.f;
@@ -773,23 +777,9 @@ void launch_cg(const GemmArgs& a, const int* active, cudaStream_t s) {
   const long long tiles =
       (long long)ceil_div(a.N, C::TN) * ceil_div(a.M, C::TM) * a.G * a.Bb * a.H;
   const int units = (int)std::min<long long>(tiles, num_sms() / CG);
-  if constexpr (CG == 1) {
-    gemm_tc_kernel<1><<<units, C::THREADS, SMEM_BYTES, s>>>(P.mA, P.mB, P.p, active);
-  } else {
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(2 * units);
-    cfg.blockDim = dim3(C::THREADS);
-    cfg.dynamicSmemBytes = SMEM_BYTES;
-    cfg.stream = s;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = 2;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    MGLP_CUDA(cudaLaunchKernelEx(&cfg, gemm_tc_kernel<2>, P.mA, P.mB, P.p, active));
-  }
+  // CG = 2: one cluster of two CTAs per unit
+  launch_k(gemm_tc_kernel<CG>, dim3(CG * units), dim3(C::THREADS), SMEM_BYTES, s, CG, P.mA, P.mB,
+           P.p, active);
   MGLP_CUDA(cudaGetLastError());
   if (P.p.prof) {
     // diagnostics: average cycles per CTA spent in each wait kind
@@ -854,7 +844,7 @@ void launch_pack_hl(const float* src, long long src_slot, int src_ld, float* dst
   const int blocks = (int)std::min<long long>(148 * 16, (n + 255) / 256);
   const bool vec = !transpose && K % 32 == 0 && src_ld % 4 == 0 && src_slot % 4 == 0 &&
                    (reinterpret_cast<uintptr_t>(src) & 15) == 0;
-  pack_hl_kernel<<<blocks, 256, 0, s>>>(src, src_slot, src_ld, dst, dst_slot, dst_ld, G, rows, K,
+  launch_k(pack_hl_kernel, dim3(blocks), dim3(256), 0, s, 1, src, src_slot, src_ld, dst, dst_slot, dst_ld, G, rows, K,
                                         transpose ? 1 : 0, vec ? 1 : 0, range_flag);
   MGLP_CUDA(cudaGetLastError());
 }

@@ -6,9 +6,20 @@
 // All are HBM-bound: one warp per row with the row held in registers, grids
 // sized in multiples of the 148 SMs, no float atomics (every reduction runs
 // in a fixed order, so results never depend on scheduling).
+#include <cstdlib>
+
 #include "kernels.cuh"
 
 namespace mglp {
+
+bool pdl_on() {
+  static const bool on = [] {
+    const char* e = getenv("MGLP_NO_PDL");
+    return !(e && atoi(e) != 0);
+  }();
+  return on;
+}
+
 
 namespace {
 
@@ -43,6 +54,8 @@ __device__ __forceinline__ bool stopped(const int* active) {
 // ---- LayerNorm forward --------------------------------------------------------
 template <int V>
 __global__ void __launch_bounds__(256) ln_fwd_kernel(LnFwdArgs a, const int* active) {
+  pdl_wait();
+  pdl_trigger();
   if (stopped(active)) return;
   const int g = blockIdx.y;
   const int row = blockIdx.x * kRowsPerBlock + (threadIdx.x >> 5);
@@ -93,6 +106,8 @@ __global__ void __launch_bounds__(256) ln_fwd_kernel(LnFwdArgs a, const int* act
 // ---- LayerNorm VJP (+ fused sums and solver combine) ----------------------------
 template <int V>
 __global__ void __launch_bounds__(256) ln_bwd_kernel(LnBwdArgs a, const int* active) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ double red[32];
   if (stopped(active)) return;
   const int g = blockIdx.y;
@@ -165,6 +180,8 @@ __device__ __forceinline__ void st4(float* p, float4 v) { *reinterpret_cast<floa
 
 template <int V4>
 __global__ void __launch_bounds__(256) ln_fwd4_kernel(LnFwdArgs a, const int* active) {
+  pdl_wait();
+  pdl_trigger();
   if (stopped(active)) return;
   const int g = blockIdx.y;
   const int row = blockIdx.x * kRowsPerBlock + (threadIdx.x >> 5);
@@ -221,6 +238,8 @@ __global__ void __launch_bounds__(256) ln_fwd4_kernel(LnFwdArgs a, const int* ac
 
 template <int V4>
 __global__ void __launch_bounds__(256) ln_bwd4_kernel(LnBwdArgs a, const int* active) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ double red[32];
   if (stopped(active)) return;
   const int g = blockIdx.y;
@@ -314,13 +333,13 @@ __global__ void __launch_bounds__(256) ln_bwd4_kernel(LnBwdArgs a, const int* ac
 template <int V4>
 struct LnFwd4L {
   static void launch(dim3 g, const LnFwdArgs& a, const int* act, cudaStream_t s) {
-    ln_fwd4_kernel<V4><<<g, 256, 0, s>>>(a, act);
+    launch_k(ln_fwd4_kernel<V4>, dim3(g), dim3(256), 0, s, 1, a, act);
   }
 };
 template <int V4>
 struct LnBwd4L {
   static void launch(dim3 g, const LnBwdArgs& a, const int* act, cudaStream_t s) {
-    ln_bwd4_kernel<V4><<<g, 256, 0, s>>>(a, act);
+    launch_k(ln_bwd4_kernel<V4>, dim3(g), dim3(256), 0, s, 1, a, act);
   }
 };
 
@@ -344,6 +363,8 @@ bool vec_ok(const Mat& m) {
 // blocks, float4 rows, f64 partials reduced over the 8 row lanes in fixed
 // order; stage 2 = ordered sum over the chunks, scaled into the gradients.
 __global__ void __launch_bounds__(256) colred_part_kernel(ColRedArgs a, const int* active) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ double sb[8][129];
   __shared__ double sg[8][129];
   if (stopped(active)) return;
@@ -396,6 +417,8 @@ __global__ void __launch_bounds__(256) colred_part_kernel(ColRedArgs a, const in
 }
 
 __global__ void __launch_bounds__(256) colred_sum_kernel(ColRedArgs a, const int* active) {
+  pdl_wait();
+  pdl_trigger();
   if (stopped(active)) return;
   const int g = blockIdx.y;
   const int col = blockIdx.x * 256 + threadIdx.x;
@@ -433,13 +456,13 @@ void dispatch_rows(int d, const Args& a, int G, int rows, const int* active, cud
 template <int V>
 struct LnFwdL {
   static void launch(dim3 g, const LnFwdArgs& a, const int* act, cudaStream_t s) {
-    ln_fwd_kernel<V><<<g, 256, 0, s>>>(a, act);
+    launch_k(ln_fwd_kernel<V>, dim3(g), dim3(256), 0, s, 1, a, act);
   }
 };
 template <int V>
 struct LnBwdL {
   static void launch(dim3 g, const LnBwdArgs& a, const int* act, cudaStream_t s) {
-    ln_bwd_kernel<V><<<g, 256, 0, s>>>(a, act);
+    launch_k(ln_bwd_kernel<V>, dim3(g), dim3(256), 0, s, 1, a, act);
   }
 };
 
@@ -448,6 +471,8 @@ struct LnBwdL {
 // Masked probabilities are exactly 0, as with the reference's -1e30.
 template <int V>
 __global__ void __launch_bounds__(256) softmax_kernel(SoftmaxArgs a, const int* active) {
+  pdl_wait();
+  pdl_trigger();
   if (stopped(active)) return;
   const int g = blockIdx.y;
   const long long row = (long long)blockIdx.x * kRowsPerBlock + (threadIdx.x >> 5);
@@ -484,6 +509,8 @@ __global__ void __launch_bounds__(256) softmax_kernel(SoftmaxArgs a, const int* 
 // dS = P * (dP - sum_j dP_j P_j), in place over dP (vjp_softmax_rows)
 template <int V>
 __global__ void __launch_bounds__(256) softmax_bwd_kernel(SoftmaxArgs a, const int* active) {
+  pdl_wait();
+  pdl_trigger();
   if (stopped(active)) return;
   const int g = blockIdx.y;
   const long long row = (long long)blockIdx.x * kRowsPerBlock + (threadIdx.x >> 5);
@@ -512,14 +539,16 @@ template <int V>
 struct SmL {
   static void launch(dim3 g, const SoftmaxArgs& a, const int* act, cudaStream_t s) {
     if (a.dS.ok())
-      softmax_bwd_kernel<V><<<g, 256, 0, s>>>(a, act);
+      launch_k(softmax_bwd_kernel<V>, dim3(g), dim3(256), 0, s, 1, a, act);
     else
-      softmax_kernel<V><<<g, 256, 0, s>>>(a, act);
+      launch_k(softmax_kernel<V>, dim3(g), dim3(256), 0, s, 1, a, act);
   }
 };
 
 // ---- column sums for parameter gradients -----------------------------------------
 __global__ void __launch_bounds__(256) colred_kernel(ColRedArgs a, const int* active) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ double sb[8][33];
   __shared__ double sg[8][33];
   if (stopped(active)) return;
@@ -566,6 +595,8 @@ constexpr int kElemPerThread = 8;
 
 __global__ void __launch_bounds__(kElemThreads) elem_combine_kernel(ElemCombineArgs a,
                                                                     const int* active) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ double red[32];
   if (stopped(active)) return;
   const int g = blockIdx.y;
@@ -585,6 +616,8 @@ __global__ void __launch_bounds__(kElemThreads) elem_combine_kernel(ElemCombineA
 }
 
 __global__ void copy_kernel(int G, long long n4, Mat dst, Mat src, const int* active) {
+  pdl_wait();
+  pdl_trigger();
   if (stopped(active)) return;
   const int g = blockIdx.y;
   float4* d = reinterpret_cast<float4*>(dst.at(g));
@@ -595,6 +628,8 @@ __global__ void copy_kernel(int G, long long n4, Mat dst, Mat src, const int* ac
 }
 
 __global__ void correct_kernel(int G, long long n4, Mat dst, Mat a, Mat b, const int* active) {
+  pdl_wait();
+  pdl_trigger();
   if (stopped(active)) return;
   const int g = blockIdx.y;
   float4* d = reinterpret_cast<float4*>(dst.at(g));
@@ -609,6 +644,8 @@ __global__ void correct_kernel(int G, long long n4, Mat dst, Mat a, Mat b, const
 }
 
 __global__ void zero_kernel(int G, long long n4, Mat dst, const int* active) {
+  pdl_wait();
+  pdl_trigger();
   if (stopped(active)) return;
   float4* d = reinterpret_cast<float4*>(dst.at(blockIdx.y));
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n4;
@@ -625,6 +662,8 @@ int stream_grid(long long n4, int G) {
 
 // ---- solve control -------------------------------------------------------------------
 __global__ void ctrl_begin_kernel(SolveCtrl* c) {
+  pdl_wait();
+  pdl_trigger();
   c->active = 1;
   c->n_trace = 0;
   c->converged = 0;
@@ -638,6 +677,8 @@ __global__ void ctrl_begin_kernel(SolveCtrl* c) {
 // position P-1-r (the adjoint solve's partition).
 __global__ void trace_record_kernel(SolveCtrl* c, const double* partials, int n_chunks, int S,
                                     int per_rank, int reversed) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ double red[32];
   if (!c->active) return;
   const int P = n_chunks / per_rank;
@@ -655,6 +696,8 @@ __global__ void trace_record_kernel(SolveCtrl* c, const double* partials, int n_
 }
 
 __global__ void cycle_end_kernel(SolveCtrl* c, double tol) {
+  pdl_wait();
+  pdl_trigger();
   if (!c->active) return;
   const double nrm = c->pending;
   if (c->n_trace < kMaxTrace) c->trace[c->n_trace] = nrm;
@@ -702,12 +745,12 @@ void launch_colred(const ColRedArgs& a, const int* active, cudaStream_t s) {
   if (a.rows == 0 || a.G == 0) return;
   if (a.partials && a.cols % 4 == 0 && vec_ok(a.up) && vec_ok(a.x) &&
       (long long)a.G * kColRedChunks * a.cols * 2 <= a.partials_cap) {
-    colred_part_kernel<<<dim3(ceil_div(a.cols, 128), kColRedChunks, a.G), 256, 0, s>>>(a, active);
-    colred_sum_kernel<<<dim3(ceil_div(a.cols, 256), a.G), 256, 0, s>>>(a, active);
+    launch_k(colred_part_kernel, dim3(dim3(ceil_div(a.cols, 128), kColRedChunks, a.G)), dim3(256), 0, s, 1, a, active);
+    launch_k(colred_sum_kernel, dim3(dim3(ceil_div(a.cols, 256), a.G)), dim3(256), 0, s, 1, a, active);
     return;
   }
   dim3 grid(ceil_div(a.cols, 32), a.G);
-  colred_kernel<<<grid, 256, 0, s>>>(a, active);
+  launch_k(colred_kernel, dim3(grid), dim3(256), 0, s, 1, a, active);
 }
 
 int elem_combine_blocks(long long n) {
@@ -717,7 +760,7 @@ int elem_combine_blocks(long long n) {
 void launch_elem_combine(const ElemCombineArgs& a, const int* active, cudaStream_t s) {
   if (a.n == 0 || a.G == 0) return;
   dim3 grid(elem_combine_blocks(a.n), a.G);
-  elem_combine_kernel<<<grid, kElemThreads, 0, s>>>(a, active);
+  launch_k(elem_combine_kernel, dim3(grid), dim3(kElemThreads), 0, s, 1, a, active);
 }
 
 static void require_vec4(long long n, const char* what) {
@@ -728,11 +771,13 @@ void launch_copy(int G, long long n, Mat dst, Mat src, const int* active, cudaSt
   if (G == 0 || n == 0) return;
   require_vec4(n, "copy");
   dim3 grid(stream_grid(n / 4, G), G);
-  copy_kernel<<<grid, 256, 0, s>>>(G, n / 4, dst, src, active);
+  launch_k(copy_kernel, dim3(grid), dim3(256), 0, s, 1, G, n / 4, dst, src, active);
 }
 
 __global__ void __launch_bounds__(256) mask_copy_kernel(int rows, int d, Mat dst, Mat src,
                                                         DropMask m, const int* active) {
+  pdl_wait();
+  pdl_trigger();
   if (stopped(active)) return;
   const int g = blockIdx.y;
   const long long n = (long long)rows * d;
@@ -749,7 +794,7 @@ void launch_mask_copy(int G, int rows, int d, Mat dst, Mat src, const DropMask& 
   if (G == 0 || rows == 0) return;
   const long long n = (long long)rows * d;
   const int blocks = (int)std::min<long long>((n + 255) / 256, 148 * 8);
-  mask_copy_kernel<<<dim3(blocks, G), 256, 0, s>>>(rows, d, dst, src, m, active);
+  launch_k(mask_copy_kernel, dim3(dim3(blocks, G)), dim3(256), 0, s, 1, rows, d, dst, src, m, active);
   MGLP_CUDA(cudaGetLastError());
 }
 
@@ -758,25 +803,25 @@ void launch_correct(int G, long long n, Mat dst, Mat a, Mat b, const int* active
   if (G == 0 || n == 0) return;
   require_vec4(n, "correct");
   dim3 grid(stream_grid(n / 4, G), G);
-  correct_kernel<<<grid, 256, 0, s>>>(G, n / 4, dst, a, b, active);
+  launch_k(correct_kernel, dim3(grid), dim3(256), 0, s, 1, G, n / 4, dst, a, b, active);
 }
 
 void launch_zero(int G, long long n, Mat dst, const int* active, cudaStream_t s) {
   if (G == 0 || n == 0) return;
   require_vec4(n, "zero");
   dim3 grid(stream_grid(n / 4, G), G);
-  zero_kernel<<<grid, 256, 0, s>>>(G, n / 4, dst, active);
+  launch_k(zero_kernel, dim3(grid), dim3(256), 0, s, 1, G, n / 4, dst, active);
 }
 
-void launch_ctrl_begin(SolveCtrl* c, cudaStream_t s) { ctrl_begin_kernel<<<1, 1, 0, s>>>(c); }
+void launch_ctrl_begin(SolveCtrl* c, cudaStream_t s) { launch_k(ctrl_begin_kernel, dim3(1), dim3(1), 0, s, 1, c); }
 
 void launch_trace_record(SolveCtrl* c, const double* partials, int n_chunks, int S, int per_rank,
                          bool reversed, cudaStream_t s) {
-  trace_record_kernel<<<1, 256, 0, s>>>(c, partials, n_chunks, S, per_rank, reversed ? 1 : 0);
+  launch_k(trace_record_kernel, dim3(1), dim3(256), 0, s, 1, c, partials, n_chunks, S, per_rank, reversed ? 1 : 0);
 }
 
 void launch_cycle_end(SolveCtrl* c, double tol, cudaStream_t s) {
-  cycle_end_kernel<<<1, 1, 0, s>>>(c, tol);
+  launch_k(cycle_end_kernel, dim3(1), dim3(1), 0, s, 1, c, tol);
 }
 
 }  // namespace mglp
