@@ -643,9 +643,9 @@ void Engine::repack_weights() {
       float* dn = Whl_ + (long long)l0 * hl_stride_ + w.n_off;
       float* dt = Whl_ + (long long)l0 * hl_stride_ + w.t_off;
       launch_pack_hl(src, layer_stride_, w.cols, dn, hl_stride_, (int)pack_hl_cols(w.cols), nl,
-                     w.rows, w.cols, false, stream_);
+                     w.rows, w.cols, false, stream_, range_flag_);
       launch_pack_hl(src, layer_stride_, w.cols, dt, hl_stride_, (int)pack_hl_cols(w.rows), nl,
-                     w.cols, w.rows, true, stream_);
+                     w.cols, w.rows, true, stream_, range_flag_);
     }
   }
 }
