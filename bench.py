@@ -144,42 +144,53 @@ def mgrit_critical_path(N, cf, levels, P):
 
 def reference_sample(cfg, workers):
     """Times the compiled reference's LayerStack::step and ::adjoint_step (with
-    grads) single-threaded at batch 1 on the config's block shape, and
-    extrapolates one MGRIT fwd+bwd iteration (ms) at the config's batch with
-    the reference Executor's critical path on `workers` ideal workers (no
-    contention assumed -- this favours the reference)."""
+    grads) at batch 1 on the config's block shape, `workers` of them running
+    concurrently on distinct layers (one host thread each -- what the
+    reference Executor does with its chunk tasks, memory contention included),
+    and extrapolates one MGRIT fwd+bwd iteration (ms) at the config's batch
+    from the Executor's critical path in such rounds of `workers` Phi."""
+    import threading
+
     import numpy as np
     from oracle import ref as R
     kind = cfg["kind"]
+    P = workers
     rc = R.RefStackConfig(kind=kind, d=cfg["d"], heads=cfg["H"], ffn=cfg["ffn"])
     if kind == "encoder":
-        rc.n_enc, rc.n_dec = 1, 0
+        rc.n_enc, rc.n_dec = P, 0
     elif kind == "decoder_only":
-        rc.n_enc, rc.n_dec = 0, 1
-    else:
-        rc.n_enc, rc.n_dec = 1, 1
+        rc.n_enc, rc.n_dec = 0, P
+    else:  # half encoder, half decoder layers in every round
+        rc.n_enc, rc.n_dec = (P + 1) // 2, max(1, P // 2)
     st = R.RefStack(rc, 7)
     d, sx, sy = cfg["d"], cfg["sx"], cfg["sy"]
     n = (sx + sy) * d
     z = R.gaussian_fill(7, K_TEST, 7, n, 0.5)
     lam = R.gaussian_fill(8, K_TEST, 8, n, 1.0)
     g = np.zeros(st.num_params())
-    times = {"enc": None, "dec": None}
-    for name, layer in (("enc", 0), ("dec", st.total - 1)):
-        if kind == "encoder_decoder" or name == "enc":
-            t0 = time.perf_counter()
-            st.step(layer, 1.0, z, 1, sx, sy)
-            t1 = time.perf_counter()
-            st.adjoint_step(layer, 1.0, z, lam, 1, sx, sy, grads=g, gscale=1.0)
-            t2 = time.perf_counter()
-            times[name] = (t1 - t0, t2 - t1)
-    if kind == "encoder_decoder":
-        t_step = (times["enc"][0] + times["dec"][0]) / 2
-        t_adj = (times["enc"][1] + times["dec"][1]) / 2
-    else:
-        t_step, t_adj = times["enc"]
+    layers = list(range(st.total))[:P]
+
+    def concurrent(fn):
+        ts = [threading.Thread(target=fn, args=(layer,)) for layer in layers]
+        t0 = time.perf_counter()
+        for t in ts:
+            t.start()
+        for t in ts:
+            t.join()
+        return time.perf_counter() - t0
+
+    def one(fn):
+        t0 = time.perf_counter()
+        fn(layers[0])
+        return time.perf_counter() - t0
+
+    step = lambda layer: st.step(layer, 1.0, z, 1, sx, sy)  # noqa: E731
+    adj = lambda layer: st.adjoint_step(layer, 1.0, z, lam, 1, sx, sy, grads=g,  # noqa: E731
+                                        gscale=1.0)
+    # ctypes releases the GIL for the duration of each reference call
+    t_step, t_adj = concurrent(step), concurrent(adj)
+    t1_step, t1_adj = one(step), one(adj)
     N = cfg["n_enc"] + cfg["n_dec"]
-    P = workers
     cp = mgrit_critical_path(N, cfg["cf"], cfg["levels"], P)
     B = cfg["B"]
     # forward: k_f cycles; backward: k_b cycles + parameter pass (N tasks).
@@ -187,14 +198,15 @@ def reference_sample(cfg, workers):
     # Phi^T without gradients costs the same as one with.
     fwd = cfg["fwd"] * cp * t_step * B
     bwd = (cfg["bwd"] * cp + -(-N // P)) * t_adj * B
-    serial = N * (t_step + t_adj) * B
+    serial = N * (t1_step + t1_adj) * B  # one thread, layer after layer
     return {"ms": (fwd + bwd) * 1e3, "serial_ms": serial * 1e3, "t_step_s": t_step,
             "t_adjoint_step_s": t_adj, "threads": P,
-            "sample": (f"LayerStack::step + ::adjoint_step(grads) timed single-threaded at batch 1 "
-                       f"on the config's block shape (compiled reference, oracle/_ref); "
-                       f"extrapolated to one MGRIT {cfg['fwd']}+{cfg['bwd']} iteration at batch "
-                       f"{B}: {cp} Phi per cycle on the critical path of the reference Executor "
-                       f"with {P} ideal workers (t_step={t_step:.3g}s, t_adj={t_adj:.3g}s)")}
+            "sample": (f"{P} concurrent LayerStack::step and {P} concurrent ::adjoint_step(grads) "
+                       f"(one host thread per layer, compiled reference oracle/_ref) at batch 1 "
+                       f"on the config's block shape; extrapolated to one MGRIT "
+                       f"{cfg['fwd']}+{cfg['bwd']} iteration at batch {B}: {cp} rounds of {P} Phi "
+                       f"per cycle on the reference Executor's critical path (round t_step="
+                       f"{t_step:.3g}s, t_adj={t_adj:.3g}s)")}
 
 
 def run_reference_arm(args, cfg, rank, world):
@@ -222,7 +234,6 @@ def run_reference_arm(args, cfg, rank, world):
                    f"cf={cfg['cf']} levels={cfg['levels']} fwd={cfg['fwd']} bwd={cfg['bwd']}"},
         "serial_ms": statistics.median(s["serial_ms"] for s in samples),
         "cpu_baseline": {"value": ms, "unit": "ms/iteration", "cores": threads,
-                         "measured_threads": 1,
                          "kind": "reference", "sample": s0["sample"]},
         "e2e": {"value": ms, "unit": "ms/iteration", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
@@ -474,7 +485,6 @@ def run_device(args, cfg, rank, world, dist):
                 threads = max(1, min(os.cpu_count() or 1, cfg["n_enc"] + cfg["n_dec"]))
                 s = reference_sample(cfg, threads)
                 cpu = {"value": s["ms"], "unit": "ms/iteration", "cores": threads,
-                       "measured_threads": 1,
                        "kind": "reference", "sample": s["sample"],
                        "serial_ms": s["serial_ms"]}
         except Exception as ex:  # reported, never fatal
