@@ -487,7 +487,10 @@ void Engine::set_shape(int batch, int s_x, int s_y) {
     hl_slot_ = 0;
     const int dh = sd_.d / sd_.heads;
     if (!off && sd_.d % 32 == 0 && sd_.ffn % 32 == 0 && dh % 32 == 0) {
-      hl_slot_ = (long long)std::max(Tx_, Ty_) * (sd_.d + std::max(sd_.d, sd_.ffn));
+      // buffer 0: LN outputs / da1 / the upstream ([rows][d]); buffer 1:
+      // attention O, GELU output, dh, dqkv ([rows][max(ffn, 3d)])
+      hl_w1_ = std::max(sd_.ffn, 3 * sd_.d);
+      hl_slot_ = (long long)std::max(Tx_, Ty_) * (sd_.d + hl_w1_);
       MGLP_CUDA(cudaMalloc(&hlscr_, (size_t)Gmax_ * hl_slot_ * sizeof(float)));
       hl_cap_ = Gmax_;
     }
@@ -708,7 +711,7 @@ Mat Engine::hl_mat(int G, int which, int cols) const {
   (void)cols;
   return m;  // the SIMT GEMMs read fp32 operands only
 #else
-  if (!hlscr_ || G > hl_cap_ || cols % 32) return m;
+  if (!hlscr_ || G > hl_cap_ || cols % 32 || cols > (which ? hl_w1_ : sd_.d)) return m;
   m.ptr = hlscr_ + (which ? (long long)std::max(Tx_, Ty_) * sd_.d : 0);
   m.slot_stride = hl_slot_;
   m.ld = cols;

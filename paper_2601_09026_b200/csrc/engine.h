@@ -348,6 +348,7 @@ class Engine {
   float* hlscr_ = nullptr;
   long long hl_slot_ = 0;
   int hl_cap_ = 0;
+  int hl_w1_ = 0;  // row width (floats) of buffer 1
   float* cache_ = nullptr;    // total_ forward activation slots (slot = layer)
   float* bscratch_ = nullptr; // Gmax backward slots
   double* colred_part_ = nullptr;  // f64 column-sum partials (rowops.cu colred)
