@@ -1,0 +1,57 @@
+"""Pre-split operand paths against the compiled reference: with d, ffn and
+the head width multiples of 32 every forward and dgrad GEMM reads its A
+operand pre-split (LayerNorm, attention O / dQKV, GELU and GELU' epilogues,
+LayerNorm VJP, the upstream pack), for all three stack kinds including
+cross-attention, with ffn < 3d (the dQKV rows are the widest pre-split
+buffer). The small golden stacks (d = 16) never take these paths."""
+import numpy as np
+import pytest
+
+from oracle import ref as R
+from paper_2601_09026_b200 import LayerParallelEngine, LayerStack, SolveConfig, StackConfig, State
+
+pytestmark = [pytest.mark.gpu,
+              pytest.mark.skipif(not R.available(), reason="reference oracle not built")]
+
+D, H, F = 64, 2, 96
+CASES = [  # kind, n_enc, n_dec, (B, sx, sy), causal buffers
+    ("encoder", 6, 0, (2, 16, 0), (0, 0)),
+    ("decoder_only", 0, 6, (2, 24, 0), (1, 1)),
+    ("encoder_decoder", 3, 3, (2, 16, 8), (0, 0)),
+]
+
+
+def rel(a, b):
+    a, b = np.asarray(a, np.float64), np.asarray(b, np.float64)
+    return float(np.abs(a - b).max() / max(float(np.abs(b).max()), 1e-300))
+
+
+@pytest.mark.parametrize("case", CASES)
+def test_engine_with_presplit_operands_matches_reference(case):
+    kind, n_enc, n_dec, (b, sx, sy), buf = case
+    cfg = StackConfig(kind=kind, d=D, heads=H, ffn=F, n_enc=n_enc, n_dec=n_dec,
+                      buffer_open=buf[0], buffer_close=buf[1])
+    st = LayerStack(cfg, 11)
+    rc = R.RefStackConfig(kind=kind, d=D, heads=H, ffn=F)
+    rc.n_enc, rc.n_dec = n_enc, n_dec
+    rc.buffer_open, rc.buffer_close = buf
+    ref = R.RefStack(rc, 11)
+    n = ref.state_size(b, sx, sy)
+    z0 = R.gaussian_fill(2, 6, 2, n, 0.5)
+    lam = R.gaussian_fill(3, 6, 3, n, 1.0)
+    interior = st.interior_end() - st.interior_begin()
+    cf = 3 if interior % 3 == 0 else 2
+    eng = LayerParallelEngine(st, SolveConfig(coarsen=cf, levels=2, fwd_iters=2, bwd_iters=2,
+                                              warm_start=False))
+    reng = R.RefEngine(ref, coarsen=cf, levels=2, fwd_iters=2, bwd_iters=2, warm_start=False)
+    fo = eng.forward(State.from_flat(z0, b, sx, sy, D))
+    rtraj, rft, _ = reng.forward(z0, b, sx, sy)
+    assert rel(np.stack([s.flat() for s in fo.traj]), rtraj) < 1e-4
+    assert rel(fo.phase.trace, rft) < 1e-4
+    g = st.zero_grads()
+    bo = eng.backward(fo.traj, State.from_flat(lam, b, sx, sy, D), g)
+    rg = np.zeros(ref.num_params())
+    rl0, rbt, _ = reng.backward(rtraj, lam, b, sx, sy, grads=rg)
+    assert rel(bo.lambda0.flat(), rl0) < 1e-4
+    assert rel(bo.phase.trace, rbt) < 1e-4
+    assert rel(g, rg) < 1e-4
