@@ -6,13 +6,14 @@
 // The probabilities are never stored: the forward keeps two per-row
 // statistics (the row max m of the scaled, masked scores and 1/l with l the
 // row sum of exp(s - m)) in the P slot of the activation arena, and the
-// backward recomputes P = exp(s - m) / l bit-identically from Q, K and those
-// statistics (same MMAs, same order, same exponential). The backward also
-// keeps t_i = dO_i . O_i there ([2 sq + i]).
+// backward recomputes P = exp(s - m) / l from Q, K and those statistics (same
+// MMAs, same order, same exponential as the forward's P~ = exp(s - m)). The
+// backward also keeps t_i = dO_i . O_i there ([2 sq + i]).
 //
 //   forward  (CTA per member, batch, head, 128-query block)
-//     pass A: per key block S = Q K^T (3-pass split MMA) -> online (m, l)
-//     pass B: per key block S again -> P = exp(S*scale - m) / l -> O += P V
+//     pass A: per key block S = Q K^T (3-pass split MMA) -> row max m only
+//     pass B: per key block S again -> P~ = exp(S*scale - m) -> O += P~ V,
+//             l += sum P~; the epilogue writes O / l
 //   backward, two deterministic kernels (no atomics, no split-K reductions):
 //     dK/dV  (CTA per 128-key block): loops over the query blocks that see it,
 //            dV += P^T dO, dK += dS^T Q accumulated in TMEM
@@ -208,40 +209,25 @@ __global__ void __launch_bounds__(kThreads, 1)
       float v[64];
       read64(trow, c0, v);
       if (!pb) {
-        // online (max, sum of exp) of the scaled, masked scores
+        // pass A: the row max of the scaled, masked scores only
         const int lim = key_limit(q, kb * 128 + c0, skv, a.causal != 0, true);
         float mh = -INFINITY;
 #pragma unroll
-        for (int e = 0; e < 64; ++e) {
-          v[e] = e < lim ? v[e] * a.scale : -INFINITY;
-          mh = fmaxf(mh, v[e]);
-        }
+        for (int e = 0; e < 64; ++e) mh = fmaxf(mh, e < lim ? v[e] * a.scale : -INFINITY);
         xch[half * 128 + i] = mh;
         sync_all();
-        const float mb = fmaxf(xch[i], xch[128 + i]);
-        const float mn = fmaxf(m, mb);
-        float sh = 0.f;
-        if (mn != -INFINITY) {
-#pragma unroll
-          for (int e = 0; e < 64; ++e) sh += v[e] == -INFINITY ? 0.f : fast_exp(v[e] - mn);
-        }
-        sync_all();
-        xch[half * 128 + i] = sh;
-        sync_all();
-        if (mn != -INFINITY) {
-          const float sc = m == -INFINITY ? 0.f : fast_exp(m - mn);
-          l = l * sc + (xch[i] + xch[128 + i]);
-          m = mn;
-        }
-        if (st == kend - 1) inv = l > 0.f ? 1.f / l : 0.f;
+        m = fmaxf(m, fmaxf(xch[i], xch[128 + i]));
         sync_all();  // xch reads done; S consumed
       } else {
-        // P = exp(S*scale - m) / l -> tile; O += P V
+        // pass B: P~ = exp(S*scale - m) (the final row max: no rescaling) ->
+        // tile; O += P~ V; l += sum P~; O is normalised by 1/l at the end
         const int vbuf = kb & 1;
         mbar_wait(&bV[vbuf], nv[vbuf] & 1);
         ++nv[vbuf];
         conv_inplace(tV[vbuf], 128, 128, dh, tid, kThreads, amax);
-        probs(v, q, kb * 128 + c0, skv, a.causal != 0, q < sq, a.scale, m, inv);
+        probs(v, q, kb * 128 + c0, skv, a.causal != 0, q < sq, a.scale, m, 1.f);
+#pragma unroll
+        for (int e = 0; e < 64; ++e) l += v[e];
 #pragma unroll
         for (int c = 0; c < 8; ++c) put8(Pk.hi, Pk.lo, 128, i, half * 8 + c, v + c * 8, amax);
         fence_async_smem();
@@ -260,12 +246,17 @@ __global__ void __launch_bounds__(kThreads, 1)
       load(tQ, bQ, TQ, g2, b2, h2, qb2 * 128);
       load(tK[0], &bK[0], TK, g2, b2, h2, 0);
     }
+    // l = the row sum of P~ over both key-column halves; O = (P~ V) / l
+    xch[half * 128 + i] = l;
+    sync_all();
+    l = xch[i] + xch[128 + i];
+    inv = l > 0.f ? 1.f / l : 0.f;
     {
       const long long ld = a.Ohl.ok() ? a.Ohl.ld : a.O.ld;
       rows_out_hl(trow + 256, trow + 384,
                   a.O.ok() ? a.O.at(g, b, h) + (long long)qb * 128 * ld : nullptr,
                   a.Ohl.ok() ? a.Ohl.at(g, b, h) + (long long)qb * 128 * ld : nullptr, ld, i,
-                  sq - qb * 128, half * (dh >> 1), dh >> 1, 1.f, amax);
+                  sq - qb * 128, half * (dh >> 1), dh >> 1, inv, amax);
     }
     if (half == 0 && q < sq) {
       float* stp = a.P.at(g, b, h) + 2LL * q;
