@@ -76,7 +76,8 @@ struct TcParams {
   int vec_ok;      // every epilogue operand row start is 16-byte aligned
   int* range_flag;
   unsigned long long* prof;  // MGLP_GEMM_PROF: cycles spent per barrier wait kind (diagnostics)
-  int debug;  // MGLP_DEBUG_GEMM bits (timing diagnostics only): 1 skip conversion, 2 skip epilogue stores
+  int debug;  // MGLP_DEBUG_GEMM bits (timing diagnostics only): 1 skip conversion, 2 skip
+              // epilogue stores, 4 every unit loads the same (L2-resident) pre-split tiles
   EpiArgs ep;
 };
 
@@ -267,7 +268,10 @@ __global__ void __launch_bounds__(Cfg<CG>::THREADS, 1)
           flush(0);
           mbar_expect_tx(&fullA[s], TILE_BYTES);
           int c[5];
-          tma_coords(p.a, kb * BK, T.m0, T.g, T.b, T.h, c);
+          if (p.debug & 4)  // diagnostics: every unit reads the same (L2-resident) A rows
+            tma_coords(p.a, kb * BK, (int)cr * 128, 0, 0, 0, c);
+          else
+            tma_coords(p.a, kb * BK, T.m0, T.g, T.b, T.h, c);
           tma_load_5d(hl_a(s), &mapA, &fullA[s], c);
         }
       }
@@ -314,7 +318,10 @@ __global__ void __launch_bounds__(Cfg<CG>::THREADS, 1)
           flush(1);
           mbar_expect_tx(&fullB[j], TILE_BYTES);
           int c[5];
-          tma_coords(p.b, kb * BK, nb0, T.g, T.b, T.h, c);
+          if (p.debug & 4)  // diagnostics: every unit reads the same (L2-resident) B rows
+            tma_coords(p.b, kb * BK, (int)cr * 128, 0, 0, 0, c);
+          else
+            tma_coords(p.b, kb * BK, nb0, T.g, T.b, T.h, c);
           tma_load_5d(b_slot(j), &mapB, &fullB[j], c);
         }
       }
