@@ -384,10 +384,6 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
         }
       }
     }
-    // dV rows (keys) while the staging of Q, K lands
-    rows_out_hl(trow + 256, trow + 384, a.dV.ok() ? a.dV.at(g, b, h) : nullptr,
-                a.dVhl.ok() ? a.dVhl.at(g, b, h) : nullptr, a.dVhl.ok() ? a.dVhl.ld : a.dV.ld, r,
-                skv, half * (dh >> 1), dh >> 1, 1.f, amax);
     // (4) Q, K -> T1 (the dV MMA is done)
     mbar_wait(st_full, stp);
     stp ^= 1;
@@ -403,6 +399,10 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
       mma3(tmem + 128, tmem + 192, dSm, Qm, dh, sq16 >> 4);   // dK = dS^T Q
       mma_commit<1>(m_bar);
     }
+    // dV rows (keys) under the dQ / dK MMAs (disjoint TMEM columns)
+    rows_out_hl(trow + 256, trow + 384, a.dV.ok() ? a.dV.at(g, b, h) : nullptr,
+                a.dVhl.ok() ? a.dVhl.at(g, b, h) : nullptr, a.dVhl.ok() ? a.dVhl.ld : a.dV.ld, r,
+                skv, half * (dh >> 1), dh >> 1, 1.f, amax);
     mbar_wait(m_bar, mp);
     mp ^= 1;
     tc_after();
