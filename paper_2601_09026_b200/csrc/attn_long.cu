@@ -314,15 +314,24 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int i = q4 * 32 + lane;
   float amax = 0.f;
   Phase ph;
-  for (int z = blockIdx.x; z < nprob; z += gridDim.x) {
-    const int kb = z % nkb;
+  auto kv_problem = [&](int z, int& kb, int& g, int& b, int& h) {
+    kb = z % nkb;
     int r = z / nkb;
-    const int h = r % a.H;
+    h = r % a.H;
     r /= a.H;
-    const int b = r % a.Bb, g = r / a.Bb;
+    b = r % a.Bb;
+    g = r / a.Bb;
+  };
+  if (tid == 0 && (int)blockIdx.x < nprob) {
+    int kb, g, b, h;
+    kv_problem(blockIdx.x, kb, g, b, h);
+    issue(L, tm, TK, g, b, h, kb * 128, dh);
+  }
+  for (int z = blockIdx.x; z < nprob; z += gridDim.x) {
+    int kb, g, b, h;
+    kv_problem(z, kb, g, b, h);
     const int qb0 = a.causal ? kb : 0;
     const float* stats = a.P.at(g, b, h);
-    if (tid == 0) issue(L, tm, TK, g, b, h, kb * 128, dh);
     wait_stage(L, ph);
     conv_rows(L.stg, 128, 128, dh, Kk.hi, Kk.lo, tid, kThreads, amax);
     fence_async_smem();
@@ -380,6 +389,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       mma_done(L, ph);
     }
+    // the staging is free: the next problem's K streams in under this epilogue
+    if (tid == 0 && z + (int)gridDim.x < nprob) {
+      int kb2, g2, b2, h2;
+      kv_problem(z + gridDim.x, kb2, g2, b2, h2);
+      issue(L, tm, TK, g2, b2, h2, kb2 * 128, dh);
+    }
     const int nv = skv - kb * 128;
     {
       const long long ldv = a.dVhl.ok() ? a.dVhl.ld : a.dV.ld;
@@ -428,17 +443,26 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int i = q4 * 32 + lane;
   float amax = 0.f;
   Phase ph;
-  for (int z = blockIdx.x; z < nprob; z += gridDim.x) {
-    const int qb = z % nqb;
+  auto q_problem = [&](int z, int& qb, int& g, int& b, int& h) {
+    qb = z % nqb;
     int r = z / nqb;
-    const int h = r % a.H;
+    h = r % a.H;
     r /= a.H;
-    const int b = r % a.Bb, g = r / a.Bb;
+    b = r % a.Bb;
+    g = r / a.Bb;
+  };
+  if (tid == 0 && (int)blockIdx.x < nprob) {
+    int qb, g, b, h;
+    q_problem(blockIdx.x, qb, g, b, h);
+    issue(L, tm, TQ, g, b, h, qb * 128, dh);
+  }
+  for (int z = blockIdx.x; z < nprob; z += gridDim.x) {
+    int qb, g, b, h;
+    q_problem(z, qb, g, b, h);
     const int q = qb * 128 + i;
     const bool live = q < sq;
     const int kend = a.causal ? min(nkb, qb + 1) : nkb;
     const float* stats = a.P.at(g, b, h);
-    if (tid == 0) issue(L, tm, TQ, g, b, h, qb * 128, dh);
     wait_stage(L, ph);
     conv_rows(L.stg, 128, 128, dh, Qk.hi, Qk.lo, tid, kThreads, amax);
     fence_async_smem();
@@ -493,6 +517,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         mma_commit<1>(&L.bars[1]);
       }
       mma_done(L, ph);
+    }
+    // the staging is free: the next problem's Q streams in under this epilogue
+    if (tid == 0 && z + (int)gridDim.x < nprob) {
+      int qb2, g2, b2, h2;
+      q_problem(z + gridDim.x, qb2, g2, b2, h2);
+      issue(L, tm, TQ, g2, b2, h2, qb2 * 128, dh);
     }
     {
       const long long ldq = a.dQhl.ok() ? a.dQhl.ld : a.dQ.ld;
