@@ -18,6 +18,10 @@ CASES = [  # kind, n_enc, n_dec, (B, sx, sy), causal buffers
     ("encoder", 6, 0, (2, 16, 0), (0, 0)),
     ("decoder_only", 0, 6, (2, 24, 0), (1, 1)),
     ("encoder_decoder", 3, 3, (2, 16, 8), (0, 0)),
+    # s = 128: the fused attention keeps P pre-split (bulk-copied out by the
+    # forward, back in by the backward) inside the engine's solve
+    ("encoder", 4, 0, (1, 128, 0), (0, 0)),
+    ("decoder_only", 0, 4, (1, 128, 0), (0, 0)),
 ]
 
 
