@@ -59,3 +59,34 @@ def test_engine_with_presplit_operands_matches_reference(case):
     assert rel(bo.lambda0.flat(), rl0) < 1e-4
     assert rel(bo.phase.trace, rbt) < 1e-4
     assert rel(g, rg) < 1e-4
+
+
+def test_presplit_operands_with_dropout_masks():
+    """dropout sites on the pre-split paths: the masked O-projection / MLP-out
+    epilogues, the masked LayerNorm VJP output written pre-split (da1) and
+    the masked upstream copy packed for the GELU' dgrad"""
+    b, sx = 2, 16
+    cfg = StackConfig(kind="encoder", d=D, heads=H, ffn=F, n_enc=4, dropout=0.25)
+    st = LayerStack(cfg, 5)
+    rc = R.RefStackConfig(kind="encoder", d=D, heads=H, ffn=F, dropout=0.25)
+    rc.n_enc, rc.n_dec = 4, 0
+    ref = R.RefStack(rc, 5)
+    st.refresh_dropout(3, 7, b, sx, 0)
+    ref.refresh_dropout(3, 7, b, sx, 0)
+    n = ref.state_size(b, sx, 0)
+    z0 = R.gaussian_fill(4, 6, 4, n, 0.5)
+    lam = R.gaussian_fill(5, 6, 5, n, 1.0)
+    eng = LayerParallelEngine(st, SolveConfig(coarsen=2, levels=2, fwd_iters=2, bwd_iters=2,
+                                              warm_start=False))
+    reng = R.RefEngine(ref, coarsen=2, levels=2, fwd_iters=2, bwd_iters=2, warm_start=False)
+    fo = eng.forward(State.from_flat(z0, b, sx, 0, D))
+    rtraj, rft, _ = reng.forward(z0, b, sx, 0)
+    assert rel(np.stack([s.flat() for s in fo.traj]), rtraj) < 1e-4
+    assert rel(fo.phase.trace, rft) < 1e-4
+    g = st.zero_grads()
+    bo = eng.backward(fo.traj, State.from_flat(lam, b, sx, 0, D), g)
+    rg = np.zeros(ref.num_params())
+    rl0, rbt, _ = reng.backward(rtraj, lam, b, sx, 0, grads=rg)
+    assert rel(bo.lambda0.flat(), rl0) < 1e-4
+    assert rel(bo.phase.trace, rbt) < 1e-4
+    assert rel(g, rg) < 1e-4
