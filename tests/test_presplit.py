@@ -90,3 +90,21 @@ def test_presplit_operands_with_dropout_masks():
     assert rel(bo.lambda0.flat(), rl0) < 1e-4
     assert rel(bo.phase.trace, rbt) < 1e-4
     assert rel(g, rg) < 1e-4
+
+
+def test_training_on_presplit_sizes_tracks_reference():
+    """the device training step (trainer.cu: head, loss, adjoint, optimizer)
+    with every GEMM operand pre-split, against the reference's run_training"""
+    from paper_2601_09026_b200 import training as T
+    stack = StackConfig(kind="encoder", d=D, heads=H, ffn=F, n_enc=4)
+    tk = T.TaskSpec(kind="copy_sequence", vocab=16, seq_len=16, train_size=16, val_size=8, seed=2)
+    mc = T.ModelConfig(stack=stack, vocab=16, max_seq=16)
+    tc = T.TrainConfig(mode="layer_parallel",
+                       solve=SolveConfig(coarsen=2, levels=2, fwd_iters=2, bwd_iters=1),
+                       batch_size=4, epochs=1, seed=3, val_every=2)
+    ref = R.run_training(tk, mc, tc)
+    res = T.run_training(tk, mc, tc)
+    rl = [float(line.split(",")[1]) for line in ref["csv"].strip().splitlines()[1:]]
+    assert len(res.rows) == len(rl)
+    for d, r in zip(res.rows, rl):
+        assert abs(d.loss - r) <= 1e-4 * abs(r), (d.batch, d.loss, r)
