@@ -9,10 +9,14 @@
 // problem stays on chip:
 //   forward   S = Q K^T (TMEM) -> softmax (one thread per query row and half
 //             of the keys; the reference's scale, -inf causal mask,
-//             max-subtracted exp and 1/sum) -> P (global, for the backward,
-//             and hi/lo' in smem) -> O = P V (TMEM) -> O
+//             max-subtracted exp and 1/sum) -> P (hi/lo' in smem; for the
+//             backward either fp32 rows or, at s = 128, the hi/lo' tiles
+//             themselves, bulk-copied out: AttnArgs::p_hl) -> O = P V (TMEM)
+//             -> O (fp32 and/or pre-split for the O-projection)
 //   backward  dP = dO V^T and dV = P^T dO (TMEM) -> dS = P (dP - rowsum(dP P))
-//             (hi/lo' in smem) -> dQ = dS K / sqrt(dh), dK = dS^T Q / sqrt(dh)
+//             (hi/lo' in smem; P read back from its hi/lo' tiles) ->
+//             dQ = dS K / sqrt(dh), dK = dS^T Q / sqrt(dh) (fp32 and/or
+//             pre-split for the QKV dgrad)
 // replacing 2 + 4 tensor-core GEMM launches and 2 softmax row kernels (and the
 // S / dS round trips through HBM) per attention evaluation.
 //
