@@ -17,7 +17,10 @@
 // the engine reports it (no silent overflow).
 //
 // Structure (persistent; one CTA, or with cta_group::2 one CTA pair, per SM):
-//   warp 0      TMA producer: fp32 operand tiles -> staging ring
+//   warp 0      TMA producer: fp32 operand tiles -> staging ring; or, with
+//               A produced pre-split (GemmArgs::Ahl: LayerNorm, attention,
+//               GELU / GELU' epilogues, LN VJP, the upstream pack), hi|lo
+//               A tiles straight into the MMA ring (no conversion at all)
 //   warp 1      MMA issuer (one elected thread): 3 x 2 tcgen05.mma per 32-K stage
 //   warp 2      TMEM allocator
 //   warp 3      TMA producer for a pre-split B (weights): hi|lo tiles straight
