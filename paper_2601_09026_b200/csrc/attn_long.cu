@@ -94,6 +94,11 @@ __device__ __forceinline__ void read64(uint32_t trow, int c0, float* v) {
   for (int c = 0; c < 64; c += 16) tmem_pair16(trow + c0 + c, trow + 128 + c0 + c, v + c);
 }
 
+// index of the (query block, key block) dS tile of a head in AttnArgs::dS
+__device__ __forceinline__ long long ds_pair(const AttnArgs& a, int qb, int kb, int nkb) {
+  return a.causal ? (long long)qb * (qb + 1) / 2 + kb : (long long)qb * nkb + kb;
+}
+
 // number of valid keys of query q among keys [key0, key0 + 64): j < skv and,
 // causal, j <= q (one compare per key in the loops)
 __device__ __forceinline__ int key_limit(int q, int key0, int skv, bool causal, bool live) {
@@ -386,8 +391,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (tid == 0) {
         mma3(tmem + 384, tmem + 448, Pm, Qm, dh, 8, !first);  // dK += dS^T Q
         mma_commit<1>(&L.bars[1]);
+        // the dQ kernel's operand: this dS tile, pre-split (async)
+        if (a.dS.ok()) bulk_store(a.dS.at(g, b, h) + ds_pair(a, qb, kb, nkb) * (long long)(128 * 128),
+                                  Pm.hi, 4 * TILE64);
       }
       mma_done(L, ph);
+      if (tid == 0 && a.dS.ok()) bulk_store_wait_read();  // Pm is rewritten next step
     }
     // the staging is free: the next problem's K streams in under this epilogue
     if (tid == 0 && z + (int)gridDim.x < nprob) {
@@ -406,6 +415,99 @@ __global__ void __launch_bounds__(kThreads, 1)
       rows_out_hl(trow + 384, trow + 448, a.dK.ok() ? a.dK.at(g, b, h) + ok : nullptr,
                   a.dKhl.ok() ? a.dKhl.at(g, b, h) + ok : nullptr, ldk, i, nv, half * (dh >> 1),
                   dh >> 1, a.scale, amax);
+    }
+    sync_all();
+  }
+  if (amax >= 65520.f && amax <= FLT_MAX && a.range_flag) atomicOr(a.range_flag, 1);
+  if (tid == 0 && a.dS.ok()) bulk_store_wait();
+  sync_all();
+  if (warp == 0) tmem_free(tmem, 512);
+}
+
+// ---- backward: t_i = dO_i . O_i for every query row (before dK/dV when the
+// dQ kernel reads the stored dS tiles) --------------------------------------------
+__global__ void __launch_bounds__(256) attn_rowdot_kernel(const AttnArgs a, const int* active) {
+  pdl_wait();
+  pdl_trigger();
+  if (active && *(volatile const int*)active == 0) return;
+  const long long n = (long long)a.G * a.Bb * a.H * a.sq;
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int q = (int)(i % a.sq);
+  long long r = i / a.sq;
+  const int h = (int)(r % a.H);
+  r /= a.H;
+  const int b = (int)(r % a.Bb), g = (int)(r / a.Bb);
+  a.P.at(g, b, h)[2LL * a.sq + q] =
+      row_dot(a.dO.at(g, b, h) + (long long)q * a.dO.ld, a.O.at(g, b, h) + (long long)q * a.O.ld,
+              a.dh);
+}
+
+// ---- backward: dQ per 128-query block from the stored dS tiles ------------------------
+// tiles: t2 = K, t4 = dS (bulk-loaded pre-split); TMEM: dQ [256,..)/[384,..)
+__global__ void __launch_bounds__(kThreads, 1)
+    attn_bwd_dq_ds_kernel(const __grid_constant__ AttnTma tm, const AttnArgs a, const int* active) {
+  pdl_wait();
+  pdl_trigger();
+  extern __shared__ uint8_t smem_raw[];
+  if (active && *(volatile const int*)active == 0) return;
+  const LongSmem L = carve(smem_raw);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int q4 = warp & 3, half = warp >> 2;
+  const int sq = a.sq, skv = a.skv, dh = a.dh;
+  const int nqb = (sq + 127) >> 7, nkb = (skv + 127) >> 7;
+  const int nprob = a.G * a.Bb * a.H * nqb;
+  const Opnd Kk = pair64(L.t2, false), Km = pair64(L.t2, true);
+  const Opnd dSk = pair128(L.t4, false);
+  uint64_t* dsb = &L.bars[2];
+  if (tid == 0) {
+    mbar_init(&L.bars[0], 1);
+    mbar_init(&L.bars[1], 1);
+    mbar_init(dsb, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) tmem_alloc(L.tslot, 512);
+  sync_all();
+  const uint32_t tmem = *L.tslot;
+  const uint32_t trow = tmem + ((uint32_t)(q4 * 32) << 16);
+  const int i = q4 * 32 + lane;
+  float amax = 0.f;
+  Phase ph;
+  uint32_t dsp = 0;
+  (void)Kk;
+  for (int z = blockIdx.x; z < nprob; z += gridDim.x) {
+    const int qb = z % nqb;
+    int r = z / nqb;
+    const int h = r % a.H;
+    r /= a.H;
+    const int b = r % a.Bb, g = r / a.Bb;
+    const int kend = a.causal ? min(nkb, qb + 1) : nkb;
+    const float* ds0 = a.dS.at(g, b, h);
+    if (tid == 0) issue(L, tm, TK, g, b, h, 0, dh);
+    for (int kb = 0; kb < kend; ++kb) {
+      if (tid == 0) {
+        mbar_expect_tx(dsb, 4 * TILE64);
+        bulk_load(L.t4, ds0 + ds_pair(a, qb, kb, nkb) * (long long)(128 * 128), 4 * TILE64, dsb);
+      }
+      wait_stage(L, ph);
+      conv_rows(L.stg, 128, 128, dh, Km.hi, Km.lo, tid, kThreads, amax);
+      fence_async_smem();
+      mbar_wait(dsb, dsp);
+      dsp ^= 1;
+      sync_all();
+      if (tid == 0) {
+        if (kb + 1 < kend) issue(L, tm, TK, g, b, h, (kb + 1) * 128, dh);
+        mma3(tmem + 256, tmem + 384, dSk, Km, dh, 8, kb > 0);  // dQ += dS K
+        mma_commit<1>(&L.bars[1]);
+      }
+      mma_done(L, ph);
+    }
+    {
+      const long long ldq = a.dQhl.ok() ? a.dQhl.ld : a.dQ.ld;
+      const long long oq = (long long)qb * 128 * ldq;
+      rows_out_hl(trow + 256, trow + 384, a.dQ.ok() ? a.dQ.at(g, b, h) + oq : nullptr,
+                  a.dQhl.ok() ? a.dQhl.at(g, b, h) + oq : nullptr, ldq, i, sq - qb * 128,
+                  half * (dh >> 1), dh >> 1, a.scale, amax);
     }
     sync_all();
   }
@@ -607,6 +709,21 @@ void launch_attn_bwd_long(const AttnArgs& a, const int* active, cudaStream_t s) 
   (void)attr;
   const AttnTma t = long_maps(a, true);
   const long long heads = (long long)a.G * a.Bb * a.H;
+  if (a.dS.ok()) {
+    static bool attr2 = [] {
+      MGLP_CUDA(cudaFuncSetAttribute(attn_bwd_dq_ds_kernel,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, kLongSmem));
+      return true;
+    }();
+    (void)attr2;
+    // t_i first; dK/dV stores every dS tile; dQ = sum over key blocks of dS K
+    const long long rows = heads * a.sq;
+    launch_k(attn_rowdot_kernel, dim3((unsigned)((rows + 255) / 256)), dim3(256), 0, s, 1, a,
+             active);
+    launch_long(attn_bwd_dkdv_kernel, t, a, heads * ((a.skv + 127) / 128), active, s);
+    launch_long(attn_bwd_dq_ds_kernel, t, a, heads * ((a.sq + 127) / 128), active, s);
+    return;
+  }
   // dQ first: it also publishes t_i = dO_i . O_i (at P + 2 sq + i) for dK / dV
   launch_long(attn_bwd_dq_kernel, t, a, heads * ((a.sq + 127) / 128), active, s);
   launch_long(attn_bwd_dkdv_kernel, t, a, heads * ((a.skv + 127) / 128), active, s);

@@ -866,6 +866,7 @@ bool Engine::attention_bwd(int G, Mat Q, Mat K, Mat V, Mat P, Mat O, Mat dO, Mat
   Q = heads(Q, sq);
   K = heads(K, skv);
   V = heads(V, skv);
+  O = heads(O, sq);  // the long backward forms t_i = dO_i . O_i per (batch, head)
   dO = heads(dO, sq);
   dQ = heads(dQ, sq);
   dK = heads(dK, skv);
@@ -917,6 +918,13 @@ bool Engine::attention_bwd(int G, Mat Q, Mat K, Mat V, Mat P, Mat O, Mat dO, Mat
     }
     if (use_long_attn() && attn_long_supported(at, true)) {
       const bool hl = with_hl();
+      // whole 128-blocks: dK/dV stores its dS tiles (pre-split) in the dP
+      // slot and dQ reads them (MGLP_LONG_DS=0 recomputes S, P, dP instead)
+      static const bool ds_on = [] {
+        const char* e = getenv("MGLP_LONG_DS");
+        return !(e && atoi(e) == 0);
+      }();
+      if (ds_on && sq % 128 == 0 && skv % 128 == 0 && dP.ld == skv) at.dS = dP;
       ++launches_;
       prof_shape_ = {-sq, skv, dh, G * B_ * H};
       timed(PROF_ATTN, fl, 0.0, [&] { launch_attn_bwd_long(at, active_, stream_); });

@@ -133,6 +133,10 @@ struct AttnArgs {
   // forward's hi|lo' MMA operand tiles (64 KiB per problem, exactly the fp32
   // P slot), bulk-copied out by the forward and back in by the backward
   int p_hl = 0;
+  // long backward, optional (s multiples of 128): the dK/dV kernel stores each
+  // (query block, key block) dS tile pre-split (64 KiB) here, P-slot strides,
+  // and the dQ kernel reads them instead of recomputing S, P and dP
+  Mat dS;
   int* range_flag = nullptr;
 };
 bool attn_tc_supported(const AttnArgs& a, bool backward);

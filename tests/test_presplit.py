@@ -22,6 +22,10 @@ CASES = [  # kind, n_enc, n_dec, (B, sx, sy), causal buffers
     # forward, back in by the backward) inside the engine's solve
     ("encoder", 4, 0, (1, 128, 0), (0, 0)),
     ("decoder_only", 0, 4, (1, 128, 0), (0, 0)),
+    # s = 256: the streamed long attention; its dK/dV kernel stores the dS
+    # tiles pre-split and the dQ kernel reads them back
+    ("encoder", 4, 0, (1, 256, 0), (0, 0)),
+    ("decoder_only", 0, 4, (1, 256, 0), (0, 0)),
 ]
 
 
