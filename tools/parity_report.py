@@ -51,17 +51,19 @@ for name in ["enc_small", "enc_small_3lvl", "causal_buffered", "encdec", "tiny_b
     out[name] = r
     print(name, json.dumps(r), flush=True)
 
-# full width (d=768, 12 heads, ffn 3072, seq 128) on 8 layers vs the numpy oracle
-for kind in ["encoder", "decoder_only"]:
-    kw = dict(n_enc=8) if kind == "encoder" else dict(n_dec=8)
+# full width (d=768, 12 heads, ffn 3072) vs the numpy oracle: seq 128 on 8
+# layers (fused short attention, pre-split P), and the streamed long attention
+# at GPT-2 (causal, 512) and ViT (197) lengths on 4 layers
+for kind, s, B, nl in [("encoder", 128, 2, 8), ("decoder_only", 128, 2, 8),
+                       ("decoder_only", 512, 1, 4), ("encoder", 197, 1, 4)]:
+    kw = dict(n_enc=nl) if kind == "encoder" else dict(n_dec=nl)
     sc = StackConfig(kind=kind, d=768, heads=12, ffn=3072, **kw)
     st = LayerStack(sc, 7)
     ost = O.Stack(O.StackConfig(kind=kind, d=768, heads=12, ffn=3072, **kw), np.asarray(st.params()))
     rng = np.random.default_rng(3)
-    B, s = 2, 128
     z0 = rng.standard_normal(B * s * 768) * 0.5
     lam = rng.standard_normal(B * s * 768)
-    cfg = dict(coarsen=4, levels=2, fwd_iters=2, bwd_iters=1)
+    cfg = dict(coarsen=4 if nl == 8 else 2, levels=2, fwd_iters=2, bwd_iters=1)
     eng = LayerParallelEngine(st, SolveConfig(**cfg))
     fo = eng.forward(State.from_flat(z0, B, s, 0, 768))
     gr = st.zero_grads()
@@ -73,7 +75,8 @@ for kind in ["encoder", "decoder_only"]:
     r = {"traj": rel(np.stack([t.flat() for t in fo.traj]), np.stack([t.flat() for t in otraj])),
          "fwd_trace": rel(fo.phase.trace, otr), "bwd_trace": rel(bo.phase.trace, obtr),
          "lambda0": rel(bo.lambda0.flat(), ol0.flat()), "grads": rel(gr, O.Stack.flatten(og))}
-    out[f"full_width_{kind}_8L"] = r
-    print(kind, json.dumps(r), flush=True)
+    key = f"full_width_{kind}_{nl}L" if s == 128 else f"full_width_{kind}_s{s}_{nl}L"
+    out[key] = r
+    print(key, json.dumps(r), flush=True)
 os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
 json.dump(out, open(os.path.join(ROOT, "gpurun_out", "parity_report.json"), "w"), indent=1)
