@@ -458,7 +458,13 @@ void Engine::set_shape(int batch, int s_x, int s_y) {
   b.dctx = take(R * d);
   b.dqkv = take(R * 3 * d);
   b.dn1 = take(R * d);
-  b.dP = take((long long)B_ * H * smax * ((smax + 3) & ~3));
+  {
+    // the long backward's dS tiles (128 x 128 pre-split per block pair) live
+    // here too: pad ragged lengths (ViT 197) to whole blocks
+    const long long blk = (smax + 127) / 128;
+    const long long tiles = smax > 128 ? blk * blk * 128 * 128 : 0;
+    b.dP = take((long long)B_ * H * std::max((long long)smax * ((smax + 3) & ~3), tiles));
+  }
   // dropout: the upstream of the MLP branch and of the cross-attention output
   // with their masks applied (the operands of those branches' dgrad / wgrad)
   b.upm = take(sd_.dropout > 0.0 ? R * d : 0);
@@ -924,7 +930,15 @@ bool Engine::attention_bwd(int G, Mat Q, Mat K, Mat V, Mat P, Mat O, Mat dO, Mat
         const char* e = getenv("MGLP_LONG_DS");
         return !(e && atoi(e) == 0);
       }();
-      if (ds_on && sq % 128 == 0 && skv % 128 == 0 && dP.ld == skv) at.dS = dP;
+      // self-attention: the dP slot holds whole-block tiles per head (padded
+      // at allocation); cross-attention only when the blocks tile it exactly
+      if (ds_on && (sq == skv || (sq % 128 == 0 && skv % 128 == 0 && dP.ld == skv))) {
+        const long long per_head = (long long)((sq + 127) / 128) * ((skv + 127) / 128) * 128 * 128;
+        Mat ds = dP;
+        ds.hstride = per_head;
+        ds.bstride = (long long)H * per_head;
+        at.dS = ds;
+      }
       ++launches_;
       prof_shape_ = {-sq, skv, dh, G * B_ * H};
       timed(PROF_ATTN, fl, 0.0, [&] { launch_attn_bwd_long(at, active_, stream_); });

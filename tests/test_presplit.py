@@ -26,6 +26,7 @@ CASES = [  # kind, n_enc, n_dec, (B, sx, sy), causal buffers
     # tiles pre-split and the dQ kernel reads them back
     ("encoder", 4, 0, (1, 256, 0), (0, 0)),
     ("decoder_only", 0, 4, (1, 256, 0), (0, 0)),
+    ("encoder", 4, 0, (2, 200, 0), (0, 0)),  # ragged blocks (padded dS tiles)
 ]
 
 
