@@ -27,6 +27,8 @@ CASES = [  # kind, n_enc, n_dec, (B, sx, sy), causal buffers
     ("encoder", 4, 0, (1, 256, 0), (0, 0)),
     ("decoder_only", 0, 4, (1, 256, 0), (0, 0)),
     ("encoder", 4, 0, (2, 200, 0), (0, 0)),  # ragged blocks (padded dS tiles)
+    # long self- and cross-attention (sq = 192 queries over 256 encoder keys)
+    ("encoder_decoder", 2, 2, (1, 256, 192), (0, 0)),
 ]
 
 
@@ -66,11 +68,13 @@ def test_engine_with_presplit_operands_matches_reference(case):
     assert rel(g, rg) < 1e-4
 
 
-def test_presplit_operands_with_dropout_masks():
+@pytest.mark.parametrize("sx", [16, 256])
+def test_presplit_operands_with_dropout_masks(sx):
     """dropout sites on the pre-split paths: the masked O-projection / MLP-out
     epilogues, the masked LayerNorm VJP output written pre-split (da1) and
-    the masked upstream copy packed for the GELU' dgrad"""
-    b, sx = 2, 16
+    the masked upstream copy packed for the GELU' dgrad (s = 256: with the
+    long attention and its stored dS tiles)"""
+    b = 2 if sx == 16 else 1
     cfg = StackConfig(kind="encoder", d=D, heads=H, ffn=F, n_enc=4, dropout=0.25)
     st = LayerStack(cfg, 5)
     rc = R.RefStackConfig(kind="encoder", d=D, heads=H, ffn=F, dropout=0.25)
