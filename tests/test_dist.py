@@ -139,15 +139,23 @@ CASES = [
 ]
 
 
+# d = 64, dh = 32, s = 128: the pre-split operand paths and the pre-split P of
+# the fused attention, partitioned across ranks
+CASES_PRESPLIT = [
+    ("encoder", dict(n_enc=8), 0, 0, 2, 2, [2, 4], (64, 2, 128), (1, 128)),
+]
+
+
 @pytest.mark.gpu
-@pytest.mark.parametrize("case", CASES)
+@pytest.mark.parametrize("case", CASES + CASES_PRESPLIT)
 def test_loopback_ranks_reproduce_single_rank_bitwise(case):
     import torch
-    kind, kw, sx_extra, sy, cf, lv, worlds = case
-    sc = StackConfig(kind=kind, d=16, heads=2, ffn=32, **kw)
+    kind, kw, sx_extra, sy, cf, lv, worlds = case[:7]
+    d, heads, ffn = case[7] if len(case) > 7 else (16, 2, 32)
+    sc = StackConfig(kind=kind, d=d, heads=heads, ffn=ffn, **kw)
     st = LayerStack(sc, 17)
     params = np.ascontiguousarray(st.params(), np.float64)
-    B, sx = 2, 6
+    B, sx = case[8] if len(case) > 8 else (2, 6)
     rng = np.random.default_rng(5)
     n = B * (sx + sy) * sc.d
     z0 = rng.standard_normal(n) * 0.5
