@@ -470,8 +470,9 @@ def run_device(args, cfg, rank, world, dist):
         "frac_of_split_ceiling": achieved / (bf16_peak / 3.0),
         "gemm_share_of_step": gemm_ms / sum(ms3) if sum(ms3) > 0 else None,
         "gemm_launches_per_step": gemm_n,
-        "attention": {"kernels": "attn_fwd/bwd (s<=128) or attn_fwd_long/bwd_dkdv/bwd_dq "
-                                 "(128<s<=512): fused tcgen05 per (batch, head)",
+        "attention": {"kernels": "attn_fwd/bwd (s<=128; P kept pre-split at s=128) or "
+                                 "attn_fwd_long + rowdot / bwd_dkdv (stores the dS tiles) / "
+                                 "bwd_dq_ds (128<s<=512): fused tcgen05 per (batch, head)",
                       "achieved": attn_fl / (attn_ms * 1e-3) / 1e12 if attn_ms > 0 else None,
                       "unit": "TFLOP/s", "launches_per_step": ln3[1]},
         "per_class_ms": {"gemm_tcgen05": ms3[0], "attention_tcgen05": ms3[1],
