@@ -225,7 +225,9 @@ mglp_status mglp_rng_gaussian_fill(unsigned long long seed, unsigned long long a
  * C + g*c_slot, row stride ldc. engine 0 = tcgen05 fp16x3 split (the
  * product kernel), 1 = fp32 CUDA-core reference. b_presplit exercises the
  * pre-split (hi|lo) weight path of the tensor-core kernel (bit 1 set: a
- * K-major A is pre-split too -- the converter-free mainloop). range_flag
+ * K-major A is pre-split too -- the converter-free mainloop); b_presplit = 4
+ * with b_mn hands B's [K][N] rows over pre-split instead (the weight-gradient
+ * operand form: the converters regroup, no split). range_flag
  * (nullable) receives 1 if a finite operand overflowed the fp16 split
  * range. Synchronous. */
 mglp_status mglp_test_gemm(int G, int M, int N, int K, const float* A, long long a_slot, int lda,

@@ -740,7 +740,18 @@ mglp_status mglp_test_gemm(int G, int M, int N, int K, const float* A, long long
     MGLP_CUDA(cudaMemset(dflag, 0, sizeof(int)));
     g.range_flag = dflag;
     float* ahl = nullptr;
-    if (b_presplit && engine == 0) {
+    float* bmn = nullptr;
+    if (b_presplit == 4 && engine == 0 && b_mn) {
+      // B MN-major ([K][N] rows) handed over pre-split row by row: the
+      // converters regroup instead of splitting (GemmArgs::b_mn_hl)
+      if (N % 32) throw ValidationError("test_gemm: pre-split MN-major B needs N % 32 == 0");
+      MGLP_CUDA(cudaMalloc(&bmn, (size_t)G * K * N * sizeof(float)));
+      launch_pack_hl(B, b_slot, ldb, bmn, (long long)K * N, N, G, K, N, false, 0);
+      g.B.ptr = bmn;
+      g.B.slot_stride = (long long)K * N;
+      g.B.ld = N;
+      g.b_mn_hl = true;
+    } else if (b_presplit && engine == 0) {
       const long long kp = pack_hl_cols(K);
       MGLP_CUDA(cudaMalloc(&hl, (size_t)G * N * kp * sizeof(float)));
       launch_pack_hl(B, b_slot, ldb, hl, (long long)N * kp, (int)kp, G, N, K, b_mn != 0, 0);
@@ -763,6 +774,7 @@ mglp_status mglp_test_gemm(int G, int M, int N, int K, const float* A, long long
     MGLP_CUDA(cudaDeviceSynchronize());
     if (hl) cudaFree(hl);
     if (ahl) cudaFree(ahl);
+    if (bmn) cudaFree(bmn);
     int flag = 0;
     MGLP_CUDA(cudaMemcpy(&flag, dflag, sizeof(int), cudaMemcpyDeviceToHost));
     cudaFree(dflag);

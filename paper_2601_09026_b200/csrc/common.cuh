@@ -639,6 +639,10 @@ struct GemmArgs {
   // hi|lo' form by the kernel that wrote it -- the mainloop runs converter-free
   Mat Ahl;
   bool a_mn = false, b_mn = false;
+  // b_mn with B's rows already pre-split (hi|lo' rows of the same byte size,
+  // e.g. the cached LN / GELU outputs the weight gradients read): the
+  // converters only regroup the halves into the K-major tile, no split
+  bool b_mn_hl = false;
   EpiArgs ep;
   // set to 1 when a finite operand value overflows fp16 (|x| >= 65520)
   int* range_flag = nullptr;

@@ -751,6 +751,14 @@ Mat Engine::pack_upstream(int G, int rows, const Mat& up) {
   return h;
 }
 
+bool Engine::cache_hl_off() {
+  static const bool off = [] {
+    const char* e = getenv("MGLP_NO_CACHE_HL");
+    return e && atoi(e) != 0;
+  }();
+  return off;
+}
+
 // the adjoint's pre-split dgrad operands (MGLP_NO_PRESPLIT_DGRAD=1 disables)
 Mat Engine::dgrad_hl(int G, int which, int cols) const {
   static const bool off = [] {
@@ -1108,8 +1116,11 @@ void Engine::encoder_forward(const EvalSpec& e, int R, bool causal, Mat X, Mat Y
     Mat m = hl_mat(G, which, cols);
     return (m.ok() && par_hl(L, w, l0, ls, false).ok()) ? m : Mat{};
   };
-  const Mat h_n1 = pre(0, d, L.w_qkv), h_ctx = pre(1, d, L.w_o), h_n2 = pre(0, d, L.w_in),
-            h_g = pre(1, f, L.w_out);
+  // a kept linearisation stores its LN / GELU outputs pre-split only: the
+  // weight gradients read them as pre-split MN-major B (GemmArgs::b_mn_hl)
+  const bool ch = keep && cache_hl();
+  const Mat h_n1 = ch ? n1 : pre(0, d, L.w_qkv), h_ctx = pre(1, d, L.w_o),
+            h_n2 = ch ? n2 : pre(0, d, L.w_in), h_g = ch ? gg : pre(1, f, L.w_out);
 
   LnFwdArgs ln;
   ln.G = G;
@@ -1117,7 +1128,7 @@ void Engine::encoder_forward(const EvalSpec& e, int R, bool causal, Mat X, Mat Y
   ln.d = d;
   ln.eps = (float)sd_.ln_eps;
   ln.x = X;
-  ln.out = (keep || !h_n1.ok()) ? n1 : Mat{};
+  ln.out = ((keep && !ch) || !h_n1.ok()) ? n1 : Mat{};
   ln.out_hl = h_n1;
   ln.range_flag = range_flag_;
   ln.stats = st1;
@@ -1163,7 +1174,7 @@ void Engine::encoder_forward(const EvalSpec& e, int R, bool causal, Mat X, Mat Y
   gemm(g);
 
   ln.x = u;
-  ln.out = (keep || !h_n2.ok()) ? n2 : Mat{};
+  ln.out = ((keep && !ch) || !h_n2.ok()) ? n2 : Mat{};
   ln.out_hl = h_n2;
   ln.stats = st2;
   ln.gain = par(L.ln2_g, 0, l0, ls);
@@ -1184,7 +1195,7 @@ void Engine::encoder_forward(const EvalSpec& e, int R, bool causal, Mat X, Mat Y
   g.Bhl = par_hl(L, L.w_in, l0, ls, false);
   g.ep.kind = EPI_BIAS_GELU;
   if (keep) g.ep.out1 = hh;  // gelu'(h): only the backward reads it
-  if (keep || !h_g.ok()) g.ep.out2 = gg;
+  if ((keep && !ch) || !h_g.ok()) g.ep.out2 = gg;
   g.ep.hl2 = h_g;
   g.ep.range_flag = range_flag_;
   g.ep.bias = par(L.b_in, 0, l0, ls);
@@ -1255,8 +1266,10 @@ void Engine::decoder_forward(const EvalSpec& e) {
     Mat m = hl_mat(G, which, cols);
     return (m.ok() && par_hl(L, w, l0, ls, false).ok()) ? m : Mat{};
   };
-  const Mat h_n1 = pre(0, d, L.w_qkv), h_ctx = pre(1, d, L.w_o), h_n3 = pre(0, d, L.w_cq),
-            h_cctx = pre(1, d, L.w_co), h_n2 = pre(0, d, L.w_in), h_g = pre(1, f, L.w_out);
+  const bool ch = keep && cache_hl();  // as in encoder_forward
+  const Mat h_n1 = ch ? n1 : pre(0, d, L.w_qkv), h_ctx = pre(1, d, L.w_o),
+            h_n3 = ch ? n3 : pre(0, d, L.w_cq), h_cctx = pre(1, d, L.w_co),
+            h_n2 = ch ? n2 : pre(0, d, L.w_in), h_g = ch ? gg : pre(1, f, L.w_out);
 
   LnFwdArgs ln;
   ln.G = G;
@@ -1264,7 +1277,7 @@ void Engine::decoder_forward(const EvalSpec& e) {
   ln.d = d;
   ln.eps = (float)sd_.ln_eps;
   ln.x = Y;
-  ln.out = (keep || !h_n1.ok()) ? n1 : Mat{};
+  ln.out = ((keep && !ch) || !h_n1.ok()) ? n1 : Mat{};
   ln.out_hl = h_n1;
   ln.range_flag = range_flag_;
   ln.stats = st1;
@@ -1307,7 +1320,7 @@ void Engine::decoder_forward(const EvalSpec& e) {
   gemm(g);
 
   ln.x = u3;
-  ln.out = (keep || !h_n3.ok()) ? n3 : Mat{};
+  ln.out = ((keep && !ch) || !h_n3.ok()) ? n3 : Mat{};
   ln.out_hl = h_n3;
   ln.stats = st3;
   ln.gain = par(L.ln3_g, 0, l0, ls);
@@ -1345,7 +1358,7 @@ void Engine::decoder_forward(const EvalSpec& e) {
   gemm(g);
 
   ln.x = u2;
-  ln.out = (keep || !h_n2.ok()) ? n2 : Mat{};
+  ln.out = ((keep && !ch) || !h_n2.ok()) ? n2 : Mat{};
   ln.out_hl = h_n2;
   ln.stats = st2;
   ln.gain = par(L.ln2_g, 0, l0, ls);
@@ -1359,7 +1372,7 @@ void Engine::decoder_forward(const EvalSpec& e) {
   g.Ahl = h_n2;
   g.ep.kind = EPI_BIAS_GELU;
   if (keep) g.ep.out1 = hh;  // gelu'(h): only the backward reads it
-  if (keep || !h_g.ok()) g.ep.out2 = gg;
+  if ((keep && !ch) || !h_g.ok()) g.ep.out2 = gg;
   g.ep.hl2 = h_g;
   g.ep.range_flag = range_flag_;
   g.ep.bias = par(L.b_in, 0, l0, ls);
@@ -1574,7 +1587,8 @@ void Engine::encoder_adjoint(const EvalSpec& e, bool causal) {
 
   if (e.want_grads) {
     const float gs = e.gscale;
-    auto wg = [&](int M, int N, Mat A, Mat Bm, long long w, int ldw) {
+    // B pre-split (bhl): a cached LN / GELU output (cache_hl)
+    auto wg = [&](int M, int N, Mat A, Mat Bm, long long w, int ldw, bool bhl = false) {
       GemmArgs w_;
       w_.G = G;
       w_.M = M;
@@ -1584,6 +1598,7 @@ void Engine::encoder_adjoint(const EvalSpec& e, bool causal) {
       w_.B = Bm;
       w_.a_mn = true;
       w_.b_mn = true;
+      w_.b_mn_hl = bhl && cache_hl();
       w_.ep.kind = EPI_GRAD_ACC;
       w_.ep.out1 = grad(w, ldw, l0, ls);
       w_.ep.gscale = gs;
@@ -1607,14 +1622,14 @@ void Engine::encoder_adjoint(const EvalSpec& e, bool causal) {
       timed(PROF_ROW, 0.0, (x.ok() ? 8.0 : 4.0) * c.G * (double)c.rows * c.cols,
             [&] { launch_colred(c, active_, stream_); });
     };
-    wg(d, f, UPm, gg, L.w_out, f);
+    wg(d, f, UPm, gg, L.w_out, f, true);
     cr(UPm, d, L.b_out, Mat{}, Mat{}, 0);
-    wg(f, d, dh, n2, L.w_in, d);
+    wg(f, d, dh, n2, L.w_in, d, true);
     cr(dh, f, L.b_in, Mat{}, Mat{}, 0);
     cr(dn2, d, L.ln2_b, u, st2, L.ln2_g);
     wg(d, d, da1, ctx, L.w_o, d);
     cr(da1, d, L.b_o, Mat{}, Mat{}, 0);
-    wg(3 * d, d, dqkv, n1, L.w_qkv, d);
+    wg(3 * d, d, dqkv, n1, L.w_qkv, d, true);
     cr(dqkv, 3 * d, L.b_qkv, Mat{}, Mat{}, 0);
     cr(dn1, d, L.ln1_b, X, st1, L.ln1_g);
   }
@@ -1797,7 +1812,7 @@ void Engine::decoder_adjoint(const EvalSpec& e) {
 
   if (e.want_grads) {
     const float gs = e.gscale;
-    auto wg = [&](int M, int N, int K, Mat A, Mat Bm, long long w, int ldw) {
+    auto wg = [&](int M, int N, int K, Mat A, Mat Bm, long long w, int ldw, bool bhl = false) {
       GemmArgs w_;
       w_.G = G;
       w_.M = M;
@@ -1807,6 +1822,7 @@ void Engine::decoder_adjoint(const EvalSpec& e) {
       w_.B = Bm;
       w_.a_mn = true;
       w_.b_mn = true;
+      w_.b_mn_hl = bhl && cache_hl();
       w_.ep.kind = EPI_GRAD_ACC;
       w_.ep.out1 = grad(w, ldw, l0, ls);
       w_.ep.gscale = gs;
@@ -1830,21 +1846,21 @@ void Engine::decoder_adjoint(const EvalSpec& e) {
       timed(PROF_ROW, 0.0, (x.ok() ? 8.0 : 4.0) * c.G * (double)c.rows * c.cols,
             [&] { launch_colred(c, active_, stream_); });
     };
-    wg(d, f, R, UPm, gg, L.w_out, f);
+    wg(d, f, R, UPm, gg, L.w_out, f, true);
     cr(R, UPm, d, L.b_out, Mat{}, Mat{}, 0);
-    wg(f, d, R, dh, n2, L.w_in, d);
+    wg(f, d, R, dh, n2, L.w_in, d, true);
     cr(R, dh, f, L.b_in, Mat{}, Mat{}, 0);
     cr(R, dn2, d, L.ln2_b, u2, st2, L.ln2_g);
     wg(d, d, R, dcp, cctx, L.w_co, d);
     cr(R, dcp, d, L.b_co, Mat{}, Mat{}, 0);
-    wg(d, d, R, dcq, n3, L.w_cq, d);
+    wg(d, d, R, dcq, n3, L.w_cq, d, true);
     cr(R, dcq, d, L.b_cq, Mat{}, Mat{}, 0);
     wg(2 * d, d, Tx_, dckv, X, L.w_ckv, d);
     cr(Tx_, dckv, 2 * d, L.b_ckv, Mat{}, Mat{}, 0);
     cr(R, dn3, d, L.ln3_b, u3, st3, L.ln3_g);
     wg(d, d, R, da1, ctx, L.w_o, d);
     cr(R, da1, d, L.b_o, Mat{}, Mat{}, 0);
-    wg(3 * d, d, R, dqkv, n1, L.w_qkv, d);
+    wg(3 * d, d, R, dqkv, n1, L.w_qkv, d, true);
     cr(R, dqkv, 3 * d, L.b_qkv, Mat{}, Mat{}, 0);
     cr(R, dn1, d, L.ln1_b, Y, st1, L.ln1_g);
   }

@@ -252,6 +252,16 @@ class Engine {
   Mat hl_mat(int G, int which, int cols) const;
   bool p_hl_ok(int sq, int skv, const Mat& P) const;
   Mat dgrad_hl(int G, int which, int cols) const;
+  // kept linearisations store their LN and GELU outputs (n1, n2, n3, g)
+  // pre-split only (the forward GEMMs and the weight gradients read them so)
+  bool cache_hl() const {
+#ifdef MGLP_GEMM_SIMT
+    return false;  // the SIMT GEMMs read fp32 operands only
+#else
+    return hlscr_ != nullptr && !cache_hl_off();
+#endif
+  }
+  static bool cache_hl_off();  // MGLP_NO_CACHE_HL=1: cache fp32 + transient pre-split copies
   Mat pack_upstream(int G, int rows, const Mat& up);
   // the activations of this evaluation are the linearization the adjoint
   // reads (cache), not per-evaluation scratch

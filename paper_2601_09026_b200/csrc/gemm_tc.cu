@@ -72,6 +72,7 @@ struct TcParams {
   int Bb, H;
   TcOperand a, b;
   int a_mn, b_mn;  // staging layout of the converted operands
+  int b_hl;        // B's MN-major staging holds pre-split rows (GemmArgs::b_mn_hl)
   int b_direct;    // B comes pre-split (hi|lo tiles TMA'd straight into the MMA ring)
   int a_direct;    // A too (K-major, produced pre-split): no conversion at all
   int passes;      // 3 = hi.hi + (lo.hi + hi.lo); 1 = hi.hi only (diagnostics)
@@ -91,6 +92,32 @@ struct TcParams {
 // ([32 K][128 rows]). Converter warp c (of 4) handles K chunk kc = c (8
 // values) of every row, lane = row within a 32-row block: all shared-memory
 // accesses are bank-conflict free.
+// MN-major staging whose rows are already pre-split (row k: per 32-column
+// chunk 32 hi | 32 lo' fp16): regroup the halves of 8 K values of row r
+// into the K-major hi|lo tile (no arithmetic; the producer range-checked)
+__device__ __forceinline__ void regroup_tile(uint32_t stg, uint32_t hl, int kc, int lane) {
+#pragma unroll
+  for (int rb = 0; rb < ROWS / 32; ++rb) {
+    const int r = rb * 32 + lane;
+    uint32_t h[4], l[4];
+#pragma unroll
+    for (int e = 0; e < 8; e += 2) {
+      const uint32_t a0 = stg + (kc * 8 + e) * (ROWS * 4) + (r >> 5) * 128 + (r & 31) * 2;
+      const uint32_t a1 = a0 + ROWS * 4;
+      uint16_t h0, h1, l0, l1;
+      asm volatile("ld.shared.u16 %0, [%1];" : "=h"(h0) : "r"(a0));
+      asm volatile("ld.shared.u16 %0, [%1];" : "=h"(h1) : "r"(a1));
+      asm volatile("ld.shared.u16 %0, [%1];" : "=h"(l0) : "r"(a0 + 64));
+      asm volatile("ld.shared.u16 %0, [%1];" : "=h"(l1) : "r"(a1 + 64));
+      h[e >> 1] = (uint32_t)h0 | ((uint32_t)h1 << 16);
+      l[e >> 1] = (uint32_t)l0 | ((uint32_t)l1 << 16);
+    }
+    const uint32_t orow = hl + r * 128;
+    sts128(orow + ((kc ^ (r & 7)) << 4), make_uint4(h[0], h[1], h[2], h[3]));
+    sts128(orow + (((4 + kc) ^ (r & 7)) << 4), make_uint4(l[0], l[1], l[2], l[3]));
+  }
+}
+
 __device__ __forceinline__ void convert_tile(uint32_t stg, uint32_t hl, bool mn, int kc,
                                              int lane, float& amax) {
   // all staging loads first (the compiler cannot reorder them across the
@@ -410,8 +437,12 @@ __global__ void __launch_bounds__(Cfg<CG>::THREADS, 1)
         if (kc == 0 && lane == 0) flush(6);
         if (!(p.debug & 1)) {
           convert_tile(smem_u32(stg_a(sa)), smem_u32(hl_a(s)), p.a_mn, kc, lane, amax);
-          if (!p.b_direct)
-            convert_tile(smem_u32(stg_b(sa)), smem_u32(hl_b(s)), p.b_mn, kc, lane, amax);
+          if (!p.b_direct) {
+            if (p.b_hl)
+              regroup_tile(smem_u32(stg_b(sa)), smem_u32(hl_b(s)), kc, lane);
+            else
+              convert_tile(smem_u32(stg_b(sa)), smem_u32(hl_b(s)), p.b_mn, kc, lane, amax);
+          }
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&sfree[sa]);
@@ -749,6 +780,9 @@ Prepared prepare(const GemmArgs& a) {
   p.a_mn = a.a_mn;
   p.b_direct = a.Bhl.ok() ? 1 : 0;
   p.b_mn = p.b_direct ? 0 : a.b_mn;
+  p.b_hl = (!p.b_direct && a.b_mn && a.b_mn_hl) ? 1 : 0;
+  if (a.b_mn_hl && (p.b_direct || !a.b_mn || a.N % 32))
+    throw ContractViolation("gemm_tc: pre-split MN-major B needs an MN-major, 32-aligned B");
   p.a_direct = (a.Ahl.ok() && p.b_direct && !a.a_mn) ? 1 : 0;
   // A: [M][K] (K-major) or [K][M] (MN-major)
   if (p.a_direct) {
