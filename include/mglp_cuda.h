@@ -227,7 +227,8 @@ mglp_status mglp_rng_gaussian_fill(unsigned long long seed, unsigned long long a
  * pre-split (hi|lo) weight path of the tensor-core kernel (bit 1 set: a
  * K-major A is pre-split too -- the converter-free mainloop); b_presplit = 4
  * with b_mn hands B's [K][N] rows over pre-split instead (the weight-gradient
- * operand form: the converters regroup, no split). range_flag
+ * operand form: the converters regroup, no split); b_presplit = 8 with a_mn
+ * does the same for A. range_flag
  * (nullable) receives 1 if a finite operand overflowed the fp16 split
  * range. Synchronous. */
 mglp_status mglp_test_gemm(int G, int M, int N, int K, const float* A, long long a_slot, int lda,

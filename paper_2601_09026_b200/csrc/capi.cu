@@ -741,6 +741,17 @@ mglp_status mglp_test_gemm(int G, int M, int N, int K, const float* A, long long
     g.range_flag = dflag;
     float* ahl = nullptr;
     float* bmn = nullptr;
+    float* amn = nullptr;
+    if (b_presplit == 8 && engine == 0 && a_mn) {
+      // A MN-major ([K][M] rows) handed over pre-split (GemmArgs::a_mn_hl)
+      if (M % 32) throw ValidationError("test_gemm: pre-split MN-major A needs M % 32 == 0");
+      MGLP_CUDA(cudaMalloc(&amn, (size_t)G * K * M * sizeof(float)));
+      launch_pack_hl(A, a_slot, lda, amn, (long long)K * M, M, G, K, M, false, 0);
+      g.A.ptr = amn;
+      g.A.slot_stride = (long long)K * M;
+      g.A.ld = M;
+      g.a_mn_hl = true;
+    }
     if (b_presplit == 4 && engine == 0 && b_mn) {
       // B MN-major ([K][N] rows) handed over pre-split row by row: the
       // converters regroup instead of splitting (GemmArgs::b_mn_hl)
@@ -751,7 +762,7 @@ mglp_status mglp_test_gemm(int G, int M, int N, int K, const float* A, long long
       g.B.slot_stride = (long long)K * N;
       g.B.ld = N;
       g.b_mn_hl = true;
-    } else if (b_presplit && engine == 0) {
+    } else if (b_presplit && b_presplit != 8 && engine == 0) {
       const long long kp = pack_hl_cols(K);
       MGLP_CUDA(cudaMalloc(&hl, (size_t)G * N * kp * sizeof(float)));
       launch_pack_hl(B, b_slot, ldb, hl, (long long)N * kp, (int)kp, G, N, K, b_mn != 0, 0);
@@ -775,6 +786,7 @@ mglp_status mglp_test_gemm(int G, int M, int N, int K, const float* A, long long
     if (hl) cudaFree(hl);
     if (ahl) cudaFree(ahl);
     if (bmn) cudaFree(bmn);
+    if (amn) cudaFree(amn);
     int flag = 0;
     MGLP_CUDA(cudaMemcpy(&flag, dflag, sizeof(int), cudaMemcpyDeviceToHost));
     cudaFree(dflag);

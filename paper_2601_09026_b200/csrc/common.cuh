@@ -643,6 +643,7 @@ struct GemmArgs {
   // e.g. the cached LN / GELU outputs the weight gradients read): the
   // converters only regroup the halves into the K-major tile, no split
   bool b_mn_hl = false;
+  bool a_mn_hl = false;  // likewise for an MN-major A (the cached dgrad chain)
   EpiArgs ep;
   // set to 1 when a finite operand value overflows fp16 (|x| >= 65520)
   int* range_flag = nullptr;

@@ -1492,8 +1492,12 @@ void Engine::encoder_adjoint(const EvalSpec& e, bool causal) {
     }
     // pre-split dgrad A operands (dh, da1; hl_mat); their fp32 forms only
     // where a weight gradient reads them (this call, or the captured chain)
-    const bool keepb = e.want_grads || e.bact.base != nullptr;
-    const Mat h_dh = dgrad_hl(G, 1, f), h_da1 = dgrad_hl(G, 0, d);
+    // with cache_hl() the dh / da1 slots hold their pre-split rows only (the
+    // weight gradients and the bias column sums read them so)
+    const bool keep32 = e.want_grads || e.bact.base != nullptr;  // fp32 dqkv for the wgrad
+    const bool keepb = keep32 && !cache_hl();
+    const Mat h_dh = cache_hl() ? dh : dgrad_hl(G, 1, f),
+              h_da1 = cache_hl() ? da1 : dgrad_hl(G, 0, d);
     GemmArgs g = mk(R, f, d, UPm, L.w_out, f);
     g.Ahl = pack_upstream(G, R, UPm);
     g.ep.kind = EPI_GELU_BWD;
@@ -1538,7 +1542,7 @@ void Engine::encoder_adjoint(const EvalSpec& e, bool causal) {
     const bool dqkv_hl =
         attention_bwd(G, qkv, qkv.offset(d), qkv.offset(2 * d), Pm, ctx, dctx, dPm, dqkv,
                       dqkv.offset(d), dqkv.offset(2 * d), R / B_, R / B_, causal, h_dqkv,
-                      h_dqkv.offset(d), h_dqkv.offset(2 * d), keepb);
+                      h_dqkv.offset(d), h_dqkv.offset(2 * d), keep32);
 
     g = mk(R, d, 3 * d, dqkv, L.w_qkv, d);
     if (dqkv_hl) g.Ahl = h_dqkv;
@@ -1588,7 +1592,8 @@ void Engine::encoder_adjoint(const EvalSpec& e, bool causal) {
   if (e.want_grads) {
     const float gs = e.gscale;
     // B pre-split (bhl): a cached LN / GELU output (cache_hl)
-    auto wg = [&](int M, int N, Mat A, Mat Bm, long long w, int ldw, bool bhl = false) {
+    auto wg = [&](int M, int N, Mat A, Mat Bm, long long w, int ldw, bool bhl = false,
+                  bool ahl = false) {
       GemmArgs w_;
       w_.G = G;
       w_.M = M;
@@ -1599,13 +1604,15 @@ void Engine::encoder_adjoint(const EvalSpec& e, bool causal) {
       w_.a_mn = true;
       w_.b_mn = true;
       w_.b_mn_hl = bhl && cache_hl();
+      w_.a_mn_hl = ahl && cache_hl();
       w_.ep.kind = EPI_GRAD_ACC;
       w_.ep.out1 = grad(w, ldw, l0, ls);
       w_.ep.gscale = gs;
       gemm(w_);
     };
-    auto cr = [&](Mat up, int cols, long long b, Mat x, Mat st, long long gn) {
+    auto cr = [&](Mat up, int cols, long long b, Mat x, Mat st, long long gn, bool uhl = false) {
       ColRedArgs c;
+      c.up_hl = uhl && cache_hl();
       c.G = G;
       c.rows = R;
       c.cols = cols;
@@ -1624,11 +1631,11 @@ void Engine::encoder_adjoint(const EvalSpec& e, bool causal) {
     };
     wg(d, f, UPm, gg, L.w_out, f, true);
     cr(UPm, d, L.b_out, Mat{}, Mat{}, 0);
-    wg(f, d, dh, n2, L.w_in, d, true);
-    cr(dh, f, L.b_in, Mat{}, Mat{}, 0);
+    wg(f, d, dh, n2, L.w_in, d, true, true);
+    cr(dh, f, L.b_in, Mat{}, Mat{}, 0, true);
     cr(dn2, d, L.ln2_b, u, st2, L.ln2_g);
-    wg(d, d, da1, ctx, L.w_o, d);
-    cr(da1, d, L.b_o, Mat{}, Mat{}, 0);
+    wg(d, d, da1, ctx, L.w_o, d, false, true);
+    cr(da1, d, L.b_o, Mat{}, Mat{}, 0, true);
     wg(3 * d, d, dqkv, n1, L.w_qkv, d, true);
     cr(dqkv, 3 * d, L.b_qkv, Mat{}, Mat{}, 0);
     cr(dn1, d, L.ln1_b, X, st1, L.ln1_g);
@@ -1683,8 +1690,12 @@ void Engine::decoder_adjoint(const EvalSpec& e) {
             [&] { launch_mask_copy(G, R, d, UPm, UPy, dmask(1, l0, ls), active_, stream_); });
     }
     // pre-split dgrad A operands as in encoder_adjoint
-    const bool keepb = e.want_grads || e.bact.base != nullptr;
-    const Mat h_dh = dgrad_hl(G, 1, f), h_da1 = dgrad_hl(G, 0, d);
+    // with cache_hl() the dh / da1 slots hold their pre-split rows only (the
+    // weight gradients and the bias column sums read them so)
+    const bool keep32 = e.want_grads || e.bact.base != nullptr;  // fp32 dqkv for the wgrad
+    const bool keepb = keep32 && !cache_hl();
+    const Mat h_dh = cache_hl() ? dh : dgrad_hl(G, 1, f),
+              h_da1 = cache_hl() ? da1 : dgrad_hl(G, 0, d);
     GemmArgs g = mk(R, f, d, UPm, L.w_out, f);
     g.Ahl = pack_upstream(G, R, UPm);
     g.ep.kind = EPI_GELU_BWD;
@@ -1766,7 +1777,7 @@ void Engine::decoder_adjoint(const EvalSpec& e) {
     const bool dqkv_hl =
         attention_bwd(G, qkv, qkv.offset(d), qkv.offset(2 * d), Pm, ctx, dctx, dPm, dqkv,
                       dqkv.offset(d), dqkv.offset(2 * d), sy_, sy_, true, h_dqkv, h_dqkv.offset(d),
-                      h_dqkv.offset(2 * d), keepb);
+                      h_dqkv.offset(2 * d), keep32);
 
     g = mk(R, d, 3 * d, dqkv, L.w_qkv, d);
     if (dqkv_hl) g.Ahl = h_dqkv;
@@ -1812,7 +1823,8 @@ void Engine::decoder_adjoint(const EvalSpec& e) {
 
   if (e.want_grads) {
     const float gs = e.gscale;
-    auto wg = [&](int M, int N, int K, Mat A, Mat Bm, long long w, int ldw, bool bhl = false) {
+    auto wg = [&](int M, int N, int K, Mat A, Mat Bm, long long w, int ldw, bool bhl = false,
+                  bool ahl = false) {
       GemmArgs w_;
       w_.G = G;
       w_.M = M;
@@ -1823,13 +1835,16 @@ void Engine::decoder_adjoint(const EvalSpec& e) {
       w_.a_mn = true;
       w_.b_mn = true;
       w_.b_mn_hl = bhl && cache_hl();
+      w_.a_mn_hl = ahl && cache_hl();
       w_.ep.kind = EPI_GRAD_ACC;
       w_.ep.out1 = grad(w, ldw, l0, ls);
       w_.ep.gscale = gs;
       gemm(w_);
     };
-    auto cr = [&](int rows, Mat up, int cols, long long b, Mat x, Mat st, long long gn) {
+    auto cr = [&](int rows, Mat up, int cols, long long b, Mat x, Mat st, long long gn,
+                  bool uhl = false) {
       ColRedArgs c;
+      c.up_hl = uhl && cache_hl();
       c.G = G;
       c.rows = rows;
       c.cols = cols;
@@ -1848,8 +1863,8 @@ void Engine::decoder_adjoint(const EvalSpec& e) {
     };
     wg(d, f, R, UPm, gg, L.w_out, f, true);
     cr(R, UPm, d, L.b_out, Mat{}, Mat{}, 0);
-    wg(f, d, R, dh, n2, L.w_in, d, true);
-    cr(R, dh, f, L.b_in, Mat{}, Mat{}, 0);
+    wg(f, d, R, dh, n2, L.w_in, d, true, true);
+    cr(R, dh, f, L.b_in, Mat{}, Mat{}, 0, true);
     cr(R, dn2, d, L.ln2_b, u2, st2, L.ln2_g);
     wg(d, d, R, dcp, cctx, L.w_co, d);
     cr(R, dcp, d, L.b_co, Mat{}, Mat{}, 0);
@@ -1858,8 +1873,8 @@ void Engine::decoder_adjoint(const EvalSpec& e) {
     wg(2 * d, d, Tx_, dckv, X, L.w_ckv, d);
     cr(Tx_, dckv, 2 * d, L.b_ckv, Mat{}, Mat{}, 0);
     cr(R, dn3, d, L.ln3_b, u3, st3, L.ln3_g);
-    wg(d, d, R, da1, ctx, L.w_o, d);
-    cr(R, da1, d, L.b_o, Mat{}, Mat{}, 0);
+    wg(d, d, R, da1, ctx, L.w_o, d, false, true);
+    cr(R, da1, d, L.b_o, Mat{}, Mat{}, 0, true);
     wg(3 * d, d, R, dqkv, n1, L.w_qkv, d, true);
     cr(R, dqkv, 3 * d, L.b_qkv, Mat{}, Mat{}, 0);
     cr(R, dn1, d, L.ln1_b, Y, st1, L.ln1_g);

@@ -73,6 +73,7 @@ struct TcParams {
   TcOperand a, b;
   int a_mn, b_mn;  // staging layout of the converted operands
   int b_hl;        // B's MN-major staging holds pre-split rows (GemmArgs::b_mn_hl)
+  int a_hl;        // likewise A (GemmArgs::a_mn_hl)
   int b_direct;    // B comes pre-split (hi|lo tiles TMA'd straight into the MMA ring)
   int a_direct;    // A too (K-major, produced pre-split): no conversion at all
   int passes;      // 3 = hi.hi + (lo.hi + hi.lo); 1 = hi.hi only (diagnostics)
@@ -436,7 +437,10 @@ __global__ void __launch_bounds__(Cfg<CG>::THREADS, 1)
         wait(&empty[s], ((kg / NH) & 1) ^ 1);  // hi|lo buffers no longer read by the MMAs
         if (kc == 0 && lane == 0) flush(6);
         if (!(p.debug & 1)) {
-          convert_tile(smem_u32(stg_a(sa)), smem_u32(hl_a(s)), p.a_mn, kc, lane, amax);
+          if (p.a_hl)
+            regroup_tile(smem_u32(stg_a(sa)), smem_u32(hl_a(s)), kc, lane);
+          else
+            convert_tile(smem_u32(stg_a(sa)), smem_u32(hl_a(s)), p.a_mn, kc, lane, amax);
           if (!p.b_direct) {
             if (p.b_hl)
               regroup_tile(smem_u32(stg_b(sa)), smem_u32(hl_b(s)), kc, lane);
@@ -781,6 +785,9 @@ Prepared prepare(const GemmArgs& a) {
   p.b_direct = a.Bhl.ok() ? 1 : 0;
   p.b_mn = p.b_direct ? 0 : a.b_mn;
   p.b_hl = (!p.b_direct && a.b_mn && a.b_mn_hl) ? 1 : 0;
+  p.a_hl = (a.a_mn && a.a_mn_hl && !a.Ahl.ok()) ? 1 : 0;
+  if (a.a_mn_hl && (!a.a_mn || a.M % 32))
+    throw ContractViolation("gemm_tc: pre-split MN-major A needs an MN-major, 32-aligned A");
   if (a.b_mn_hl && (p.b_direct || !a.b_mn || a.N % 32))
     throw ContractViolation("gemm_tc: pre-split MN-major B needs an MN-major, 32-aligned B");
   p.a_direct = (a.Ahl.ok() && p.b_direct && !a.a_mn) ? 1 : 0;

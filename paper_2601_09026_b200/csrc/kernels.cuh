@@ -45,6 +45,8 @@ struct ColRedArgs {
   // two-stage row-chunked form (fixed-order partials, then an ordered sum)
   double* partials = nullptr;
   long long partials_cap = 0;
+  // up rows pre-split (hi|lo' per 32-column chunk; value = hi + 2^-11 lo')
+  int up_hl = 0;
 };
 constexpr int kColRedChunks = 8;
 void launch_colred(const ColRedArgs& a, const int* active, cudaStream_t s);

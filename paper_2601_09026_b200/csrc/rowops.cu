@@ -380,7 +380,21 @@ __global__ void __launch_bounds__(256) colred_part_kernel(ColRedArgs a, const in
     const float* st = x ? a.stats.at(g) : nullptr;
 #pragma unroll 4
     for (int r = r0 + ty; r < r1; r += 8) {
-      const float4 u = ld4(up + (long long)r * a.up.ld + c);
+      float4 u;
+      if (a.up_hl) {
+        const char* row = reinterpret_cast<const char*>(up + (long long)r * a.up.ld);
+        const char* hp = row + (c >> 5) * 128 + (c & 31) * 2;
+        const uint2 hv = *reinterpret_cast<const uint2*>(hp);
+        const uint2 lv = *reinterpret_cast<const uint2*>(hp + 64);
+        const float2 h01 = __half22float2(*reinterpret_cast<const __half2*>(&hv.x));
+        const float2 h23 = __half22float2(*reinterpret_cast<const __half2*>(&hv.y));
+        const float2 l01 = __half22float2(*reinterpret_cast<const __half2*>(&lv.x));
+        const float2 l23 = __half22float2(*reinterpret_cast<const __half2*>(&lv.y));
+        u = make_float4(fmaf(l01.x, 1.f / 2048.f, h01.x), fmaf(l01.y, 1.f / 2048.f, h01.y),
+                        fmaf(l23.x, 1.f / 2048.f, h23.x), fmaf(l23.y, 1.f / 2048.f, h23.y));
+      } else {
+        u = ld4(up + (long long)r * a.up.ld + c);
+      }
       b[0] += (double)u.x;
       b[1] += (double)u.y;
       b[2] += (double)u.z;
@@ -743,8 +757,11 @@ void launch_softmax(const SoftmaxArgs& a, const int* active, cudaStream_t s) {
 
 void launch_colred(const ColRedArgs& a, const int* active, cudaStream_t s) {
   if (a.rows == 0 || a.G == 0) return;
-  if (a.partials && a.cols % 4 == 0 && vec_ok(a.up) && vec_ok(a.x) &&
-      (long long)a.G * kColRedChunks * a.cols * 2 <= a.partials_cap) {
+  const bool two_stage = a.partials && a.cols % 4 == 0 && vec_ok(a.up) && vec_ok(a.x) &&
+                         (long long)a.G * kColRedChunks * a.cols * 2 <= a.partials_cap;
+  if (a.up_hl && (!two_stage || a.cols % 32))
+    throw ContractViolation("colred: pre-split rows need the two-stage form and 32-aligned columns");
+  if (two_stage) {
     launch_k(colred_part_kernel, dim3(dim3(ceil_div(a.cols, 128), kColRedChunks, a.G)), dim3(256), 0, s, 1, a, active);
     launch_k(colred_sum_kernel, dim3(dim3(ceil_div(a.cols, 256), a.G)), dim3(256), 0, s, 1, a, active);
     return;

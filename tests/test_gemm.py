@@ -101,6 +101,24 @@ def test_presplit_mn_major_b_is_bitwise_the_converted_path(shape):
     assert torch.equal(outs[0], outs[1])
 
 
+@pytest.mark.parametrize("shape", [(2, 256, 384, 512), (1, 3072, 768, 1000)])
+def test_presplit_mn_major_a_is_bitwise_the_converted_path(shape):
+    """the weight-gradient A operand (the cached dgrad chain) handed over as
+    pre-split rows: regrouped by the converters, same bits as the split"""
+    G, M, N_, K = shape
+    g = torch.Generator(device="cpu").manual_seed(6)
+    A = torch.randn(G, K, M, generator=g).float().cuda()       # [K][M]
+    B = (torch.randn(G, K, N_, generator=g) * 0.3).float().cuda()  # [K][N]
+    outs = []
+    for flag in (0, 8):
+        C = torch.full((G, M, N_), float("nan"), device="cuda")
+        N.call("mglp_test_gemm", G, M, N_, K, A.data_ptr(), K * M, M, 1, B.data_ptr(), K * N_, N_,
+               1, flag, None, C.data_ptr(), M * N_, N_, 0, None)
+        outs.append(C)
+    assert not torch.isnan(outs[1]).any()
+    assert torch.equal(outs[0], outs[1])
+
+
 def test_split_is_effective():
     """the 3-pass fp16 split with a separate correction accumulator must be
     fp32-class (~6e-6 at K=2048); a single fp16 pass sits at ~5e-4"""
