@@ -115,10 +115,21 @@ mglp_status mglp_engine_backward(mglp_engine* e, int batch, int s_x, int s_y,
                                  double* grads_accum, double* trace_out, int max_trace,
                                  int* n_trace, int* converged);
 
-/* WarmSnapshot snapshot() / restore() / reset() (adjoint.hpp:187-206) */
+/* WarmSnapshot snapshot() / restore() / reset() (adjoint.hpp:187-206).
+ * The engine keeps ONE snapshot slot: snapshot_id returns the id of the
+ * snapshot just taken, restore_id(id) fails with status 1 if that snapshot
+ * was overwritten (a later snapshot or a shape change); restore() restores
+ * whatever the slot holds. */
 mglp_status mglp_engine_snapshot(mglp_engine* e);
 mglp_status mglp_engine_restore(mglp_engine* e);
+mglp_status mglp_engine_snapshot_id(mglp_engine* e, long long* id);
+mglp_status mglp_engine_restore_id(mglp_engine* e, long long id);
 mglp_status mglp_engine_reset(mglp_engine* e);
+/* The forward solver's warm states := the device trajectory currently held
+ * (e.g. after mglp_serial_forward): the next warm-guess forward starts there.
+ * (Serial sweeps and uploaded trajectories otherwise never touch the
+ * solver's warm states, as in the reference.) */
+mglp_status mglp_engine_seed_forward_from_traj(mglp_engine* e);
 
 /* serial_forward / serial_adjoint (blocks.cpp:659-682). lam_all_out
  * (nullable) receives lambda at every time point. */
@@ -157,10 +168,18 @@ mglp_status mglp_engine_graph_replay(mglp_engine* e);
 mglp_status mglp_engine_zero_grads(mglp_engine* e);
 /* flat (visit_params order) += device gradient bank */
 mglp_status mglp_engine_get_grads(mglp_engine* e, double* flat, long long n);
+/* flat (n = the parameter count of layers [layer_lo, layer_hi), visit_params
+ * order) += those layers' gradients: per-layer-block download (a rank's
+ * owned block; full-depth parity checks without a whole-model host copy) */
+mglp_status mglp_engine_get_grads_layers(mglp_engine* e, int layer_lo, int layer_hi,
+                                         double* flat, long long n);
 /* PhaseTrace of the last forward (which=0) or backward (which=1) solve */
 mglp_status mglp_engine_trace(mglp_engine* e, int which, double* trace_out, int max_trace,
                               int* n_trace, int* converged);
 /* device pointer of the trajectory (total_layers+1 states) */
+/* copies time points [first, first+count) of the device trajectory (fp32,
+ * state_elems floats per point, padding included) to dst (host or device) */
+mglp_status mglp_engine_read_traj(mglp_engine* e, int first, int count, float* dst);
 mglp_status mglp_engine_traj_device(mglp_engine* e, float** traj);
 mglp_status mglp_engine_sync(mglp_engine* e);
 /* hot-path kernel launches issued since the last call (then reset) */

@@ -71,6 +71,9 @@ _SIGS = {
                              _ip, _ip],
     "mglp_engine_snapshot": [_vp],
     "mglp_engine_restore": [_vp],
+    "mglp_engine_snapshot_id": [_vp, C.POINTER(C.c_longlong)],
+    "mglp_engine_restore_id": [_vp, C.c_longlong],
+    "mglp_engine_seed_forward_from_traj": [_vp],
     "mglp_engine_reset": [_vp],
     "mglp_serial_forward": [_vp, C.c_int, C.c_int, C.c_int, _dp, _dp],
     "mglp_serial_adjoint": [_vp, C.c_int, C.c_int, C.c_int, _dp, _dp, _dp, _dp],
@@ -87,6 +90,8 @@ _SIGS = {
     "mglp_engine_graph_capture": [_vp, _vp, _vp, _vp, C.c_int],
     "mglp_engine_graph_replay": [_vp],
     "mglp_engine_get_grads": [_vp, _dp, C.c_longlong],
+    "mglp_engine_get_grads_layers": [_vp, C.c_int, C.c_int, _dp, C.c_longlong],
+    "mglp_engine_read_traj": [_vp, C.c_int, C.c_int, _vp],
     "mglp_engine_trace": [_vp, C.c_int, _dp, C.c_int, _ip, _ip],
     "mglp_engine_traj_device": [_vp, C.POINTER(_vp)],
     "mglp_engine_sync": [_vp],

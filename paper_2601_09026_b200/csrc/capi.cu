@@ -91,6 +91,8 @@ void download(mglp_engine* e, double* dst, const float* src, const Shape& sh, lo
 
 void upload_traj(mglp_engine* e, const double* traj, const Shape& sh) {
   const long long T = e->eng->total_layers() + 1;
+  // traj_ also holds the forward solver's warm window: keep it apart
+  e->eng->displace_forward_window();
   std::vector<float> h(sh.n_dev * T, 0.f);
   for (long long s = 0; s < T; ++s)
     for (long long i = 0; i < sh.n_logical; ++i) h[s * sh.n_dev + i] = (float)traj[s * sh.n_logical + i];
@@ -387,6 +389,12 @@ mglp_status mglp_engine_set_config(mglp_engine* e, const mglp_solve_config* cfg)
     SolveCfg& c = e->eng->config();
     if (cfg->coarsen != c.coarsen || cfg->levels != c.levels)
       throw ValidationError("set_config: the hierarchy (coarsen, levels) is fixed at creation");
+    // the iteration budgets, tolerances and guess policy are baked into a
+    // captured step: a change drops it (replay then refuses until recapture)
+    if (cfg->fwd_iters != c.fwd_iters || cfg->bwd_iters != c.bwd_iters ||
+        cfg->fwd_tol != c.fwd_tol || cfg->bwd_tol != c.bwd_tol ||
+        cfg->cold_guess != c.cold_guess || cfg->warm_start != c.warm_start)
+      e->eng->drop_graph();
     c.fwd_iters = cfg->fwd_iters;
     c.bwd_iters = cfg->bwd_iters;
     c.fwd_tol = cfg->fwd_tol;
@@ -444,6 +452,29 @@ mglp_status mglp_engine_restore(mglp_engine* e) {
   });
 }
 
+mglp_status mglp_engine_snapshot_id(mglp_engine* e, long long* id) {
+  return guard([&] {
+    need(e, "engine");
+    need(id, "id");
+    *id = e->eng->snapshot();
+  });
+}
+
+mglp_status mglp_engine_restore_id(mglp_engine* e, long long id) {
+  return guard([&] {
+    need(e, "engine");
+    if (id <= 0) throw ValidationError("restore: invalid snapshot id");
+    e->eng->restore(id);
+  });
+}
+
+mglp_status mglp_engine_seed_forward_from_traj(mglp_engine* e) {
+  return guard([&] {
+    need(e, "engine");
+    e->eng->seed_forward_from_traj();
+  });
+}
+
 mglp_status mglp_engine_reset(mglp_engine* e) {
   return guard([&] {
     need(e, "engine");
@@ -459,10 +490,8 @@ mglp_status mglp_serial_forward(mglp_engine* e, int batch, int s_x, int s_y, con
     const Shape sh = ensure_shape(e, batch, s_x, s_y, e->eng->width());
     upload(e, e->dz, z0, sh);
     e->eng->serial_forward_device(e->dz);
-    if (traj_out)
-      download(e, traj_out, e->eng->traj_dev(), sh, e->eng->total_layers() + 1);
-    else
-      MGLP_CUDA(cudaStreamSynchronize(e->eng->stream()));
+    e->eng->check_range();
+    if (traj_out) download(e, traj_out, e->eng->traj_dev(), sh, e->eng->total_layers() + 1);
   });
 }
 
@@ -482,6 +511,7 @@ mglp_status mglp_serial_adjoint(mglp_engine* e, int batch, int s_x, int s_y,
     upload(e, e->dl, lam_n, sh);
     if (grads_accum) e->eng->zero_grads();
     e->eng->serial_adjoint_device(e->dl, e->dl0, grads_accum != nullptr);
+    e->eng->check_range();
     if (lam_all_out)
       download(e, lam_all_out, e->eng->lam_all_dev(), sh, e->eng->total_layers() + 1);
     if (grads_accum) e->eng->get_grads(grads_accum);
@@ -498,6 +528,7 @@ mglp_status mglp_stack_step(mglp_engine* e, int layer, double dt, int batch, int
     const Shape sh = ensure_shape(e, batch, s_x, s_y, e->eng->width());
     upload(e, e->dz, z, sh);
     e->eng->step_device(layer, dt, e->dz, e->dl0);
+    e->eng->check_range();
     download(e, out, e->dl0, sh, 1);
   });
 }
@@ -515,6 +546,7 @@ mglp_status mglp_stack_adjoint_step(mglp_engine* e, int layer, double dt, int ba
     upload(e, e->dl, lam, sh);
     if (grads_accum) e->eng->zero_grads();
     e->eng->adjoint_step_device(layer, dt, e->dz, e->dl, e->dl0, grads_accum != nullptr, gscale);
+    e->eng->check_range();
     download(e, out, e->dl0, sh, 1);
     if (grads_accum) e->eng->get_grads(grads_accum);
   });
@@ -584,6 +616,34 @@ mglp_status mglp_engine_get_grads(mglp_engine* e, double* flat, long long n) {
     need(flat, "flat");
     if (n != e->eng->num_params()) throw ValidationError("get_grads: parameter count mismatch");
     e->eng->get_grads(flat);
+  });
+}
+
+mglp_status mglp_engine_get_grads_layers(mglp_engine* e, int layer_lo, int layer_hi,
+                                        double* flat, long long n) {
+  return guard([&] {
+    need(e, "engine");
+    need(flat, "flat");
+    if (layer_lo < 0 || layer_hi > e->eng->total_layers() || layer_lo >= layer_hi)
+      throw ValidationError("get_grads_layers: bad layer range");
+    const long long want = e->eng->flat_offset(layer_hi) - e->eng->flat_offset(layer_lo);
+    if (n != want) throw ValidationError("get_grads_layers: parameter count mismatch");
+    e->eng->get_grads_range(layer_lo, layer_hi, flat);
+  });
+}
+
+mglp_status mglp_engine_read_traj(mglp_engine* e, int first, int count, float* dst) {
+  return guard([&] {
+    need(e, "engine");
+    need(dst, "dst");
+    const int T = e->eng->total_layers() + 1;
+    if (first < 0 || count < 0 || first + count > T)
+      throw ValidationError("read_traj: time points out of range");
+    const size_t n = (size_t)e->eng->state_elems();
+    MGLP_CUDA(cudaMemcpyAsync(dst, e->eng->traj_dev() + (size_t)first * n,
+                              (size_t)count * n * sizeof(float), cudaMemcpyDefault,
+                              e->eng->stream()));
+    MGLP_CUDA(cudaStreamSynchronize(e->eng->stream()));
   });
 }
 

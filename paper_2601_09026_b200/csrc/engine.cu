@@ -143,7 +143,7 @@ Engine::~Engine() {
   free_solver(bwd_);
   if (range_flag_) cudaFree(range_flag_);
   for (float* p : {P_, Whl_, Gr_, scratch_, hlscr_, cache_, bscratch_, bcache_, traj_, lam_all_,
-                   zero_state_, snap_fwd_, snap_bwd_})
+                   zero_state_, snap_fwd_, snap_bwd_, fwd_stash_})
     if (p) cudaFree(p);
   if (colred_part_) cudaFree(colred_part_);
   if (drop_masks_) cudaFree(drop_masks_);
@@ -353,6 +353,8 @@ void Engine::set_params(const double* flat) {
   const size_t n = host.size();
   MGLP_CUDA(cudaMemcpyAsync(P_, host.data(), n * sizeof(float), cudaMemcpyHostToDevice, stream_));
   repack_weights();
+  // cached activations were computed with the old parameters
+  invalidate_linearization();
   MGLP_CUDA(cudaStreamSynchronize(stream_));
 }
 
@@ -369,14 +371,24 @@ void Engine::get_params(double* flat) const {
   }
 }
 
-void Engine::get_grads(double* flat) const {
-  MGLP_CUDA(cudaStreamSynchronize(stream_));
-  std::vector<float> host((size_t)total_ * layer_stride_);
-  MGLP_CUDA(cudaMemcpy(host.data(), Gr_, host.size() * sizeof(float), cudaMemcpyDeviceToHost));
+void Engine::get_grads(double* flat) const { get_grads_range(0, total_, flat); }
+
+long long Engine::flat_offset(int layer) const {
   long long fo = 0;
-  for (int l = 0; l < total_; ++l) {
+  for (int l = 0; l < layer; ++l) fo += lay_[(sd_.kind == 2 && l >= n_split_) ? 1 : 0].flat_size;
+  return fo;
+}
+
+void Engine::get_grads_range(int lo, int hi, double* flat) const {
+  if (lo < 0 || hi > total_ || lo > hi) throw ValidationError("get_grads: bad layer range");
+  MGLP_CUDA(cudaStreamSynchronize(stream_));
+  std::vector<float> host((size_t)(hi - lo) * layer_stride_);
+  MGLP_CUDA(cudaMemcpy(host.data(), Gr_ + (size_t)lo * layer_stride_, host.size() * sizeof(float),
+                       cudaMemcpyDeviceToHost));
+  long long fo = 0;
+  for (int l = lo; l < hi; ++l) {
     const LayerLayout& L = lay_[(sd_.kind == 2 && l >= n_split_) ? 1 : 0];
-    const float* src = host.data() + (size_t)l * layer_stride_;
+    const float* src = host.data() + (size_t)(l - lo) * layer_stride_;
     for (const Piece& p : L.pieces)
       for (long long e = 0; e < p.n; ++e) flat[fo + p.flat_off + e] += src[p.dev_off + e];
     fo += L.flat_size;
@@ -405,7 +417,7 @@ void Engine::set_shape(int batch, int s_x, int s_y) {
   if (colred_part_) cudaFree(colred_part_);
   colred_part_ = nullptr;
   for (float** p : {&scratch_, &hlscr_, &cache_, &bscratch_, &bcache_, &traj_, &lam_all_, &zero_state_,
-                    &snap_fwd_, &snap_bwd_}) {
+                    &snap_fwd_, &snap_bwd_, &fwd_stash_}) {
     if (*p) cudaFree(*p);
     *p = nullptr;
   }
@@ -529,6 +541,8 @@ void Engine::set_shape(int batch, int s_x, int s_y) {
   }
   std::fill(cache_valid_.begin(), cache_valid_.end(), 0);
   first_fwd_ = first_bwd_ = true;
+  fwd_displaced_ = false;
+  snap_id_ = 0;  // the snapshot slot was freed with the old shape
   MGLP_CUDA(cudaStreamSynchronize(stream_));
 }
 
@@ -2152,6 +2166,15 @@ void Engine::forward_device(const float* z0_dev) {
   for (int l = 0; l < ib_; ++l) serial_step(l);
   const int guess = (first_fwd_ || !cfg_.warm_start) ? cfg_.cold_guess : 2;
   first_fwd_ = false;
+  if (fwd_displaced_) {
+    // the warm window was displaced by another trajectory: bring it back
+    // (points 1..N; point 0 is the initial condition just set)
+    if (guess == 2)
+      MGLP_CUDA(cudaMemcpyAsync(fwd_.lv[0].v + state_n_, fwd_stash_ + state_n_,
+                                (size_t)N_ * state_n_ * sizeof(float), cudaMemcpyDeviceToDevice,
+                                stream_));
+    fwd_displaced_ = false;
+  }
   Mat v0 = lv_v(fwd_, 0, 0, 0);
   if (guess == 0) {
     launch_copy(N_, state_n_, lv_v(fwd_, 0, 1, 1), v0, nullptr, stream_);
@@ -2324,43 +2347,75 @@ void Engine::drop_graph() {
 
 void Engine::read_trace(bool fwd, std::vector<double>* trace, bool* converged) {
   SolveCtrl c;
-  int range = 0;
   MGLP_CUDA(cudaMemcpyAsync(&c, fwd ? fwd_.ctrl : bwd_.ctrl, sizeof(SolveCtrl),
                             cudaMemcpyDeviceToHost, stream_));
-  MGLP_CUDA(cudaMemcpyAsync(&range, range_flag_, sizeof(int), cudaMemcpyDeviceToHost, stream_));
-  MGLP_CUDA(cudaStreamSynchronize(stream_));
-  if (range) {
-    MGLP_CUDA(cudaMemsetAsync(range_flag_, 0, sizeof(int), stream_));
-    throw ContractViolation(
-        "a GEMM operand exceeded the fp16 range of the split tensor-core path (|x| >= 65520)");
-  }
+  check_range();
   trace->assign(c.trace, c.trace + std::min(c.n_trace, kMaxTrace));
   *converged = c.converged != 0;
 }
 
-void Engine::snapshot() {  // adjoint.hpp:187-194
+long long Engine::snapshot() {  // adjoint.hpp:187-194
   const size_t bytes = (size_t)(N_ + 1) * state_n_ * sizeof(float);
   if (!snap_fwd_) MGLP_CUDA(cudaMalloc(&snap_fwd_, bytes));
   if (!snap_bwd_) MGLP_CUDA(cudaMalloc(&snap_bwd_, bytes));
-  MGLP_CUDA(cudaMemcpyAsync(snap_fwd_, fwd_.lv[0].v, bytes, cudaMemcpyDeviceToDevice, stream_));
+  // the forward solver's warm states: the trajectory window, or its stash
+  // while another trajectory occupies traj_
+  const float* fv = fwd_displaced_ ? fwd_stash_ : fwd_.lv[0].v;
+  MGLP_CUDA(cudaMemcpyAsync(snap_fwd_, fv, bytes, cudaMemcpyDeviceToDevice, stream_));
   MGLP_CUDA(cudaMemcpyAsync(snap_bwd_, bwd_.lv[0].v, bytes, cudaMemcpyDeviceToDevice, stream_));
   snap_first_fwd_ = first_fwd_;
   snap_first_bwd_ = first_bwd_;
+  snap_id_ = ++snap_seq_;
+  return snap_id_;
 }
 
-void Engine::restore() {  // adjoint.hpp:196-201
-  if (!snap_fwd_) throw ValidationError("restore: no snapshot taken");
+void Engine::restore(long long id) {  // adjoint.hpp:196-201
+  if (!snap_fwd_ || snap_id_ == 0) throw ValidationError("restore: no snapshot taken");
+  if (id >= 0 && id != snap_id_)
+    throw ValidationError("restore: that snapshot was overwritten by a later snapshot or a shape "
+                          "change (the engine keeps one snapshot slot)");
   const size_t bytes = (size_t)(N_ + 1) * state_n_ * sizeof(float);
-  MGLP_CUDA(cudaMemcpyAsync(fwd_.lv[0].v, snap_fwd_, bytes, cudaMemcpyDeviceToDevice, stream_));
+  // restore the forward warm states into the stash: traj_ keeps the current
+  // trajectory (a following backward may linearise at it); the next forward
+  // solve moves the stash back into its window
+  if (!fwd_stash_) MGLP_CUDA(cudaMalloc(&fwd_stash_, bytes));
+  MGLP_CUDA(cudaMemcpyAsync(fwd_stash_, snap_fwd_, bytes, cudaMemcpyDeviceToDevice, stream_));
+  fwd_displaced_ = true;
   MGLP_CUDA(cudaMemcpyAsync(bwd_.lv[0].v, snap_bwd_, bytes, cudaMemcpyDeviceToDevice, stream_));
   first_fwd_ = snap_first_fwd_;
   first_bwd_ = snap_first_bwd_;
-  std::fill(cache_valid_.begin(), cache_valid_.end(), 0);
+}
+
+void Engine::displace_forward_window() {
+  if (fwd_displaced_ || eval_only_ || !traj_ || fwd_.lv.empty()) return;
+  const size_t bytes = (size_t)(N_ + 1) * state_n_ * sizeof(float);
+  if (!fwd_stash_) MGLP_CUDA(cudaMalloc(&fwd_stash_, bytes));
+  MGLP_CUDA(cudaMemcpyAsync(fwd_stash_, fwd_.lv[0].v, bytes, cudaMemcpyDeviceToDevice, stream_));
+  fwd_displaced_ = true;
+}
+
+void Engine::seed_forward_from_traj() {
+  if (eval_only_ || !traj_ || fwd_.lv.empty()) throw ValidationError("seed: set_shape first");
+  fwd_displaced_ = false;
+  displace_forward_window();  // stash := the window as it is now
+}
+
+void Engine::check_range() {
+  int range = 0;
+  MGLP_CUDA(cudaMemcpyAsync(&range, range_flag_, sizeof(int), cudaMemcpyDeviceToHost, stream_));
+  MGLP_CUDA(cudaStreamSynchronize(stream_));
+  if (range) {
+    MGLP_CUDA(cudaMemsetAsync(range_flag_, 0, sizeof(int), stream_));
+    MGLP_CUDA(cudaStreamSynchronize(stream_));
+    throw ContractViolation(
+        "a GEMM operand exceeded the fp16 range of the split tensor-core path (|x| >= 65520)");
+  }
 }
 
 // ---- serial sweeps (blocks.cpp:659-682) ----
 void Engine::serial_forward_device(const float* z0_dev) {
   MGLP_CUDA(cudaSetDevice(device_));
+  displace_forward_window();
   MGLP_CUDA(cudaMemcpyAsync(traj_, z0_dev, state_n_ * sizeof(float), cudaMemcpyDeviceToDevice,
                             stream_));
   for (int l = 0; l < total_; ++l) {
@@ -2421,9 +2476,20 @@ __global__ void dropout_gen_kernel(unsigned char* m, const unsigned long long* k
 }
 }  // namespace
 
+void Engine::clear_dropout() {
+  if (!drop_on_) return;
+  drop_on_ = false;
+  // cached activations / a captured step used the masks
+  invalidate_linearization();
+  drop_graph();
+}
+
 void Engine::refresh_dropout(uint64_t seed, uint64_t batch_index) {
+  const bool was_on = drop_on_;
   drop_on_ = false;
   if (sd_.dropout <= 0.0) return;
+  invalidate_linearization();  // the cached activations used the old masks
+  if (!was_on) drop_graph();   // a captured step ran without masks
   if (!traj_) throw ValidationError("refresh_dropout: set the shape first");
   const long long slot = (long long)std::max(Tx_, Ty_) * sd_.d;
   const int nblk = total_ * 3;

@@ -78,6 +78,9 @@ class Engine {
   void set_params(const double* flat);
   void get_params(double* flat) const;
   void get_grads(double* flat_accum) const;  // flat += device grads
+  // flat (covering layers [lo, hi) only, visit_params order) += their grads
+  void get_grads_range(int lo, int hi, double* flat_accum) const;
+  long long flat_offset(int layer) const;  // first flat index of `layer`
   void zero_grads();
   // device parameter / gradient slabs (fp32, layer-major, kernel layout) and
   // the host mapping between that layout and the flat visit_params order
@@ -97,7 +100,7 @@ class Engine {
   // on the fly from the reference's counter streams); clear: no masks (the
   // exact map, as for evaluation). No-ops when the stack's dropout is 0.
   void refresh_dropout(uint64_t seed, uint64_t batch_index);
-  void clear_dropout() { drop_on_ = false; }
+  void clear_dropout();
   bool dropout_active() const { return drop_on_; }
 
   // ---- shape ----
@@ -119,10 +122,29 @@ class Engine {
   void backward_device(const float* lamN_dev, float* lam0_dev, bool want_grads,
                        bool traj_is_current);
   void read_trace(bool fwd, std::vector<double>* trace, bool* converged);
-  void snapshot();
-  void restore();
+  // WarmSnapshot (adjoint.hpp:187-206): one slot per engine; snapshot()
+  // returns its id, restore(id) refuses an id that has been overwritten
+  long long snapshot();
+  void restore(long long id = -1);
   void reset() { first_fwd_ = first_bwd_ = true; }
   void invalidate_linearization() { std::fill(cache_valid_.begin(), cache_valid_.end(), 0); }
+  // The forward solver's level-0 states ARE the trajectory window
+  // traj[ib..ie] (no copy per solve). Anything else that writes traj_ -- a
+  // serial sweep, evaluation, an uploaded trajectory -- first calls this: the
+  // warm window moves to a stash and the next forward solve brings it back,
+  // so the solver's warm start never sees another trajectory (the reference
+  // keeps serial_forward's output apart from the engine's solver states,
+  // blocks.cpp:659-666, adjoint.hpp:113-137).
+  void displace_forward_window();
+  // the forward solver's warm states := the current device trajectory (e.g.
+  // the serial sweep's): seeds the next warm-guess solve with it (the
+  // fixed-point self-test of SURVEY 8(c))
+  void seed_forward_from_traj();
+  // fp16-split range flag: throws ContractViolation (and clears the flag) if
+  // a GEMM operand or pre-split producer saw |x| >= 65520 since the last
+  // check. Synchronises the engine stream; host-facing entry points call it.
+  void check_range();
+  int* range_flag() const { return range_flag_; }
 
   // CUDA graph of one full training-step solve (forward_device +
   // backward_device on fixed device buffers). Every host decision of the
@@ -374,6 +396,10 @@ class Engine {
   // snapshot
   float* snap_fwd_ = nullptr;
   float* snap_bwd_ = nullptr;
+  long long snap_id_ = 0;       // id of the snapshot in the slot (0: none)
+  long long snap_seq_ = 0;
+  float* fwd_stash_ = nullptr;  // displaced forward warm window (N+1 states)
+  bool fwd_displaced_ = false;
   bool snap_first_fwd_ = true, snap_first_bwd_ = true;
   long long launches_ = 0;
   cudaGraphExec_t graph_exec_ = nullptr;

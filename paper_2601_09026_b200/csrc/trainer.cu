@@ -512,8 +512,10 @@ void Trainer::sync_fp32() {
   eng_->params_updated();
   // head.w pre-split: logits (B = W, K = d) and dn = dlogits . W (B = W^T, K = V)
   const long long kd = pack_hl_cols(d_), kv = pack_hl_cols(V_);
-  launch_pack_hl(H32_ + hl_.w, 0, d_, Whl_, 0, (int)kd, 1, V_, d_, false, s_);
-  launch_pack_hl(H32_ + hl_.w, 0, d_, Whl_ + (long long)V_ * kd, 0, (int)kv, 1, d_, V_, true, s_);
+  launch_pack_hl(H32_ + hl_.w, 0, d_, Whl_, 0, (int)kd, 1, V_, d_, false, s_,
+                 eng_->range_flag());
+  launch_pack_hl(H32_ + hl_.w, 0, d_, Whl_ + (long long)V_ * kd, 0, (int)kv, 1, d_, V_, true, s_,
+                 eng_->range_flag());
 }
 
 void Trainer::make_batch(int split, long long start) {
@@ -558,6 +560,7 @@ double Trainer::head_forward_loss(const float* zfin, bool want_dl) {
   g.ep.kind = EPI_STORE;
   g.ep.out1 = mat(logits_, ldv_);
   g.ep.bias = mat(H32_ + hl_.b, 0);
+  g.range_flag = eng_->range_flag();
   launch_gemm_tc(g, nullptr, s_);
   cross_entropy_kernel<<<(T_ + 7) / 8, 256, 0, s_>>>(logits_, ldv_, tout_, T_, V_, dl_, row_loss_,
                                                       want_dl ? 1 : 0);
@@ -590,6 +593,7 @@ void Trainer::head_backward(const float* zfin) {
   w.ep.kind = EPI_GRAD_ACC;
   w.ep.out1 = mat(HG_ + hl_.w, d_);
   w.ep.gscale = 1.f;
+  w.range_flag = eng_->range_flag();
   launch_gemm_tc(w, nullptr, s_);
   // dn = dlogits . W
   GemmArgs g;
@@ -602,6 +606,7 @@ void Trainer::head_backward(const float* zfin) {
   g.Bhl = mat(Whl_ + (long long)V_ * pack_hl_cols(d_), (int)pack_hl_cols(V_));
   g.ep.kind = EPI_STORE;
   g.ep.out1 = mat(dn_, d_);
+  g.range_flag = eng_->range_flag();
   launch_gemm_tc(g, nullptr, s_);
   // lambda on the advancing stream = LN_f^T dn; the other stream is zero
   MGLP_CUDA(cudaMemsetAsync(lamN_, 0, eng_->state_elems() * sizeof(float), s_));
@@ -659,8 +664,10 @@ void Trainer::optimizer_step() {
   MGLP_CUDA(cudaGetLastError());
   eng_->params_updated();
   const long long kd = pack_hl_cols(d_), kv = pack_hl_cols(V_);
-  launch_pack_hl(H32_ + hl_.w, 0, d_, Whl_, 0, (int)kd, 1, V_, d_, false, s_);
-  launch_pack_hl(H32_ + hl_.w, 0, d_, Whl_ + (long long)V_ * kd, 0, (int)kv, 1, d_, V_, true, s_);
+  launch_pack_hl(H32_ + hl_.w, 0, d_, Whl_, 0, (int)kd, 1, V_, d_, false, s_,
+                 eng_->range_flag());
+  launch_pack_hl(H32_ + hl_.w, 0, d_, Whl_ + (long long)V_ * kd, 0, (int)kv, 1, d_, V_, true, s_,
+                 eng_->range_flag());
 }
 
 double Trainer::update(long long k, bool parallel, bool apply) {
@@ -686,6 +693,7 @@ double Trainer::update(long long k, bool parallel, bool apply) {
   embed_backward(lam0_);
   if (apply) optimizer_step();
   MGLP_CUDA(cudaStreamSynchronize(s_));
+  eng_->check_range();
   return loss;
 }
 
@@ -712,6 +720,7 @@ double Trainer::evaluate() {
     head_forward_loss(zfin, false);
     acc += (double)correct_predictions() / (double)T_;
   }
+  eng_->check_range();
   return acc / vb;
 }
 

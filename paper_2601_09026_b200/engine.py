@@ -253,6 +253,12 @@ def serial_adjoint(stack: LayerStack, traj: List[State], lam_n: State,
     return [State.from_flat(t, b, sx, sy, stack.cfg.d) for t in lam]
 
 
+@dataclass(frozen=True)
+class WarmSnapshot:
+    """Handle of the engine's (single) warm-state snapshot slot."""
+    id: int
+
+
 class LayerParallelEngine:
     """adjoint.hpp:99-219 on the device: buffers serial, the interior window
     through MGRIT forward + adjoint MGRIT, then the parameter-gradient pass."""
@@ -319,12 +325,19 @@ class LayerParallelEngine:
                                PhaseTrace(list(tr[:n.value]), bool(conv.value)))
 
     # ---- WarmSnapshot (adjoint.hpp:187-206); one snapshot slot per engine ----
-    def snapshot(self):
-        N.call("mglp_engine_snapshot", self._eng.h)
-        return self
+    def snapshot(self) -> "WarmSnapshot":
+        sid = C.c_longlong()
+        N.call("mglp_engine_snapshot_id", self._eng.h, C.byref(sid))
+        return WarmSnapshot(sid.value)
 
-    def restore(self, _snap=None):
-        N.call("mglp_engine_restore", self._eng.h)
+    def restore(self, snap: Optional["WarmSnapshot"] = None):
+        """restore(snap) raises ValidationError if `snap` is no longer the
+        engine's snapshot slot (a later snapshot or a shape change replaced
+        it); restore() without an argument restores the slot."""
+        if snap is None:
+            N.call("mglp_engine_restore", self._eng.h)
+        else:
+            N.call("mglp_engine_restore_id", self._eng.h, snap.id)
 
     def reset(self):
         N.call("mglp_engine_reset", self._eng.h)

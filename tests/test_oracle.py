@@ -147,7 +147,10 @@ def test_controller_matches_reference():
 
 
 def _golden_files():
-    return sorted(glob.glob(os.path.join(GOLDEN, "*.npz")))
+    # deep_*.npz / bench_*.npz are outputs OF the numpy oracle (make_deep.py);
+    # the oracle is pinned at their layer shapes by test_oracle_full_width_layers
+    return sorted(p for p in glob.glob(os.path.join(GOLDEN, "*.npz"))
+                  if not os.path.basename(p).startswith(("deep_", "bench_")))
 
 
 @pytest.mark.parametrize("path", _golden_files())
@@ -175,3 +178,35 @@ def test_oracle_reproduces_golden(path):
     assert rel(btr, g["bwd_trace"]) < 1e-12
     assert rel(l0.flat(), g["lam0"]) < 1e-12
     assert rel(O.Stack.flatten(gr), g["grads"]) < 1e-12
+
+
+@pytest.mark.skipif(not R.available(), reason="reference oracle not built")
+@pytest.mark.parametrize("shape", [("encoder", 768, 12, 3072, 20, 0),
+                                   ("decoder_only", 768, 12, 3072, 24, 0),
+                                   ("encoder_decoder", 512, 8, 2048, 12, 10)])
+def test_oracle_full_width_layers(shape):
+    """Pins the numpy restatement at the deep fixtures' layer widths (d=768 /
+    512, 12 / 8 heads, ffn=4d; encoder, causal, cross-attention) against the
+    compiled reference: LayerStack::step and ::adjoint_step with gradients
+    (blocks.cpp:509-574) on a short sequence (the scalar reference costs
+    ~1 s per full-length layer)."""
+    kind, d, H, ffn, sx, sy = shape
+    n_enc, n_dec = {"encoder": (2, 0), "decoder_only": (0, 2), "encoder_decoder": (1, 1)}[kind]
+    rs = R.RefStack(R.RefStackConfig(kind=kind, d=d, heads=H, ffn=ffn, n_enc=n_enc,
+                                     n_dec=n_dec), 7)
+    st = O.Stack(O.StackConfig(kind=kind, d=d, heads=H, ffn=ffn, n_enc=n_enc, n_dec=n_dec),
+                 rs.get_params())
+    n = sx * d + sy * d
+    z = R.gaussian_fill(7, 6, 7, n, 0.5)
+    lam = R.gaussian_fill(8, 6, 8, n, 1.0)
+    for layer in range(st.total):
+        want = rs.step(layer, 0.5, z, 1, sx, sy)
+        got = st.step(layer, 0.5, O.State.from_flat(z, 1, sx, sy, d)).flat()
+        assert rel(got, want) < 1e-12
+        rg = np.zeros(rs.num_params())
+        want = rs.adjoint_step(layer, 0.5, z, lam, 1, sx, sy, grads=rg, gscale=0.25)
+        og = st.zero_grads()
+        got = st.adjoint_step(layer, 0.5, O.State.from_flat(z, 1, sx, sy, d),
+                              O.State.from_flat(lam, 1, sx, sy, d), og, 0.25).flat()
+        assert rel(got, want) < 1e-12
+        assert rel(O.Stack.flatten(og), rg) < 1e-12

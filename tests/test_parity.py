@@ -169,6 +169,7 @@ def test_fixed_point_is_bitwise():
         zf = z0.flat()
         T0 = np.empty((st.total_layers() + 1, zf.size))
         N.call("mglp_serial_forward", eng.handle, b, sx, sy, N.dptr(zf), N.dptr(T0))
+        N.call("mglp_engine_seed_forward_from_traj", eng.handle)
         fo = eng.forward(z0)
         assert fo.phase.trace == [0.0]
         T1 = np.stack([t.flat() for t in fo.traj])
@@ -313,6 +314,7 @@ def test_full_size_fixed_point_and_convergence(kind):
     zf = z0.flat()
     T0 = np.empty((st.total_layers() + 1, zf.size))
     N.call("mglp_serial_forward", eng.handle, B, sx, sy, N.dptr(zf), N.dptr(T0))
+    N.call("mglp_engine_seed_forward_from_traj", eng.handle)
     fo = eng.forward(z0)
     assert fo.phase.trace == [0.0]
     assert np.array_equal(T0, np.stack([t.flat() for t in fo.traj]))

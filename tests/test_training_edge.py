@@ -177,3 +177,28 @@ def test_switching_replay_is_bitwise():
     assert out.switched and out.switch_batch == 3
     assert out.compared_batches == 5
     assert out.losses_match and out.state_matches
+
+
+@gpu
+def test_warm_start_survives_evaluation():
+    """evaluation (a serial sweep) must not become the next batch's
+    warm start. A 16-layer stack with c_f=4 and ONE forward / backward cycle
+    per batch, so the initial guess changes every inexact solve, evaluated
+    after every batch (val_every=1): losses, validation accuracy and final
+    parameters track the reference's run_training, whose evaluation never
+    touches the engine's solver states (training.cpp:280-293)."""
+    stack = StackConfig(kind="encoder", d=32, heads=2, ffn=64, n_enc=16)
+    tk = T.TaskSpec(kind="copy_sequence", vocab=16, seq_len=8, train_size=16, val_size=8, seed=1)
+    mc = T.ModelConfig(stack=stack, vocab=16, max_seq=8)
+    tc = T.TrainConfig(mode="layer_parallel",
+                       solve=SolveConfig(coarsen=4, levels=2, fwd_iters=1, bwd_iters=1),
+                       batch_size=4, epochs=2, seed=7, val_every=1)
+    ref = R.run_training(tk, mc, tc)
+    res = T.run_training(tk, mc, tc)
+    rrows = parse_csv(ref["csv"])
+    assert len(res.rows) == len(rrows) == 8
+    for d, r in zip(res.rows, rrows):
+        assert abs(d.loss - r.loss) <= 1e-4 * abs(r.loss), (d.batch, d.loss, r.loss)
+    dp = np.concatenate([t.ravel() for t in T.parse_checkpoint(res.final_state)["params"]])
+    rp = np.concatenate([t.ravel() for t in T.parse_checkpoint(ref["final_state"])["params"]])
+    assert relerr(dp, rp) < 1e-4
