@@ -115,6 +115,17 @@ mglp_status mglp_engine_backward(mglp_engine* e, int batch, int s_x, int s_y,
                                  double* grads_accum, double* trace_out, int max_trace,
                                  int* n_trace, int* converged);
 
+/* mglp_engine_backward with the parameter gradients kept in the engine's
+ * device slab (zeroed, then this call's gradients; scaled by h as the
+ * reference's) for a device optimizer or a later mglp_engine_get_grads /
+ * _get_grads_layers -- the host sees lambda_0 and the trace only. This is
+ * the boundary a device-resident training step uses (the reference's
+ * Trainer::run_update hands its grads straight to the optimizer, training.cpp:224-239). */
+mglp_status mglp_engine_backward_keep_grads(mglp_engine* e, int batch, int s_x, int s_y,
+                                            const double* traj_in, const double* lam_n,
+                                            double* lam0_out, double* trace_out, int max_trace,
+                                            int* n_trace, int* converged);
+
 /* WarmSnapshot snapshot() / restore() / reset() (adjoint.hpp:187-206).
  * The engine keeps ONE snapshot slot: snapshot_id returns the id of the
  * snapshot just taken, restore_id(id) fails with status 1 if that snapshot
@@ -212,6 +223,11 @@ mglp_status mglp_engine_create_dist(const mglp_stack_desc* stack, const mglp_sol
 /* rank, world and the owned interior layer range [layer_lo, layer_hi) */
 mglp_status mglp_engine_rank_info(mglp_engine* e, int* rank, int* world, int* layer_lo,
                                   int* layer_hi);
+/* The communicator behind a multi-rank engine: *backend 0 = none (one GPU),
+ * 1 = NCCL, 2 = in-process loopback; *nranks = the rank count the backend
+ * itself reports (ncclCommCount), recorded by bench.py next to n_gpus. */
+mglp_status mglp_engine_comm_info(mglp_engine* e, int* backend, int* nranks);
+
 /* Test support: P virtual ranks as P engines on ONE device exchanging through
  * device buffers (same partitioned control flow as NCCL). run_fwd_bwd runs
  * forward_device + backward_device on all P engines concurrently (one host

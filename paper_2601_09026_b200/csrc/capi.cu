@@ -22,6 +22,10 @@ struct mglp_engine {
   float* dl = nullptr;
   float* dl0 = nullptr;
   long long cap = 0;
+  // pinned host staging of one state (fp32): the f64 <-> fp32 conversion runs
+  // multithreaded into it and the copies are DMA from pinned memory
+  float* pin = nullptr;
+  long long pin_cap = 0;
   int B = 0, sx = 0, sy = 0;
 };
 
@@ -72,12 +76,50 @@ Shape ensure_shape(mglp_engine* e, int batch, int s_x, int s_y, int d) {
   return Shape{(long long)batch * (s_x + s_y) * d, nd};
 }
 
+// f(i) for i in [0, n) on up to 8 host threads (chunks of >= 256K elements)
+template <class F>
+void host_parallel(long long n, F&& f) {
+  const long long chunk = 1LL << 18;
+  const int nt = (int)std::min<long long>(8, std::max<long long>(1, n / chunk));
+  if (nt <= 1) {
+    for (long long i = 0; i < n; ++i) f(i);
+    return;
+  }
+  std::vector<std::thread> th;
+  for (int t = 0; t < nt; ++t)
+    th.emplace_back([&, t] {
+      const long long a = n * t / nt, b = n * (t + 1) / nt;
+      for (long long i = a; i < b; ++i) f(i);
+    });
+  for (auto& x : th) x.join();
+}
+
+float* pinned(mglp_engine* e, long long n) {
+  if (n > e->pin_cap) {
+    if (e->pin) cudaFreeHost(e->pin);
+    e->pin = nullptr;
+    MGLP_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&e->pin), n * sizeof(float),
+                            cudaHostAllocDefault));
+    e->pin_cap = n;
+  }
+  return e->pin;
+}
+
 void upload(mglp_engine* e, float* dst, const double* src, const Shape& sh) {
-  std::vector<float> h(sh.n_dev, 0.f);
-  for (long long i = 0; i < sh.n_logical; ++i) h[i] = (float)src[i];
-  MGLP_CUDA(cudaMemcpyAsync(dst, h.data(), sh.n_dev * sizeof(float), cudaMemcpyHostToDevice,
+  float* h = pinned(e, sh.n_dev);
+  host_parallel(sh.n_dev, [&](long long i) { h[i] = i < sh.n_logical ? (float)src[i] : 0.f; });
+  MGLP_CUDA(cudaMemcpyAsync(dst, h, sh.n_dev * sizeof(float), cudaMemcpyHostToDevice,
                             e->eng->stream()));
   MGLP_CUDA(cudaStreamSynchronize(e->eng->stream()));
+}
+
+// one state (device fp32) -> host f64 through the pinned staging buffer
+void download_state(mglp_engine* e, double* dst, const float* src, const Shape& sh) {
+  float* h = pinned(e, sh.n_dev);
+  MGLP_CUDA(cudaMemcpyAsync(h, src, sh.n_dev * sizeof(float), cudaMemcpyDeviceToHost,
+                            e->eng->stream()));
+  MGLP_CUDA(cudaStreamSynchronize(e->eng->stream()));
+  host_parallel(sh.n_logical, [&](long long i) { dst[i] = h[i]; });
 }
 
 void download(mglp_engine* e, double* dst, const float* src, const Shape& sh, long long count) {
@@ -231,6 +273,15 @@ mglp_status mglp_engine_rank_info(mglp_engine* e, int* rank, int* world, int* lo
   });
 }
 
+mglp_status mglp_engine_comm_info(mglp_engine* e, int* backend, int* nranks) {
+  return guard([&] {
+    need(e, "engine");
+    Transport* t = e->eng->transport();
+    if (backend) *backend = t ? t->backend() : 0;
+    if (nranks) *nranks = t ? t->backend_nranks() : 1;
+  });
+}
+
 mglp_status mglp_loopback_create(const mglp_stack_desc* stack, const mglp_solve_config* solve,
                                  int device, int world, mglp_engine** engines) {
   return guard([&] {
@@ -281,6 +332,7 @@ mglp_status mglp_engine_destroy(mglp_engine* e) {
     cudaSetDevice(e->eng->device());
     for (float* p : {e->dz, e->dl, e->dl0})
       if (p) cudaFree(p);
+    if (e->pin) cudaFreeHost(e->pin);
     delete e;
   });
 }
@@ -432,8 +484,27 @@ mglp_status mglp_engine_backward(mglp_engine* e, int batch, int s_x, int s_y,
     upload(e, e->dl, lam_n, sh);
     if (grads_accum) e->eng->zero_grads();
     e->eng->backward_device(e->dl, e->dl0, grads_accum != nullptr, traj_in == nullptr);
-    if (lam0_out) download(e, lam0_out, e->dl0, sh, 1);
+    if (lam0_out) download_state(e, lam0_out, e->dl0, sh);
     if (grads_accum) e->eng->get_grads(grads_accum);
+    put_trace(e, false, trace_out, max_trace, n_trace, converged);
+  });
+}
+
+mglp_status mglp_engine_backward_keep_grads(mglp_engine* e, int batch, int s_x, int s_y,
+                                            const double* traj_in, const double* lam_n,
+                                            double* lam0_out, double* trace_out, int max_trace,
+                                            int* n_trace, int* converged) {
+  return guard([&] {
+    need(e, "engine");
+    need(lam_n, "lam_n");
+    if (!traj_in && (batch != e->B || s_x != e->sx || s_y != e->sy))
+      throw ValidationError("backward: no device trajectory for this shape; pass traj_in");
+    const Shape sh = ensure_shape(e, batch, s_x, s_y, e->eng->width());
+    if (traj_in) upload_traj(e, traj_in, sh);
+    upload(e, e->dl, lam_n, sh);
+    e->eng->zero_grads();
+    e->eng->backward_device(e->dl, e->dl0, true, traj_in == nullptr);
+    if (lam0_out) download_state(e, lam0_out, e->dl0, sh);
     put_trace(e, false, trace_out, max_trace, n_trace, converged);
   });
 }
@@ -512,8 +583,13 @@ mglp_status mglp_serial_adjoint(mglp_engine* e, int batch, int s_x, int s_y,
     if (grads_accum) e->eng->zero_grads();
     e->eng->serial_adjoint_device(e->dl, e->dl0, grads_accum != nullptr);
     e->eng->check_range();
-    if (lam_all_out)
+    if (lam_all_out) {
+      // lam_all_ holds the adjoint at 2^k lambda_N: undo the exact factor
       download(e, lam_all_out, e->eng->lam_all_dev(), sh, e->eng->total_layers() + 1);
+      const double down = e->eng->lam_unscale();
+      const long long n = sh.n_logical * (e->eng->total_layers() + 1);
+      for (long long i = 0; i < n; ++i) lam_all_out[i] *= down;
+    }
     if (grads_accum) e->eng->get_grads(grads_accum);
     MGLP_CUDA(cudaStreamSynchronize(e->eng->stream()));
   });

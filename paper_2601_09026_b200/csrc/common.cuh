@@ -269,6 +269,9 @@ struct EpiArgs {
   Mat out1, out2, add1, add2, aux;
   Mat bias;  // bias vector family (slot = layer); null => no bias
   float gscale = 1.f;
+  // EPI_GRAD_ACC, optional: the effective scale is gscale * *gscale_mul (the
+  // adjoint's exact 2^-k, LamScale::down, read on the device)
+  const float* gscale_mul = nullptr;
   float alpha = 1.f;  // EPI_STORE: out1 = alpha*acc (+ bias)
   Combine cmb;  // EPI_FINAL
   // EPI_BIAS_GELU: gelu(h) also (or only) as a pre-split hi|lo' buffer for
@@ -400,8 +403,9 @@ __device__ __forceinline__ double epilogue_rowv(const EpiArgs& e, int g, int b, 
     case EPI_GRAD_ACC: {
       float* p = e.out1.at(g) + (long long)row * e.out1.ld + col0;
       ld4(p, t1);
+      const float gs = e.gscale_mul ? e.gscale * *e.gscale_mul : e.gscale;
 #pragma unroll
-      for (int i = 0; i < W; ++i) o[i] = t1[i] + e.gscale * acc[i];
+      for (int i = 0; i < W; ++i) o[i] = t1[i] + gs * acc[i];
       st4(p, o);
     } break;
     default:
@@ -498,7 +502,7 @@ __device__ __forceinline__ double epilogue_4x4(const EpiArgs& e, int g, int b, i
 #pragma unroll
       for (int i = 0; i < 4; ++i)
         if (rows[i] >= 0) x1[i] = ld4g(rowp(e.out1, g, rows[i], col));
-      const float gs = e.gscale;
+      const float gs = e.gscale_mul ? e.gscale * *e.gscale_mul : e.gscale;
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         if (rows[i] < 0) continue;
@@ -615,7 +619,8 @@ __device__ __forceinline__ double epilogue_row(const EpiArgs& e, int g, int b, i
     } break;
     case EPI_GRAD_ACC: {
       float* o = e.out1.at(g) + (long long)row * e.out1.ld + col0;
-      for (int i = 0; i < n; ++i) o[i] = o[i] + e.gscale * acc[i];
+      const float gs = e.gscale_mul ? e.gscale * *e.gscale_mul : e.gscale;
+      for (int i = 0; i < n; ++i) o[i] = o[i] + gs * acc[i];
     } break;
   }
   return r2;

@@ -128,6 +128,9 @@ Engine::Engine(const StackDesc& sd, const SolveCfg& cfg, int device,
   const size_t hbytes = (size_t)total_ * hl_stride_ * sizeof(float);
   MGLP_CUDA(cudaMalloc(&Whl_, hbytes));
   MGLP_CUDA(cudaMalloc(&range_flag_, sizeof(int)));
+  MGLP_CUDA(cudaMalloc(&lam_sc_, sizeof(LamScale)));
+  MGLP_CUDA(cudaMemsetAsync(lam_sc_, 0, sizeof(LamScale), stream_));
+  if (world_ > 1) MGLP_CUDA(cudaMalloc(&lam_gather_, 2 * world_ * sizeof(double)));
   MGLP_CUDA(cudaMemsetAsync(P_, 0, pbytes, stream_));
   MGLP_CUDA(cudaMemsetAsync(Whl_, 0, hbytes, stream_));
   MGLP_CUDA(cudaMemsetAsync(range_flag_, 0, sizeof(int), stream_));
@@ -142,6 +145,9 @@ Engine::~Engine() {
   free_solver(fwd_);
   free_solver(bwd_);
   if (range_flag_) cudaFree(range_flag_);
+  if (lam_sc_) cudaFree(lam_sc_);
+  if (snap_sc_) cudaFree(snap_sc_);
+  if (lam_gather_) cudaFree(lam_gather_);
   for (float* p : {P_, Whl_, Gr_, scratch_, hlscr_, cache_, bscratch_, bcache_, traj_, lam_all_,
                    zero_state_, snap_fwd_, snap_bwd_, fwd_stash_})
     if (p) cudaFree(p);
@@ -1622,6 +1628,7 @@ void Engine::encoder_adjoint(const EvalSpec& e, bool causal) {
       w_.ep.kind = EPI_GRAD_ACC;
       w_.ep.out1 = grad(w, ldw, l0, ls);
       w_.ep.gscale = gs;
+      w_.ep.gscale_mul = e.gscale_mul;
       gemm(w_);
     };
     auto cr = [&](Mat up, int cols, long long b, Mat x, Mat st, long long gn, bool uhl = false) {
@@ -1636,6 +1643,7 @@ void Engine::encoder_adjoint(const EvalSpec& e, bool causal) {
       c.dbias = grad(b, 0, l0, ls);
       if (x.ok()) c.dgain = grad(gn, 0, l0, ls);
       c.gscale = gs;
+      c.gscale_mul = e.gscale_mul;
       c.partials = colred_part_;
       c.partials_cap = colred_cap_;
       ++launches_;
@@ -1853,6 +1861,7 @@ void Engine::decoder_adjoint(const EvalSpec& e) {
       w_.ep.kind = EPI_GRAD_ACC;
       w_.ep.out1 = grad(w, ldw, l0, ls);
       w_.ep.gscale = gs;
+      w_.ep.gscale_mul = e.gscale_mul;
       gemm(w_);
     };
     auto cr = [&](int rows, Mat up, int cols, long long b, Mat x, Mat st, long long gn,
@@ -1868,6 +1877,7 @@ void Engine::decoder_adjoint(const EvalSpec& e) {
       c.dbias = grad(b, 0, l0, ls);
       if (x.ok()) c.dgain = grad(gn, 0, l0, ls);
       c.gscale = gs;
+      c.gscale_mul = e.gscale_mul;
       c.partials = colred_part_;
       c.partials_cap = colred_cap_;
       ++launches_;
@@ -2038,7 +2048,7 @@ void Engine::residual_c_rows(Solver& s, int level, bool capture) {
     }
     launch_trace_record(s.ctrl, summed, s.n_chunks, s.slots_per_chunk,
                         world_ > 1 ? s.n_chunks / world_ : s.n_chunks, s.adjoint && world_ > 1,
-                        stream_);
+                        stream_, s.adjoint ? lam_sc_ : nullptr);
     ++launches_;
   } else {
     c.mode = CM_RESL;
@@ -2224,8 +2234,34 @@ void Engine::backward_device(const float* lamN_dev, float* lam0_dev, bool want_g
   if (!traj_is_current) std::fill(cache_valid_.begin(), cache_valid_.end(), 0);
   ensure_linearization();
   const Mat LAM = state_mat(lam_all_, state_n_, sd_.d, 0, 1);
-  MGLP_CUDA(cudaMemcpyAsync(lam_all_ + (size_t)total_ * state_n_, lamN_dev,
-                            state_n_ * sizeof(float), cudaMemcpyDeviceToDevice, stream_));
+  const int guess = (first_bwd_ || !cfg_.warm_start) ? cfg_.cold_guess : 2;
+  first_bwd_ = false;
+  // lambda_N -> 2^k lambda_N (LamScale): the last rank's lambda_N (and, for a
+  // warm guess, every rank's stored adjoint states in their true scale)
+  // decides k; every rank uses the same factor
+  if (rank_ == world_ - 1) launch_lam_amax(lamN_dev, state_n_, lam_sc_, stream_);
+  else MGLP_CUDA(cudaMemsetAsync(&lam_sc_->amax_bits, 0, sizeof(unsigned), stream_));
+  if (guess == 2) {
+    // this rank's owned adjoint points (the ghost is another rank's)
+    const int a = bwd_.p_lo[0] + 1, b = bwd_.p_hi[0];
+    launch_lam_amax_warm(bwd_.lv[0].v + (size_t)a * state_n_, (long long)(b - a + 1) * state_n_,
+                         lam_sc_, stream_);
+    ++launches_;
+    if (world_ > 1) {
+      // max over ranks: all-gather the per-rank maxima (as doubles), then max
+      double* mx = lam_gather_;
+      launch_lam_bits_to_f64(lam_sc_, mx + world_, stream_);
+      tr_->allgather(mx + world_, mx, 1, stream_);
+      launch_lam_bits_max(mx, world_, lam_sc_, stream_);
+      launches_ += 2;
+    }
+  } else if (world_ > 1) {
+    tr_->bcast(reinterpret_cast<float*>(lam_sc_), 1, world_ - 1, stream_);
+  }
+  launch_lam_scale(lamN_dev, lam_all_ + (size_t)total_ * state_n_, state_n_, lam_sc_, +1,
+                   stream_);
+  launches_ += 2;
+  const float* gmul = &lam_sc_->down;
   auto serial_adj = [&](int l) {
     EvalSpec e;
     e.G = 1;
@@ -2238,6 +2274,7 @@ void Engine::backward_device(const float* lamN_dev, float* lam0_dev, bool want_g
     e.cmb.out = shift(LAM, l);
     e.want_grads = want_grads;
     e.gscale = (float)h_[l];
+    e.gscale_mul = gmul;
     eval_adjoint(e);
   };
   // closing buffers on the last rank, then mu[0] = lambda at the interior end
@@ -2246,12 +2283,17 @@ void Engine::backward_device(const float* lamN_dev, float* lam0_dev, bool want_g
   MGLP_CUDA(cudaMemcpyAsync(bwd_.lv[0].v, lam_all_ + (size_t)ie_ * state_n_,
                             state_n_ * sizeof(float), cudaMemcpyDeviceToDevice, stream_));
   if (world_ > 1) tr_->bcast(bwd_.lv[0].v, (size_t)state_n_, world_ - 1, stream_);
-  const int guess = (first_bwd_ || !cfg_.warm_start) ? cfg_.cold_guess : 2;
-  first_bwd_ = false;
   if (guess == 0)
     launch_copy(N_, state_n_, lv_v(bwd_, 0, 1, 1), lv_v(bwd_, 0, 0, 0), nullptr, stream_);
   else if (guess == 1)
     launch_zero(N_, state_n_, lv_v(bwd_, 0, 1, 1), nullptr, stream_);
+  else {
+    // warm states were stored at the previous solve's 2^k
+    launch_lam_rescale(N_, state_n_, lv_v(bwd_, 0, 1, 1), lam_sc_, stream_);
+    ++launches_;
+  }
+  launch_lam_commit(lam_sc_, stream_);
+  ++launches_;
   solve(bwd_, cfg_.bwd_iters, cfg_.bwd_tol);
   // parameter pass over the owned layers (adjoint.hpp:165-175): layer ib+i at
   // traj[ib+i] with upstream mu[N-1-i], gscale = h. The final level-0
@@ -2275,6 +2317,7 @@ void Engine::backward_device(const float* lamN_dev, float* lam0_dev, bool want_g
       e.want_grads = true;
       e.wgrad_only = cached;
       e.gscale = (float)h_[ib_];
+      e.gscale_mul = gmul;
       eval_adjoint(e);
     };
     auto cached = [&](int i) { return cfg_.levels == 1 || ((N_ - 1 - i) % cf) != cf - 1; };
@@ -2300,9 +2343,10 @@ void Engine::backward_device(const float* lamN_dev, float* lam0_dev, bool want_g
                               bwd_.lv[0].v + (size_t)N_ * state_n_, state_n_ * sizeof(float),
                               cudaMemcpyDeviceToDevice, stream_));
     for (int l = ib_ - 1; l >= 0; --l) serial_adj(l);
-    if (lam0_dev)
-      MGLP_CUDA(cudaMemcpyAsync(lam0_dev, lam_all_, state_n_ * sizeof(float),
-                                cudaMemcpyDeviceToDevice, stream_));
+    if (lam0_dev) {
+      launch_lam_scale(lam_all_, lam0_dev, state_n_, lam_sc_, -1, stream_);
+      ++launches_;
+    }
   }
 }
 
@@ -2363,6 +2407,9 @@ long long Engine::snapshot() {  // adjoint.hpp:187-194
   const float* fv = fwd_displaced_ ? fwd_stash_ : fwd_.lv[0].v;
   MGLP_CUDA(cudaMemcpyAsync(snap_fwd_, fv, bytes, cudaMemcpyDeviceToDevice, stream_));
   MGLP_CUDA(cudaMemcpyAsync(snap_bwd_, bwd_.lv[0].v, bytes, cudaMemcpyDeviceToDevice, stream_));
+  // ... and the 2^k those adjoint states are stored at
+  if (!snap_sc_) MGLP_CUDA(cudaMalloc(&snap_sc_, sizeof(LamScale)));
+  MGLP_CUDA(cudaMemcpyAsync(snap_sc_, lam_sc_, sizeof(LamScale), cudaMemcpyDeviceToDevice, stream_));
   snap_first_fwd_ = first_fwd_;
   snap_first_bwd_ = first_bwd_;
   snap_id_ = ++snap_seq_;
@@ -2382,8 +2429,17 @@ void Engine::restore(long long id) {  // adjoint.hpp:196-201
   MGLP_CUDA(cudaMemcpyAsync(fwd_stash_, snap_fwd_, bytes, cudaMemcpyDeviceToDevice, stream_));
   fwd_displaced_ = true;
   MGLP_CUDA(cudaMemcpyAsync(bwd_.lv[0].v, snap_bwd_, bytes, cudaMemcpyDeviceToDevice, stream_));
+  MGLP_CUDA(cudaMemcpyAsync(&lam_sc_->k_state, &snap_sc_->k_state, sizeof(int),
+                            cudaMemcpyDeviceToDevice, stream_));
   first_fwd_ = snap_first_fwd_;
   first_bwd_ = snap_first_bwd_;
+}
+
+double Engine::lam_unscale() const {
+  LamScale h;
+  MGLP_CUDA(cudaMemcpyAsync(&h, lam_sc_, sizeof(LamScale), cudaMemcpyDeviceToHost, stream_));
+  MGLP_CUDA(cudaStreamSynchronize(stream_));
+  return h.down_d;
 }
 
 void Engine::displace_forward_window() {
@@ -2436,8 +2492,10 @@ void Engine::serial_adjoint_device(const float* lamN_dev, float* lam0_dev, bool 
   MGLP_CUDA(cudaSetDevice(device_));
   ensure_linearization();
   const Mat LAM = state_mat(lam_all_, state_n_, sd_.d, 0, 1);
-  MGLP_CUDA(cudaMemcpyAsync(lam_all_ + (size_t)total_ * state_n_, lamN_dev,
-                            state_n_ * sizeof(float), cudaMemcpyDeviceToDevice, stream_));
+  launch_lam_amax(lamN_dev, state_n_, lam_sc_, stream_);
+  launch_lam_scale(lamN_dev, lam_all_ + (size_t)total_ * state_n_, state_n_, lam_sc_, +1,
+                   stream_);
+  launches_ += 2;
   for (int l = total_ - 1; l >= 0; --l) {
     EvalSpec e;
     e.G = 1;
@@ -2450,11 +2508,13 @@ void Engine::serial_adjoint_device(const float* lamN_dev, float* lam0_dev, bool 
     e.cmb.out = shift(LAM, l);
     e.want_grads = want_grads;
     e.gscale = (float)h_[l];
+    e.gscale_mul = &lam_sc_->down;
     eval_adjoint(e);
   }
-  if (lam0_dev)
-    MGLP_CUDA(cudaMemcpyAsync(lam0_dev, lam_all_, state_n_ * sizeof(float),
-                              cudaMemcpyDeviceToDevice, stream_));
+  if (lam0_dev) {
+    launch_lam_scale(lam_all_, lam0_dev, state_n_, lam_sc_, -1, stream_);
+    ++launches_;
+  }
 }
 
 // ---- single-step hooks ----

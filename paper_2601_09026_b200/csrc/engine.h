@@ -48,6 +48,10 @@ class Transport {
   virtual void bcast(float* buf, size_t n, int root, cudaStream_t s) = 0;
   virtual void group_start() {}
   virtual void group_end() {}
+  // 1 NCCL, 2 loopback; and the rank count the backend itself reports
+  // (ncclCommCount for NCCL) -- bench.py records it next to n_gpus
+  virtual int backend() const = 0;
+  virtual int backend_nranks() const { return size(); }
 };
 
 // out[i] = scale * gaussian(seed, a, b, i), multithreaded, bit-identical to rng.hpp
@@ -61,6 +65,7 @@ class Engine {
   Engine(const StackDesc& sd, const SolveCfg& cfg, int device, std::shared_ptr<Transport> tr);
   int rank() const { return rank_; }
   int world() const { return world_; }
+  Transport* transport() const { return tr_.get(); }
   // owned interior layer range [lo, hi) (interior indices)
   void owned_layers(int* lo, int* hi) const {
     *lo = fwd_.p_lo.empty() ? 0 : fwd_.p_lo[0];
@@ -168,7 +173,11 @@ class Engine {
 
   // device-resident trajectory, slot i = time point i (total+1 slots)
   float* traj_dev() const { return traj_; }
+  // lambda at every time point of the last serial adjoint, SCALED by 2^k
+  // (lam_scale_dev()->up); lam_unscale() returns 2^-k (synchronises)
   float* lam_all_dev() const { return lam_all_; }
+  const LamScale* lam_scale_dev() const { return lam_sc_; }
+  double lam_unscale() const;
   cudaStream_t stream() const { return stream_; }
   int device() const { return device_; }
   // number of hot-path kernel launches issued since the last reset_launch_count()
@@ -252,6 +261,7 @@ class Engine {
     bool wgrad_only = false;  // intermediates already in bact: only form dW, db
     bool keep_act = false;    // scratch activations are read by a following adjoint
     bool residual_only = false;  // out = F(z) (the combine starts from a zero state)
+    const float* gscale_mul = nullptr;  // device factor of gscale (LamScale::down)
   };
   void eval_forward(const EvalSpec& e);
   void eval_adjoint(const EvalSpec& e);
@@ -366,6 +376,9 @@ class Engine {
   float* Whl_ = nullptr;   // pre-split weights (LayerLayout::wpack), hl_stride_ floats per layer
   long long hl_stride_ = 0;
   int* range_flag_ = nullptr;  // device: a GEMM operand overflowed fp16 (gemm_tc.cu)
+  LamScale* lam_sc_ = nullptr;  // device: the adjoint's exact 2^k scaling of lambda_N
+  LamScale* snap_sc_ = nullptr;
+  double* lam_gather_ = nullptr;  // [2 * world] per-rank maxima (multi-rank warm scaling)  // the scaling stored with the snapshot's adjoint states
   float* Gr_ = nullptr;    // fp32 grads
   // shape
   int B_ = 0, sx_ = 0, sy_ = 0, Tx_ = 0, Ty_ = 0;

@@ -41,6 +41,7 @@ struct ColRedArgs {
   Mat up, x, stats;
   Mat dgain, dbias;  // slot = layer
   float gscale = 1.f;
+  const float* gscale_mul = nullptr;  // optional device factor (EpiArgs::gscale_mul)
   // optional f64 scratch (>= G * kColRedChunks * cols * 2 doubles): enables the
   // two-stage row-chunked form (fixed-order partials, then an ordered sum)
   double* partials = nullptr;
@@ -96,10 +97,47 @@ struct SolveCtrl {
   double trace[kMaxTrace];
 };
 void launch_ctrl_begin(SolveCtrl* c, cudaStream_t s);
+
+// Exact power-of-two scaling of the adjoint. The adjoint
+// (Phi^T, the parameter pass, the residual norms) is linear in lambda, so the
+// engine runs it on 2^k lambda_N with max|2^k lambda_N| in [1, 2) and undoes
+// the factor exactly where values leave the solve: lambda_0, the gradient
+// accumulation (gscale * 2^-k), the residual trace (norm * 2^-k). With every
+// value a normal number the result is bitwise that of the unscaled adjoint;
+// lambda_N of O(1e-5..1e-8) (a mean-token cross entropy over many tokens)
+// no longer lands in the fp16 split's subnormal range, and |lambda| >= 65520
+// no longer overflows it. A zero or non-finite lambda_N keeps k = 0.
+struct LamScale {
+  unsigned int amax_bits;  // max |lambda_N| as float bits (non-negative: uint order = float order)
+  float up;                // 2^k
+  float down;              // 2^-k
+  int k;
+  double down_d;           // 2^-k
+  int k_state;             // k of the adjoint solver's stored states (its warm start)
+  int pad;
+};
+// s->amax_bits = 0; then max |x| over n floats (deterministic atomicMax)
+void launch_lam_amax(const float* x, long long n, LamScale* sc, cudaStream_t s);
+// warm start: also fold in max |x| * 2^-k_state over n floats (the stored
+// adjoint states in their true scale), so the rescaled warm guess cannot
+// overflow when lambda_N drops by binades between solves
+void launch_lam_amax_warm(const float* x, long long n, LamScale* sc, cudaStream_t s);
+// multi-rank max of amax_bits: out[0] = (double)amax_bits (exact), gathered
+// over ranks by the caller, then amax_bits = max_r in[r]
+void launch_lam_bits_to_f64(const LamScale* sc, double* out, cudaStream_t s);
+void launch_lam_bits_max(const double* in, int n, LamScale* sc, cudaStream_t s);
+// dst = src * 2^(+k) (dir > 0; also publishes up/down/k) or * 2^-k (dir < 0)
+void launch_lam_scale(const float* src, float* dst, long long n, LamScale* sc, int dir,
+                      cudaStream_t s);
+// warm-start states stored at k_state, this solve runs at k: dst *= 2^(k - k_state)
+// (no-op when equal)
+void launch_lam_rescale(int G, long long n, Mat dst, const LamScale* sc, cudaStream_t s);
+// k_state := k (the adjoint solver's states now hold this solve's scaling)
+void launch_lam_commit(LamScale* sc, cudaStream_t s);
 // trace entry = sqrt(sum of the per-interval partials [n_chunks][S]), measured
 // mid-cycle (mgrit.hpp:235-238)
 void launch_trace_record(SolveCtrl* c, const double* partials, int n_chunks, int S, int per_rank,
-                         bool reversed, cudaStream_t s);
+                         bool reversed, cudaStream_t s, const LamScale* sc = nullptr);
 // end of one V-cycle: push the trace, stop on non-finite / converged (mgrit.hpp:252-259)
 void launch_cycle_end(SolveCtrl* c, double tol, cudaStream_t s);
 

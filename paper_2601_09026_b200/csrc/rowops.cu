@@ -445,11 +445,11 @@ __global__ void __launch_bounds__(256) colred_sum_kernel(ColRedArgs a, const int
   }
   if (a.dbias.ok()) {
     float* db = a.dbias.at(g);
-    db[col] = db[col] + a.gscale * (float)tb;
+    db[col] = db[col] + (a.gscale_mul ? a.gscale * *a.gscale_mul : a.gscale) * (float)tb;
   }
   if (a.x.ok() && a.dgain.ok()) {
     float* dg = a.dgain.at(g);
-    dg[col] = dg[col] + a.gscale * (float)tg;
+    dg[col] = dg[col] + (a.gscale_mul ? a.gscale * *a.gscale_mul : a.gscale) * (float)tg;
   }
 }
 
@@ -594,11 +594,11 @@ __global__ void __launch_bounds__(256) colred_kernel(ColRedArgs a, const int* ac
     }
     if (a.dbias.ok()) {
       float* db = a.dbias.at(g);
-      db[col] = db[col] + a.gscale * (float)tb;
+      db[col] = db[col] + (a.gscale_mul ? a.gscale * *a.gscale_mul : a.gscale) * (float)tb;
     }
     if (a.x.ok() && a.dgain.ok()) {
       float* dg = a.dgain.at(g);
-      dg[col] = dg[col] + a.gscale * (float)tg;
+      dg[col] = dg[col] + (a.gscale_mul ? a.gscale * *a.gscale_mul : a.gscale) * (float)tg;
     }
   }
 }
@@ -690,7 +690,7 @@ __global__ void ctrl_begin_kernel(SolveCtrl* c) {
 // `reversed`, rank r's block of `per_rank` intervals holds intervals of time
 // position P-1-r (the adjoint solve's partition).
 __global__ void trace_record_kernel(SolveCtrl* c, const double* partials, int n_chunks, int S,
-                                    int per_rank, int reversed) {
+                                    int per_rank, int reversed, const LamScale* sc) {
   pdl_wait();
   pdl_trigger();
   __shared__ double red[32];
@@ -706,7 +706,86 @@ __global__ void trace_record_kernel(SolveCtrl* c, const double* partials, int n_
     if (threadIdx.x == 0) total += t;
     __syncthreads();
   }
-  if (threadIdx.x == 0) c->pending = sqrt(total);
+  // the adjoint's norms are of 2^k-scaled rows: * 2^-k is exact
+  if (threadIdx.x == 0) c->pending = sc ? sqrt(total) * sc->down_d : sqrt(total);
+}
+
+__global__ void lam_amax_kernel(const float* x, long long n, LamScale* sc, int warm) {
+  pdl_wait();
+  pdl_trigger();
+  unsigned int m = 0;
+  // warm: the stored states are at 2^k_state; * 2^-k_state is exact (the
+  // states are normal floats, k_state in [-100, 100])
+  const float f = warm ? ldexpf(1.f, -sc->k_state) : 1.f;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    m = max(m, __float_as_uint(x[i] * f) & 0x7fffffffu);  // NaN bits sort above inf
+#pragma unroll
+  for (int o = 16; o; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0 && m) atomicMax(&sc->amax_bits, m);
+}
+
+// k with max|x| * 2^k in [1, 2): k = -(unbiased exponent of max); kept in
+// [-100, 100] so 2^k and 2^-k are normal floats; 0 for 0 / inf / NaN
+__device__ __forceinline__ int lam_k(unsigned int bits) {
+  if (bits == 0u || bits >= 0x7f800000u) return 0;
+  const int e = (int)(bits >> 23) - 127;  // subnormal max: e = -127 (k clamps anyway)
+  return max(-100, min(100, -e));
+}
+
+__global__ void lam_rescale_kernel(long long n4, Mat dst, const LamScale* sc) {
+  pdl_wait();
+  pdl_trigger();
+  const int dk = sc->k - sc->k_state;
+  if (dk == 0) return;
+  const float f = ldexpf(1.f, dk);
+  float4* d = reinterpret_cast<float4*>(dst.at(blockIdx.y));
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n4;
+       i += (long long)gridDim.x * blockDim.x) {
+    const float4 v = d[i];
+    d[i] = make_float4(v.x * f, v.y * f, v.z * f, v.w * f);
+  }
+}
+
+__global__ void lam_bits_to_f64_kernel(const LamScale* sc, double* out) {
+  pdl_wait();
+  pdl_trigger();
+  out[0] = (double)sc->amax_bits;
+}
+
+__global__ void lam_bits_max_kernel(const double* in, int n, LamScale* sc) {
+  pdl_wait();
+  pdl_trigger();
+  unsigned int m = 0;
+  for (int r = 0; r < n; ++r) m = max(m, (unsigned int)in[r]);
+  sc->amax_bits = m;
+}
+
+__global__ void lam_commit_kernel(LamScale* sc) {
+  pdl_wait();
+  pdl_trigger();
+  sc->k_state = sc->k;
+}
+
+__global__ void lam_scale_kernel(const float* src, float* dst, long long n4, LamScale* sc,
+                                 int dir) {
+  pdl_wait();
+  pdl_trigger();
+  const int k = lam_k(sc->amax_bits);
+  const float f = ldexpf(1.f, dir > 0 ? k : -k);
+  if (dir > 0 && blockIdx.x == 0 && threadIdx.x == 0) {
+    sc->k = k;
+    sc->up = ldexpf(1.f, k);
+    sc->down = ldexpf(1.f, -k);
+    sc->down_d = ldexp(1.0, -k);
+  }
+  const float4* s4 = reinterpret_cast<const float4*>(src);
+  float4* d4 = reinterpret_cast<float4*>(dst);
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n4;
+       i += (long long)gridDim.x * blockDim.x) {
+    const float4 v = s4[i];
+    d4[i] = make_float4(v.x * f, v.y * f, v.z * f, v.w * f);
+  }
 }
 
 __global__ void cycle_end_kernel(SolveCtrl* c, double tol) {
@@ -833,8 +912,48 @@ void launch_zero(int G, long long n, Mat dst, const int* active, cudaStream_t s)
 void launch_ctrl_begin(SolveCtrl* c, cudaStream_t s) { launch_k(ctrl_begin_kernel, dim3(1), dim3(1), 0, s, 1, c); }
 
 void launch_trace_record(SolveCtrl* c, const double* partials, int n_chunks, int S, int per_rank,
-                         bool reversed, cudaStream_t s) {
-  launch_k(trace_record_kernel, dim3(1), dim3(256), 0, s, 1, c, partials, n_chunks, S, per_rank, reversed ? 1 : 0);
+                         bool reversed, cudaStream_t s, const LamScale* sc) {
+  launch_k(trace_record_kernel, dim3(1), dim3(256), 0, s, 1, c, partials, n_chunks, S, per_rank,
+           reversed ? 1 : 0, sc);
+}
+
+void launch_lam_rescale(int G, long long n, Mat dst, const LamScale* sc, cudaStream_t s) {
+  if (G == 0 || n == 0) return;
+  require_vec4(n, "lam_rescale");
+  dim3 grid(stream_grid(n / 4, G), G);
+  launch_k(lam_rescale_kernel, grid, dim3(256), 0, s, 1, n / 4, dst, sc);
+}
+
+void launch_lam_bits_to_f64(const LamScale* sc, double* out, cudaStream_t s) {
+  launch_k(lam_bits_to_f64_kernel, dim3(1), dim3(1), 0, s, 1, sc, out);
+}
+
+void launch_lam_bits_max(const double* in, int n, LamScale* sc, cudaStream_t s) {
+  launch_k(lam_bits_max_kernel, dim3(1), dim3(1), 0, s, 1, in, n, sc);
+}
+
+void launch_lam_commit(LamScale* sc, cudaStream_t s) {
+  launch_k(lam_commit_kernel, dim3(1), dim3(1), 0, s, 1, sc);
+}
+
+void launch_lam_amax(const float* x, long long n, LamScale* sc, cudaStream_t s) {
+  MGLP_CUDA(cudaMemsetAsync(&sc->amax_bits, 0, sizeof(unsigned int), s));
+  if (n == 0) return;
+  const int grid = (int)std::max<long long>(1, std::min<long long>(592, (n + 255) / 256));
+  launch_k(lam_amax_kernel, dim3(grid), dim3(256), 0, s, 1, x, n, sc, 0);
+}
+
+void launch_lam_amax_warm(const float* x, long long n, LamScale* sc, cudaStream_t s) {
+  if (n == 0) return;
+  const int grid = (int)std::max<long long>(1, std::min<long long>(1184, (n + 255) / 256));
+  launch_k(lam_amax_kernel, dim3(grid), dim3(256), 0, s, 1, x, n, sc, 1);
+}
+
+void launch_lam_scale(const float* src, float* dst, long long n, LamScale* sc, int dir,
+                      cudaStream_t s) {
+  require_vec4(n, "lam_scale");
+  const int grid = std::max(1, stream_grid(n / 4, 1));
+  launch_k(lam_scale_kernel, dim3(grid), dim3(256), 0, s, 1, src, dst, n / 4, sc, dir);
 }
 
 void launch_cycle_end(SolveCtrl* c, double tol, cudaStream_t s) {

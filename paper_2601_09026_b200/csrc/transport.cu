@@ -40,6 +40,7 @@ struct NcclApi {
   ncclResult_t (*GroupStart)() = nullptr;
   ncclResult_t (*GroupEnd)() = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
+  ncclResult_t (*CommCount)(ncclComm_t, int*) = nullptr;
 };
 
 NcclApi& nccl() {
@@ -63,6 +64,7 @@ NcclApi& nccl() {
     api.GroupStart = (decltype(api.GroupStart))sym("ncclGroupStart");
     api.GroupEnd = (decltype(api.GroupEnd))sym("ncclGroupEnd");
     api.GetErrorString = (decltype(api.GetErrorString))sym("ncclGetErrorString");
+    api.CommCount = (decltype(api.CommCount))sym("ncclCommCount");
   });
   if (!api.h || !api.CommInitRank || !api.Send || !api.Recv || !api.AllGather)
     throw ContractViolation("NCCL (libnccl.so.2) could not be loaded for a multi-GPU engine");
@@ -102,6 +104,12 @@ class NcclTransport final : public Transport {
   }
   void group_start() override { nccl_check(nccl().GroupStart(), "GroupStart"); }
   void group_end() override { nccl_check(nccl().GroupEnd(), "GroupEnd"); }
+  int backend() const override { return 1; }
+  int backend_nranks() const override {
+    int n = -1;
+    if (nccl().CommCount) nccl_check(nccl().CommCount(comm_, &n), "CommCount");
+    return n;
+  }
 
  private:
   int rank_, world_;
@@ -162,6 +170,7 @@ class LoopbackTransport final : public Transport {
   LoopbackTransport(std::shared_ptr<LoopbackHub> hub, int rank) : hub_(std::move(hub)), rank_(rank) {}
   int rank() const override { return rank_; }
   int size() const override { return hub_->world(); }
+  int backend() const override { return 2; }
   void send(const float* buf, size_t n, int peer, cudaStream_t s) override {
     hub_->post(rank_, peer, buf, n * sizeof(float), s);
   }

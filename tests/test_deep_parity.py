@@ -21,8 +21,10 @@ Checked, each at the north-star tolerance 1e-4 (relative):
     (relative to the tensor's max |g|) and the Frobenius norm of the WHOLE
     error estimated by 8 Rademacher sketches (tests/_deep.py).
 Tensors whose exact gradient vanishes (the attention key bias: softmax is
-shift invariant) hold rounding noise on both sides; they are measured
-against 1e-3 of the layer's largest gradient norm instead of their own.
+shift invariant; the f64 reference holds ~1e-15 against O(10) gradients
+elsewhere in the layer) hold rounding noise on both sides; they are measured
+against their layer's largest gradient, every other tensor against its own
+(floored at 1e-3 of the layer's largest).
 Set MGLP_PARITY_REPORT=<path> to write the per-config errors as JSON.
 """
 import ctypes as C
@@ -111,16 +113,32 @@ def grad_errors(c, dev_flat, ref):
             o += k
         return np.concatenate(out)
 
-    den = np.maximum(ref["g_norm"], 1e-3 * per_layer_max(ref["g_norm"]))
+    # tensors whose exact gradient vanishes identically (the attention key
+    # bias, softmax shift invariance: the f64 reference holds ~1e-15 noise of
+    # a layer whose gradients are O(10-100)) carry only rounding noise on both
+    # sides; they are measured against their layer's scale, all others against
+    # their own (floored at 1e-3 of the layer's largest)
+    def floor_of(v):
+        lm = per_layer_max(v)
+        return np.where(v < 1e-9 * lm, lm, np.maximum(v, 1e-3 * lm))
+
+    den = floor_of(ref["g_norm"])
     sketch = np.sqrt(np.mean((d["g_sketch"] - ref["g_sketch"]) ** 2, axis=1)) / den
     norm = np.abs(d["g_norm"] - ref["g_norm"]) / den
     # sampled entries relative to each tensor's max |g| (same floor)
     sizes = [min(sz, D.N_GRAD_IDX) for l in range(total)
              for _, sz in D.components(c["kind"], c["n_enc"], c["d"], c["ffn"], l)]
-    gden = np.maximum(ref["g_max"], 1e-3 * per_layer_max(ref["g_max"]))
+    gden = floor_of(ref["g_max"])
     samp = np.abs(d["g_samp"] - ref["g_samp"]) / np.repeat(gden, sizes)
+    names = [f"layer {l} {nm}" for l in range(total)
+             for nm, _ in D.components(c["kind"], c["n_enc"], c["d"], c["ffn"], l)]
+    owner = np.repeat(np.arange(len(names)), sizes)
+    ws = int(owner[int(np.argmax(samp))])
     return dict(grad_sketch_frobenius=float(sketch.max()), grad_norms=float(norm.max()),
-                grad_samples=float(samp.max()), grad_tensors=int(sketch.size))
+                grad_samples=float(samp.max()), grad_tensors=int(sketch.size),
+                worst_sketch=names[int(np.argmax(sketch))], worst_norm=names[int(np.argmax(norm))],
+                worst_sample=f"{names[ws]} (|g|max {ref['g_max'][ws]:.3e}, floor "
+                             f"{gden[ws]:.3e}, norm {ref['g_norm'][ws]:.3e})")
 
 
 def _report(name, errs):

@@ -13,9 +13,9 @@ from paper_2601_09026_b200 import _native as N  # noqa: E402
 pytestmark = pytest.mark.gpu
 
 
-def run(G, M, N_, K, a_mn, b_mn, presplit, engine, bias=False, seed=0):
+def run(G, M, N_, K, a_mn, b_mn, presplit, engine, bias=False, seed=0, a_scale=1.0):
     g = torch.Generator(device="cpu").manual_seed(seed)
-    A = torch.randn(G, *( (K, M) if a_mn else (M, K) ), generator=g).float().cuda()
+    A = (torch.randn(G, *( (K, M) if a_mn else (M, K) ), generator=g) * a_scale).float().cuda()
     B = (torch.randn(G, *( (K, N_) if b_mn else (N_, K) ), generator=g) * 0.05).float().cuda()
     bv = torch.randn(N_, generator=g).float().cuda() if bias else None
     Cm = torch.full((G, M, N_), float("nan"), device="cuda")

@@ -54,8 +54,23 @@ def test_weight_beyond_fp16_raises():
         eng.forward(state(0, 0.5))
 
 
-def test_upstream_beyond_fp16_raises():
+def test_large_upstream_is_rescaled_not_overflowed():
+    """lambda_N of 1e6 used to overflow the upstream pack; the adjoint now runs
+    on 2^k lambda_N (LamScale) and returns the exact linear multiple"""
     st, eng = make()
     fo = eng.forward(state(0, 0.5))
+    g1, g2 = st.zero_grads(), st.zero_grads()
+    b1 = eng.backward(fo.traj, state(1, 1.0), g1)
+    b2 = eng.backward(fo.traj, state(1, 2.0 ** 20), g2)
+    assert np.array_equal(np.asarray(b2.lambda0.flat()), np.asarray(b1.lambda0.flat()) * 2.0 ** 20)
+    assert np.array_equal(np.asarray(g2), np.asarray(g1) * 2.0 ** 20)
+
+
+def test_upstream_growth_beyond_fp16_raises():
+    """the scaling normalises lambda_N only: an adjoint that itself grows past
+    the fp16 range inside the stack still raises (MLP-out weight 5e4: the
+    dgrad of the MLP branch multiplies the upstream by ~|W| * sqrt(d))"""
+    st, eng = make("mlp.out.w", 5e4)
     with pytest.raises(ContractViolation):
-        eng.backward(fo.traj, state(1, 1e6), st.zero_grads())  # the upstream pack
+        fo = eng.forward(state(0, 0.5))
+        eng.backward(fo.traj, state(1, 1.0), st.zero_grads())

@@ -202,3 +202,30 @@ def test_warm_start_survives_evaluation():
     dp = np.concatenate([t.ravel() for t in T.parse_checkpoint(res.final_state)["params"]])
     rp = np.concatenate([t.ravel() for t in T.parse_checkpoint(ref["final_state"])["params"]])
     assert relerr(dp, rp) < 1e-4
+
+
+@gpu
+def test_one_update_at_4096_tokens(mode="layer_parallel"):
+    """a batch of 32 x 128 = 4096 tokens, so the mean-token
+    cross entropy puts lambda_N at O(1e-5) (model.cpp:213-248) -- the regime
+    the fp16 split would lose to subnormals without the adjoint's 2^k scaling
+    (the parameter gradients sum 4096 such rows, so they are O(0.1) again).
+    Loss and every gradient (Adam's first moment) against run_training."""
+    stack = StackConfig(kind="encoder", d=32, heads=2, ffn=64, n_enc=8)
+    tk = T.TaskSpec(kind="copy_sequence", vocab=16, seq_len=128, train_size=32, val_size=32,
+                    seed=1)
+    mc = T.ModelConfig(stack=stack, vocab=16, max_seq=128)
+    tc = T.TrainConfig(mode=mode, solve=SolveConfig(coarsen=2, levels=2, fwd_iters=2, bwd_iters=1),
+                       batch_size=32, epochs=1, seed=7, val_every=2)
+    ref = R.run_training(tk, mc, tc)
+    rrows = parse_csv(ref["csv"])
+    res = T.run_training(tk, mc, tc)
+    assert len(res.rows) == 1
+    assert abs(res.rows[0].loss - rrows[0].loss) <= 1e-5 * abs(rrows[0].loss)
+    rck = T.parse_checkpoint(ref["final_state"])
+    dck = T.parse_checkpoint(res.final_state)
+    gmax = max(np.abs(rm).max() for rm in rck["m"])
+    for i, (dm, rm) in enumerate(zip(dck["m"], rck["m"])):
+        den = max(np.abs(rm).max(), 1e-3 * gmax)
+        err = float(np.abs(dm - rm).max() / den)
+        assert err < 1e-4, (i, err)
