@@ -237,16 +237,37 @@ mglp_status mglp_loopback_create(const mglp_stack_desc* stack, const mglp_solve_
 mglp_status mglp_loopback_run_fwd_bwd(mglp_engine** engines, int world, const float* z0_dev,
                                       const float* lam_n_dev, float* lam0_dev, int want_grads);
 
-/* ---- controller (controller.hpp:63-155) ----
- * Pure decision rule, evaluated on the device from the device-resident
- * residual traces of the last forward and backward solves:
- * f = last_pair_factor(trace) for each phase, decision = decide(...)
- * (0 keep, 1 increase iterations, 2 switch to serial). On "increase", the
- * engine's fwd/bwd iteration budgets are doubled (capped), as
- * InexactnessMonitor::record does (controller.hpp:126-147). */
-mglp_status mglp_monitor_record(mglp_engine* e, double threshold, int policy_switch,
-                                int max_iter_cap, double* fwd_factor, double* bwd_factor,
-                                int* decision);
+/* ---- gradient-bias monitor on the device (controller.hpp:32-166) ----
+ * attach: InexactnessMonitor(IndicatorConfig{threshold, policy, cap}); the
+ * engine's fwd/bwd iteration budgets (SolveConfig::fwd_iters / bwd_iters)
+ * move into device memory and every solve runs the DEVICE budget (the host
+ * issues an upper bound of cycles; surplus cycles are no-ops on the device).
+ * probe(1/0): ProbeScope begin / end -- both budgets doubled for one batch
+ * (controller.hpp:88-105), on the device.
+ * mglp_monitor_record: InexactnessMonitor::record(batch, ...)
+ * as ONE kernel on the engine stream: f = last_pair_factor of the forward /
+ * adjoint traces the last solves left in device memory, decision = decide(f)
+ * (0 keep, 1 increase iterations, 2 switch to serial), budgets doubled
+ * (capped) on increase, the switch flag set on switch, the report logged.
+ * No allocation, no host round trip; with decision == NULL it is fully
+ * asynchronous (and graph-capturable); otherwise it synchronises to return
+ * the decision. mglp_engine_monitor_read synchronises and returns the
+ * device state (last report, budgets now, budgets the last solves used);
+ * _reports copies the report log (oldest first, up to 1024 kept).
+ * mglp_engine_capture_cycles(n): a CUDA graph captured next issues n cycles
+ * per solve, gated by the device budget, so a monitor decision changes the
+ * replayed budget without recapture; a budget above n makes the trace read
+ * fail (status 2) instead of silently truncating. */
+mglp_status mglp_engine_monitor_attach(mglp_engine* e, double threshold, int policy_switch,
+                                      int max_iter_cap);
+mglp_status mglp_engine_monitor_probe(mglp_engine* e, int begin);
+mglp_status mglp_monitor_record(mglp_engine* e, long long batch, int* decision);
+mglp_status mglp_engine_monitor_read(mglp_engine* e, int* switched, int* decision,
+                                    double* fwd_factor, double* bwd_factor, int* fwd_iters,
+                                    int* bwd_iters, int* used_fwd, int* used_bwd);
+mglp_status mglp_engine_monitor_reports(mglp_engine* e, long long* batch, double* fwd_factor,
+                                       double* bwd_factor, int* decision, int cap, int* n);
+mglp_status mglp_engine_capture_cycles(mglp_engine* e, int cycles);
 
 /* Host helper: out[i] = scale * rng::gaussian(seed, a, b, i) (rng.hpp:70-79),
  * bit-identical to the reference (same libm); the reference bench's z0 draw
@@ -353,6 +374,24 @@ mglp_status mglp_trainer_destroy(mglp_trainer* t);
 /* run_update(k, parallel, apply) (training.cpp:230-268): loss of batch k */
 mglp_status mglp_trainer_update(mglp_trainer* t, long long k, int parallel, int apply,
                                 double* loss);
+/* probe_batch(k) (training.cpp:244-276) with the engine's device monitor
+ * (mglp_trainer_monitor_attach first): ProbeScope on the device budgets, the
+ * update (use_probe_gradient: the doubled run IS the update; else a
+ * measurement-only run behind a warm-state snapshot, then the nominal update
+ * at the decided budget), record() on the device. Outputs: the row's loss,
+ * budgets and factors, the decision and the switch flag. */
+mglp_status mglp_trainer_monitor_attach(mglp_trainer* t, double threshold, int policy_switch,
+                                       int max_iter_cap);
+mglp_status mglp_trainer_update_probe(mglp_trainer* t, long long k, int use_probe_gradient,
+                                      double* loss, int* fwd_iters, int* bwd_iters,
+                                      double* fwd_factor, double* bwd_factor, int* decision,
+                                      int* switched);
+/* last_pair_factor of the last parallel update's traces and the budgets it
+ * ran with, evaluated on the device (monitor attached) */
+mglp_status mglp_trainer_last_factors(mglp_trainer* t, double* fwd_factor, double* bwd_factor,
+                                      int* fwd_iters, int* bwd_iters);
+mglp_status mglp_trainer_monitor_reports(mglp_trainer* t, long long* batch, double* fwd_factor,
+                                        double* bwd_factor, int* decision, int cap, int* n);
 /* evaluate() (training.cpp:296-310): validation token accuracy */
 mglp_status mglp_trainer_evaluate(mglp_trainer* t, double* accuracy);
 mglp_status mglp_trainer_num_params(mglp_trainer* t, long long* n);

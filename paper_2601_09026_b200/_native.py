@@ -99,7 +99,16 @@ _SIGS = {
     "mglp_engine_traj_device": [_vp, C.POINTER(_vp)],
     "mglp_engine_sync": [_vp],
     "mglp_engine_take_launch_count": [_vp, _llp],
-    "mglp_monitor_record": [_vp, C.c_double, C.c_int, C.c_int, _dp, _dp, _ip],
+    "mglp_monitor_record": [_vp, C.c_longlong, _ip],
+    "mglp_engine_monitor_attach": [_vp, C.c_double, C.c_int, C.c_int],
+    "mglp_engine_monitor_probe": [_vp, C.c_int],
+    "mglp_engine_monitor_read": [_vp, _ip, _ip, _dp, _dp, _ip, _ip, _ip, _ip],
+    "mglp_engine_monitor_reports": [_vp, _llp, _dp, _dp, _ip, C.c_int, _ip],
+    "mglp_engine_capture_cycles": [_vp, C.c_int],
+    "mglp_trainer_monitor_attach": [_vp, C.c_double, C.c_int, C.c_int],
+    "mglp_trainer_update_probe": [_vp, C.c_longlong, C.c_int, _dp, _ip, _ip, _dp, _dp, _ip, _ip],
+    "mglp_trainer_last_factors": [_vp, _dp, _dp, _ip, _ip],
+    "mglp_trainer_monitor_reports": [_vp, _llp, _dp, _dp, _ip, C.c_int, _ip],
     "mglp_engine_profile": [_vp, C.c_int],
     "mglp_rng_gaussian_fill": [C.c_ulonglong, C.c_ulonglong, C.c_ulonglong, C.c_double, _dp,
                                C.c_longlong],

@@ -115,25 +115,48 @@ class InexactnessMonitor:
 
 
 class DeviceMonitor(InexactnessMonitor):
-    """InexactnessMonitor whose factors and decision come from the device:
-    last_pair_factor is evaluated on the traces resident in GPU memory
-    after engine.forward/backward, and the engine's budgets are updated in
-    place by the library (mglp_monitor_record)."""
+    """InexactnessMonitor whose state lives on the GPU (mglp_*_monitor_*):
+    the budgets the solves run with, the switch flag and the report log are
+    device memory; record() is one kernel evaluating last_pair_factor on the
+    device-resident traces, decide() and the budget update. The host keeps a
+    mirror of `switched` (refreshed by every probe) for due(); reports()
+    copies the device log."""
 
-    def record_engine(self, batch, engine) -> IndicatorReport:
-        ff, bf, dec = C.c_double(), C.c_double(), C.c_int()
-        N.call("mglp_monitor_record", engine.handle, self.cfg.threshold,
-               int(self.cfg.policy == POLICY_SWITCH), self.cfg.max_iter_cap, C.byref(ff),
-               C.byref(bf), C.byref(dec))
-        rep = IndicatorReport(batch, ff.value, bf.value, dec.value)
-        cfg = engine.config()
-        if rep.decision == INCREASE_ITERATIONS:
-            cfg.fwd_iters = min(2 * cfg.fwd_iters, self.cfg.max_iter_cap)
-            cfg.bwd_iters = min(2 * cfg.bwd_iters, self.cfg.max_iter_cap)
-        elif rep.decision == SWITCH_SERIAL:
-            self._switched = True
-        self.reports.append(rep)
-        return rep
+    def __init__(self, cfg: IndicatorConfig, handle, trainer: bool):
+        super().__init__(cfg)
+        self._h = handle
+        self._trainer = trainer
+        pre = "mglp_trainer" if trainer else "mglp_engine"
+        N.call(pre + "_monitor_attach", handle, cfg.threshold,
+               int(cfg.policy == POLICY_SWITCH), cfg.max_iter_cap)
+
+    def record_engine(self, batch) -> IndicatorReport:
+        """engine users: record() after engine.forward/backward"""
+        dec, sw = C.c_int(), C.c_int()
+        ff, bf = C.c_double(), C.c_double()
+        N.call("mglp_monitor_record", self._h, batch, None)
+        N.call("mglp_engine_monitor_read", self._h, C.byref(sw), C.byref(dec), C.byref(ff),
+               C.byref(bf), None, None, None, None)
+        self._switched = bool(sw.value)
+        return IndicatorReport(batch, ff.value, bf.value, dec.value)
+
+    def note(self, switched: bool):
+        self._switched = bool(switched)
+
+    @property
+    def reports(self) -> List[IndicatorReport]:
+        cap = 1024
+        b = (C.c_longlong * cap)()
+        ff, bf = (C.c_double * cap)(), (C.c_double * cap)()
+        dec = (C.c_int * cap)()
+        n = C.c_int()
+        pre = "mglp_trainer" if self._trainer else "mglp_engine"
+        N.call(pre + "_monitor_reports", self._h, b, ff, bf, dec, cap, C.byref(n))
+        return [IndicatorReport(b[i], ff[i], bf[i], dec[i]) for i in range(min(n.value, cap))]
+
+    @reports.setter
+    def reports(self, v):  # InexactnessMonitor.__init__ assigns []
+        pass
 
 
 def indicator_csv(reports) -> str:

@@ -153,16 +153,6 @@ void put_trace(mglp_engine* e, bool fwd, double* out, int max_trace, int* n, int
   if (conv) *conv = c ? 1 : 0;
 }
 
-__global__ void monitor_kernel(const SolveCtrl* f, const SolveCtrl* b, double* out) {
-  // last_pair_factor (controller.hpp:63-67) on both device traces
-  auto factor = [](const SolveCtrl* c) {
-    const int n = min(c->n_trace, kMaxTrace);
-    if (n < 2 || c->trace[n - 2] == 0.0) return 0.0;
-    return c->trace[n - 1] / c->trace[n - 2];
-  };
-  out[0] = factor(f);
-  out[1] = factor(b);
-}
 
 }  // namespace
 
@@ -443,12 +433,16 @@ mglp_status mglp_engine_set_config(mglp_engine* e, const mglp_solve_config* cfg)
       throw ValidationError("set_config: the hierarchy (coarsen, levels) is fixed at creation");
     // the iteration budgets, tolerances and guess policy are baked into a
     // captured step: a change drops it (replay then refuses until recapture)
-    if (cfg->fwd_iters != c.fwd_iters || cfg->bwd_iters != c.bwd_iters ||
-        cfg->fwd_tol != c.fwd_tol || cfg->bwd_tol != c.bwd_tol ||
-        cfg->cold_guess != c.cold_guess || cfg->warm_start != c.warm_start)
+    // With a device monitor attached the budgets live on the device and gate
+    // the captured cycles: a budget change alone keeps the graph.
+    if (cfg->fwd_iters < 1 || cfg->bwd_iters < 1)
+      throw ValidationError("set_config: iteration budgets must be >= 1");
+    const bool iters = cfg->fwd_iters != c.fwd_iters || cfg->bwd_iters != c.bwd_iters;
+    if ((iters && !e->eng->monitor_on()) || cfg->fwd_tol != c.fwd_tol ||
+        cfg->bwd_tol != c.bwd_tol || cfg->cold_guess != c.cold_guess ||
+        cfg->warm_start != c.warm_start)
       e->eng->drop_graph();
-    c.fwd_iters = cfg->fwd_iters;
-    c.bwd_iters = cfg->bwd_iters;
+    if (iters) e->eng->set_budget(cfg->fwd_iters, cfg->bwd_iters);
     c.fwd_tol = cfg->fwd_tol;
     c.bwd_tol = cfg->bwd_tol;
     c.cold_guess = cfg->cold_guess;
@@ -808,36 +802,61 @@ mglp_status mglp_engine_profile_dump(mglp_engine* e, double* rows, int max_rows,
   });
 }
 
-mglp_status mglp_monitor_record(mglp_engine* e, double threshold, int policy_switch,
-                                int max_iter_cap, double* fwd_factor, double* bwd_factor,
-                                int* decision) {
+mglp_status mglp_engine_monitor_attach(mglp_engine* e, double threshold, int policy_switch,
+                                      int max_iter_cap) {
   return guard([&] {
     need(e, "engine");
-    if (threshold <= 0.0) throw ValidationError("decide: threshold must be positive");
-    double* d_out = nullptr;
-    MGLP_CUDA(cudaMalloc(&d_out, 2 * sizeof(double)));
-    monitor_kernel<<<1, 1, 0, e->eng->stream()>>>(e->eng->ctrl(true), e->eng->ctrl(false), d_out);
-    double h[2];
-    MGLP_CUDA(cudaMemcpyAsync(h, d_out, sizeof h, cudaMemcpyDeviceToHost, e->eng->stream()));
-    MGLP_CUDA(cudaStreamSynchronize(e->eng->stream()));
-    cudaFree(d_out);
-    // decide (controller.hpp:71-84) + InexactnessMonitor::record's budget update (126-147)
-    const double worst = std::max(h[0], h[1]);
-    SolveCfg& c = e->eng->config();
-    int dec = 0;
-    if (worst > threshold) {
-      if (policy_switch)
-        dec = 2;
-      else
-        dec = (c.fwd_iters < max_iter_cap || c.bwd_iters < max_iter_cap) ? 1 : 2;
-    }
-    if (dec == 1) {
-      c.fwd_iters = std::min(2 * c.fwd_iters, max_iter_cap);
-      c.bwd_iters = std::min(2 * c.bwd_iters, max_iter_cap);
-    }
-    if (fwd_factor) *fwd_factor = h[0];
-    if (bwd_factor) *bwd_factor = h[1];
-    if (decision) *decision = dec;
+    e->eng->monitor_attach(threshold, policy_switch, max_iter_cap);
+  });
+}
+
+mglp_status mglp_engine_monitor_probe(mglp_engine* e, int begin) {
+  return guard([&] {
+    need(e, "engine");
+    e->eng->monitor_probe(begin != 0);
+  });
+}
+
+mglp_status mglp_monitor_record(mglp_engine* e, long long batch, int* decision) {
+  return guard([&] {
+    need(e, "engine");
+    e->eng->monitor_record(batch);
+    if (decision) *decision = e->eng->monitor_read().last_decision;
+  });
+}
+
+mglp_status mglp_engine_monitor_read(mglp_engine* e, int* switched, int* decision,
+                                    double* fwd_factor, double* bwd_factor, int* fwd_iters,
+                                    int* bwd_iters, int* used_fwd, int* used_bwd) {
+  return guard([&] {
+    need(e, "engine");
+    const MonitorSummary& m = e->eng->monitor_read();
+    if (switched) *switched = m.switched;
+    if (decision) *decision = m.last_decision;
+    if (fwd_factor) *fwd_factor = m.last_ff;
+    if (bwd_factor) *bwd_factor = m.last_bf;
+    if (fwd_iters) *fwd_iters = m.budget[0];
+    if (bwd_iters) *bwd_iters = m.budget[1];
+    if (used_fwd) *used_fwd = m.used[0];
+    if (used_bwd) *used_bwd = m.used[1];
+  });
+}
+
+mglp_status mglp_engine_monitor_reports(mglp_engine* e, long long* batch, double* fwd_factor,
+                                       double* bwd_factor, int* decision, int cap, int* n) {
+  return guard([&] {
+    need(e, "engine");
+    const int k = e->eng->monitor_reports(batch, fwd_factor, bwd_factor, decision, cap);
+    if (n) *n = k;
+  });
+}
+
+mglp_status mglp_engine_capture_cycles(mglp_engine* e, int cycles) {
+  return guard([&] {
+    need(e, "engine");
+    if (cycles < 0) throw ValidationError("capture cycles must be >= 0");
+    e->eng->set_capture_cycles(cycles);
+    e->eng->drop_graph();
   });
 }
 
@@ -1219,6 +1238,46 @@ mglp_status mglp_trainer_update(mglp_trainer* t, long long k, int parallel, int 
   });
 }
 
+mglp_status mglp_trainer_monitor_attach(mglp_trainer* t, double threshold, int policy_switch,
+                                       int max_iter_cap) {
+  return guard([&] { tr(t).engine().monitor_attach(threshold, policy_switch, max_iter_cap); });
+}
+
+mglp_status mglp_trainer_update_probe(mglp_trainer* t, long long k, int use_probe_gradient,
+                                      double* loss, int* fwd_iters, int* bwd_iters,
+                                      double* fwd_factor, double* bwd_factor, int* decision,
+                                      int* switched) {
+  return guard([&] {
+    const ProbeOutcome o = tr(t).update_probe(k, use_probe_gradient != 0);
+    if (loss) *loss = o.loss;
+    if (fwd_iters) *fwd_iters = o.fwd_iters;
+    if (bwd_iters) *bwd_iters = o.bwd_iters;
+    if (fwd_factor) *fwd_factor = o.fwd_factor;
+    if (bwd_factor) *bwd_factor = o.bwd_factor;
+    if (decision) *decision = o.decision;
+    if (switched) *switched = o.switched;
+  });
+}
+
+mglp_status mglp_trainer_last_factors(mglp_trainer* t, double* fwd_factor, double* bwd_factor,
+                                      int* fwd_iters, int* bwd_iters) {
+  return guard([&] {
+    const MonitorSummary& m = tr(t).engine().monitor_read();
+    if (fwd_factor) *fwd_factor = m.trace_ff;
+    if (bwd_factor) *bwd_factor = m.trace_bf;
+    if (fwd_iters) *fwd_iters = m.used[0];
+    if (bwd_iters) *bwd_iters = m.used[1];
+  });
+}
+
+mglp_status mglp_trainer_monitor_reports(mglp_trainer* t, long long* batch, double* fwd_factor,
+                                        double* bwd_factor, int* decision, int cap, int* n) {
+  return guard([&] {
+    const int k = tr(t).engine().monitor_reports(batch, fwd_factor, bwd_factor, decision, cap);
+    if (n) *n = k;
+  });
+}
+
 mglp_status mglp_trainer_evaluate(mglp_trainer* t, double* accuracy) {
   return guard([&] {
     need(accuracy, "accuracy");
@@ -1281,10 +1340,9 @@ mglp_status mglp_trainer_get_iters(mglp_trainer* t, int* fwd_iters, int* bwd_ite
 mglp_status mglp_trainer_set_iters(mglp_trainer* t, int fwd_iters, int bwd_iters) {
   return guard([&] {
     if (fwd_iters < 1 || bwd_iters < 1) throw ValidationError("iterations must be >= 1");
-    SolveCfg& c = tr(t).engine().config();
-    c.fwd_iters = fwd_iters;
-    c.bwd_iters = bwd_iters;
-    tr(t).engine().drop_graph();
+    Engine& en = tr(t).engine();
+    if (!en.monitor_on()) en.drop_graph();
+    en.set_budget(fwd_iters, bwd_iters);
   });
 }
 

@@ -148,6 +148,9 @@ Engine::~Engine() {
   if (lam_sc_) cudaFree(lam_sc_);
   if (snap_sc_) cudaFree(snap_sc_);
   if (lam_gather_) cudaFree(lam_gather_);
+  if (mon_) cudaFree(mon_);
+  if (mon_sum_) cudaFree(mon_sum_);
+  if (mon_host_) cudaFreeHost(mon_host_);
   for (float* p : {P_, Whl_, Gr_, scratch_, hlscr_, cache_, bscratch_, bcache_, traj_, lam_all_,
                    zero_state_, snap_fwd_, snap_bwd_, fwd_stash_})
     if (p) cudaFree(p);
@@ -2134,9 +2137,99 @@ void Engine::v_cycle(Solver& s, double tol, bool first) {  // mgrit.hpp:235-246
   ++launches_;
 }
 
+int Engine::host_cycles(int which) const {
+  if (!mon_) return which == 0 ? cfg_.fwd_iters : cfg_.bwd_iters;
+  return capture_cycles_ > 0 ? capture_cycles_ : bound_[which];
+}
+
+void Engine::monitor_attach(double threshold, int policy_switch, int cap) {
+  if (threshold <= 0.0) throw ValidationError("InexactnessMonitor: threshold must be positive");
+  if (cap < 1) throw ValidationError("InexactnessMonitor: max_iter_cap must be >= 1");
+  MGLP_CUDA(cudaSetDevice(device_));
+  if (!mon_) {
+    MGLP_CUDA(cudaMalloc(&mon_, sizeof(MonitorDev)));
+    MGLP_CUDA(cudaMalloc(&mon_sum_, sizeof(MonitorSummary)));
+    MGLP_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&mon_host_), sizeof(MonitorSummary),
+                            cudaHostAllocDefault));
+  }
+  launch_monitor_init(mon_, threshold, policy_switch, cap, cfg_.fwd_iters, cfg_.bwd_iters, stream_);
+  MGLP_CUDA(cudaMemsetAsync(mon_sum_, 0, sizeof(MonitorSummary), stream_));
+  MGLP_CUDA(cudaMemsetAsync(mon_host_, 0, sizeof(MonitorSummary), stream_));
+  bound_[0] = cfg_.fwd_iters;
+  bound_[1] = cfg_.bwd_iters;
+  mon_cap_ = cap;
+  drop_graph();
+}
+
+void Engine::monitor_probe(bool begin) {
+  if (!mon_) throw ValidationError("monitor: not attached");
+  launch_monitor_probe(mon_, begin ? 1 : 0, stream_);
+  ++launches_;
+  if (begin) {
+    bound_saved_[0] = bound_[0];
+    bound_saved_[1] = bound_[1];
+    bound_[0] *= 2;
+    bound_[1] *= 2;
+  } else {
+    bound_[0] = bound_saved_[0];
+    bound_[1] = bound_saved_[1];
+  }
+}
+
+void Engine::monitor_record(long long batch) {
+  if (!mon_) throw ValidationError("monitor: not attached");
+  if (!fwd_.ctrl || !bwd_.ctrl) throw ValidationError("monitor: record before any solve");
+  launch_monitor_record(mon_, fwd_.ctrl, bwd_.ctrl, batch, mon_sum_, stream_);
+  MGLP_CUDA(cudaMemcpyAsync(mon_host_, mon_sum_, sizeof(MonitorSummary), cudaMemcpyDeviceToHost,
+                            stream_));
+  ++launches_;
+  if (batch >= 0) {  // the decision may double both budgets (capped)
+    bound_[0] = std::max(bound_[0], std::min(2 * bound_[0], mon_cap_));
+    bound_[1] = std::max(bound_[1], std::min(2 * bound_[1], mon_cap_));
+  }
+}
+
+const MonitorSummary& Engine::monitor_read() {
+  if (!mon_) throw ValidationError("monitor: not attached");
+  MGLP_CUDA(cudaStreamSynchronize(stream_));
+  cfg_.fwd_iters = bound_[0] = mon_host_->budget[0];
+  cfg_.bwd_iters = bound_[1] = mon_host_->budget[1];
+  return *mon_host_;
+}
+
+int Engine::monitor_reports(long long* batch, double* ff, double* bf, int* dec, int cap) {
+  if (!mon_) throw ValidationError("monitor: not attached");
+  MonitorDev* h = nullptr;
+  MGLP_CUDA(cudaMallocHost(reinterpret_cast<void**>(&h), sizeof(MonitorDev)));
+  MGLP_CUDA(cudaMemcpyAsync(h, mon_, sizeof(MonitorDev), cudaMemcpyDeviceToHost, stream_));
+  MGLP_CUDA(cudaStreamSynchronize(stream_));
+  const int n = std::min(h->n_reports, kMonReports);
+  const int first = h->n_reports - n;  // oldest kept report
+  int k = 0;
+  for (; k < n && k < cap; ++k) {
+    const int i = (first + k) % kMonReports;
+    if (batch) batch[k] = h->rep_batch[i];
+    if (ff) ff[k] = h->rep_ff[i];
+    if (bf) bf[k] = h->rep_bf[i];
+    if (dec) dec[k] = h->rep_dec[i];
+  }
+  cudaFreeHost(h);
+  return n;
+}
+
+void Engine::set_budget(int fwd_iters, int bwd_iters) {
+  cfg_.fwd_iters = fwd_iters;
+  cfg_.bwd_iters = bwd_iters;
+  if (mon_) {
+    launch_monitor_set_budget(mon_, fwd_iters, bwd_iters, stream_);
+    bound_[0] = fwd_iters;
+    bound_[1] = bwd_iters;
+  }
+}
+
 void Engine::solve(Solver& s, int iters, double tol) {  // mgrit.hpp:248-262
   if (iters < 1) throw ValidationError("solve_forward: need at least one iteration");
-  launch_ctrl_begin(s.ctrl, stream_);
+  launch_ctrl_begin(s.ctrl, iters, mon_ ? &mon_->budget[s.adjoint ? 1 : 0] : nullptr, stream_);
   active_ = &s.ctrl->active;
   for (int it = 0; it < iters; ++it) v_cycle(s, tol, it == 0);
   active_ = nullptr;
@@ -2191,7 +2284,7 @@ void Engine::forward_device(const float* z0_dev) {
   } else if (guess == 1) {
     launch_zero(N_, state_n_, lv_v(fwd_, 0, 1, 1), nullptr, stream_);
   }
-  solve(fwd_, cfg_.fwd_iters, cfg_.fwd_tol);
+  solve(fwd_, host_cycles(0), cfg_.fwd_tol);
   // the level-0 F-relaxations captured the linearization of every layer
   // whose input is final: all but the last layer of each coarse interval
   // (with one level the C-point residual evaluations capture those too)
@@ -2294,7 +2387,7 @@ void Engine::backward_device(const float* lamN_dev, float* lam0_dev, bool want_g
   }
   launch_lam_commit(lam_sc_, stream_);
   ++launches_;
-  solve(bwd_, cfg_.bwd_iters, cfg_.bwd_tol);
+  solve(bwd_, host_cycles(1), cfg_.bwd_tol);
   // parameter pass over the owned layers (adjoint.hpp:165-175): layer ib+i at
   // traj[ib+i] with upstream mu[N-1-i], gscale = h. The final level-0
   // relaxation evaluated exactly these (layer, upstream) pairs for every
@@ -2394,6 +2487,9 @@ void Engine::read_trace(bool fwd, std::vector<double>* trace, bool* converged) {
   MGLP_CUDA(cudaMemcpyAsync(&c, fwd ? fwd_.ctrl : bwd_.ctrl, sizeof(SolveCtrl),
                             cudaMemcpyDeviceToHost, stream_));
   check_range();
+  if (c.truncated)
+    throw ContractViolation("the device iteration budget exceeds the cycles this (captured) solve "
+                            "issues: recapture with more cycles (set_capture_cycles)");
   trace->assign(c.trace, c.trace + std::min(c.n_trace, kMaxTrace));
   *converged = c.converged != 0;
 }

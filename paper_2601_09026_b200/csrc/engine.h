@@ -151,6 +151,25 @@ class Engine {
   void check_range();
   int* range_flag() const { return range_flag_; }
 
+  // ---- gradient-bias monitor on the device (controller.hpp:63-155) ----
+  // attach: the solves' iteration budgets move into device memory
+  // (MonitorDev::budget) and every solve runs the device budget; record()
+  // evaluates last_pair_factor + decide + the budget / switch update as one
+  // kernel from the traces the solves left on the device -- no host round
+  // trip, no allocation, capturable. The host keeps an upper bound of the
+  // device budget to size its cycle loop (exact after monitor_read(), which
+  // synchronises and copies the small summary; surplus cycles are no-ops).
+  void monitor_attach(double threshold, int policy_switch, int cap);
+  bool monitor_on() const { return mon_ != nullptr; }
+  void monitor_probe(bool begin);        // ProbeScope on the device budgets
+  void monitor_record(long long batch);  // batch < 0: refresh the summary only
+  const MonitorSummary& monitor_read();  // synchronises; host budgets := device budgets
+  int monitor_reports(long long* batch, double* ff, double* bf, int* dec, int cap);
+  void set_budget(int fwd_iters, int bwd_iters);  // host-side budget change -> device
+  // graph capture with a monitor: the host issues `n` cycles per solve and
+  // the device budget gates them (0: the host bound)
+  void set_capture_cycles(int n) { capture_cycles_ = n; }
+
   // CUDA graph of one full training-step solve (forward_device +
   // backward_device on fixed device buffers). Every host decision of the
   // step is shape/config-static and the solve's stopping rule lives on the
@@ -378,7 +397,15 @@ class Engine {
   int* range_flag_ = nullptr;  // device: a GEMM operand overflowed fp16 (gemm_tc.cu)
   LamScale* lam_sc_ = nullptr;  // device: the adjoint's exact 2^k scaling of lambda_N
   LamScale* snap_sc_ = nullptr;
-  double* lam_gather_ = nullptr;  // [2 * world] per-rank maxima (multi-rank warm scaling)  // the scaling stored with the snapshot's adjoint states
+  double* lam_gather_ = nullptr;
+  MonitorDev* mon_ = nullptr;
+  MonitorSummary* mon_host_ = nullptr;  // pinned mirror
+  MonitorSummary* mon_sum_ = nullptr;   // device summary
+  int bound_[2] = {0, 0};               // host upper bound of the device budgets
+  int capture_cycles_ = 0;
+  int bound_saved_[2] = {0, 0};
+  int mon_cap_ = 1;
+  int host_cycles(int which) const;  // [2 * world] per-rank maxima (multi-rank warm scaling)  // the scaling stored with the snapshot's adjoint states
   float* Gr_ = nullptr;    // fp32 grads
   // shape
   int B_ = 0, sx_ = 0, sy_ = 0, Tx_ = 0, Ty_ = 0;

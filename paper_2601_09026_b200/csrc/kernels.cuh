@@ -95,8 +95,49 @@ struct SolveCtrl {
   int cycles_run;
   double pending;
   double trace[kMaxTrace];
+  int budget;     // cycles this solve may run (the host loop or the device budget)
+  int truncated;  // the device budget asked for more cycles than the host loop issued
 };
-void launch_ctrl_begin(SolveCtrl* c, cudaStream_t s);
+// budget_dev == nullptr: budget = host_cycles (the host loop count); else the
+// solve's budget is the device-resident *budget_dev (the gradient-bias
+// monitor's, controller.hpp:126-147), capped at host_cycles (truncated = 1
+// if it asked for more)
+void launch_ctrl_begin(SolveCtrl* c, int host_cycles, const int* budget_dev, cudaStream_t s);
+
+// ---- gradient-bias monitor on the device (controller.hpp:63-155) ----------------
+// InexactnessMonitor state, the live iteration budgets the solves read, and
+// the report log, all in device memory: record() runs as one kernel on the
+// engine stream right after a probe's solves (no host round trip, capturable).
+constexpr int kMonReports = 1024;
+struct MonitorDev {
+  double threshold;
+  int policy_switch, cap;
+  int switched, n_reports;
+  int budget[2];  // [fwd, bwd] SolveConfig::fwd_iters / bwd_iters
+  int saved[2];   // ProbeScope
+  int last_decision, pad;
+  double last_ff, last_bf;
+  long long rep_batch[kMonReports];
+  double rep_ff[kMonReports], rep_bf[kMonReports];
+  int rep_dec[kMonReports];
+};
+// what the host mirrors after a step (pinned, copied asynchronously)
+struct MonitorSummary {
+  int switched, n_reports, last_decision, pad;
+  int budget[2];  // budgets now
+  int used[2];    // budgets the last forward / adjoint solve ran with
+  double last_ff, last_bf;  // factors of the last record()
+  double trace_ff, trace_bf;  // last_pair_factor of the last solves' traces
+};
+void launch_monitor_init(MonitorDev* m, double threshold, int policy_switch, int cap, int fwd,
+                         int bwd, cudaStream_t s);
+void launch_monitor_set_budget(MonitorDev* m, int fwd, int bwd, cudaStream_t s);
+// ProbeScope (controller.hpp:88-105): begin doubles both budgets, end restores
+void launch_monitor_probe(MonitorDev* m, int begin, cudaStream_t s);
+// record (controller.hpp:126-147) from the traces in f / b when batch >= 0;
+// always refreshes *out
+void launch_monitor_record(MonitorDev* m, const SolveCtrl* f, const SolveCtrl* b,
+                           long long batch, MonitorSummary* out, cudaStream_t s);
 
 // Exact power-of-two scaling of the adjoint. The adjoint
 // (Phi^T, the parameter pass, the residual norms) is linear in lambda, so the

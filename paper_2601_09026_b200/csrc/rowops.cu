@@ -675,7 +675,7 @@ int stream_grid(long long n4, int G) {
 }
 
 // ---- solve control -------------------------------------------------------------------
-__global__ void ctrl_begin_kernel(SolveCtrl* c) {
+__global__ void ctrl_begin_kernel(SolveCtrl* c, int host_cycles, const int* budget_dev) {
   pdl_wait();
   pdl_trigger();
   c->active = 1;
@@ -683,6 +683,99 @@ __global__ void ctrl_begin_kernel(SolveCtrl* c) {
   c->converged = 0;
   c->cycles_run = 0;
   c->pending = 0.0;
+  const int want = budget_dev ? *budget_dev : host_cycles;
+  c->budget = min(want, host_cycles);
+  c->truncated = want > host_cycles ? 1 : 0;
+  if (c->budget < 1) c->active = 0;
+}
+
+// last_pair_factor (controller.hpp:63-67) of a solve's trace
+__device__ double trace_factor(const SolveCtrl* c) {
+  const int n = min(c->n_trace, kMaxTrace);
+  if (n < 2 || c->trace[n - 2] == 0.0) return 0.0;
+  return c->trace[n - 1] / c->trace[n - 2];
+}
+
+__global__ void monitor_init_kernel(MonitorDev* m, double thr, int policy_switch, int cap, int fwd,
+                                    int bwd) {
+  pdl_wait();
+  pdl_trigger();
+  m->threshold = thr;
+  m->policy_switch = policy_switch;
+  m->cap = cap;
+  m->switched = 0;
+  m->n_reports = 0;
+  m->budget[0] = fwd;
+  m->budget[1] = bwd;
+  m->saved[0] = fwd;
+  m->saved[1] = bwd;
+  m->last_decision = 0;
+  m->last_ff = m->last_bf = 0.0;
+}
+
+__global__ void monitor_set_budget_kernel(MonitorDev* m, int fwd, int bwd) {
+  pdl_wait();
+  pdl_trigger();
+  m->budget[0] = fwd;
+  m->budget[1] = bwd;
+}
+
+__global__ void monitor_probe_kernel(MonitorDev* m, int begin) {
+  pdl_wait();
+  pdl_trigger();
+  if (begin) {
+    m->saved[0] = m->budget[0];
+    m->saved[1] = m->budget[1];
+    m->budget[0] *= 2;
+    m->budget[1] *= 2;
+  } else {
+    m->budget[0] = m->saved[0];
+    m->budget[1] = m->saved[1];
+  }
+}
+
+__global__ void monitor_record_kernel(MonitorDev* m, const SolveCtrl* f, const SolveCtrl* b,
+                                      long long batch, MonitorSummary* out) {
+  pdl_wait();
+  pdl_trigger();
+  const double ff = trace_factor(f), bf = trace_factor(b);
+  if (batch >= 0) {
+    // decide (controller.hpp:71-84) with the budgets as they are now
+    const double worst = ff > bf ? ff : bf;  // std::max(f, b): NaN-free traces
+    int dec = 0;
+    if (worst > m->threshold) {
+      if (m->policy_switch)
+        dec = 2;
+      else
+        dec = (m->budget[0] < m->cap || m->budget[1] < m->cap) ? 1 : 2;
+    }
+    if (dec == 1) {
+      m->budget[0] = min(2 * m->budget[0], m->cap);
+      m->budget[1] = min(2 * m->budget[1], m->cap);
+    } else if (dec == 2) {
+      m->switched = 1;
+    }
+    const int i = m->n_reports % kMonReports;
+    m->rep_batch[i] = batch;
+    m->rep_ff[i] = ff;
+    m->rep_bf[i] = bf;
+    m->rep_dec[i] = dec;
+    m->n_reports += 1;
+    m->last_decision = dec;
+    m->last_ff = ff;
+    m->last_bf = bf;
+  }
+  out->switched = m->switched;
+  out->n_reports = m->n_reports;
+  out->last_decision = m->last_decision;
+  out->budget[0] = m->budget[0];
+  out->budget[1] = m->budget[1];
+  out->used[0] = f->budget;
+  out->used[1] = b->budget;
+  out->last_ff = m->last_ff;
+  out->last_bf = m->last_bf;
+  out->trace_ff = ff;
+  out->trace_bf = bf;
 }
 
 // sum of the per-interval partials in interval order (each interval's slots
@@ -801,6 +894,8 @@ __global__ void cycle_end_kernel(SolveCtrl* c, double tol) {
   } else if (nrm <= tol * c->trace[0]) {
     c->converged = 1;
     c->active = 0;
+  } else if (c->cycles_run >= c->budget) {
+    c->active = 0;  // budget spent (the remaining host-issued cycles are no-ops)
   }
 }
 
@@ -909,7 +1004,28 @@ void launch_zero(int G, long long n, Mat dst, const int* active, cudaStream_t s)
   launch_k(zero_kernel, dim3(grid), dim3(256), 0, s, 1, G, n / 4, dst, active);
 }
 
-void launch_ctrl_begin(SolveCtrl* c, cudaStream_t s) { launch_k(ctrl_begin_kernel, dim3(1), dim3(1), 0, s, 1, c); }
+void launch_ctrl_begin(SolveCtrl* c, int host_cycles, const int* budget_dev, cudaStream_t s) {
+  launch_k(ctrl_begin_kernel, dim3(1), dim3(1), 0, s, 1, c, host_cycles, budget_dev);
+}
+
+void launch_monitor_init(MonitorDev* m, double threshold, int policy_switch, int cap, int fwd,
+                         int bwd, cudaStream_t s) {
+  launch_k(monitor_init_kernel, dim3(1), dim3(1), 0, s, 1, m, threshold, policy_switch, cap, fwd,
+           bwd);
+}
+
+void launch_monitor_set_budget(MonitorDev* m, int fwd, int bwd, cudaStream_t s) {
+  launch_k(monitor_set_budget_kernel, dim3(1), dim3(1), 0, s, 1, m, fwd, bwd);
+}
+
+void launch_monitor_probe(MonitorDev* m, int begin, cudaStream_t s) {
+  launch_k(monitor_probe_kernel, dim3(1), dim3(1), 0, s, 1, m, begin);
+}
+
+void launch_monitor_record(MonitorDev* m, const SolveCtrl* f, const SolveCtrl* b,
+                           long long batch, MonitorSummary* out, cudaStream_t s) {
+  launch_k(monitor_record_kernel, dim3(1), dim3(1), 0, s, 1, m, f, b, batch, out);
+}
 
 void launch_trace_record(SolveCtrl* c, const double* partials, int n_chunks, int S, int per_rank,
                          bool reversed, cudaStream_t s, const LamScale* sc) {

@@ -692,9 +692,46 @@ double Trainer::update(long long k, bool parallel, bool apply) {
     e.serial_adjoint_device(lamN_, lam0_, true);
   embed_backward(lam0_);
   if (apply) optimizer_step();
+  // the factors of this update's traces into the monitor's summary (device)
+  if (parallel && e.monitor_on()) e.monitor_record(-1);
   MGLP_CUDA(cudaStreamSynchronize(s_));
   eng_->check_range();
   return loss;
+}
+
+ProbeOutcome Trainer::update_probe(long long k, bool use_probe_gradient) {
+  Engine& e = *eng_;
+  if (!e.monitor_on()) throw ValidationError("update_probe: attach the monitor first");
+  ProbeOutcome o;
+  if (use_probe_gradient) {
+    e.monitor_probe(true);
+    o.loss = update(k, true, true);
+    e.monitor_probe(false);
+    e.monitor_record(k);
+    const MonitorSummary& m = e.monitor_read();
+    o.fwd_iters = m.used[0];  // the doubled budget the update ran with
+    o.bwd_iters = m.used[1];
+    o.fwd_factor = m.last_ff;
+    o.bwd_factor = m.last_bf;
+    o.decision = m.last_decision;
+    o.switched = m.switched;
+    return o;
+  }
+  const long long snap = e.snapshot();
+  e.monitor_probe(true);
+  update(k, true, false);
+  e.monitor_probe(false);
+  e.restore(snap);
+  e.monitor_record(k);
+  const MonitorSummary& m = e.monitor_read();
+  o.fwd_factor = m.last_ff;
+  o.bwd_factor = m.last_bf;
+  o.decision = m.last_decision;
+  o.switched = m.switched;
+  o.fwd_iters = m.budget[0];
+  o.bwd_iters = m.budget[1];
+  o.loss = update(k, true, true);
+  return o;
 }
 
 int Trainer::correct_predictions() {

@@ -39,6 +39,14 @@ struct CheckpointMeta {
   bool has_optimizer = false;
 };
 
+// one indicator probe batch (training.cpp:244-276), decided on the device
+struct ProbeOutcome {
+  double loss = 0.0;
+  int fwd_iters = 0, bwd_iters = 0;  // the row's budgets
+  double fwd_factor = 0.0, bwd_factor = 0.0;
+  int decision = 0, switched = 0;
+};
+
 class Trainer {
  public:
   Trainer(const StackDesc& sd, const SolveCfg& solve, int vocab, int max_seq, const TaskDesc& task,
@@ -51,6 +59,11 @@ class Trainer {
   // split; parallel = layer-parallel engine, else the serial sweeps; apply =
   // take the optimizer step. Returns the mean cross-entropy loss.
   double update(long long k, bool parallel, bool apply);
+  // probe_batch (training.cpp:244-276) with the engine's device monitor
+  // (attached first): ProbeScope, the update (the doubled run IS the update
+  // with use_probe_gradient, else a measurement-only run behind a warm-state
+  // snapshot followed by the nominal update), record() on the device
+  ProbeOutcome update_probe(long long k, bool use_probe_gradient);
   // token accuracy on the validation split through the serial forward
   double evaluate();
   // logits of the last update's final state ([B*seq][vocab])

@@ -19,7 +19,8 @@ import numpy as np
 
 from . import _native as N
 from ._native import ValidationError
-from .controller import (INCREASE_ITERATIONS, SWITCH_SERIAL, IndicatorConfig, IndicatorReport,
+from .controller import (INCREASE_ITERATIONS, SWITCH_SERIAL, DeviceMonitor, IndicatorConfig,
+                         IndicatorReport,
                          InexactnessMonitor, ProbeScope, last_pair_factor)
 from .engine import KINDS, SolveConfig, StackConfig
 
@@ -265,7 +266,10 @@ class Trainer:
         self._validate(task, mcfg, tcfg)
         self.task, self.mcfg, self.tcfg = task, mcfg, tcfg
         self.dev = DeviceTrainer(task, mcfg, tcfg, device)
-        self.mon = InexactnessMonitor(tcfg.indicator)
+        # the switching mode's monitor runs on the device (DeviceMonitor):
+        # budgets, decisions, switch flag and report log in GPU memory
+        self.mon = (DeviceMonitor(tcfg.indicator, self.dev.h, trainer=True)
+                    if tcfg.mode == "switching" else InexactnessMonitor(tcfg.indicator))
         self.batches_per_epoch = task.train_size // tcfg.batch_size
         self.total_batches = tcfg.epochs * self.batches_per_epoch
         self.echo = config_echo(task, mcfg, tcfg)
@@ -301,24 +305,19 @@ class Trainer:
                 btr[:] = self.dev.trace(False)
         return loss
 
-    def _probe_batch(self, k, row: MetricsRow):  # training.cpp:272-294
-        ftr, btr = [], []
-        budget = self.dev.budget
-        if self.tcfg.indicator.use_probe_gradient:
-            with ProbeScope(budget):
-                row.fwd_iters, row.bwd_iters = budget.fwd_iters, budget.bwd_iters
-                row.loss = self._update(k, True, ftr, btr, True)
-            rep = self.mon.record(k, last_pair_factor(ftr), last_pair_factor(btr), budget)
-            row.fwd_factor, row.bwd_factor = rep.fwd_factor, rep.bwd_factor
-            return
-        self.dev.snapshot()
-        with ProbeScope(budget):
-            self._update(k, True, ftr, btr, False)
-        self.dev.restore()
-        rep = self.mon.record(k, last_pair_factor(ftr), last_pair_factor(btr), budget)
-        row.fwd_factor, row.bwd_factor = rep.fwd_factor, rep.bwd_factor
-        row.fwd_iters, row.bwd_iters = budget.fwd_iters, budget.bwd_iters
-        row.loss = self._update(k, True, [], [], True)
+    def _probe_batch(self, k, row: MetricsRow):  # training.cpp:244-276
+        """ProbeScope, the update and record() run on the device
+        (mglp_trainer_update_probe); one synchronisation for the whole row."""
+        loss = C.c_double()
+        fi, bi, dec, sw = C.c_int(), C.c_int(), C.c_int(), C.c_int()
+        ff, bf = C.c_double(), C.c_double()
+        N.call("mglp_trainer_update_probe", self.dev.h, k,
+               int(self.tcfg.indicator.use_probe_gradient), C.byref(loss), C.byref(fi),
+               C.byref(bi), C.byref(ff), C.byref(bf), C.byref(dec), C.byref(sw))
+        row.loss = loss.value
+        row.fwd_iters, row.bwd_iters = fi.value, bi.value
+        row.fwd_factor, row.bwd_factor = ff.value, bf.value
+        self.mon.note(sw.value)
 
     def capture(self, next_batch: int) -> bytes:
         return self.dev.save_checkpoint(next_batch, self.echo)
@@ -343,6 +342,14 @@ class Trainer:
                     res.switch_state = self.capture(k + 1)
                     res.switched, res.switch_batch = True, k + 1
                     serial_now = True
+            elif monitored:
+                # factors of this update's traces, evaluated on the device
+                row.loss = self._update(k, True)
+                ff, bf, fi, bi = C.c_double(), C.c_double(), C.c_int(), C.c_int()
+                N.call("mglp_trainer_last_factors", self.dev.h, C.byref(ff), C.byref(bf),
+                       C.byref(fi), C.byref(bi))
+                row.fwd_iters, row.bwd_iters = fi.value, bi.value
+                row.fwd_factor, row.bwd_factor = ff.value, bf.value
             else:
                 ftr, btr = [], []
                 row.fwd_iters = self.dev.budget.fwd_iters

@@ -76,7 +76,9 @@ def make(name, c):
         total = traj.shape[0] - 1
         out.update(traj_last=traj[-1], traj_mid=traj[total // 2], serial_last=straj[-1],
                    serial_lam0=slam[0], grads_l2=np.array([np.linalg.norm(g)]),
-                   grads_head=g[:4096].copy(), serial_grads_head=sg[:4096].copy())
+                   grads_head=g[:4096].copy(), serial_grads_head=sg[:4096].copy(),
+                   # every gradient entry (float32 is ample for a 1e-4 bar)
+                   grads=g.astype(np.float32))
     else:
         out.update(params=params, traj=traj, grads=g, serial_traj=straj, serial_lam=slam,
                    serial_grads=sg)
@@ -86,5 +88,6 @@ def make(name, c):
 
 
 if __name__ == "__main__":
-    for k, v in CASES.items():
-        make(k, v)
+    names = sys.argv[1:] or list(CASES)
+    for k in names:
+        make(k, CASES[k])

@@ -152,6 +152,22 @@ def test_tiny_baseline_config():
     assert rel(bo.lambda0.flat(), g["lam0"]) < TOL
     assert rel(gr[:4096], g["grads_head"]) < TOL
     assert abs(np.linalg.norm(gr) - g["grads_l2"][0]) / g["grads_l2"][0] < TOL
+    # every one of the ~800k gradient entries: against the whole vector's max,
+    # and per (layer, tensor) against that tensor's max (a tensor whose exact
+    # gradient vanishes -- the attention key bias -- against its layer's)
+    ref = np.asarray(g["grads"], np.float64)
+    assert rel(gr, ref) < TOL
+    from paper_2601_09026_b200 import lipschitz as L
+    lay = L.param_layout(st.cfg)
+    layer_max = {}
+    for layer, comp, off, n in lay:
+        layer_max[layer] = max(layer_max.get(layer, 0.0), float(np.abs(ref[off:off + n]).max()))
+    for layer, comp, off, n in lay:
+        r = ref[off:off + n]
+        den = float(np.abs(r).max())
+        den = layer_max[layer] if den < 1e-9 * layer_max[layer] else max(den, 1e-3 * layer_max[layer])
+        err = float(np.abs(np.asarray(gr[off:off + n]) - r).max()) / den
+        assert err < TOL, (layer, comp, err)
     traj = serial_forward(st, sf(g["z0"]))
     assert rel(traj[-1].flat(), g["serial_last"]) < TOL
 
