@@ -141,7 +141,10 @@ def test_gated_graph_follows_device_budget():
         N.call("mglp_engine_graph_replay", h)  # same graph, no recapture
         N.call("mglp_engine_sync", h)
         ft, bt = traces()
-        assert (len(ft), len(bt)) == (f, b)
+        # the budget, or fewer cycles when a solve converges exactly (tol 0:
+        # this small stack's exactness front reaches the end after 3 cycles)
+        assert 1 <= len(ft) <= f and 1 <= len(bt) <= b
+        assert len(ft) == f or ft[-1] == 0.0
         out[(f, b)] = (ft, bt, lam0.clone())
     # eager solves at the same budgets: bitwise the gated replays
     N.call("mglp_engine_capture_cycles", h, 0)
