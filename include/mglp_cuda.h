@@ -55,7 +55,7 @@ typedef struct {
   int buffer_open, buffer_close;
   double ln_eps;
   double base_h;
-  double dropout; /* must be 0 on the device path */
+  double dropout; /* frozen per-batch masks: mglp_engine_refresh_dropout / _set_dropout_masks */
   double init_std;
   int depth_scaled_init;
 } mglp_stack_desc;
@@ -223,6 +223,14 @@ mglp_status mglp_engine_create_dist(const mglp_stack_desc* stack, const mglp_sol
 /* rank, world and the owned interior layer range [layer_lo, layer_hi) */
 mglp_status mglp_engine_rank_info(mglp_engine* e, int* rank, int* world, int* layer_lo,
                                   int* layer_hi);
+/* LayerStack::masks() set explicitly (a reference-side stack's frozen masks,
+ * blocks.cpp:576-599): keep[(layer * 3 + site) * max(B*s_x, B*s_y) * d + i]
+ * = 1 keeps element i of that layer's site (0 attention out phi1, 1 MLP out
+ * phi2, 2 cross-attention out phi3 -- decoder layers only), 0 drops it; the
+ * kept values are scaled by 1 / (1 - dropout) as in the reference. */
+mglp_status mglp_engine_set_dropout_masks(mglp_engine* e, int batch, int s_x, int s_y,
+                                          const unsigned char* keep);
+
 /* The communicator behind a multi-rank engine: *backend 0 = none (one GPU),
  * 1 = NCCL, 2 = in-process loopback; *nranks = the rank count the backend
  * itself reports (ncclCommCount), recorded by bench.py next to n_gpus. */

@@ -263,6 +263,16 @@ mglp_status mglp_engine_rank_info(mglp_engine* e, int* rank, int* world, int* lo
   });
 }
 
+mglp_status mglp_engine_set_dropout_masks(mglp_engine* e, int batch, int s_x, int s_y,
+                                          const unsigned char* keep) {
+  return guard([&] {
+    need(e, "engine");
+    need(keep, "keep");
+    ensure_shape(e, batch, s_x, s_y, e->eng->width());
+    e->eng->set_dropout_masks(keep);
+  });
+}
+
 mglp_status mglp_engine_comm_info(mglp_engine* e, int* backend, int* nranks) {
   return guard([&] {
     need(e, "engine");

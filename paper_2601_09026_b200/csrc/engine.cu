@@ -1074,7 +1074,42 @@ int Engine::gemm_blocks(const GemmArgs& g) const {
 // Phi: one layer step z + dt*F(z) for a family of G layers (blocks.cpp:466-514)
 // =============================================================================
 
+// Write-ownership contract of a launch family (the reference Executor
+// rejects overlapping task write ranges before running them,
+// executor.cpp:75-110): member g writes [at(g), at(g) + extent) of every
+// output family, so the members' ranges must be pairwise disjoint --
+// equally strided families are iff |step * slot_stride| >= extent -- and no
+// member may write a state it (or another member) reads as its input.
+void Engine::check_family_writes(const EvalSpec& e, bool adjoint) const {
+  if (e.G <= 1) return;
+  auto disjoint = [&](const Mat& m, long long extent, const char* what) {
+    if (!m.ok()) return;
+    const long long stride = std::llabs((long long)m.step * m.slot_stride);
+    if (stride < extent)
+      throw ContractViolation(std::string("launch family: members' write ranges overlap (") +
+                              what + ")");
+  };
+  const long long sn = state_n_;
+  disjoint(e.cmb.out, sn, "solver state");
+  if (e.act.base != nullptr && e.act.step == 0)
+    throw ContractViolation("launch family: members share one activation slot");
+  if (e.bact.base != nullptr && e.bact.step == 0 && !e.wgrad_only)
+    throw ContractViolation("launch family: members share one backward slot");
+  // in-place families (out = in) are fine member by member; a member's output
+  // must not be another member's input
+  const Mat& in = adjoint ? e.lam : e.in;
+  if (e.cmb.out.ok() && in.ok() && e.cmb.out.ptr == in.ptr && e.cmb.out.slot_stride == in.slot_stride) {
+    for (int g = 1; g < e.G && g < 4; ++g) {
+      const long long o = (long long)e.cmb.out.slot0 + (long long)g * e.cmb.out.step;
+      for (int h = 0; h < e.G; ++h)
+        if (h != g && (long long)in.slot0 + (long long)h * in.step == o)
+          throw ContractViolation("launch family: a member writes another member's input");
+    }
+  }
+}
+
 void Engine::eval_forward(const EvalSpec& e0) {
+  check_family_writes(e0, false);
   // split families that straddle the encoder/decoder boundary
   if (sd_.kind == 2) {
     const int first = e0.layer0, last = e0.layer0 + (e0.G - 1) * e0.layer_step;
@@ -1435,6 +1470,7 @@ void Engine::decoder_forward(const EvalSpec& e) {
 // =============================================================================
 
 void Engine::eval_adjoint(const EvalSpec& e0) {
+  check_family_writes(e0, true);
   if (sd_.kind == 2) {
     const int first = e0.layer0, last = e0.layer0 + (e0.G - 1) * e0.layer_step;
     const bool fdec = first >= n_split_, ldec = last >= n_split_;
@@ -2688,6 +2724,27 @@ void Engine::refresh_dropout(uint64_t seed, uint64_t batch_index) {
   MGLP_CUDA(cudaStreamSynchronize(stream_));
   cudaFree(dkeys);
   cudaFree(drows);
+  drop_on_ = true;
+}
+
+void Engine::set_dropout_masks(const unsigned char* keep_host) {
+  const bool was_on = drop_on_;
+  drop_on_ = false;
+  if (sd_.dropout <= 0.0) return;
+  invalidate_linearization();
+  if (!was_on) drop_graph();
+  if (!traj_) throw ValidationError("set_dropout_masks: set the shape first");
+  const long long slot = (long long)std::max(Tx_, Ty_) * sd_.d;
+  MGLP_CUDA(cudaSetDevice(device_));
+  if (drop_slot_ != slot) {
+    if (drop_masks_) cudaFree(drop_masks_);
+    drop_masks_ = nullptr;
+    MGLP_CUDA(cudaMalloc(&drop_masks_, (size_t)total_ * 3 * slot));
+    drop_slot_ = slot;
+  }
+  MGLP_CUDA(cudaMemcpyAsync(drop_masks_, keep_host, (size_t)total_ * 3 * slot,
+                            cudaMemcpyHostToDevice, stream_));
+  MGLP_CUDA(cudaStreamSynchronize(stream_));
   drop_on_ = true;
 }
 

@@ -106,6 +106,9 @@ class Engine {
   // exact map, as for evaluation). No-ops when the stack's dropout is 0.
   void refresh_dropout(uint64_t seed, uint64_t batch_index);
   void clear_dropout();
+  // explicit masks (a reference LayerStack's masks(), blocks.cpp:576-599):
+  // keep bytes [total][3 sites][max(Tx, Ty) * d], site 2 on decoder layers only
+  void set_dropout_masks(const unsigned char* keep_host);
   bool dropout_active() const { return drop_on_; }
 
   // ---- shape ----
@@ -282,6 +285,7 @@ class Engine {
     bool residual_only = false;  // out = F(z) (the combine starts from a zero state)
     const float* gscale_mul = nullptr;  // device factor of gscale (LamScale::down)
   };
+  void check_family_writes(const EvalSpec& e, bool adjoint) const;
   void eval_forward(const EvalSpec& e);
   void eval_adjoint(const EvalSpec& e);
   void encoder_forward(const EvalSpec& e, int Rx, bool causal, Mat xin, Mat yin_passive);

@@ -65,6 +65,25 @@ constexpr int NSLOTS = 12;
 constexpr int MAXR = 8;  // barrier array length
 // + barriers (1 KiB) + per-epilogue-warp 32 x 16 fp32 transpose buffers
 constexpr int SMEM_BYTES = NSLOTS * TILE_BYTES + 1024 /*align*/ + 1024 + 8 * 2048;
+// Drain variant (DR = 1; CTA pair, both operands pre-split): the epilogue
+// first copies the whole accumulator (main + 2^-11 correction, combined)
+// from TMEM into shared memory -- 32 rows x 128 columns fp32 per epilogue
+// warp, 128 KiB per CTA -- and releases TMEM at once, so the next tile's
+// MMAs run while the bias / activation / combine math and the global stores
+// of this tile proceed from shared memory. The hi|lo rings shrink to 3 + 3
+// stages to make room.
+constexpr int NSLOTS_DR = 6;
+constexpr int DRAIN_WARP_BYTES = 32 * 128 * 4;
+constexpr int SMEM_BYTES_DR = NSLOTS_DR * TILE_BYTES + 1024 + 1024 + 8 * DRAIN_WARP_BYTES;
+static_assert(SMEM_BYTES_DR <= 232448, "drain variant exceeds 227 KiB of shared memory");
+template <int DR>
+constexpr int nslots() { return DR ? NSLOTS_DR : NSLOTS; }
+template <int DR>
+constexpr int smem_bytes() { return DR ? SMEM_BYTES_DR : SMEM_BYTES; }
+// 16-byte piece swizzle of the drain buffer (512-byte rows): the drain's
+// lane = row stores and the epilogue's 4-lanes-per-row loads are both
+// bank-conflict free
+__device__ __forceinline__ int drain_swz(int r) { return ((r & 1) << 2) | ((r >> 1) & 3); }
 
 
 struct TcParams {
@@ -166,7 +185,7 @@ struct Cfg {
   static constexpr int THREADS = 32 * (8 + EPI_WARPS);
 };
 
-template <int CG>
+template <int CG, int DR>
 __global__ void __launch_bounds__(Cfg<CG>::THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap mapA,
                    const __grid_constant__ CUtensorMap mapB, const TcParams p,
@@ -181,7 +200,8 @@ __global__ void __launch_bounds__(Cfg<CG>::THREADS, 1)
   if (active && *(volatile const int*)active == 0) return;
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
-  uint64_t* fullA = reinterpret_cast<uint64_t*>(smem + NSLOTS * TILE_BYTES);  // [NA]
+  constexpr int NS = nslots<DR>();
+  uint64_t* fullA = reinterpret_cast<uint64_t*>(smem + NS * TILE_BYTES);  // [NA]
   uint64_t* fullB = fullA + MAXR;    // [NB]
   uint64_t* emptyB = fullB + MAXR;   // [NB]
   uint64_t* sfree = emptyB + MAXR;   // [NA]
@@ -208,8 +228,8 @@ __global__ void __launch_bounds__(Cfg<CG>::THREADS, 1)
   const bool direct = p.b_direct != 0, adirect = p.a_direct != 0;
   // both operands pre-split: 6 A + 6 B hi|lo slots, no staging
   const int NA = adirect ? 0 : (direct ? p.ring_a : 3);
-  const int NH = adirect ? 6 : (direct ? p.ring_h : 3);
-  const int NB = adirect ? 6 : p.ring_b;
+  const int NH = adirect ? (DR ? 3 : 6) : (direct ? p.ring_h : 3);
+  const int NB = adirect ? (DR ? 3 : 6) : p.ring_b;
   auto slot = [&](int i) { return smem + i * TILE_BYTES; };
   auto stg_a = [&](int s) { return direct ? slot(s) : slot(2 * s); };
   auto stg_b = [&](int s) { return slot(2 * s + 1); };
@@ -469,9 +489,85 @@ __global__ void __launch_bounds__(Cfg<CG>::THREADS, 1)
     constexpr int COLS = TN / CG;  // columns per epilogue warp
     const bool res0 = p.ep.kind == EPI_FINAL && p.ep.cmb.mode == CM_RES0;
     const uint32_t tempty_leader = CG == 2 ? map_to_rank(smem_u32(&tempty[0]), 0) : 0u;
-    const uint32_t ebuf = smem_u32(smem + NSLOTS * TILE_BYTES + 1024) + ew * 2048;
+    const uint32_t ebuf = smem_u32(smem + NS * TILE_BYTES + 1024) + ew * (DR ? DRAIN_WARP_BYTES : 2048);
     int tc = 0;
     for (int t = unit; t < total; t += nunits, ++tc) {
+      if constexpr (DR != 0 && CG == 2) {
+        const Tile T = tile_of(t);
+        wait(&tfull[0], tc & 1);
+        if (ew == 0 && lane == 0) flush(8);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t lane_addr = tmem_base + ((uint32_t)(q * 32) << 16);
+        // (1) drain: TMEM (main + correction) -> combined fp32 rows in smem
+#pragma unroll 1
+        for (int c = 0; c < COLS; c += 16) {
+          uint32_t rv[16], rw[16];
+          tmem_ld16(lane_addr + half * COLS + c, rv);
+          if (p.passes > 1) tmem_ld16(lane_addr + TN + half * COLS + c, rw);
+          tmem_wait();
+#pragma unroll
+          for (int cc = 0; cc < 4; ++cc) {
+            uint4 w4;
+            float* f = reinterpret_cast<float*>(&w4);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const float mv = __uint_as_float(rv[4 * cc + i]);
+              f[i] = p.passes > 1 ? fmaf(__uint_as_float(rw[4 * cc + i]), kLoInv, mv) : mv;
+            }
+            sts128(ebuf + lane * 512 + ((((c >> 2) + cc) ^ drain_swz(lane)) << 4), w4);
+          }
+        }
+        // the accumulator is free for the next tile's MMAs
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        asm volatile("bar.sync 2, %0;" ::"n"(32 * C::EPI_WARPS) : "memory");
+        if (ew == 0 && lane == 0) {
+          if (leader)
+            mbar_arrive(&tempty[0]);
+          else
+            mbar_arrive_cluster(tempty_leader);
+        }
+        __syncwarp();
+        // (2) the epilogue proper from shared memory, 4 lanes per row
+        double r2 = 0.0;
+#pragma unroll 1
+        for (int c = 0; c < COLS; c += 16) {
+          const int col = T.n0 + half * COLS + c + (lane & 3) * 4;
+          const int nvalid = min(4, p.N - col);
+          float4 w[4];
+          int rows[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const int r = i * 8 + (lane >> 2);
+            w[i] = lds128(ebuf + r * 512 + ((((c >> 2) + (lane & 3)) ^ drain_swz(r)) << 4));
+            const int row = T.m0 + q * 32 + r;
+            rows[i] = (row < p.M && nvalid > 0) ? row : -1;
+          }
+          if (!(p.debug & 2)) {
+            if (nvalid == 4 && p.vec_ok) {
+              r2 += epilogue_4x4(p.ep, T.g, T.b, T.h, rows, col, w);
+            } else {
+#pragma unroll
+              for (int i = 0; i < 4; ++i)
+                if (rows[i] >= 0)
+                  r2 += epilogue_row(p.ep, T.g, T.b, T.h, rows[i], col, &w[i].x, nvalid);
+            }
+          }
+        }
+        __syncwarp();  // this warp's reads of the drain buffer precede the next drain
+        if (res0) {
+          for (int o = 16; o > 0; o >>= 1) r2 += __shfl_xor_sync(0xffffffffu, r2, o);
+          if (lane == 0) red[ew] = r2;
+          asm volatile("bar.sync 1, %0;" ::"n"(32 * C::EPI_WARPS) : "memory");
+          if (ew == 0 && lane == 0 && T.mt < tiles_m128) {
+            double tsum = 0.0;
+            for (int i = 0; i < C::EPI_WARPS; ++i) tsum += red[i];
+            p.ep.cmb.norm_partials[p.ep.cmb.norm_base + T.z * p.ep.cmb.norm_member_stride +
+                                   T.mt * tiles_n + T.nt] = tsum;
+          }
+          asm volatile("bar.sync 1, %0;" ::"n"(32 * C::EPI_WARPS) : "memory");
+        }
+        continue;
+      }
       const Tile T = tile_of(t);
       const int acc = tc % NACC;
       const uint32_t aph = (tc / NACC) & 1;
@@ -815,13 +911,13 @@ int num_sms() {
   return sms;
 }
 
-template <int CG>
-void launch_cg(const GemmArgs& a, const int* active, cudaStream_t s) {
+template <int CG, int DR>
+void launch_cg(const GemmArgs& a, const int* active, cudaStream_t s, Prepared& P) {
   using C = Cfg<CG>;
-  Prepared P = prepare(a);
+  constexpr int SMEM = smem_bytes<DR>();
   static bool attr = [] {
-    MGLP_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<CG>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
+    MGLP_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<CG, DR>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
     return true;
   }();
   (void)attr;
@@ -829,7 +925,7 @@ void launch_cg(const GemmArgs& a, const int* active, cudaStream_t s) {
       (long long)ceil_div(a.N, C::TN) * ceil_div(a.M, C::TM) * a.G * a.Bb * a.H;
   const int units = (int)std::min<long long>(tiles, num_sms() / CG);
   // CG = 2: one cluster of two CTAs per unit
-  launch_k(gemm_tc_kernel<CG>, dim3(CG * units), dim3(C::THREADS), SMEM_BYTES, s, CG, P.mA, P.mB,
+  launch_k(gemm_tc_kernel<CG, DR>, dim3(CG * units), dim3(C::THREADS), SMEM, s, CG, P.mA, P.mB,
            P.p, active);
   MGLP_CUDA(cudaGetLastError());
   if (P.p.prof) {
@@ -877,10 +973,23 @@ int gemm_tc_blocks(const GemmArgs& a) {
 void launch_gemm_tc(const GemmArgs& a, const int* active, cudaStream_t s) {
   if (a.G == 0 || a.M == 0 || a.N == 0) return;
   if (a.K == 0) throw ContractViolation("gemm_tc: K must be positive");
-  if (use_pair(a))
-    launch_cg<2>(a, active, s);
-  else
-    launch_cg<1>(a, active, s);
+  Prepared P = prepare(a);
+  // MGLP_GEMM_DRAIN=0: the pair kernel releases TMEM only after its epilogue
+  static const bool drain = [] {
+    const char* e = getenv("MGLP_GEMM_DRAIN");
+    return !(e && atoi(e) == 0);
+  }();
+  if (use_pair(a)) {
+    // measured (tools/gpu_drain_diag.sh): draining wins where the epilogue is
+    // large against the K loop (K = 768: MLP-in, QKV), the full-depth rings
+    // win for long K (K = 3072: MLP-out -7%)
+    if (drain && P.p.a_direct && a.K <= 1024)
+      launch_cg<2, 1>(a, active, s, P);
+    else
+      launch_cg<2, 0>(a, active, s, P);
+  } else {
+    launch_cg<1, 0>(a, active, s, P);
+  }
 }
 
 long long pack_hl_cols(int K) { return (long long)ceil_div(K, BK) * BK; }
