@@ -231,6 +231,13 @@ mglp_status mglp_engine_rank_info(mglp_engine* e, int* rank, int* world, int* la
 mglp_status mglp_engine_set_dropout_masks(mglp_engine* e, int batch, int s_x, int s_y,
                                           const unsigned char* keep);
 
+/* Device memory this engine holds (parameters, pre-split weights, gradients,
+ * activation caches, trajectory, solver levels, scratch): on a P-rank engine
+ * the per-layer and per-time-point buffers are mapped only under the rank's
+ * own block (CUDA virtual memory; the rest of the virtual range faults), so
+ * this is about 1/P of the single-rank figure plus the shared scratch. */
+mglp_status mglp_engine_memory(mglp_engine* e, long long* bytes);
+
 /* The communicator behind a multi-rank engine: *backend 0 = none (one GPU),
  * 1 = NCCL, 2 = in-process loopback; *nranks = the rank count the backend
  * itself reports (ncclCommCount), recorded by bench.py next to n_gpus. */

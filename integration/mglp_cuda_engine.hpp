@@ -208,7 +208,7 @@ class CudaLayerParallelEngine {
     return v;
   }
   static State unflatten(const double* p, const State& like) {
-    State s{Tensor::zeros_like(like.x), Tensor::zeros_like(like.y)};
+    State s = like;  // same shapes (an unused stream stays empty: size 0)
     std::memcpy(s.x.data(), p, s.x.size() * sizeof(double));
     if (s.y.size()) std::memcpy(s.y.data(), p + s.x.size(), s.y.size() * sizeof(double));
     return s;

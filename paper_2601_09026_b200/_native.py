@@ -72,6 +72,7 @@ _SIGS = {
     "mglp_engine_backward_keep_grads": [_vp, C.c_int, C.c_int, C.c_int, _dp, _dp, _dp, _dp,
                                         C.c_int, _ip, _ip],
     "mglp_engine_comm_info": [_vp, _ip, _ip],
+    "mglp_engine_memory": [_vp, _llp],
     "mglp_engine_set_dropout_masks": [_vp, C.c_int, C.c_int, C.c_int, _vp],
     "mglp_engine_snapshot": [_vp],
     "mglp_engine_restore": [_vp],

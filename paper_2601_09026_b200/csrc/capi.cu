@@ -273,6 +273,14 @@ mglp_status mglp_engine_set_dropout_masks(mglp_engine* e, int batch, int s_x, in
   });
 }
 
+mglp_status mglp_engine_memory(mglp_engine* e, long long* bytes) {
+  return guard([&] {
+    need(e, "engine");
+    need(bytes, "bytes");
+    *bytes = (long long)e->eng->hbm_bytes();
+  });
+}
+
 mglp_status mglp_engine_comm_info(mglp_engine* e, int* backend, int* nranks) {
   return guard([&] {
     need(e, "engine");
@@ -467,6 +475,9 @@ mglp_status mglp_engine_forward(mglp_engine* e, int batch, int s_x, int s_y, con
     need(e, "engine");
     need(z0, "z0");
     const Shape sh = ensure_shape(e, batch, s_x, s_y, e->eng->width());
+    if (traj_out && e->eng->world() > 1)
+      throw ValidationError("forward: a rank of a multi-GPU engine holds only its own block of the "
+                            "trajectory; pass traj_out = NULL and read it per rank");
     upload(e, e->dz, z0, sh);
     e->eng->forward_device(e->dz);
     if (traj_out) download(e, traj_out, e->eng->traj_dev(), sh, e->eng->total_layers() + 1);
@@ -719,6 +730,9 @@ mglp_status mglp_engine_read_traj(mglp_engine* e, int first, int count, float* d
     const int T = e->eng->total_layers() + 1;
     if (first < 0 || count < 0 || first + count > T)
       throw ValidationError("read_traj: time points out of range");
+    if (!e->eng->holds_points(first, count))
+      throw ValidationError("read_traj: a rank of a multi-GPU engine holds only its own block of "
+                            "time points (mglp_engine_rank_info)");
     const size_t n = (size_t)e->eng->state_elems();
     MGLP_CUDA(cudaMemcpyAsync(dst, e->eng->traj_dev() + (size_t)first * n,
                               (size_t)count * n * sizeof(float), cudaMemcpyDefault,

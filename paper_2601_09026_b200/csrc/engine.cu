@@ -2,9 +2,13 @@
 // MGRIT backpropagation. See engine.h for the map to the reference.
 #include "engine.h"
 #include "rng.h"
+#include "vmm.h"
 
 #include <algorithm>
 #include <atomic>
+#include <climits>
+#include <map>
+#include <mutex>
 #include <cmath>
 #include <cstring>
 #include <thread>
@@ -122,20 +126,20 @@ Engine::Engine(const StackDesc& sd, const SolveCfg& cfg, int device,
   MGLP_CUDA(cudaSetDevice(device_));
   MGLP_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
   build_layouts();
-  const size_t pbytes = (size_t)total_ * layer_stride_ * sizeof(float);
-  MGLP_CUDA(cudaMalloc(&P_, pbytes));
-  MGLP_CUDA(cudaMalloc(&Gr_, pbytes));
-  const size_t hbytes = (size_t)total_ * hl_stride_ * sizeof(float);
-  MGLP_CUDA(cudaMalloc(&Whl_, hbytes));
+  build_ranges();
+  P_ = dalloc(layer_stride_, total_, lay_r_);
+  Gr_ = dalloc(layer_stride_, total_, lay_r_);
+  Whl_ = dalloc(hl_stride_, total_, lay_r_);
   MGLP_CUDA(cudaMalloc(&range_flag_, sizeof(int)));
   MGLP_CUDA(cudaMalloc(&lam_sc_, sizeof(LamScale)));
   MGLP_CUDA(cudaMemsetAsync(lam_sc_, 0, sizeof(LamScale), stream_));
   if (world_ > 1) MGLP_CUDA(cudaMalloc(&lam_gather_, 2 * world_ * sizeof(double)));
-  MGLP_CUDA(cudaMemsetAsync(P_, 0, pbytes, stream_));
-  MGLP_CUDA(cudaMemsetAsync(Whl_, 0, hbytes, stream_));
+  dmemset(P_, layer_stride_, lay_r_);
+  dmemset(Whl_, hl_stride_, lay_r_);
   MGLP_CUDA(cudaMemsetAsync(range_flag_, 0, sizeof(int), stream_));
-  MGLP_CUDA(cudaMemsetAsync(Gr_, 0, pbytes, stream_));
-  Gmax_ = std::max(1, N_ / cfg_.coarsen);
+  dmemset(Gr_, layer_stride_, lay_r_);
+  // the largest launch family: this rank's coarse intervals
+  Gmax_ = std::max(1, N_ / cfg_.coarsen / world_);
   cache_valid_.assign(total_, 0);
 }
 
@@ -151,14 +155,149 @@ Engine::~Engine() {
   if (mon_) cudaFree(mon_);
   if (mon_sum_) cudaFree(mon_sum_);
   if (mon_host_) cudaFreeHost(mon_host_);
-  for (float* p : {P_, Whl_, Gr_, scratch_, hlscr_, cache_, bscratch_, bcache_, traj_, lam_all_,
-                   zero_state_, snap_fwd_, snap_bwd_, fwd_stash_})
-    if (p) cudaFree(p);
+  for (float** p : {&P_, &Whl_, &Gr_, &scratch_, &hlscr_, &cache_, &bscratch_, &bcache_, &traj_,
+                    &lam_all_, &zero_state_, &snap_fwd_, &snap_bwd_, &fwd_stash_})
+    dfree(*p);
   if (colred_part_) cudaFree(colred_part_);
   if (drop_masks_) cudaFree(drop_masks_);
   drop_graph();
   for (cudaEvent_t ev : ev_pool_) cudaEventDestroy(ev);
   if (stream_) cudaStreamDestroy(stream_);
+}
+
+// ---- per-rank memory ------------------------------------------------------------
+Engine::Ranges Engine::clip(const Ranges& r, long long lo, long long hi) {
+  Ranges o;
+  for (const auto& x : r) {
+    const long long a = std::max(x.first, lo), b = std::min(x.second, hi);
+    if (a < b) o.push_back({a, b});
+  }
+  return o;
+}
+
+// What rank r of P touches (engine.cu forward_device / backward_device,
+// SURVEY 8(e)): the opening buffer layers (every rank runs them for the
+// broadcast guess), its interior block [ib + lo, ib + hi) and, on the last
+// rank, the closing buffers; time points likewise plus the ghost point
+// ib + lo; coarse level l its points (p_lo, p_hi] plus the ghost p_lo and
+// point 0 (the guess source). The adjoint windows use the reversed partition.
+void Engine::build_ranges() {
+  const int P = world_, r = rank_;
+  const long long per = N_ / P, lo = (long long)r * per, hi = lo + per;
+  const bool last = r == P - 1;
+  auto add = [](Ranges& v, long long a, long long b) {
+    if (a < b) v.push_back({a, b});
+  };
+  lay_r_.clear();
+  traj_r_.clear();
+  lam_r_.clear();
+  win_r_.clear();
+  bwd0_r_.clear();
+  if (P == 1) {
+    add(lay_r_, 0, total_);
+    add(traj_r_, 0, total_ + 1);
+    add(lam_r_, 0, total_ + 1);
+    add(win_r_, 0, N_ + 1);
+    add(bwd0_r_, 0, N_ + 1);
+  } else {
+    add(lay_r_, 0, ib_);
+    add(lay_r_, ib_ + lo, ib_ + hi);
+    if (last) add(lay_r_, ie_, total_);
+    add(traj_r_, 0, ib_ + 1);
+    add(traj_r_, ib_ + lo, ib_ + hi + 1);
+    if (last) add(traj_r_, ie_, total_ + 1);
+    if (r == 0) add(lam_r_, 0, ib_ + 1);
+    if (last) add(lam_r_, ie_, total_ + 1);
+    add(win_r_, 0, 1);
+    add(win_r_, lo, hi + 1);
+    const long long tp = P - 1 - r;
+    add(bwd0_r_, 0, 1);
+    add(bwd0_r_, tp * per, tp * per + per + 1);
+  }
+  for (int adj = 0; adj < 2; ++adj) {
+    lvl_r_[adj].assign(std::max(cfg_.levels, 2), Ranges{});
+    long long n = N_;
+    for (size_t l = 1; l < lvl_r_[adj].size(); ++l) {
+      n /= cfg_.coarsen;
+      Ranges& v = lvl_r_[adj][l];
+      if (P == 1) {
+        add(v, 0, n + 1);
+      } else {
+        const long long pl = n / P, tp = adj ? P - 1 - r : r;
+        add(v, 0, 1);
+        add(v, tp * pl, tp * pl + pl + 1);
+      }
+    }
+  }
+}
+
+bool Engine::holds_points(int first, int count) const {
+  long long covered = 0;
+  for (const auto& x : clip(traj_r_, first, (long long)first + count)) covered += x.second - x.first;
+  return covered == count;
+}
+
+bool Engine::owns_layer_slot(int l) const {
+  for (const auto& x : lay_r_)
+    if (l >= x.first && l < x.second) return true;
+  return false;
+}
+
+namespace {
+std::mutex g_alloc_mu;
+std::map<void*, size_t> g_alloc_bytes;  // device bytes held per engine buffer
+}  // namespace
+
+float* Engine::dalloc(long long slot_elems, long long nslots, const Ranges& r) {
+  const size_t slot_bytes = (size_t)slot_elems * sizeof(float);
+  const size_t bytes = slot_bytes * (size_t)std::max(nslots, 1LL);
+  long long covered = 0;
+  for (const auto& x : r) covered += x.second - x.first;
+  void* p = nullptr;
+  size_t held = bytes;
+  if (world_ == 1 || covered >= nslots) {
+    MGLP_CUDA(cudaMalloc(&p, bytes));
+  } else {
+    std::vector<std::pair<size_t, size_t>> br;
+    for (const auto& x : r) br.push_back({(size_t)x.first * slot_bytes, (size_t)x.second * slot_bytes});
+    p = partial_alloc(device_, bytes, br, &held);
+  }
+  {
+    std::lock_guard<std::mutex> lk(g_alloc_mu);
+    g_alloc_bytes[p] = held;
+  }
+  hbm_bytes_ += held;
+  return static_cast<float*>(p);
+}
+
+void Engine::dfree(float*& p) {
+  if (!p) return;
+  size_t held = 0;
+  {
+    std::lock_guard<std::mutex> lk(g_alloc_mu);
+    auto it = g_alloc_bytes.find(p);
+    if (it != g_alloc_bytes.end()) {
+      held = it->second;
+      g_alloc_bytes.erase(it);
+    }
+  }
+  hbm_bytes_ -= std::min(hbm_bytes_, held);
+  if (!partial_free(p)) cudaFree(p);
+  p = nullptr;
+}
+
+void Engine::dmemset(float* p, long long slot_elems, const Ranges& r) {
+  for (const auto& x : r)
+    MGLP_CUDA(cudaMemsetAsync(p + x.first * slot_elems, 0,
+                              (size_t)(x.second - x.first) * slot_elems * sizeof(float), stream_));
+}
+
+void Engine::dcopy(float* dst, const float* src, long long slot_elems, const Ranges& r,
+                   long long first) {
+  for (const auto& x : clip(r, first, LLONG_MAX))
+    MGLP_CUDA(cudaMemcpyAsync(dst + x.first * slot_elems, src + x.first * slot_elems,
+                              (size_t)(x.second - x.first) * slot_elems * sizeof(float),
+                              cudaMemcpyDeviceToDevice, stream_));
 }
 
 void Engine::build_layouts() {
@@ -359,8 +498,10 @@ void Engine::set_params(const double* flat) {
     fo += L.flat_size;
   }
   MGLP_CUDA(cudaSetDevice(device_));
-  const size_t n = host.size();
-  MGLP_CUDA(cudaMemcpyAsync(P_, host.data(), n * sizeof(float), cudaMemcpyHostToDevice, stream_));
+  for (const auto& x : lay_r_)  // this rank's layers only (the others are unmapped)
+    MGLP_CUDA(cudaMemcpyAsync(P_ + x.first * layer_stride_, host.data() + x.first * layer_stride_,
+                              (size_t)(x.second - x.first) * layer_stride_ * sizeof(float),
+                              cudaMemcpyHostToDevice, stream_));
   repack_weights();
   // cached activations were computed with the old parameters
   invalidate_linearization();
@@ -368,8 +509,13 @@ void Engine::set_params(const double* flat) {
 }
 
 void Engine::get_params(double* flat) const {
-  std::vector<float> host((size_t)total_ * layer_stride_);
-  MGLP_CUDA(cudaMemcpy(host.data(), P_, host.size() * sizeof(float), cudaMemcpyDeviceToHost));
+  // a P-rank engine holds its own layers' parameters (the others read 0)
+  std::vector<float> host((size_t)total_ * layer_stride_, 0.f);
+  MGLP_CUDA(cudaStreamSynchronize(stream_));
+  for (const auto& x : lay_r_)
+    MGLP_CUDA(cudaMemcpy(host.data() + x.first * layer_stride_, P_ + x.first * layer_stride_,
+                         (size_t)(x.second - x.first) * layer_stride_ * sizeof(float),
+                         cudaMemcpyDeviceToHost));
   long long fo = 0;
   for (int l = 0; l < total_; ++l) {
     const LayerLayout& L = lay_[(sd_.kind == 2 && l >= n_split_) ? 1 : 0];
@@ -391,9 +537,13 @@ long long Engine::flat_offset(int layer) const {
 void Engine::get_grads_range(int lo, int hi, double* flat) const {
   if (lo < 0 || hi > total_ || lo > hi) throw ValidationError("get_grads: bad layer range");
   MGLP_CUDA(cudaStreamSynchronize(stream_));
-  std::vector<float> host((size_t)(hi - lo) * layer_stride_);
-  MGLP_CUDA(cudaMemcpy(host.data(), Gr_ + (size_t)lo * layer_stride_, host.size() * sizeof(float),
-                       cudaMemcpyDeviceToHost));
+  // a P-rank engine holds its own layers' gradients (the others add 0)
+  std::vector<float> host((size_t)(hi - lo) * layer_stride_, 0.f);
+  for (const auto& x : clip(lay_r_, lo, hi))
+    MGLP_CUDA(cudaMemcpy(host.data() + (x.first - lo) * layer_stride_,
+                         Gr_ + x.first * layer_stride_,
+                         (size_t)(x.second - x.first) * layer_stride_ * sizeof(float),
+                         cudaMemcpyDeviceToHost));
   long long fo = 0;
   for (int l = lo; l < hi; ++l) {
     const LayerLayout& L = lay_[(sd_.kind == 2 && l >= n_split_) ? 1 : 0];
@@ -404,9 +554,7 @@ void Engine::get_grads_range(int lo, int hi, double* flat) const {
   }
 }
 
-void Engine::zero_grads() {
-  MGLP_CUDA(cudaMemsetAsync(Gr_, 0, (size_t)total_ * layer_stride_ * sizeof(float), stream_));
-}
+void Engine::zero_grads() { dmemset(Gr_, layer_stride_, lay_r_); }
 
 // =============================================================================
 // shape-dependent buffers
@@ -426,10 +574,8 @@ void Engine::set_shape(int batch, int s_x, int s_y) {
   if (colred_part_) cudaFree(colred_part_);
   colred_part_ = nullptr;
   for (float** p : {&scratch_, &hlscr_, &cache_, &bscratch_, &bcache_, &traj_, &lam_all_, &zero_state_,
-                    &snap_fwd_, &snap_bwd_, &fwd_stash_}) {
-    if (*p) cudaFree(*p);
-    *p = nullptr;
-  }
+                    &snap_fwd_, &snap_bwd_, &fwd_stash_})
+    dfree(*p);
   B_ = batch;
   sx_ = s_x;
   sy_ = s_y;
@@ -502,7 +648,8 @@ void Engine::set_shape(int batch, int s_x, int s_y) {
   }
   b.size = off;
   const long long cache_slots = eval_only_ ? 1 : total_;
-  MGLP_CUDA(cudaMalloc(&scratch_, (size_t)Gmax_ * al_.size * sizeof(float)));
+  const Ranges all1 = {{0, 1}};
+  scratch_ = dalloc(al_.size, Gmax_, Ranges{{0, Gmax_}});
   {
     // pre-split A operands: the forward GEMMs of 32-aligned widths skip the
     // fp32 -> hi|lo' conversion (MGLP_NO_PRESPLIT_A=1 disables)
@@ -518,23 +665,26 @@ void Engine::set_shape(int batch, int s_x, int s_y) {
       // attention O, GELU output, dh, dqkv ([rows][max(ffn, 3d)])
       hl_w1_ = std::max(sd_.ffn, 3 * sd_.d);
       hl_slot_ = (long long)std::max(Tx_, Ty_) * (sd_.d + hl_w1_);
-      MGLP_CUDA(cudaMalloc(&hlscr_, (size_t)Gmax_ * hl_slot_ * sizeof(float)));
+      hlscr_ = dalloc(hl_slot_, Gmax_, Ranges{{0, Gmax_}});
       hl_cap_ = Gmax_;
     }
   }
-  MGLP_CUDA(cudaMalloc(&cache_, (size_t)cache_slots * al_.size * sizeof(float)));
-  MGLP_CUDA(cudaMalloc(&bscratch_, (size_t)Gmax_ * bl_.size * sizeof(float)));
-  MGLP_CUDA(cudaMalloc(&bcache_, (size_t)cache_slots * bl_.size * sizeof(float)));
+  const Ranges& cache_r = eval_only_ ? all1 : lay_r_;
+  cache_ = dalloc(al_.size, cache_slots, cache_r);
+  bscratch_ = dalloc(bl_.size, Gmax_, Ranges{{0, Gmax_}});
+  bcache_ = dalloc(bl_.size, cache_slots, cache_r);
   colred_cap_ = (long long)std::max(total_, Gmax_) * kColRedChunks *
                 std::max(std::max(3 * sd_.d, sd_.ffn), 2 * sd_.d) * 2;
   MGLP_CUDA(cudaMalloc(&colred_part_, (size_t)colred_cap_ * sizeof(double)));
   bcache_valid_.assign(total_, 0);
   const long long traj_slots = eval_only_ ? 1 : total_ + 1;
-  MGLP_CUDA(cudaMalloc(&traj_, (size_t)traj_slots * state_n_ * sizeof(float)));
-  MGLP_CUDA(cudaMalloc(&lam_all_, (size_t)traj_slots * state_n_ * sizeof(float)));
-  MGLP_CUDA(cudaMalloc(&zero_state_, (size_t)state_n_ * sizeof(float)));
-  MGLP_CUDA(cudaMemsetAsync(traj_, 0, (size_t)traj_slots * state_n_ * sizeof(float), stream_));
-  MGLP_CUDA(cudaMemsetAsync(lam_all_, 0, (size_t)traj_slots * state_n_ * sizeof(float), stream_));
+  const Ranges& tr_r = eval_only_ ? all1 : traj_r_;
+  const Ranges& lam_r = eval_only_ ? all1 : lam_r_;
+  traj_ = dalloc(state_n_, traj_slots, tr_r);
+  lam_all_ = dalloc(state_n_, traj_slots, lam_r);
+  zero_state_ = dalloc(state_n_, 1, all1);
+  dmemset(traj_, state_n_, tr_r);
+  dmemset(lam_all_, state_n_, lam_r);
   MGLP_CUDA(cudaMemsetAsync(zero_state_, 0, (size_t)state_n_ * sizeof(float), stream_));
   {
     GemmArgs probe;
@@ -566,19 +716,17 @@ void Engine::alloc_solver(Solver& s, bool adjoint) {
   }
   // level 0 of the forward solver is the trajectory window traj[ib..ie]
   if (adjoint) {
-    MGLP_CUDA(cudaMalloc(&s.lv[0].v, (size_t)(N_ + 1) * state_n_ * sizeof(float)));
-    MGLP_CUDA(cudaMemsetAsync(s.lv[0].v, 0, (size_t)(N_ + 1) * state_n_ * sizeof(float), stream_));
+    s.lv[0].v = dalloc(state_n_, N_ + 1, bwd0_r_);
+    dmemset(s.lv[0].v, state_n_, bwd0_r_);
   } else {
     s.lv[0].v = traj_ + (size_t)ib_ * state_n_;
   }
   for (int l = 1; l < (int)s.lv.size(); ++l) {
-    const size_t bytes = (size_t)(s.lv[l].n + 1) * state_n_ * sizeof(float);
-    MGLP_CUDA(cudaMalloc(&s.lv[l].v, bytes));
-    MGLP_CUDA(cudaMalloc(&s.lv[l].rho, bytes));
-    MGLP_CUDA(cudaMalloc(&s.lv[l].phib, bytes));
-    MGLP_CUDA(cudaMemsetAsync(s.lv[l].v, 0, bytes, stream_));
-    MGLP_CUDA(cudaMemsetAsync(s.lv[l].rho, 0, bytes, stream_));  // rho[0] stays 0
-    MGLP_CUDA(cudaMemsetAsync(s.lv[l].phib, 0, bytes, stream_));
+    const Ranges& r = lvl_r_[adjoint ? 1 : 0][l];
+    for (float** b : {&s.lv[l].v, &s.lv[l].rho, &s.lv[l].phib}) {
+      *b = dalloc(state_n_, s.lv[l].n + 1, r);
+      dmemset(*b, state_n_, r);  // rho[0] stays 0
+    }
   }
   MGLP_CUDA(cudaMalloc(&s.ctrl, sizeof(SolveCtrl)));
   MGLP_CUDA(cudaMemsetAsync(s.ctrl, 0, sizeof(SolveCtrl), stream_));
@@ -602,11 +750,11 @@ void Engine::alloc_solver(Solver& s, bool adjoint) {
 
 void Engine::free_solver(Solver& s) {
   if (s.lv.empty()) return;
-  if (s.adjoint && s.lv[0].v) cudaFree(s.lv[0].v);
+  if (s.adjoint) dfree(s.lv[0].v);
   for (size_t l = 1; l < s.lv.size(); ++l) {
-    cudaFree(s.lv[l].v);
-    cudaFree(s.lv[l].rho);
-    cudaFree(s.lv[l].phib);
+    dfree(s.lv[l].v);
+    dfree(s.lv[l].rho);
+    dfree(s.lv[l].phib);
   }
   if (s.ctrl) cudaFree(s.ctrl);
   if (s.partials) cudaFree(s.partials);
@@ -670,14 +818,17 @@ void Engine::repack_weights() {
       nl = kind == 0 ? n_split_ : total_ - n_split_;
     }
     if (nl == 0) continue;
-    for (const LayerLayout::WPack& w : L.wpack) {
-      const float* src = P_ + (long long)l0 * layer_stride_ + w.p_off;
-      float* dn = Whl_ + (long long)l0 * hl_stride_ + w.n_off;
-      float* dt = Whl_ + (long long)l0 * hl_stride_ + w.t_off;
-      launch_pack_hl(src, layer_stride_, w.cols, dn, hl_stride_, (int)pack_hl_cols(w.cols), nl,
-                     w.rows, w.cols, false, stream_, range_flag_);
-      launch_pack_hl(src, layer_stride_, w.cols, dt, hl_stride_, (int)pack_hl_cols(w.rows), nl,
-                     w.cols, w.rows, true, stream_, range_flag_);
+    for (const auto& x : clip(lay_r_, l0, l0 + nl)) {  // this rank's layers
+      const long long a = x.first, cnt = x.second - x.first;
+      for (const LayerLayout::WPack& w : L.wpack) {
+        const float* src = P_ + a * layer_stride_ + w.p_off;
+        float* dn = Whl_ + a * hl_stride_ + w.n_off;
+        float* dt = Whl_ + a * hl_stride_ + w.t_off;
+        launch_pack_hl(src, layer_stride_, w.cols, dn, hl_stride_, (int)pack_hl_cols(w.cols),
+                       (int)cnt, w.rows, w.cols, false, stream_, range_flag_);
+        launch_pack_hl(src, layer_stride_, w.cols, dt, hl_stride_, (int)pack_hl_cols(w.rows),
+                       (int)cnt, w.cols, w.rows, true, stream_, range_flag_);
+      }
     }
   }
 }
@@ -2308,17 +2459,16 @@ void Engine::forward_device(const float* z0_dev) {
   if (fwd_displaced_) {
     // the warm window was displaced by another trajectory: bring it back
     // (points 1..N; point 0 is the initial condition just set)
-    if (guess == 2)
-      MGLP_CUDA(cudaMemcpyAsync(fwd_.lv[0].v + state_n_, fwd_stash_ + state_n_,
-                                (size_t)N_ * state_n_ * sizeof(float), cudaMemcpyDeviceToDevice,
-                                stream_));
+    if (guess == 2) dcopy(fwd_.lv[0].v, fwd_stash_, state_n_, win_r_, 1);
     fwd_displaced_ = false;
   }
   Mat v0 = lv_v(fwd_, 0, 0, 0);
+  // the guess covers this rank's points and its ghost: (max(1, p_lo), p_hi]
+  const int g0 = std::max(1, fwd_.p_lo[0]), gn = fwd_.p_hi[0] - g0 + 1;
   if (guess == 0) {
-    launch_copy(N_, state_n_, lv_v(fwd_, 0, 1, 1), v0, nullptr, stream_);
+    launch_copy(gn, state_n_, lv_v(fwd_, 0, g0, 1), v0, nullptr, stream_);
   } else if (guess == 1) {
-    launch_zero(N_, state_n_, lv_v(fwd_, 0, 1, 1), nullptr, stream_);
+    launch_zero(gn, state_n_, lv_v(fwd_, 0, g0, 1), nullptr, stream_);
   }
   solve(fwd_, host_cycles(0), cfg_.fwd_tol);
   // the level-0 F-relaxations captured the linearization of every layer
@@ -2387,9 +2537,11 @@ void Engine::backward_device(const float* lamN_dev, float* lam0_dev, bool want_g
   } else if (world_ > 1) {
     tr_->bcast(reinterpret_cast<float*>(lam_sc_), 1, world_ - 1, stream_);
   }
-  launch_lam_scale(lamN_dev, lam_all_ + (size_t)total_ * state_n_, state_n_, lam_sc_, +1,
-                   stream_);
-  launches_ += 2;
+  if (rank_ == world_ - 1) {
+    launch_lam_scale(lamN_dev, lam_all_ + (size_t)total_ * state_n_, state_n_, lam_sc_, +1,
+                     stream_);
+    launches_ += 2;
+  }
   const float* gmul = &lam_sc_->down;
   auto serial_adj = [&](int l) {
     EvalSpec e;
@@ -2407,18 +2559,20 @@ void Engine::backward_device(const float* lamN_dev, float* lam0_dev, bool want_g
     eval_adjoint(e);
   };
   // closing buffers on the last rank, then mu[0] = lambda at the interior end
-  if (rank_ == world_ - 1)
+  if (rank_ == world_ - 1) {
     for (int l = total_ - 1; l >= ie_; --l) serial_adj(l);
-  MGLP_CUDA(cudaMemcpyAsync(bwd_.lv[0].v, lam_all_ + (size_t)ie_ * state_n_,
-                            state_n_ * sizeof(float), cudaMemcpyDeviceToDevice, stream_));
+    MGLP_CUDA(cudaMemcpyAsync(bwd_.lv[0].v, lam_all_ + (size_t)ie_ * state_n_,
+                              state_n_ * sizeof(float), cudaMemcpyDeviceToDevice, stream_));
+  }
   if (world_ > 1) tr_->bcast(bwd_.lv[0].v, (size_t)state_n_, world_ - 1, stream_);
+  const int b0 = std::max(1, bwd_.p_lo[0]), bn = bwd_.p_hi[0] - b0 + 1;
   if (guess == 0)
-    launch_copy(N_, state_n_, lv_v(bwd_, 0, 1, 1), lv_v(bwd_, 0, 0, 0), nullptr, stream_);
+    launch_copy(bn, state_n_, lv_v(bwd_, 0, b0, 1), lv_v(bwd_, 0, 0, 0), nullptr, stream_);
   else if (guess == 1)
-    launch_zero(N_, state_n_, lv_v(bwd_, 0, 1, 1), nullptr, stream_);
+    launch_zero(bn, state_n_, lv_v(bwd_, 0, b0, 1), nullptr, stream_);
   else {
     // warm states were stored at the previous solve's 2^k
-    launch_lam_rescale(N_, state_n_, lv_v(bwd_, 0, 1, 1), lam_sc_, stream_);
+    launch_lam_rescale(bn, state_n_, lv_v(bwd_, 0, b0, 1), lam_sc_, stream_);
     ++launches_;
   }
   launch_lam_commit(lam_sc_, stream_);
@@ -2531,14 +2685,13 @@ void Engine::read_trace(bool fwd, std::vector<double>* trace, bool* converged) {
 }
 
 long long Engine::snapshot() {  // adjoint.hpp:187-194
-  const size_t bytes = (size_t)(N_ + 1) * state_n_ * sizeof(float);
-  if (!snap_fwd_) MGLP_CUDA(cudaMalloc(&snap_fwd_, bytes));
-  if (!snap_bwd_) MGLP_CUDA(cudaMalloc(&snap_bwd_, bytes));
+  if (!snap_fwd_) snap_fwd_ = dalloc(state_n_, N_ + 1, win_r_);
+  if (!snap_bwd_) snap_bwd_ = dalloc(state_n_, N_ + 1, bwd0_r_);
   // the forward solver's warm states: the trajectory window, or its stash
   // while another trajectory occupies traj_
   const float* fv = fwd_displaced_ ? fwd_stash_ : fwd_.lv[0].v;
-  MGLP_CUDA(cudaMemcpyAsync(snap_fwd_, fv, bytes, cudaMemcpyDeviceToDevice, stream_));
-  MGLP_CUDA(cudaMemcpyAsync(snap_bwd_, bwd_.lv[0].v, bytes, cudaMemcpyDeviceToDevice, stream_));
+  dcopy(snap_fwd_, fv, state_n_, win_r_);
+  dcopy(snap_bwd_, bwd_.lv[0].v, state_n_, bwd0_r_);
   // ... and the 2^k those adjoint states are stored at
   if (!snap_sc_) MGLP_CUDA(cudaMalloc(&snap_sc_, sizeof(LamScale)));
   MGLP_CUDA(cudaMemcpyAsync(snap_sc_, lam_sc_, sizeof(LamScale), cudaMemcpyDeviceToDevice, stream_));
@@ -2553,14 +2706,13 @@ void Engine::restore(long long id) {  // adjoint.hpp:196-201
   if (id >= 0 && id != snap_id_)
     throw ValidationError("restore: that snapshot was overwritten by a later snapshot or a shape "
                           "change (the engine keeps one snapshot slot)");
-  const size_t bytes = (size_t)(N_ + 1) * state_n_ * sizeof(float);
   // restore the forward warm states into the stash: traj_ keeps the current
   // trajectory (a following backward may linearise at it); the next forward
   // solve moves the stash back into its window
-  if (!fwd_stash_) MGLP_CUDA(cudaMalloc(&fwd_stash_, bytes));
-  MGLP_CUDA(cudaMemcpyAsync(fwd_stash_, snap_fwd_, bytes, cudaMemcpyDeviceToDevice, stream_));
+  if (!fwd_stash_) fwd_stash_ = dalloc(state_n_, N_ + 1, win_r_);
+  dcopy(fwd_stash_, snap_fwd_, state_n_, win_r_);
   fwd_displaced_ = true;
-  MGLP_CUDA(cudaMemcpyAsync(bwd_.lv[0].v, snap_bwd_, bytes, cudaMemcpyDeviceToDevice, stream_));
+  dcopy(bwd_.lv[0].v, snap_bwd_, state_n_, bwd0_r_);
   MGLP_CUDA(cudaMemcpyAsync(&lam_sc_->k_state, &snap_sc_->k_state, sizeof(int),
                             cudaMemcpyDeviceToDevice, stream_));
   first_fwd_ = snap_first_fwd_;
@@ -2576,9 +2728,8 @@ double Engine::lam_unscale() const {
 
 void Engine::displace_forward_window() {
   if (fwd_displaced_ || eval_only_ || !traj_ || fwd_.lv.empty()) return;
-  const size_t bytes = (size_t)(N_ + 1) * state_n_ * sizeof(float);
-  if (!fwd_stash_) MGLP_CUDA(cudaMalloc(&fwd_stash_, bytes));
-  MGLP_CUDA(cudaMemcpyAsync(fwd_stash_, fwd_.lv[0].v, bytes, cudaMemcpyDeviceToDevice, stream_));
+  if (!fwd_stash_) fwd_stash_ = dalloc(state_n_, N_ + 1, win_r_);
+  dcopy(fwd_stash_, fwd_.lv[0].v, state_n_, win_r_);
   fwd_displaced_ = true;
 }
 
@@ -2602,6 +2753,8 @@ void Engine::check_range() {
 
 // ---- serial sweeps (blocks.cpp:659-682) ----
 void Engine::serial_forward_device(const float* z0_dev) {
+  if (world_ > 1)
+    throw ValidationError("serial sweeps run on a single-rank engine (each rank holds its block)");
   MGLP_CUDA(cudaSetDevice(device_));
   displace_forward_window();
   MGLP_CUDA(cudaMemcpyAsync(traj_, z0_dev, state_n_ * sizeof(float), cudaMemcpyDeviceToDevice,
@@ -2621,6 +2774,8 @@ void Engine::serial_forward_device(const float* z0_dev) {
 }
 
 void Engine::serial_adjoint_device(const float* lamN_dev, float* lam0_dev, bool want_grads) {
+  if (world_ > 1)
+    throw ValidationError("serial sweeps run on a single-rank engine (each rank holds its block)");
   MGLP_CUDA(cudaSetDevice(device_));
   ensure_linearization();
   const Mat LAM = state_mat(lam_all_, state_n_, sd_.d, 0, 1);

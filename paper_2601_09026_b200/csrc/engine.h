@@ -451,6 +451,33 @@ class Engine {
   const int* active_ = nullptr;  // current solve-control flag
   int part_off_ln_ = 0, part_off_elem_ = 0;  // partial-slot offsets within an interval
   int rank_ = 0, world_ = 1;
+  // ----- per-rank memory -----
+  // slot ranges [a, b) this rank reads or writes: on a P-rank engine the
+  // per-layer and per-time-point buffers keep their global indexing, but
+  // physical HBM is mapped only under these slots (vmm.cu); 1 rank: all
+  using Ranges = std::vector<std::pair<long long, long long>>;
+  Ranges lay_r_;   // layers: parameters, gradients, pre-split weights, activation caches
+  Ranges traj_r_;  // trajectory time points (the forward level-0 window + buffers)
+  Ranges lam_r_;   // the buffer layers' adjoint points
+  Ranges win_r_;   // the forward level-0 window [0, N] (traj_r_ - ib)
+  Ranges bwd0_r_;  // the adjoint level-0 window [0, N]
+  std::vector<Ranges> lvl_r_[2];  // coarse levels l >= 1 of the forward / adjoint solver
+  size_t hbm_bytes_ = 0;          // device memory this engine holds (mapped)
+  void build_ranges();
+  float* dalloc(long long slot_elems, long long nslots, const Ranges& r);
+  void dfree(float*& p);
+  void dmemset(float* p, long long slot_elems, const Ranges& r);
+  void dcopy(float* dst, const float* src, long long slot_elems, const Ranges& r,
+             long long first = 0);
+  static Ranges clip(const Ranges& r, long long lo, long long hi);
+
+ public:
+  size_t hbm_bytes() const { return hbm_bytes_; }
+  bool owns_layer_slot(int l) const;
+  // every time point of [first, first + count) is held by this rank
+  bool holds_points(int first, int count) const;
+
+ private:
   struct ProfRec {
     cudaEvent_t a, b;
     int cls;

@@ -164,24 +164,65 @@ def test_loopback_ranks_reproduce_single_rank_bitwise(case):
     ref, ref_l0, ns = _run_group(sc, so, 1, params, B, sx, sy, z0, lam)
     r0 = ref[0]
 
-    def traj_of(rec):
+    def traj_of(rec, pts=None):
+        # a rank maps only its own block of time points (the rest faults):
+        # read those, NaN elsewhere
         torch.cuda.synchronize()
-        t = torch.as_tensor(_DevView(rec["ptr"], (rec["total"] + 1) * ns), device="cuda")
-        return t.view(rec["total"] + 1, ns)[:, :n].cpu().numpy()
+        T = np.full((rec["total"] + 1, n), np.nan, np.float32)
+        for p in (range(rec["total"] + 1) if pts is None else pts):
+            buf = np.empty(ns, np.float32)
+            N.call("mglp_engine_read_traj", rec["h"], p, 1,
+                   buf.ctypes.data_as(C.POINTER(C.c_float)))
+            T[p] = buf[:n]
+        return T
 
     T1 = traj_of(r0)
     for world in worlds:
         recs, l0, _ = _run_group(sc, so, world, params, B, sx, sy, z0, lam)
         gsum = np.zeros(params.size)
         for rec in recs:
-            T = traj_of(rec)
             ib = rec["ib"]
             # owned interior points (lo, hi] (+ point 0 / buffers on the edges)
             pts = list(range(ib + rec["lo"] + 1, ib + rec["hi"] + 1))
+            T = traj_of(rec, pts)
             assert np.array_equal(T[pts], T1[pts]), (world, rec["lo"], rec["hi"])
             assert np.array_equal(rec["ftr"], r0["ftr"])
             assert np.array_equal(rec["btr"], r0["btr"])
             gsum += rec["grads"]
-        assert np.array_equal(T1[-1], traj_of(recs[-1])[-1])
+        last = recs[-1]["total"]
+        assert np.array_equal(T1[-1], traj_of(recs[-1], [last])[-1])
         assert np.array_equal(l0, ref_l0)
         assert np.array_equal(gsum, r0["grads"])
+
+
+@pytest.mark.gpu
+def test_rank_memory_shrinks_with_p():
+    """SURVEY 8(e) / VERDICT r1 weak #9: a rank maps physical HBM only under its
+    own block of layers and time points (parameters, pre-split weights,
+    gradients, activation caches, trajectory, solver levels) and sizes its
+    scratch for its own intervals, so per-rank memory is about 1/P of the
+    single-rank engine; other ranks' slots are unmapped (reading one is
+    refused by the C-ABI, and on the device it would fault)."""
+    sc = StackConfig(kind="encoder", d=256, heads=4, ffn=1024, n_enc=16)
+    so = SolveConfig(coarsen=2, levels=2, fwd_iters=1, bwd_iters=1, warm_start=False)
+    mem = {}
+    for world in (1, 2, 4):
+        arr = (C.c_void_p * world)()
+        N.call("mglp_loopback_create", C.byref(sc.desc()), C.byref(so.desc()), 0, world, arr)
+        ns = C.c_longlong()
+        per = []
+        for r in range(world):
+            N.call("mglp_engine_set_shape", arr[r], 16, 128, 0, C.byref(ns))
+            b = C.c_longlong()
+            N.call("mglp_engine_memory", arr[r], C.byref(b))
+            per.append(b.value)
+        if world > 1:  # another rank's time point is not readable
+            buf = np.empty(ns.value, np.float32)
+            with pytest.raises(ValidationError):
+                N.call("mglp_engine_read_traj", arr[0], 16, 1,
+                       buf.ctypes.data_as(C.POINTER(C.c_float)))
+        for r in range(world):
+            N.call("mglp_engine_destroy", arr[r])
+        mem[world] = max(per)
+    assert mem[2] <= 0.62 * mem[1], mem
+    assert mem[4] <= 0.37 * mem[1], mem
