@@ -7,6 +7,10 @@
 //   swap_trainer <out_prefix> kind task d heads ffn n_enc n_dec vocab seq
 //                train val batch epochs mode cf levels fwd bwd probe thr policy
 //                cap use_probe_grad val_every dropout
+#include <execinfo.h>
+#include <unistd.h>
+
+#include <csignal>
 #include <cstdio>
 #include <cstdlib>
 #include <fstream>
@@ -16,7 +20,16 @@
 
 using namespace mglp;
 
+static void on_fault(int sig) {
+  void* frames[64];
+  const int n = backtrace(frames, 64);
+  std::fprintf(stderr, "signal %d\n", sig);
+  backtrace_symbols_fd(frames, n, STDERR_FILENO);
+  std::_Exit(128 + sig);
+}
+
 int main(int argc, char** argv) {
+  std::signal(SIGSEGV, on_fault);
   if (argc != 27) {
     std::fprintf(stderr, "usage: see swap_trainer.cpp (%d args)\n", argc);
     return 64;

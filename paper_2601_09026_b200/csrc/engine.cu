@@ -214,6 +214,19 @@ void Engine::build_ranges() {
     add(bwd0_r_, 0, 1);
     add(bwd0_r_, tp * per, tp * per + per + 1);
   }
+  // sorted, disjoint, merged (the pieces overlap at the ghosts and point 0)
+  auto norm = [](Ranges& v) {
+    std::sort(v.begin(), v.end());
+    Ranges o;
+    for (const auto& x : v) {
+      if (!o.empty() && x.first <= o.back().second)
+        o.back().second = std::max(o.back().second, x.second);
+      else
+        o.push_back(x);
+    }
+    v = o;
+  };
+  for (Ranges* v : {&lay_r_, &traj_r_, &lam_r_, &win_r_, &bwd0_r_}) norm(*v);
   for (int adj = 0; adj < 2; ++adj) {
     lvl_r_[adj].assign(std::max(cfg_.levels, 2), Ranges{});
     long long n = N_;
@@ -227,6 +240,7 @@ void Engine::build_ranges() {
         add(v, 0, 1);
         add(v, tp * pl, tp * pl + pl + 1);
       }
+      norm(v);
     }
   }
 }
@@ -701,7 +715,7 @@ void Engine::set_shape(int batch, int s_x, int s_y) {
   std::fill(cache_valid_.begin(), cache_valid_.end(), 0);
   first_fwd_ = first_bwd_ = true;
   fwd_displaced_ = false;
-  snap_id_ = 0;  // the snapshot slot was freed with the old shape
+  if (!snap_empty_) snap_id_ = 0;  // the slot's states were freed with the old shape
   MGLP_CUDA(cudaStreamSynchronize(stream_));
 }
 
@@ -2540,8 +2554,11 @@ void Engine::backward_device(const float* lamN_dev, float* lam0_dev, bool want_g
   if (rank_ == world_ - 1) {
     launch_lam_scale(lamN_dev, lam_all_ + (size_t)total_ * state_n_, state_n_, lam_sc_, +1,
                      stream_);
-    launches_ += 2;
+  } else {
+    // no lambda_N here (its slot is another rank's): publish the factor only
+    launch_lam_scale(nullptr, nullptr, 0, lam_sc_, +1, stream_);
   }
+  launches_ += 2;
   const float* gmul = &lam_sc_->down;
   auto serial_adj = [&](int l) {
     EvalSpec e;
@@ -2685,6 +2702,15 @@ void Engine::read_trace(bool fwd, std::vector<double>* trace, bool* converged) {
 }
 
 long long Engine::snapshot() {  // adjoint.hpp:187-194
+  if (!traj_ || fwd_.lv.empty()) {
+    // nothing solved yet (no shape): the snapshot is the first-call flags
+    snap_first_fwd_ = first_fwd_;
+    snap_first_bwd_ = first_bwd_;
+    snap_empty_ = true;
+    snap_id_ = ++snap_seq_;
+    return snap_id_;
+  }
+  snap_empty_ = false;
   if (!snap_fwd_) snap_fwd_ = dalloc(state_n_, N_ + 1, win_r_);
   if (!snap_bwd_) snap_bwd_ = dalloc(state_n_, N_ + 1, bwd0_r_);
   // the forward solver's warm states: the trajectory window, or its stash
@@ -2702,10 +2728,15 @@ long long Engine::snapshot() {  // adjoint.hpp:187-194
 }
 
 void Engine::restore(long long id) {  // adjoint.hpp:196-201
-  if (!snap_fwd_ || snap_id_ == 0) throw ValidationError("restore: no snapshot taken");
+  if (snap_id_ == 0) throw ValidationError("restore: no snapshot taken");
   if (id >= 0 && id != snap_id_)
     throw ValidationError("restore: that snapshot was overwritten by a later snapshot or a shape "
                           "change (the engine keeps one snapshot slot)");
+  if (snap_empty_) {  // taken before any solve: only the first-call flags
+    first_fwd_ = snap_first_fwd_;
+    first_bwd_ = snap_first_bwd_;
+    return;
+  }
   // restore the forward warm states into the stash: traj_ keeps the current
   // trajectory (a following backward may linearise at it); the next forward
   // solve moves the stash back into its window

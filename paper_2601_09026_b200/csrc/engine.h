@@ -441,6 +441,7 @@ class Engine {
   float* snap_fwd_ = nullptr;
   float* snap_bwd_ = nullptr;
   long long snap_id_ = 0;       // id of the snapshot in the slot (0: none)
+  bool snap_empty_ = false;     // taken before any shape / solve: flags only
   long long snap_seq_ = 0;
   float* fwd_stash_ = nullptr;  // displaced forward warm window (N+1 states)
   bool fwd_displaced_ = false;
