@@ -204,7 +204,9 @@ mglp_status mglp_engine_take_launch_count(mglp_engine* e, long long* n);
 mglp_status mglp_engine_profile(mglp_engine* e, int enable);
 mglp_status mglp_engine_profile_read(mglp_engine* e, double* ms, double* flops, double* bytes,
                                      long long* launches);
-/* per-launch rows (7 doubles each: class, M, N, K, batch, flops, ms) */
+/* per-launch rows (8 doubles each: class, M, N, K, batch, flops, ms, variant; variant
+ * for GEMMs = epilogue kind + 16 A pre-split + 32 B pre-split + 64 A MN-major +
+ * 128 B MN-major, -1 otherwise) */
 mglp_status mglp_engine_profile_dump(mglp_engine* e, double* rows, int max_rows, int* n);
 
 /* ---- multi-GPU: layer blocks over ranks ----
@@ -338,7 +340,9 @@ mglp_status mglp_engine_lipschitz(mglp_engine* e, int samples, double delta_scal
  * per head, instead of the probabilities); dh 32 or 64 (else status 1).
  * causal bit 0: causal mask; bit 1 (sq = skv = 128 only): P is kept in the
  * pre-split form the engine uses at s = 128 (the forward's hi|lo' tiles, 64
- * KiB per head; not probabilities). The reference's attention /
+ * KiB per head; not probabilities); bit 2 (dh = 64, s <= 128): Q, K, V and dO
+ * are given in the head-split pre-split form the engine's GEMMs write (per
+ * 64 columns: 64 fp16 hi, 64 fp16 lo' = fp16((x - hi) 2^11)). The reference's attention /
  * vjp_attention (blocks.cpp:142-236). Synchronous. */
 mglp_status mglp_test_attention(int B, int H, int sq, int skv, int dh, int causal, const float* Q,
                                 const float* K, const float* V, int ld, float* O, float* P,

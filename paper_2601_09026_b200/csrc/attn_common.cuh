@@ -281,9 +281,9 @@ struct AttnTma {
 enum { TQ = 0, TK = 1, TV = 2, TP = 3, TDO = 4 };
 
 __device__ __forceinline__ void tma_box(uint32_t dst, const AttnTma& t, int which, int g, int b,
-                                        int h, uint64_t* bar, int row0 = 0) {
+                                        int h, uint64_t* bar, int row0 = 0, int col = 0) {
   int c[5];
-  tma_coords(t.op[which], 0, row0, g, b, h, c);
+  tma_coords(t.op[which], col, row0, g, b, h, c);
   asm volatile(
       "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes"
       " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(dst),
@@ -292,6 +292,16 @@ __device__ __forceinline__ void tma_box(uint32_t dst, const AttnTma& t, int whic
       : "memory");
 }
 
+
+// A head-split pre-split operand (AttnArgs::qkv_hs / do_hs): its hi and lo'
+// halves ([rows][32] fp32-sized boxes, SWIZZLE_128B) land by TMA directly as
+// the tile pair X (no staging, no conversion): 2 x 128 rows x 128 B
+__device__ __forceinline__ void tma_pair(const Opnd& X, const AttnTma& t, int which, int g, int b,
+                                         int h, uint64_t* bar, int row0 = 0) {
+  tma_box(X.hi, t, which, g, b, h, bar, row0, 0);
+  tma_box(X.lo, t, which, g, b, h, bar, row0, 32);
+}
+constexpr uint32_t kHsBytes = 2 * 128 * 128;  // one operand tile pair by TMA
 
 }  // namespace attn
 }  // namespace mglp

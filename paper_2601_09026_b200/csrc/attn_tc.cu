@@ -77,9 +77,17 @@ __global__ void __launch_bounds__(kThreads, 2) attn_fwd_kernel(const __grid_cons
   uint32_t* tslot = reinterpret_cast<uint32_t*>(xch + 256);
   const int nprob = a.G * a.Bb * a.H;
 
+  const bool hs = a.qkv_hs != 0;
   auto issue_loads = [&](int z) {  // one thread
     int g, b, h;
     problem_of(a, z, g, b, h);
+    if (hs) {  // pre-split: straight into the tiles (rows >= s zero-filled)
+      mbar_expect_tx(st_full, 3 * kHsBytes);
+      tma_pair(Qt, tm, TQ, g, b, h, st_full);
+      tma_pair(Kt, tm, TK, g, b, h, st_full);
+      tma_pair(Vt, tm, TV, g, b, h, st_full);
+      return;
+    }
     mbar_expect_tx(st_full, (uint32_t)((sq + 2 * skv) * dh * 4));
     tma_box(Qt.hi, tm, TQ, g, b, h, st_full);
     tma_box(Kt.hi, tm, TK, g, b, h, st_full);
@@ -108,13 +116,15 @@ __global__ void __launch_bounds__(kThreads, 2) attn_fwd_kernel(const __grid_cons
     problem_of(a, z, g, b, h);
     const uint32_t ph = it & 1;
     mbar_wait(st_full, ph);
-    conv_inplace(Qt.hi, sq, 128, dh, tid, kThreads, amax);
-    conv_inplace(Kt.hi, skv, skv16, dh, tid, kThreads, amax);
-    conv_inplace(Vt.hi, skv, skv16, dh, tid, kThreads, amax);
-    fence_async_smem();
-    tc_before();
-    __syncthreads();
-    tc_after();
+    if (!hs) {
+      conv_inplace(Qt.hi, sq, 128, dh, tid, kThreads, amax);
+      conv_inplace(Kt.hi, skv, skv16, dh, tid, kThreads, amax);
+      conv_inplace(Vt.hi, skv, skv16, dh, tid, kThreads, amax);
+      fence_async_smem();
+      tc_before();
+      __syncthreads();
+      tc_after();
+    }
     if (tid == 0) {
       mma3(tmem, tmem + 128, Qt, Kt, skv16, dh >> 4);  // S
       mma_commit<1>(s_bar);
@@ -243,13 +253,33 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
   uint32_t* tslot = reinterpret_cast<uint32_t*>(xch + 256);
   const int nprob = a.G * a.Bb * a.H;
 
+  // pre-split operands (qkv_hs / do_hs) land straight in their tiles, once
+  // those are free; fp32 ones go through the staging and are converted
+  const bool hsq = a.qkv_hs != 0, hsd = a.do_hs != 0;
   auto load_dov = [&](int z) {
     int g, b, h;
     problem_of(a, z, g, b, h);
     if (lane == 0) {
-      mbar_expect_tx(st_full, (uint32_t)((sq + skv) * dh * 4));
-      tma_box(stg, tm, TDO, g, b, h, st_full);
-      tma_box(st2, tm, TV, g, b, h, st_full);
+      mbar_expect_tx(st_full, (hsd ? kHsBytes : (uint32_t)(sq * dh * 4)) +
+                                  (hsq ? kHsBytes : (uint32_t)(skv * dh * 4)));
+      if (hsd) tma_pair(dOk, tm, TDO, g, b, h, st_full);
+      else tma_box(stg, tm, TDO, g, b, h, st_full);
+      if (hsq) tma_pair(Vk, tm, TV, g, b, h, st_full);
+      else tma_box(st2, tm, TV, g, b, h, st_full);
+    }
+    __syncwarp();
+  };
+  auto load_qk = [&](int g, int b, int h) {
+    if (lane == 0) {
+      if (hsq) {
+        mbar_expect_tx(st_full, 2 * kHsBytes);
+        tma_pair(Qm, tm, TQ, g, b, h, st_full);
+        tma_pair(Km, tm, TK, g, b, h, st_full);
+      } else {
+        mbar_expect_tx(st_full, (uint32_t)((sq + skv) * dh * 4));
+        tma_box(stg, tm, TQ, g, b, h, st_full);
+        tma_box(st2, tm, TK, g, b, h, st_full);
+      }
     }
     __syncwarp();
   };
@@ -286,8 +316,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
     // (1) dO, V -> T0
     mbar_wait(st_full, stp);
     stp ^= 1;
-    conv_rows(stg, sq, 128, dh, dOk.hi, dOk.lo, tid, kThreads, amax);
-    conv_rows(st2, skv, skv16, dh, Vk.hi, Vk.lo, tid, kThreads, amax);
+    if (!hsd) conv_rows(stg, sq, 128, dh, dOk.hi, dOk.lo, tid, kThreads, amax);
+    if (!hsq) conv_rows(st2, skv, skv16, dh, Vk.hi, Vk.lo, tid, kThreads, amax);
     fence_async_smem();  // staging reads ordered before the bulk copies that reuse it
     __syncthreads();
     if (phl) {
@@ -311,14 +341,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
     tc_before();
     __syncthreads();
     tc_after();
-    if (warp == 0) {
-      if (lane == 0) {
-        mbar_expect_tx(st_full, (uint32_t)((sq + skv) * dh * 4));
-        tma_box(stg, tm, TQ, g, b, h, st_full);
-        tma_box(st2, tm, TK, g, b, h, st_full);
-      }
-      __syncwarp();
-    }
+    if (warp == 0 && !hsq) load_qk(g, b, h);  // into the staging
     if (tid == 0) {
       mma3(tmem, tmem + 128, dOk, Vk, skv16, dh >> 4);        // dP = dO V^T
       mma3(tmem + 256, tmem + 384, Pm, dOm, dh, sq16 >> 4);  // dV = P^T dO
@@ -375,6 +398,9 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
       xch[half * 128 + r] = t;
       tc_before();
       __syncthreads();  // also: dP / dV MMAs done -> T0 may take dS
+      // every P half-row is in registers and the dV MMA has read P: pre-split
+      // Q, K go straight into T1
+      if (warp == 0 && hsq) load_qk(g, b, h);
       t = xch[r] + xch[128 + r];
       if (any) {
 #pragma unroll
@@ -391,13 +417,17 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
     // (4) Q, K -> T1 (the dV MMA is done)
     mbar_wait(st_full, stp);
     stp ^= 1;
-    conv_rows(stg, sq, sq16, dh, Qm.hi, Qm.lo, tid, kThreads, amax);
-    conv_rows(st2, skv, skv16, dh, Km.hi, Km.lo, tid, kThreads, amax);
+    if (!hsq) {
+      conv_rows(stg, sq, sq16, dh, Qm.hi, Qm.lo, tid, kThreads, amax);
+      conv_rows(st2, skv, skv16, dh, Km.hi, Km.lo, tid, kThreads, amax);
+    }
     fence_async_smem();
     tc_before();
     __syncthreads();
     tc_after();
-    if (warp == 0 && z + (int)gridDim.x < nprob) load_dov(z + gridDim.x);
+    // the staging is free (and T0 is not: the dS tiles feed dQ / dK)
+    const bool next = z + (int)gridDim.x < nprob;
+    if (warp == 0 && next && !hsq && !hsd) load_dov(z + gridDim.x);
     if (tid == 0) {
       mma3(tmem, tmem + 64, dSk, Km, dh, skv16 >> 4);         // dQ = dS K
       mma3(tmem + 128, tmem + 192, dSm, Qm, dh, sq16 >> 4);   // dK = dS^T Q
@@ -410,8 +440,10 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
     mbar_wait(m_bar, mp);
     mp ^= 1;
     tc_after();
+    // T0 (dS) is free: pre-split dO / V go straight in under this epilogue
+    if (warp == 0 && next && (hsq || hsd)) load_dov(z + gridDim.x);
     // T1 (Q | K) is free: the next problem's P streams in under this epilogue
-    if (phl && tid == 0 && z + (int)gridDim.x < nprob) load_p(z + gridDim.x);
+    if (phl && tid == 0 && next) load_p(z + gridDim.x);
     rows_out_hl(trow, trow + 64, a.dQ.ok() ? a.dQ.at(g, b, h) : nullptr,
                 a.dQhl.ok() ? a.dQhl.at(g, b, h) : nullptr, a.dQhl.ok() ? a.dQhl.ld : a.dQ.ld, r,
                 sq, half * (dh >> 1), dh >> 1, a.scale, amax);
@@ -442,15 +474,18 @@ int num_sms() {
 
 AttnTma maps(const AttnArgs& a, bool backward) {
   AttnTma t{};
-  auto mk = [&](int which, const Mat& m, int rows, int cols) {
-    t.m[which] = tc_make_map(m, a.G, a.Bb, a.H, rows, cols, rows, cols, false, &t.op[which]);
+  auto mk = [&](int which, const Mat& m, int rows, int cols, bool hs) {
+    // head-split pre-split: [128][32] boxes (hi, lo' halves) in the tiles'
+    // SWIZZLE_128B layout; rows >= s arrive zero-filled
+    t.m[which] = hs ? tc_make_map(m, a.G, a.Bb, a.H, rows, cols, 128, 32, true, &t.op[which])
+                    : tc_make_map(m, a.G, a.Bb, a.H, rows, cols, rows, cols, false, &t.op[which]);
   };
-  mk(TQ, a.Q, a.sq, a.dh);
-  mk(TK, a.K, a.skv, a.dh);
-  mk(TV, a.V, a.skv, a.dh);
+  mk(TQ, a.Q, a.sq, a.dh, a.qkv_hs);
+  mk(TK, a.K, a.skv, a.dh, a.qkv_hs);
+  mk(TV, a.V, a.skv, a.dh, a.qkv_hs);
   if (backward) {
-    mk(TP, a.P, a.sq, a.skv);
-    mk(TDO, a.dO, a.sq, a.dh);
+    mk(TP, a.P, a.sq, a.skv, false);
+    mk(TDO, a.dO, a.sq, a.dh, a.do_hs);
   }
   return t;
 }
@@ -461,6 +496,7 @@ bool attn_tc_supported(const AttnArgs& a, bool backward) {
   if (a.sq < 1 || a.skv < 1 || a.sq > 128 || a.skv > 128) return false;
   if (a.sq % 8 || a.skv % 8) return false;
   if (a.dh != 32 && a.dh != 64) return false;
+  if ((a.qkv_hs || a.do_hs) && a.dh != 64) return false;
   if (!aligned(a.Q) || !aligned(a.K) || !aligned(a.V) || !aligned(a.O) || !aligned(a.P))
     return false;
   if (backward && (!aligned(a.dO) || !aligned(a.dQ) || !aligned(a.dK) || !aligned(a.dV) || !a.P.ok()))

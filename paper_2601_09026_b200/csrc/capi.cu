@@ -1025,9 +1025,11 @@ mglp_status mglp_test_attention(int B, int H, int sq, int skv, int dh, int causa
     need(O, "O");
     need(P, "P");
     const int p_hl = (causal >> 1) & 1;  // bit 1: P kept pre-split (s = 128)
+    const int hs = (causal >> 2) & 1;    // bit 2: Q, K, V, dO head-split pre-split
     causal &= 1;
     AttnArgs a = attn_args(B, H, sq, skv, dh, causal, Q, K, V, ld, O, P, dO, dQ, dK, dV);
     a.p_hl = p_hl;
+    a.qkv_hs = a.do_hs = hs;
     const bool bwd = dO != nullptr;
     const bool shortp = attn_tc_supported(a, bwd);
     if (!shortp && !attn_long_supported(a, bwd))

@@ -240,6 +240,31 @@ __device__ __forceinline__ void st_hl1(float* row, int col, float v, float& amax
   b[0] = h;
   b[32] = l;
 }
+// Head-split pre-split rows (attention operands Q, K, V, dO with dh = 64):
+// every 64-column group (one head) is stored as 64 fp16 hi then 64 fp16 lo'
+// (256 bytes, the size of its 64 fp32 values), so a [rows][64] box of each
+// half lands by TMA directly as the attention kernels' SWIZZLE_128B hi / lo'
+// tiles (attn_common.cuh).
+__device__ __forceinline__ void st_hs4(float* row, int col, float4 v, float& amax) {
+  const __half2 h01 = __floats2half2_rn(v.x, v.y), h23 = __floats2half2_rn(v.z, v.w);
+  const float2 f01 = __half22float2(h01), f23 = __half22float2(h23);
+  const __half2 l01 = __floats2half2_rn((v.x - f01.x) * 2048.f, (v.y - f01.y) * 2048.f);
+  const __half2 l23 = __floats2half2_rn((v.z - f23.x) * 2048.f, (v.w - f23.y) * 2048.f);
+  amax = fmaxf(amax, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
+  char* b = reinterpret_cast<char*>(row) + (col >> 6) * 256 + (col & 63) * 2;
+  *reinterpret_cast<uint2*>(b) =
+      make_uint2(*reinterpret_cast<const uint32_t*>(&h01), *reinterpret_cast<const uint32_t*>(&h23));
+  *reinterpret_cast<uint2*>(b + 128) =
+      make_uint2(*reinterpret_cast<const uint32_t*>(&l01), *reinterpret_cast<const uint32_t*>(&l23));
+}
+__device__ __forceinline__ void st_hs1(float* row, int col, float v, float& amax) {
+  const __half h = __float2half_rn(v);
+  const __half l = __float2half_rn((v - __half2float(h)) * 2048.f);
+  amax = fmaxf(amax, fabsf(v));
+  __half* b = reinterpret_cast<__half*>(reinterpret_cast<char*>(row) + (col >> 6) * 256) + (col & 63);
+  b[0] = h;
+  b[64] = l;
+}
 // a finite value beyond the fp16 split range (the GEMM converters' flag)
 __device__ __forceinline__ void hl_range_check(float amax, int* flag) {
   if (flag && amax >= 65520.f && amax <= 3.402823466e38f) atomicOr(flag, 1);
@@ -273,6 +298,9 @@ struct EpiArgs {
   // adjoint's exact 2^-k, LamScale::down, read on the device)
   const float* gscale_mul = nullptr;
   float alpha = 1.f;  // EPI_STORE: out1 = alpha*acc (+ bias)
+  // EPI_STORE: out1 is written in the head-split pre-split form (st_hs4; the
+  // fused attention's Q, K, V / dO operands), range-checked into range_flag
+  int hs = 0;
   Combine cmb;  // EPI_FINAL
   // EPI_BIAS_GELU: gelu(h) also (or only) as a pre-split hi|lo' buffer for
   // the next GEMM's A operand (see st_hl4); range_flag for its split
@@ -353,7 +381,16 @@ __device__ __forceinline__ double epilogue_rowv(const EpiArgs& e, int g, int b, 
     case EPI_STORE: {
 #pragma unroll
       for (int i = 0; i < W; ++i) o[i] = bias ? e.alpha * acc[i] + bv[i] : e.alpha * acc[i];
-      st4(e.out1.at(g, b, h) + (long long)row * e.out1.ld + col0, o);
+      if (e.hs) {
+        float amax = 0.f;
+        float* hr = e.out1.at(g, b, h) + (long long)row * e.out1.ld;
+#pragma unroll
+        for (int i = 0; i < W; i += 4)
+          st_hs4(hr, col0 + i, make_float4(o[i], o[i + 1], o[i + 2], o[i + 3]), amax);
+        hl_range_check(amax, e.range_flag);
+      } else {
+        st4(e.out1.at(g, b, h) + (long long)row * e.out1.ld + col0, o);
+      }
     } break;
     case EPI_BIAS_ADD2: {
       float a2[W];
@@ -443,7 +480,13 @@ __device__ __forceinline__ double epilogue_4x4(const EpiArgs& e, int g, int b, i
         const float4 a = acc[i];
         float4 o = make_float4(al * a.x, al * a.y, al * a.z, al * a.w);
         if (e.bias.ok()) o = add(o, bv);
-        st4g(e.out1.at(g, b, h) + (long long)rows[i] * e.out1.ld + col, o);
+        if (e.hs) {
+          float amax = 0.f;
+          st_hs4(e.out1.at(g, b, h) + (long long)rows[i] * e.out1.ld, col, o, amax);
+          hl_range_check(amax, e.range_flag);
+        } else {
+          st4g(e.out1.at(g, b, h) + (long long)rows[i] * e.out1.ld + col, o);
+        }
       }
     } break;
     case EPI_BIAS_ADD2: {
@@ -563,8 +606,16 @@ __device__ __forceinline__ double epilogue_row(const EpiArgs& e, int g, int b, i
   const float* bias = e.bias.ok() ? e.bias.at(g) : nullptr;
   switch (e.kind) {
     case EPI_STORE: {
-      float* o = e.out1.at(g, b, h) + (long long)row * e.out1.ld + col0;
       const float al = e.alpha;
+      if (e.hs) {
+        float* hr = e.out1.at(g, b, h) + (long long)row * e.out1.ld;
+        float amax = 0.f;
+        for (int i = 0; i < n; ++i)
+          st_hs1(hr, col0 + i, bias ? al * acc[i] + bias[col0 + i] : al * acc[i], amax);
+        hl_range_check(amax, e.range_flag);
+        break;
+      }
+      float* o = e.out1.at(g, b, h) + (long long)row * e.out1.ld + col0;
       for (int i = 0; i < n; ++i) o[i] = bias ? al * acc[i] + bias[col0 + i] : al * acc[i];
     } break;
     case EPI_BIAS_ADD2: {

@@ -855,7 +855,10 @@ Mat Engine::grad(long long off, int ld, int layer0, int step) const {
 void Engine::gemm(GemmArgs g) {
   ++launches_;
   const double flops = 2.0 * g.G * g.Bb * g.H * (double)g.M * g.N * g.K;
-  prof_shape_ = {g.M, g.N, g.K, g.G * g.Bb * g.H};
+  // variant (diagnostics): epilogue kind | 16 A pre-split | 32 B pre-split | 64 A MN | 128 B MN
+  prof_shape_ = {g.M, g.N, g.K, g.G * g.Bb * g.H,
+                 g.ep.kind + (g.Ahl.ok() ? 16 : 0) + (g.Bhl.ok() ? 32 : 0) + (g.a_mn ? 64 : 0) +
+                     (g.b_mn ? 128 : 0)};
   g.range_flag = range_flag_;
   timed(PROF_GEMM, flops, 0.0, [&] {
 #ifdef MGLP_GEMM_SIMT
@@ -956,8 +959,17 @@ Mat Engine::dgrad_hl(int G, int which, int cols) const {
   return off ? Mat{} : hl_mat(G, which, cols);
 }
 
+bool Engine::attn_hs(int sq, int skv) const {
+  static const bool off = [] {
+    const char* e = getenv("MGLP_NO_ATTN_HS");
+    return e && atoi(e) != 0;
+  }();
+  return !off && use_fused_attn() && sd_.d == 64 * sd_.heads && sq <= 128 && skv <= 128 &&
+         sq % 8 == 0 && skv % 8 == 0;
+}
+
 bool Engine::attention_fwd(int G, Mat Q, Mat K, Mat V, Mat O, Mat P, int sq, int skv,
-                           bool causal, bool keep_p, Mat Ohl) {
+                           bool causal, bool keep_p, Mat Ohl, bool qkv_hs) {
   const int H = sd_.heads, dh = sd_.d / H;
   auto heads = [&](Mat m, int s) {
     m.bstride = (long long)s * m.ld;
@@ -989,6 +1001,7 @@ bool Engine::attention_fwd(int G, Mat Q, Mat K, Mat V, Mat O, Mat P, int sq, int
     at.P = P;
     at.range_flag = range_flag_;
     at.p_hl = p_hl_ok(sq, skv, P) ? 1 : 0;
+    at.qkv_hs = qkv_hs ? 1 : 0;
     const double fl = 4.0 * G * B_ * H * (double)sq * skv * dh * (causal ? 0.5 : 1.0);
     // O pre-split for the O-projection; fp32 O only where the backward reads it
     auto with_hl = [&] {
@@ -1006,6 +1019,7 @@ bool Engine::attention_fwd(int G, Mat Q, Mat K, Mat V, Mat O, Mat P, int sq, int
       timed(PROF_ATTN, fl, 0.0, [&] { launch_attn_fwd(at, active_, stream_); });
       return hl;
     }
+    if (qkv_hs) throw ContractViolation("attention: pre-split Q/K/V need the fused s <= 128 kernel");
     if (use_long_attn() && attn_long_supported(at, false)) {
       // longer sequences: P is recomputed by the backward from per-row
       // statistics stored in the P slot (attn_long.cu)
@@ -1057,7 +1071,7 @@ bool Engine::attention_fwd(int G, Mat Q, Mat K, Mat V, Mat O, Mat P, int sq, int
 
 bool Engine::attention_bwd(int G, Mat Q, Mat K, Mat V, Mat P, Mat O, Mat dO, Mat dP, Mat dQ, Mat dK,
                            Mat dV, int sq, int skv, bool causal, Mat dQhl, Mat dKhl, Mat dVhl,
-                           bool keep32) {
+                           bool keep32, bool qkv_hs, bool do_hs) {
   const int H = sd_.heads, dh = sd_.d / H;
   const float scale = (float)(1.0 / std::sqrt((double)dh));
   auto heads = [&](Mat m, int s) {
@@ -1100,6 +1114,8 @@ bool Engine::attention_bwd(int G, Mat Q, Mat K, Mat V, Mat P, Mat O, Mat dO, Mat
     at.dV = dV;
     at.range_flag = range_flag_;
     at.p_hl = p_hl_ok(sq, skv, P) ? 1 : 0;  // as the forward stored it
+    at.qkv_hs = qkv_hs ? 1 : 0;
+    at.do_hs = do_hs ? 1 : 0;
     const double fl = 8.0 * G * B_ * H * (double)sq * skv * dh;
     // pre-split gradients for the QKV dgrad; fp32 only where a weight
     // gradient reads them
@@ -1118,6 +1134,8 @@ bool Engine::attention_bwd(int G, Mat Q, Mat K, Mat V, Mat P, Mat O, Mat dO, Mat
       timed(PROF_ATTN, fl, 0.0, [&] { launch_attn_bwd(at, active_, stream_); });
       return hl;
     }
+    if (qkv_hs || do_hs)
+      throw ContractViolation("attention: pre-split operands need the fused s <= 128 kernel");
     if (use_long_attn() && attn_long_supported(at, true)) {
       const bool hl = with_hl();
       // whole 128-blocks: dK/dV stores its dS tiles (pre-split) in the dP
@@ -1197,7 +1215,7 @@ int Engine::dump_profile(double* out, int max_rows) {
     if (n >= max_rows) break;
     float t = 0.f;
     MGLP_CUDA(cudaEventElapsedTime(&t, r.a, r.b));
-    double* o = out + 7 * n;
+    double* o = out + 8 * n;
     o[0] = r.cls;
     o[1] = r.shape[0];
     o[2] = r.shape[1];
@@ -1205,6 +1223,7 @@ int Engine::dump_profile(double* out, int max_rows) {
     o[4] = r.shape[3];
     o[5] = r.cls == PROF_ROW ? r.bytes : r.flops;  // row kernels: HBM bytes
     o[6] = t;
+    o[7] = r.shape.size() > 4 ? r.shape[4] : -1;
     ++n;
   }
   return n;
@@ -1374,10 +1393,13 @@ void Engine::encoder_forward(const EvalSpec& e, int R, bool causal, Mat X, Mat Y
   g.ep.kind = EPI_STORE;
   g.ep.out1 = qkv;
   g.ep.bias = par(L.b_qkv, 0, l0, ls);
+  const bool hs = attn_hs(R / B_, R / B_);
+  g.ep.hs = hs ? 1 : 0;
+  g.ep.range_flag = range_flag_;
   gemm(g);
 
   const bool ctx_hl = attention_fwd(G, qkv, qkv.offset(d), qkv.offset(2 * d), ctx, Pm, R / B_,
-                                    R / B_, causal, keep, h_ctx);
+                                    R / B_, causal, keep, h_ctx, hs);
 
   g = GemmArgs{};
   g.G = G;
@@ -1527,10 +1549,13 @@ void Engine::decoder_forward(const EvalSpec& e) {
   g.ep.kind = EPI_STORE;
   g.ep.out1 = qkv;
   g.ep.bias = par(L.b_qkv, 0, l0, ls);
+  const bool hs = attn_hs(sy_, sy_);
+  g.ep.hs = hs ? 1 : 0;
+  g.ep.range_flag = range_flag_;
   gemm(g);
 
-  const bool ctx_hl =
-      attention_fwd(G, qkv, qkv.offset(d), qkv.offset(2 * d), ctx, Pm, sy_, sy_, true, keep, h_ctx);
+  const bool ctx_hl = attention_fwd(G, qkv, qkv.offset(d), qkv.offset(2 * d), ctx, Pm, sy_, sy_,
+                                    true, keep, h_ctx, hs);
 
   g = mk(R, d, d, ctx, L.w_o, d);
   if (ctx_hl) g.Ahl = h_ctx;
@@ -1553,21 +1578,26 @@ void Engine::decoder_forward(const EvalSpec& e) {
   timed(PROF_ROW, 0.0, 8.0 * ln.G * (double)ln.rows * ln.d,
         [&] { launch_ln_fwd(ln, active_, stream_); });
 
+  const bool chs = attn_hs(sy_, sx_);
   g = mk(R, d, d, n3, L.w_cq, d);
   g.Ahl = h_n3;
   g.ep.kind = EPI_STORE;
   g.ep.out1 = cq;
   g.ep.bias = par(L.b_cq, 0, l0, ls);
+  g.ep.hs = chs ? 1 : 0;
+  g.ep.range_flag = range_flag_;
   gemm(g);
 
   g = mk(Tx_, 2 * d, d, X, L.w_ckv, d);
   g.ep.kind = EPI_STORE;
   g.ep.out1 = ckv;
   g.ep.bias = par(L.b_ckv, 0, l0, ls);
+  g.ep.hs = chs ? 1 : 0;
+  g.ep.range_flag = range_flag_;
   gemm(g);
 
   const bool cctx_hl =
-      attention_fwd(G, cq, ckv, ckv.offset(d), cctx, cP, sy_, sx_, false, keep, h_cctx);
+      attention_fwd(G, cq, ckv, ckv.offset(d), cctx, cP, sy_, sx_, false, keep, h_cctx, chs);
 
   g = mk(R, d, d, cctx, L.w_co, d);
   if (cctx_hl) g.Ahl = h_cctx;
@@ -1756,17 +1786,20 @@ void Engine::encoder_adjoint(const EvalSpec& e, bool causal) {
     timed(PROF_ROW, 0.0, 20.0 * lb.G * (double)lb.rows * lb.d,
           [&] { launch_ln_bwd(lb, active_, stream_); });
 
+    const bool hs = attn_hs(R / B_, R / B_);
     g = mk(R, d, d, da1, L.w_o, d);
     g.Ahl = h_da1;
     g.ep.kind = EPI_STORE;
     g.ep.out1 = dctx;
+    g.ep.hs = hs ? 1 : 0;
+    g.ep.range_flag = range_flag_;
     gemm(g);
 
     const Mat h_dqkv = dgrad_hl(G, 1, 3 * d);
     const bool dqkv_hl =
         attention_bwd(G, qkv, qkv.offset(d), qkv.offset(2 * d), Pm, ctx, dctx, dPm, dqkv,
                       dqkv.offset(d), dqkv.offset(2 * d), R / B_, R / B_, causal, h_dqkv,
-                      h_dqkv.offset(d), h_dqkv.offset(2 * d), keep32);
+                      h_dqkv.offset(d), h_dqkv.offset(2 * d), keep32, hs, hs);
 
     g = mk(R, d, 3 * d, dqkv, L.w_qkv, d);
     if (dqkv_hl) g.Ahl = h_dqkv;
@@ -1959,13 +1992,16 @@ void Engine::decoder_adjoint(const EvalSpec& e) {
       timed(PROF_ROW, 0.0, 8.0 * G * (double)R * d,
             [&] { launch_mask_copy(G, R, d, dcp, dybar, dmask(2, l0, ls), active_, stream_); });
     }
+    const bool chs = attn_hs(sy_, sx_);
     g = mk(R, d, d, dcp, L.w_co, d);
     g.ep.kind = EPI_STORE;
     g.ep.out1 = dcctx;
+    g.ep.hs = chs ? 1 : 0;
+    g.ep.range_flag = range_flag_;
     gemm(g);
 
     attention_bwd(G, cq, ckv, ckv.offset(d), cP, cctx, dcctx, dP2, dcq, dckv, dckv.offset(d), sy_,
-                  sx_, false);
+                  sx_, false, Mat{}, Mat{}, Mat{}, true, chs, chs);
 
     g = mk(R, d, d, dcq, L.w_cq, d);
     g.ep.kind = EPI_STORE;
@@ -1993,17 +2029,20 @@ void Engine::decoder_adjoint(const EvalSpec& e) {
     timed(PROF_ROW, 0.0, 20.0 * lb.G * (double)lb.rows * lb.d,
           [&] { launch_ln_bwd(lb, active_, stream_); });
 
+    const bool hs = attn_hs(sy_, sy_);
     g = mk(R, d, d, da1, L.w_o, d);
     g.Ahl = h_da1;
     g.ep.kind = EPI_STORE;
     g.ep.out1 = dctx;
+    g.ep.hs = hs ? 1 : 0;
+    g.ep.range_flag = range_flag_;
     gemm(g);
 
     const Mat h_dqkv = dgrad_hl(G, 1, 3 * d);
     const bool dqkv_hl =
         attention_bwd(G, qkv, qkv.offset(d), qkv.offset(2 * d), Pm, ctx, dctx, dPm, dqkv,
                       dqkv.offset(d), dqkv.offset(2 * d), sy_, sy_, true, h_dqkv, h_dqkv.offset(d),
-                      h_dqkv.offset(2 * d), keep32);
+                      h_dqkv.offset(2 * d), keep32, hs, hs);
 
     g = mk(R, d, 3 * d, dqkv, L.w_qkv, d);
     if (dqkv_hl) g.Ahl = h_dqkv;

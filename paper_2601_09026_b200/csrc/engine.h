@@ -299,8 +299,15 @@ class Engine {
   // slices (head h at columns h*dh); P is [B][H][sq][skv] per member.
   // Ohl (optional): also write O pre-split for the O-projection (returns
   // whether it did; O itself is then skipped unless keep_p)
+  // qkv_hs: Q, K, V were written head-split pre-split (attn_hs) by their GEMMs
   bool attention_fwd(int G, Mat Q, Mat K, Mat V, Mat O, Mat P, int sq, int skv, bool causal,
-                     bool keep_p, Mat Ohl = Mat{});
+                     bool keep_p, Mat Ohl = Mat{}, bool qkv_hs = false);
+  // the attention operands of an (sq, skv) problem travel head-split
+  // pre-split (AttnArgs::qkv_hs / do_hs): the QKV (cross Q / KV) GEMMs and the
+  // O-projection dgrad write them so for the fused s <= 128 kernels, dh = 64.
+  // A function of the shape only (forward and backward agree);
+  // MGLP_NO_ATTN_HS=1 keeps them fp32.
+  bool attn_hs(int sq, int skv) const;
   // the family's pre-split activation buffer `which` (0: [rows][d] LN outputs,
   // 1: [rows][cols <= max(d, ffn)] attention O / GELU output; hi|lo' rows, the
   // next forward GEMM's A operand); empty when unavailable
@@ -326,7 +333,8 @@ class Engine {
   // keep32)
   bool attention_bwd(int G, Mat Q, Mat K, Mat V, Mat P, Mat O, Mat dO, Mat dP, Mat dQ, Mat dK, Mat dV,
                      int sq, int skv, bool causal, Mat dQhl = Mat{}, Mat dKhl = Mat{},
-                     Mat dVhl = Mat{}, bool keep32 = true);
+                     Mat dVhl = Mat{}, bool keep32 = true, bool qkv_hs = false,
+                     bool do_hs = false);
   int gemm_blocks(const GemmArgs& g) const;
   Mat act_mat(const ActRef& r, long long off, int ld) const;
   Mat bwd_mat(const EvalSpec& e, long long off, int ld) const;
@@ -498,7 +506,7 @@ class Engine {
       return;
     }
     ProfRec r{prof_event(), prof_event(), cls, flops, bytes, prof_shape_};
-    prof_shape_ = {0, 0, 0, 0};
+    prof_shape_ = {0, 0, 0, 0, -1};
     cudaEventRecord(r.a, stream_);
     launch();
     cudaEventRecord(r.b, stream_);

@@ -218,6 +218,10 @@ struct AttnArgs {
   // (query block, key block) dS tile pre-split (64 KiB) here, P-slot strides,
   // and the dQ kernel reads them instead of recomputing S, P and dP
   Mat dS;
+  // Q, K, V (qkv_hs) and dO (do_hs) written by their producer GEMMs in the
+  // head-split pre-split form (common.cuh st_hs4; dh = 64): TMA'd straight
+  // into the operand tiles, no fp32 staging or conversion in the kernel
+  int qkv_hs = 0, do_hs = 0;
   int* range_flag = nullptr;
 };
 bool attn_tc_supported(const AttnArgs& a, bool backward);

@@ -38,6 +38,17 @@ def reference(Q, K, V, dO, B, H, sq, skv, dh, causal):
     return O, P, dQ, dK, dV
 
 
+def head_split(x):
+    """fp32 rows -> the head-split pre-split form the QKV GEMM epilogue writes
+    (common.cuh st_hs4): per 64 columns, 64 fp16 hi then 64 fp16 lo' =
+    fp16((x - hi) * 2^11), the same bytes per row"""
+    sh = x.shape
+    y = x.reshape(*sh[:-1], -1, 64)
+    hi = y.half()
+    lo = ((y - hi.float()) * 2048.0).half()
+    return torch.cat([hi, lo], -1).contiguous().view(torch.float32).reshape(sh).contiguous()
+
+
 def run(B, H, sq, skv, dh, causal, seed=0, scale=1.0):
     g = torch.Generator().manual_seed(seed)
     d = H * dh
@@ -53,6 +64,8 @@ def run(B, H, sq, skv, dh, causal, seed=0, scale=1.0):
     dkv = qkv_kv.clone().cuda()
     ddo = torch.zeros(B, sq, ld, device="cuda")
     ddo[..., :d] = dO.cuda()
+    if int(causal) & 4:  # operands in the head-split pre-split form (AttnArgs::qkv_hs / do_hs)
+        dq, dkv, ddo = head_split(dq), head_split(dkv), head_split(ddo)
     O = torch.full((B, sq, ld), float("nan"), device="cuda")
     ldp = (skv + 3) & ~3
     P = torch.full((B, H, sq, ldp), float("nan"), device="cuda")
@@ -164,3 +177,16 @@ def test_presplit_p_is_bitwise_the_fp32_p_path(causal):
     for n, x, y in zip(["O", "dQ", "dK", "dV"], (a[0],) + a[2:], (b[0],) + b[2:]):
         assert torch.equal(x, y), n
     assert relerr(b[0], ref[0]) < 1e-5
+
+
+@pytest.mark.parametrize("shape", [s for s in SHAPES if s[4] == 64])
+def test_presplit_operands_are_bitwise_the_fp32_path(shape):
+    """Q, K, V and dO arriving head-split pre-split (TMA'd straight into the
+    operand tiles) give bit-identical O, P, dQ, dK, dV: the kernel's own
+    conversion of fp32 operands builds exactly those tiles"""
+    B, H, sq, skv, dh, causal = shape
+    a, ref = run(B, H, sq, skv, dh, causal, seed=7)
+    b, _ = run(B, H, sq, skv, dh, int(causal) | 4, seed=7)
+    for n, x, y in zip(["O", "P", "dQ", "dK", "dV"], a, b):
+        assert torch.equal(x, y), n
+    assert relerr(b[0], ref[0]) < 2e-5

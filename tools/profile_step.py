@@ -39,13 +39,14 @@ step()
 N.call("mglp_engine_sync", h)
 N.call("mglp_engine_profile", h, 1)
 step()
-rows = np.zeros((20000, 7))
+rows = np.zeros((20000, 8))
 n = C.c_int()
 N.call("mglp_engine_profile_dump", h, N.dptr(rows), 20000, C.byref(n))
 rows = rows[:n.value]
 agg = collections.defaultdict(lambda: [0, 0.0, 0.0])
-for cls, M, Nn, K, b, fl, ms in rows:
-    key = (int(cls), int(M), int(Nn), int(K), int(b))
+EPI = {0: "store", 1: "add2", 2: "gelu", 3: "final", 4: "gelu'", 5: "gacc"}
+for cls, M, Nn, K, b, fl, ms, var in rows:
+    key = (int(cls), int(M), int(Nn), int(K), int(b), int(var))
     agg[key][0] += 1
     agg[key][1] += ms
     agg[key][2] += fl
@@ -54,7 +55,7 @@ print(f"{name}: {n.value} launches, {tot:.1f} ms in profiled kernels")
 ROWK = {0: "row?", 1: "softmax", 2: "softmax_bwd", 3: "ln_fwd", 4: "ln_bwd", 5: "colred",
         6: "combine", 7: "copy", 8: "correct|pack"}
 for key, (cnt, ms, fl) in sorted(agg.items(), key=lambda kv: -kv[1][1])[:60]:
-    cls, M, Nn, K, b = key
+    cls, M, Nn, K, b, var = key
     if cls == 2:  # row kernel: (kind, cols, -, G); fl = HBM bytes
         gbs = fl / (ms * 1e-3) / 1e9 if ms > 0 else 0
         print(f"row   {ROWK.get(M, M):12s} cols {Nn:5d}   x{b:5d}  n={cnt:4d}  {ms:8.2f} ms "
@@ -62,4 +63,8 @@ for key, (cnt, ms, fl) in sorted(agg.items(), key=lambda kv: -kv[1][1])[:60]:
         continue
     tf = fl / (ms * 1e-3) / 1e12 if ms > 0 else 0
     label = ["gemm", "other", "row"][cls]
-    print(f"{label:5s} M{M:6d} N{Nn:5d} K{K:5d} x{b:5d}  n={cnt:4d}  {ms:8.2f} ms ({100*ms/tot:5.1f}%)  {tf:7.1f} TF/s")
+    vs = ""
+    if var >= 0:
+        vs = EPI.get(var & 15, str(var & 15)) + ("" if not var & 16 else " Ahl") + \
+            ("" if not var & 32 else " Bhl") + ("" if not var & 64 else " Amn") + ("" if not var & 128 else " Bmn")
+    print(f"{label:5s} M{M:6d} N{Nn:5d} K{K:5d} x{b:5d} {vs:22s} n={cnt:4d}  {ms:8.2f} ms ({100*ms/tot:5.1f}%)  {tf:7.1f} TF/s")
