@@ -675,6 +675,7 @@ void launch_long(K kernel, const AttnTma& t, const AttnArgs& a, long long nprob,
 }  // namespace
 
 bool attn_long_supported(const AttnArgs& a, bool backward) {
+  if (a.qkv_hs || a.do_hs) return attn_flash_supported(a, backward);
   if (a.sq < 128 || a.skv < 128 || a.sq > 512 || a.skv > 512) return false;
   if (a.dh != 32 && a.dh != 64) return false;
   if (!a.P.ok() || !aligned(a.Q) || !aligned(a.K) || !aligned(a.V) || !aligned(a.O) ||
@@ -686,6 +687,7 @@ bool attn_long_supported(const AttnArgs& a, bool backward) {
 }
 
 void launch_attn_fwd_long(const AttnArgs& a, const int* active, cudaStream_t s) {
+  if (a.qkv_hs) return launch_attn_fwd_flash(a, active, s);  // pre-split operands: attn_flash.cu
   if (!attn_long_supported(a, false)) throw ContractViolation("attn_fwd_long: unsupported shape");
   static bool attr = [] {
     MGLP_CUDA(cudaFuncSetAttribute(attn_fwd_long_kernel,

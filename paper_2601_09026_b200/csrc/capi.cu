@@ -1082,8 +1082,10 @@ mglp_status mglp_bench_attention(int G, int B, int H, int s, int dh, int causal,
     for (Mat* m : {&a.O, &a.dO}) m->slot_stride = (long long)B * s * d;
     a.P.slot_stride = (long long)B * H * s * ldp;
     // backward: 0 forward (P / row statistics stored), 1 backward,
-    // 2 forward without P (s <= 128), 3 as 2 with O written pre-split only
-    const int mode = backward;
+    // 2 forward without P (s <= 128), 3 as 2 with O written pre-split only;
+    // + 4: Q, K, V, dO head-split pre-split (dh = 64)
+    const int mode = backward & 3;
+    a.qkv_hs = a.do_hs = (backward >> 2) & 1;
     backward = mode == 1;
     const bool shortp = attn_tc_supported(a, backward != 0);
     if (!shortp && !attn_long_supported(a, backward != 0))

@@ -233,5 +233,10 @@ void launch_attn_bwd(const AttnArgs& a, const int* active, cudaStream_t s);
 bool attn_long_supported(const AttnArgs& a, bool backward);
 void launch_attn_fwd_long(const AttnArgs& a, const int* active, cudaStream_t s);
 void launch_attn_bwd_long(const AttnArgs& a, const int* active, cudaStream_t s);
+// 128 < sq, skv <= 512 with head-split pre-split operands (qkv_hs, dh = 64;
+// attn_flash.cu): single-pass online softmax, P~ kept in TMEM; same P-slot row
+// statistics (max, 1/sum) as the long form
+bool attn_flash_supported(const AttnArgs& a, bool backward);
+void launch_attn_fwd_flash(const AttnArgs& a, const int* active, cudaStream_t s);
 
 }  // namespace mglp

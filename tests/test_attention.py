@@ -190,3 +190,37 @@ def test_presplit_operands_are_bitwise_the_fp32_path(shape):
     for n, x, y in zip(["O", "P", "dQ", "dK", "dV"], a, b):
         assert torch.equal(x, y), n
     assert relerr(b[0], ref[0]) < 2e-5
+
+
+@pytest.mark.parametrize("shape", [(1, 2, 512, 512, 64, True), (2, 2, 197, 197, 64, False),
+                                   (1, 1, 256, 384, 64, False), (1, 3, 320, 320, 64, True)])
+def test_flash_forward_presplit(shape):
+    """128 < s <= 512 with head-split pre-split Q, K, V (attn_flash.cu):
+    single-pass online softmax with P~ in TMEM. O against fp64, and the row
+    statistics through their invariant m - log(1/l) = logsumexp_j(s_j scale)
+    (the reference max m may lag the true max: lazy rescaling)"""
+    B, H, sq, skv, dh, causal = shape
+    g = torch.Generator().manual_seed(11)
+    d = H * dh
+    qkv_q = torch.randn(B, sq, 3 * d, generator=g)
+    qkv_kv = torch.randn(B, skv, 3 * d, generator=g)
+    dq, dkv = head_split(qkv_q.clone().cuda()), head_split(qkv_kv.clone().cuda())
+    O = torch.full((B, sq, 3 * d), float("nan"), device="cuda")
+    ldp = (skv + 3) & ~3
+    P = torch.full((B, H, sq, ldp), float("nan"), device="cuda")
+    N.call("mglp_test_attention", B, H, sq, skv, dh, int(causal) | 4, dq.data_ptr(),
+           dkv[..., d:].data_ptr(), dkv[..., 2 * d:].data_ptr(), 3 * d, O.data_ptr(), P.data_ptr(),
+           None, None, None, None, None)
+    Q, K, V = qkv_q[..., :d], qkv_kv[..., d:2 * d], qkv_kv[..., 2 * d:]
+    ref_O, _, _, _, _ = reference(Q, K, V, torch.zeros(B, sq, d), B, H, sq, skv, dh, causal)
+    assert relerr(O[..., :d].cpu(), ref_O) < 2e-5
+    st = P.cpu().reshape(B, H, -1)[..., : 2 * sq].reshape(B, H, sq, 2).double()
+    for b in range(B):
+        for h in range(H):
+            sl = slice(h * dh, (h + 1) * dh)
+            s = (Q[b, :, sl].double() @ K[b, :, sl].double().T) / math.sqrt(dh)
+            if causal:
+                s = s.masked_fill(torch.ones(sq, skv).triu(1).bool(), float("-inf"))
+            lse = torch.logsumexp(s, -1)
+            got = st[b, h, :, 0] - torch.log(st[b, h, :, 1])
+            assert float((got - lse).abs().max()) < 1e-5
