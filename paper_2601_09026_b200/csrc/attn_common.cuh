@@ -277,6 +277,7 @@ __device__ __forceinline__ void tmem_free(uint32_t base, uint32_t cols) {
 struct AttnTma {
   CUtensorMap m[5];
   TcOperand op[5];
+  int hs_mask = 0;  // bit `which`: the operand is head-split pre-split (AttnArgs::qkv_hs / do_hs)
 };
 enum { TQ = 0, TK = 1, TV = 2, TP = 3, TDO = 4 };
 

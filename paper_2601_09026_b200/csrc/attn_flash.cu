@@ -430,17 +430,562 @@ __global__ void __launch_bounds__(kFwdThreads, 2)
   if (warp == 0) tmem_free(tmem, 256);
 }
 
+// ---- backward ---------------------------------------------------------------------
+// Deterministic two-kernel form (no atomics): per 128-key block, dK and dV
+// accumulate over 64-query blocks in TMEM and every dS tile is stored
+// pre-split for the dQ kernel, which sums dQ = dS K per 128-query block.
+// Keys are the TMEM lanes (S^T = K Q^T, M = 128 keys, N = 64 queries):
+//   S^T  = K_hi Q_hi + K_lo'' Q_hi + K_hi'' Q_lo'      (K forms made once per CTA problem)
+//   dP^T = V_hi dO_hi + V_lo'' dO_hi + V_hi'' dO_lo'   (V likewise)
+//   P^T  = exp(S^T scale - m_q) / l_q (the forward's row statistics), dS^T = P^T (dP^T - t_q)
+//   dV  += P_hi dO_hi + P_lo'' dO_hi + P_hi'' dO_lo'   (A = P^T from TMEM)
+//   dK  += dS_hi Q_hi + 2^-11 (dS_lo' Q_hi + dS_hi Q_lo')  (two accumulators: dS is a
+//          gradient and may be small, so its 2^-11 stays in the accumulation)
+// t_q = dO_q . O_q comes from flash_rowdot_kernel first.
+constexpr int kKvThreads = 576;  // warps 0-15 compute, 16 MMA issue, 17 TMA
+constexpr int kQB = 64;          // queries per step
+constexpr int QT = kQB * 128;    // one 64-row hi (or lo') tile: 8 KiB
+// smem: K hi | lo'' | hi'' (16 KiB each) | V likewise | Q[3] (hi|lo', 16 KiB) | dO[3] | stats[3]
+// (three query stages: step j's loads go out once step j-3 is done, a whole
+// step ahead of when S_j can start)
+constexpr int kKvOff = 6 * 16384 + 6 * 2 * QT;
+constexpr int kKvSmem = 1024 + kKvOff + 3 * 1024 + 128 + 16;
+// TMEM: S/P~ [0,96) [96,192); dP/dS [192,256) [256,320); dV [320,384); dK main [384,448), corr [448,512)
+__device__ __forceinline__ uint32_t tsb(int s) { return s ? 96u : 0u; }
+__device__ __forceinline__ uint32_t tdb(int s) { return s ? 256u : 192u; }
+constexpr uint32_t kTdV = 320, kTdK = 384, kTdKc = 448;
+
+// x *= 2^-11 over `bytes` of fp16 (dst may equal src), threads [tid, nthr)
+__device__ __forceinline__ void scale_copy(uint32_t dst, uint32_t src, int bytes, int tid, int nthr) {
+  const __half2 sc = __float2half2_rn(kLo2);
+  for (int c = tid * 16; c < bytes; c += nthr * 16) {
+    uint4 v = lds128u(src + c);
+    uint32_t* w = &v.x;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const __half2 x = __hmul2(*reinterpret_cast<const __half2*>(&w[e]), sc);
+      w[e] = *reinterpret_cast<const uint32_t*>(&x);
+    }
+    sts128(dst + c, v);
+  }
+}
+
+// MGLP_FLASH_TRACE (diagnostics): clock64 stamps of CTA 0 of the dK/dV kernel
+#ifdef MGLP_FLASH_TRACE
+__device__ long long g_flash_trace[4096];
+#define FTRACE(slot) \
+  do { if (blockIdx.x == 0 && (slot) < 4096) g_flash_trace[(slot)] = clock64(); } while (0)
+#else
+#define FTRACE(slot) do { } while (0)
+#endif
+
+// the t_q offset in a head's P slot (after the forward's [sq][2] statistics)
+__device__ __host__ __forceinline__ long long t_off(int sq) { return 2LL * ((sq + 63) & ~63); }
+
+// t_q = dO_q . O_q with dO head-split pre-split (d = hi + 2^-11 lo', the value
+// the MMAs use) and O fp32, fixed order
+__global__ void __launch_bounds__(256) flash_rowdot_kernel(const AttnArgs a, const int* active) {
+  pdl_wait();
+  pdl_trigger();
+  if (active && *(volatile const int*)active == 0) return;
+  const long long n = (long long)a.G * a.Bb * a.H * a.sq;
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int q = (int)(i % a.sq);
+  long long r = i / a.sq;
+  const int h = (int)(r % a.H);
+  r /= a.H;
+  const int b = (int)(r % a.Bb), g = (int)(r / a.Bb);
+  const __half* d = reinterpret_cast<const __half*>(a.dO.at(g, b, h) + (long long)q * a.dO.ld);
+  const float* o = a.O.at(g, b, h) + (long long)q * a.O.ld;
+  float t = 0.f;
+  for (int e = 0; e < 64; e += 8) {
+    const uint4 hv = *reinterpret_cast<const uint4*>(d + e);
+    const uint4 lv = *reinterpret_cast<const uint4*>(d + 64 + e);
+    const float4 o0 = *reinterpret_cast<const float4*>(o + e);
+    const float4 o1 = *reinterpret_cast<const float4*>(o + e + 4);
+    const float ov[8] = {o0.x, o0.y, o0.z, o0.w, o1.x, o1.y, o1.z, o1.w};
+    const uint32_t hw[4] = {hv.x, hv.y, hv.z, hv.w}, lw[4] = {lv.x, lv.y, lv.z, lv.w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float2 hf = __half22float2(*reinterpret_cast<const __half2*>(&hw[k]));
+      const float2 lf = __half22float2(*reinterpret_cast<const __half2*>(&lw[k]));
+      t += fmaf(lf.x, kLo2, hf.x) * ov[2 * k];
+      t += fmaf(lf.y, kLo2, hf.y) * ov[2 * k + 1];
+    }
+  }
+  a.P.at(g, b, h)[t_off(a.sq) + q] = t;
+}
+
+__global__ void __launch_bounds__(kKvThreads, 1)
+    attn_bwd_kv_flash_kernel(const __grid_constant__ AttnTma tm, const AttnArgs a, const int* active) {
+  pdl_wait();
+  pdl_trigger();
+  extern __shared__ uint8_t smem_raw[];
+  if (active && *(volatile const int*)active == 0) return;
+  uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
+  const uint32_t base = smem_u32(smem);
+  const uint32_t khi = base, klo = base + 16384, khi2 = base + 32768;
+  const uint32_t vhi = base + 49152, vlo = base + 65536, vhi2 = base + 81920;
+  const Opnd Ka{khi, klo, 128, false}, Kb{khi2, khi2, 128, false};
+  const Opnd Va{vhi, vlo, 128, false}, Vb{vhi2, vhi2, 128, false};
+  auto Qt = [&](int s, bool mn) {
+    const uint32_t q0 = base + 98304 + s * 2 * QT;
+    return Opnd{q0, q0 + QT, 64, mn};
+  };
+  auto dOt = [&](int s, bool mn) {
+    const uint32_t q0 = base + 98304 + 6 * QT + s * 2 * QT;
+    return Opnd{q0, q0 + QT, 64, mn};
+  };
+  float* stats = reinterpret_cast<float*>(smem + kKvOff);  // [3][256]: m, inv pairs | t
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kKvOff + 3 * 1024);
+  uint64_t* bKV = &bars[0];   // K, V landed
+  uint64_t* bKVc = &bars[1];  // K, V forms made (512 arrivals)
+  uint64_t* bQ = &bars[2];    // [3] Q_j, dO_j, stats_j landed (stage j % 3)
+  uint64_t* bSD = &bars[5];   // [2] S_j, dP_j done (TMEM buffer j & 1)
+  uint64_t* bPD = &bars[7];   // [2] P~_j, dS_j written (512 arrivals)
+  uint64_t* bM = &bars[9];    // [3] step j's dV / dK MMAs done (by j % 3)
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 13);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int sq = a.sq, skv = a.skv;
+  const int nkb = (skv + 127) >> 7, nq64 = (sq + kQB - 1) / kQB;
+  const int nprob = a.G * a.Bb * a.H * nkb;
+  if (tid == 0) {
+    for (int k = 0; k < 12; ++k) mbar_init(&bars[k], (k == 1 || k == 7 || k == 8) ? 512 : 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) tmem_alloc(tslot, 512);
+  bar_sync();
+  const uint32_t tmem = *tslot;
+  float amax = 0.f;
+  auto coords = [&](int z, int& g, int& b, int& h, int& kb) {
+    kb = z % nkb;
+    int r = z / nkb;
+    h = r % a.H;
+    r /= a.H;
+    b = r % a.Bb;
+    g = r / a.Bb;
+  };
+  auto first_q = [&](int kb) { return a.causal ? (kb * 128) / kQB : 0; };
+  if (warp == 17) {
+    // ================= TMA loads (one thread) =================
+    if (lane == 0) {
+      uint32_t cm = 0;  // steps before this problem (global step index base)
+      for (int z = blockIdx.x; z < nprob; z += gridDim.x) {
+        int g, b, h, kb;
+        coords(z, g, b, h, kb);
+        const int q0 = first_q(kb), n = nq64 - q0;
+        mbar_expect_tx(bKV, 4 * 16384);  // (the previous problem's MMAs are all done)
+        tma_box(khi, tm, TK, g, b, h, bKV, kb * 128, 0);
+        tma_box(klo, tm, TK, g, b, h, bKV, kb * 128, 32);
+        tma_box(vhi, tm, TV, g, b, h, bKV, kb * 128, 0);
+        tma_box(vlo, tm, TV, g, b, h, bKV, kb * 128, 32);
+        const float* st = a.P.at(g, b, h);
+        for (int j = 0; j < n; ++j) {
+          const int s = j % 3;
+          if (j >= 3) {  // stage s: step j-3 fully consumed
+            const uint32_t k = cm + j - 3;
+            mbar_wait(&bM[k % 3], (k / 3) & 1);
+          }
+          const int qr = (q0 + j) * kQB;
+          FTRACE(8 * (cm + j) + 6);
+          mbar_expect_tx(&bQ[s], 4 * QT + 768);
+          const Opnd Q = Qt(s, false), D = dOt(s, false);
+          tma_box(Q.hi, tm, TQ, g, b, h, &bQ[s], qr, 0);
+          tma_box(Q.lo, tm, TQ, g, b, h, &bQ[s], qr, 32);
+          tma_box(D.hi, tm, TDO, g, b, h, &bQ[s], qr, 0);
+          tma_box(D.lo, tm, TDO, g, b, h, &bQ[s], qr, 32);
+          bulk_load(smem_u32(stats + s * 256), st + 2LL * qr, 512, &bQ[s]);  // m, 1/l
+          bulk_load(smem_u32(stats + s * 256 + 128), st + t_off(sq) + qr, 256, &bQ[s]);
+        }
+        // every step of this problem done before the next one's K, V (waits
+        // stay consecutive: no bM phase is skipped)
+        for (int j = max(n - 3, 0); j < n; ++j) {
+          const uint32_t k = cm + j;
+          mbar_wait(&bM[k % 3], (k / 3) & 1);
+        }
+        cm += n;
+      }
+    }
+    __syncwarp();
+  } else if (warp == 16) {
+    // ================= MMA issue (one thread) =================
+    if (lane == 0) {
+      uint32_t nkv = 0, nq[3] = {0, 0, 0}, npd[2] = {0, 0}, cm = 0;
+      const uint32_t idN64 = idesc(64, false, false), idG = idesc(64, false, true);
+      for (int z = blockIdx.x; z < nprob; z += gridDim.x) {
+        int g, b, h, kb;
+        coords(z, g, b, h, kb);
+        const int n = nq64 - first_q(kb);
+        mbar_wait(bKVc, nkv & 1);
+        ++nkv;
+        for (int j = 0; j <= n; ++j) {
+          if (j < n) {
+            const int s = j & 1, q3 = j % 3;
+            mbar_wait(&bQ[q3], nq[q3] & 1);
+            ++nq[q3];
+            FTRACE(8 * (cm + j) + 0);
+            if (j >= 2) {  // TMEM buffers s free: step j-2's gradient MMAs done
+              const uint32_t k = cm + j - 2;
+              mbar_wait(&bM[k % 3], (k / 3) & 1);
+            }
+            FTRACE(8 * (cm + j) + 1);
+            tc_after();
+            const Opnd Q = Qt(q3, false), D = dOt(q3, false);
+            const uint32_t dS_ = tmem + tsb(s), dD = tmem + tdb(s);
+            for (int k = 0; k < 4; ++k) {
+              mma_ss(dS_, Ka, false, Q, false, k, idN64, k > 0 ? 1u : 0u);  // S^T = K Q^T
+              mma_ss(dS_, Ka, true, Q, false, k, idN64, 1u);
+              mma_ss(dS_, Kb, false, Q, true, k, idN64, 1u);
+              mma_ss(dD, Va, false, D, false, k, idN64, k > 0 ? 1u : 0u);  // dP^T = V dO^T
+              mma_ss(dD, Va, true, D, false, k, idN64, 1u);
+              mma_ss(dD, Vb, false, D, true, k, idN64, 1u);
+            }
+            mma_commit<1>(&bSD[s]);
+          }
+          if (j >= 1) {
+            const int s = (j - 1) & 1;
+            mbar_wait(&bPD[s], npd[s] & 1);
+            ++npd[s];
+            FTRACE(8 * (cm + j - 1) + 2);
+            tc_after();
+            const Opnd Qm = Qt((j - 1) % 3, true), Dm = dOt((j - 1) % 3, true);
+            const uint32_t pa = tmem + tsb(s), da = tmem + tdb(s);
+            const bool first = j == 1;
+            for (int k = 0; k < 4; ++k) {
+              const uint32_t oq = Qm.at(k), od = Dm.at(k);
+              const uint64_t dqh = desc_sw128(Qm.hi + oq, Qm.lbo()), dql = desc_sw128(Qm.lo + oq, Qm.lbo());
+              const uint64_t ddh = desc_sw128(Dm.hi + od, Dm.lbo()), ddl = desc_sw128(Dm.lo + od, Dm.lbo());
+              const uint32_t acc = (!first || k > 0) ? 1u : 0u;
+              mma_ts(tmem + kTdV, pa + 8 * k, ddh, idG, acc);  // dV += P^T dO
+              mma_ts(tmem + kTdV, pa + 32 + 8 * k, ddh, idG, 1u);
+              mma_ts(tmem + kTdV, pa + 64 + 8 * k, ddl, idG, 1u);
+              mma_ts(tmem + kTdK, da + 8 * k, dqh, idG, acc);  // dK += dS^T Q
+              mma_ts(tmem + kTdKc, da + 32 + 8 * k, dqh, idG, acc);
+              mma_ts(tmem + kTdKc, da + 8 * k, dql, idG, 1u);
+            }
+            mma_commit<1>(&bM[(cm + j - 1) % 3]);
+          }
+        }
+        cm += n;
+      }
+    }
+    __syncwarp();
+  } else {
+    // ================= compute warps 0-15 =================
+    // warp w: key rows 32 (w & 3) + lane (TMEM lanes), queries 16 (w >> 2) .. + 16
+    const int q4 = warp & 3, qq = warp >> 2;
+    const uint32_t lanes = (uint32_t)(q4 * 32) << 16;
+    const int r = q4 * 32 + lane;  // key row within the block
+    uint32_t nkv = 0, nsd[2] = {0, 0}, cm = 0;
+    for (int z = blockIdx.x; z < nprob; z += gridDim.x) {
+      int g, b, h, kb;
+      coords(z, g, b, h, kb);
+      const int q0 = first_q(kb), n = nq64 - q0;
+      const int key = kb * 128 + r;
+      // K, V landed: lo' -> lo'' in place, hi'' = hi 2^-11
+      mbar_wait(bKV, nkv & 1);
+      ++nkv;
+      scale_copy(klo, klo, 16384, tid, 512);
+      scale_copy(khi2, khi, 16384, tid, 512);
+      scale_copy(vlo, vlo, 16384, tid, 512);
+      scale_copy(vhi2, vhi, 16384, tid, 512);
+      fence_async_smem();
+      mbar_arrive(bKVc);
+      float* dsg = a.dS.at(g, b, h);
+      for (int j = 0; j < n; ++j) {
+        const int s = j & 1;
+        if (tid == 0) FTRACE(8 * (cm + j) + 3);
+        mbar_wait(&bSD[s], nsd[s] & 1);
+        ++nsd[s];
+        if (tid == 0) FTRACE(8 * (cm + j) + 4);
+        tc_after();
+        float sv[16], dp[16];
+        {
+          uint32_t u[16], w[16];
+          tmem_ld16(tmem + tsb(s) + lanes + qq * 16, u);
+          tmem_ld16(tmem + tdb(s) + lanes + qq * 16, w);
+          tmem_wait();
+#pragma unroll
+          for (int e = 0; e < 16; ++e) {
+            sv[e] = __uint_as_float(u[e]);
+            dp[e] = __uint_as_float(w[e]);
+          }
+        }
+        // P~ and dS overwrite S / dP columns the other three warps of these
+        // TMEM lanes read: they all have read theirs first
+        named_sync(2 + q4, 128);
+        const float* st = stats + (j % 3) * 256;
+        const int qa = (q0 + j) * kQB + qq * 16;  // this thread's first query
+        uint32_t ph[8], pl[8], ph2[8], dh[8], dl[8];
+        const __half2 sc = __float2half2_rn(kLo2);
+#pragma unroll
+        for (int e = 0; e < 16; e += 2) {
+          float p[2], ds[2];
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            const int ql = qq * 16 + e + u, q = qa + e + u;
+            const bool ok = q < sq && key < skv && (!a.causal || key <= q);
+            const float m = st[2 * ql], inv = st[2 * ql + 1], t = st[128 + ql];
+            p[u] = ok ? fast_exp(sv[e + u] * a.scale - m) * inv : 0.f;
+            ds[u] = ok ? p[u] * (dp[e + u] - t) : 0.f;
+          }
+          const __half2 hh = __floats2half2_rn(p[0], p[1]);
+          const float2 hf = __half22float2(hh);
+          const __half2 ll = __floats2half2_rn(p[0] - hf.x, p[1] - hf.y);
+          const __half2 h2 = __hmul2(hh, sc);
+          ph[e >> 1] = *reinterpret_cast<const uint32_t*>(&hh);
+          pl[e >> 1] = *reinterpret_cast<const uint32_t*>(&ll);
+          ph2[e >> 1] = *reinterpret_cast<const uint32_t*>(&h2);
+          const __half2 dhh = __floats2half2_rn(ds[0], ds[1]);
+          const float2 dhf = __half22float2(dhh);
+          const __half2 dll = __floats2half2_rn((ds[0] - dhf.x) * kLoScale, (ds[1] - dhf.y) * kLoScale);
+          dh[e >> 1] = *reinterpret_cast<const uint32_t*>(&dhh);
+          dl[e >> 1] = *reinterpret_cast<const uint32_t*>(&dll);
+          amax = fmaxf(amax, fmaxf(fabsf(ds[0]), fabsf(ds[1])));
+        }
+        // P~ -> buffer s (hi | lo'' | hi''), dS -> dP buffer s (hi | lo'): 8 columns each
+        asm volatile(
+            "tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(
+                tmem + tsb(s) + lanes + qq * 8),
+            "r"(ph[0]), "r"(ph[1]), "r"(ph[2]), "r"(ph[3]), "r"(ph[4]), "r"(ph[5]), "r"(ph[6]),
+            "r"(ph[7])
+            : "memory");
+        asm volatile(
+            "tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(
+                tmem + tsb(s) + lanes + 32 + qq * 8),
+            "r"(pl[0]), "r"(pl[1]), "r"(pl[2]), "r"(pl[3]), "r"(pl[4]), "r"(pl[5]), "r"(pl[6]),
+            "r"(pl[7])
+            : "memory");
+        asm volatile(
+            "tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(
+                tmem + tsb(s) + lanes + 64 + qq * 8),
+            "r"(ph2[0]), "r"(ph2[1]), "r"(ph2[2]), "r"(ph2[3]), "r"(ph2[4]), "r"(ph2[5]),
+            "r"(ph2[6]), "r"(ph2[7])
+            : "memory");
+        asm volatile(
+            "tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(
+                tmem + tdb(s) + lanes + qq * 8),
+            "r"(dh[0]), "r"(dh[1]), "r"(dh[2]), "r"(dh[3]), "r"(dh[4]), "r"(dh[5]), "r"(dh[6]),
+            "r"(dh[7])
+            : "memory");
+        asm volatile(
+            "tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(
+                tmem + tdb(s) + lanes + 32 + qq * 8),
+            "r"(dl[0]), "r"(dl[1]), "r"(dl[2]), "r"(dl[3]), "r"(dl[4]), "r"(dl[5]), "r"(dl[6]),
+            "r"(dl[7])
+            : "memory");
+        // dS for the dQ kernel: the (64-query block, 128-key block) tile pair
+        // image [128 key rows][64 queries] hi | lo', SWIZZLE_128B layout
+        {
+          char* img = reinterpret_cast<char*>(dsg + ((long long)(q0 + j) * nkb + kb) * 8192);
+          const int c0 = qq * 2;  // this thread's two 16-byte chunks of its row
+#pragma unroll
+          for (int c = 0; c < 2; ++c) {
+            const uint32_t off = (uint32_t)(r * 128 + (((c0 + c) ^ (r & 7)) << 4));
+            *reinterpret_cast<uint4*>(img + off) = make_uint4(dh[4 * c], dh[4 * c + 1], dh[4 * c + 2], dh[4 * c + 3]);
+            *reinterpret_cast<uint4*>(img + 16384 + off) =
+                make_uint4(dl[4 * c], dl[4 * c + 1], dl[4 * c + 2], dl[4 * c + 3]);
+          }
+        }
+        tmem_st_wait();
+        tc_before();
+        if (tid == 0) FTRACE(8 * (cm + j) + 5);
+        mbar_arrive(&bPD[s]);
+      }
+      // ---- epilogue: dV, dK = (main + 2^-11 corr) scale (this warp: 16 columns) ----
+      {
+        const uint32_t k = cm + n - 1;
+        mbar_wait(&bM[k % 3], (k / 3) & 1);
+        tc_after();
+      }
+      {
+        uint32_t u[16], w[16], x[16];
+        tmem_ld16(tmem + kTdV + lanes + qq * 16, u);
+        tmem_ld16(tmem + kTdK + lanes + qq * 16, w);
+        tmem_ld16(tmem + kTdKc + lanes + qq * 16, x);
+        tmem_wait();
+        float dv[16], dk[16];
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+          dv[e] = __uint_as_float(u[e]);
+          dk[e] = fmaf(__uint_as_float(x[e]), kLo2, __uint_as_float(w[e])) * a.scale;
+        }
+        if (key < skv) {
+          const int col = qq * 16;
+          auto put = [&](const Mat& o, const Mat& ohl, const float* v) {
+            if (o.ok()) {
+              float* p = o.at(g, b, h) + (long long)key * o.ld + col;
+#pragma unroll
+              for (int e = 0; e < 16; e += 4)
+                *reinterpret_cast<float4*>(p + e) = make_float4(v[e], v[e + 1], v[e + 2], v[e + 3]);
+            }
+            if (ohl.ok()) {
+              char* p = reinterpret_cast<char*>(ohl.at(g, b, h) + (long long)key * ohl.ld);
+#pragma unroll
+              for (int e = 0; e < 16; e += 8) {
+                uint4 hi, lo;
+                split8(v + e, hi, lo, amax);
+                char* q = p + ((col + e) >> 5) * 128 + ((col + e) & 31) * 2;
+                *reinterpret_cast<uint4*>(q) = hi;
+                *reinterpret_cast<uint4*>(q + 64) = lo;
+              }
+            }
+          };
+          put(a.dV, a.dVhl, dv);
+          put(a.dK, a.dKhl, dk);
+        }
+      }
+      cm += n;
+      tc_before();
+      named_sync(1, 512);  // TMEM accumulators read before the next problem's first MMAs
+    }
+  }
+  if (amax >= 65520.f && amax <= FLT_MAX && a.range_flag) atomicOr(a.range_flag, 1);
+  bar_sync();
+  if (warp == 0) tmem_free(tmem, 512);
+}
+
+// ---- backward: dQ = sum over key blocks of dS K (per 128-query block) ----------
+// A = dS [128 queries x 128 keys] from two stored tile-pair images (MN-major:
+// queries contiguous), B = K (MN-major), main + correction accumulators.
+constexpr int kQThreads = 192;  // warps 0-3 epilogue, 4 MMA issue, 5 loads
+constexpr int kQStage = 65536 + 32768;  // dS (hi q0 | hi q1 | lo q0 | lo q1) + K (hi | lo')
+constexpr int kQSmem = 1024 + 2 * kQStage + 64 + 16;
+
+__global__ void __launch_bounds__(kQThreads, 1)
+    attn_bwd_q_flash_kernel(const __grid_constant__ AttnTma tm, const AttnArgs a, const int* active) {
+  pdl_wait();
+  pdl_trigger();
+  extern __shared__ uint8_t smem_raw[];
+  if (active && *(volatile const int*)active == 0) return;
+  uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
+  const uint32_t base = smem_u32(smem);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 2 * kQStage);
+  uint64_t* bL = &bars[0];  // [2] stage landed
+  uint64_t* bF = &bars[2];  // [2] stage consumed (MMA commit)
+  uint64_t* bD = &bars[4];  // dQ of the problem done (MMA commit)
+  uint64_t* bE = &bars[5];  // the epilogue has read dQ (TMEM free)
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 6);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int sq = a.sq, skv = a.skv;
+  const int nkb = (skv + 127) >> 7, nqb = (sq + 127) >> 7;
+  const int nprob = a.G * a.Bb * a.H * nqb;
+  if (tid == 0) {
+    for (int k = 0; k < 6; ++k) mbar_init(&bars[k], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) tmem_alloc(tslot, 128);
+  bar_sync();
+  const uint32_t tmem = *tslot;
+  float amax = 0.f;
+  auto coords = [&](int z, int& g, int& b, int& h, int& qb) {
+    qb = nqb - 1 - z % nqb;
+    int r = z / nqb;
+    h = r % a.H;
+    r /= a.H;
+    b = r % a.Bb;
+    g = r / a.Bb;
+  };
+  auto nblocks = [&](int qb) { return a.causal ? min(nkb, qb + 1) : nkb; };
+  if (warp == 5) {
+    if (lane == 0) {
+      uint32_t c = 0;  // stages issued
+      for (int z = blockIdx.x; z < nprob; z += gridDim.x) {
+        int g, b, h, qb;
+        coords(z, g, b, h, qb);
+        const int n = nblocks(qb);
+        const float* dsg = a.dS.at(g, b, h);
+        for (int kb = 0; kb < n; ++kb, ++c) {
+          const int s = c & 1;
+          if (c >= 2) mbar_wait(&bF[s], ((c - 2) >> 1) & 1);
+          const uint32_t st = base + s * kQStage;
+          mbar_expect_tx(&bL[s], kQStage);
+          for (int hf = 0; hf < 2; ++hf) {
+            const char* img = reinterpret_cast<const char*>(
+                dsg + ((long long)(2 * qb + hf) * nkb + kb) * 8192);
+            bulk_load(st + hf * 16384, img, 16384, &bL[s]);
+            bulk_load(st + 32768 + hf * 16384, img + 16384, 16384, &bL[s]);
+          }
+          tma_box(st + 65536, tm, TK, g, b, h, &bL[s], kb * 128, 0);
+          tma_box(st + 65536 + 16384, tm, TK, g, b, h, &bL[s], kb * 128, 32);
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 4) {
+    if (lane == 0) {
+      uint32_t c = 0, nd = 0;
+      const uint32_t id = idesc(64, true, true);
+      for (int z = blockIdx.x; z < nprob; z += gridDim.x) {
+        int g, b, h, qb;
+        coords(z, g, b, h, qb);
+        const int n = nblocks(qb);
+        if (nd > 0) mbar_wait(bE, (nd - 1) & 1);  // the epilogue read the previous dQ
+        for (int kb = 0; kb < n; ++kb, ++c) {
+          const int s = c & 1;
+          mbar_wait(&bL[s], (c >> 1) & 1);
+          tc_after();
+          const uint32_t st = base + s * kQStage;
+          const Opnd A{st, st + 32768, 128, true};          // dS: K = keys (rows)
+          const Opnd B{st + 65536, st + 65536 + 16384, 128, true};  // K: K = keys (rows)
+          for (int k = 0; k < 8; ++k) {
+            const uint32_t oa = A.at(k), ob = B.at(k);
+            const uint64_t dah = desc_sw128(A.hi + oa, A.lbo()), dal = desc_sw128(A.lo + oa, A.lbo());
+            const uint64_t dbh = desc_sw128(B.hi + ob, B.lbo()), dbl = desc_sw128(B.lo + ob, B.lbo());
+            const uint32_t acc = (kb > 0 || k > 0) ? 1u : 0u;
+            mma_f16<1>(tmem, dah, dbh, id, acc);
+            mma_f16<1>(tmem + 64, dal, dbh, id, acc);
+            mma_f16<1>(tmem + 64, dah, dbl, id, 1u);
+          }
+          mma_commit<1>(&bF[s]);
+        }
+        mma_commit<1>(bD);
+        ++nd;
+      }
+    }
+    __syncwarp();
+  } else {
+    // ================= epilogue warps 0-3: one query row per thread =================
+    const uint32_t lanes = (uint32_t)(warp * 32) << 16;
+    const int i = warp * 32 + lane;
+    uint32_t nd = 0;
+    for (int z = blockIdx.x; z < nprob; z += gridDim.x) {
+      int g, b, h, qb;
+      coords(z, g, b, h, qb);
+      mbar_wait(bD, nd & 1);
+      ++nd;
+      tc_after();
+      const long long ldq = a.dQhl.ok() ? a.dQhl.ld : a.dQ.ld;
+      const long long oq = (long long)qb * 128 * ldq;
+      rows_out_hl(tmem + lanes, tmem + lanes + 64, a.dQ.ok() ? a.dQ.at(g, b, h) + oq : nullptr,
+                  a.dQhl.ok() ? a.dQhl.at(g, b, h) + oq : nullptr, ldq, i, sq - qb * 128, 0, 32,
+                  a.scale, amax);
+      rows_out_hl(tmem + lanes, tmem + lanes + 64, a.dQ.ok() ? a.dQ.at(g, b, h) + oq : nullptr,
+                  a.dQhl.ok() ? a.dQhl.at(g, b, h) + oq : nullptr, ldq, i, sq - qb * 128, 32, 32,
+                  a.scale, amax);
+      tc_before();
+      named_sync(1, 128);
+      if (tid == 0) mbar_arrive(bE);
+    }
+  }
+  if (amax >= 65520.f && amax <= FLT_MAX && a.range_flag) atomicOr(a.range_flag, 1);
+  bar_sync();
+  if (warp == 0) tmem_free(tmem, 128);
+}
+
 AttnTma flash_maps(const AttnArgs& a, bool backward) {
   AttnTma t{};
   // head-split pre-split operands: [rows][32] fp32-sized boxes (hi, lo'
-  // halves) in the tiles' SWIZZLE_128B layout; rows >= s arrive zero-filled
+  // halves) in the tiles' SWIZZLE_128B layout; rows >= s arrive zero-filled.
+  // Forward: 128-query Q, 64-key K / V; backward: 64-query Q / dO, 128-key K / V
   auto mk = [&](int which, const Mat& m, int rows, int box_rows) {
     t.m[which] = tc_make_map(m, a.G, a.Bb, a.H, rows, 64, box_rows, 32, true, &t.op[which]);
   };
-  mk(TQ, a.Q, a.sq, 128);
-  mk(TK, a.K, a.skv, KB);
-  mk(TV, a.V, a.skv, KB);
-  if (backward) mk(TDO, a.dO, a.sq, 128);
+  mk(TQ, a.Q, a.sq, backward ? kQB : 128);
+  mk(TK, a.K, a.skv, backward ? 128 : KB);
+  mk(TV, a.V, a.skv, backward ? 128 : KB);
+  if (backward) mk(TDO, a.dO, a.sq, kQB);
   return t;
 }
 
@@ -453,9 +998,41 @@ int n_sms() {
 }  // namespace
 
 bool attn_flash_supported(const AttnArgs& a, bool backward) {
-  if (backward) return false;  // backward: not yet
-  return a.qkv_hs && a.dh == 64 && a.sq > 128 && a.skv > 128 && a.sq <= 512 && a.skv <= 512 &&
-         a.P.ok();
+  if (!(a.qkv_hs && a.dh == 64 && a.sq > 128 && a.skv > 128 && a.sq <= 512 && a.skv <= 512 &&
+        a.P.ok()))
+    return false;
+  // backward: pre-split dO, fp32 O (t_q) and the dS tile-pair store (a whole
+  // [64-query][128-key] block grid per head)
+  return !backward || (a.do_hs && a.O.ok() && a.dS.ok());
+}
+
+void launch_attn_bwd_flash(const AttnArgs& a, const int* active, cudaStream_t s) {
+  if (!attn_flash_supported(a, true)) throw ContractViolation("attn_bwd_flash: unsupported");
+  static bool attr = [] {
+    MGLP_CUDA(cudaFuncSetAttribute(attn_bwd_kv_flash_kernel,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, kKvSmem));
+    MGLP_CUDA(cudaFuncSetAttribute(attn_bwd_q_flash_kernel,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, kQSmem));
+    return true;
+  }();
+  (void)attr;
+  const long long heads = (long long)a.G * a.Bb * a.H;
+  if (heads == 0) return;
+  const AttnTma t = flash_maps(a, true);
+  const long long rows = heads * a.sq;
+  launch_k(flash_rowdot_kernel, dim3((unsigned)((rows + 255) / 256)), dim3(256), 0, s, 1, a, active);
+  MGLP_CUDA(cudaGetLastError());
+  const long long nkv = heads * ((a.skv + 127) / 128), nq = heads * ((a.sq + 127) / 128);
+  static const int full = [] {  // diagnostics: 1 = kv kernel one problem per CTA, 2 = q kernel
+    const char* e = getenv("MGLP_FLASH_GRID");
+    return e ? atoi(e) : 0;
+  }();
+  launch_k(attn_bwd_kv_flash_kernel, dim3((unsigned)((full & 1) ? nkv : std::min<long long>(nkv, n_sms()))),
+           dim3(kKvThreads), kKvSmem, s, 1, t, a, active);
+  MGLP_CUDA(cudaGetLastError());
+  launch_k(attn_bwd_q_flash_kernel, dim3((unsigned)((full & 2) ? nq : std::min<long long>(nq, n_sms()))),
+           dim3(kQThreads), kQSmem, s, 1, t, a, active);
+  MGLP_CUDA(cudaGetLastError());
 }
 
 void launch_attn_fwd_flash(const AttnArgs& a, const int* active, cudaStream_t s) {
@@ -475,3 +1052,9 @@ void launch_attn_fwd_flash(const AttnArgs& a, const int* active, cudaStream_t s)
 }
 
 }  // namespace mglp
+
+#ifdef MGLP_FLASH_TRACE
+extern "C" int mglp_debug_flash_trace(long long* out, int n) {
+  return (int)cudaMemcpyFromSymbol(out, mglp::g_flash_trace, sizeof(long long) * (n < 4096 ? n : 4096));
+}
+#endif

@@ -63,11 +63,31 @@ __device__ __forceinline__ Opnd pair128(uint32_t t, bool mn) {
   return Opnd{t, t + 2 * TILE64, 128, mn};
 }
 
-// one thread issues a [128][dh] box (rows row0.. of operand `which`) into the staging
+// one thread issues a [128][dh] box (rows row0.. of operand `which`) into the
+// staging; a head-split pre-split operand arrives as its hi and lo' tiles
+// (two [128][32] SWIZZLE_128B boxes, the same 32 KiB)
 __device__ __forceinline__ void issue(const LongSmem& L, const AttnTma& tm, int which, int g, int b,
                                       int h, int row0, int dh) {
   mbar_expect_tx(&L.bars[0], (uint32_t)(128 * dh * 4));
-  tma_box(L.stg, tm, which, g, b, h, &L.bars[0], row0);
+  if ((tm.hs_mask >> which) & 1) {
+    tma_box(L.stg, tm, which, g, b, h, &L.bars[0], row0, 0);
+    tma_box(L.stg + TILE64, tm, which, g, b, h, &L.bars[0], row0, 32);
+  } else {
+    tma_box(L.stg, tm, which, g, b, h, &L.bars[0], row0);
+  }
+}
+// the staged operand `which` -> its tile pair: converted (fp32) or copied
+// (pre-split: the staging already holds the two tiles in their layout)
+__device__ __forceinline__ void land(const LongSmem& L, const AttnTma& tm, int which, uint32_t thi,
+                                     uint32_t tlo, int dh, int tid, float& amax) {
+  if ((tm.hs_mask >> which) & 1) {
+    for (int c = tid; c < 2048; c += kThreads) {
+      const uint32_t off = (uint32_t)(c & 1023) * 16;
+      sts128((c < 1024 ? thi : tlo) + off, lds128u(L.stg + (c < 1024 ? 0 : TILE64) + off));
+    }
+  } else {
+    conv_rows(L.stg, 128, 128, dh, thi, tlo, tid, kThreads, amax);
+  }
 }
 
 struct Phase {
@@ -338,12 +358,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int qb0 = a.causal ? kb : 0;
     const float* stats = a.P.at(g, b, h);
     wait_stage(L, ph);
-    conv_rows(L.stg, 128, 128, dh, Kk.hi, Kk.lo, tid, kThreads, amax);
+    land(L, tm, TK, Kk.hi, Kk.lo, dh, tid, amax);
     fence_async_smem();
     sync_all();
     if (tid == 0) issue(L, tm, TV, g, b, h, kb * 128, dh);
     wait_stage(L, ph);
-    conv_rows(L.stg, 128, 128, dh, Vk.hi, Vk.lo, tid, kThreads, amax);
+    land(L, tm, TV, Vk.hi, Vk.lo, dh, tid, amax);
     fence_async_smem();
     sync_all();
     if (tid == 0) issue(L, tm, TQ, g, b, h, qb0 * 128, dh);
@@ -352,7 +372,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int q = qb * 128 + i;
       const bool live = q < sq;
       wait_stage(L, ph);
-      conv_rows(L.stg, 128, 128, dh, Qm.hi, Qm.lo, tid, kThreads, amax);
+      land(L, tm, TQ, Qm.hi, Qm.lo, dh, tid, amax);
       fence_async_smem();
       sync_all();
       if (tid == 0) {
@@ -369,7 +389,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
       for (int c = 0; c < 8; ++c) put8(Pm.hi, Pm.lo, 128, i, half * 8 + c, p + c * 8, amax);
       wait_stage(L, ph);
-      conv_rows(L.stg, 128, 128, dh, dOk.hi, dOk.lo, tid, kThreads, amax);
+      land(L, tm, TDO, dOk.hi, dOk.lo, dh, tid, amax);
       fence_async_smem();
       sync_all();
       if (tid == 0) {
@@ -490,7 +510,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         bulk_load(L.t4, ds0 + ds_pair(a, qb, kb, nkb) * (long long)(128 * 128), 4 * TILE64, dsb);
       }
       wait_stage(L, ph);
-      conv_rows(L.stg, 128, 128, dh, Km.hi, Km.lo, tid, kThreads, amax);
+      land(L, tm, TK, Km.hi, Km.lo, dh, tid, amax);
       fence_async_smem();
       mbar_wait(dsb, dsp);
       dsp ^= 1;
@@ -566,12 +586,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int kend = a.causal ? min(nkb, qb + 1) : nkb;
     const float* stats = a.P.at(g, b, h);
     wait_stage(L, ph);
-    conv_rows(L.stg, 128, 128, dh, Qk.hi, Qk.lo, tid, kThreads, amax);
+    land(L, tm, TQ, Qk.hi, Qk.lo, dh, tid, amax);
     fence_async_smem();
     sync_all();
     if (tid == 0) issue(L, tm, TDO, g, b, h, qb * 128, dh);
     wait_stage(L, ph);
-    conv_rows(L.stg, 128, 128, dh, dOk.hi, dOk.lo, tid, kThreads, amax);
+    land(L, tm, TDO, dOk.hi, dOk.lo, dh, tid, amax);
     fence_async_smem();
     sync_all();
     if (tid == 0) issue(L, tm, TK, g, b, h, 0, dh);
@@ -584,7 +604,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (live && half == 0) const_cast<float*>(stats)[2LL * sq + q] = t;
     for (int kb = 0; kb < kend; ++kb) {
       wait_stage(L, ph);
-      conv_rows(L.stg, 128, 128, dh, Kk.hi, Kk.lo, tid, kThreads, amax);
+      land(L, tm, TK, Kk.hi, Kk.lo, dh, tid, amax);
       fence_async_smem();
       sync_all();
       if (tid == 0) {
@@ -597,7 +617,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       read64(trow, c0, p);
       probs(p, q, kb * 128 + c0, skv, a.causal != 0, live, a.scale, mi, inv);
       wait_stage(L, ph);
-      conv_rows(L.stg, 128, 128, dh, Vk.hi, Vk.lo, tid, kThreads, amax);
+      land(L, tm, TV, Vk.hi, Vk.lo, dh, tid, amax);
       fence_async_smem();
       sync_all();
       if (tid == 0) {
@@ -647,8 +667,11 @@ bool aligned(const Mat& m) {
 
 AttnTma long_maps(const AttnArgs& a, bool backward) {
   AttnTma t{};
+  t.hs_mask = (a.qkv_hs ? (1 << TQ) | (1 << TK) | (1 << TV) : 0) | (a.do_hs ? 1 << TDO : 0);
   auto mk = [&](int which, const Mat& m, int rows) {
-    t.m[which] = tc_make_map(m, a.G, a.Bb, a.H, rows, a.dh, 128, a.dh, false, &t.op[which]);
+    t.m[which] = ((t.hs_mask >> which) & 1)
+                     ? tc_make_map(m, a.G, a.Bb, a.H, rows, 64, 128, 32, true, &t.op[which])
+                     : tc_make_map(m, a.G, a.Bb, a.H, rows, a.dh, 128, a.dh, false, &t.op[which]);
   };
   mk(TQ, a.Q, a.sq);
   mk(TK, a.K, a.skv);
@@ -675,7 +698,10 @@ void launch_long(K kernel, const AttnTma& t, const AttnArgs& a, long long nprob,
 }  // namespace
 
 bool attn_long_supported(const AttnArgs& a, bool backward) {
-  if (a.qkv_hs || a.do_hs) return attn_flash_supported(a, backward);
+  if (!backward && (a.qkv_hs || a.do_hs)) return attn_flash_supported(a, backward);
+  if (backward && a.do_hs) return attn_flash_supported(a, true);
+  if (a.do_hs) return false;  // the row dot t_i = dO_i . O_i reads fp32 dO
+  if (a.qkv_hs && a.dh != 64) return false;
   if (a.sq < 128 || a.skv < 128 || a.sq > 512 || a.skv > 512) return false;
   if (a.dh != 32 && a.dh != 64) return false;
   if (!a.P.ok() || !aligned(a.Q) || !aligned(a.K) || !aligned(a.V) || !aligned(a.O) ||
@@ -700,6 +726,7 @@ void launch_attn_fwd_long(const AttnArgs& a, const int* active, cudaStream_t s) 
 }
 
 void launch_attn_bwd_long(const AttnArgs& a, const int* active, cudaStream_t s) {
+  if (a.do_hs) return launch_attn_bwd_flash(a, active, s);  // pre-split dO: attn_flash.cu
   if (!attn_long_supported(a, true)) throw ContractViolation("attn_bwd_long: unsupported shape");
   static bool attr = [] {
     MGLP_CUDA(cudaFuncSetAttribute(attn_bwd_dkdv_kernel,

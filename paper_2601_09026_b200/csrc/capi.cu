@@ -1026,10 +1026,21 @@ mglp_status mglp_test_attention(int B, int H, int sq, int skv, int dh, int causa
     need(P, "P");
     const int p_hl = (causal >> 1) & 1;  // bit 1: P kept pre-split (s = 128)
     const int hs = (causal >> 2) & 1;    // bit 2: Q, K, V, dO head-split pre-split
+    const int flash = (causal >> 3) & 1;  // bit 3 (long, with bit 2): single-pass backward
     causal &= 1;
     AttnArgs a = attn_args(B, H, sq, skv, dh, causal, Q, K, V, ld, O, P, dO, dQ, dK, dV);
     a.p_hl = p_hl;
-    a.qkv_hs = a.do_hs = hs;
+    a.qkv_hs = hs;
+    // the long backward's row dot reads fp32 dO; the single-pass one pre-split dO
+    a.do_hs = hs && ((sq <= 128 && skv <= 128) || flash);
+    float* dsbuf = nullptr;
+    if (hs && flash && dO) {  // the dS tile-pair store of the single-pass backward
+      const long long per_head = (long long)((sq + 63) / 64) * ((skv + 127) / 128) * 8192;
+      MGLP_CUDA(cudaMalloc(&dsbuf, (size_t)B * H * per_head * sizeof(float)));
+      a.dS.ptr = dsbuf;
+      a.dS.hstride = per_head;
+      a.dS.bstride = (long long)H * per_head;
+    }
     const bool bwd = dO != nullptr;
     const bool shortp = attn_tc_supported(a, bwd);
     if (!shortp && !attn_long_supported(a, bwd))
@@ -1049,6 +1060,7 @@ mglp_status mglp_test_attention(int B, int H, int sq, int skv, int dh, int causa
       if (bwd) launch_attn_bwd_long(a, nullptr, 0);
     }
     MGLP_CUDA(cudaDeviceSynchronize());
+    if (dsbuf) cudaFree(dsbuf);
     int flag = 0;
     MGLP_CUDA(cudaMemcpy(&flag, dflag, sizeof(int), cudaMemcpyDeviceToHost));
     cudaFree(dflag);
@@ -1085,7 +1097,18 @@ mglp_status mglp_bench_attention(int G, int B, int H, int s, int dh, int causal,
     // 2 forward without P (s <= 128), 3 as 2 with O written pre-split only;
     // + 4: Q, K, V, dO head-split pre-split (dh = 64)
     const int mode = backward & 3;
-    a.qkv_hs = a.do_hs = (backward >> 2) & 1;
+    a.qkv_hs = (backward >> 2) & 1;
+    const bool flash = ((backward >> 3) & 1) && a.qkv_hs && s > 128;
+    a.do_hs = a.qkv_hs && (s <= 128 || flash);
+    float* dsbuf = nullptr;
+    if (flash) {
+      const long long per_head = (long long)((s + 63) / 64) * ((s + 127) / 128) * 8192;
+      MGLP_CUDA(cudaMalloc(&dsbuf, (size_t)G * B * H * per_head * sizeof(float)));
+      a.dS.ptr = dsbuf;
+      a.dS.hstride = per_head;
+      a.dS.bstride = (long long)H * per_head;
+      a.dS.slot_stride = (long long)B * H * per_head;
+    }
     backward = mode == 1;
     const bool shortp = attn_tc_supported(a, backward != 0);
     if (!shortp && !attn_long_supported(a, backward != 0))
@@ -1122,7 +1145,7 @@ mglp_status mglp_bench_attention(int G, int B, int H, int s, int dh, int causal,
     *ms_per_launch = ms / reps;
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
-    for (float* p : {qkv, O, P, dO, dqkv}) cudaFree(p);
+    for (float* p : {qkv, O, P, dO, dqkv, dsbuf}) cudaFree(p);
   });
 }
 

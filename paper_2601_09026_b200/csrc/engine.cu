@@ -959,13 +959,23 @@ Mat Engine::dgrad_hl(int G, int which, int cols) const {
   return off ? Mat{} : hl_mat(G, which, cols);
 }
 
-bool Engine::attn_hs(int sq, int skv) const {
+bool Engine::attn_hs(int sq, int skv, bool grad) const {
   static const bool off = [] {
     const char* e = getenv("MGLP_NO_ATTN_HS");
     return e && atoi(e) != 0;
   }();
-  return !off && use_fused_attn() && sd_.d == 64 * sd_.heads && sq <= 128 && skv <= 128 &&
-         sq % 8 == 0 && skv % 8 == 0;
+  if (off || !use_fused_attn() || sd_.d != 64 * sd_.heads) return false;
+  if (sq <= 128 && skv <= 128) return sq % 8 == 0 && skv % 8 == 0;  // attn_tc.cu
+  // 128 < s <= 512 (attn_flash.cu): Q, K, V for the single-pass forward; dO for
+  // the single-pass backward, which stores its dS tiles in the dP slot (self-
+  // attention, whole blocks per head: allocated so); MGLP_FLASH_BWD=0 keeps
+  // the long backward (fp32 dO)
+  static const bool flash_bwd = [] {
+    const char* e = getenv("MGLP_FLASH_BWD");
+    return !(e && atoi(e) == 0);
+  }();
+  if (!use_long_attn() || sq <= 128 || skv <= 128 || sq > 512 || skv > 512) return false;
+  return !grad || (flash_bwd && sq == skv);
 }
 
 bool Engine::attention_fwd(int G, Mat Q, Mat K, Mat V, Mat O, Mat P, int sq, int skv,
@@ -1019,7 +1029,7 @@ bool Engine::attention_fwd(int G, Mat Q, Mat K, Mat V, Mat O, Mat P, int sq, int
       timed(PROF_ATTN, fl, 0.0, [&] { launch_attn_fwd(at, active_, stream_); });
       return hl;
     }
-    if (qkv_hs) throw ContractViolation("attention: pre-split Q/K/V need the fused s <= 128 kernel");
+
     if (use_long_attn() && attn_long_supported(at, false)) {
       // longer sequences: P is recomputed by the backward from per-row
       // statistics stored in the P slot (attn_long.cu)
@@ -1030,6 +1040,7 @@ bool Engine::attention_fwd(int G, Mat Q, Mat K, Mat V, Mat O, Mat P, int sq, int
       return hl;
     }
   }
+  if (qkv_hs) throw ContractViolation("attention: pre-split Q/K/V need a fused kernel");
   GemmArgs g;
   g.G = G;
   g.Bb = B_;
@@ -1134,31 +1145,32 @@ bool Engine::attention_bwd(int G, Mat Q, Mat K, Mat V, Mat P, Mat O, Mat dO, Mat
       timed(PROF_ATTN, fl, 0.0, [&] { launch_attn_bwd(at, active_, stream_); });
       return hl;
     }
-    if (qkv_hs || do_hs)
-      throw ContractViolation("attention: pre-split operands need the fused s <= 128 kernel");
+
+    // whole 128-blocks: the long dK/dV kernel stores its dS tiles (pre-split)
+    // in the dP slot and dQ reads them (MGLP_LONG_DS=0 recomputes S, P, dP
+    // instead); the single-pass backward (pre-split dO) always does
+    static const bool ds_on = [] {
+      const char* e = getenv("MGLP_LONG_DS");
+      return !(e && atoi(e) == 0);
+    }();
+    // self-attention: the dP slot holds whole-block tiles per head (padded
+    // at allocation); cross-attention only when the blocks tile it exactly
+    if (do_hs || (ds_on && (sq == skv || (sq % 128 == 0 && skv % 128 == 0 && dP.ld == skv)))) {
+      const long long per_head = (long long)((sq + 127) / 128) * ((skv + 127) / 128) * 128 * 128;
+      Mat ds = dP;
+      ds.hstride = per_head;
+      ds.bstride = (long long)H * per_head;
+      at.dS = ds;
+    }
     if (use_long_attn() && attn_long_supported(at, true)) {
       const bool hl = with_hl();
-      // whole 128-blocks: dK/dV stores its dS tiles (pre-split) in the dP
-      // slot and dQ reads them (MGLP_LONG_DS=0 recomputes S, P, dP instead)
-      static const bool ds_on = [] {
-        const char* e = getenv("MGLP_LONG_DS");
-        return !(e && atoi(e) == 0);
-      }();
-      // self-attention: the dP slot holds whole-block tiles per head (padded
-      // at allocation); cross-attention only when the blocks tile it exactly
-      if (ds_on && (sq == skv || (sq % 128 == 0 && skv % 128 == 0 && dP.ld == skv))) {
-        const long long per_head = (long long)((sq + 127) / 128) * ((skv + 127) / 128) * 128 * 128;
-        Mat ds = dP;
-        ds.hstride = per_head;
-        ds.bstride = (long long)H * per_head;
-        at.dS = ds;
-      }
       ++launches_;
       prof_shape_ = {-sq, skv, dh, G * B_ * H};
       timed(PROF_ATTN, fl, 0.0, [&] { launch_attn_bwd_long(at, active_, stream_); });
       return hl;
     }
   }
+  if (qkv_hs || do_hs) throw ContractViolation("attention: pre-split operands need a fused kernel");
   auto mk = [&](int M, int N, int K_, Mat A, bool amn, Mat B, bool bmn, Mat out, float alpha) {
     GemmArgs g;
     g.G = G;
@@ -1786,12 +1798,12 @@ void Engine::encoder_adjoint(const EvalSpec& e, bool causal) {
     timed(PROF_ROW, 0.0, 20.0 * lb.G * (double)lb.rows * lb.d,
           [&] { launch_ln_bwd(lb, active_, stream_); });
 
-    const bool hs = attn_hs(R / B_, R / B_);
+    const bool hs = attn_hs(R / B_, R / B_), dhs = attn_hs(R / B_, R / B_, true);
     g = mk(R, d, d, da1, L.w_o, d);
     g.Ahl = h_da1;
     g.ep.kind = EPI_STORE;
     g.ep.out1 = dctx;
-    g.ep.hs = hs ? 1 : 0;
+    g.ep.hs = dhs ? 1 : 0;
     g.ep.range_flag = range_flag_;
     gemm(g);
 
@@ -1799,7 +1811,7 @@ void Engine::encoder_adjoint(const EvalSpec& e, bool causal) {
     const bool dqkv_hl =
         attention_bwd(G, qkv, qkv.offset(d), qkv.offset(2 * d), Pm, ctx, dctx, dPm, dqkv,
                       dqkv.offset(d), dqkv.offset(2 * d), R / B_, R / B_, causal, h_dqkv,
-                      h_dqkv.offset(d), h_dqkv.offset(2 * d), keep32, hs, hs);
+                      h_dqkv.offset(d), h_dqkv.offset(2 * d), keep32, hs, dhs);
 
     g = mk(R, d, 3 * d, dqkv, L.w_qkv, d);
     if (dqkv_hl) g.Ahl = h_dqkv;
@@ -1992,16 +2004,16 @@ void Engine::decoder_adjoint(const EvalSpec& e) {
       timed(PROF_ROW, 0.0, 8.0 * G * (double)R * d,
             [&] { launch_mask_copy(G, R, d, dcp, dybar, dmask(2, l0, ls), active_, stream_); });
     }
-    const bool chs = attn_hs(sy_, sx_);
+    const bool chs = attn_hs(sy_, sx_), cdhs = attn_hs(sy_, sx_, true);
     g = mk(R, d, d, dcp, L.w_co, d);
     g.ep.kind = EPI_STORE;
     g.ep.out1 = dcctx;
-    g.ep.hs = chs ? 1 : 0;
+    g.ep.hs = cdhs ? 1 : 0;
     g.ep.range_flag = range_flag_;
     gemm(g);
 
     attention_bwd(G, cq, ckv, ckv.offset(d), cP, cctx, dcctx, dP2, dcq, dckv, dckv.offset(d), sy_,
-                  sx_, false, Mat{}, Mat{}, Mat{}, true, chs, chs);
+                  sx_, false, Mat{}, Mat{}, Mat{}, true, chs, cdhs);
 
     g = mk(R, d, d, dcq, L.w_cq, d);
     g.ep.kind = EPI_STORE;
@@ -2029,12 +2041,12 @@ void Engine::decoder_adjoint(const EvalSpec& e) {
     timed(PROF_ROW, 0.0, 20.0 * lb.G * (double)lb.rows * lb.d,
           [&] { launch_ln_bwd(lb, active_, stream_); });
 
-    const bool hs = attn_hs(sy_, sy_);
+    const bool hs = attn_hs(sy_, sy_), dhs = attn_hs(sy_, sy_, true);
     g = mk(R, d, d, da1, L.w_o, d);
     g.Ahl = h_da1;
     g.ep.kind = EPI_STORE;
     g.ep.out1 = dctx;
-    g.ep.hs = hs ? 1 : 0;
+    g.ep.hs = dhs ? 1 : 0;
     g.ep.range_flag = range_flag_;
     gemm(g);
 
@@ -2042,7 +2054,7 @@ void Engine::decoder_adjoint(const EvalSpec& e) {
     const bool dqkv_hl =
         attention_bwd(G, qkv, qkv.offset(d), qkv.offset(2 * d), Pm, ctx, dctx, dPm, dqkv,
                       dqkv.offset(d), dqkv.offset(2 * d), sy_, sy_, true, h_dqkv, h_dqkv.offset(d),
-                      h_dqkv.offset(2 * d), keep32, hs, hs);
+                      h_dqkv.offset(2 * d), keep32, hs, dhs);
 
     g = mk(R, d, 3 * d, dqkv, L.w_qkv, d);
     if (dqkv_hl) g.Ahl = h_dqkv;

@@ -307,7 +307,8 @@ class Engine {
   // O-projection dgrad write them so for the fused s <= 128 kernels, dh = 64.
   // A function of the shape only (forward and backward agree);
   // MGLP_NO_ATTN_HS=1 keeps them fp32.
-  bool attn_hs(int sq, int skv) const;
+  // grad: the dO operand of the backward (fused s <= 128 kernels only)
+  bool attn_hs(int sq, int skv, bool grad = false) const;
   // the family's pre-split activation buffer `which` (0: [rows][d] LN outputs,
   // 1: [rows][cols <= max(d, ffn)] attention O / GELU output; hi|lo' rows, the
   // next forward GEMM's A operand); empty when unavailable

@@ -238,5 +238,8 @@ void launch_attn_bwd_long(const AttnArgs& a, const int* active, cudaStream_t s);
 // statistics (max, 1/sum) as the long form
 bool attn_flash_supported(const AttnArgs& a, bool backward);
 void launch_attn_fwd_flash(const AttnArgs& a, const int* active, cudaStream_t s);
+// backward (qkv_hs and do_hs, fp32 O, AttnArgs::dS): t_q row dot, dK / dV per
+// 128-key block storing the dS tiles, dQ per 128-query block
+void launch_attn_bwd_flash(const AttnArgs& a, const int* active, cudaStream_t s);
 
 }  // namespace mglp

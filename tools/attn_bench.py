@@ -18,7 +18,7 @@ SHAPES = [  # name, G, B, H, s, dh, causal
 ]
 reps = int(sys.argv[1]) if len(sys.argv) > 1 else 10
 out = {}
-MODES = [int(x) for x in os.environ.get("MODES", "0,1,2,3,4,5").split(",")]
+MODES = [int(x) for x in os.environ.get("MODES", "0,1,2,3,4,5,13").split(",")]
 for name, G, B, H, s, dh, causal in SHAPES:
     for bwd in MODES:
         ms = C.c_float()
@@ -28,7 +28,7 @@ for name, G, B, H, s, dh, causal in SHAPES:
             print(f"{name} mode {bwd}: {e}")
             continue
         fl = (8.0 if (bwd & 3) == 1 else 4.0) * G * B * H * s * s * dh * (0.5 if causal else 1.0)
-        key = f"{name} {['fwd', 'bwd', 'fwd noP', 'fwd noP Ohl'][bwd & 3]}{' hs' if bwd & 4 else ''}"
+        key = f"{name} {['fwd', 'bwd', 'fwd noP', 'fwd noP Ohl'][bwd & 3]}{' hs' if bwd & 4 else ''}{' flash' if bwd & 8 else ''}"
         print(f"{key:24s} {ms.value:8.3f} ms  {fl / (ms.value * 1e-3) / 1e12:7.1f} TF/s", flush=True)
         out[key] = {"ms": ms.value, "tflops": fl / (ms.value * 1e-3) / 1e12}
 os.makedirs("gpurun_out", exist_ok=True)
