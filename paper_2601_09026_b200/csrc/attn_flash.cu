@@ -998,7 +998,7 @@ int n_sms() {
 }  // namespace
 
 bool attn_flash_supported(const AttnArgs& a, bool backward) {
-  if (!(a.qkv_hs && a.dh == 64 && a.sq > 128 && a.skv > 128 && a.sq <= 512 && a.skv <= 512 &&
+  if (!(a.qkv_hs && a.dh == 64 && a.sq >= 128 && a.skv >= 128 && a.sq <= 512 && a.skv <= 512 &&
         a.P.ok()))
     return false;
   // backward: pre-split dO, fp32 O (t_q) and the dS tile-pair store (a whole

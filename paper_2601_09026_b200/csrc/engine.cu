@@ -959,6 +959,16 @@ Mat Engine::dgrad_hl(int G, int which, int cols) const {
   return off ? Mat{} : hl_mat(G, which, cols);
 }
 
+// MGLP_FLASH128=1 (A/B): s = 128 self-attention through the single-pass
+// kernels (attn_flash.cu) instead of the on-chip fused ones (attn_tc.cu)
+static bool flash128() {
+  static const bool on = [] {
+    const char* e = getenv("MGLP_FLASH128");
+    return e && atoi(e) != 0;
+  }();
+  return on;
+}
+
 bool Engine::attn_hs(int sq, int skv, bool grad) const {
   static const bool off = [] {
     const char* e = getenv("MGLP_NO_ATTN_HS");
@@ -1020,7 +1030,8 @@ bool Engine::attention_fwd(int G, Mat Q, Mat K, Mat V, Mat O, Mat P, int sq, int
       if (!keep_p) at.O = Mat{};
       return true;
     };
-    if (attn_tc_supported(at, false)) {
+    const bool f128 = flash128() && qkv_hs && sq == 128 && skv == 128 && dh == 64;
+    if (!f128 && attn_tc_supported(at, false)) {
       // P is only an intermediate of the backward: not stored for scratch evaluations
       if (!keep_p) at.P = Mat{};
       const bool hl = with_hl();
@@ -1138,7 +1149,8 @@ bool Engine::attention_bwd(int G, Mat Q, Mat K, Mat V, Mat P, Mat O, Mat dO, Mat
       if (!keep32) at.dQ = at.dK = at.dV = Mat{};
       return true;
     };
-    if (attn_tc_supported(at, true)) {
+    const bool f128 = flash128() && do_hs && sq == 128 && skv == 128 && dh == 64;
+    if (!f128 && attn_tc_supported(at, true)) {
       const bool hl = with_hl();
       ++launches_;
       prof_shape_ = {-sq, skv, dh, G * B_ * H};
