@@ -974,16 +974,22 @@ void launch_gemm_tc(const GemmArgs& a, const int* active, cudaStream_t s) {
   if (a.G == 0 || a.M == 0 || a.N == 0) return;
   if (a.K == 0) throw ContractViolation("gemm_tc: K must be positive");
   Prepared P = prepare(a);
-  // MGLP_GEMM_DRAIN=0: the pair kernel releases TMEM only after its epilogue
-  static const bool drain = [] {
+  // MGLP_GEMM_DRAIN=0: the pair kernel releases TMEM only after its epilogue;
+  // 1: drain converter-free launches with K <= 1024 only; 2: every
+  // converter-free launch; 3 (default): K <= 1024, and long K when the
+  // epilogue is the MGRIT combine (EPI_FINAL)
+  static const int drain = [] {
     const char* e = getenv("MGLP_GEMM_DRAIN");
-    return !(e && atoi(e) == 0);
+    return e ? atoi(e) : 3;
   }();
   if (use_pair(a)) {
-    // measured (tools/gpu_drain_diag.sh): draining wins where the epilogue is
-    // large against the K loop (K = 768: MLP-in, QKV), the full-depth rings
-    // win for long K (K = 3072: MLP-out -7%)
-    if (drain && P.p.a_direct && a.K <= 1024)
+    // measured (tools/gpu_drain_diag.sh, same box): draining wins where the
+    // epilogue is large against the K loop (K = 768: MLP-in, QKV) and for the
+    // MGRIT-combine epilogue at K = 3072 (MLP-out family 14.8 -> 13.6 ms per
+    // BERT step); the full-depth rings win for the other long-K shapes
+    // (MLP-in dgrad K = 3072: 12.4 vs 12.9 ms)
+    const bool long_k_ok = drain == 2 || (drain == 3 && a.ep.kind == EPI_FINAL);
+    if (drain && P.p.a_direct && (a.K <= 1024 || long_k_ok))
       launch_cg<2, 1>(a, active, s, P);
     else
       launch_cg<2, 0>(a, active, s, P);
