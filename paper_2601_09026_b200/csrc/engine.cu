@@ -155,6 +155,7 @@ Engine::~Engine() {
   if (mon_) cudaFree(mon_);
   if (mon_sum_) cudaFree(mon_sum_);
   if (mon_host_) cudaFreeHost(mon_host_);
+  if (grad_pin_) cudaFreeHost(grad_pin_);
   for (float** p : {&P_, &Whl_, &Gr_, &scratch_, &hlscr_, &cache_, &bscratch_, &bcache_, &traj_,
                     &lam_all_, &zero_state_, &snap_fwd_, &snap_bwd_, &fwd_stash_})
     dfree(*p);
@@ -548,24 +549,66 @@ long long Engine::flat_offset(int layer) const {
   return fo;
 }
 
+// Gradients -> host f64 accumulation (+=), the reference's BlockParams
+// contract: owned layers only (a P-rank engine's other layers add 0), in
+// chunks of layers through two pinned staging buffers -- the DMA of chunk k+1
+// overlaps the multithreaded scatter-add of chunk k (layers are disjoint flat
+// ranges, so threads split them without synchronisation).
 void Engine::get_grads_range(int lo, int hi, double* flat) const {
   if (lo < 0 || hi > total_ || lo > hi) throw ValidationError("get_grads: bad layer range");
+  MGLP_CUDA(cudaSetDevice(device_));
   MGLP_CUDA(cudaStreamSynchronize(stream_));
-  // a P-rank engine holds its own layers' gradients (the others add 0)
-  std::vector<float> host((size_t)(hi - lo) * layer_stride_, 0.f);
-  for (const auto& x : clip(lay_r_, lo, hi))
-    MGLP_CUDA(cudaMemcpy(host.data() + (x.first - lo) * layer_stride_,
-                         Gr_ + x.first * layer_stride_,
-                         (size_t)(x.second - x.first) * layer_stride_ * sizeof(float),
-                         cudaMemcpyDeviceToHost));
-  long long fo = 0;
-  for (int l = lo; l < hi; ++l) {
-    const LayerLayout& L = lay_[(sd_.kind == 2 && l >= n_split_) ? 1 : 0];
-    const float* src = host.data() + (size_t)(l - lo) * layer_stride_;
-    for (const Piece& p : L.pieces)
-      for (long long e = 0; e < p.n; ++e) flat[fo + p.flat_off + e] += src[p.dev_off + e];
-    fo += L.flat_size;
+  constexpr long long kChunk = 4;  // layers per staging buffer
+  if (!grad_pin_) {
+    MGLP_CUDA(cudaMallocHost(&grad_pin_, (size_t)(2 * kChunk * layer_stride_) * sizeof(float)));
+    grad_pin_layers_ = kChunk;
   }
+  // flat offset of every layer of [lo, hi)
+  std::vector<long long> fo((size_t)(hi - lo + 1), 0);
+  for (int l = lo; l < hi; ++l)
+    fo[l - lo + 1] = fo[l - lo] + lay_[(sd_.kind == 2 && l >= n_split_) ? 1 : 0].flat_size;
+  // owned layers of [lo, hi) in chunks
+  std::vector<std::pair<int, int>> chunks;
+  for (const auto& x : clip(lay_r_, lo, hi))
+    for (long long c = x.first; c < x.second; c += kChunk)
+      chunks.emplace_back((int)c, (int)std::min<long long>(x.second, c + kChunk));
+  if (chunks.empty()) return;
+  cudaEvent_t ev[2];
+  for (auto& e : ev) MGLP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  auto issue = [&](size_t k) {
+    float* dst = grad_pin_ + (k & 1) * kChunk * layer_stride_;
+    const int a = chunks[k].first, b = chunks[k].second;
+    MGLP_CUDA(cudaMemcpyAsync(dst, Gr_ + (long long)a * layer_stride_,
+                              (size_t)(b - a) * layer_stride_ * sizeof(float),
+                              cudaMemcpyDeviceToHost, stream_));
+    MGLP_CUDA(cudaEventRecord(ev[k & 1], stream_));
+  };
+  const int nth = (int)std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+  issue(0);
+  for (size_t k = 0; k < chunks.size(); ++k) {
+    MGLP_CUDA(cudaEventSynchronize(ev[k & 1]));
+    if (k + 1 < chunks.size()) issue(k + 1);  // the other buffer: consumed in step k-1
+    const float* buf = grad_pin_ + (k & 1) * kChunk * layer_stride_;
+    const int a = chunks[k].first, b = chunks[k].second;
+    auto work = [&](int t) {
+      for (int l = a; l < b; ++l) {
+        const LayerLayout& L = lay_[(sd_.kind == 2 && l >= n_split_) ? 1 : 0];
+        const float* src = buf + (size_t)(l - a) * layer_stride_;
+        double* dst = flat + fo[l - lo];
+        for (const Piece& p : L.pieces) {
+          // piece split evenly over the threads
+          const long long per = (p.n + nth - 1) / nth, e0 = t * per,
+                          e1 = std::min<long long>(p.n, e0 + per);
+          for (long long e = e0; e < e1; ++e) dst[p.flat_off + e] += src[p.dev_off + e];
+        }
+      }
+    };
+    std::vector<std::thread> th;
+    for (int t = 1; t < nth; ++t) th.emplace_back(work, t);
+    work(0);
+    for (auto& x : th) x.join();
+  }
+  for (auto& e : ev) cudaEventDestroy(e);
 }
 
 void Engine::zero_grads() { dmemset(Gr_, layer_stride_, lay_r_); }

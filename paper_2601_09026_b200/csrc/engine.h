@@ -85,6 +85,9 @@ class Engine {
   void get_grads(double* flat_accum) const;  // flat += device grads
   // flat (covering layers [lo, hi) only, visit_params order) += their grads
   void get_grads_range(int lo, int hi, double* flat_accum) const;
+  // pinned double-buffered staging of the gradient download (get_grads_range)
+  mutable float* grad_pin_ = nullptr;
+  mutable long long grad_pin_layers_ = 0;
   long long flat_offset(int layer) const;  // first flat index of `layer`
   void zero_grads();
   // device parameter / gradient slabs (fp32, layer-major, kernel layout) and
