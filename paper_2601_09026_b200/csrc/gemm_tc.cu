@@ -138,6 +138,35 @@ __device__ __forceinline__ void regroup_tile(uint32_t stg, uint32_t hl, int kc, 
   }
 }
 
+// The same regroup from a SWIZZLE_128B staging: the MN-major pre-split rows
+// arrive as four [32 K rows][32 M columns] boxes (each 128-byte row = 32 hi |
+// 32 lo' fp16; box j = M columns 32 j ..), so every 8 K rows x 8 M values of
+// one half are an 8x8 b16 matrix whose 16-byte rows sit in distinct bank
+// groups: ldmatrix .trans reads them conflict-free and hands each thread two
+// consecutive K values of one M row (4 bytes of the K-major output chunk).
+// Converter warp kc: K rows kc*8 .. +7, all 128 M rows, both halves.
+__device__ __forceinline__ void regroup_tile_sw(uint32_t stg, uint32_t hl, int kc, int lane) {
+  const int krow = kc * 8 + (lane & 7);
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {  // 8 x 4 matrices = 16 M blocks of 8 x {hi, lo'}
+    const int g = 4 * c + (lane >> 3);       // the matrix this lane addresses a row of
+    const int mb = g & 15, part = g >> 4;    // M block, half
+    const int ch = (mb & 3) + 4 * part;      // 16-byte chunk within the staging row
+    const uint32_t addr = stg + (mb >> 2) * 4096 + krow * 128 + ((ch ^ (krow & 7)) << 4);
+    uint32_t d[4];
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(d[0]), "=r"(d[1]), "=r"(d[2]), "=r"(d[3])
+                 : "r"(addr));
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int gi = 4 * c + i, mbi = gi & 15, pi = gi >> 4;
+      const int M = mbi * 8 + (lane >> 2);  // K values 2 (lane & 3), +1 of M row M
+      const uint32_t o = hl + M * 128 + (((pi * 4 + kc) ^ (M & 7)) << 4) + (lane & 3) * 4;
+      asm volatile("st.shared.b32 [%0], %1;" ::"r"(o), "r"(d[i]) : "memory");
+    }
+  }
+}
+
 __device__ __forceinline__ void convert_tile(uint32_t stg, uint32_t hl, bool mn, int kc,
                                              int lane, float& amax) {
   // all staging loads first (the compiler cannot reorder them across the
@@ -340,17 +369,31 @@ __global__ void __launch_bounds__(Cfg<CG>::THREADS, 1)
           mbar_expect_tx(&fullA[s], bytes);
           const int k0 = kb * BK;
           int c[5];
-          if (!p.a_mn)
-            tma_coords(p.a, k0, T.m0, T.g, T.b, T.h, c);
-          else
-            tma_coords(p.a, T.m0, k0, T.g, T.b, T.h, c);
-          tma_load_5d(stg_a(s), &mapA, &fullA[s], c);
-          if (!p.b_direct) {
-            if (!p.b_mn)
-              tma_coords(p.b, k0, nb0, T.g, T.b, T.h, c);
+          if (p.a_hl) {  // four swizzled [32][32] boxes (regroup_tile_sw)
+            for (int j = 0; j < 4; ++j) {
+              tma_coords(p.a, T.m0 + 32 * j, k0, T.g, T.b, T.h, c);
+              tma_load_5d(stg_a(s) + j * 4096, &mapA, &fullA[s], c);
+            }
+          } else {
+            if (!p.a_mn)
+              tma_coords(p.a, k0, T.m0, T.g, T.b, T.h, c);
             else
-              tma_coords(p.b, nb0, k0, T.g, T.b, T.h, c);
-            tma_load_5d(stg_b(s), &mapB, &fullA[s], c);
+              tma_coords(p.a, T.m0, k0, T.g, T.b, T.h, c);
+            tma_load_5d(stg_a(s), &mapA, &fullA[s], c);
+          }
+          if (!p.b_direct) {
+            if (p.b_hl) {
+              for (int j = 0; j < 4; ++j) {
+                tma_coords(p.b, nb0 + 32 * j, k0, T.g, T.b, T.h, c);
+                tma_load_5d(stg_b(s) + j * 4096, &mapB, &fullA[s], c);
+              }
+            } else {
+              if (!p.b_mn)
+                tma_coords(p.b, k0, nb0, T.g, T.b, T.h, c);
+              else
+                tma_coords(p.b, nb0, k0, T.g, T.b, T.h, c);
+              tma_load_5d(stg_b(s), &mapB, &fullA[s], c);
+            }
           }
         }
       }
@@ -458,12 +501,12 @@ __global__ void __launch_bounds__(Cfg<CG>::THREADS, 1)
         if (kc == 0 && lane == 0) flush(6);
         if (!(p.debug & 1)) {
           if (p.a_hl)
-            regroup_tile(smem_u32(stg_a(sa)), smem_u32(hl_a(s)), kc, lane);
+            regroup_tile_sw(smem_u32(stg_a(sa)), smem_u32(hl_a(s)), kc, lane);
           else
             convert_tile(smem_u32(stg_a(sa)), smem_u32(hl_a(s)), p.a_mn, kc, lane, amax);
           if (!p.b_direct) {
             if (p.b_hl)
-              regroup_tile(smem_u32(stg_b(sa)), smem_u32(hl_b(s)), kc, lane);
+              regroup_tile_sw(smem_u32(stg_b(sa)), smem_u32(hl_b(s)), kc, lane);
             else
               convert_tile(smem_u32(stg_b(sa)), smem_u32(hl_b(s)), p.b_mn, kc, lane, amax);
           }
@@ -892,15 +935,17 @@ Prepared prepare(const GemmArgs& a) {
     const int kpa = ceil_div(a.K, BK) * BK;  // packed row: hi|lo per 32-wide K block
     P.mA = make_map(a.Ahl, a.G, a.Bb, a.H, a.M, kpa, ROWS, BK, true, &p.a);
   } else {
-    P.mA = a.a_mn ? make_map(a.A, a.G, a.Bb, a.H, a.K, a.M, BK, ROWS, false, &p.a)
-                  : make_map(a.A, a.G, a.Bb, a.H, a.M, a.K, ROWS, BK, true, &p.a);
+    P.mA = p.a_hl  ? make_map(a.A, a.G, a.Bb, a.H, a.K, a.M, BK, 32, true, &p.a)
+           : a.a_mn ? make_map(a.A, a.G, a.Bb, a.H, a.K, a.M, BK, ROWS, false, &p.a)
+                    : make_map(a.A, a.G, a.Bb, a.H, a.M, a.K, ROWS, BK, true, &p.a);
   }
   if (p.b_direct) {
     const int kp = ceil_div(a.K, BK) * BK;  // packed row: kp floats = kp hi + kp lo'
     P.mB = make_map(a.Bhl, a.G, a.Bb, a.H, a.N, kp, ROWS, BK, true, &p.b);
   } else {
-    P.mB = a.b_mn ? make_map(a.B, a.G, a.Bb, a.H, a.K, a.N, BK, ROWS, false, &p.b)
-                  : make_map(a.B, a.G, a.Bb, a.H, a.N, a.K, ROWS, BK, true, &p.b);
+    P.mB = p.b_hl  ? make_map(a.B, a.G, a.Bb, a.H, a.K, a.N, BK, 32, true, &p.b)
+           : a.b_mn ? make_map(a.B, a.G, a.Bb, a.H, a.K, a.N, BK, ROWS, false, &p.b)
+                    : make_map(a.B, a.G, a.Bb, a.H, a.N, a.K, ROWS, BK, true, &p.b);
   }
   return P;
 }
