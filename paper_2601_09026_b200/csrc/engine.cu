@@ -1181,7 +1181,8 @@ bool Engine::attention_bwd(int G, Mat Q, Mat K, Mat V, Mat P, Mat O, Mat dO, Mat
     at.p_hl = p_hl_ok(sq, skv, P) ? 1 : 0;  // as the forward stored it
     at.qkv_hs = qkv_hs ? 1 : 0;
     at.do_hs = do_hs ? 1 : 0;
-    const double fl = 8.0 * G * B_ * H * (double)sq * skv * dh;
+    // algorithmic: causal problems count the lower triangle only (as the forward)
+    const double fl = 8.0 * G * B_ * H * (double)sq * skv * dh * (causal ? 0.5 : 1.0);
     // pre-split gradients for the QKV dgrad; fp32 only where a weight
     // gradient reads them
     auto with_hl = [&] {
