@@ -237,11 +237,15 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
   const uint32_t st2 = base + 128 * 64 * 4;     // second half of the staging
   const uint32_t T0 = base + 2 * 128 * 64 * 4;  // 64 KB
   const uint32_t T1 = T0 + PAIR128;             // 64 KB
-  const Opnd dOk{T0, T0 + TILE64, 128, false};            // dP: A
-  const Opnd dOm{T0, T0 + TILE64, 128, true};             // dV: B
-  const Opnd Vk{T0 + PAIR64, T0 + PAIR64 + TILE64, 128, false};  // dP: B
-  const Opnd dSk{T0, T0 + 2 * TILE64, 128, false};        // dQ: A
-  const Opnd dSm{T0, T0 + 2 * TILE64, 128, true};         // dK: A
+  // [dO | V] -> dS region of problem `it`: T0, or -- when every operand
+  // arrives pre-split and P too (the staging is then unused) -- T0 and the
+  // staging alternately, so the next problem's dO / V load under this one
+  const bool pp2 = a.qkv_hs && a.do_hs && a.p_hl && a.pingpong;
+  auto rbase = [&](int it) -> uint32_t { return (pp2 && (it & 1)) ? stg : T0; };
+  auto dOk_ = [&](int it) { return Opnd{rbase(it), rbase(it) + TILE64, 128, false}; };  // dP: A
+  auto Vk_ = [&](int it) {
+    return Opnd{rbase(it) + PAIR64, rbase(it) + PAIR64 + TILE64, 128, false};  // dP: B
+  };
   const Opnd Pm{T1, T1 + 2 * TILE64, 128, true};          // dV: A
   const Opnd Qm{T1, T1 + TILE64, 128, true};              // dK: B
   const Opnd Km{T1 + PAIR64, T1 + PAIR64 + TILE64, 128, true};  // dQ: B
@@ -249,23 +253,25 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
   uint64_t* st_full = &bars[0];
   uint64_t* m_bar = &bars[1];
   uint64_t* p_full = &bars[2];  // p_hl: the pre-split P tiles landed in T1
-  float* xch = reinterpret_cast<float*>(bars + 4);  // [2][128] row-sum exchange
+  uint64_t* dov_full = &bars[3];  // [2] (pp2) dO / V landed in region it & 1
+  float* xch = reinterpret_cast<float*>(bars + 8);  // [2][128] row-sum exchange
   uint32_t* tslot = reinterpret_cast<uint32_t*>(xch + 256);
   const int nprob = a.G * a.Bb * a.H;
 
   // pre-split operands (qkv_hs / do_hs) land straight in their tiles, once
   // those are free; fp32 ones go through the staging and are converted
   const bool hsq = a.qkv_hs != 0, hsd = a.do_hs != 0;
-  auto load_dov = [&](int z) {
+  auto load_dov = [&](int z, int it) {
     int g, b, h;
     problem_of(a, z, g, b, h);
     if (lane == 0) {
-      mbar_expect_tx(st_full, (hsd ? kHsBytes : (uint32_t)(sq * dh * 4)) +
-                                  (hsq ? kHsBytes : (uint32_t)(skv * dh * 4)));
-      if (hsd) tma_pair(dOk, tm, TDO, g, b, h, st_full);
-      else tma_box(stg, tm, TDO, g, b, h, st_full);
-      if (hsq) tma_pair(Vk, tm, TV, g, b, h, st_full);
-      else tma_box(st2, tm, TV, g, b, h, st_full);
+      uint64_t* bar = pp2 ? &dov_full[it & 1] : st_full;
+      mbar_expect_tx(bar, (hsd ? kHsBytes : (uint32_t)(sq * dh * 4)) +
+                              (hsq ? kHsBytes : (uint32_t)(skv * dh * 4)));
+      if (hsd) tma_pair(dOk_(it), tm, TDO, g, b, h, bar);
+      else tma_box(stg, tm, TDO, g, b, h, bar);
+      if (hsq) tma_pair(Vk_(it), tm, TV, g, b, h, bar);
+      else tma_box(st2, tm, TV, g, b, h, bar);
     }
     __syncwarp();
   };
@@ -296,6 +302,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
     mbar_init(st_full, 1);
     mbar_init(m_bar, 1);
     mbar_init(p_full, 1);
+    mbar_init(&dov_full[0], 1);
+    mbar_init(&dov_full[1], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) tmem_alloc(tslot, 512);
@@ -306,16 +314,29 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
   const uint32_t trow = tmem + ((uint32_t)(q4 * 32) << 16);
   const int r = q4 * 32 + lane;  // TMEM lane: query row (dP, dQ) or key row (dV, dK)
   float amax = 0.f;
-  if (warp == 0 && (int)blockIdx.x < nprob) load_dov(blockIdx.x);
+  if (warp == 0 && (int)blockIdx.x < nprob) load_dov(blockIdx.x, 0);
   if (phl && tid == 0 && (int)blockIdx.x < nprob) load_p(blockIdx.x);
 
   uint32_t stp = 0, mp = 0, pp = 0;  // barrier phases
-  for (int z = blockIdx.x; z < nprob; z += gridDim.x) {
+  int it = 0;
+  for (int z = blockIdx.x; z < nprob; z += gridDim.x, ++it) {
     int g, b, h;
     problem_of(a, z, g, b, h);
-    // (1) dO, V -> T0
-    mbar_wait(st_full, stp);
-    stp ^= 1;
+    const bool next = z + (int)gridDim.x < nprob;
+    const Opnd dOk = dOk_(it), Vk = Vk_(it);
+    const Opnd dOm{dOk.hi, dOk.lo, 128, true};                      // dV: B
+    const Opnd dSk{rbase(it), rbase(it) + 2 * TILE64, 128, false};  // dQ: A
+    const Opnd dSm{rbase(it), rbase(it) + 2 * TILE64, 128, true};   // dK: A
+    // (1) dO, V -> this problem's region
+    if (pp2) {
+      mbar_wait(&dov_full[it & 1], (it >> 1) & 1);
+      // the other region's dS was consumed by the previous problem's dQ / dK
+      // MMAs: the next problem's dO / V stream in under this whole problem
+      if (warp == 0 && next) load_dov(z + gridDim.x, it + 1);
+    } else {
+      mbar_wait(st_full, stp);
+      stp ^= 1;
+    }
     if (!hsd) conv_rows(stg, sq, 128, dh, dOk.hi, dOk.lo, tid, kThreads, amax);
     if (!hsq) conv_rows(st2, skv, skv16, dh, Vk.hi, Vk.lo, tid, kThreads, amax);
     fence_async_smem();  // staging reads ordered before the bulk copies that reuse it
@@ -426,8 +447,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
     __syncthreads();
     tc_after();
     // the staging is free (and T0 is not: the dS tiles feed dQ / dK)
-    const bool next = z + (int)gridDim.x < nprob;
-    if (warp == 0 && next && !hsq && !hsd) load_dov(z + gridDim.x);
+    if (warp == 0 && next && !hsq && !hsd) load_dov(z + gridDim.x, it + 1);
     if (tid == 0) {
       mma3(tmem, tmem + 64, dSk, Km, dh, skv16 >> 4);         // dQ = dS K
       mma3(tmem + 128, tmem + 192, dSm, Qm, dh, sq16 >> 4);   // dK = dS^T Q
@@ -441,7 +461,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
     mp ^= 1;
     tc_after();
     // T0 (dS) is free: pre-split dO / V go straight in under this epilogue
-    if (warp == 0 && next && (hsq || hsd)) load_dov(z + gridDim.x);
+    if (warp == 0 && next && (hsq || hsd) && !pp2) load_dov(z + gridDim.x, it + 1);
     // T1 (Q | K) is free: the next problem's P streams in under this epilogue
     if (phl && tid == 0 && next) load_p(z + gridDim.x);
     rows_out_hl(trow, trow + 64, a.dQ.ok() ? a.dQ.at(g, b, h) : nullptr,
@@ -525,7 +545,14 @@ void launch_attn_fwd(const AttnArgs& a, const int* active, cudaStream_t s) {
   MGLP_CUDA(cudaGetLastError());
 }
 
-void launch_attn_bwd(const AttnArgs& a, const int* active, cudaStream_t s) {
+void launch_attn_bwd(const AttnArgs& a_in, const int* active, cudaStream_t s) {
+  // MGLP_ATTN_PINGPONG=0 (A/B): one dO / V region, loaded under the epilogue
+  static const int pingpong = [] {
+    const char* e = getenv("MGLP_ATTN_PINGPONG");
+    return (e && atoi(e) == 0) ? 0 : 1;
+  }();
+  AttnArgs a = a_in;
+  a.pingpong = pingpong;
   if (!attn_tc_supported(a, true)) throw ContractViolation("attn_bwd: unsupported shape");
   static bool attr = [] {
     MGLP_CUDA(cudaFuncSetAttribute(attn_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,

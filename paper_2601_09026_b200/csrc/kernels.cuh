@@ -222,6 +222,7 @@ struct AttnArgs {
   // head-split pre-split form (common.cuh st_hs4; dh = 64): TMA'd straight
   // into the operand tiles, no fp32 staging or conversion in the kernel
   int qkv_hs = 0, do_hs = 0;
+  int pingpong = 1;  // s <= 128 backward: alternate the dO / V region (launch_attn_bwd)
   int* range_flag = nullptr;
 };
 bool attn_tc_supported(const AttnArgs& a, bool backward);
