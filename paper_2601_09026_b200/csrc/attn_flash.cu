@@ -1,23 +1,26 @@
-// Single-pass streamed attention for 128 < s <= 512 with head-split pre-split
-// operands (AttnArgs::qkv_hs / do_hs, dh = 64): the GPT-2-style causal decoder
-// (s = 512) and ViT (s = 197). The reference's attention / vjp_attention
-// (blocks.cpp:142-236; softmax_rows / vjp_softmax_rows, tensor.cpp:310-342).
+// Single-pass streamed attention for 128 <= s <= 512 with head-split
+// pre-split operands (AttnArgs::qkv_hs / do_hs, dh = 64): the GPT-2-style
+// causal decoder (s = 512) and ViT (s = 197). The reference's attention /
+// vjp_attention (blocks.cpp:142-236; softmax_rows / vjp_softmax_rows,
+// tensor.cpp:310-342).
 //
-// Forward (CTA = one (member, batch, head, 128-query block); two CTAs per SM,
-// 96 KB of shared memory and 256 TMEM columns each, so one CTA's softmax runs
-// under the other's MMAs):
-//   Q (hi|lo' tiles) once; 64-key blocks j of K and V double-buffered, all
-//   TMA'd straight into their tiles (no staging, no conversion);
-//   S_j = Q K_j^T -> TMEM [0,128) (main | 2^-11 correction);
-//   online softmax with a lazy max: the reference max m of a row moves only
-//   when a block raises the row max by more than kLazy (then O and the row
-//   sum are rescaled by exp(m_old - m_new)); P~_j = exp(S scale - m) split
-//   hi|lo' and written back into TMEM over S_j (fp16x2 packed columns);
-//   O += P~_j V_j with A = P~ from TMEM (tcgen05.mma ... [a-tmem]) -> TMEM
-//   [128,256); the epilogue writes O / l (fp32 and/or pre-split) and the row
-//   statistics (m, 1/l) the backward recomputes P = exp(S scale - m) / l from.
-// S is computed once (the two-pass form computed it twice) and no probability
-// tile ever goes through shared memory.
+// Forward (attn_fwd_flash_kernel): CTA = one (member, batch, head, 128-query
+// block), two CTAs per SM; warps 0-7 softmax (two threads per query row),
+// warp 8 MMA issue, warp 9 TMA. Q once, 64-key blocks of K (double-buffered)
+// and V TMA'd straight into their tiles; S_j = Q K_j^T into one of two TMEM
+// buffers; online softmax with a lazy reference max (it moves only when a
+// block raises the row max by more than kLazy; O and l are then rescaled);
+// P~_j = exp(S scale - m) written back into TMEM over S_j as fp16x2 columns
+// and used as the A operand of O += P~_j V_j (tcgen05.mma ... [a-tmem]); the
+// epilogue writes O / l and the row statistics (m, 1/l). S is computed once
+// and no probability tile goes through shared memory. The split's 2^-11
+// correction terms are folded into operands (one accumulator per product:
+// see the forward section below).
+//
+// Backward: flash_rowdot_kernel (t_q = dO_q . O_q), attn_bwd_kv_flash_kernel
+// (dK, dV per 128-key block with keys as TMEM lanes; every dS tile stored
+// pre-split), attn_bwd_q_flash_kernel (dQ = sum dS K per 128-query block).
+// Deterministic: no atomics.
 #include "attn_common.cuh"
 
 namespace mglp {
