@@ -401,6 +401,12 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
           for (int e = 0; e < 8; ++e) pv[cc * 8 + e] = 0.f;
         }
       }
+      // every P half-row is in registers and the dV MMA (m_bar) has read P:
+      // pre-split Q, K go straight into T1, their load under the dP reads
+      if (hsq) {
+        __syncthreads();
+        if (warp == 0) load_qk(g, b, h);
+      }
       float dp[64];
       float t = 0.f;
       if (any) {
@@ -419,9 +425,6 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(const __grid_cons
       xch[half * 128 + r] = t;
       tc_before();
       __syncthreads();  // also: dP / dV MMAs done -> T0 may take dS
-      // every P half-row is in registers and the dV MMA has read P: pre-split
-      // Q, K go straight into T1
-      if (warp == 0 && hsq) load_qk(g, b, h);
       t = xch[r] + xch[128 + r];
       if (any) {
 #pragma unroll
