@@ -157,9 +157,15 @@ __global__ void __launch_bounds__(kFwdThreads, 2)
   bar_sync();
   const uint32_t tmem = *tslot;
   float amax = 0.f;
+  // block-major problem order, heaviest (latest) causal query blocks first:
+  // a persistent CTA's problems z, z + grid, ... take every block index in
+  // turn (with z % nqb the block index was fixed per CTA whenever the grid is
+  // a multiple of nqb, and the CTAs holding the last query block ran 8/5 of
+  // the mean causal work)
+  const int heads = a.G * a.Bb * a.H;
   auto coords = [&](int z, int& g, int& b, int& h, int& qb) {
-    qb = nqb - 1 - z % nqb;  // heavier (later) causal query blocks first
-    int r = z / nqb;
+    qb = nqb - 1 - z / heads;
+    int r = z % heads;
     h = r % a.H;
     r /= a.H;
     b = r % a.Bb;
@@ -561,9 +567,10 @@ __global__ void __launch_bounds__(kKvThreads, 1)
   bar_sync();
   const uint32_t tmem = *tslot;
   float amax = 0.f;
-  auto coords = [&](int z, int& g, int& b, int& h, int& kb) {
-    kb = z % nkb;
-    int r = z / nkb;
+  const int heads = a.G * a.Bb * a.H;
+  auto coords = [&](int z, int& g, int& b, int& h, int& kb) {  // block-major, heaviest first
+    kb = z / heads;
+    int r = z % heads;
     h = r % a.H;
     r /= a.H;
     b = r % a.Bb;
@@ -882,9 +889,10 @@ __global__ void __launch_bounds__(kQThreads, 1)
   bar_sync();
   const uint32_t tmem = *tslot;
   float amax = 0.f;
-  auto coords = [&](int z, int& g, int& b, int& h, int& qb) {
-    qb = nqb - 1 - z % nqb;
-    int r = z / nqb;
+  const int heads = a.G * a.Bb * a.H;
+  auto coords = [&](int z, int& g, int& b, int& h, int& qb) {  // block-major, heaviest first
+    qb = nqb - 1 - z / heads;
+    int r = z % heads;
     h = r % a.H;
     r /= a.H;
     b = r % a.Bb;
