@@ -444,39 +444,53 @@ __global__ void __launch_bounds__(kFwdThreads, 2)
 // accumulate over 64-query blocks in TMEM and every dS tile is stored
 // pre-split for the dQ kernel, which sums dQ = dS K per 128-query block.
 // Keys are the TMEM lanes (S^T = K Q^T, M = 128 keys, N = 64 queries):
-//   S^T  = K_hi Q_hi + K_lo'' Q_hi + K_hi'' Q_lo'      (K forms made once per CTA problem)
-//   dP^T = V_hi dO_hi + V_lo'' dO_hi + V_hi'' dO_lo'   (V likewise)
+//   S^T  = K_hi Q_hi + 2^-11 (K_lo' Q_hi + K_hi Q_lo')       one accumulator each: the
+//   dP^T = V_hi dO_hi + 2^-11 (V_lo' dO_hi + V_hi dO_lo')    correction products go
+//          first and the first main MMA scales them (tcgen05.mma scale-input-d = 11:
+//          D = A B + D 2^-11), so K, V are used exactly as TMA lands them
 //   P^T  = exp(S^T scale - m_q) / l_q (the forward's row statistics), dS^T = P^T (dP^T - t_q)
-//   dV  += P_hi dO_hi + P_lo'' dO_hi + P_hi'' dO_lo'   (A = P^T from TMEM)
-//   dK  += dS_hi Q_hi + 2^-11 (dS_lo' Q_hi + dS_hi Q_lo')  (two accumulators: dS is a
-//          gradient and may be small, so its 2^-11 stays in the accumulation)
+//   dV  += P_hi dO_hi + 2^-11 (P_lo' dO_hi + P_hi dO_lo')    (A = P^T from TMEM; main and
+//   dK  += dS_hi Q_hi + 2^-11 (dS_lo' Q_hi + dS_hi Q_lo')     correction accumulators)
 // t_q = dO_q . O_q comes from flash_rowdot_kernel first.
+//
+// Pipeline: one step = one 64-query block of one problem; steps are numbered
+// globally over the CTA's problems (k), so every barrier phase is a function
+// of k and nothing drains between problems: the next K, V land once the last
+// S^T / dP^T of the current problem have read theirs (under its last softmax
+// step), and the dV / dK epilogue of a problem runs while the next problem's
+// first S^T / dP^T are computed. Four query stages (Q, dO, statistics): step
+// k's loads go out once step k-4's gradient MMAs are done.
 constexpr int kKvThreads = 576;  // warps 0-15 compute, 16 MMA issue, 17 TMA
 constexpr int kQB = 64;          // queries per step
 constexpr int QT = kQB * 128;    // one 64-row hi (or lo') tile: 8 KiB
-// smem: K hi | lo'' | hi'' (16 KiB each) | V likewise | Q[3] (hi|lo', 16 KiB) | dO[3] | stats[3]
-// (three query stages: step j's loads go out once step j-3 is done, a whole
-// step ahead of when S_j can start)
-constexpr int kKvOff = 6 * 16384 + 6 * 2 * QT;
-constexpr int kKvSmem = 1024 + kKvOff + 3 * 1024 + 128 + 16;
-// TMEM: S/P~ [0,96) [96,192); dP/dS [192,256) [256,320); dV [320,384); dK main [384,448), corr [448,512)
-__device__ __forceinline__ uint32_t tsb(int s) { return s ? 96u : 0u; }
-__device__ __forceinline__ uint32_t tdb(int s) { return s ? 256u : 192u; }
-constexpr uint32_t kTdV = 320, kTdK = 384, kTdKc = 448;
+constexpr int kSt = 4;           // query stages
+// smem: K hi | lo' (16 KiB each) | V likewise | Q[4] (hi|lo', 16 KiB) | dO[4] | stats[4]
+constexpr int kKvOff = 4 * 16384 + kSt * 4 * QT;
+constexpr int kKvSmem = 1024 + kKvOff + kSt * 1024 + 256 + 16;
+// TMEM: S/P~ [0,64) [64,128); dP/dS [128,192) [192,256); dV main [256,320), corr [320,384);
+//       dK main [384,448), corr [448,512)
+__device__ __forceinline__ uint32_t tsb(int s) { return s ? 64u : 0u; }
+__device__ __forceinline__ uint32_t tdb(int s) { return s ? 192u : 128u; }
+constexpr uint32_t kTdV = 256, kTdVc = 320, kTdK = 384, kTdKc = 448;
 
-// x *= 2^-11 over `bytes` of fp16 (dst may equal src), threads [tid, nthr)
-__device__ __forceinline__ void scale_copy(uint32_t dst, uint32_t src, int bytes, int tid, int nthr) {
-  const __half2 sc = __float2half2_rn(kLo2);
-  for (int c = tid * 16; c < bytes; c += nthr * 16) {
-    uint4 v = lds128u(src + c);
-    uint32_t* w = &v.x;
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const __half2 x = __hmul2(*reinterpret_cast<const __half2*>(&w[e]), sc);
-      w[e] = *reinterpret_cast<const uint32_t*>(&x);
-    }
-    sts128(dst + c, v);
-  }
+// D = A . B^T + D 2^-11 (scale-input-d), both operands in shared memory
+__device__ __forceinline__ void mma_ss_scaled(uint32_t d, const Opnd& A, const Opnd& B, int k,
+                                              uint32_t id) {
+  const uint32_t oa = A.at(k), ob = B.at(k);
+  asm volatile(
+      "{\n\t"
+      ".reg .pred p;\n\t"
+      "setp.eq.u32 p, 1, 1;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p, 11;\n\t"
+      "}" ::"r"(d),
+      "l"(desc_sw128(A.hi + oa, A.lbo())), "l"(desc_sw128(B.hi + ob, B.lbo())), "r"(id));
+}
+
+// 32 lanes x 8 columns into TMEM (this warp's lane quarter)
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t* r) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr),
+               "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+               : "memory");
 }
 
 // MGLP_FLASH_TRACE (diagnostics): clock64 stamps of CTA 0 of the dK/dV kernel
@@ -534,33 +548,30 @@ __global__ void __launch_bounds__(kKvThreads, 1)
   if (active && *(volatile const int*)active == 0) return;
   uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
   const uint32_t base = smem_u32(smem);
-  const uint32_t khi = base, klo = base + 16384, khi2 = base + 32768;
-  const uint32_t vhi = base + 49152, vlo = base + 65536, vhi2 = base + 81920;
-  const Opnd Ka{khi, klo, 128, false}, Kb{khi2, khi2, 128, false};
-  const Opnd Va{vhi, vlo, 128, false}, Vb{vhi2, vhi2, 128, false};
+  const uint32_t khi = base, klo = base + 16384, vhi = base + 32768, vlo = base + 49152;
+  const Opnd Ka{khi, klo, 128, false}, Va{vhi, vlo, 128, false};
   auto Qt = [&](int s, bool mn) {
-    const uint32_t q0 = base + 98304 + s * 2 * QT;
+    const uint32_t q0 = base + 65536 + s * 2 * QT;
     return Opnd{q0, q0 + QT, 64, mn};
   };
   auto dOt = [&](int s, bool mn) {
-    const uint32_t q0 = base + 98304 + 6 * QT + s * 2 * QT;
+    const uint32_t q0 = base + 65536 + kSt * 2 * QT + s * 2 * QT;
     return Opnd{q0, q0 + QT, 64, mn};
   };
-  float* stats = reinterpret_cast<float*>(smem + kKvOff);  // [3][256]: m, inv pairs | t
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kKvOff + 3 * 1024);
-  uint64_t* bKV = &bars[0];   // K, V landed
-  uint64_t* bKVc = &bars[1];  // K, V forms made (512 arrivals)
-  uint64_t* bQ = &bars[2];    // [3] Q_j, dO_j, stats_j landed (stage j % 3)
-  uint64_t* bSD = &bars[5];   // [2] S_j, dP_j done (TMEM buffer j & 1)
-  uint64_t* bPD = &bars[7];   // [2] P~_j, dS_j written (512 arrivals)
-  uint64_t* bM = &bars[9];    // [3] step j's dV / dK MMAs done (by j % 3)
+  float* stats = reinterpret_cast<float*>(smem + kKvOff);  // [kSt][256]: m, inv pairs | t
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kKvOff + kSt * 1024);
+  uint64_t* bKV = &bars[0];  // K, V of the problem landed
+  uint64_t* bQ = &bars[1];   // [kSt] Q_k, dO_k, stats_k landed (stage k % kSt)
+  uint64_t* bSD = &bars[5];  // [2] S_k, dP_k done (TMEM buffer k & 1)
+  uint64_t* bPD = &bars[7];  // [2] P~_k, dS_k written (512 arrivals)
+  uint64_t* bM = &bars[9];   // [kSt] step k's dV / dK MMAs done (by k % kSt)
   uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 13);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int sq = a.sq, skv = a.skv;
   const int nkb = (skv + 127) >> 7, nq64 = (sq + kQB - 1) / kQB;
   const int nprob = a.G * a.Bb * a.H * nkb;
   if (tid == 0) {
-    for (int k = 0; k < 12; ++k) mbar_init(&bars[k], (k == 1 || k == 7 || k == 8) ? 512 : 1);
+    for (int k = 0; k < 13; ++k) mbar_init(&bars[k], (k == 7 || k == 8) ? 512 : 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) tmem_alloc(tslot, 512);
@@ -577,28 +588,28 @@ __global__ void __launch_bounds__(kKvThreads, 1)
     g = r / a.Bb;
   };
   auto first_q = [&](int kb) { return a.causal ? (kb * 128) / kQB : 0; };
+  // Every role walks the same problems and steps, so a parity wait is for
+  // exactly the phase it needs: the phase before it is complete and the one
+  // after it cannot complete before the wait (checked per barrier below).
   if (warp == 17) {
     // ================= TMA loads (one thread) =================
     if (lane == 0) {
-      uint32_t cm = 0;  // steps before this problem (global step index base)
-      for (int z = blockIdx.x; z < nprob; z += gridDim.x) {
+      uint32_t k = 0;       // global step
+      int klast = -1;       // last step of the previous problem
+      int pi = 0;           // problems (trace slots)
+      for (int z = blockIdx.x; z < nprob; z += gridDim.x, ++pi) {
         int g, b, h, kb;
         coords(z, g, b, h, kb);
         const int q0 = first_q(kb), n = nq64 - q0;
-        mbar_expect_tx(bKV, 4 * 16384);  // (the previous problem's MMAs are all done)
-        tma_box(khi, tm, TK, g, b, h, bKV, kb * 128, 0);
-        tma_box(klo, tm, TK, g, b, h, bKV, kb * 128, 32);
-        tma_box(vhi, tm, TV, g, b, h, bKV, kb * 128, 0);
-        tma_box(vlo, tm, TV, g, b, h, bKV, kb * 128, 32);
+        if (n <= 0) continue;
         const float* st = a.P.at(g, b, h);
-        for (int j = 0; j < n; ++j) {
-          const int s = j % 3;
-          if (j >= 3) {  // stage s: step j-3 fully consumed
-            const uint32_t k = cm + j - 3;
-            mbar_wait(&bM[k % 3], (k / 3) & 1);
-          }
+        for (int j = 0; j < n; ++j, ++k) {
+          const int s = (int)(k % kSt);
+          // stage s: step k - kSt's gradient MMAs done (bM's next phase is step
+          // k's, which needs this load)
+          if (k >= (uint32_t)kSt) mbar_wait(&bM[s], ((k - kSt) / kSt) & 1);
           const int qr = (q0 + j) * kQB;
-          FTRACE(8 * (cm + j) + 6);
+          FTRACE((k) < 256 ? 8 * (k) + 6 : 4096);
           mbar_expect_tx(&bQ[s], 4 * QT + 768);
           const Opnd Q = Qt(s, false), D = dOt(s, false);
           tma_box(Q.hi, tm, TQ, g, b, h, &bQ[s], qr, 0);
@@ -607,77 +618,87 @@ __global__ void __launch_bounds__(kKvThreads, 1)
           tma_box(D.lo, tm, TDO, g, b, h, &bQ[s], qr, 32);
           bulk_load(smem_u32(stats + s * 256), st + 2LL * qr, 512, &bQ[s]);  // m, 1/l
           bulk_load(smem_u32(stats + s * 256 + 128), st + t_off(sq) + qr, 256, &bQ[s]);
+          if (j == 0) {
+            // K, V once the previous problem's last S^T / dP^T have read theirs
+            // (bSD's next phase is step klast + 2's, which needs these K, V)
+            if (klast >= 0) mbar_wait(&bSD[klast & 1], ((uint32_t)klast >> 1) & 1);
+            mbar_expect_tx(bKV, 4 * 16384);
+            tma_box(khi, tm, TK, g, b, h, bKV, kb * 128, 0);
+            tma_box(klo, tm, TK, g, b, h, bKV, kb * 128, 32);
+            tma_box(vhi, tm, TV, g, b, h, bKV, kb * 128, 0);
+            tma_box(vlo, tm, TV, g, b, h, bKV, kb * 128, 32);
+            FTRACE(2048 + 4 * pi + 0);
+          }
         }
-        // every step of this problem done before the next one's K, V (waits
-        // stay consecutive: no bM phase is skipped)
-        for (int j = max(n - 3, 0); j < n; ++j) {
-          const uint32_t k = cm + j;
-          mbar_wait(&bM[k % 3], (k / 3) & 1);
-        }
-        cm += n;
+        klast = (int)k - 1;
       }
     }
     __syncwarp();
   } else if (warp == 16) {
     // ================= MMA issue (one thread) =================
     if (lane == 0) {
-      uint32_t nkv = 0, nq[3] = {0, 0, 0}, npd[2] = {0, 0}, cm = 0;
+      uint32_t k = 0, np = 0;  // global step base of the problem, problems
       const uint32_t idN64 = idesc(64, false, false), idG = idesc(64, false, true);
       for (int z = blockIdx.x; z < nprob; z += gridDim.x) {
         int g, b, h, kb;
         coords(z, g, b, h, kb);
         const int n = nq64 - first_q(kb);
-        mbar_wait(bKVc, nkv & 1);
-        ++nkv;
+        if (n <= 0) continue;
+        // K, V of this problem (the next load needs this problem's last S^T)
+        mbar_wait(bKV, np & 1);
+        FTRACE(2048 + 4 * np + 3);
+        ++np;
         for (int j = 0; j <= n; ++j) {
           if (j < n) {
-            const int s = j & 1, q3 = j % 3;
-            mbar_wait(&bQ[q3], nq[q3] & 1);
-            ++nq[q3];
-            FTRACE(8 * (cm + j) + 0);
-            if (j >= 2) {  // TMEM buffers s free: step j-2's gradient MMAs done
-              const uint32_t k = cm + j - 2;
-              mbar_wait(&bM[k % 3], (k / 3) & 1);
-            }
-            FTRACE(8 * (cm + j) + 1);
+            const uint32_t kk = k + j;
+            const int s = (int)(kk & 1), q = (int)(kk % kSt);
+            mbar_wait(&bQ[q], (kk / kSt) & 1);
+            FTRACE((kk) < 256 ? 8 * (kk) + 0 : 4096);
+            // TMEM buffers s: step kk-2's gradient MMAs have read its P~ / dS
+            if (kk >= 2) mbar_wait(&bM[(kk - 2) % kSt], ((kk - 2) / kSt) & 1);
+            FTRACE((kk) < 256 ? 8 * (kk) + 1 : 4096);
             tc_after();
-            const Opnd Q = Qt(q3, false), D = dOt(q3, false);
+            const Opnd Q = Qt(q, false), D = dOt(q, false);
             const uint32_t dS_ = tmem + tsb(s), dD = tmem + tdb(s);
-            for (int k = 0; k < 4; ++k) {
-              mma_ss(dS_, Ka, false, Q, false, k, idN64, k > 0 ? 1u : 0u);  // S^T = K Q^T
-              mma_ss(dS_, Ka, true, Q, false, k, idN64, 1u);
-              mma_ss(dS_, Kb, false, Q, true, k, idN64, 1u);
-              mma_ss(dD, Va, false, D, false, k, idN64, k > 0 ? 1u : 0u);  // dP^T = V dO^T
-              mma_ss(dD, Va, true, D, false, k, idN64, 1u);
-              mma_ss(dD, Vb, false, D, true, k, idN64, 1u);
+            for (int c = 0; c < 4; ++c) {  // corrections (2^11 domain)
+              mma_ss(dS_, Ka, true, Q, false, c, idN64, c > 0 ? 1u : 0u);  // S^T = K Q^T
+              mma_ss(dS_, Ka, false, Q, true, c, idN64, 1u);
+              mma_ss(dD, Va, true, D, false, c, idN64, c > 0 ? 1u : 0u);   // dP^T = V dO^T
+              mma_ss(dD, Va, false, D, true, c, idN64, 1u);
+            }
+            mma_ss_scaled(dS_, Ka, Q, 0, idN64);
+            mma_ss_scaled(dD, Va, D, 0, idN64);
+            for (int c = 1; c < 4; ++c) {
+              mma_ss(dS_, Ka, false, Q, false, c, idN64, 1u);
+              mma_ss(dD, Va, false, D, false, c, idN64, 1u);
             }
             mma_commit<1>(&bSD[s]);
           }
           if (j >= 1) {
-            const int s = (j - 1) & 1;
-            mbar_wait(&bPD[s], npd[s] & 1);
-            ++npd[s];
-            FTRACE(8 * (cm + j - 1) + 2);
+            const uint32_t kk = k + j - 1;
+            const int s = (int)(kk & 1), q = (int)(kk % kSt);
+            mbar_wait(&bPD[s], (kk >> 1) & 1);
+            FTRACE((kk) < 256 ? 8 * (kk) + 2 : 4096);
             tc_after();
-            const Opnd Qm = Qt((j - 1) % 3, true), Dm = dOt((j - 1) % 3, true);
+            const Opnd Qm = Qt(q, true), Dm = dOt(q, true);
             const uint32_t pa = tmem + tsb(s), da = tmem + tdb(s);
             const bool first = j == 1;
-            for (int k = 0; k < 4; ++k) {
-              const uint32_t oq = Qm.at(k), od = Dm.at(k);
+            for (int c = 0; c < 4; ++c) {
+              const uint32_t oq = Qm.at(c), od = Dm.at(c);
               const uint64_t dqh = desc_sw128(Qm.hi + oq, Qm.lbo()), dql = desc_sw128(Qm.lo + oq, Qm.lbo());
               const uint64_t ddh = desc_sw128(Dm.hi + od, Dm.lbo()), ddl = desc_sw128(Dm.lo + od, Dm.lbo());
-              const uint32_t acc = (!first || k > 0) ? 1u : 0u;
-              mma_ts(tmem + kTdV, pa + 8 * k, ddh, idG, acc);  // dV += P^T dO
-              mma_ts(tmem + kTdV, pa + 32 + 8 * k, ddh, idG, 1u);
-              mma_ts(tmem + kTdV, pa + 64 + 8 * k, ddl, idG, 1u);
-              mma_ts(tmem + kTdK, da + 8 * k, dqh, idG, acc);  // dK += dS^T Q
-              mma_ts(tmem + kTdKc, da + 32 + 8 * k, dqh, idG, acc);
-              mma_ts(tmem + kTdKc, da + 8 * k, dql, idG, 1u);
+              const uint32_t acc = (!first || c > 0) ? 1u : 0u;
+              mma_ts(tmem + kTdV, pa + 8 * c, ddh, idG, acc);  // dV += P^T dO
+              mma_ts(tmem + kTdVc, pa + 32 + 8 * c, ddh, idG, acc);
+              mma_ts(tmem + kTdVc, pa + 8 * c, ddl, idG, 1u);
+              mma_ts(tmem + kTdK, da + 8 * c, dqh, idG, acc);  // dK += dS^T Q
+              mma_ts(tmem + kTdKc, da + 32 + 8 * c, dqh, idG, acc);
+              mma_ts(tmem + kTdKc, da + 8 * c, dql, idG, 1u);
             }
-            mma_commit<1>(&bM[(cm + j - 1) % 3]);
+            mma_commit<1>(&bM[kk % kSt]);
           }
         }
-        cm += n;
+        k += n;
       }
     }
     __syncwarp();
@@ -687,28 +708,21 @@ __global__ void __launch_bounds__(kKvThreads, 1)
     const int q4 = warp & 3, qq = warp >> 2;
     const uint32_t lanes = (uint32_t)(q4 * 32) << 16;
     const int r = q4 * 32 + lane;  // key row within the block
-    uint32_t nkv = 0, nsd[2] = {0, 0}, cm = 0;
-    for (int z = blockIdx.x; z < nprob; z += gridDim.x) {
+    uint32_t k = 0;
+    int pi = 0;  // problems (trace slots)
+    for (int z = blockIdx.x; z < nprob; z += gridDim.x, ++pi) {
       int g, b, h, kb;
       coords(z, g, b, h, kb);
       const int q0 = first_q(kb), n = nq64 - q0;
+      if (n <= 0) continue;
       const int key = kb * 128 + r;
-      // K, V landed: lo' -> lo'' in place, hi'' = hi 2^-11
-      mbar_wait(bKV, nkv & 1);
-      ++nkv;
-      scale_copy(klo, klo, 16384, tid, 512);
-      scale_copy(khi2, khi, 16384, tid, 512);
-      scale_copy(vlo, vlo, 16384, tid, 512);
-      scale_copy(vhi2, vhi, 16384, tid, 512);
-      fence_async_smem();
-      mbar_arrive(bKVc);
       float* dsg = a.dS.at(g, b, h);
-      for (int j = 0; j < n; ++j) {
-        const int s = j & 1;
-        if (tid == 0) FTRACE(8 * (cm + j) + 3);
-        mbar_wait(&bSD[s], nsd[s] & 1);
-        ++nsd[s];
-        if (tid == 0) FTRACE(8 * (cm + j) + 4);
+      for (int j = 0; j < n; ++j, ++k) {
+        const int s = (int)(k & 1);
+        if (tid == 0) FTRACE((k) < 256 ? 8 * (k) + 3 : 4096);
+        // bSD's next phase is step k+2's S^T, which needs this step's bPD
+        mbar_wait(&bSD[s], (k >> 1) & 1);
+        if (tid == 0) FTRACE((k) < 256 ? 8 * (k) + 4 : 4096);
         tc_after();
         float sv[16], dp[16];
         {
@@ -725,10 +739,9 @@ __global__ void __launch_bounds__(kKvThreads, 1)
         // P~ and dS overwrite S / dP columns the other three warps of these
         // TMEM lanes read: they all have read theirs first
         named_sync(2 + q4, 128);
-        const float* st = stats + (j % 3) * 256;
+        const float* st = stats + (k % kSt) * 256;
         const int qa = (q0 + j) * kQB + qq * 16;  // this thread's first query
-        uint32_t ph[8], pl[8], ph2[8], dh[8], dl[8];
-        const __half2 sc = __float2half2_rn(kLo2);
+        uint32_t ph[8], pl[8], dh[8], dl[8];
 #pragma unroll
         for (int e = 0; e < 16; e += 2) {
           float p[2], ds[2];
@@ -742,11 +755,9 @@ __global__ void __launch_bounds__(kKvThreads, 1)
           }
           const __half2 hh = __floats2half2_rn(p[0], p[1]);
           const float2 hf = __half22float2(hh);
-          const __half2 ll = __floats2half2_rn(p[0] - hf.x, p[1] - hf.y);
-          const __half2 h2 = __hmul2(hh, sc);
+          const __half2 ll = __floats2half2_rn((p[0] - hf.x) * kLoScale, (p[1] - hf.y) * kLoScale);
           ph[e >> 1] = *reinterpret_cast<const uint32_t*>(&hh);
           pl[e >> 1] = *reinterpret_cast<const uint32_t*>(&ll);
-          ph2[e >> 1] = *reinterpret_cast<const uint32_t*>(&h2);
           const __half2 dhh = __floats2half2_rn(ds[0], ds[1]);
           const float2 dhf = __half22float2(dhh);
           const __half2 dll = __floats2half2_rn((ds[0] - dhf.x) * kLoScale, (ds[1] - dhf.y) * kLoScale);
@@ -754,37 +765,11 @@ __global__ void __launch_bounds__(kKvThreads, 1)
           dl[e >> 1] = *reinterpret_cast<const uint32_t*>(&dll);
           amax = fmaxf(amax, fmaxf(fabsf(ds[0]), fabsf(ds[1])));
         }
-        // P~ -> buffer s (hi | lo'' | hi''), dS -> dP buffer s (hi | lo'): 8 columns each
-        asm volatile(
-            "tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(
-                tmem + tsb(s) + lanes + qq * 8),
-            "r"(ph[0]), "r"(ph[1]), "r"(ph[2]), "r"(ph[3]), "r"(ph[4]), "r"(ph[5]), "r"(ph[6]),
-            "r"(ph[7])
-            : "memory");
-        asm volatile(
-            "tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(
-                tmem + tsb(s) + lanes + 32 + qq * 8),
-            "r"(pl[0]), "r"(pl[1]), "r"(pl[2]), "r"(pl[3]), "r"(pl[4]), "r"(pl[5]), "r"(pl[6]),
-            "r"(pl[7])
-            : "memory");
-        asm volatile(
-            "tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(
-                tmem + tsb(s) + lanes + 64 + qq * 8),
-            "r"(ph2[0]), "r"(ph2[1]), "r"(ph2[2]), "r"(ph2[3]), "r"(ph2[4]), "r"(ph2[5]),
-            "r"(ph2[6]), "r"(ph2[7])
-            : "memory");
-        asm volatile(
-            "tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(
-                tmem + tdb(s) + lanes + qq * 8),
-            "r"(dh[0]), "r"(dh[1]), "r"(dh[2]), "r"(dh[3]), "r"(dh[4]), "r"(dh[5]), "r"(dh[6]),
-            "r"(dh[7])
-            : "memory");
-        asm volatile(
-            "tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(
-                tmem + tdb(s) + lanes + 32 + qq * 8),
-            "r"(dl[0]), "r"(dl[1]), "r"(dl[2]), "r"(dl[3]), "r"(dl[4]), "r"(dl[5]), "r"(dl[6]),
-            "r"(dl[7])
-            : "memory");
+        // P~ -> buffer s (hi | lo'), dS -> dP buffer s (hi | lo'): 8 columns each
+        tmem_st8(tmem + tsb(s) + lanes + qq * 8, ph);
+        tmem_st8(tmem + tsb(s) + lanes + 32 + qq * 8, pl);
+        tmem_st8(tmem + tdb(s) + lanes + qq * 8, dh);
+        tmem_st8(tmem + tdb(s) + lanes + 32 + qq * 8, dl);
         // dS for the dQ kernel: the (64-query block, 128-key block) tile pair
         // image [128 key rows][64 queries] hi | lo', SWIZZLE_128B layout
         {
@@ -800,55 +785,59 @@ __global__ void __launch_bounds__(kKvThreads, 1)
         }
         tmem_st_wait();
         tc_before();
-        if (tid == 0) FTRACE(8 * (cm + j) + 5);
+        if (tid == 0) FTRACE((k) < 256 ? 8 * (k) + 5 : 4096);
+        // bPD's next phase is step k+2's, which needs S^T_{k+2} -> this arrival seen
         mbar_arrive(&bPD[s]);
       }
-      // ---- epilogue: dV, dK = (main + 2^-11 corr) scale (this warp: 16 columns) ----
+      // ---- epilogue: dV, dK = (main + 2^-11 corr) [scale] (this warp: 16 columns);
+      // the next problem's first S^T / dP^T run meanwhile (other TMEM columns),
+      // its first gradient MMAs (which overwrite dV / dK) wait for this CTA's
+      // bPD arrivals of its first step, issued after these reads ----
       {
-        const uint32_t k = cm + n - 1;
-        mbar_wait(&bM[k % 3], (k / 3) & 1);
+        const uint32_t kl = k - 1;  // bM's next phase is step kl + kSt's: needs our bPD
+        mbar_wait(&bM[kl % kSt], (kl / kSt) & 1);
         tc_after();
+        if (tid == 0) FTRACE(2048 + 4 * pi + 1);
       }
       {
-        uint32_t u[16], w[16], x[16];
-        tmem_ld16(tmem + kTdV + lanes + qq * 16, u);
-        tmem_ld16(tmem + kTdK + lanes + qq * 16, w);
-        tmem_ld16(tmem + kTdKc + lanes + qq * 16, x);
+        const int col = qq * 16;
+        auto put = [&](const Mat& o, const Mat& ohl, const float* v) {
+          if (o.ok()) {
+            float* p = o.at(g, b, h) + (long long)key * o.ld + col;
+#pragma unroll
+            for (int e = 0; e < 16; e += 4)
+              *reinterpret_cast<float4*>(p + e) = make_float4(v[e], v[e + 1], v[e + 2], v[e + 3]);
+          }
+          if (ohl.ok()) {
+            char* p = reinterpret_cast<char*>(ohl.at(g, b, h) + (long long)key * ohl.ld);
+#pragma unroll
+            for (int e = 0; e < 16; e += 8) {
+              uint4 hi, lo;
+              split8(v + e, hi, lo, amax);
+              char* q = p + ((col + e) >> 5) * 128 + ((col + e) & 31) * 2;
+              *reinterpret_cast<uint4*>(q) = hi;
+              *reinterpret_cast<uint4*>(q + 64) = lo;
+            }
+          }
+        };
+        uint32_t u[16], w[16];
+        float v[16];
+        tmem_ld16(tmem + kTdV + lanes + col, u);
+        tmem_ld16(tmem + kTdVc + lanes + col, w);
         tmem_wait();
-        float dv[16], dk[16];
 #pragma unroll
-        for (int e = 0; e < 16; ++e) {
-          dv[e] = __uint_as_float(u[e]);
-          dk[e] = fmaf(__uint_as_float(x[e]), kLo2, __uint_as_float(w[e])) * a.scale;
-        }
-        if (key < skv) {
-          const int col = qq * 16;
-          auto put = [&](const Mat& o, const Mat& ohl, const float* v) {
-            if (o.ok()) {
-              float* p = o.at(g, b, h) + (long long)key * o.ld + col;
+        for (int e = 0; e < 16; ++e) v[e] = fmaf(__uint_as_float(w[e]), kLo2, __uint_as_float(u[e]));
+        if (key < skv) put(a.dV, a.dVhl, v);
+        tmem_ld16(tmem + kTdK + lanes + col, u);
+        tmem_ld16(tmem + kTdKc + lanes + col, w);
+        tmem_wait();
 #pragma unroll
-              for (int e = 0; e < 16; e += 4)
-                *reinterpret_cast<float4*>(p + e) = make_float4(v[e], v[e + 1], v[e + 2], v[e + 3]);
-            }
-            if (ohl.ok()) {
-              char* p = reinterpret_cast<char*>(ohl.at(g, b, h) + (long long)key * ohl.ld);
-#pragma unroll
-              for (int e = 0; e < 16; e += 8) {
-                uint4 hi, lo;
-                split8(v + e, hi, lo, amax);
-                char* q = p + ((col + e) >> 5) * 128 + ((col + e) & 31) * 2;
-                *reinterpret_cast<uint4*>(q) = hi;
-                *reinterpret_cast<uint4*>(q + 64) = lo;
-              }
-            }
-          };
-          put(a.dV, a.dVhl, dv);
-          put(a.dK, a.dKhl, dk);
-        }
+        for (int e = 0; e < 16; ++e)
+          v[e] = fmaf(__uint_as_float(w[e]), kLo2, __uint_as_float(u[e])) * a.scale;
+        if (key < skv) put(a.dK, a.dKhl, v);
       }
-      cm += n;
+      if (tid == 0) FTRACE(2048 + 4 * pi + 2);
       tc_before();
-      named_sync(1, 512);  // TMEM accumulators read before the next problem's first MMAs
     }
   }
   if (amax >= 65520.f && amax <= FLT_MAX && a.range_flag) atomicOr(a.range_flag, 1);

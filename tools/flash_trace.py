@@ -16,3 +16,7 @@ names = ["mma:Q ready", "mma:S issue", "mma:grads issue(prev)", "cmp:wait S", "c
 for step in range(40):
     row = [buf[8 * step + k] - t0 if buf[8 * step + k] else None for k in range(7)]
     print(step, "  ".join(f"{n.split(':')[1][:10]:>10s}={v if v is not None else '-':>8}" for n, v in zip(names, row)))
+print("problem   KV issue   MMA KV ready   epi start   epi end   (cycles from the first Q issue)")
+for p in range(8):
+    row = [buf[2048 + 4 * p + k] - t0 if buf[2048 + 4 * p + k] else None for k in (0, 3, 1, 2)]
+    print(p, "  ".join(f"{v if v is not None else '-':>10}" for v in row))
