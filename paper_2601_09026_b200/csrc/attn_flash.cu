@@ -107,6 +107,20 @@ constexpr float kLo2 = 1.f / 2048.f;
 __device__ __forceinline__ void named_sync(int id, int n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
+// Problem z of a persistent CTA (z = blockIdx + round * grid) -> (head, block).
+// The blocks of one head are consecutive problems, so CTAs running at the
+// same time share that head's K / V (or Q / dO) rows in L2, and the block
+// index is rotated by the round z / R (R = the grid rounded down to whole
+// heads), so every CTA cycles through all block indices: under the causal
+// mask the blocks carry 1..n units of work, and a CTA that kept one block
+// index (z mod n with a grid that is a multiple of n) ran up to 8/5 of the
+// mean. A bijection for any grid (R is a multiple of nblk).
+__device__ __forceinline__ void head_block(int z, int nblk, int& head, int& blk) {
+  const int R = max(nblk, ((int)gridDim.x / nblk) * nblk);
+  head = z / nblk;
+  blk = (z % nblk + z / R) % nblk;
+}
+
 __device__ __forceinline__ void mma_ss(uint32_t d, const Opnd& A, bool a_lo, const Opnd& B, bool b_lo,
                                        int k, uint32_t id, uint32_t acc) {
   const uint32_t oa = A.at(k), ob = B.at(k);
@@ -157,15 +171,9 @@ __global__ void __launch_bounds__(kFwdThreads, 2)
   bar_sync();
   const uint32_t tmem = *tslot;
   float amax = 0.f;
-  // block-major problem order, heaviest (latest) causal query blocks first:
-  // a persistent CTA's problems z, z + grid, ... take every block index in
-  // turn (with z % nqb the block index was fixed per CTA whenever the grid is
-  // a multiple of nqb, and the CTAs holding the last query block ran 8/5 of
-  // the mean causal work)
-  const int heads = a.G * a.Bb * a.H;
   auto coords = [&](int z, int& g, int& b, int& h, int& qb) {
-    qb = nqb - 1 - z / heads;
-    int r = z % heads;
+    int r;
+    head_block(z, nqb, r, qb);
     h = r % a.H;
     r /= a.H;
     b = r % a.Bb;
@@ -578,10 +586,9 @@ __global__ void __launch_bounds__(kKvThreads, 1)
   bar_sync();
   const uint32_t tmem = *tslot;
   float amax = 0.f;
-  const int heads = a.G * a.Bb * a.H;
-  auto coords = [&](int z, int& g, int& b, int& h, int& kb) {  // block-major, heaviest first
-    kb = z / heads;
-    int r = z % heads;
+  auto coords = [&](int z, int& g, int& b, int& h, int& kb) {
+    int r;
+    head_block(z, nkb, r, kb);
     h = r % a.H;
     r /= a.H;
     b = r % a.Bb;
@@ -878,10 +885,9 @@ __global__ void __launch_bounds__(kQThreads, 1)
   bar_sync();
   const uint32_t tmem = *tslot;
   float amax = 0.f;
-  const int heads = a.G * a.Bb * a.H;
-  auto coords = [&](int z, int& g, int& b, int& h, int& qb) {  // block-major, heaviest first
-    qb = nqb - 1 - z / heads;
-    int r = z % heads;
+  auto coords = [&](int z, int& g, int& b, int& h, int& qb) {
+    int r;
+    head_block(z, nqb, r, qb);
     h = r % a.H;
     r /= a.H;
     b = r % a.Bb;

@@ -28,6 +28,13 @@ print("gemm drain ok", flush=True)
 for (B, H, s, causal) in [(1, 1, 128, False), (1, 1, 256, True)]:
     out = TA.run(B, H, s, s, 64, causal)
     print("attention", (B, H, s, causal), "ok", flush=True)
+# single-pass long attention with every operand pre-split (attn_flash.cu):
+# several problems per CTA of the dK/dV kernel (steps chained across
+# problems), a ragged 197-token shape and a 512-token causal one
+for (B, H, s, causal) in [(2, 2, 197, False), (1, 2, 512, True), (1, 1, 256, True)]:
+    got, ref = TA.run(B, H, s, s, 64, int(causal) | 4 | 8, seed=9)
+    print("flash attention", (B, H, s, causal),
+          [round(TA.relerr(a, b), 8) for n, a, b in zip("OPQKV", got, ref) if n != "P"], flush=True)
 import __graft_entry__ as GE  # noqa: E402
 GE.smoke()
 print("engine ok", flush=True)
