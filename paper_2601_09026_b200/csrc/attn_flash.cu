@@ -779,6 +779,7 @@ __global__ void __launch_bounds__(kKvThreads, 1)
         tmem_st8(tmem + tdb(s) + lanes + 32 + qq * 8, dl);
         // dS for the dQ kernel: the (64-query block, 128-key block) tile pair
         // image [128 key rows][64 queries] hi | lo', SWIZZLE_128B layout
+#ifndef MGLP_DIAG_NO_DS_STORE
         {
           char* img = reinterpret_cast<char*>(dsg + ((long long)(q0 + j) * nkb + kb) * 8192);
           const int c0 = qq * 2;  // this thread's two 16-byte chunks of its row
@@ -790,6 +791,7 @@ __global__ void __launch_bounds__(kKvThreads, 1)
                 make_uint4(dl[4 * c], dl[4 * c + 1], dl[4 * c + 2], dl[4 * c + 3]);
           }
         }
+#endif
         tmem_st_wait();
         tc_before();
         if (tid == 0) FTRACE((k) < 256 ? 8 * (k) + 5 : 4096);
