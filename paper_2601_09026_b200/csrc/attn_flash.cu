@@ -494,6 +494,14 @@ __device__ __forceinline__ void mma_ss_scaled(uint32_t d, const Opnd& A, const O
       "l"(desc_sw128(A.hi + oa, A.lbo())), "l"(desc_sw128(B.hi + ob, B.lbo())), "r"(id));
 }
 
+// one 256-bit global store (sm_100: STG.256), 32-byte aligned
+__device__ __forceinline__ void st_v8(void* p, uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                                      uint32_t a4, uint32_t a5, uint32_t a6, uint32_t a7) {
+  asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(a0), "r"(a1), "r"(a2),
+               "r"(a3), "r"(a4), "r"(a5), "r"(a6), "r"(a7)
+               : "memory");
+}
+
 // 32 lanes x 8 columns into TMEM (this warp's lane quarter)
 __device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t* r) {
   asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr),
@@ -724,6 +732,7 @@ __global__ void __launch_bounds__(kKvThreads, 1)
       if (n <= 0) continue;
       const int key = kb * 128 + r;
       float* dsg = a.dS.at(g, b, h);
+      const bool ds_v8 = (reinterpret_cast<uintptr_t>(dsg) & 31) == 0;  // 256-bit stores
       for (int j = 0; j < n; ++j, ++k) {
         const int s = (int)(k & 1);
         if (tid == 0) FTRACE((k) < 256 ? 8 * (k) + 3 : 4096);
@@ -783,12 +792,29 @@ __global__ void __launch_bounds__(kKvThreads, 1)
         {
           char* img = reinterpret_cast<char*>(dsg + ((long long)(q0 + j) * nkb + kb) * 8192);
           const int c0 = qq * 2;  // this thread's two 16-byte chunks of its row
+          if (ds_v8) {
+            // chunks c0, c0 + 1 (c0 even) land at (c0 ^ x), (c0 ^ x) ^ 1, x = r & 7:
+            // one aligned 32-byte sector, in swapped order when x is odd
+            const uint32_t off = (uint32_t)(r * 128 + (((c0 ^ (r & 7)) & ~1) << 4));
+            const bool sw = r & 1;
+            uint32_t h8[8], l8[8];
 #pragma unroll
-          for (int c = 0; c < 2; ++c) {
-            const uint32_t off = (uint32_t)(r * 128 + (((c0 + c) ^ (r & 7)) << 4));
-            *reinterpret_cast<uint4*>(img + off) = make_uint4(dh[4 * c], dh[4 * c + 1], dh[4 * c + 2], dh[4 * c + 3]);
-            *reinterpret_cast<uint4*>(img + 16384 + off) =
-                make_uint4(dl[4 * c], dl[4 * c + 1], dl[4 * c + 2], dl[4 * c + 3]);
+            for (int e = 0; e < 4; ++e) {
+              h8[e] = sw ? dh[4 + e] : dh[e];
+              h8[4 + e] = sw ? dh[e] : dh[4 + e];
+              l8[e] = sw ? dl[4 + e] : dl[e];
+              l8[4 + e] = sw ? dl[e] : dl[4 + e];
+            }
+            st_v8(img + off, h8[0], h8[1], h8[2], h8[3], h8[4], h8[5], h8[6], h8[7]);
+            st_v8(img + 16384 + off, l8[0], l8[1], l8[2], l8[3], l8[4], l8[5], l8[6], l8[7]);
+          } else {
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+              const uint32_t off = (uint32_t)(r * 128 + (((c0 + c) ^ (r & 7)) << 4));
+              *reinterpret_cast<uint4*>(img + off) = make_uint4(dh[4 * c], dh[4 * c + 1], dh[4 * c + 2], dh[4 * c + 3]);
+              *reinterpret_cast<uint4*>(img + 16384 + off) =
+                  make_uint4(dl[4 * c], dl[4 * c + 1], dl[4 * c + 2], dl[4 * c + 3]);
+            }
           }
         }
 #endif
@@ -813,19 +839,34 @@ __global__ void __launch_bounds__(kKvThreads, 1)
         auto put = [&](const Mat& o, const Mat& ohl, const float* v) {
           if (o.ok()) {
             float* p = o.at(g, b, h) + (long long)key * o.ld + col;
+            if ((reinterpret_cast<uintptr_t>(p) & 31) == 0) {  // 256-bit stores
 #pragma unroll
-            for (int e = 0; e < 16; e += 4)
-              *reinterpret_cast<float4*>(p + e) = make_float4(v[e], v[e + 1], v[e + 2], v[e + 3]);
+              for (int e = 0; e < 16; e += 8)
+                st_v8(p + e, __float_as_uint(v[e]), __float_as_uint(v[e + 1]), __float_as_uint(v[e + 2]),
+                      __float_as_uint(v[e + 3]), __float_as_uint(v[e + 4]), __float_as_uint(v[e + 5]),
+                      __float_as_uint(v[e + 6]), __float_as_uint(v[e + 7]));
+            } else {
+#pragma unroll
+              for (int e = 0; e < 16; e += 4)
+                *reinterpret_cast<float4*>(p + e) = make_float4(v[e], v[e + 1], v[e + 2], v[e + 3]);
+            }
           }
           if (ohl.ok()) {
             char* p = reinterpret_cast<char*>(ohl.at(g, b, h) + (long long)key * ohl.ld);
+            uint4 hi[2], lo[2];
 #pragma unroll
-            for (int e = 0; e < 16; e += 8) {
-              uint4 hi, lo;
-              split8(v + e, hi, lo, amax);
-              char* q = p + ((col + e) >> 5) * 128 + ((col + e) & 31) * 2;
-              *reinterpret_cast<uint4*>(q) = hi;
-              *reinterpret_cast<uint4*>(q + 64) = lo;
+            for (int e = 0; e < 2; ++e) split8(v + 8 * e, hi[e], lo[e], amax);
+            // columns col .. col + 15 (col % 16 == 0): hi at q, q + 16, lo' at q + 64, q + 80
+            char* q = p + (col >> 5) * 128 + (col & 31) * 2;
+            if ((reinterpret_cast<uintptr_t>(q) & 31) == 0) {
+              st_v8(q, hi[0].x, hi[0].y, hi[0].z, hi[0].w, hi[1].x, hi[1].y, hi[1].z, hi[1].w);
+              st_v8(q + 64, lo[0].x, lo[0].y, lo[0].z, lo[0].w, lo[1].x, lo[1].y, lo[1].z, lo[1].w);
+            } else {
+#pragma unroll
+              for (int e = 0; e < 2; ++e) {
+                *reinterpret_cast<uint4*>(q + 16 * e) = hi[e];
+                *reinterpret_cast<uint4*>(q + 64 + 16 * e) = lo[e];
+              }
             }
           }
         };
