@@ -198,6 +198,14 @@ __device__ __forceinline__ void rows_out(uint32_t tmain, uint32_t tcor, float* o
 // nullable) and/or pre-split hi|lo' (hl, nullable; the next GEMM's A operand,
 // common.cuh). hl follows out's strides; the head's column offset must be a
 // multiple of 32 so the fp32 offset of the head equals its packed byte offset.
+// one 256-bit global store (sm_100: STG.256), 32-byte aligned
+__device__ __forceinline__ void st_v8(void* p, uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                                      uint32_t a4, uint32_t a5, uint32_t a6, uint32_t a7) {
+  asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(a0), "r"(a1), "r"(a2),
+               "r"(a3), "r"(a4), "r"(a5), "r"(a6), "r"(a7)
+               : "memory");
+}
+
 __device__ __forceinline__ void rows_out_hl(uint32_t tmain, uint32_t tcor, float* out, float* hl,
                                             long long ld, int row, int nvalid, int c0, int nc,
                                             float alpha, float& amax) {
@@ -212,22 +220,38 @@ __device__ __forceinline__ void rows_out_hl(uint32_t tmain, uint32_t tcor, float
       }
       if (row < nvalid) {
         if (out) {
+          float* o = out + row * ld + c0 + c;
+          if ((reinterpret_cast<uintptr_t>(o) & 31) == 0) {  // 256-bit stores
 #pragma unroll
-          for (int e = 0; e < 16; e += 4)
-            *reinterpret_cast<float4*>(out + row * ld + c0 + c + e) =
-                make_float4(v[e], v[e + 1], v[e + 2], v[e + 3]);
+            for (int e = 0; e < 16; e += 8)
+              st_v8(o + e, __float_as_uint(v[e]), __float_as_uint(v[e + 1]), __float_as_uint(v[e + 2]),
+                    __float_as_uint(v[e + 3]), __float_as_uint(v[e + 4]), __float_as_uint(v[e + 5]),
+                    __float_as_uint(v[e + 6]), __float_as_uint(v[e + 7]));
+          } else {
+#pragma unroll
+            for (int e = 0; e < 16; e += 4)
+              *reinterpret_cast<float4*>(o + e) = make_float4(v[e], v[e + 1], v[e + 2], v[e + 3]);
+          }
         }
         if (hl) {
-          // 8 values -> one 16-byte hi and one 16-byte lo' store (as many
-          // stores as the fp32 row)
+          // 16 values -> hi at p, p + 16 and lo' at p + 64, p + 80 (c0 + c is
+          // a multiple of 16: one 32-byte run each)
+          uint4 hi[2], lo[2];
 #pragma unroll
-          for (int e = 0; e < 16; e += 8) {
-            uint4 hi, lo;
-            split8(v + e, hi, lo, amax);
-            const int col = c0 + c + e;
-            char* p = reinterpret_cast<char*>(hl + row * ld) + (col >> 5) * 128 + (col & 31) * 2;
-            *reinterpret_cast<uint4*>(p) = hi;
-            *reinterpret_cast<uint4*>(p + 64) = lo;
+          for (int e = 0; e < 2; ++e) split8(v + 8 * e, hi[e], lo[e], amax);
+          const int col = c0 + c;
+          char* p = reinterpret_cast<char*>(hl + row * ld) + (col >> 5) * 128 + (col & 31) * 2;
+          if (((reinterpret_cast<uintptr_t>(p) & 31) == 0) && (col & 15) == 0) {
+            st_v8(p, hi[0].x, hi[0].y, hi[0].z, hi[0].w, hi[1].x, hi[1].y, hi[1].z, hi[1].w);
+            st_v8(p + 64, lo[0].x, lo[0].y, lo[0].z, lo[0].w, lo[1].x, lo[1].y, lo[1].z, lo[1].w);
+          } else {
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const int ce = col + 8 * e;
+              char* q = reinterpret_cast<char*>(hl + row * ld) + (ce >> 5) * 128 + (ce & 31) * 2;
+              *reinterpret_cast<uint4*>(q) = hi[e];
+              *reinterpret_cast<uint4*>(q + 64) = lo[e];
+            }
           }
         }
       }

@@ -494,14 +494,6 @@ __device__ __forceinline__ void mma_ss_scaled(uint32_t d, const Opnd& A, const O
       "l"(desc_sw128(A.hi + oa, A.lbo())), "l"(desc_sw128(B.hi + ob, B.lbo())), "r"(id));
 }
 
-// one 256-bit global store (sm_100: STG.256), 32-byte aligned
-__device__ __forceinline__ void st_v8(void* p, uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
-                                      uint32_t a4, uint32_t a5, uint32_t a6, uint32_t a7) {
-  asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(a0), "r"(a1), "r"(a2),
-               "r"(a3), "r"(a4), "r"(a5), "r"(a6), "r"(a7)
-               : "memory");
-}
-
 // 32 lanes x 8 columns into TMEM (this warp's lane quarter)
 __device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t* r) {
   asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr),
