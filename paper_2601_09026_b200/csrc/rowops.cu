@@ -9,6 +9,7 @@
 #include <cstdlib>
 
 #include "kernels.cuh"
+#include "tc_common.cuh"
 
 namespace mglp {
 
@@ -236,6 +237,80 @@ __global__ void __launch_bounds__(256) ln_fwd4_kernel(LnFwdArgs a, const int* ac
   }
 }
 
+// 256-bit form of ln_fwd4 (d % 256 == 0, 32-byte aligned rows): lane l holds
+// columns 8 (l + 32 i) .. + 7, one LDG.256 / STG.256 per 8 values (half the
+// memory instructions of the float4 form; its own fixed reduction order)
+__device__ __forceinline__ void ld8g(const float* p, float* v) {
+  asm volatile("ld.global.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]),
+                 "=f"(v[7])
+               : "l"(p));
+}
+__device__ __forceinline__ void st8g(float* p, const float* v) {
+  asm volatile("st.global.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "f"(v[0]), "f"(v[1]),
+               "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7])
+               : "memory");
+}
+
+template <int V8>
+__global__ void __launch_bounds__(256) ln_fwd8_kernel(LnFwdArgs a, const int* active) {
+  pdl_wait();
+  pdl_trigger();
+  if (stopped(active)) return;
+  const int g = blockIdx.y;
+  const int row = blockIdx.x * kRowsPerBlock + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= a.rows) return;
+  const float* x = a.x.at(g) + (long long)row * a.x.ld;
+  float v[V8][8];
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < V8; ++i) ld8g(x + 8 * (lane + 32 * i), v[i]);
+#pragma unroll
+  for (int i = 0; i < V8; ++i)
+    s += ((v[i][0] + v[i][1]) + (v[i][2] + v[i][3])) + ((v[i][4] + v[i][5]) + (v[i][6] + v[i][7]));
+  const float inv_d = 1.f / (float)a.d;
+  const float mean = warp_sum(s) * inv_d;
+  float qs = 0.f;
+#pragma unroll
+  for (int i = 0; i < V8; ++i)
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const float c = v[i][e] - mean;
+      qs = fmaf(c, c, qs);
+    }
+  const float var = warp_sum(qs) * inv_d;
+  const float rstd = 1.f / sqrtf(var + a.eps);
+  const float* gain = a.gain.at(g);
+  const float* bias = a.bias.at(g);
+  float* o = a.out.ok() ? a.out.at(g) + (long long)row * a.out.ld : nullptr;
+  float* hl = a.out_hl.ok() ? a.out_hl.at(g) + (long long)row * a.out_hl.ld : nullptr;
+  float amax = 0.f;
+#pragma unroll
+  for (int i = 0; i < V8; ++i) {
+    const int c0 = 8 * (lane + 32 * i);
+    float gn[8], bs[8], y[8];
+    ld8g(gain + c0, gn);
+    ld8g(bias + c0, bs);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) y[e] = gn[e] * ((v[i][e] - mean) * rstd) + bs[e];
+    if (o) st8g(o + c0, y);
+    if (hl) {
+      uint4 h, l;
+      tc::split8(y, h, l, amax);
+      char* b = reinterpret_cast<char*>(hl) + (c0 >> 5) * 128 + (c0 & 31) * 2;
+      *reinterpret_cast<uint4*>(b) = h;
+      *reinterpret_cast<uint4*>(b + 64) = l;
+    }
+  }
+  if (hl) hl_range_check(amax, a.range_flag);
+  if (lane == 0 && a.stats.ok()) {
+    float* st = a.stats.at(g) + 2LL * row;
+    st[0] = mean;
+    st[1] = rstd;
+  }
+}
+
 template <int V4>
 __global__ void __launch_bounds__(256) ln_bwd4_kernel(LnBwdArgs a, const int* active) {
   pdl_wait();
@@ -330,6 +405,106 @@ __global__ void __launch_bounds__(256) ln_bwd4_kernel(LnBwdArgs a, const int* ac
   }
 }
 
+// 256-bit form of ln_bwd4 (d % 256 == 0, 32-byte aligned rows): lane l holds
+// columns 8 (l + 32 i) .. + 7 (its own fixed reduction order)
+template <int V8>
+__global__ void __launch_bounds__(256) ln_bwd8_kernel(LnBwdArgs a, const int* active) {
+  pdl_wait();
+  pdl_trigger();
+  __shared__ double red[32];
+  if (stopped(active)) return;
+  const int g = blockIdx.y;
+  const int row = blockIdx.x * kRowsPerBlock + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  double r2 = 0.0;
+  if (row < a.rows) {
+    const float* x = a.x.at(g) + (long long)row * a.x.ld;
+    const float* up = a.up.at(g) + (long long)row * a.up.ld;
+    const float* gain = a.gain.at(g);
+    const float mean = a.stats.at(g)[2LL * row];
+    const float rstd = a.stats.at(g)[2LL * row + 1];
+    float xh[V8][8], dxh[V8][8];
+#pragma unroll
+    for (int i = 0; i < V8; ++i) {
+      const int c0 = 8 * (lane + 32 * i);
+      ld8g(x + c0, xh[i]);
+      ld8g(up + c0, dxh[i]);
+    }
+    float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+    for (int i = 0; i < V8; ++i) {
+      float gn[8];
+      ld8g(gain + 8 * (lane + 32 * i), gn);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        xh[i][e] = (xh[i][e] - mean) * rstd;
+        dxh[i][e] *= gn[e];
+        s1 += dxh[i][e];
+        s2 = fmaf(dxh[i][e], xh[i][e], s2);
+      }
+    }
+    const float inv_d = 1.f / (float)a.d;
+    const float m1 = warp_sum(s1) * inv_d;
+    const float m2 = warp_sum(s2) * inv_d;
+    const float* addA = a.addA.ok() ? a.addA.at(g) + (long long)row * a.addA.ld : nullptr;
+    const float* addB = a.addB.ok() ? a.addB.at(g) + (long long)row * a.addB.ld : nullptr;
+    float* o1 = a.out1.ok() ? a.out1.at(g) + (long long)row * a.out1.ld : nullptr;
+    float* o2 = a.out2.ok() ? a.out2.at(g) + (long long)row * a.out2.ld : nullptr;
+    float* h2 = a.out2_hl.ok() ? a.out2_hl.at(g) + (long long)row * a.out2_hl.ld : nullptr;
+    float amax = 0.f;
+    const bool comb = a.cmb.mode != CM_NONE;
+    const long long off_out = comb ? (long long)row * a.cmb.out.ld : 0;
+    const long long off_z = comb ? (long long)row * a.cmb.z.ld : 0;
+#pragma unroll
+    for (int i = 0; i < V8; ++i) {
+      const int c0 = 8 * (lane + 32 * i);
+      float L[8], v1[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) L[e] = rstd * (dxh[i][e] - m1 - xh[i][e] * m2);
+      if (addA) {
+        float ad[8];
+        ld8g(addA + c0, ad);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) v1[e] = ad[e] + L[e];
+      } else {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) v1[e] = L[e];
+      }
+      if (o1) st8g(o1 + c0, v1);
+      if (o2 || h2) {
+        float bb[8], w[8];
+        if (addB) ld8g(addB + c0, bb);
+        else
+#pragma unroll
+          for (int e = 0; e < 8; ++e) bb[e] = 0.f;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) w[e] = bb[e] + L[e];
+        if (a.drop2.on())
+#pragma unroll
+          for (int e = 0; e < 8; ++e) w[e] *= drop_val(a.drop2, g, row, c0 + e);
+        if (o2) st8g(o2 + c0, w);
+        if (h2) {
+          uint4 h, l;
+          tc::split8(w, h, l, amax);
+          char* b = reinterpret_cast<char*>(h2) + (c0 >> 5) * 128 + (c0 & 31) * 2;
+          *reinterpret_cast<uint4*>(b) = h;
+          *reinterpret_cast<uint4*>(b + 64) = l;
+        }
+      }
+      if (comb) {
+        combine_apply4(a.cmb, g, off_out + c0, off_z + c0, make_float4(v1[0], v1[1], v1[2], v1[3]), r2);
+        combine_apply4(a.cmb, g, off_out + c0 + 4, off_z + c0 + 4, make_float4(v1[4], v1[5], v1[6], v1[7]), r2);
+      }
+    }
+    if (h2) hl_range_check(amax, a.range_flag);
+  }
+  if (a.cmb.mode == CM_RES0) {
+    const double t = block_sum_f64(r2, red);
+    if (threadIdx.x == 0)
+      a.cmb.norm_partials[a.cmb.norm_base + blockIdx.y * a.cmb.norm_member_stride + blockIdx.x] = t;
+  }
+}
+
 template <int V4>
 struct LnFwd4L {
   static void launch(dim3 g, const LnFwdArgs& a, const int* act, cudaStream_t s) {
@@ -352,6 +527,11 @@ void dispatch_rows4(int d, const Args& a, int G, int rows, const int* active, cu
   else if (v <= 4) K<4>::launch(grid, a, active, s);
   else if (v <= 6) K<6>::launch(grid, a, active, s);
   else K<8>::launch(grid, a, active, s);
+}
+
+bool vec8_ok(const Mat& m) {
+  return !m.ok() || ((reinterpret_cast<uintptr_t>(m.ptr) & 31) == 0 && m.ld % 8 == 0 &&
+                     m.slot_stride % 8 == 0);
 }
 
 bool vec_ok(const Mat& m) {
@@ -903,7 +1083,17 @@ __global__ void cycle_end_kernel(SolveCtrl* c, double tol) {
 
 void launch_ln_fwd(const LnFwdArgs& a, const int* active, cudaStream_t s) {
   if (a.rows == 0 || a.G == 0) return;
-  if (a.d % 4 == 0 && vec_ok(a.x) && vec_ok(a.out) && vec_ok(a.out_hl) && vec_ok(a.gain) &&
+  static const bool v8 = [] {  // MGLP_LN_V8=0: the float4 form only (A/B)
+    const char* e = getenv("MGLP_LN_V8");
+    return !(e && atoi(e) == 0);
+  }();
+  if (v8 && (a.d == 512 || a.d == 768 || a.d == 1024) && vec8_ok(a.x) && vec8_ok(a.out) &&
+      vec8_ok(a.out_hl) && vec8_ok(a.gain) && vec8_ok(a.bias)) {
+    dim3 grid(ceil_div(a.rows, kRowsPerBlock), a.G);
+    if (a.d == 512) launch_k(ln_fwd8_kernel<2>, grid, dim3(256), 0, s, 1, a, active);
+    else if (a.d == 768) launch_k(ln_fwd8_kernel<3>, grid, dim3(256), 0, s, 1, a, active);
+    else launch_k(ln_fwd8_kernel<4>, grid, dim3(256), 0, s, 1, a, active);
+  } else if (a.d % 4 == 0 && vec_ok(a.x) && vec_ok(a.out) && vec_ok(a.out_hl) && vec_ok(a.gain) &&
       vec_ok(a.bias))
     dispatch_rows4<LnFwd4L>(a.d, a, a.G, a.rows, active, s);
   else
@@ -915,7 +1105,19 @@ int ln_bwd_blocks(int rows) { return ceil_div(rows, kRowsPerBlock); }
 void launch_ln_bwd(const LnBwdArgs& a, const int* active, cudaStream_t s) {
   if (a.rows == 0 || a.G == 0) return;
   const Combine& c = a.cmb;
-  if (a.d % 4 == 0 && vec_ok(a.x) && vec_ok(a.up) && vec_ok(a.gain) && vec_ok(a.addA) &&
+  static const bool v8 = [] {  // MGLP_LN_V8=0: the float4 form only (A/B)
+    const char* e = getenv("MGLP_LN_V8");
+    return !(e && atoi(e) == 0);
+  }();
+  if (v8 && (a.d == 512 || a.d == 768 || a.d == 1024) && vec8_ok(a.x) && vec8_ok(a.up) &&
+      vec8_ok(a.gain) && vec8_ok(a.addA) && vec8_ok(a.addB) && vec8_ok(a.out1) && vec8_ok(a.out2) &&
+      vec8_ok(a.out2_hl) && vec_ok(c.z) && vec_ok(c.out) && vec_ok(c.base) && vec_ok(c.phib) &&
+      vec_ok(c.rho) && vec_ok(c.v)) {
+    dim3 grid(ceil_div(a.rows, kRowsPerBlock), a.G);
+    if (a.d == 512) launch_k(ln_bwd8_kernel<2>, grid, dim3(256), 0, s, 1, a, active);
+    else if (a.d == 768) launch_k(ln_bwd8_kernel<3>, grid, dim3(256), 0, s, 1, a, active);
+    else launch_k(ln_bwd8_kernel<4>, grid, dim3(256), 0, s, 1, a, active);
+  } else if (a.d % 4 == 0 && vec_ok(a.x) && vec_ok(a.up) && vec_ok(a.gain) && vec_ok(a.addA) &&
       vec_ok(a.addB) && vec_ok(a.out1) && vec_ok(a.out2) && vec_ok(a.out2_hl) && vec_ok(c.z) && vec_ok(c.out) &&
       vec_ok(c.base) && vec_ok(c.phib) && vec_ok(c.rho) && vec_ok(c.v))
     dispatch_rows4<LnBwd4L>(a.d, a, a.G, a.rows, active, s);
