@@ -413,20 +413,34 @@ __global__ void __launch_bounds__(kFwdThreads, 2)
           if (live) {
             const int col = kh * 32 + c;
             if (orow) {
+              float* o = orow + i * ld + col;
+              if ((reinterpret_cast<uintptr_t>(o) & 31) == 0) {  // 256-bit stores
 #pragma unroll
-              for (int e = 0; e < 16; e += 4)
-                *reinterpret_cast<float4*>(orow + i * ld + col + e) =
-                    make_float4(v[e], v[e + 1], v[e + 2], v[e + 3]);
+                for (int e = 0; e < 16; e += 8)
+                  st_v8(o + e, __float_as_uint(v[e]), __float_as_uint(v[e + 1]), __float_as_uint(v[e + 2]),
+                        __float_as_uint(v[e + 3]), __float_as_uint(v[e + 4]), __float_as_uint(v[e + 5]),
+                        __float_as_uint(v[e + 6]), __float_as_uint(v[e + 7]));
+              } else {
+#pragma unroll
+                for (int e = 0; e < 16; e += 4)
+                  *reinterpret_cast<float4*>(o + e) = make_float4(v[e], v[e + 1], v[e + 2], v[e + 3]);
+              }
             }
             if (hrow) {
+              uint4 hi[2], lo[2];
 #pragma unroll
-              for (int e = 0; e < 16; e += 8) {
-                uint4 hi, lo;
-                split8(v + e, hi, lo, amax);
-                char* p = reinterpret_cast<char*>(hrow + i * ld) + ((col + e) >> 5) * 128 +
-                          ((col + e) & 31) * 2;
-                *reinterpret_cast<uint4*>(p) = hi;
-                *reinterpret_cast<uint4*>(p + 64) = lo;
+              for (int e = 0; e < 2; ++e) split8(v + 8 * e, hi[e], lo[e], amax);
+              // col % 16 == 0: hi at p, p + 16, lo' at p + 64, p + 80
+              char* p = reinterpret_cast<char*>(hrow + i * ld) + (col >> 5) * 128 + (col & 31) * 2;
+              if ((reinterpret_cast<uintptr_t>(p) & 31) == 0) {
+                st_v8(p, hi[0].x, hi[0].y, hi[0].z, hi[0].w, hi[1].x, hi[1].y, hi[1].z, hi[1].w);
+                st_v8(p + 64, lo[0].x, lo[0].y, lo[0].z, lo[0].w, lo[1].x, lo[1].y, lo[1].z, lo[1].w);
+              } else {
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                  *reinterpret_cast<uint4*>(p + 16 * e) = hi[e];
+                  *reinterpret_cast<uint4*>(p + 64 + 16 * e) = lo[e];
+                }
               }
             }
           }
