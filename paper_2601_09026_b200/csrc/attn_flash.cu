@@ -544,6 +544,38 @@ __global__ void __launch_bounds__(256) flash_rowdot_kernel(const AttnArgs a, con
   const __half* d = reinterpret_cast<const __half*>(a.dO.at(g, b, h) + (long long)q * a.dO.ld);
   const float* o = a.O.at(g, b, h) + (long long)q * a.O.ld;
   float t = 0.f;
+  // a thread reads its own row: 256-bit loads where the rows allow (the same
+  // values in the same order as the 128-bit form below)
+  if (((reinterpret_cast<uintptr_t>(d) | reinterpret_cast<uintptr_t>(o)) & 31) == 0) {
+#pragma unroll
+    for (int e = 0; e < 64; e += 16) {
+      uint32_t hw[8], lw[8];
+      float ov[16];
+      asm volatile("ld.global.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                   : "=r"(hw[0]), "=r"(hw[1]), "=r"(hw[2]), "=r"(hw[3]), "=r"(hw[4]), "=r"(hw[5]),
+                     "=r"(hw[6]), "=r"(hw[7])
+                   : "l"(d + e));
+      asm volatile("ld.global.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                   : "=r"(lw[0]), "=r"(lw[1]), "=r"(lw[2]), "=r"(lw[3]), "=r"(lw[4]), "=r"(lw[5]),
+                     "=r"(lw[6]), "=r"(lw[7])
+                   : "l"(d + 64 + e));
+#pragma unroll
+      for (int hh = 0; hh < 2; ++hh)
+        asm volatile("ld.global.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                     : "=f"(ov[8 * hh]), "=f"(ov[8 * hh + 1]), "=f"(ov[8 * hh + 2]), "=f"(ov[8 * hh + 3]),
+                       "=f"(ov[8 * hh + 4]), "=f"(ov[8 * hh + 5]), "=f"(ov[8 * hh + 6]), "=f"(ov[8 * hh + 7])
+                     : "l"(o + e + 8 * hh));
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const float2 hf = __half22float2(*reinterpret_cast<const __half2*>(&hw[k]));
+        const float2 lf = __half22float2(*reinterpret_cast<const __half2*>(&lw[k]));
+        t += fmaf(lf.x, kLo2, hf.x) * ov[2 * k];
+        t += fmaf(lf.y, kLo2, hf.y) * ov[2 * k + 1];
+      }
+    }
+    a.P.at(g, b, h)[t_off(a.sq) + q] = t;
+    return;
+  }
   for (int e = 0; e < 64; e += 8) {
     const uint4 hv = *reinterpret_cast<const uint4*>(d + e);
     const uint4 lv = *reinterpret_cast<const uint4*>(d + 64 + e);
