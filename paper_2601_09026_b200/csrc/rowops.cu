@@ -405,6 +405,49 @@ __global__ void __launch_bounds__(256) ln_bwd4_kernel(LnBwdArgs a, const int* ac
   }
 }
 
+// combine_apply4 over 8 consecutive values with 256-bit loads / stores
+// (elementwise: the same results as two combine_apply4 calls)
+__device__ __forceinline__ void combine_apply8(const Combine& c, int g, long long off_out,
+                                               long long off_z, const float* F, double& r2) {
+  float z[8], o[8];
+  ld8g(c.z.at(g) + off_z, z);
+#pragma unroll
+  for (int e = 0; e < 8; ++e) o[e] = z[e] + c.dt * F[e];
+  switch (c.mode) {
+    case CM_PLAIN:
+      break;
+    case CM_FAS: {
+      float pb[8], rh[8], bs[8];
+      ld8g(c.phib.at(g) + off_out, pb);
+      ld8g(c.rho.at(g) + off_out, rh);
+      ld8g(c.base.at(g) + off_out, bs);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) o[e] = bs[e] + ((o[e] - pb[e]) + rh[e]);
+    } break;
+    case CM_RES0: {
+      float v[8];
+      ld8g(c.v.at(g) + off_out, v);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        o[e] = o[e] - v[e];
+        r2 += (double)o[e] * (double)o[e];
+      }
+    } break;
+    case CM_RESL: {
+      float pb[8], rh[8], bs[8], v[8];
+      ld8g(c.phib.at(g) + off_out, pb);
+      ld8g(c.rho.at(g) + off_out, rh);
+      ld8g(c.base.at(g) + off_out, bs);
+      ld8g(c.v.at(g) + off_out, v);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) o[e] = ((o[e] - pb[e]) + rh[e]) - (v[e] - bs[e]);
+    } break;
+    default:
+      return;
+  }
+  st8g(c.out.at(g) + off_out, o);
+}
+
 // 256-bit form of ln_bwd4 (d % 256 == 0, 32-byte aligned rows): lane l holds
 // columns 8 (l + 32 i) .. + 7 (its own fixed reduction order)
 template <int V8>
@@ -491,10 +534,7 @@ __global__ void __launch_bounds__(256) ln_bwd8_kernel(LnBwdArgs a, const int* ac
           *reinterpret_cast<uint4*>(b + 64) = l;
         }
       }
-      if (comb) {
-        combine_apply4(a.cmb, g, off_out + c0, off_z + c0, make_float4(v1[0], v1[1], v1[2], v1[3]), r2);
-        combine_apply4(a.cmb, g, off_out + c0 + 4, off_z + c0 + 4, make_float4(v1[4], v1[5], v1[6], v1[7]), r2);
-      }
+      if (comb) combine_apply8(a.cmb, g, off_out + c0, off_z + c0, v1, r2);
     }
     if (h2) hl_range_check(amax, a.range_flag);
   }
@@ -1111,8 +1151,8 @@ void launch_ln_bwd(const LnBwdArgs& a, const int* active, cudaStream_t s) {
   }();
   if (v8 && (a.d == 512 || a.d == 768 || a.d == 1024) && vec8_ok(a.x) && vec8_ok(a.up) &&
       vec8_ok(a.gain) && vec8_ok(a.addA) && vec8_ok(a.addB) && vec8_ok(a.out1) && vec8_ok(a.out2) &&
-      vec8_ok(a.out2_hl) && vec_ok(c.z) && vec_ok(c.out) && vec_ok(c.base) && vec_ok(c.phib) &&
-      vec_ok(c.rho) && vec_ok(c.v)) {
+      vec8_ok(a.out2_hl) && vec8_ok(c.z) && vec8_ok(c.out) && vec8_ok(c.base) && vec8_ok(c.phib) &&
+      vec8_ok(c.rho) && vec8_ok(c.v)) {
     dim3 grid(ceil_div(a.rows, kRowsPerBlock), a.G);
     if (a.d == 512) launch_k(ln_bwd8_kernel<2>, grid, dim3(256), 0, s, 1, a, active);
     else if (a.d == 768) launch_k(ln_bwd8_kernel<3>, grid, dim3(256), 0, s, 1, a, active);
