@@ -856,9 +856,18 @@ __global__ void copy_kernel(int G, long long n4, Mat dst, Mat src, const int* ac
   const int g = blockIdx.y;
   float4* d = reinterpret_cast<float4*>(dst.at(g));
   const float4* s = reinterpret_cast<const float4*>(src.at(g));
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n4;
-       i += (long long)gridDim.x * blockDim.x)
-    d[i] = s[i];
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  // four independent loads in flight per thread (the stream is latency-bound
+  // with one), then the tail
+  for (; i + 3 * stride < n4; i += 4 * stride) {
+    const float4 v0 = s[i], v1 = s[i + stride], v2 = s[i + 2 * stride], v3 = s[i + 3 * stride];
+    d[i] = v0;
+    d[i + stride] = v1;
+    d[i + 2 * stride] = v2;
+    d[i + 3 * stride] = v3;
+  }
+  for (; i < n4; i += stride) d[i] = s[i];
 }
 
 __global__ void correct_kernel(int G, long long n4, Mat dst, Mat a, Mat b, const int* active) {
@@ -869,12 +878,18 @@ __global__ void correct_kernel(int G, long long n4, Mat dst, Mat a, Mat b, const
   float4* d = reinterpret_cast<float4*>(dst.at(g));
   const float4* pa = reinterpret_cast<const float4*>(a.at(g));
   const float4* pb = reinterpret_cast<const float4*>(b.at(g));
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n4;
-       i += (long long)gridDim.x * blockDim.x) {
-    const float4 x = d[i], u = pa[i], w = pb[i];
-    d[i] = make_float4(x.x + (u.x - w.x), x.y + (u.y - w.y), x.z + (u.z - w.z),
-                       x.w + (u.w - w.w));
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  auto fix = [](float4 x, float4 u, float4 w) {
+    return make_float4(x.x + (u.x - w.x), x.y + (u.y - w.y), x.z + (u.z - w.z), x.w + (u.w - w.w));
+  };
+  for (; i + stride < n4; i += 2 * stride) {  // two rows of loads in flight per thread
+    const float4 x0 = d[i], u0 = pa[i], w0 = pb[i];
+    const float4 x1 = d[i + stride], u1 = pa[i + stride], w1 = pb[i + stride];
+    d[i] = fix(x0, u0, w0);
+    d[i + stride] = fix(x1, u1, w1);
   }
+  for (; i < n4; i += stride) d[i] = fix(d[i], pa[i], pb[i]);
 }
 
 __global__ void zero_kernel(int G, long long n4, Mat dst, const int* active) {
